@@ -1,0 +1,221 @@
+/*
+ * cs_api.h -- C ABI of the B200-native CityGaussian rendering hot path.
+ *
+ * libcsgpu.so (built from paper_2404_01133_b200/csrc, sm_100a only) exports
+ * exactly the functions declared here.  Signatures use plain pointers, sizes
+ * and POD structs; no torch or CUDA types cross the boundary (streams are
+ * passed as void* holding a cudaStream_t).  All device buffers passed in are
+ * caller-owned; the context owns only its scratch workspace.
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/pkg/src/citysplat/<file>:<line>).  INTEGRATION.md shows the
+ * ctypes binding a citysplat maintainer would add.
+ *
+ * Return codes: 0 on success, negative on failure (CS_EINVAL, CS_ECUDA,
+ * CS_ENOMEM, CS_ERANGE).  cs_last_error() returns a thread-local message.
+ */
+#ifndef CS_API_H
+#define CS_API_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CS_OK 0
+#define CS_EINVAL (-1)  /* -> ValueError (render.py:46-59, lod.py:314-321, lod.py:391-392) */
+#define CS_ECUDA (-2)   /* -> RuntimeError */
+#define CS_ENOMEM (-3)  /* -> MemoryError */
+#define CS_ERANGE (-4)  /* select_level: no interval covers a distance (lod.py:321) */
+
+/* Pinhole camera, core.py:339-377.  camera_center is passed as the reference
+ * computes it (core.py:369-374) so LoD distances are bit-identical. */
+typedef struct cs_camera {
+  double R[9];      /* rotation_w2c, row-major */
+  double t[3];      /* translation_w2c */
+  double center[3]; /* camera_center */
+  double fx, fy, cx, cy;
+  int32_t width, height;
+} cs_camera;
+
+/* RenderSettings, render.py:37-64, plus the derived constants the reference
+ * computes in Python (support_sigmas, LOW_PASS, _SINGULAR_DET) so the device
+ * uses the identical float64 values. */
+typedef struct cs_settings {
+  double background[3];
+  double alpha_floor;
+  double transmittance_floor;
+  double near_plane;
+  double support_sigmas; /* sqrt(2 ln(1/alpha_floor)), render.py:61-64 */
+  double low_pass;       /* 0.3, render.py:33 */
+  double singular_det;   /* 1e-12, render.py:34 */
+  int32_t sh_degree;
+  int32_t tile_size;
+} cs_settings;
+
+/* One GaussianCloud (core.py:210-328) resident in HBM.  Geometry is stored
+ * as 16-byte (fp32) or 32-byte (fp64) quads per Gaussian:
+ *   pos_op = (x, y, z, opacity), scale = (sx, sy, sz, 0), quat = (w, x, y, z)
+ * SH is fp32, channel-major (core.py:214-222): coefficient (c, n) of Gaussian
+ * k at sh[k*sh_stride + c*sh_coeffs + n]; sh_stride >= 3*sh_coeffs, %4 == 0. */
+typedef struct cs_cloud {
+  const void* pos_op;
+  const void* scale;
+  const void* quat;
+  const float* sh;
+  int64_t count;
+  int32_t sh_coeffs; /* 1, 4, 9 or 16 */
+  int32_t sh_stride;
+  int32_t fp64;      /* 1: geometry quads are double */
+  int32_t reserved;
+} cs_cloud;
+
+/* Per-frame statistics (FrameStats, render.py:81-86, plus pipeline counts).
+ * Written on the device by cs_render; read back only when asked. */
+typedef struct cs_frame_stats {
+  int64_t assembled;        /* AssembledSet.cloud.count (lod.py:395-401) */
+  int64_t visible;          /* FrameStats.visible_splats */
+  int64_t skipped_singular; /* FrameStats.skipped_singular */
+  int64_t pairs;            /* tile pairs P (render.py:233-243) */
+  int64_t fragments;        /* FrameStats.blended_fragments */
+  int32_t n_segments;       /* (level, block) pieces concatenated */
+  int32_t status;           /* bit0 pair-buffer overflow, bit1 CS_ERANGE */
+} cs_frame_stats;
+
+/* One block decision, VisibilityDecision (lod.py:255-264). level -1 = None. */
+typedef struct cs_decision {
+  double distance;
+  double box[4];
+  int32_t level;
+  uint8_t visible;
+  uint8_t has_box;
+  uint8_t pad[2];
+} cs_decision;
+
+/* LodScene (lod.py:150-208) description for cs_lod_create.  All arrays are
+ * host memory and are copied; cloud geometry stays where the caller put it. */
+typedef struct cs_lod_desc {
+  int32_t n_levels;
+  int32_t n_blocks;
+  const cs_cloud* clouds;     /* [n_levels * n_blocks], level-major (levels[L][j]) */
+  const double* bounds_min;   /* [n_blocks * 3] world-space MAD bounds */
+  const double* bounds_max;
+  const double* intervals;    /* [n_levels * 2] (lo, hi), nearest-first */
+} cs_lod_desc;
+
+typedef struct cs_ctx cs_ctx;
+typedef struct cs_lod cs_lod;
+
+/* Frame sources */
+#define CS_SRC_CLOUD 0     /* render one cloud: rasterize_stats(cloud, ...) */
+#define CS_SRC_LOD_BLOCK 1 /* assemble_render_set(mode="block") then render */
+#define CS_SRC_LOD_POINT 2 /* assemble_render_set(mode="pointwise") then render */
+
+typedef struct cs_source {
+  int32_t kind;
+  int32_t force_level; /* -1 = None */
+  cs_cloud cloud;      /* CS_SRC_CLOUD */
+  const cs_lod* lod;   /* CS_SRC_LOD_* */
+} cs_source;
+
+/* cs_render flags */
+#define CS_RENDER_SYNC 1u        /* synchronise, grow buffers and re-run on overflow */
+#define CS_RENDER_F64_OUT 2u     /* out_rgb is double (compatibility tier) */
+#define CS_RENDER_NO_CLIP 4u     /* leave the image unclipped */
+#define CS_RENDER_KEEP_STATE 8u  /* keep per-pixel state for cs_render_backward */
+#define CS_RENDER_PROJECT_ONLY 16u /* stop after projection + depth order (cs_dump_projected) */
+
+/* ---- context ----------------------------------------------------------- */
+int cs_create(int device, cs_ctx** out);
+void cs_destroy(cs_ctx* ctx);
+const char* cs_last_error(void);
+int cs_version(void);
+
+/* ---- LoD scene (lod.py:150-208) ---------------------------------------- */
+int cs_lod_create(cs_ctx* ctx, const cs_lod_desc* desc, cs_lod** out);
+void cs_lod_destroy(cs_lod* lod);
+
+/* decide_visibility (lod.py:330-348) incl. block_visible (lod.py:267-295),
+ * _screen_box (lod.py:298-308) and select_level (lod.py:311-321).
+ * out: host array [n_blocks].  Synchronous.  CS_ERANGE if select_level fails. */
+int cs_decide_visibility(cs_ctx* ctx, const cs_lod* lod, const cs_camera* cam,
+                         int32_t force_level, cs_decision* out_host, void* stream);
+
+/* block_visible for n arbitrary boxes (lod.py:267-295); host in/out. */
+int cs_block_visible(cs_ctx* ctx, int32_t n, const double* bmin, const double* bmax,
+                     const cs_camera* cam, uint8_t* visible_out, double* distance_out,
+                     void* stream);
+
+/* select_level for n distances (lod.py:311-321); host in/out.
+ * CS_EINVAL for a negative distance, CS_ERANGE if no interval covers one. */
+int cs_select_level(cs_ctx* ctx, int32_t n, const double* distances, int32_t n_intervals,
+                    const double* intervals, int32_t* level_out, void* stream);
+
+/* ---- whole frame --------------------------------------------------------
+ * rasterize_stats (render.py:252-280) of the source, with LoD selection +
+ * assembly (lod.py:360-401) on device when src is a LoD source.
+ * out_rgb: device (H, W, 3) float32 (or double with CS_RENDER_F64_OUT).
+ * stats_host: optional; filled (after a sync) when non-NULL.
+ * Without CS_RENDER_SYNC the call is fully asynchronous on `stream` and the
+ * device-side stats can be read later with cs_frame_stats_get. */
+int cs_render(cs_ctx* ctx, const cs_source* src, const cs_camera* cam, const cs_settings* st,
+              void* out_rgb, uint32_t flags, cs_frame_stats* stats_host, void* stream);
+
+/* Stats of the last frame (synchronises the stream). */
+int cs_frame_stats_get(cs_ctx* ctx, cs_frame_stats* out, void* stream);
+
+/* Golden-intermediate dumps of the last frame, host destinations.
+ * cs_dump_projected mirrors render._Projected (render.py:89-108): arrays in
+ * depth order; source = index into the assembled cloud.
+ * cs_dump_tiles mirrors render._bin_tiles (render.py:217-249): tile_ids
+ * (indices into the depth-sorted splats) and CSR offsets [n_tiles+1]. */
+int cs_dump_projected(cs_ctx* ctx, double* means, double* conics, double* covs, double* depths,
+                      double* colors, double* opacities, double* radii, int64_t* source,
+                      void* stream);
+int cs_dump_tiles(cs_ctx* ctx, int64_t* tile_ids, int64_t* offsets, void* stream);
+/* Assembled-order (segment) table of the last LoD frame:
+ * per piece (cloud index = level*n_blocks + block, count). */
+int cs_dump_segments(cs_ctx* ctx, int32_t* cloud_index, int64_t* count, int32_t max_n,
+                     int32_t* n_out, void* stream);
+/* Assembled order of the last pointwise frame (lod.py:378-390): packed
+ * (cloud_index << 40 | row) per assembled Gaussian. */
+int cs_dump_assembled_list(cs_ctx* ctx, uint64_t* packed, int64_t max_n, int64_t* n_out,
+                           void* stream);
+
+/* ---- the reference's native kernel, one for one --------------------------
+ * _kernels.blend_tiles (_kernels.py:17-76) with the same argument list; all
+ * arrays are DEVICE pointers, same dtypes and shapes as the numba kernel. */
+int cs_blend_tiles(cs_ctx* ctx, const int64_t* tile_ids, const int64_t* tile_offsets,
+                   int64_t n_tiles, const double* means, const double* conics,
+                   const double* colors, const double* opacities, int64_t n_splats,
+                   const double* background, int32_t tile_size, int32_t width, int32_t height,
+                   int32_t n_tiles_x, double alpha_floor, double t_floor, double* out,
+                   int64_t* fragments, void* stream);
+
+/* ---- utilities used by the API mirror (core.py) -------------------------- */
+/* build_covariances (core.py:107-111): n quats (w,x,y,z) + scales -> 3x3. */
+int cs_build_covariances(cs_ctx* ctx, int64_t n, const double* scales, const double* quats,
+                         double* out, void* stream);
+/* sh_to_colors (core.py:166-172): sh (n,3,C) f64, dirs (n,3) -> colors (n,3). */
+int cs_sh_to_colors(cs_ctx* ctx, int64_t n, const double* sh, int32_t coeffs,
+                    const double* dirs, int32_t degree, double* out, void* stream);
+
+/* ---- fusion (partition.py:570-587) ---------------------------------------
+ * Block membership of n positions: normalize_position (partition.py:110-114)
+ * -> contract (partition.py:117-126) -> block_of_points (partition.py:161-169).
+ * positions: device, fp32 (f32=1) or fp64 xyz triples.  out: device int32. */
+int cs_block_of_points(cs_ctx* ctx, int64_t n, const void* positions, int32_t f32,
+                       const double* p_min, const double* p_max, int32_t nx, int32_t ny,
+                       int32_t nz, int32_t* out, void* stream);
+/* Stable compaction of the rows of one block cloud that still belong to block j
+ * (the keep mask of fuse, partition.py:582-585): writes kept row indices
+ * (device int64, ascending) and the count (device int64). */
+int cs_fuse_filter(cs_ctx* ctx, int64_t n, const void* positions, int32_t f32,
+                   const double* p_min, const double* p_max, int32_t nx, int32_t ny, int32_t nz,
+                   int32_t block, int64_t* kept_idx, int64_t* kept_count, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CS_API_H */

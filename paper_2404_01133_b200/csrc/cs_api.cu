@@ -1,0 +1,765 @@
+// cs_api.cu -- C ABI (include/cs_api.h): context, workspace and the frame
+// pipeline K1..K9 on one stream with no host round trip.
+//
+//   K1  lod_select / pointwise      (lod.py:330-401)            cs_lod.cu
+//   K3  project + compaction        (render.py:111-172)         cs_project.cu
+//   K4  depth radix sort, 64-bit    (render.py:176-177)         cs_sort.cu
+//   K5  rank gather + pair scan     (render.py:178-188,226-236) cs_bin.cu
+//   K6  pair duplication            (render.py:237-243)         cs_bin.cu
+//   K7  tile radix sort             (render.py:245)             cs_sort.cu
+//   K8  tile ranges                 (render.py:247-248)         cs_bin.cu
+//   K9  blend                       (_kernels.py:17-76)         cs_blend.cu
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "cs_internal.cuh"
+
+namespace cs {
+// cs_project.cu
+void launch_project(const cs_cloud* d_clouds, const Seg* d_segs, DevStats* d_stats,
+                    const cs_camera& cam, const cs_settings& st, uint64_t* status,
+                    int64_t capacity, uint64_t* keys, uint32_t* vals, ProjRec* recs,
+                    const uint64_t* list, cudaStream_t s);
+void launch_setup_cloud(const cs_cloud& c, cs_cloud* d_clouds, Seg* d_segs, DevStats* d_stats,
+                        cudaStream_t s);
+void launch_build_covariances(int64_t n, const double* scales, const double* quats, double* out,
+                              cudaStream_t s);
+void launch_sh_to_colors(int64_t n, const double* sh, int C, const double* dirs, int degree,
+                         double* out, cudaStream_t s);
+// cs_lod.cu
+void launch_lod_select(const LodTables& T, const cs_camera& cam, int force_level,
+                       cs_decision* dec, Seg* segs, DevStats* stats, cudaStream_t s);
+void launch_pointwise(const LodTables& T, const cs_camera& cam, int force_level, uint64_t* status,
+                      uint64_t* list, Seg* segs, DevStats* stats, cudaStream_t s);
+void launch_block_visible(int n, const double* bmin, const double* bmax, const cs_camera& cam,
+                          uint8_t* vis, double* dist, cudaStream_t s);
+void launch_select_level(int n, const double* d, int ni, const double* iv, int32_t* out,
+                         cudaStream_t s);
+// cs_sort.cu
+size_t radix_status_words(int64_t capacity, int key_bytes);
+template <typename K>
+int radix_sort(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_dev, int64_t capacity,
+               int begin_bit, int end_bit, uint32_t* hist, uint32_t* status, uint32_t* tickets,
+               cudaStream_t s);
+// cs_bin.cu
+void launch_gather_count(const uint32_t* order, const ProjRec* recs, DevStats* stats,
+                         int tile_size, int width, int height, double alpha_floor,
+                         int64_t pair_cap, int64_t capacity, uint64_t* status, HotRec* hot,
+                         ColdRec* cold, int4* rects, int64_t* src_sorted, int64_t* pair_off,
+                         cudaStream_t s);
+void launch_duplicate(const int64_t* pair_off, const int4* rects, const DevStats* stats, int ntx,
+                      int64_t pair_cap, uint32_t* keys, uint32_t* vals, cudaStream_t s);
+void launch_tile_ranges(const uint32_t* keys, const DevStats* stats, uint2* ranges,
+                        cudaStream_t s);
+void launch_dump_projected(const uint32_t* order, const ProjRec* recs, const DevStats* stats,
+                           double* means, double* conics, double* covs, double* depths,
+                           double* colors, double* opac, double* radii, int64_t* src,
+                           cudaStream_t s);
+void launch_dump_tiles(const uint32_t* vals, const uint2* ranges, const DevStats* stats,
+                       int n_tiles, int64_t* tile_ids, int64_t* offsets, cudaStream_t s);
+// cs_blend.cu
+int blend_ppt(int tile_size);
+void launch_blend(int n_tiles, const uint32_t* list, const uint2* ranges, const HotRec* hot,
+                  const ColdRec* cold, const BlendParams& bp, void* out, bool f64_out,
+                  int32_t* frag_tile, DevStats* stats, const BlendState* keep, cudaStream_t s);
+void launch_pack(int64_t m, const double* means, const double* conics, const double* colors,
+                 const double* opac, double alpha_floor, HotRec* hot, ColdRec* cold, int64_t p,
+                 const int64_t* tile_ids, int64_t n_tiles, const int64_t* offsets, uint32_t* list,
+                 uint2* ranges, cudaStream_t s);
+// cs_fuse.cu
+void launch_block_of_points(int64_t n, const void* pos, int f32, const double* pmin,
+                            const double* pmax, int nx, int ny, int nz, int32_t* out,
+                            cudaStream_t s);
+void launch_fuse_filter(int64_t n, const void* pos, int f32, const double* pmin, const double* pmax,
+                        int nx, int ny, int nz, int block, uint64_t* status, uint32_t* ticket,
+                        int64_t* kept, int64_t* kept_count, cudaStream_t s);
+}  // namespace cs
+
+using namespace cs;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CS_CUDA(call)                                                                      \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess) {                                                               \
+      if (e_ == cudaErrorMemoryAllocation)                                                 \
+        return fail(CS_ENOMEM, "%s: %s", #call, cudaGetErrorString(e_));                   \
+      return fail(CS_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_)); \
+    }                                                                                      \
+  } while (0)
+
+#define CS_CHECK_LAUNCH() CS_CUDA(cudaGetLastError())
+
+// A growable device buffer.
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    size_t b = std::max<size_t>(want, 256);
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e == cudaSuccess) bytes = b;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+struct cs_lod {
+  cs_ctx* ctx = nullptr;
+  int n_levels = 0, n_blocks = 0;
+  std::vector<cs_cloud> clouds;
+  std::vector<int64_t> counts;
+  int64_t max_assembled = 0;
+  int64_t total_all = 0;
+  DBuf d_clouds, d_bmin, d_bmax, d_int, d_occ, d_allsegs;
+  LodTables tables() const {
+    LodTables T;
+    T.clouds = d_clouds.as<cs_cloud>();
+    T.bmin = d_bmin.as<double>();
+    T.bmax = d_bmax.as<double>();
+    T.intervals = d_int.as<double>();
+    T.occupied = d_occ.as<uint8_t>();
+    T.all_segs = d_allsegs.as<Seg>();
+    T.n_levels = n_levels;
+    T.n_blocks = n_blocks;
+    T.total_all = total_all;
+    return T;
+  }
+};
+
+struct cs_ctx {
+  int device = 0;
+  std::mutex mu;  // one frame at a time per context (contexts are per thread/stream)
+  DBuf stats, clouds1, segs, dec;
+  DBuf st_proj, st_gather, st_pw, st_fuse, st_sort, hist, sort_tickets, fuse_ticket;
+  DBuf keysA, valsA, keysB, valsB, recs;
+  DBuf hot, cold, rects, src_sorted, pair_off;
+  DBuf pkA, pvA, pkB, pvB, ranges, frag_tile, pw_list;
+  DBuf st_t, st_last, st_acc;
+  DBuf scratch1, scratch2, scratch3, scratch4;  // API utilities
+  cs_frame_stats* h_stats = nullptr;            // pinned
+  int64_t cap_vis = 0, cap_pairs = 0, cap_pw = 0, cap_tiles = 0;
+  // last frame bookkeeping (for dumps / backward)
+  const uint32_t* last_order = nullptr;
+  const uint32_t* last_list = nullptr;
+  const uint2* last_ranges = nullptr;
+  int last_tiles = 0;
+  int last_width = 0, last_height = 0;
+};
+
+extern "C" {
+
+int cs_version(void) { return 1; }
+const char* cs_last_error(void) { return g_err.c_str(); }
+
+int cs_create(int device, cs_ctx** out) {
+  if (!out) return fail(CS_EINVAL, "out is NULL");
+  int n = 0;
+  CS_CUDA(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) return fail(CS_EINVAL, "device %d not present (%d)", device, n);
+  CS_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CS_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(CS_EINVAL, "libcsgpu is built for sm_100a; device %d is sm_%d%d", device,
+                prop.major, prop.minor);
+  cs_ctx* c = new cs_ctx();
+  c->device = device;
+  CS_CUDA(cudaMallocHost(&c->h_stats, sizeof(cs_frame_stats)));
+  if (c->stats.ensure(sizeof(DevStats)) != cudaSuccess) return fail(CS_ENOMEM, "stats");
+  if (c->hist.ensure(sizeof(uint32_t) * 256 * 8) != cudaSuccess) return fail(CS_ENOMEM, "hist");
+  if (c->sort_tickets.ensure(sizeof(uint32_t) * 16) != cudaSuccess) return fail(CS_ENOMEM, "tk");
+  if (c->fuse_ticket.ensure(sizeof(uint32_t) * 4) != cudaSuccess) return fail(CS_ENOMEM, "tk");
+  if (c->clouds1.ensure(sizeof(cs_cloud)) != cudaSuccess) return fail(CS_ENOMEM, "clouds");
+  *out = c;
+  return CS_OK;
+}
+
+void cs_destroy(cs_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  DBuf* all[] = {&c->stats, &c->clouds1, &c->segs, &c->dec, &c->st_proj, &c->st_gather,
+                 &c->st_pw, &c->st_fuse, &c->st_sort, &c->hist, &c->sort_tickets,
+                 &c->fuse_ticket, &c->keysA, &c->valsA, &c->keysB, &c->valsB, &c->recs, &c->hot,
+                 &c->cold, &c->rects, &c->src_sorted, &c->pair_off, &c->pkA, &c->pvA, &c->pkB,
+                 &c->pvB, &c->ranges, &c->frag_tile, &c->pw_list, &c->st_t, &c->st_last,
+                 &c->st_acc, &c->scratch1, &c->scratch2, &c->scratch3, &c->scratch4};
+  for (DBuf* b : all) b->release();
+  if (c->h_stats) cudaFreeHost(c->h_stats);
+  delete c;
+}
+
+// ---------------------------------------------------------------------------
+// LoD scene
+
+int cs_lod_create(cs_ctx* ctx, const cs_lod_desc* d, cs_lod** out) {
+  if (!ctx || !d || !out) return fail(CS_EINVAL, "NULL argument");
+  if (d->n_levels <= 0 || d->n_blocks <= 0) return fail(CS_EINVAL, "empty LoD scene");
+  CS_CUDA(cudaSetDevice(ctx->device));
+  cs_lod* L = new cs_lod();
+  L->ctx = ctx;
+  L->n_levels = d->n_levels;
+  L->n_blocks = d->n_blocks;
+  const int LJ = d->n_levels * d->n_blocks;
+  L->clouds.assign(d->clouds, d->clouds + LJ);
+  L->counts.resize(LJ);
+  std::vector<Seg> allsegs(LJ);
+  int64_t start = 0;
+  for (int i = 0; i < LJ; ++i) {
+    const cs_cloud& c = L->clouds[i];
+    if (c.count < 0 || (c.count > 0 && (!c.pos_op || !c.scale || !c.quat || !c.sh)))
+      return fail(CS_EINVAL, "cloud %d: bad descriptor", i);
+    if (c.count > 0 && (c.sh_stride < 3 * c.sh_coeffs || (c.sh_stride & 3)))
+      return fail(CS_EINVAL, "cloud %d: sh_stride %d", i, c.sh_stride);
+    L->counts[i] = c.count;
+    allsegs[i].start = start;
+    allsegs[i].count = c.count;
+    allsegs[i].cloud = i;
+    allsegs[i].pad = 0;
+    start += c.count;
+  }
+  L->total_all = start;
+  std::vector<uint8_t> occ(d->n_blocks);
+  for (int j = 0; j < d->n_blocks; ++j) {
+    occ[j] = L->counts[(d->n_levels - 1) * d->n_blocks + j] > 0;  // LodScene.occupied (lod.py:207-208)
+    int64_t mx = 0;
+    for (int l = 0; l < d->n_levels; ++l) mx = std::max(mx, L->counts[l * d->n_blocks + j]);
+    L->max_assembled += mx;
+  }
+  if (L->d_clouds.ensure(sizeof(cs_cloud) * LJ) || L->d_bmin.ensure(sizeof(double) * 3 * d->n_blocks) ||
+      L->d_bmax.ensure(sizeof(double) * 3 * d->n_blocks) ||
+      L->d_int.ensure(sizeof(double) * 2 * d->n_levels) || L->d_occ.ensure(d->n_blocks) ||
+      L->d_allsegs.ensure(sizeof(Seg) * LJ))
+    return fail(CS_ENOMEM, "lod tables");
+  CS_CUDA(cudaMemcpy(L->d_clouds.p, L->clouds.data(), sizeof(cs_cloud) * LJ, cudaMemcpyHostToDevice));
+  CS_CUDA(cudaMemcpy(L->d_bmin.p, d->bounds_min, sizeof(double) * 3 * d->n_blocks, cudaMemcpyHostToDevice));
+  CS_CUDA(cudaMemcpy(L->d_bmax.p, d->bounds_max, sizeof(double) * 3 * d->n_blocks, cudaMemcpyHostToDevice));
+  CS_CUDA(cudaMemcpy(L->d_int.p, d->intervals, sizeof(double) * 2 * d->n_levels, cudaMemcpyHostToDevice));
+  CS_CUDA(cudaMemcpy(L->d_occ.p, occ.data(), d->n_blocks, cudaMemcpyHostToDevice));
+  CS_CUDA(cudaMemcpy(L->d_allsegs.p, allsegs.data(), sizeof(Seg) * LJ, cudaMemcpyHostToDevice));
+  *out = L;
+  return CS_OK;
+}
+
+void cs_lod_destroy(cs_lod* L) {
+  if (!L) return;
+  cudaSetDevice(L->ctx->device);
+  cudaDeviceSynchronize();
+  L->d_clouds.release(); L->d_bmin.release(); L->d_bmax.release(); L->d_int.release();
+  L->d_occ.release(); L->d_allsegs.release();
+  delete L;
+}
+
+static int ensure_frame_buffers(cs_ctx* c, int64_t cap_vis, int n_segs, int n_blocks,
+                                int n_tiles, int64_t cap_pw) {
+  cap_vis = std::max<int64_t>(cap_vis, 1);
+  if (c->segs.ensure(sizeof(Seg) * std::max(n_segs, 1)) ||
+      c->dec.ensure(sizeof(cs_decision) * std::max(n_blocks, 1)))
+    return fail(CS_ENOMEM, "segment tables");
+  if (cap_vis > c->cap_vis) {
+    int64_t cap = std::max<int64_t>(cap_vis, c->cap_vis + c->cap_vis / 2);
+    if (cap >= (1ll << 30)) return fail(CS_EINVAL, "more than 2^30 assembled Gaussians");
+    const int64_t chunks = (cap + 255) / 256 + 1;
+    if (c->st_proj.ensure(8 * chunks) || c->st_gather.ensure(8 * chunks) ||
+        c->keysA.ensure(8 * cap) || c->keysB.ensure(8 * cap) || c->valsA.ensure(4 * cap) ||
+        c->valsB.ensure(4 * cap) || c->recs.ensure(sizeof(ProjRec) * cap) ||
+        c->hot.ensure(sizeof(HotRec) * cap) || c->cold.ensure(sizeof(ColdRec) * cap) ||
+        c->rects.ensure(16 * cap) || c->src_sorted.ensure(8 * cap) || c->pair_off.ensure(8 * cap))
+      return fail(CS_ENOMEM, "visible-splat buffers (%lld)", (long long)cap);
+    c->cap_vis = cap;
+  }
+  if (c->cap_pairs == 0) c->cap_pairs = std::max<int64_t>(1 << 20, 8 * c->cap_vis);
+  if (c->cap_pairs >= (1ll << 30)) c->cap_pairs = (1ll << 30) - 1;
+  if (c->pkA.ensure(4 * c->cap_pairs) || c->pvA.ensure(4 * c->cap_pairs) ||
+      c->pkB.ensure(4 * c->cap_pairs) || c->pvB.ensure(4 * c->cap_pairs))
+    return fail(CS_ENOMEM, "pair buffers (%lld)", (long long)c->cap_pairs);
+  const size_t sw = std::max(radix_status_words(c->cap_vis, 8), radix_status_words(c->cap_pairs, 4));
+  if (c->st_sort.ensure(4 * sw)) return fail(CS_ENOMEM, "sort status");
+  if (n_tiles > c->cap_tiles) {
+    if (c->ranges.ensure(sizeof(uint2) * n_tiles) || c->frag_tile.ensure(4 * n_tiles))
+      return fail(CS_ENOMEM, "tile buffers");
+    c->cap_tiles = n_tiles;
+  }
+  if (cap_pw > 0 && cap_pw > c->cap_pw) {
+    if (c->pw_list.ensure(8 * cap_pw) || c->st_pw.ensure(8 * ((cap_pw + 255) / 256 + 1)))
+      return fail(CS_ENOMEM, "pointwise buffers");
+    c->cap_pw = cap_pw;
+  }
+  return CS_OK;
+}
+
+static int validate(const cs_camera* cam, const cs_settings* st) {
+  if (!cam || !st) return fail(CS_EINVAL, "camera/settings NULL");
+  if (cam->width <= 0 || cam->height <= 0) return fail(CS_EINVAL, "image dimensions must be positive");
+  if (st->tile_size < 8) return fail(CS_EINVAL, "tile_size must be at least 8");
+  if (blend_ppt(st->tile_size) == 0) return fail(CS_EINVAL, "tile_size > 64 not supported");
+  if (st->sh_degree < 0 || st->sh_degree > 3) return fail(CS_EINVAL, "sh_degree must be 0..3");
+  if (!(st->alpha_floor > 0.0 && st->alpha_floor < 1.0)) return fail(CS_EINVAL, "alpha_floor");
+  if (!(st->transmittance_floor > 0.0 && st->transmittance_floor < 1.0))
+    return fail(CS_EINVAL, "transmittance_floor");
+  if (!(st->near_plane > 0.0)) return fail(CS_EINVAL, "near_plane must be positive");
+  return CS_OK;
+}
+
+static int bits_for(int64_t n) {
+  int b = 1;
+  while ((1ll << b) < n) ++b;
+  return b;
+}
+
+// One pass of the whole pipeline (no sync).
+static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
+                       const cs_settings* st, void* out, uint32_t flags, cudaStream_t s) {
+  const int ts = st->tile_size;
+  const int ntx = (cam->width + ts - 1) / ts, nty = (cam->height + ts - 1) / ts;
+  const int n_tiles = ntx * nty;
+  int64_t cap_vis = 0, cap_pw = 0;
+  int n_segs = 1, n_blocks = 1;
+  const cs_lod* L = src->lod;
+  if (src->kind == CS_SRC_CLOUD) {
+    const cs_cloud& cl = src->cloud;
+    if (cl.count < 0 || (cl.count > 0 && (!cl.pos_op || !cl.scale || !cl.quat || !cl.sh)))
+      return fail(CS_EINVAL, "bad cloud descriptor");
+    if (cl.count > 0 && (cl.sh_stride < 3 * cl.sh_coeffs || (cl.sh_stride & 3)))
+      return fail(CS_EINVAL, "bad sh_stride");
+    cap_vis = cl.count;
+  } else {
+    if (!L) return fail(CS_EINVAL, "LoD source without scene");
+    n_segs = L->n_levels * L->n_blocks;
+    n_blocks = L->n_blocks;
+    if (src->kind == CS_SRC_LOD_BLOCK) {
+      cap_vis = src->force_level >= 0 ? 0 : L->max_assembled;
+      if (src->force_level >= 0) {
+        if (src->force_level >= L->n_levels) return fail(CS_EINVAL, "force_level out of range");
+        for (int j = 0; j < L->n_blocks; ++j) cap_vis += L->counts[src->force_level * L->n_blocks + j];
+      }
+    } else if (src->kind == CS_SRC_LOD_POINT) {
+      cap_vis = L->total_all;
+      cap_pw = L->total_all;
+    } else {
+      return fail(CS_EINVAL, "unknown source kind %d", src->kind);
+    }
+  }
+  int rc = ensure_frame_buffers(c, cap_vis, n_segs, n_blocks, n_tiles, cap_pw);
+  if (rc) return rc;
+  DevStats* stats = c->stats.as<DevStats>();
+  CS_CUDA(cudaMemsetAsync(stats, 0, sizeof(DevStats), s));
+  const cs_cloud* clouds = nullptr;
+  const uint64_t* list = nullptr;
+  if (src->kind == CS_SRC_CLOUD) {
+    launch_setup_cloud(src->cloud, c->clouds1.as<cs_cloud>(), c->segs.as<Seg>(), stats, s);
+    clouds = c->clouds1.as<cs_cloud>();
+  } else if (src->kind == CS_SRC_LOD_BLOCK) {
+    launch_lod_select(L->tables(), *cam, src->force_level, c->dec.as<cs_decision>(),
+                      c->segs.as<Seg>(), stats, s);
+    clouds = L->d_clouds.as<cs_cloud>();
+  } else {
+    CS_CUDA(cudaMemsetAsync(c->st_pw.p, 0, 8 * ((cap_pw + 255) / 256 + 1), s));
+    launch_pointwise(L->tables(), *cam, src->force_level, c->st_pw.as<uint64_t>(),
+                     c->pw_list.as<uint64_t>(), c->segs.as<Seg>(), stats, s);
+    clouds = L->d_clouds.as<cs_cloud>();
+    list = c->pw_list.as<uint64_t>();
+  }
+  CS_CHECK_LAUNCH();
+  const int64_t cap = std::max<int64_t>(cap_vis, 1);
+  CS_CUDA(cudaMemsetAsync(c->st_proj.p, 0, 8 * ((cap + 255) / 256 + 1), s));
+  launch_project(clouds, c->segs.as<Seg>(), stats, *cam, *st, c->st_proj.as<uint64_t>(), cap,
+                 c->keysA.as<uint64_t>(), c->valsA.as<uint32_t>(), c->recs.as<ProjRec>(), list, s);
+  CS_CHECK_LAUNCH();
+  // K4: global depth order (stable => ties keep assembled order)
+  const int which = radix_sort<uint64_t>(c->keysA.as<uint64_t>(), c->valsA.as<uint32_t>(),
+                                         c->keysB.as<uint64_t>(), c->valsB.as<uint32_t>(),
+                                         &stats->visible, cap, 0, 64, c->hist.as<uint32_t>(),
+                                         c->st_sort.as<uint32_t>(), c->sort_tickets.as<uint32_t>(), s);
+  CS_CHECK_LAUNCH();
+  const uint32_t* order = which ? c->valsB.as<uint32_t>() : c->valsA.as<uint32_t>();
+  // K5: gather by rank, rects, pair-count scan
+  CS_CUDA(cudaMemsetAsync(c->st_gather.p, 0, 8 * ((cap + 255) / 256 + 1), s));
+  launch_gather_count(order, c->recs.as<ProjRec>(), stats, ts, cam->width, cam->height,
+                      st->alpha_floor, c->cap_pairs, cap, c->st_gather.as<uint64_t>(),
+                      c->hot.as<HotRec>(), c->cold.as<ColdRec>(), c->rects.as<int4>(),
+                      c->src_sorted.as<int64_t>(), c->pair_off.as<int64_t>(), s);
+  CS_CHECK_LAUNCH();
+  if (flags & CS_RENDER_PROJECT_ONLY) {
+    c->last_order = order;
+    c->last_list = nullptr;
+    return CS_OK;
+  }
+  // K6: duplicate
+  launch_duplicate(c->pair_off.as<int64_t>(), c->rects.as<int4>(), stats, ntx, c->cap_pairs,
+                   c->pkA.as<uint32_t>(), c->pvA.as<uint32_t>(), s);
+  CS_CHECK_LAUNCH();
+  // K7: stable sort by tile id only (ceil(log2 T) bits)
+  const int which2 = radix_sort<uint32_t>(c->pkA.as<uint32_t>(), c->pvA.as<uint32_t>(),
+                                          c->pkB.as<uint32_t>(), c->pvB.as<uint32_t>(),
+                                          &stats->pairs_eff, c->cap_pairs, 0, bits_for(n_tiles),
+                                          c->hist.as<uint32_t>(), c->st_sort.as<uint32_t>(),
+                                          c->sort_tickets.as<uint32_t>() + 8, s);
+  CS_CHECK_LAUNCH();
+  const uint32_t* tkeys = which2 ? c->pkB.as<uint32_t>() : c->pkA.as<uint32_t>();
+  const uint32_t* tvals = which2 ? c->pvB.as<uint32_t>() : c->pvA.as<uint32_t>();
+  // K8: tile ranges
+  CS_CUDA(cudaMemsetAsync(c->ranges.p, 0, sizeof(uint2) * n_tiles, s));
+  launch_tile_ranges(tkeys, stats, c->ranges.as<uint2>(), s);
+  CS_CHECK_LAUNCH();
+  // K9: blend
+  BlendParams bp;
+  for (int i = 0; i < 3; ++i) bp.bg[i] = st->background[i];
+  bp.alpha_floor = st->alpha_floor;
+  bp.t_floor = st->transmittance_floor;
+  bp.tile_size = ts;
+  bp.width = cam->width;
+  bp.height = cam->height;
+  bp.ntx = ntx;
+  bp.flags = flags;
+  BlendState keep{nullptr, nullptr, nullptr};
+  const int64_t npx = (int64_t)cam->width * cam->height;
+  if (flags & CS_RENDER_KEEP_STATE) {
+    if (c->st_t.ensure(4 * npx) || c->st_last.ensure(4 * npx) || c->st_acc.ensure(12 * npx))
+      return fail(CS_ENOMEM, "blend state");
+    keep = BlendState{c->st_t.as<float>(), c->st_last.as<int32_t>(), c->st_acc.as<float>()};
+  }
+  launch_blend(n_tiles, tvals, c->ranges.as<uint2>(), c->hot.as<HotRec>(), c->cold.as<ColdRec>(),
+               bp, out, (flags & CS_RENDER_F64_OUT) != 0, c->frag_tile.as<int32_t>(), stats,
+               (flags & CS_RENDER_KEEP_STATE) ? &keep : nullptr, s);
+  CS_CHECK_LAUNCH();
+  c->last_order = order;
+  c->last_list = tvals;
+  c->last_ranges = c->ranges.as<uint2>();
+  c->last_tiles = n_tiles;
+  c->last_width = cam->width;
+  c->last_height = cam->height;
+  return CS_OK;
+}
+
+static int fetch_stats(cs_ctx* c, cudaStream_t s) {
+  // DevStats and cs_frame_stats share the leading layout
+  CS_CUDA(cudaMemcpyAsync(c->h_stats, c->stats.p, sizeof(cs_frame_stats), cudaMemcpyDeviceToHost, s));
+  CS_CUDA(cudaStreamSynchronize(s));
+  return CS_OK;
+}
+
+int cs_render(cs_ctx* c, const cs_source* src, const cs_camera* cam, const cs_settings* st,
+              void* out, uint32_t flags, cs_frame_stats* stats_host, void* stream) {
+  if (!c || !src || !out) return fail(CS_EINVAL, "NULL argument");
+  int rc = validate(cam, st);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lock(c->mu);
+  CS_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    rc = render_once(c, src, cam, st, out, flags, s);
+    if (rc) return rc;
+    if (!(flags & CS_RENDER_SYNC) && !stats_host) return CS_OK;
+    rc = fetch_stats(c, s);
+    if (rc) return rc;
+    if (c->h_stats->status & 2) return fail(CS_ERANGE, "no interval covers a block distance");
+    if (!(c->h_stats->status & 1)) {
+      if (stats_host) *stats_host = *c->h_stats;
+      return CS_OK;
+    }
+    if (!(flags & CS_RENDER_SYNC)) {
+      if (stats_host) *stats_host = *c->h_stats;
+      return fail(CS_ENOMEM, "pair buffer overflow (%lld pairs > %lld)",
+                  (long long)c->h_stats->pairs, (long long)c->cap_pairs);
+    }
+    // grow the pair buffers to the observed count and re-run
+    c->cap_pairs = std::min<int64_t>((1ll << 30) - 1, c->h_stats->pairs + c->h_stats->pairs / 4 + 1024);
+    if (c->h_stats->pairs >= (1ll << 30)) return fail(CS_ENOMEM, "more than 2^30 tile pairs");
+  }
+  return fail(CS_ECUDA, "pair buffer did not converge");
+}
+
+int cs_frame_stats_get(cs_ctx* c, cs_frame_stats* out, void* stream) {
+  if (!c || !out) return fail(CS_EINVAL, "NULL argument");
+  CS_CUDA(cudaSetDevice(c->device));
+  int rc = fetch_stats(c, (cudaStream_t)stream);
+  if (rc) return rc;
+  *out = *c->h_stats;
+  return CS_OK;
+}
+
+int cs_dump_projected(cs_ctx* c, double* means, double* conics, double* covs, double* depths,
+                      double* colors, double* opacities, double* radii, int64_t* source,
+                      void* stream) {
+  if (!c || !c->last_order) return fail(CS_EINVAL, "no frame rendered");
+  CS_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = fetch_stats(c, s);
+  if (rc) return rc;
+  const int64_t M = c->h_stats->visible;
+  if (M == 0) return CS_OK;
+  const size_t b = sizeof(double) * M;
+  if (c->scratch1.ensure(b * 15 + 8 * M)) return fail(CS_ENOMEM, "dump");
+  double* base = c->scratch1.as<double>();
+  double *dm = base, *dc = dm + 2 * M, *dv = dc + 3 * M, *dd = dv + 3 * M, *dcol = dd + M,
+         *dop = dcol + 3 * M, *dr = dop + M;
+  int64_t* ds = reinterpret_cast<int64_t*>(dr + 2 * M);
+  launch_dump_projected(c->last_order, c->recs.as<ProjRec>(), c->stats.as<DevStats>(), dm, dc, dv,
+                        dd, dcol, dop, dr, ds, s);
+  CS_CHECK_LAUNCH();
+  struct { void* h; void* d; size_t n; } cp[] = {
+      {means, dm, 2 * b}, {conics, dc, 3 * b}, {covs, dv, 3 * b}, {depths, dd, b},
+      {colors, dcol, 3 * b}, {opacities, dop, b}, {radii, dr, 2 * b}, {source, ds, 8 * (size_t)M}};
+  for (auto& x : cp)
+    if (x.h) CS_CUDA(cudaMemcpyAsync(x.h, x.d, x.n, cudaMemcpyDeviceToHost, s));
+  CS_CUDA(cudaStreamSynchronize(s));
+  return CS_OK;
+}
+
+int cs_dump_tiles(cs_ctx* c, int64_t* tile_ids, int64_t* offsets, void* stream) {
+  if (!c || !c->last_list) return fail(CS_EINVAL, "no frame rendered");
+  CS_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = fetch_stats(c, s);
+  if (rc) return rc;
+  const int64_t P = c->h_stats->pairs;
+  if (c->scratch2.ensure(8 * (P + c->last_tiles + 1))) return fail(CS_ENOMEM, "dump");
+  int64_t* dt = c->scratch2.as<int64_t>();
+  int64_t* doff = dt + P;
+  launch_dump_tiles(c->last_list, c->last_ranges, c->stats.as<DevStats>(), c->last_tiles, dt, doff, s);
+  CS_CHECK_LAUNCH();
+  if (tile_ids && P) CS_CUDA(cudaMemcpyAsync(tile_ids, dt, 8 * P, cudaMemcpyDeviceToHost, s));
+  if (offsets) CS_CUDA(cudaMemcpyAsync(offsets, doff, 8 * (c->last_tiles + 1), cudaMemcpyDeviceToHost, s));
+  CS_CUDA(cudaStreamSynchronize(s));
+  return CS_OK;
+}
+
+int cs_dump_segments(cs_ctx* c, int32_t* cloud_index, int64_t* count, int32_t max_n,
+                     int32_t* n_out, void* stream) {
+  if (!c) return fail(CS_EINVAL, "NULL ctx");
+  CS_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = fetch_stats(c, s);
+  if (rc) return rc;
+  const int n = std::min<int>(c->h_stats->n_segments, max_n);
+  std::vector<Seg> h(std::max(n, 1));
+  if (n) CS_CUDA(cudaMemcpyAsync(h.data(), c->segs.p, sizeof(Seg) * n, cudaMemcpyDeviceToHost, s));
+  CS_CUDA(cudaStreamSynchronize(s));
+  for (int i = 0; i < n; ++i) {
+    cloud_index[i] = h[i].cloud;
+    count[i] = h[i].count;
+  }
+  *n_out = n;
+  return CS_OK;
+}
+
+int cs_dump_assembled_list(cs_ctx* c, uint64_t* packed, int64_t max_n, int64_t* n_out,
+                           void* stream) {
+  if (!c || !packed || !n_out) return fail(CS_EINVAL, "NULL argument");
+  CS_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = fetch_stats(c, s);
+  if (rc) return rc;
+  const int64_t n = std::min<int64_t>(c->h_stats->assembled, max_n);
+  if (n > 0 && c->pw_list.p)
+    CS_CUDA(cudaMemcpyAsync(packed, c->pw_list.p, 8 * n, cudaMemcpyDeviceToHost, s));
+  CS_CUDA(cudaStreamSynchronize(s));
+  *n_out = n;
+  return CS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// LoD API mirror
+
+int cs_decide_visibility(cs_ctx* c, const cs_lod* L, const cs_camera* cam, int32_t force_level,
+                         cs_decision* out_host, void* stream) {
+  if (!c || !L || !cam || !out_host) return fail(CS_EINVAL, "NULL argument");
+  std::lock_guard<std::mutex> lock(c->mu);
+  CS_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = ensure_frame_buffers(c, 1, L->n_levels * L->n_blocks, L->n_blocks, 1, 0);
+  if (rc) return rc;
+  DevStats* stats = c->stats.as<DevStats>();
+  CS_CUDA(cudaMemsetAsync(stats, 0, sizeof(DevStats), s));
+  launch_lod_select(L->tables(), *cam, force_level, c->dec.as<cs_decision>(), c->segs.as<Seg>(),
+                    stats, s);
+  CS_CHECK_LAUNCH();
+  CS_CUDA(cudaMemcpyAsync(out_host, c->dec.p, sizeof(cs_decision) * L->n_blocks,
+                          cudaMemcpyDeviceToHost, s));
+  rc = fetch_stats(c, s);
+  if (rc) return rc;
+  if (c->h_stats->status & 2) return fail(CS_ERANGE, "no interval covers a block distance");
+  return CS_OK;
+}
+
+int cs_block_visible(cs_ctx* c, int32_t n, const double* bmin, const double* bmax,
+                     const cs_camera* cam, uint8_t* vis, double* dist, void* stream) {
+  if (!c || !cam || n < 0) return fail(CS_EINVAL, "bad argument");
+  if (n == 0) return CS_OK;
+  std::lock_guard<std::mutex> lock(c->mu);
+  CS_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (c->scratch3.ensure(64 * (size_t)n)) return fail(CS_ENOMEM, "scratch");
+  double* db = c->scratch3.as<double>();
+  double* dmax = db + 3 * n;
+  double* dd = dmax + 3 * n;
+  uint8_t* dv = reinterpret_cast<uint8_t*>(dd + n);
+  CS_CUDA(cudaMemcpyAsync(db, bmin, 24 * (size_t)n, cudaMemcpyHostToDevice, s));
+  CS_CUDA(cudaMemcpyAsync(dmax, bmax, 24 * (size_t)n, cudaMemcpyHostToDevice, s));
+  launch_block_visible(n, db, dmax, *cam, dv, dd, s);
+  CS_CHECK_LAUNCH();
+  CS_CUDA(cudaMemcpyAsync(vis, dv, n, cudaMemcpyDeviceToHost, s));
+  CS_CUDA(cudaMemcpyAsync(dist, dd, 8 * (size_t)n, cudaMemcpyDeviceToHost, s));
+  CS_CUDA(cudaStreamSynchronize(s));
+  return CS_OK;
+}
+
+int cs_select_level(cs_ctx* c, int32_t n, const double* d, int32_t ni, const double* iv,
+                    int32_t* out, void* stream) {
+  if (!c || n < 0 || ni <= 0) return fail(CS_EINVAL, "bad argument");
+  if (n == 0) return CS_OK;
+  std::lock_guard<std::mutex> lock(c->mu);
+  CS_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (c->scratch4.ensure(8 * (size_t)n + 16 * (size_t)ni + 4 * (size_t)n)) return fail(CS_ENOMEM, "scratch");
+  double* dd = c->scratch4.as<double>();
+  double* div = dd + n;
+  int32_t* dout = reinterpret_cast<int32_t*>(div + 2 * ni);
+  CS_CUDA(cudaMemcpyAsync(dd, d, 8 * (size_t)n, cudaMemcpyHostToDevice, s));
+  CS_CUDA(cudaMemcpyAsync(div, iv, 16 * (size_t)ni, cudaMemcpyHostToDevice, s));
+  launch_select_level(n, dd, ni, div, dout, s);
+  CS_CHECK_LAUNCH();
+  CS_CUDA(cudaMemcpyAsync(out, dout, 4 * (size_t)n, cudaMemcpyDeviceToHost, s));
+  CS_CUDA(cudaStreamSynchronize(s));
+  for (int i = 0; i < n; ++i) {
+    if (out[i] == -2) return fail(CS_EINVAL, "distance must be nonnegative");
+    if (out[i] == -1) return fail(CS_ERANGE, "no interval covers distance %g", d[i]);
+  }
+  return CS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// reference-kernel mirror and core utilities
+
+int cs_blend_tiles(cs_ctx* c, const int64_t* tile_ids, const int64_t* tile_offsets,
+                   int64_t n_tiles, const double* means, const double* conics,
+                   const double* colors, const double* opacities, int64_t n_splats,
+                   const double* background, int32_t tile_size, int32_t width, int32_t height,
+                   int32_t n_tiles_x, double alpha_floor, double t_floor, double* out,
+                   int64_t* fragments, void* stream) {
+  if (!c || !tile_offsets || !out || !fragments || !background)
+    return fail(CS_EINVAL, "NULL argument");
+  if (tile_size < 8 || blend_ppt(tile_size) == 0) return fail(CS_EINVAL, "tile_size");
+  std::lock_guard<std::mutex> lock(c->mu);
+  CS_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t P = 0;
+  CS_CUDA(cudaMemcpyAsync(&P, tile_offsets + n_tiles, 8, cudaMemcpyDeviceToHost, s));
+  double bg[3];
+  CS_CUDA(cudaMemcpyAsync(bg, background, 24, cudaMemcpyDeviceToHost, s));
+  CS_CUDA(cudaStreamSynchronize(s));
+  const int64_t m = std::max<int64_t>(n_splats, 1);
+  if (c->scratch1.ensure((sizeof(HotRec) + sizeof(ColdRec)) * m) ||
+      c->scratch2.ensure(4 * std::max<int64_t>(P, 1) + sizeof(uint2) * n_tiles + 4 * n_tiles) ||
+      c->stats.ensure(sizeof(DevStats)))
+    return fail(CS_ENOMEM, "blend scratch");
+  HotRec* hot = c->scratch1.as<HotRec>();
+  ColdRec* cold = reinterpret_cast<ColdRec*>(hot + m);
+  uint32_t* list = c->scratch2.as<uint32_t>();
+  uint2* ranges = reinterpret_cast<uint2*>(list + std::max<int64_t>(P, 1) + (P & 1 ? 0 : 0));
+  // keep uint2 8-byte aligned
+  ranges = reinterpret_cast<uint2*>((reinterpret_cast<uintptr_t>(ranges) + 7) & ~uintptr_t(7));
+  int32_t* ftile = reinterpret_cast<int32_t*>(ranges + n_tiles);
+  launch_pack(n_splats, means, conics, colors, opacities, alpha_floor, hot, cold, P, tile_ids,
+              n_tiles, tile_offsets, list, ranges, s);
+  CS_CHECK_LAUNCH();
+  CS_CUDA(cudaMemsetAsync(c->stats.p, 0, sizeof(DevStats), s));
+  BlendParams bp;
+  for (int i = 0; i < 3; ++i) bp.bg[i] = bg[i];
+  bp.alpha_floor = alpha_floor;
+  bp.t_floor = t_floor;
+  bp.tile_size = tile_size;
+  bp.width = width;
+  bp.height = height;
+  bp.ntx = n_tiles_x;
+  bp.flags = CS_RENDER_NO_CLIP;
+  launch_blend((int)n_tiles, list, ranges, hot, cold, bp, out, true, ftile, c->stats.as<DevStats>(),
+               nullptr, s);
+  CS_CHECK_LAUNCH();
+  // fragments: int32 per tile -> int64
+  std::vector<int32_t> h(n_tiles);
+  std::vector<int64_t> h64(n_tiles);
+  CS_CUDA(cudaMemcpyAsync(h.data(), ftile, 4 * n_tiles, cudaMemcpyDeviceToHost, s));
+  CS_CUDA(cudaStreamSynchronize(s));
+  for (int64_t t = 0; t < n_tiles; ++t) h64[t] = h[t];
+  CS_CUDA(cudaMemcpy(fragments, h64.data(), 8 * n_tiles, cudaMemcpyHostToDevice));
+  return CS_OK;
+}
+
+int cs_build_covariances(cs_ctx* c, int64_t n, const double* scales, const double* quats,
+                         double* out, void* stream) {
+  if (!c || n < 0) return fail(CS_EINVAL, "bad argument");
+  CS_CUDA(cudaSetDevice(c->device));
+  launch_build_covariances(n, scales, quats, out, (cudaStream_t)stream);
+  CS_CHECK_LAUNCH();
+  return CS_OK;
+}
+
+int cs_sh_to_colors(cs_ctx* c, int64_t n, const double* sh, int32_t coeffs, const double* dirs,
+                    int32_t degree, double* out, void* stream) {
+  if (!c || n < 0) return fail(CS_EINVAL, "bad argument");
+  if (degree < 0 || degree > 3) return fail(CS_EINVAL, "degree must be 0..3");
+  if ((degree + 1) * (degree + 1) > coeffs) return fail(CS_EINVAL, "sh narrower than degree");
+  CS_CUDA(cudaSetDevice(c->device));
+  launch_sh_to_colors(n, sh, coeffs, dirs, degree, out, (cudaStream_t)stream);
+  CS_CHECK_LAUNCH();
+  return CS_OK;
+}
+
+int cs_block_of_points(cs_ctx* c, int64_t n, const void* positions, int32_t f32,
+                       const double* p_min, const double* p_max, int32_t nx, int32_t ny,
+                       int32_t nz, int32_t* out, void* stream) {
+  if (!c || n < 0 || nx < 1 || ny < 1 || nz < 1) return fail(CS_EINVAL, "bad argument");
+  CS_CUDA(cudaSetDevice(c->device));
+  launch_block_of_points(n, positions, f32, p_min, p_max, nx, ny, nz, out, (cudaStream_t)stream);
+  CS_CHECK_LAUNCH();
+  return CS_OK;
+}
+
+int cs_fuse_filter(cs_ctx* c, int64_t n, const void* positions, int32_t f32, const double* p_min,
+                   const double* p_max, int32_t nx, int32_t ny, int32_t nz, int32_t block,
+                   int64_t* kept_idx, int64_t* kept_count, void* stream) {
+  if (!c || n < 0 || nx < 1 || ny < 1 || nz < 1) return fail(CS_EINVAL, "bad argument");
+  std::lock_guard<std::mutex> lock(c->mu);
+  CS_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t chunks = (n + 255) / 256 + 1;
+  if (c->st_fuse.ensure(8 * chunks)) return fail(CS_ENOMEM, "fuse status");
+  CS_CUDA(cudaMemsetAsync(c->st_fuse.p, 0, 8 * chunks, s));
+  CS_CUDA(cudaMemsetAsync(c->fuse_ticket.p, 0, 4, s));
+  launch_fuse_filter(n, positions, f32, p_min, p_max, nx, ny, nz, block, c->st_fuse.as<uint64_t>(),
+                     c->fuse_ticket.as<uint32_t>(), kept_idx, kept_count, s);
+  CS_CHECK_LAUNCH();
+  return CS_OK;
+}
+
+}  // extern "C"

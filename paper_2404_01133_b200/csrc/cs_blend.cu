@@ -1,0 +1,243 @@
+// cs_blend.cu -- K9: per-tile front-to-back alpha blending.
+//
+// Replaces _kernels.blend_tiles (_kernels.py:17-76), the reference's only
+// native kernel.  One CTA per tile, one thread per pixel (tile_size <= 16;
+// 4 or 16 pixels per thread for 32/64).  The tile's splat list (depth-rank
+// order) is streamed through shared memory in batches of 256 HotRec records
+// (48 B each) with cp.async double buffering; each thread walks the batch for
+// its pixel and the CTA leaves as soon as every pixel has terminated
+// (__syncthreads_count).
+//
+// Precision: the quadratic form is float64 in the
+// reference's exact op order (no FMA).  A float64 power below
+// log(alpha_floor / o) - 1e-6 is a guaranteed skip and costs no exp; every
+// other fragment takes the reference path exactly: alpha = min(0.99,
+// o * exp(power)) in float64, float64 alpha/transmittance decisions, so the
+// accepted-fragment set equals the reference's.  Colour accumulates in
+// float64 from float32 splat colours.
+#include "cs_internal.cuh"
+
+namespace cs {
+
+constexpr int kBlendThreads = 256;
+constexpr int kBatch = 256;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int PPT, typename OutT, bool KEEP>
+__global__ void __launch_bounds__(kBlendThreads)
+k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
+        const HotRec* __restrict__ hot, const ColdRec* __restrict__ cold, BlendParams bp,
+        OutT* __restrict__ out, int32_t* __restrict__ frag_tile, DevStats* __restrict__ stats,
+        BlendState state) {
+  __shared__ __align__(16) HotRec buf[2][kBatch];
+  __shared__ int s_red[kBlendThreads / 32];
+  const int t = blockIdx.x;
+  const int tx = t % bp.ntx, ty = t / bp.ntx;
+  const int ts = bp.tile_size;
+  const uint2 rg = ranges[t];
+  const int64_t s0 = rg.x, s1 = rg.y;
+
+  double sx[PPT], sy[PPT], T[PPT], cr[PPT], cg[PPT], cb[PPT];
+  int cnt[PPT], last[PPT];
+  bool done[PPT], valid[PPT];
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    const int li = threadIdx.x + q * kBlendThreads;
+    const int lx = li % ts, ly = li / ts;
+    const int px = tx * ts + lx, py = ty * ts + ly;
+    valid[q] = li < ts * ts && px < bp.width && py < bp.height;
+    sx[q] = (double)px + 0.5;  // pixel centres (_kernels.py:43-45)
+    sy[q] = (double)py + 0.5;
+    T[q] = 1.0; cr[q] = 0.0; cg[q] = 0.0; cb[q] = 0.0;
+    cnt[q] = 0; last[q] = (int)s0;
+    done[q] = !valid[q];
+  }
+
+  const int64_t n = s1 - s0;
+  const int nbatches = (int)((n + kBatch - 1) / kBatch);
+  // prefetch batch 0
+  if (nbatches > 0 && threadIdx.x < n) {
+    const uint32_t rk = __ldg(list + s0 + threadIdx.x);
+    const char* g = reinterpret_cast<const char*>(hot + rk);
+    char* d = reinterpret_cast<char*>(&buf[0][threadIdx.x]);
+    cp_async16(d, g); cp_async16(d + 16, g + 16); cp_async16(d + 32, g + 32);
+  }
+  cp_async_commit();
+  for (int b = 0; b < nbatches; ++b) {
+    const int64_t bstart = s0 + (int64_t)b * kBatch;
+    if (b + 1 < nbatches) {
+      const int64_t k = bstart + kBatch + threadIdx.x;
+      if (k < s1) {
+        const uint32_t rk = __ldg(list + k);
+        const char* g = reinterpret_cast<const char*>(hot + rk);
+        char* d = reinterpret_cast<char*>(&buf[(b + 1) & 1][threadIdx.x]);
+        cp_async16(d, g); cp_async16(d + 16, g + 16); cp_async16(d + 32, g + 32);
+      }
+    }
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const HotRec* hb = buf[b & 1];
+    const int nb = (int)min((int64_t)kBatch, s1 - bstart);
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      if (done[q]) continue;
+      double Tq = T[q];
+      for (int j = 0; j < nb; ++j) {
+        const HotRec h = hb[j];
+        const double dx = dsub(sx[q], h.mx);
+        const double dy = dsub(sy[q], h.my);
+        // -0.5 * (c0*dx*dx + c2*dy*dy) - c1*dx*dy   (_kernels.py:54-57)
+        const double power =
+            dsub(dmul(-0.5, dadd(dmul(dmul(h.c0, dx), dx), dmul(dmul(h.c2, dy), dy))),
+                 dmul(dmul(h.c1, dx), dy));
+        if (power < (double)h.lthr) continue;  // alpha < alpha_floor guaranteed
+        const ColdRec c = cold[h.rank];
+        double alpha = dmul(c.opacity, exp(power));  // _kernels.py:58
+        if (alpha > 0.99) alpha = 0.99;              // _kernels.py:59-60
+        if (alpha < bp.alpha_floor) continue;        // _kernels.py:61-62
+        const double nt = dmul(Tq, dsub(1.0, alpha));
+        if (nt < bp.t_floor) { done[q] = true; break; }  // _kernels.py:63-66
+        const double w = dmul(Tq, alpha);
+        cr[q] += w * (double)c.r;
+        cg[q] += w * (double)c.g;
+        cb[q] += w * (double)c.b;
+        Tq = nt;
+        cnt[q] += 1;
+        last[q] = (int)(bstart + j + 1);
+      }
+      T[q] = Tq;
+    }
+    int alive = 0;
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) alive |= done[q] ? 0 : 1;
+    if (__syncthreads_count(alive) == 0) break;
+  }
+  cp_async_wait<0>();
+  int my = 0;
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    if (!valid[q]) continue;
+    my += cnt[q];
+    const int li = threadIdx.x + q * kBlendThreads;
+    const int px = tx * ts + li % ts, py = ty * ts + li / ts;
+    const int64_t pix = (int64_t)py * bp.width + px;
+    double o[3] = {cr[q] + T[q] * bp.bg[0], cg[q] + T[q] * bp.bg[1], cb[q] + T[q] * bp.bg[2]};
+    if (!(bp.flags & CS_RENDER_NO_CLIP)) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) o[c] = o[c] < 0.0 ? 0.0 : (o[c] > 1.0 ? 1.0 : o[c]);
+    }
+    out[3 * pix] = (OutT)o[0];
+    out[3 * pix + 1] = (OutT)o[1];
+    out[3 * pix + 2] = (OutT)o[2];
+    if (KEEP) {
+      state.final_t[pix] = (float)T[q];
+      state.last[pix] = last[q];
+      state.color_acc[3 * pix] = (float)cr[q];
+      state.color_acc[3 * pix + 1] = (float)cg[q];
+      state.color_acc[3 * pix + 2] = (float)cb[q];
+    }
+  }
+  my = warp_sum(my);
+  if (lane_id() == 0) s_red[threadIdx.x >> 5] = my;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int w = 0; w < kBlendThreads / 32; ++w) tot += s_red[w];
+    frag_tile[t] = tot;
+    if (tot) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->fragments),
+                       (unsigned long long)tot);
+  }
+}
+
+template <typename OutT, bool KEEP>
+static void launch_blend_t(int ppt, int n_tiles, const uint32_t* list, const uint2* ranges,
+                           const HotRec* hot, const ColdRec* cold, const BlendParams& bp,
+                           OutT* out, int32_t* frag_tile, DevStats* stats, BlendState st,
+                           cudaStream_t s) {
+  if (ppt == 1)
+    k_blend<1, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, ranges, hot, cold, bp, out,
+                                                            frag_tile, stats, st);
+  else if (ppt == 4)
+    k_blend<4, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, ranges, hot, cold, bp, out,
+                                                            frag_tile, stats, st);
+  else
+    k_blend<16, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, ranges, hot, cold, bp, out,
+                                                             frag_tile, stats, st);
+}
+
+int blend_ppt(int tile_size) {
+  const int px = tile_size * tile_size;
+  if (px <= 256) return 1;
+  if (px <= 1024) return 4;
+  if (px <= 4096) return 16;
+  return 0;
+}
+
+void launch_blend(int n_tiles, const uint32_t* list, const uint2* ranges, const HotRec* hot,
+                  const ColdRec* cold, const BlendParams& bp, void* out, bool f64_out,
+                  int32_t* frag_tile, DevStats* stats, const BlendState* keep, cudaStream_t s) {
+  const int ppt = blend_ppt(bp.tile_size);
+  BlendState st = keep ? *keep : BlendState{nullptr, nullptr, nullptr};
+  if (f64_out) {
+    if (keep) launch_blend_t<double, true>(ppt, n_tiles, list, ranges, hot, cold, bp, (double*)out, frag_tile, stats, st, s);
+    else launch_blend_t<double, false>(ppt, n_tiles, list, ranges, hot, cold, bp, (double*)out, frag_tile, stats, st, s);
+  } else {
+    if (keep) launch_blend_t<float, true>(ppt, n_tiles, list, ranges, hot, cold, bp, (float*)out, frag_tile, stats, st, s);
+    else launch_blend_t<float, false>(ppt, n_tiles, list, ranges, hot, cold, bp, (float*)out, frag_tile, stats, st, s);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// cs_blend_tiles: the numba kernel's exact interface (_kernels.py:18-30).
+// Packs the caller's float64 arrays into HotRec/ColdRec and the int64 CSR
+// into (list, ranges); then runs the same blend kernel.
+
+__global__ void k_pack_records(int64_t m, const double* means, const double* conics,
+                               const double* colors, const double* opac, double alpha_floor,
+                               HotRec* hot, ColdRec* cold) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    HotRec h;
+    h.mx = means[2 * s]; h.my = means[2 * s + 1];
+    h.c0 = conics[3 * s]; h.c1 = conics[3 * s + 1]; h.c2 = conics[3 * s + 2];
+    const double o = opac[s];
+    const double lt = o > 0.0 ? log(alpha_floor / o) - 1e-6
+                              : __longlong_as_double(0x7ff0000000000000ll);
+    h.lthr = __double2float_rd(lt);
+    h.rank = (uint32_t)s;
+    hot[s] = h;
+    ColdRec c;
+    c.opacity = o;
+    c.r = (float)colors[3 * s]; c.g = (float)colors[3 * s + 1]; c.b = (float)colors[3 * s + 2];
+    c.pad = 0.f; c.pad2 = 0.0;
+    cold[s] = c;
+  }
+}
+
+__global__ void k_pack_tiles(int64_t p, const int64_t* tile_ids, int64_t n_tiles,
+                             const int64_t* offsets, uint32_t* list, uint2* ranges) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p; i += stride)
+    list[i] = (uint32_t)tile_ids[i];
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_tiles; t += stride)
+    ranges[t] = make_uint2((uint32_t)offsets[t], (uint32_t)offsets[t + 1]);
+}
+
+void launch_pack(int64_t m, const double* means, const double* conics, const double* colors,
+                 const double* opac, double alpha_floor, HotRec* hot, ColdRec* cold, int64_t p,
+                 const int64_t* tile_ids, int64_t n_tiles, const int64_t* offsets, uint32_t* list,
+                 uint2* ranges, cudaStream_t s) {
+  if (m > 0)
+    k_pack_records<<<148 * 4, 256, 0, s>>>(m, means, conics, colors, opac, alpha_floor, hot, cold);
+  k_pack_tiles<<<148 * 4, 256, 0, s>>>(p, tile_ids, n_tiles, offsets, list, ranges);
+}
+
+}  // namespace cs

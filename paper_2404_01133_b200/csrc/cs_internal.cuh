@@ -1,0 +1,267 @@
+// cs_internal.cuh -- shared device-side types and primitives for libcsgpu.
+//
+// Layouts in HBM:
+//   ProjRec   : 128 B per visible splat, compact (assembled-index) order
+//   HotRec    :  48 B per visible splat, depth-rank order -- staged in smem by the blend
+//   ColdRec   :  32 B per visible splat, depth-rank order -- read only for accepted fragments
+//   pairs     :  u32 tile key + u32 depth rank, sorted stably by tile
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/cs_api.h"
+
+namespace cs {
+
+constexpr int kWarp = 32;
+
+// Status word for decoupled look-back scans (single-pass chained scan).
+// bits 63..62: 0 = not ready, 1 = aggregate only, 2 = inclusive prefix.
+constexpr uint64_t kFlagAgg = 1ull << 62;
+constexpr uint64_t kFlagPre = 2ull << 62;
+constexpr uint64_t kValMask = (1ull << 62) - 1;
+
+struct Seg {          // one assembled piece: levels[L][j] (or the single cloud)
+  int64_t start;      // first assembled index of this piece
+  int64_t count;
+  int32_t cloud;      // index into the descriptor table
+  int32_t pad;
+};
+
+struct __align__(16) ProjRec {
+  double mx, my;        // mean2d  (render.py:128-129)
+  double c0, c1, c2;    // conic   (render.py:172)
+  double a, b, c;       // cov2d + low-pass (render.py:142-144)
+  double rx, ry;        // marginal support radii (render.py:153-154)
+  double opacity;
+  double depth;         // camera z
+  float r, g, bl;       // SH colour (fp32 of the float64 value)
+  uint32_t pad;
+  int64_t src;          // assembled index
+  int64_t pad2;
+};
+static_assert(sizeof(ProjRec) == 128, "ProjRec layout");
+
+struct __align__(16) HotRec {   // what every (pixel, splat) evaluation reads
+  double mx, my, c0, c1, c2;
+  float lthr;                    // fast-reject threshold on power (<= log(alpha_floor/o) - margin)
+  uint32_t rank;                 // depth rank, index into ColdRec
+};
+static_assert(sizeof(HotRec) == 48, "HotRec layout");
+
+struct __align__(16) ColdRec {  // read only when a fragment may be accepted
+  double opacity;
+  float r, g, b, pad;
+  double pad2;
+};
+static_assert(sizeof(ColdRec) == 32, "ColdRec layout");
+
+struct DevStats {     // device mirror of cs_frame_stats + scratch counters
+  int64_t assembled;
+  int64_t visible;
+  int64_t skipped;
+  int64_t pairs;
+  int64_t fragments;
+  int32_t n_segs;
+  int32_t status;
+  int64_t pairs_eff;     // pairs actually processed (0 when the pair buffer overflowed)
+  uint32_t tickets[16];  // chunk tickets for single-pass kernels, zeroed per frame
+};
+
+
+// LoD scene tables on device (cs_lod.cu)
+struct LodTables {
+  const cs_cloud* clouds;      // [L*J] level-major
+  const double* bmin;          // [J*3]
+  const double* bmax;
+  const double* intervals;     // [L*2] (lo, hi), nearest-first
+  const uint8_t* occupied;     // [J]
+  const Seg* all_segs;         // [L*J] level-major virtual concatenation (pointwise mode)
+  int n_levels, n_blocks;
+  int64_t total_all;
+};
+
+// blend kernel parameters (cs_blend.cu)
+struct BlendParams {
+  double bg[3];
+  double alpha_floor, t_floor;
+  int tile_size, width, height, ntx;
+  uint32_t flags;
+};
+
+struct BlendState {  // per-pixel state kept for the backward pass
+  float* final_t;       // (H*W) final transmittance
+  int32_t* last;        // (H*W) list position one past the last accepted fragment
+  float* color_acc;     // (H*W*3) sum of w*c (before the background term)
+};
+
+// ---------------------------------------------------------------------------
+// no-FMA float64 arithmetic in numpy order
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// numpy float64 -> int64 cast (x86 cvttsd2si: out of range / NaN -> INT64_MIN)
+__device__ __forceinline__ int64_t np_to_i64(double x) {
+  if (!(x >= -9223372036854775808.0 && x < 9223372036854775808.0)) return INT64_MIN;
+  return (int64_t)x;
+}
+__device__ __forceinline__ int64_t clip_i64(int64_t v, int64_t lo, int64_t hi) {
+  return v < lo ? lo : (v > hi ? hi : v);
+}
+
+// ---------------------------------------------------------------------------
+// warp / block primitives
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T n = __shfl_up_sync(0xffffffffu, v, o);
+    if ((int)lane_id() >= o) v += n;
+  }
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide exclusive scan of one value per thread; returns exclusive prefix,
+// writes the block total.  `scratch` needs (blockDim/32 + 1) entries.
+template <typename T>
+__device__ __forceinline__ T block_excl_scan(T v, T* scratch, T& total) {
+  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  T incl = warp_incl_scan(v);
+  if (lane_id() == 31) scratch[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    T w = (int)lane_id() < nwarps ? scratch[lane_id()] : T(0);
+    T wi = warp_incl_scan(w);
+    if ((int)lane_id() < nwarps) scratch[lane_id()] = wi - w;
+    if (lane_id() == 31) scratch[nwarps] = wi;
+  }
+  __syncthreads();
+  T res = incl - v + scratch[warp];
+  total = scratch[nwarps];
+  __syncthreads();
+  return res;
+}
+
+__device__ __forceinline__ uint64_t ld_volatile_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Decoupled look-back (single-pass chained scan).  Called by ALL lanes of
+// warp 0 of the block owning `chunk` (chunks handed out in launch order by a
+// ticket counter, so every predecessor is resident or finished).  Publishes
+// the aggregate, walks back over predecessors 32 at a time and returns the
+// exclusive prefix of this chunk; publishes the inclusive prefix.
+__device__ __forceinline__ uint64_t lookback_exclusive(uint64_t* status, int64_t chunk,
+                                                       uint64_t aggregate) {
+  const uint32_t lane = lane_id();
+  if (chunk == 0) {
+    if (lane == 0) st_release_u64(&status[0], kFlagPre | aggregate);
+    return 0;
+  }
+  if (lane == 0) st_release_u64(&status[chunk], kFlagAgg | aggregate);
+  uint64_t exclusive = 0;
+  int64_t pred = chunk - 1;
+  while (true) {
+    int64_t idx = pred - (int64_t)lane;
+    uint64_t s = idx >= 0 ? ld_volatile_u64(&status[idx]) : (kFlagPre | 0ull);
+    while (__any_sync(0xffffffffu, (s >> 62) == 0)) {
+      if ((s >> 62) == 0) s = ld_volatile_u64(&status[idx]);
+    }
+    uint32_t pre_mask = __ballot_sync(0xffffffffu, (s >> 62) == 2);
+    uint64_t v = s & kValMask;
+    if (pre_mask) {
+      int first = __ffs(pre_mask) - 1;
+      uint64_t contrib = (int)lane <= first ? v : 0ull;
+      exclusive += warp_sum(contrib);
+      break;
+    }
+    exclusive += warp_sum(v);
+    pred -= 32;
+  }
+  if (lane == 0) st_release_u64(&status[chunk], kFlagPre | (exclusive + aggregate));
+  return exclusive;
+}
+
+// ---------------------------------------------------------------------------
+// geometry loads (fp32 or fp64 quads)
+struct Geom {
+  double px, py, pz, op;
+  double sx, sy, sz;
+  double qw, qx, qy, qz;
+};
+
+__device__ __forceinline__ Geom load_geom(const cs_cloud& c, int64_t k) {
+  Geom g;
+  if (c.fp64) {
+    const double2* p = reinterpret_cast<const double2*>(c.pos_op) + 2 * k;
+    const double2* s = reinterpret_cast<const double2*>(c.scale) + 2 * k;
+    const double2* q = reinterpret_cast<const double2*>(c.quat) + 2 * k;
+    double2 p0 = __ldg(p), p1 = __ldg(p + 1), s0 = __ldg(s), s1 = __ldg(s + 1), q0 = __ldg(q),
+            q1 = __ldg(q + 1);
+    g.px = p0.x; g.py = p0.y; g.pz = p1.x; g.op = p1.y;
+    g.sx = s0.x; g.sy = s0.y; g.sz = s1.x;
+    g.qw = q0.x; g.qx = q0.y; g.qy = q1.x; g.qz = q1.y;
+  } else {
+    float4 p = __ldg(reinterpret_cast<const float4*>(c.pos_op) + k);
+    float4 s = __ldg(reinterpret_cast<const float4*>(c.scale) + k);
+    float4 q = __ldg(reinterpret_cast<const float4*>(c.quat) + k);
+    g.px = p.x; g.py = p.y; g.pz = p.z; g.op = p.w;
+    g.sx = s.x; g.sy = s.y; g.sz = s.z;
+    g.qw = q.x; g.qx = q.y; g.qy = q.z; g.qz = q.w;
+  }
+  return g;
+}
+
+__device__ __forceinline__ void load_pos(const cs_cloud& c, int64_t k, double& x, double& y,
+                                         double& z) {
+  if (c.fp64) {
+    const double2* p = reinterpret_cast<const double2*>(c.pos_op) + 2 * k;
+    double2 p0 = __ldg(p), p1 = __ldg(p + 1);
+    x = p0.x; y = p0.y; z = p1.x;
+  } else {
+    float4 p = __ldg(reinterpret_cast<const float4*>(c.pos_op) + k);
+    x = p.x; y = p.y; z = p.z;
+  }
+}
+
+// Upper-bound binary search over segment starts: last s with seg[s].start <= i.
+__device__ __forceinline__ int find_seg(const Seg* segs, int n, int64_t i) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (segs[mid].start <= i) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+}  // namespace cs

@@ -1,0 +1,371 @@
+// cs_project.cu -- K3: EWA projection + SH colour + visible-set compaction.
+//
+// Replaces render._project_cloud (render.py:111-188) up to the depth sort.
+// One thread per assembled Gaussian; chunks of 256 assembled indices are
+// handed out in launch order and compacted with a decoupled look-back scan, so
+// visible splats land in ascending assembled order (the np.nonzero order of
+// render.py:121/163) in a single pass over HBM.
+//
+// All decision math (cull, mean, covariance, conic, radii, on-image test) is
+// float64 written with explicit round-to-nearest intrinsics in numpy's
+// operation order (no FMA contraction), so results are bit-identical to the
+// reference run under OPENBLAS_CORETYPE=Sandybridge.
+#include "cs_internal.cuh"
+
+namespace cs {
+
+__constant__ double kShC0 = 0.28209479177387814;
+__constant__ double kShC1 = 0.4886025119029199;
+__constant__ double kShC2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
+                                -1.0925484305920792, 0.5462742152960396};
+__constant__ double kShC3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658,
+                                0.3731763325901154, -0.4570457994644658, 1.445305721320277,
+                                -0.5900435899266435};
+
+__device__ __forceinline__ int degree_of(int c) { return c >= 16 ? 3 : c >= 9 ? 2 : c >= 4 ? 1 : 0; }
+
+// eval_sh_basis (core.py:114-146) fused with sh_to_colors (core.py:166-172):
+// colour = clip(0.5 + sum_n sh[c, n] * Y_n(dir), 0, 1).  Tolerance-only
+// quantity (the reference sums through numpy einsum), evaluated in float64.
+__device__ void sh_colour(const float* row, int C, int degree, double x, double y, double z,
+                          double out[3]) {
+  double basis[16];
+  basis[0] = kShC0;
+  if (degree >= 1) {
+    basis[1] = -kShC1 * y;
+    basis[2] = kShC1 * z;
+    basis[3] = -kShC1 * x;
+  }
+  if (degree >= 2) {
+    double xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    basis[4] = kShC2[0] * xy;
+    basis[5] = kShC2[1] * yz;
+    basis[6] = kShC2[2] * (2.0 * zz - xx - yy);
+    basis[7] = kShC2[3] * xz;
+    basis[8] = kShC2[4] * (xx - yy);
+    if (degree >= 3) {
+      basis[9] = kShC3[0] * y * (3.0 * xx - yy);
+      basis[10] = kShC3[1] * xy * z;
+      basis[11] = kShC3[2] * y * (4.0 * zz - xx - yy);
+      basis[12] = kShC3[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+      basis[13] = kShC3[4] * x * (4.0 * zz - xx - yy);
+      basis[14] = kShC3[5] * z * (xx - yy);
+      basis[15] = kShC3[6] * x * (xx - 3.0 * yy);
+    }
+  }
+  const int nb = (degree + 1) * (degree + 1);
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    double acc = 0.0;
+    const float* cr = row + ch * C;
+    for (int n = 0; n < nb; ++n) acc += (double)__ldg(cr + n) * basis[n];
+    double v = 0.5 + acc;
+    out[ch] = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+  }
+}
+
+struct ProjOut {
+  bool in_front, ok, keep;
+  double z, mx, my, a, b, c, det, rx, ry;
+};
+
+// Decision math of render.py:118-160 for one Gaussian, numpy op order.
+__device__ __forceinline__ ProjOut project_one(const Geom& g, const cs_camera& cam,
+                                               const cs_settings& st) {
+  ProjOut o;
+  const double* R = cam.R;
+  double t0 = dadd(dadd(dadd(dmul(g.px, R[0]), dmul(g.py, R[1])), dmul(g.pz, R[2])), cam.t[0]);
+  double t1 = dadd(dadd(dadd(dmul(g.px, R[3]), dmul(g.py, R[4])), dmul(g.pz, R[5])), cam.t[1]);
+  double z = dadd(dadd(dadd(dmul(g.px, R[6]), dmul(g.py, R[7])), dmul(g.pz, R[8])), cam.t[2]);
+  o.z = z;
+  o.in_front = z > st.near_plane;            // render.py:120
+  o.ok = false;
+  o.keep = false;
+  if (!o.in_front) return o;
+  o.mx = dadd(ddiv(dmul(cam.fx, t0), z), cam.cx);   // render.py:128
+  o.my = dadd(ddiv(dmul(cam.fy, t1), z), cam.cy);   // render.py:129
+  // quat_to_rotmat, core.py:74-82
+  const double w = g.qw, x = g.qx, y = g.qy, q = g.qz;
+  double r[9];
+  r[0] = dsub(1.0, dmul(2.0, dadd(dmul(y, y), dmul(q, q))));
+  r[1] = dmul(2.0, dsub(dmul(x, y), dmul(w, q)));
+  r[2] = dmul(2.0, dadd(dmul(x, q), dmul(w, y)));
+  r[3] = dmul(2.0, dadd(dmul(x, y), dmul(w, q)));
+  r[4] = dsub(1.0, dmul(2.0, dadd(dmul(x, x), dmul(q, q))));
+  r[5] = dmul(2.0, dsub(dmul(y, q), dmul(w, x)));
+  r[6] = dmul(2.0, dsub(dmul(x, q), dmul(w, y)));
+  r[7] = dmul(2.0, dadd(dmul(y, q), dmul(w, x)));
+  r[8] = dsub(1.0, dmul(2.0, dadd(dmul(x, x), dmul(y, y))));
+  // build_covariances (core.py:107-111): rs = r * s^2 ; einsum kij,klj->kil.
+  // numpy's contiguous 2-lane sum-of-products adds the three terms (t0 + t2) + t1.
+  const double s2[3] = {dmul(g.sx, g.sx), dmul(g.sy, g.sy), dmul(g.sz, g.sz)};
+  double rs[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) rs[3 * i + j] = dmul(r[3 * i + j], s2[j]);
+  double sig[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int l = 0; l < 3; ++l)
+      sig[3 * i + l] = dadd(dadd(dmul(rs[3 * i + 0], r[3 * l + 0]), dmul(rs[3 * i + 2], r[3 * l + 2])),
+                            dmul(rs[3 * i + 1], r[3 * l + 1]));
+  // V = W Sigma W^T, einsum ij,kjl,ml->kim: ((W_ij * S_jl) * W_ml), j-major l-minor (render.py:133)
+  double V[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int m = i; m < 3; ++m) {
+      double acc = dmul(dmul(R[3 * i + 0], sig[0]), R[3 * m + 0]);
+#pragma unroll
+      for (int jl = 1; jl < 9; ++jl) {
+        const int j = jl / 3, l = jl % 3;
+        acc = dadd(acc, dmul(dmul(R[3 * i + j], sig[3 * j + l]), R[3 * m + l]));
+      }
+      V[3 * i + m] = acc;
+    }
+  // cov2d = J V J^T (render.py:136-141); J has zeros at (0,1) and (1,0), which
+  // add exact zeros in numpy's 9-term sum and are skipped here.
+  const double zz = dmul(z, z);
+  const double j00 = ddiv(cam.fx, z);
+  const double j02 = ddiv(dmul(-cam.fx, t0), zz);
+  const double j11 = ddiv(cam.fy, z);
+  const double j12 = ddiv(dmul(-cam.fy, t1), zz);
+  // V entries below the diagonal: recompute in numpy order (V is symmetric only
+  // up to rounding, so compute the exact (i, m) entry used).
+  double V20, V21;
+  {
+    double acc = dmul(dmul(R[6], sig[0]), R[0]);
+#pragma unroll
+    for (int jl = 1; jl < 9; ++jl) {
+      const int j = jl / 3, l = jl % 3;
+      acc = dadd(acc, dmul(dmul(R[6 + j], sig[3 * j + l]), R[l]));
+    }
+    V20 = acc;
+    acc = dmul(dmul(R[6], sig[0]), R[3]);
+#pragma unroll
+    for (int jl = 1; jl < 9; ++jl) {
+      const int j = jl / 3, l = jl % 3;
+      acc = dadd(acc, dmul(dmul(R[6 + j], sig[3 * j + l]), R[3 + l]));
+    }
+    V21 = acc;
+  }
+  const double V00 = V[0], V01 = V[1], V02 = V[2], V11 = V[4], V12 = V[5], V22 = V[8];
+  // cov2d[0][0]: terms (0,0),(0,2),(2,0),(2,2) with t_jl = (J0j V_jl) J0l
+  double c00 = dmul(dmul(j00, V00), j00);
+  c00 = dadd(c00, dmul(dmul(j00, V02), j02));
+  c00 = dadd(c00, dmul(dmul(j02, V20), j00));
+  c00 = dadd(c00, dmul(dmul(j02, V22), j02));
+  // cov2d[0][1]: (0,1),(0,2),(2,1),(2,2) with t_jl = (J0j V_jl) J1l
+  double c01 = dmul(dmul(j00, V01), j11);
+  c01 = dadd(c01, dmul(dmul(j00, V02), j12));
+  c01 = dadd(c01, dmul(dmul(j02, V21), j11));
+  c01 = dadd(c01, dmul(dmul(j02, V22), j12));
+  // cov2d[1][1]: (1,1),(1,2),(2,1),(2,2) with t_jl = (J1j V_jl) J1l
+  double c11 = dmul(dmul(j11, V11), j11);
+  c11 = dadd(c11, dmul(dmul(j11, V12), j12));
+  c11 = dadd(c11, dmul(dmul(j12, V21), j11));
+  c11 = dadd(c11, dmul(dmul(j12, V22), j12));
+  o.a = dadd(c00, st.low_pass);                // render.py:142-144
+  o.b = c01;
+  o.c = dadd(c11, st.low_pass);
+  o.det = dsub(dmul(o.a, o.c), dmul(o.b, o.b)); // render.py:146
+  o.ok = o.det > st.singular_det;              // render.py:147
+  o.rx = dmul(st.support_sigmas, __dsqrt_rn(o.a));  // render.py:153-154
+  o.ry = dmul(st.support_sigmas, __dsqrt_rn(o.c));
+  const bool on_image = (dadd(o.mx, o.rx) > 0.0) && (dsub(o.mx, o.rx) < (double)cam.width) &&
+                        (dadd(o.my, o.ry) > 0.0) && (dsub(o.my, o.ry) < (double)cam.height);
+  o.keep = o.ok && on_image;                   // render.py:156-161
+  return o;
+}
+
+constexpr int kProjThreads = 256;
+
+// Single-pass projection + stable compaction.
+__global__ void __launch_bounds__(kProjThreads)
+k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
+          DevStats* __restrict__ stats, cs_camera cam, cs_settings st,
+          uint64_t* __restrict__ status, uint64_t* __restrict__ keys_out,
+          uint32_t* __restrict__ vals_out, ProjRec* __restrict__ recs,
+          const uint64_t* __restrict__ list) {
+  __shared__ int64_t s_chunk;
+  __shared__ uint32_t s_scan[kProjThreads / 32 + 1];
+  __shared__ uint32_t s_skip[kProjThreads / 32];
+  __shared__ uint64_t s_prefix;
+  const int64_t n = stats->assembled;
+  if (threadIdx.x == 0) s_chunk = atomicAdd(&stats->tickets[0], 1u);
+  __syncthreads();
+  const int64_t chunk = s_chunk;
+  const int64_t base = chunk * kProjThreads;
+  if (base >= n) return;
+  const int64_t i = base + threadIdx.x;
+  ProjOut po;
+  po.in_front = po.ok = po.keep = false;
+  Geom g;
+  int64_t local = 0;
+  int cloud_id = 0;
+  if (i < n) {
+    const int si = find_seg(segs, stats->n_segs, i);
+    const Seg sg = segs[si];
+    cloud_id = sg.cloud;
+    local = i - sg.start;
+    if (cloud_id < 0) {  // pointwise list mode: packed (cloud << 40 | local)
+      const uint64_t e = list[i];
+      cloud_id = (int)(e >> 40);
+      local = (int64_t)(e & ((1ull << 40) - 1));
+    }
+    g = load_geom(clouds[cloud_id], local);
+    po = project_one(g, cam, st);
+  }
+  // skipped_singular: in front but det <= 1e-12 (render.py:146-148)
+  uint32_t skip = (po.in_front && !po.ok) ? 1u : 0u;
+  uint32_t wskip = warp_sum(skip);
+  if (lane_id() == 0) s_skip[threadIdx.x >> 5] = wskip;
+  uint32_t total;
+  uint32_t excl = block_excl_scan<uint32_t>(po.keep ? 1u : 0u, s_scan, total);
+  if (threadIdx.x < 32) {
+    uint32_t ws = threadIdx.x < kProjThreads / 32 ? s_skip[threadIdx.x] : 0u;
+    ws = warp_sum(ws);
+    uint64_t pre = lookback_exclusive(status, chunk, total);
+    if (threadIdx.x == 0) {
+      s_prefix = pre;
+      if (ws) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->skipped),
+                        (unsigned long long)ws);
+      if (base + kProjThreads >= n) stats->visible = (int64_t)(pre + total);
+    }
+  }
+  __syncthreads();
+  if (!po.keep) return;
+  const uint64_t idx = s_prefix + excl;
+  const cs_cloud& cd = clouds[cloud_id];
+  // view direction and SH colour (render.py:167-169, core.py:166-172)
+  double dx = g.px - cam.center[0], dy = g.py - cam.center[1], dz = g.pz - cam.center[2];
+  double nrm = sqrt((dx * dx + dy * dy) + dz * dz);
+  int degree = min((int)st.sh_degree, degree_of(cd.sh_coeffs));
+  double col[3];
+  sh_colour(cd.sh + local * cd.sh_stride, cd.sh_coeffs, degree, dx / nrm, dy / nrm, dz / nrm, col);
+  ProjRec rec;
+  rec.mx = po.mx;
+  rec.my = po.my;
+  rec.c0 = ddiv(po.c, po.det);    // render.py:172
+  rec.c1 = ddiv(-po.b, po.det);
+  rec.c2 = ddiv(po.a, po.det);
+  rec.a = po.a;
+  rec.b = po.b;
+  rec.c = po.c;
+  rec.rx = po.rx;
+  rec.ry = po.ry;
+  rec.opacity = g.op;
+  rec.depth = po.z;
+  rec.r = (float)col[0];
+  rec.g = (float)col[1];
+  rec.bl = (float)col[2];
+  rec.pad = 0;
+  rec.src = i;
+  rec.pad2 = 0;
+  recs[idx] = rec;
+  keys_out[idx] = (uint64_t)__double_as_longlong(po.z);  // z > near > 0: bits are monotone
+  vals_out[idx] = (uint32_t)idx;
+}
+
+// Single-cloud source: one segment covering the whole cloud.
+__global__ void k_setup_cloud(cs_cloud c, cs_cloud* clouds, Seg* segs, DevStats* stats) {
+  clouds[0] = c;
+  segs[0].start = 0;
+  segs[0].count = c.count;
+  segs[0].cloud = 0;
+  segs[0].pad = 0;
+  stats->n_segs = 1;
+  stats->assembled = c.count;
+}
+
+void launch_project(const cs_cloud* d_clouds, const Seg* d_segs, DevStats* d_stats,
+                    const cs_camera& cam, const cs_settings& st, uint64_t* status,
+                    int64_t capacity, uint64_t* keys, uint32_t* vals, ProjRec* recs,
+                    const uint64_t* list, cudaStream_t s) {
+  const int64_t chunks = (capacity + kProjThreads - 1) / kProjThreads;
+  if (chunks == 0) return;
+  k_project<<<(unsigned)chunks, kProjThreads, 0, s>>>(d_clouds, d_segs, d_stats, cam, st, status,
+                                                      keys, vals, recs, list);
+}
+
+void launch_setup_cloud(const cs_cloud& c, cs_cloud* d_clouds, Seg* d_segs, DevStats* d_stats,
+                        cudaStream_t s) {
+  k_setup_cloud<<<1, 1, 0, s>>>(c, d_clouds, d_segs, d_stats);
+}
+
+// ---------------------------------------------------------------------------
+// core.py utilities on device (API mirror: build_covariances, sh_to_colors)
+
+__global__ void k_build_covariances(int64_t n, const double* scales, const double* quats,
+                                    double* out) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  Geom g;
+  g.sx = scales[3 * k]; g.sy = scales[3 * k + 1]; g.sz = scales[3 * k + 2];
+  g.qw = quats[4 * k]; g.qx = quats[4 * k + 1]; g.qy = quats[4 * k + 2]; g.qz = quats[4 * k + 3];
+  const double w = g.qw, x = g.qx, y = g.qy, q = g.qz;
+  double r[9];
+  r[0] = dsub(1.0, dmul(2.0, dadd(dmul(y, y), dmul(q, q))));
+  r[1] = dmul(2.0, dsub(dmul(x, y), dmul(w, q)));
+  r[2] = dmul(2.0, dadd(dmul(x, q), dmul(w, y)));
+  r[3] = dmul(2.0, dadd(dmul(x, y), dmul(w, q)));
+  r[4] = dsub(1.0, dmul(2.0, dadd(dmul(x, x), dmul(q, q))));
+  r[5] = dmul(2.0, dsub(dmul(y, q), dmul(w, x)));
+  r[6] = dmul(2.0, dsub(dmul(x, q), dmul(w, y)));
+  r[7] = dmul(2.0, dadd(dmul(y, q), dmul(w, x)));
+  r[8] = dsub(1.0, dmul(2.0, dadd(dmul(x, x), dmul(y, y))));
+  const double s2[3] = {dmul(g.sx, g.sx), dmul(g.sy, g.sy), dmul(g.sz, g.sz)};
+  for (int i = 0; i < 3; ++i)
+    for (int l = 0; l < 3; ++l)
+      out[9 * k + 3 * i + l] =
+          dadd(dadd(dmul(dmul(r[3 * i + 0], s2[0]), r[3 * l + 0]),
+                    dmul(dmul(r[3 * i + 2], s2[2]), r[3 * l + 2])),
+               dmul(dmul(r[3 * i + 1], s2[1]), r[3 * l + 1]));
+}
+
+__global__ void k_sh_to_colors(int64_t n, const double* sh, int C, const double* dirs, int degree,
+                               double* out) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  double x = dirs[3 * k], y = dirs[3 * k + 1], z = dirs[3 * k + 2];
+  double basis[16];
+  basis[0] = kShC0;
+  if (degree >= 1) { basis[1] = -kShC1 * y; basis[2] = kShC1 * z; basis[3] = -kShC1 * x; }
+  if (degree >= 2) {
+    double xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    basis[4] = kShC2[0] * xy; basis[5] = kShC2[1] * yz;
+    basis[6] = kShC2[2] * (2.0 * zz - xx - yy); basis[7] = kShC2[3] * xz;
+    basis[8] = kShC2[4] * (xx - yy);
+    if (degree >= 3) {
+      basis[9] = kShC3[0] * y * (3.0 * xx - yy);
+      basis[10] = kShC3[1] * xy * z;
+      basis[11] = kShC3[2] * y * (4.0 * zz - xx - yy);
+      basis[12] = kShC3[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+      basis[13] = kShC3[4] * x * (4.0 * zz - xx - yy);
+      basis[14] = kShC3[5] * z * (xx - yy);
+      basis[15] = kShC3[6] * x * (xx - 3.0 * yy);
+    }
+  }
+  const int nb = (degree + 1) * (degree + 1);
+  for (int ch = 0; ch < 3; ++ch) {
+    double acc = 0.0;
+    for (int m = 0; m < nb; ++m) acc += sh[(k * 3 + ch) * C + m] * basis[m];
+    double v = 0.5 + acc;
+    out[3 * k + ch] = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+  }
+}
+
+void launch_build_covariances(int64_t n, const double* scales, const double* quats, double* out,
+                              cudaStream_t s) {
+  if (n <= 0) return;
+  k_build_covariances<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, scales, quats, out);
+}
+void launch_sh_to_colors(int64_t n, const double* sh, int C, const double* dirs, int degree,
+                         double* out, cudaStream_t s) {
+  if (n <= 0) return;
+  k_sh_to_colors<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, sh, C, dirs, degree, out);
+}
+
+}  // namespace cs

@@ -1,0 +1,216 @@
+// cs_sort.cu -- K4/K7: stable LSD radix sort (onesweep-style), device-side count.
+//
+// Used for the global depth order (np.argsort(depths, kind="stable"),
+// render.py:176-177; 64-bit keys = IEEE bits of positive float64 depths) and
+// for the stable tile grouping (np.argsort(tiles, kind="stable"),
+// render.py:245; keys = tile id, only ceil(log2 n_tiles) bits sorted).
+//
+// Per pass one kernel reads keys+values once and writes them once:
+//   * chunks of kTile elements are taken in launch order (ticket counter);
+//   * each warp ranks its keys stably with __match_any_sync and per-warp
+//     digit counters; warps are combined in warp order, so the chunk-local
+//     order equals the input order within every digit (stability);
+//   * per-digit chunk counts are published and a decoupled look-back per
+//     digit gives the chunk's global offset (no separate scan pass);
+//   * keys are first scattered to shared memory in digit order, then written
+//     out so consecutive threads store consecutive addresses of one digit run.
+// A single histogram kernel computes the digit counts of every pass up front.
+// The element count is read from device memory, so the whole frame runs
+// without a host round trip (and is CUDA-graph capturable).
+#include <algorithm>
+
+#include "cs_internal.cuh"
+
+namespace cs {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr uint32_t kStFlagAgg = 1u << 30;
+constexpr uint32_t kStFlagPre = 2u << 30;
+constexpr uint32_t kStMask = (1u << 30) - 1;
+
+template <typename K> struct SortCfg;
+template <> struct SortCfg<uint64_t> { static constexpr int kItems = 8; };
+template <> struct SortCfg<uint32_t> { static constexpr int kItems = 12; };
+
+template <typename K>
+__global__ void __launch_bounds__(kSortThreads)
+k_radix_hist(const K* __restrict__ keys, const int64_t* __restrict__ n_ptr, int begin_bit,
+             int n_passes, uint32_t* __restrict__ hist) {
+  __shared__ uint32_t sh[8 * 256];
+  for (int i = threadIdx.x; i < n_passes * 256; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const int64_t n = *n_ptr;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const K k = keys[i];
+    for (int p = 0; p < n_passes; ++p)
+      atomicAdd(&sh[p * 256 + (uint32_t)((k >> (begin_bit + 8 * p)) & 255)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_passes * 256; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+// exclusive scan of each pass's 256-bin histogram, in place
+__global__ void k_radix_hist_scan(uint32_t* hist, int n_passes) {
+  __shared__ uint32_t scratch[kSortWarps + 1];
+  for (int p = 0; p < n_passes; ++p) {
+    uint32_t v = hist[p * 256 + threadIdx.x];
+    uint32_t total;
+    uint32_t ex = block_excl_scan<uint32_t>(v, scratch, total);
+    hist[p * 256 + threadIdx.x] = ex;
+  }
+}
+
+template <typename K>
+__global__ void __launch_bounds__(kSortThreads)
+k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
+           K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
+           const int64_t* __restrict__ n_ptr, int shift, const uint32_t* __restrict__ digit_base,
+           uint32_t* __restrict__ status, uint32_t* __restrict__ ticket) {
+  constexpr int kItems = SortCfg<K>::kItems;
+  constexpr int kTile = kSortThreads * kItems;
+  __shared__ uint32_t warp_hist[kSortWarps][256];
+  __shared__ uint32_t digit_off[256];
+  __shared__ int64_t gbase[256];
+  __shared__ uint32_t scratch[kSortWarps + 1];
+  __shared__ int64_t s_chunk;
+  __shared__ K keys_s[kTile];
+  __shared__ uint32_t vals_s[kTile];
+
+  const int64_t n = *n_ptr;
+  if (threadIdx.x == 0) s_chunk = atomicAdd(ticket, 1u);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int d = lane; d < 256; d += 32) warp_hist[warp][d] = 0;
+  __syncthreads();
+  const int64_t chunk = s_chunk;
+  const int64_t base = chunk * kTile;
+  if (base >= n) return;
+  const int64_t valid_count = min((int64_t)kTile, n - base);
+
+  K key[kItems];
+  uint32_t val[kItems];
+  uint32_t rank[kItems];
+  const int64_t wbase = base + (int64_t)warp * 32 * kItems;
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    const int64_t idx = wbase + r * 32 + lane;
+    if (idx < n) {
+      key[r] = keys_in[idx];
+      val[r] = vals_in[idx];
+    }
+  }
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    const int64_t idx = wbase + r * 32 + lane;
+    const bool valid = idx < n;
+    const uint32_t d = valid ? (uint32_t)((key[r] >> shift) & 255) : 256u + lane;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t pr = __popc(peers & lt);
+    uint32_t old = 0;
+    if (valid) old = warp_hist[warp][d];
+    __syncwarp();
+    if (valid && pr == 0) warp_hist[warp][d] = old + __popc(peers);
+    __syncwarp();
+    rank[r] = old + pr;
+  }
+  __syncthreads();
+  // combine warps (warp order == input order) -> per-digit chunk counts
+  const int d = threadIdx.x;  // 256 threads == 256 digits
+  uint32_t sum = 0;
+#pragma unroll
+  for (int w = 0; w < kSortWarps; ++w) {
+    const uint32_t c = warp_hist[w][d];
+    warp_hist[w][d] = sum;
+    sum += c;
+  }
+  uint32_t* my_status = status + chunk * 256 + d;
+  if (chunk == 0) {
+    atomicExch(my_status, kStFlagPre | sum);
+  } else {
+    atomicExch(my_status, kStFlagAgg | sum);
+  }
+  uint32_t total;
+  const uint32_t local_start = block_excl_scan<uint32_t>(sum, scratch, total);
+  digit_off[d] = local_start;
+  // decoupled look-back for this digit
+  int64_t excl = 0;
+  if (chunk > 0) {
+    int64_t p = chunk - 1;
+    while (p >= 0) {
+      uint32_t s = ld_volatile_u32(status + p * 256 + d);
+      const uint32_t flag = s >> 30;
+      if (flag == 0) continue;
+      excl += s & kStMask;
+      if (flag == 2) break;
+      --p;
+    }
+    atomicExch(my_status, kStFlagPre | (uint32_t)(excl + sum));
+  }
+  gbase[d] = (int64_t)digit_base[d] + excl - (int64_t)local_start;
+  __syncthreads();
+  // scatter into shared memory in chunk-local sorted order
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    const int64_t idx = wbase + r * 32 + lane;
+    if (idx < n) {
+      const uint32_t dg = (uint32_t)((key[r] >> shift) & 255);
+      const uint32_t pos = digit_off[dg] + warp_hist[warp][dg] + rank[r];
+      keys_s[pos] = key[r];
+      vals_s[pos] = val[r];
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < valid_count; i += kSortThreads) {
+    const K k = keys_s[i];
+    const uint32_t dg = (uint32_t)((k >> shift) & 255);
+    const int64_t o = gbase[dg] + i;
+    keys_out[o] = k;
+    vals_out[o] = vals_s[i];
+  }
+}
+
+// Workspace: hist (8*256 u32), status (chunks*256 u32), tickets (8 u32).
+size_t radix_status_words(int64_t capacity, int key_bytes) {
+  const int items = key_bytes == 8 ? SortCfg<uint64_t>::kItems : SortCfg<uint32_t>::kItems;
+  const int64_t tile = (int64_t)kSortThreads * items;
+  return (size_t)((capacity + tile - 1) / tile) * 256;
+}
+
+// Sorts (keys, vals) of length *n_dev (<= capacity) by bits [begin_bit, end_bit).
+// Ping-pongs between (k0,v0) and (k1,v1); returns 1 when the result is in
+// (k1,v1), 0 when in (k0,v0).
+template <typename K>
+int radix_sort(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_dev, int64_t capacity,
+               int begin_bit, int end_bit, uint32_t* hist, uint32_t* status, uint32_t* tickets,
+               cudaStream_t s) {
+  const int n_passes = (end_bit - begin_bit + 7) / 8;
+  if (n_passes <= 0 || capacity <= 0) return 0;
+  constexpr int kTile = kSortThreads * SortCfg<K>::kItems;
+  const int64_t chunks = (capacity + kTile - 1) / kTile;
+  cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 256 * n_passes, s);
+  cudaMemsetAsync(tickets, 0, sizeof(uint32_t) * n_passes, s);
+  int hist_grid = (int)std::min<int64_t>(148 * 4, (capacity + kSortThreads - 1) / kSortThreads);
+  k_radix_hist<K><<<hist_grid, kSortThreads, 0, s>>>(k0, n_dev, begin_bit, n_passes, hist);
+  k_radix_hist_scan<<<1, 256, 0, s>>>(hist, n_passes);
+  K* kin = k0; K* kout = k1;
+  uint32_t* vin = v0; uint32_t* vout = v1;
+  for (int p = 0; p < n_passes; ++p) {
+    cudaMemsetAsync(status, 0, sizeof(uint32_t) * 256 * chunks, s);
+    k_onesweep<K><<<(unsigned)chunks, kSortThreads, 0, s>>>(kin, vin, kout, vout, n_dev,
+                                                           begin_bit + 8 * p, hist + 256 * p,
+                                                           status, tickets + p);
+    K* tk = kin; kin = kout; kout = tk;
+    uint32_t* tv = vin; vin = vout; vout = tv;
+  }
+  return (n_passes & 1) ? 1 : 0;
+}
+
+template int radix_sort<uint64_t>(uint64_t*, uint32_t*, uint64_t*, uint32_t*, const int64_t*,
+                                  int64_t, int, int, uint32_t*, uint32_t*, uint32_t*, cudaStream_t);
+template int radix_sort<uint32_t>(uint32_t*, uint32_t*, uint32_t*, uint32_t*, const int64_t*,
+                                  int64_t, int, int, uint32_t*, uint32_t*, uint32_t*, cudaStream_t);
+
+}  // namespace cs

@@ -1,0 +1,146 @@
+"""Block fusion (partition.fuse, partition.py:570-587) on the device.
+
+``fuse_device`` keeps, from each fine-tuned block cloud j, the rows whose
+contracted position still bins into block j (K12 cs_fuse_filter: the
+normalize -> contract -> bin chain in float64 numpy order, stable
+compaction), and concatenates the kept rows in ascending block order -- the
+same bytes as the CPU ``fuse``.
+
+``fuse_all_gather`` is the multi-GPU form used after block-parallel training
+(SURVEY.md section 8e): every rank filters the blocks it owns on its own GPU,
+the per-block kept counts are summed with one all-reduce, and the kept rows are
+exchanged with one broadcast per block in ascending block order (an
+all-gather-v), so every rank ends with the byte-identical fused cloud.
+"""
+
+from __future__ import annotations
+
+from typing import Dict, List, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import _lib, device
+from ._lib import check
+from .core import pad_sh
+
+
+def _dims3(dims):
+    dims = tuple(int(d) for d in dims)
+    return dims + (1,) if len(dims) == 2 else dims
+
+
+def fuse_filter(positions: torch.Tensor, p_min, p_max, dims, block: int) -> torch.Tensor:
+    """Ascending row indices (device int64) of `positions` that bin into `block`."""
+    nx, ny, nz = _dims3(dims)
+    pos = positions.contiguous()
+    f32 = 1 if pos.dtype == torch.float32 else 0
+    if not f32:
+        pos = pos.double().contiguous()
+    n = pos.shape[0]
+    kept = torch.empty(max(n, 1), dtype=torch.int64, device=pos.device)
+    cnt = torch.zeros(1, dtype=torch.int64, device=pos.device)
+    pmin = np.ascontiguousarray(p_min, dtype=np.float64)
+    pmax = np.ascontiguousarray(p_max, dtype=np.float64)
+    check(_lib.load().cs_fuse_filter(device.context(pos.device.index), n, pos.data_ptr(), f32,
+                                     pmin.ctypes.data, pmax.ctypes.data, nx, ny, nz, int(block),
+                                     kept.data_ptr(), cnt.data_ptr(),
+                                     device.stream_handle(pos.device)), "fuse_filter")
+    return kept[: int(cnt.item())]
+
+
+class FusedArrays:
+    def __init__(self, positions, opacities, scales, rotations, sh):
+        self.positions, self.opacities, self.scales = positions, opacities, scales
+        self.rotations, self.sh = rotations, sh
+
+    @property
+    def count(self) -> int:
+        return int(self.positions.shape[0])
+
+
+def fuse_device(block_clouds: Sequence, p_min, p_max, dims) -> FusedArrays:
+    """partition.fuse with the membership test on the GPU; host arrays out."""
+    n_blocks = int(np.prod(_dims3(dims)))
+    pieces = []
+    dev = torch.device("cuda", device._device_index())
+    for cloud, j in sorted(block_clouds, key=lambda item: item[1]):
+        if not 0 <= j < n_blocks:
+            raise ValueError(f"block index {j} outside the grid")
+        pos = np.asarray(cloud.positions, dtype=np.float64)
+        if pos.shape[0] == 0:
+            continue
+        idx = fuse_filter(torch.from_numpy(np.ascontiguousarray(pos)).to(dev), p_min, p_max, dims, j)
+        if idx.numel():
+            rows = idx.cpu().numpy()
+            pieces.append([np.asarray(getattr(cloud, f))[rows]
+                           for f in ("positions", "opacities", "scales", "rotations", "sh")])
+    if not pieces:
+        return FusedArrays(np.zeros((0, 3)), np.zeros(0), np.zeros((0, 3)), np.zeros((0, 4)),
+                           np.zeros((0, 3, 16)))
+    width = max(p[4].shape[2] for p in pieces)
+    return FusedArrays(*(np.concatenate([p[i] for p in pieces]) for i in range(4)),
+                       np.concatenate([pad_sh(p[4], width) for p in pieces]))
+
+
+# ---------------------------------------------------------------------------
+# multi-GPU fusion: all-gather-v in block order
+
+PARAM_WIDTH_NOSH = 3 + 1 + 3 + 4  # positions, opacity, scales, rotations
+
+
+def pack_rows(positions, opacities, scales, rotations, sh) -> torch.Tensor:
+    """Rows as one contiguous float tensor [n, 11 + 3C] for a single collective."""
+    n = positions.shape[0]
+    return torch.cat([positions.reshape(n, 3), opacities.reshape(n, 1), scales.reshape(n, 3),
+                      rotations.reshape(n, 4), sh.reshape(n, -1)], dim=1).contiguous()
+
+
+def unpack_rows(rows: torch.Tensor, sh_coeffs: int):
+    n = rows.shape[0]
+    return (rows[:, 0:3], rows[:, 3], rows[:, 4:7], rows[:, 7:11],
+            rows[:, 11:11 + 3 * sh_coeffs].reshape(n, 3, sh_coeffs))
+
+
+def fuse_all_gather(local_blocks: Dict[int, Tuple[torch.Tensor, ...]], n_blocks: int, owner: List[int],
+                    p_min, p_max, dims, sh_coeffs: int, group=None, filter_fn=None) -> torch.Tensor:
+    """Fuse block clouds trained on different ranks.
+
+    local_blocks: {block j: (positions, opacities, scales, rotations, sh)} for the
+    blocks this rank owns (owner[j] == rank).  Returns the fused rows
+    [N, 11 + 3C] on every rank, blocks in ascending order, rows within a block
+    in ascending index order (partition.py:578-587).  ``filter_fn`` defaults to
+    the CUDA membership filter; tests on CPU ranks pass the oracle's.
+    """
+    import torch.distributed as dist
+    filter_fn = filter_fn or (lambda pos, j: fuse_filter(pos, p_min, p_max, dims, j))
+    rank = dist.get_rank(group)
+    some = next(iter(local_blocks.values()))[0] if local_blocks else None
+    dev = some.device if some is not None else (
+        torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu"))
+    dtype = some.dtype if some is not None else torch.float32
+    kept_rows = {}
+    counts = torch.zeros(n_blocks, dtype=torch.int64, device=dev)
+    for j, params in local_blocks.items():
+        if owner[j] != rank:
+            raise ValueError(f"rank {rank} does not own block {j}")
+        idx = filter_fn(params[0], j)
+        rows = pack_rows(*(p[idx] for p in params))
+        kept_rows[j] = rows
+        counts[j] = rows.shape[0]
+    dist.all_reduce(counts, group=group)             # owners fill their slots
+    width = PARAM_WIDTH_NOSH + 3 * sh_coeffs
+    offsets = torch.cumsum(counts, 0) - counts
+    total = int(counts.sum().item())
+    fused = torch.empty((total, width), dtype=dtype, device=dev)
+    counts_h = counts.cpu().tolist()
+    offs_h = offsets.cpu().tolist()
+    for j in range(n_blocks):                        # all-gather-v in ascending block order
+        n = counts_h[j]
+        if n == 0:
+            continue
+        view = fused[offs_h[j]: offs_h[j] + n]
+        if owner[j] == rank:
+            view.copy_(kept_rows[j])
+        dist.broadcast(view, src=owner[j], group=group)
+    return fused

@@ -1,0 +1,281 @@
+"""Drop-in for the selection/aggregation half of citysplat.lod (lod.py:150-401).
+
+* ``LodScene``             (lod.py:150-208) -- same fields/validation; uploaded
+                           once to HBM (device.DeviceLodScene) on first use.
+* ``VisibilityDecision``   (lod.py:255-264)
+* ``AssembledSet``         (lod.py:351-357)
+* ``block_visible``        (lod.py:267-295)  -> device kernel
+* ``select_level``         (lod.py:311-321)  -> device kernel
+* ``decide_visibility``    (lod.py:330-348)  -> device kernel (K1)
+* ``assemble_render_set``  (lod.py:360-401)  -> segment table on device (K2),
+  no concatenation copy.  ``AssembledSet.cloud`` is an ``AssembledCloud``: a
+  lazy, device-backed view that duck-types GaussianCloud (``count`` and the
+  column arrays, materialised on access) and that ``rasterize_stats``
+  recognises and renders straight from the scene in HBM.
+
+Accepts the reference's own LodScene objects as well (duck-typed fields).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+from dataclasses import dataclass
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import _lib, device
+from ._lib import CsDecision, CsFrameStats, check
+from .core import GaussianCloud, pad_sh
+
+__all__ = ["LodScene", "VisibilityDecision", "AssembledSet", "AssembledCloud", "block_visible",
+           "select_level", "decide_visibility", "assemble_render_set"]
+
+
+@dataclass(frozen=True)
+class LodScene:
+    """levels[L][j]: block j at level L (0 = coarsest); intervals nearest-first."""
+
+    levels: tuple
+    bounds_min: np.ndarray
+    bounds_max: np.ndarray
+    distance_intervals: tuple
+    sh_degrees: tuple
+    n_mad: float
+    full: object
+
+    def __post_init__(self):
+        levels = tuple(tuple(level) for level in self.levels)
+        object.__setattr__(self, "levels", levels)
+        object.__setattr__(self, "distance_intervals",
+                           tuple((float(a), float(b)) for a, b in self.distance_intervals))
+        object.__setattr__(self, "sh_degrees", tuple(int(d) for d in self.sh_degrees))
+        if not levels:
+            raise ValueError("at least one level required")
+        n_blocks = len(levels[0])
+        if any(len(level) != n_blocks for level in levels):
+            raise ValueError("every level must carry the same block set")
+        if len(self.distance_intervals) != len(levels):
+            raise ValueError("one distance interval per level required")
+        if len(self.sh_degrees) != len(levels):
+            raise ValueError("one sh_degree per level required")
+        bmin = np.asarray(self.bounds_min, dtype=np.float64).reshape(n_blocks, 3)
+        bmax = np.asarray(self.bounds_max, dtype=np.float64).reshape(n_blocks, 3)
+        if not (np.isfinite(bmin).all() and np.isfinite(bmax).all()):
+            raise ValueError("block bounds must be finite")
+        object.__setattr__(self, "bounds_min", bmin)
+        object.__setattr__(self, "bounds_max", bmax)
+
+    @property
+    def n_levels(self) -> int:
+        return len(self.levels)
+
+    @property
+    def n_blocks(self) -> int:
+        return len(self.levels[0])
+
+    @property
+    def finest(self) -> int:
+        return self.n_levels - 1
+
+    def level_size(self, level: int) -> int:
+        return sum(_count(c) for c in self.levels[level])
+
+    def occupied(self, j: int) -> bool:
+        return _count(self.levels[self.finest][j]) > 0
+
+
+def _count(c) -> int:
+    return int(c.count) if hasattr(c, "count") else int(np.asarray(c.positions).shape[0])
+
+
+@dataclass(frozen=True)
+class VisibilityDecision:
+    block: int
+    visible: bool
+    level: Optional[int]
+    distance: float
+    screen_box: Optional[tuple]
+
+
+@dataclass(frozen=True)
+class AssembledSet:
+    cloud: object
+    decisions: tuple
+    selection_ms: float
+
+
+class AssembledCloud:
+    """The concatenated render set of one frame, kept on the device.
+
+    Holds the scene handle plus the selection parameters; rendering it runs
+    the selection kernel again inside the frame (it is deterministic, so the
+    set is identical).  Column arrays are gathered to the host only when read.
+    """
+
+    def __init__(self, scene: device.DeviceLodScene, cam, mode: str, force_level, count: int,
+                 pieces):
+        self.scene = scene
+        self.cam = cam
+        self.mode = mode
+        self.force_level = force_level
+        self._count = int(count)
+        self._pieces = pieces  # [(level, block)] in assembled order (block mode)
+        self._host = None
+        self.source_kind = _lib.CS_SRC_LOD_BLOCK if mode == "block" else _lib.CS_SRC_LOD_POINT
+
+    @property
+    def count(self) -> int:
+        return self._count
+
+    def __len__(self) -> int:
+        return self._count
+
+    def _materialise(self):
+        if self._host is None:
+            if self.mode == "block":
+                parts = [self.scene.block_cloud_host(L, j) for L, j in self._pieces]
+            else:
+                parts = _pointwise_host(self.scene, self.cam, self.force_level)
+            if not parts:
+                self._host = GaussianCloud.empty()
+            else:
+                width = max(p["sh"].shape[2] for p in parts)
+                self._host = GaussianCloud(
+                    np.concatenate([p["positions"] for p in parts]),
+                    np.concatenate([p["opacities"] for p in parts]),
+                    np.concatenate([p["scales"] for p in parts]),
+                    np.concatenate([p["rotations"] for p in parts]),
+                    np.concatenate([pad_sh(p["sh"], width) for p in parts]))
+        return self._host
+
+    positions = property(lambda self: self._materialise().positions)
+    opacities = property(lambda self: self._materialise().opacities)
+    scales = property(lambda self: self._materialise().scales)
+    rotations = property(lambda self: self._materialise().rotations)
+    sh = property(lambda self: self._materialise().sh)
+
+    def to_cloud(self) -> GaussianCloud:
+        return self._materialise()
+
+
+def _pointwise_host(scene, cam, force_level):
+    """Host copy of a pointwise render set: the device selection's packed
+    (cloud << 40 | row) list, gathered from the level buffers."""
+    n = _pointwise_count(scene, cam, force_level)
+    packed = np.zeros(max(n, 1), dtype=np.uint64)
+    got = ctypes.c_int64(0)
+    check(_lib.load().cs_dump_assembled_list(device.context(scene.device_index), packed.ctypes.data,
+                                             n, ctypes.byref(got), device.stream_handle()))
+    packed = packed[:got.value]
+    if packed.size == 0:
+        return []
+    cloud = (packed >> np.uint64(40)).astype(np.int64)
+    row = (packed & np.uint64((1 << 40) - 1)).astype(np.int64)
+    J = scene.n_blocks
+    parts = []
+    # runs of equal cloud index are contiguous (level-major, block order)
+    cuts = np.flatnonzero(np.diff(cloud)) + 1
+    for seg in np.split(np.arange(packed.size), cuts):
+        ci = int(cloud[seg[0]])
+        L, j = divmod(ci, J)
+        host = scene.block_cloud_host(L, j)
+        rows = row[seg]
+        parts.append({k: v[rows] for k, v in host.items()})
+    return parts
+
+
+def block_visible(bounds, cam) -> Tuple[bool, float]:
+    """lod.block_visible (lod.py:267-295) on the device."""
+    lo = np.ascontiguousarray(np.asarray(bounds[0], dtype=np.float64).reshape(1, 3))
+    hi = np.ascontiguousarray(np.asarray(bounds[1], dtype=np.float64).reshape(1, 3))
+    vis = np.zeros(1, dtype=np.uint8)
+    dist = np.zeros(1)
+    c = device.camera_struct(cam)
+    check(_lib.load().cs_block_visible(device.context(), 1, lo.ctypes.data, hi.ctypes.data,
+                                       ctypes.byref(c), vis.ctypes.data, dist.ctypes.data,
+                                       device.stream_handle()), "block_visible")
+    return bool(vis[0]), float(dist[0])
+
+
+def select_level(distance: float, intervals: Sequence) -> int:
+    """lod.select_level (lod.py:311-321) on the device."""
+    d = np.array([float(distance)])
+    iv = np.ascontiguousarray(np.array([(float(a), float(b)) for a, b in intervals]).reshape(-1, 2))
+    out = np.zeros(1, dtype=np.int32)
+    rc = _lib.load().cs_select_level(device.context(), 1, d.ctypes.data, iv.shape[0],
+                                     iv.ctypes.data, out.ctypes.data, device.stream_handle())
+    if rc == _lib.CS_EINVAL:
+        raise ValueError("distance must be nonnegative")
+    if rc == _lib.CS_ERANGE:
+        raise ValueError(f"no interval covers distance {float(distance)}")
+    check(rc, "select_level")
+    return int(out[0])
+
+
+def _decisions(dscene: device.DeviceLodScene, cam, force_level) -> tuple:
+    J = dscene.n_blocks
+    arr = (CsDecision * J)()
+    c = device.camera_struct(cam)
+    rc = _lib.load().cs_decide_visibility(device.context(dscene.device_index), dscene.handle,
+                                          ctypes.byref(c), -1 if force_level is None else int(force_level),
+                                          arr, device.stream_handle())
+    if rc == _lib.CS_ERANGE:
+        raise ValueError("no interval covers a block distance")
+    check(rc, "decide_visibility")
+    out = []
+    for j in range(J):
+        d = arr[j]
+        vis = bool(d.visible)
+        out.append(VisibilityDecision(
+            block=j, visible=vis, level=int(d.level) if vis else None,
+            distance=float(d.distance),
+            screen_box=tuple(float(v) for v in d.box) if d.has_box else None))
+    return tuple(out)
+
+
+def decide_visibility(scene, cam, force_level: Optional[int] = None) -> tuple:
+    """lod.decide_visibility (lod.py:330-348) -> tuple of VisibilityDecision."""
+    return _decisions(device.device_lod_scene(scene), cam, force_level)
+
+
+def assemble_render_set(scene, cam, *, mode: str = "block",
+                        force_level: Optional[int] = None) -> AssembledSet:
+    """lod.assemble_render_set (lod.py:360-401) without the concatenation copy."""
+    dscene = device.device_lod_scene(scene)
+    start = time.perf_counter()
+    if mode == "block":
+        decisions = _decisions(dscene, cam, force_level)
+        pieces = [(d.level, d.block) for d in decisions
+                  if d.visible and 0 <= d.level < dscene.n_levels and dscene.counts[d.level, d.block] > 0]
+        count = int(sum(dscene.counts[L, j] for L, j in pieces))
+    elif mode == "pointwise":
+        decisions = ()
+        pieces = None
+        count = _pointwise_count(dscene, cam, force_level)
+    else:
+        raise ValueError(f"unknown selection mode: {mode}")
+    selection_ms = (time.perf_counter() - start) * 1000.0
+    return AssembledSet(cloud=AssembledCloud(dscene, cam, mode, force_level, count, pieces),
+                        decisions=decisions, selection_ms=selection_ms)
+
+
+def _pointwise_count(dscene, cam, force_level) -> int:
+    from ._lib import CsSource
+    from .render import RenderSettings
+    src = CsSource()
+    src.kind = _lib.CS_SRC_LOD_POINT
+    src.force_level = -1 if force_level is None else int(force_level)
+    src.lod = dscene.handle
+    out = torch.empty((1, 1, 3), dtype=torch.float32, device=torch.device("cuda", dscene.device_index))
+    stats = CsFrameStats()
+    c = device.camera_struct(cam)
+    s = device.settings_struct(RenderSettings())
+    check(_lib.load().cs_render(device.context(dscene.device_index), ctypes.byref(src), ctypes.byref(c),
+                                ctypes.byref(s), out.data_ptr(),
+                                _lib.CS_RENDER_SYNC | _lib.CS_RENDER_PROJECT_ONLY,
+                                ctypes.byref(stats), device.stream_handle()), "pointwise")
+    return int(stats.assembled)

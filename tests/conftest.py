@@ -1,0 +1,99 @@
+"""Shared fixtures: golden-vector loading and the gpu marker.
+
+Tests marked ``gpu`` need a B200 (run with ``-m gpu``); everything else runs
+on CPU.  The oracle (oracle/) is the parity checker only.
+"""
+
+import os
+import sys
+from pathlib import Path
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+GOLDEN = ROOT / "tests" / "golden"
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA (sm_100a) device")
+
+
+def gpu_available() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def pytest_collection_modifyitems(config, items):
+    if gpu_available():
+        return
+    skip = pytest.mark.skip(reason="no CUDA device")
+    for item in items:
+        if "gpu" in item.keywords:
+            item.add_marker(skip)
+
+
+class Golden:
+    """Lazy view of one golden .npz with '/'-separated keys."""
+
+    def __init__(self, name):
+        self.z = np.load(GOLDEN / name, allow_pickle=False)
+
+    def __getitem__(self, k):
+        return self.z[k]
+
+    def has(self, k):
+        return k in self.z.files
+
+    def cases(self):
+        return [str(c) for c in self.z["cases"]]
+
+    def cloud(self, prefix):
+        g = lambda k: self.z[f"{prefix}/{k}"]
+        return SimpleNamespace(positions=g("positions"), opacities=g("opacities"),
+                               scales=g("scales"), rotations=g("rotations"), sh=g("sh"),
+                               count=int(g("positions").shape[0]))
+
+    def camera(self, prefix):
+        g = lambda k: self.z[f"{prefix}/{k}"]
+        fx, fy, cx, cy = (float(v) for v in g("intr"))
+        w, h = (int(v) for v in g("size"))
+        return SimpleNamespace(rotation_w2c=g("R"), translation_w2c=g("t"), camera_center=g("center"),
+                               fx=fx, fy=fy, cx=cx, cy=cy, width=w, height=h)
+
+    def settings(self, prefix):
+        g = lambda k: self.z[f"{prefix}/{k}"]
+        return SimpleNamespace(background=tuple(float(v) for v in g("bg")),
+                               sh_degree=int(g("sh_degree")), tile_size=int(g("tile_size")),
+                               alpha_floor=float(g("alpha_floor")),
+                               transmittance_floor=float(g("t_floor")), near_plane=float(g("near")))
+
+    def lod(self):
+        L, J = int(self.z["n_levels"]), int(self.z["n_blocks"])
+        levels = tuple(tuple(self.cloud(f"level{l}/block{j}") for j in range(J)) for l in range(L))
+        return SimpleNamespace(levels=levels, bounds_min=self.z["bounds_min"],
+                               bounds_max=self.z["bounds_max"],
+                               distance_intervals=tuple(map(tuple, self.z["intervals"])),
+                               sh_degrees=tuple(int(d) for d in self.z["sh_degrees"]),
+                               n_levels=L, n_blocks=J)
+
+
+@pytest.fixture(scope="session")
+def golden_render():
+    return Golden("render.npz")
+
+
+@pytest.fixture(scope="session")
+def golden_city():
+    return Golden("city.npz")
+
+
+@pytest.fixture(scope="session")
+def golden_fuse():
+    return Golden("fuse.npz")

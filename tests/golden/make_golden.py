@@ -1,0 +1,231 @@
+"""Generate the golden vectors in tests/golden/ by running the REFERENCE itself.
+
+    OPENBLAS_CORETYPE=Sandybridge python tests/golden/make_golden.py
+
+Imports citysplat from /root/reference/pkg/src (read-only; only present in
+the build container, never on the GPU box) and records, for seeded inputs,
+the reference's own outputs of the hot-path functions:
+
+  render.npz   _project_cloud (render.py:111-188), _bin_tiles (render.py:217-249),
+               rasterize_stats (render.py:252-280) on the closed-form cases of
+               tests/test_render.py and on random cloud_in_view scenes
+               (tests/conftest.py:37-54), tile sizes 8/16/32
+  city.npz     a synthetic city (synthetic.py:96-203) cut into a 2x2 / 3-level
+               LodScene (build_lod, lod.py:211-248): decide_visibility,
+               assemble_render_set (block, forced, pointwise) and the render of
+               the assembled cloud, for several cameras
+  fuse.npz     partition.fuse (partition.py:570-587) of perturbed block clouds
+
+OPENBLAS_CORETYPE=Sandybridge pins numpy's dgemm to the no-FMA kernel
+(SURVEY.md Appendix B.1); the script refuses to run without it.
+"""
+
+import os
+import sys
+
+if os.environ.get("OPENBLAS_CORETYPE") != "Sandybridge":
+    os.environ["OPENBLAS_CORETYPE"] = "Sandybridge"
+    os.execv(sys.executable, [sys.executable] + sys.argv)
+
+import math  # noqa: E402
+from pathlib import Path  # noqa: E402
+
+import numpy as np  # noqa: E402
+
+REF = Path("/root/reference/pkg")
+sys.path.insert(0, str(REF / "src"))
+sys.path.insert(0, str(REF / "tests"))
+
+from citysplat.config import RunConfig  # noqa: E402
+from citysplat.core import CameraView, Gaussian, GaussianCloud, SH_C0  # noqa: E402
+from citysplat.lod import assemble_render_set, build_lod, decide_visibility  # noqa: E402
+from citysplat.partition import ContractionMap, fuse, grid_partition  # noqa: E402
+from citysplat.render import RenderSettings, _bin_tiles, _project_cloud, rasterize_stats  # noqa: E402
+from citysplat.synthetic import generate_synthetic_city, look_at  # noqa: E402
+from conftest import cloud_in_view, identity_camera, random_camera  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+
+
+def q32(a):
+    """Round to float32-representable float64."""
+    return np.asarray(a, dtype=np.float32).astype(np.float64)
+
+
+def quantize(cloud: GaussianCloud) -> GaussianCloud:
+    rot = q32(cloud.rotations)
+    return GaussianCloud(positions=q32(cloud.positions), opacities=q32(cloud.opacities),
+                         scales=q32(cloud.scales), rotations=rot, sh=q32(cloud.sh))
+
+
+def cam_dict(cam):
+    return dict(R=np.asarray(cam.rotation_w2c), t=np.asarray(cam.translation_w2c),
+                center=np.asarray(cam.camera_center),
+                intr=np.array([cam.fx, cam.fy, cam.cx, cam.cy]),
+                size=np.array([cam.width, cam.height], dtype=np.int64))
+
+
+def settings_dict(s):
+    return dict(bg=np.array(s.background), sh_degree=np.int64(s.sh_degree),
+                tile_size=np.int64(s.tile_size), alpha_floor=np.float64(s.alpha_floor),
+                t_floor=np.float64(s.transmittance_floor), near=np.float64(s.near_plane))
+
+
+def cloud_dict(c):
+    return dict(positions=c.positions, opacities=c.opacities, scales=c.scales,
+                rotations=c.rotations, sh=c.sh)
+
+
+def render_record(cloud, cam, settings):
+    p = _project_cloud(cloud, cam, settings)
+    tid, off, _, _ = _bin_tiles(p, cam, settings.tile_size)
+    img, st = rasterize_stats(cloud, cam, settings)
+    rec = dict(
+        p_means=p.means, p_conics=p.conics, p_covs=p.covs, p_depths=p.depths,
+        p_colors=p.colors, p_opacities=p.opacities, p_radii=p.radii, p_source=p.source,
+        p_skipped=np.int64(p.skipped_singular), tile_ids=tid, offsets=off,
+        image=img.pixels, visible=np.int64(st.visible_splats),
+        fragments=np.int64(st.blended_fragments), skipped=np.int64(st.skipped_singular))
+    return rec
+
+
+def put(store, prefix, d):
+    for k, v in d.items():
+        store[f"{prefix}/{k}"] = np.asarray(v)
+
+
+def on_axis(z, opacity=1.0, scale=0.3, color=None):
+    sh = np.zeros((3, 16))
+    if color is not None:
+        sh[:, 0] = (np.asarray(color) - 0.5) / SH_C0
+    return Gaussian(position=np.array([0.0, 0.0, z]), opacity=opacity, scale=np.full(3, scale),
+                    rotation=np.array([1.0, 0.0, 0.0, 0.0]), sh=sh)
+
+
+def make_render():
+    store = {}
+    cases = []
+    # closed-form cases (tests/test_render.py:145-200)
+    cases.append(("empty", GaussianCloud.empty(), identity_camera(40, 30),
+                  RenderSettings(background=(0.1, 0.5, 0.9))))
+    cases.append(("opaque_center", GaussianCloud.from_gaussians([on_axis(5.0, 1.0, color=(1.0, 0.5, 0.0))]),
+                  identity_camera(65, 49, 60.0), RenderSettings(background=(0.2, 0.2, 0.2))))
+    cases.append(("two_coincident", GaussianCloud.from_gaussians([
+        on_axis(8.0, 0.5, color=(0.0, 1.0, 0.0)), on_axis(5.0, 0.5, color=(1.0, 0.0, 0.0))]),
+        identity_camera(65, 49, 60.0), RenderSettings(background=(0.0, 0.0, 1.0))))
+    cases.append(("t_floor_drop", GaussianCloud.from_gaussians([
+        on_axis(float(z), 1.0, color=c) for z, c in
+        ((1, (1.0, 0.0, 0.0)), (2, (0.0, 1.0, 0.0)), (3, (0.0, 0.0, 1.0)))]),
+        identity_camera(1, 1, 10.0), RenderSettings()))
+    cases.append(("faint_skip", GaussianCloud.from_gaussians([on_axis(5.0, 1.0 / 300.0, color=(1, 1, 1))]),
+                  identity_camera(65, 49, 60.0), RenderSettings()))
+    cases.append(("near_cull", GaussianCloud.from_gaussians([on_axis(-5.0), on_axis(0.1), on_axis(0.25)]),
+                  identity_camera(), RenderSettings()))
+    cases.append(("occluder", GaussianCloud.from_gaussians([
+        on_axis(4.0, 1.0, 30.0, (0.1, 0.1, 0.1)), on_axis(8.0, 1.0, 30.0, (1.0, 1.0, 1.0))]),
+        identity_camera(33, 25, 30.0), RenderSettings()))
+    # random scenes like tests/test_render.py:207-221 (tile sizes 8/16/32)
+    rng = np.random.default_rng(20260814)
+    for i in range(24):
+        cam = random_camera(rng)
+        cloud = cloud_in_view(rng, cam, int(rng.integers(0, 41)))
+        settings = RenderSettings(background=tuple(rng.uniform(0.0, 1.0, 3)),
+                                  tile_size=int(rng.choice([8, 16, 32])),
+                                  transmittance_floor=float(rng.choice([1e-4, 1e-12])),
+                                  sh_degree=int(rng.integers(0, 4)))
+        cases.append((f"random{i:02d}", cloud, cam, settings))
+    # a denser scene with many tile pairs
+    cam = identity_camera(width=96, height=72, f=70.0)
+    cases.append(("dense", cloud_in_view(np.random.default_rng(99), cam, 300), cam, RenderSettings()))
+    names = []
+    for name, cloud, cam, settings in cases:
+        put(store, name, cloud_dict(cloud))
+        put(store, name, cam_dict(cam))
+        put(store, name, settings_dict(settings))
+        put(store, name, render_record(cloud, cam, settings))
+        names.append(name)
+    store["cases"] = np.array(names)
+    np.savez_compressed(OUT / "render.npz", **store)
+    print("render.npz", len(names), "cases")
+
+
+def make_city():
+    bundle = generate_synthetic_city(seed=7, extent=60.0, n_buildings=8, n_cameras=16,
+                                     target_gaussians=4000, image_size=(64, 48))
+    cloud = quantize(bundle.cloud)
+    cmap = ContractionMap.central_third(cloud)
+    grid = grid_partition(cloud, cmap, (2, 2))
+    config = RunConfig(block_dims=(2, 2), distance_intervals=((0.0, 20.0), (20.0, 45.0), (45.0, math.inf)))
+    cams = [r.view for r in bundle.train_cameras()]
+    lod = build_lod(cloud, grid, cams, config)
+    store = {}
+    L, J = lod.n_levels, lod.n_blocks
+    store["n_levels"] = np.int64(L)
+    store["n_blocks"] = np.int64(J)
+    store["bounds_min"] = lod.bounds_min
+    store["bounds_max"] = lod.bounds_max
+    store["intervals"] = np.array(lod.distance_intervals)
+    store["sh_degrees"] = np.array(lod.sh_degrees)
+    for l in range(L):
+        for j in range(J):
+            put(store, f"level{l}/block{j}", cloud_dict(lod.levels[l][j]))
+    views = [r.view for r in bundle.cameras]
+    center = cloud.positions.mean(axis=0)
+    views.append(look_at(center + np.array([0.0, 0.0, 2000.0]), center, 64, 48, 54.0))  # far: coarse
+    bc = 0.5 * (lod.bounds_min[0] + lod.bounds_max[0])
+    views.append(CameraView(64, 48, 50.0, 50.0, 32.0, 24.0, np.eye(3), -bc))  # inside block 0
+    names = []
+    for i, cam in enumerate(views):
+        name = f"cam{i:02d}"
+        put(store, name, cam_dict(cam))
+        dec = decide_visibility(lod, cam)
+        store[f"{name}/dec_visible"] = np.array([d.visible for d in dec])
+        store[f"{name}/dec_level"] = np.array([-1 if d.level is None else d.level for d in dec])
+        store[f"{name}/dec_distance"] = np.array([d.distance for d in dec])
+        store[f"{name}/dec_box"] = np.array([d.screen_box if d.screen_box else (np.nan,) * 4 for d in dec])
+        for tag, kw in (("block", dict()), ("forced", dict(force_level=lod.finest)),
+                        ("point", dict(mode="pointwise"))):
+            a = assemble_render_set(lod, cam, **kw)
+            store[f"{name}/{tag}_count"] = np.int64(a.cloud.count)
+            if i % 4 == 0:
+                store[f"{name}/{tag}_positions"] = a.cloud.positions.astype(np.float32)
+            if tag == "block" or i % 4 == 0:
+                put(store, f"{name}/{tag}", render_record(a.cloud, cam, RenderSettings()))
+        names.append(name)
+    store["cases"] = np.array(names)
+    np.savez_compressed(OUT / "city.npz", **store)
+    print("city.npz", len(names), "cameras")
+
+
+def make_fuse():
+    bundle = generate_synthetic_city(seed=3, extent=80.0, n_buildings=10, n_cameras=8,
+                                     target_gaussians=3000, image_size=(32, 24))
+    cloud = bundle.cloud
+    cmap = ContractionMap.central_third(cloud)
+    grid = grid_partition(cloud, cmap, (3, 3))
+    rng = np.random.default_rng(5)
+    blocks = []
+    store = {"p_min": cmap.p_min, "p_max": cmap.p_max, "dims": np.array([3, 3])}
+    for j in range(grid.n_blocks):
+        m = grid.members(j)
+        if j == 4:
+            continue  # a missing block
+        sub = cloud.take(m)
+        moved = GaussianCloud(positions=sub.positions + rng.normal(0, 1.5, sub.positions.shape),
+                              opacities=sub.opacities, scales=sub.scales,
+                              rotations=sub.rotations, sh=sub.sh)
+        blocks.append((moved, j))
+        put(store, f"block{j}", cloud_dict(moved))
+    fused = fuse(list(reversed(blocks)), grid)
+    put(store, "fused", cloud_dict(fused))
+    store["block_ids"] = np.array([j for _, j in blocks])
+    np.savez_compressed(OUT / "fuse.npz", **store)
+    print("fuse.npz", fused.count, "fused of", sum(b.count for b, _ in blocks))
+
+
+if __name__ == "__main__":
+    make_render()
+    make_city()
+    make_fuse()
+    for f in sorted(OUT.glob("*.npz")):
+        print(f.name, f.stat().st_size // 1024, "KiB")
