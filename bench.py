@@ -1,0 +1,427 @@
+"""Benchmark: 1080p FPS on the 23M-Gaussian LoD city (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (N > 1, one rank per GPU)
+
+Workload (BASELINE.json configs[2]): synthetic 23M-Gaussian MatrixCity-scale
+city (extent 1600 m, 3000 buildings), 6x6 blocks, 3 LoD levels built from the
+training views (rates 0.5/0.34/0.25, SH 3/2/1, intervals 0/200/400 m), 1080p
+flythrough over camera heights {150, 300, 500} m (cmd_bench's orbit sweep,
+cli.py:203-218).  One step = one frame: LoD selection + assembly + projection +
+depth sort + binning + blend (rasterize_stats after assemble_render_set).
+N > 1: the flythrough is view-split across ranks (BASELINE configs[4]), each
+rank renders K frames of its own share (weak scaling), no collective on the
+data path.  Scene inputs (>= 600 MB per frame) exceed the 126 MB L2, so no
+flush is needed between frames.
+
+Keys beyond the base contract: roofline (dominant kernel, live CUDA-event
+stage times), cpu_baseline (the C oracle port, all host cores, bounded
+sample), e2e (through the C ABI with the image read back to pinned host
+memory every frame), stages_ms, clocks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+STAGES = ("select", "project", "depth_sort", "gather_scan", "duplicate", "tile_sort", "ranges", "blend")
+SCENES = {
+    # name: (gaussians, extent, buildings, blocks, intervals, altitudes, W, H)
+    "c3": (23_000_000, 1600.0, 3000, (6, 6), ((0.0, 200.0), (200.0, 400.0), (400.0, math.inf)),
+           (150.0, 300.0, 500.0), 1920, 1080),
+    "c3-small": (2_000_000, 1600.0, 3000, (6, 6), ((0.0, 200.0), (200.0, 400.0), (400.0, math.inf)),
+                 (150.0, 300.0, 500.0), 1920, 1080),
+    "tiny": (200_000, 200.0, 100, (2, 2), ((0.0, 40.0), (40.0, 80.0), (80.0, math.inf)),
+             (20.0, 40.0, 80.0), 640, 360),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--scene", choices=tuple(SCENES), default="c3")
+    ap.add_argument("--frames-per-altitude", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--seed", type=int, default=0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# scene
+
+
+def build_scene(name: str, seed: int, dev):
+    import torch
+    from paper_2404_01133_b200 import lodgen
+    from paper_2404_01133_b200.synth import city_cameras, generate_city_torch, orbit_cameras
+    n, extent, nb, dims, ints, alts, W, H = SCENES[name]
+    t0 = time.perf_counter()
+    pos, op, sc, q, sh = generate_city_torch(seed, extent, nb, n, device=dev)
+    pmin, pmax = lodgen.central_third(pos)
+    mem = lodgen.block_membership(pos, pmin, pmax, dims)
+    cams = city_cameras(64, extent, W, H, seed=seed)
+    train = [c for i, c in enumerate(cams) if i % 8 != 0]   # every 8th is test (colmap.py:152-156)
+    scene = lodgen.build_lod_device(pos, op, sc, q, sh, mem, int(np.prod(dims)), train,
+                                    distance_intervals=ints)
+    lo = pos.double().min(dim=0).values.cpu().numpy()
+    hi = pos.double().max(dim=0).values.cpu().numpy()
+    center = 0.5 * (lo + hi)
+    radius = 0.5 * max(hi[0] - lo[0], hi[1] - lo[1])
+    del pos, op, sc, q, sh, mem
+    torch.cuda.empty_cache()
+    return scene, center, radius, alts, (W, H), time.perf_counter() - t0
+
+
+def flythrough(center, radius, alts, wh, per_alt):
+    from paper_2404_01133_b200.synth import orbit_cameras
+    cams = []
+    for a in alts:
+        cams += orbit_cameras(center, radius, a, per_alt, wh[0], wh[1])
+    return cams
+
+
+# ---------------------------------------------------------------------------
+# clocks
+
+
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = Path(f"/tmp/cs_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        rows = [l.split(",") for l in self.path.read_text().splitlines() if l.strip()]
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for name, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(name)
+            except (ValueError, IndexError):
+                continue
+        self.path.unlink(missing_ok=True)
+        busy = [s for s in sm if mx and s > 0.3 * mx] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic work per stage
+
+
+def stage_bytes(st: dict) -> dict:
+    """Algorithmic HBM bytes of each stage summed over the measured frames."""
+    na, m, p = st["assembled"], st["visible"], st["pairs"]
+    sh_bytes = st["sh_bytes_visible"]
+    return {
+        "project": na * 48 + sh_bytes + m * (128 + 8 + 4),
+        "depth_sort": m * 8 + 8 * 2 * m * 12,                 # histogram read + 8 passes r/w
+        "gather_scan": m * (4 + 128 + 48 + 32 + 16 + 8 + 8),
+        "duplicate": m * 24 + p * 8,
+        "tile_sort": p * 4 + 2 * 2 * p * 8,                   # histogram read + 2 passes r/w
+        "ranges": p * 4,
+    }
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import ctypes
+
+    import paper_2404_01133_b200 as cs
+    from paper_2404_01133_b200 import _lib, device
+    from paper_2404_01133_b200._lib import CsFrameStats, CsSource
+
+    scene, center, radius, alts, wh, build_s = build_scene(args.scene, args.seed, dev)
+    cams_all = flythrough(center, radius, alts, wh, args.frames_per_altitude)
+    # view split: rank r renders its contiguous share of the flythrough, cycling
+    share = [cams_all[i] for i in range(len(cams_all)) if i * world // len(cams_all) == rank] or cams_all
+    settings = cs.RenderSettings()
+    lib = _lib.load()
+    ctx = device.context(local)
+    stream = torch.cuda.current_stream(dev)
+    sh = ctypes.c_void_p(stream.cuda_stream)
+    src = CsSource()
+    src.kind = _lib.CS_SRC_LOD_BLOCK
+    src.force_level = -1
+    src.lod = scene.handle
+    cset = device.settings_struct(settings)
+    W, H = wh
+    out = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
+    ccams = [device.camera_struct(c) for c in share]
+
+    def frame(i, flags=0, stats=None):
+        rc = lib.cs_render(ctx, ctypes.byref(src), ctypes.byref(ccams[i % len(ccams)]), ctypes.byref(cset),
+                           out.data_ptr(), flags, ctypes.byref(stats) if stats is not None else None, sh)
+        _lib.check(rc, "cs_render")
+
+    # sizing pass (synchronous, grows pair buffers) + per-frame counts for the roofline
+    K = args.steps
+    counts = dict(assembled=0, visible=0, pairs=0, evals=0, fragments=0, sh_bytes_visible=0)
+    for i in range(min(len(ccams), max(K, 1))):
+        s = CsFrameStats()
+        frame(i, _lib.CS_RENDER_SYNC, s)
+    for i in range(K):
+        s = CsFrameStats()
+        frame(i, _lib.CS_RENDER_SYNC, s)
+        counts["assembled"] += s.assembled
+        counts["visible"] += s.visible
+        counts["pairs"] += s.pairs
+        counts["evals"] += s.evals
+        counts["fragments"] += s.fragments
+    # SH bytes read per visible splat depend on its level (C = 16/9/4 -> 192/108/48 B);
+    # bounded by the finest width, estimated from the assembled level mix
+    counts["sh_bytes_visible"] = counts["visible"] * 12 * 9
+    for i in range(args.warmup):
+        frame(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    lib.cs_timing_begin(ctx, K)
+    with ClockSampler(local) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(K):
+            frame(i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    stage = (ctypes.c_double * 8)()
+    nfr = ctypes.c_int32(0)
+    _lib.check(lib.cs_timing_end(ctx, stage, ctypes.byref(nfr)))
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    ms_max = float(t.item())
+    stages_ms = {k: stage[i] / max(nfr.value, 1) for i, k in enumerate(STAGES)}
+
+    # e2e: same frames through the C ABI, image copied to pinned host memory each frame
+    e2e = None
+    if not args.no_e2e:
+        host = [torch.empty((H, W, 3), dtype=torch.float32, pin_memory=True) for _ in range(2)]
+        outs = [out, torch.empty_like(out)]
+        copy_stream = torch.cuda.Stream(dev)
+        done = [torch.cuda.Event(), torch.cuda.Event()]
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for i in range(K):
+            b = i & 1
+            done[b].synchronize()  # host buffer b free again
+            rc = lib.cs_render(ctx, ctypes.byref(src), ctypes.byref(ccams[i % len(ccams)]),
+                               ctypes.byref(cset), outs[b].data_ptr(), 0, None, sh)
+            _lib.check(rc)
+            ready = torch.cuda.Event()
+            ready.record(stream)
+            with torch.cuda.stream(copy_stream):
+                copy_stream.wait_event(ready)
+                host[b].copy_(outs[b], non_blocking=True)
+                done[b].record(copy_stream)
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_s = float(te.item())
+        e2e = {"value": world * K / e2e_s, "unit": "frames/s",
+               "h2d_bytes_per_step": ctypes.sizeof(_lib.CsCamera) + ctypes.sizeof(_lib.CsSettings),
+               "d2h_bytes_per_step": H * W * 3 * 4,
+               "path": "cs_render (C ABI) + D2H of the float32 image into pinned host memory"}
+
+    clocks = clk.summary()
+    value = world * K / (ms_max / 1000.0)
+    # roofline of the dominant kernel
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    bytes_ = stage_bytes(counts)
+    dom = max(STAGES, key=lambda k: stages_ms[k])
+    roof = {}
+    if dom in bytes_:
+        achieved = (bytes_[dom] / K) / (stages_ms[dom] / 1000.0) / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback"}
+    else:  # blend: float64 pipe (quadratic form per evaluation, exact path per fragment)
+        fp64_peak = 148 * 64 * 2 * (clocks.get("sm_mhz") or 1965.0) * 1e6 / 1e12  # TFLOP/s at observed clock
+        flops = (22.0 * counts["evals"] + 60.0 * counts["fragments"]) / K
+        achieved = flops / (stages_ms[dom] / 1000.0) / 1e12
+        roof = {"kernel": dom, "bound": "fp64", "achieved": achieved, "peak": fp64_peak,
+                "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": None,
+                "peak_source": "nominal 148 SM x 64 DFMA/clk at the sampled SM clock"}
+    roof["stage_bytes_per_frame"] = {k: v / K for k, v in bytes_.items()}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(scene, cams_all, settings, n_frames=1)
+
+    if rank == 0:
+        line = {
+            "metric": "1080p FPS on 23M-Gaussian LoD city" if args.scene == "c3" else f"FPS ({args.scene})",
+            "value": value, "unit": "frames/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (generate_city_torch, reference distributions), random-init scene",
+            "config": {"workload": f"{args.scene}: {SCENES[args.scene][0]} Gaussians, "
+                                   f"{SCENES[args.scene][3][0]}x{SCENES[args.scene][3][1]} blocks, 3 LoD levels, "
+                                   f"{wh[0]}x{wh[1]} flythrough at {list(alts)} m",
+                       "frames_in_flythrough": len(cams_all), "view_split": world > 1,
+                       "l2": "per-frame inputs (>600 MB) exceed L2; no flush",
+                       "scene_build_s": round(build_s, 1)},
+            "stages_ms": stages_ms,
+            "counts_per_frame": {k: v / K for k, v in counts.items()},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": K * launches_per_frame(),
+            "clocks": clocks,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def launches_per_frame() -> int:
+    # memset(stats), select, memset(status), project, [hist memset, ticket memset, hist, scan,
+    # 8 x (status memset + onesweep)], memset, gather, duplicate, [memset x2, hist, scan,
+    # 2 x (memset + onesweep)], memset, ranges, blend  -- kernels only:
+    return 1 + 1 + 2 + 8 + 1 + 1 + 2 + 2 + 1 + 1
+
+
+def host_scene(scene):
+    """Materialise the device LoD scene as float32 host arrays for the oracle."""
+    from types import SimpleNamespace
+    levels = []
+    for L in range(scene.n_levels):
+        lc = scene.level_clouds[L]
+        pos_op = lc.pos_op.float().cpu().numpy()
+        scl = lc.scale.float().cpu().numpy()
+        quat = lc.quat.float().cpu().numpy()
+        C = lc.sh_coeffs
+        sh = lc.sh[:, :3 * C].cpu().numpy().reshape(-1, 3, C)
+        blocks = []
+        for j in range(scene.n_blocks):
+            o = int(scene.block_offsets[L][j])
+            n = int(scene.counts[L, j])
+            blocks.append(SimpleNamespace(positions=pos_op[o:o + n, :3], opacities=pos_op[o:o + n, 3],
+                                          scales=scl[o:o + n, :3], rotations=quat[o:o + n], sh=sh[o:o + n],
+                                          count=n))
+        levels.append(tuple(blocks))
+    return SimpleNamespace(levels=tuple(levels), bounds_min=scene.bounds_min, bounds_max=scene.bounds_max,
+                           distance_intervals=scene.distance_intervals)
+
+
+def cpu_baseline(scene, cams, settings, n_frames=1):
+    """The C oracle port (oracle/), all host threads, on a bounded sample."""
+    from oracle import oracle as O
+    hs = host_scene(scene)
+    pick = [cams[len(cams) // 2 + i] for i in range(n_frames)]   # 300 m altitude frames
+    O.lib()
+    t0 = time.perf_counter()
+    for cam in pick:
+        cloud, _ = O.assemble(hs, cam)
+        O.rasterize_frame_c(cloud, cam, settings, nthreads=os.cpu_count() or 1)
+    dt = time.perf_counter() - t0
+    return {"value": n_frames / dt, "unit": "frames/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{n_frames} frame(s) of the 300 m orbit (assemble + project + sort + bin + blend)"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm on the host cores (the C oracle
+    port, oracle/; the reference package itself is Python and does not travel)."""
+    if rank != 0:
+        return 0
+    import torch
+    torch.cuda.set_device(0)
+    import paper_2404_01133_b200 as cs
+    scene, center, radius, alts, wh, build_s = build_scene(args.scene, args.seed, torch.device("cuda", 0))
+    cams = flythrough(center, radius, alts, wh, args.frames_per_altitude)
+    from oracle import oracle as O
+    hs = host_scene(scene)
+    settings = cs.RenderSettings()
+    nthreads = os.cpu_count() or 1
+    steps = max(1, min(args.steps, 4))
+    warm = min(args.warmup, 1)
+    for i in range(warm):
+        cloud, _ = O.assemble(hs, cams[i])
+        O.rasterize_frame_c(cloud, cams[i], settings, nthreads=nthreads)
+    t0 = time.perf_counter()
+    for i in range(steps):
+        cam = cams[(i * len(cams)) // steps]
+        cloud, _ = O.assemble(hs, cam)
+        O.rasterize_frame_c(cloud, cam, settings, nthreads=nthreads)
+    dt = time.perf_counter() - t0
+    v = steps / dt
+    print(json.dumps({
+        "impl": "reference", "metric": "1080p FPS on 23M-Gaussian LoD city", "value": v,
+        "unit": "frames/s", "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": 1000 * dt / steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": f"{args.scene} flythrough, {steps} frames spread over "
+                                                    f"altitudes {list(alts)} m"},
+        "cpu_baseline": {"value": v, "unit": "frames/s", "cores": nthreads, "kind": "port",
+                         "sample": f"{steps} of {len(cams)} flythrough frames (requested steps={args.steps})"},
+        "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main() or 0)

@@ -81,6 +81,7 @@ typedef struct cs_frame_stats {
   int64_t fragments;        /* FrameStats.blended_fragments */
   int32_t n_segments;       /* (level, block) pieces concatenated */
   int32_t status;           /* bit0 pair-buffer overflow, bit1 CS_ERANGE */
+  int64_t evals;            /* blend evaluations E (pixel x splat pairs walked) */
 } cs_frame_stats;
 
 /* One block decision, VisibilityDecision (lod.py:255-264). level -1 = None. */
@@ -161,6 +162,12 @@ int cs_select_level(cs_ctx* ctx, int32_t n, const double* distances, int32_t n_i
  * device-side stats can be read later with cs_frame_stats_get. */
 int cs_render(cs_ctx* ctx, const cs_source* src, const cs_camera* cam, const cs_settings* st,
               void* out_rgb, uint32_t flags, cs_frame_stats* stats_host, void* stream);
+
+/* Per-stage CUDA-event timing of the next max_frames cs_render calls on this
+ * context; cs_timing_end returns per-stage sums in ms over the frames timed:
+ * [select, project, depth_sort, gather_scan, duplicate, tile_sort, ranges, blend]. */
+int cs_timing_begin(cs_ctx* ctx, int32_t max_frames);
+int cs_timing_end(cs_ctx* ctx, double* stage_ms, int32_t* frames);
 
 /* Stats of the last frame (synchronises the stream). */
 int cs_frame_stats_get(cs_ctx* ctx, cs_frame_stats* out, void* stream);

@@ -44,7 +44,8 @@ class CsCloud(ctypes.Structure):
 
 class CsFrameStats(ctypes.Structure):
     _fields_ = [("assembled", i64), ("visible", i64), ("skipped_singular", i64),
-                ("pairs", i64), ("fragments", i64), ("n_segments", i32), ("status", i32)]
+                ("pairs", i64), ("fragments", i64), ("n_segments", i32), ("status", i32),
+                ("evals", i64)]
 
 
 class CsDecision(ctypes.Structure):
@@ -78,6 +79,8 @@ _SIGS = {
                                  ctypes.POINTER(CsSettings), vp, ctypes.c_uint32,
                                  ctypes.POINTER(CsFrameStats), vp]),
     "cs_frame_stats_get": (ctypes.c_int, [vp, ctypes.POINTER(CsFrameStats), vp]),
+    "cs_timing_begin": (ctypes.c_int, [vp, i32]),
+    "cs_timing_end": (ctypes.c_int, [vp, vp, vp]),
     "cs_dump_projected": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "cs_dump_tiles": (ctypes.c_int, [vp, vp, vp, vp]),
     "cs_dump_segments": (ctypes.c_int, [vp, vp, vp, i32, vp, vp]),

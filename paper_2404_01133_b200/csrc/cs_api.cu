@@ -172,7 +172,18 @@ struct cs_ctx {
   const uint2* last_ranges = nullptr;
   int last_tiles = 0;
   int last_width = 0, last_height = 0;
+  // per-stage CUDA-event timing (cs_timing_begin/end)
+  bool timing_on = false;
+  int timing_max = 0, timing_frame = 0;
+  std::vector<cudaEvent_t> tev;
 };
+
+static constexpr int kStages = 8;  // select, project, depth sort, gather+scan, duplicate,
+                                   // tile sort, ranges, blend
+static void mark(cs_ctx* c, int stage, cudaStream_t s) {
+  if (c->timing_on && c->timing_frame < c->timing_max)
+    cudaEventRecord(c->tev[(size_t)c->timing_frame * (kStages + 1) + stage], s);
+}
 
 extern "C" {
 
@@ -214,6 +225,7 @@ void cs_destroy(cs_ctx* c) {
                  &c->st_acc, &c->scratch1, &c->scratch2, &c->scratch3, &c->scratch4};
   for (DBuf* b : all) b->release();
   if (c->h_stats) cudaFreeHost(c->h_stats);
+  for (cudaEvent_t e : c->tev) cudaEventDestroy(e);
   delete c;
 }
 
@@ -371,6 +383,8 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
   int rc = ensure_frame_buffers(c, cap_vis, n_segs, n_blocks, n_tiles, cap_pw);
   if (rc) return rc;
   DevStats* stats = c->stats.as<DevStats>();
+  const bool timed = !(flags & CS_RENDER_PROJECT_ONLY);
+  if (timed) mark(c, 0, s);
   CS_CUDA(cudaMemsetAsync(stats, 0, sizeof(DevStats), s));
   const cs_cloud* clouds = nullptr;
   const uint64_t* list = nullptr;
@@ -389,11 +403,13 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
     list = c->pw_list.as<uint64_t>();
   }
   CS_CHECK_LAUNCH();
+  if (timed) mark(c, 1, s);
   const int64_t cap = std::max<int64_t>(cap_vis, 1);
   CS_CUDA(cudaMemsetAsync(c->st_proj.p, 0, 8 * ((cap + 255) / 256 + 1), s));
   launch_project(clouds, c->segs.as<Seg>(), stats, *cam, *st, c->st_proj.as<uint64_t>(), cap,
                  c->keysA.as<uint64_t>(), c->valsA.as<uint32_t>(), c->recs.as<ProjRec>(), list, s);
   CS_CHECK_LAUNCH();
+  if (timed) mark(c, 2, s);
   // K4: global depth order (stable => ties keep assembled order)
   const int which = radix_sort<uint64_t>(c->keysA.as<uint64_t>(), c->valsA.as<uint32_t>(),
                                          c->keysB.as<uint64_t>(), c->valsB.as<uint32_t>(),
@@ -401,6 +417,7 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
                                          c->st_sort.as<uint32_t>(), c->sort_tickets.as<uint32_t>(), s);
   CS_CHECK_LAUNCH();
   const uint32_t* order = which ? c->valsB.as<uint32_t>() : c->valsA.as<uint32_t>();
+  if (timed) mark(c, 3, s);
   // K5: gather by rank, rects, pair-count scan
   CS_CUDA(cudaMemsetAsync(c->st_gather.p, 0, 8 * ((cap + 255) / 256 + 1), s));
   launch_gather_count(order, c->recs.as<ProjRec>(), stats, ts, cam->width, cam->height,
@@ -408,6 +425,7 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
                       c->hot.as<HotRec>(), c->cold.as<ColdRec>(), c->rects.as<int4>(),
                       c->src_sorted.as<int64_t>(), c->pair_off.as<int64_t>(), s);
   CS_CHECK_LAUNCH();
+  if (timed) mark(c, 4, s);
   if (flags & CS_RENDER_PROJECT_ONLY) {
     c->last_order = order;
     c->last_list = nullptr;
@@ -417,6 +435,7 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
   launch_duplicate(c->pair_off.as<int64_t>(), c->rects.as<int4>(), stats, ntx, c->cap_pairs,
                    c->pkA.as<uint32_t>(), c->pvA.as<uint32_t>(), s);
   CS_CHECK_LAUNCH();
+  mark(c, 5, s);
   // K7: stable sort by tile id only (ceil(log2 T) bits)
   const int which2 = radix_sort<uint32_t>(c->pkA.as<uint32_t>(), c->pvA.as<uint32_t>(),
                                           c->pkB.as<uint32_t>(), c->pvB.as<uint32_t>(),
@@ -426,10 +445,12 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
   CS_CHECK_LAUNCH();
   const uint32_t* tkeys = which2 ? c->pkB.as<uint32_t>() : c->pkA.as<uint32_t>();
   const uint32_t* tvals = which2 ? c->pvB.as<uint32_t>() : c->pvA.as<uint32_t>();
+  mark(c, 6, s);
   // K8: tile ranges
   CS_CUDA(cudaMemsetAsync(c->ranges.p, 0, sizeof(uint2) * n_tiles, s));
   launch_tile_ranges(tkeys, stats, c->ranges.as<uint2>(), s);
   CS_CHECK_LAUNCH();
+  mark(c, 7, s);
   // K9: blend
   BlendParams bp;
   for (int i = 0; i < 3; ++i) bp.bg[i] = st->background[i];
@@ -451,6 +472,8 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
                bp, out, (flags & CS_RENDER_F64_OUT) != 0, c->frag_tile.as<int32_t>(), stats,
                (flags & CS_RENDER_KEEP_STATE) ? &keep : nullptr, s);
   CS_CHECK_LAUNCH();
+  mark(c, 8, s);
+  if (c->timing_on && c->timing_frame < c->timing_max) ++c->timing_frame;
   c->last_order = order;
   c->last_list = tvals;
   c->last_ranges = c->ranges.as<uint2>();
@@ -496,6 +519,39 @@ int cs_render(cs_ctx* c, const cs_source* src, const cs_camera* cam, const cs_se
     if (c->h_stats->pairs >= (1ll << 30)) return fail(CS_ENOMEM, "more than 2^30 tile pairs");
   }
   return fail(CS_ECUDA, "pair buffer did not converge");
+}
+
+int cs_timing_begin(cs_ctx* c, int32_t max_frames) {
+  if (!c || max_frames <= 0) return fail(CS_EINVAL, "bad argument");
+  CS_CUDA(cudaSetDevice(c->device));
+  const size_t need = (size_t)max_frames * (kStages + 1);
+  while (c->tev.size() < need) {
+    cudaEvent_t e;
+    CS_CUDA(cudaEventCreate(&e));
+    c->tev.push_back(e);
+  }
+  c->timing_max = max_frames;
+  c->timing_frame = 0;
+  c->timing_on = true;
+  return CS_OK;
+}
+
+int cs_timing_end(cs_ctx* c, double* stage_ms, int32_t* frames) {
+  if (!c || !stage_ms || !frames) return fail(CS_EINVAL, "NULL argument");
+  CS_CUDA(cudaSetDevice(c->device));
+  c->timing_on = false;
+  for (int k = 0; k < kStages; ++k) stage_ms[k] = 0.0;
+  for (int f = 0; f < c->timing_frame; ++f) {
+    cudaEvent_t* e = &c->tev[(size_t)f * (kStages + 1)];
+    CS_CUDA(cudaEventSynchronize(e[kStages]));
+    for (int k = 0; k < kStages; ++k) {
+      float ms = 0.f;
+      CS_CUDA(cudaEventElapsedTime(&ms, e[k], e[k + 1]));
+      stage_ms[k] += ms;
+    }
+  }
+  *frames = c->timing_frame;
+  return CS_OK;
 }
 
 int cs_frame_stats_get(cs_ctx* c, cs_frame_stats* out, void* stream) {

@@ -38,6 +38,7 @@ k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
         BlendState state) {
   __shared__ __align__(16) HotRec buf[2][kBatch];
   __shared__ int s_red[kBlendThreads / 32];
+  __shared__ int s_ev[kBlendThreads / 32];
   const int t = blockIdx.x;
   const int tx = t % bp.ntx, ty = t / bp.ntx;
   const int ts = bp.tile_size;
@@ -46,6 +47,7 @@ k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
 
   double sx[PPT], sy[PPT], T[PPT], cr[PPT], cg[PPT], cb[PPT];
   int cnt[PPT], last[PPT];
+  int evals = 0;
   bool done[PPT], valid[PPT];
 #pragma unroll
   for (int q = 0; q < PPT; ++q) {
@@ -90,7 +92,8 @@ k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
     for (int q = 0; q < PPT; ++q) {
       if (done[q]) continue;
       double Tq = T[q];
-      for (int j = 0; j < nb; ++j) {
+      int j = 0;
+      for (; j < nb; ++j) {
         const HotRec h = hb[j];
         const double dx = dsub(sx[q], h.mx);
         const double dy = dsub(sy[q], h.my);
@@ -104,7 +107,7 @@ k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
         if (alpha > 0.99) alpha = 0.99;              // _kernels.py:59-60
         if (alpha < bp.alpha_floor) continue;        // _kernels.py:61-62
         const double nt = dmul(Tq, dsub(1.0, alpha));
-        if (nt < bp.t_floor) { done[q] = true; break; }  // _kernels.py:63-66
+        if (nt < bp.t_floor) { done[q] = true; ++j; break; }  // _kernels.py:63-66
         const double w = dmul(Tq, alpha);
         cr[q] += w * (double)c.r;
         cg[q] += w * (double)c.g;
@@ -113,6 +116,7 @@ k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
         cnt[q] += 1;
         last[q] = (int)(bstart + j + 1);
       }
+      evals += j;
       T[q] = Tq;
     }
     int alive = 0;
@@ -146,14 +150,20 @@ k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
     }
   }
   my = warp_sum(my);
-  if (lane_id() == 0) s_red[threadIdx.x >> 5] = my;
+  evals = warp_sum(evals);
+  if (lane_id() == 0) {
+    s_red[threadIdx.x >> 5] = my;
+    s_ev[threadIdx.x >> 5] = evals;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     int tot = 0;
-    for (int w = 0; w < kBlendThreads / 32; ++w) tot += s_red[w];
+    long long ev = 0;
+    for (int w = 0; w < kBlendThreads / 32; ++w) { tot += s_red[w]; ev += s_ev[w]; }
     frag_tile[t] = tot;
     if (tot) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->fragments),
                        (unsigned long long)tot);
+    if (ev) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->evals), (unsigned long long)ev);
   }
 }
 

@@ -64,6 +64,7 @@ struct DevStats {     // device mirror of cs_frame_stats + scratch counters
   int64_t fragments;
   int32_t n_segs;
   int32_t status;
+  int64_t evals;         // blend (pixel, splat) evaluations executed (E)
   int64_t pairs_eff;     // pairs actually processed (0 when the pair buffer overflowed)
   uint32_t tickets[16];  // chunk tickets for single-pass kernels, zeroed per frame
 };
