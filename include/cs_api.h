@@ -126,6 +126,7 @@ typedef struct cs_source {
 #define CS_RENDER_NO_CLIP 4u     /* leave the image unclipped */
 #define CS_RENDER_KEEP_STATE 8u  /* keep per-pixel state for cs_render_backward */
 #define CS_RENDER_PROJECT_ONLY 16u /* stop after projection + depth order (cs_dump_projected) */
+#define CS_RENDER_DEBUG 32u        /* also keep the full projected records (cs_dump_projected) */
 
 /* ---- context ----------------------------------------------------------- */
 int cs_create(int device, cs_ctx** out);
@@ -162,6 +163,26 @@ int cs_select_level(cs_ctx* ctx, int32_t n, const double* distances, int32_t n_i
  * device-side stats can be read later with cs_frame_stats_get. */
 int cs_render(cs_ctx* ctx, const cs_source* src, const cs_camera* cam, const cs_settings* st,
               void* out_rgb, uint32_t flags, cs_frame_stats* stats_host, void* stream);
+
+/* Parameter gradients (device, float32, caller-allocated) for cs_render_backward,
+ * laid out like the cloud's rows: positions (K,3), scales (K,3), rotations (K,4)
+ * w.r.t. the raw (w,x,y,z) entering quat_to_rotmat, opacities (K) w.r.t. the
+ * activated opacity, sh (K,3,C). */
+typedef struct cs_grads {
+  float* positions;
+  float* scales;
+  float* rotations;
+  float* opacities;
+  float* sh;
+} cs_grads;
+
+/* Backward of the last cs_render on this context (which must have used
+ * CS_RENDER_KEEP_STATE with the same single-cloud source, camera and settings):
+ * dL/dimage (device (H,W,3) float32) -> parameter gradients.  Not in the
+ * reference; semantics in SURVEY.md Appendix A. */
+int cs_render_backward(cs_ctx* ctx, const cs_source* src, const cs_camera* cam,
+                       const cs_settings* st, const float* dl_dimg, const cs_grads* out,
+                       void* stream);
 
 /* Per-stage CUDA-event timing of the next max_frames cs_render calls on this
  * context; cs_timing_end returns per-stage sums in ms over the frames timed:

@@ -16,6 +16,7 @@ CS_OK, CS_EINVAL, CS_ECUDA, CS_ENOMEM, CS_ERANGE = 0, -1, -2, -3, -4
 CS_SRC_CLOUD, CS_SRC_LOD_BLOCK, CS_SRC_LOD_POINT = 0, 1, 2
 CS_RENDER_SYNC, CS_RENDER_F64_OUT, CS_RENDER_NO_CLIP, CS_RENDER_KEEP_STATE = 1, 2, 4, 8
 CS_RENDER_PROJECT_ONLY = 16
+CS_RENDER_DEBUG = 32
 
 c_double_p = ctypes.POINTER(ctypes.c_double)
 vp = ctypes.c_void_p
@@ -60,6 +61,10 @@ class CsLodDesc(ctypes.Structure):
                 ("intervals", c_double_p)]
 
 
+class CsGrads(ctypes.Structure):
+    _fields_ = [("positions", vp), ("scales", vp), ("rotations", vp), ("opacities", vp), ("sh", vp)]
+
+
 class CsSource(ctypes.Structure):
     _fields_ = [("kind", i32), ("force_level", i32), ("cloud", CsCloud), ("lod", vp)]
 
@@ -79,6 +84,8 @@ _SIGS = {
                                  ctypes.POINTER(CsSettings), vp, ctypes.c_uint32,
                                  ctypes.POINTER(CsFrameStats), vp]),
     "cs_frame_stats_get": (ctypes.c_int, [vp, ctypes.POINTER(CsFrameStats), vp]),
+    "cs_render_backward": (ctypes.c_int, [vp, ctypes.POINTER(CsSource), ctypes.POINTER(CsCamera),
+                                          ctypes.POINTER(CsSettings), vp, ctypes.POINTER(CsGrads), vp]),
     "cs_timing_begin": (ctypes.c_int, [vp, i32]),
     "cs_timing_end": (ctypes.c_int, [vp, vp, vp]),
     "cs_dump_projected": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),

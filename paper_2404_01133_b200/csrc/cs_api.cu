@@ -25,8 +25,7 @@ namespace cs {
 // cs_project.cu
 void launch_project(const cs_cloud* d_clouds, const Seg* d_segs, DevStats* d_stats,
                     const cs_camera& cam, const cs_settings& st, uint64_t* status,
-                    int64_t capacity, uint64_t* keys, uint32_t* vals, ProjRec* recs,
-                    const uint64_t* list, cudaStream_t s);
+                    int64_t capacity, const ProjOutputs& out, const uint64_t* list, cudaStream_t s);
 void launch_setup_cloud(const cs_cloud& c, cs_cloud* d_clouds, Seg* d_segs, DevStats* d_stats,
                         cudaStream_t s);
 void launch_build_covariances(int64_t n, const double* scales, const double* quats, double* out,
@@ -49,21 +48,20 @@ int radix_sort(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_dev, i
                int begin_bit, int end_bit, uint32_t* hist, uint32_t* status, uint32_t* tickets,
                cudaStream_t s);
 // cs_bin.cu
-void launch_gather_count(const uint32_t* order, const ProjRec* recs, DevStats* stats,
-                         int tile_size, int width, int height, double alpha_floor,
-                         int64_t pair_cap, int64_t capacity, uint64_t* status, HotRec* hot,
-                         ColdRec* cold, int4* rects, int64_t* src_sorted, int64_t* pair_off,
-                         cudaStream_t s);
-void launch_duplicate(const int64_t* pair_off, const int4* rects, const DevStats* stats, int ntx,
-                      int64_t pair_cap, uint32_t* keys, uint32_t* vals, cudaStream_t s);
+void launch_pair_count(const uint32_t* order, const int4* rects, DevStats* stats, int64_t pair_cap,
+                       int64_t capacity, uint64_t* status, int64_t* pair_off, cudaStream_t s);
+void launch_duplicate(const int64_t* pair_off, const uint32_t* order, const int4* rects,
+                      const DevStats* stats, int ntx, int64_t pair_cap, uint32_t* keys,
+                      uint32_t* vals, cudaStream_t s);
 void launch_tile_ranges(const uint32_t* keys, const DevStats* stats, uint2* ranges,
                         cudaStream_t s);
 void launch_dump_projected(const uint32_t* order, const ProjRec* recs, const DevStats* stats,
                            double* means, double* conics, double* covs, double* depths,
                            double* colors, double* opac, double* radii, int64_t* src,
                            cudaStream_t s);
-void launch_dump_tiles(const uint32_t* vals, const uint2* ranges, const DevStats* stats,
-                       int n_tiles, int64_t* tile_ids, int64_t* offsets, cudaStream_t s);
+void launch_dump_tiles(const uint32_t* order, const uint32_t* vals, const uint2* ranges,
+                       const DevStats* stats, int n_tiles, int64_t* rank_of, int64_t* tile_ids,
+                       int64_t* offsets, cudaStream_t s);
 // cs_blend.cu
 int blend_ppt(int tile_size);
 void launch_blend(int n_tiles, const uint32_t* list, const uint2* ranges, const HotRec* hot,
@@ -80,6 +78,14 @@ void launch_block_of_points(int64_t n, const void* pos, int f32, const double* p
 void launch_fuse_filter(int64_t n, const void* pos, int f32, const double* pmin, const double* pmax,
                         int nx, int ny, int nz, int block, uint64_t* status, uint32_t* ticket,
                         int64_t* kept, int64_t* kept_count, cudaStream_t s);
+// cs_backward.cu
+void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint2* ranges, const HotRec* hot,
+                      const ColdRec* cold, const cs_settings& st, int width, int height, int ntx,
+                      const float* dl_dimg, const BlendState& state, float* grads, int64_t cap,
+                      cudaStream_t s);
+void launch_project_bwd(const cs_cloud& cl, const int64_t* src,
+                        const DevStats* stats, const cs_camera& cam, const cs_settings& st,
+                        const float* grads, int64_t cap, const cs_grads& out, cudaStream_t s);
 }  // namespace cs
 
 using namespace cs;
@@ -160,14 +166,16 @@ struct cs_ctx {
   DBuf stats, clouds1, segs, dec;
   DBuf st_proj, st_gather, st_pw, st_fuse, st_sort, hist, sort_tickets, fuse_ticket;
   DBuf keysA, valsA, keysB, valsB, recs;
-  DBuf hot, cold, rects, src_sorted, pair_off;
+  DBuf hot, cold, rects, src, pair_off;
   DBuf pkA, pvA, pkB, pvB, ranges, frag_tile, pw_list;
   DBuf st_t, st_last, st_acc;
   DBuf scratch1, scratch2, scratch3, scratch4;  // API utilities
+  DBuf gacc;                                    // per-rank blend-backward partials
   cs_frame_stats* h_stats = nullptr;            // pinned
   int64_t cap_vis = 0, cap_pairs = 0, cap_pw = 0, cap_tiles = 0;
   // last frame bookkeeping (for dumps / backward)
   const uint32_t* last_order = nullptr;
+  bool last_debug = false;
   const uint32_t* last_list = nullptr;
   const uint2* last_ranges = nullptr;
   int last_tiles = 0;
@@ -220,9 +228,9 @@ void cs_destroy(cs_ctx* c) {
   DBuf* all[] = {&c->stats, &c->clouds1, &c->segs, &c->dec, &c->st_proj, &c->st_gather,
                  &c->st_pw, &c->st_fuse, &c->st_sort, &c->hist, &c->sort_tickets,
                  &c->fuse_ticket, &c->keysA, &c->valsA, &c->keysB, &c->valsB, &c->recs, &c->hot,
-                 &c->cold, &c->rects, &c->src_sorted, &c->pair_off, &c->pkA, &c->pvA, &c->pkB,
+                 &c->cold, &c->rects, &c->src, &c->pair_off, &c->pkA, &c->pvA, &c->pkB,
                  &c->pvB, &c->ranges, &c->frag_tile, &c->pw_list, &c->st_t, &c->st_last,
-                 &c->st_acc, &c->scratch1, &c->scratch2, &c->scratch3, &c->scratch4};
+                 &c->st_acc, &c->gacc, &c->scratch1, &c->scratch2, &c->scratch3, &c->scratch4};
   for (DBuf* b : all) b->release();
   if (c->h_stats) cudaFreeHost(c->h_stats);
   for (cudaEvent_t e : c->tev) cudaEventDestroy(e);
@@ -302,9 +310,9 @@ static int ensure_frame_buffers(cs_ctx* c, int64_t cap_vis, int n_segs, int n_bl
     const int64_t chunks = (cap + 255) / 256 + 1;
     if (c->st_proj.ensure(8 * chunks) || c->st_gather.ensure(8 * chunks) ||
         c->keysA.ensure(8 * cap) || c->keysB.ensure(8 * cap) || c->valsA.ensure(4 * cap) ||
-        c->valsB.ensure(4 * cap) || c->recs.ensure(sizeof(ProjRec) * cap) ||
-        c->hot.ensure(sizeof(HotRec) * cap) || c->cold.ensure(sizeof(ColdRec) * cap) ||
-        c->rects.ensure(16 * cap) || c->src_sorted.ensure(8 * cap) || c->pair_off.ensure(8 * cap))
+        c->valsB.ensure(4 * cap) || c->hot.ensure(sizeof(HotRec) * cap) ||
+        c->cold.ensure(sizeof(ColdRec) * cap) || c->rects.ensure(16 * cap) ||
+        c->src.ensure(8 * cap) || c->pair_off.ensure(8 * cap))
       return fail(CS_ENOMEM, "visible-splat buffers (%lld)", (long long)cap);
     c->cap_vis = cap;
   }
@@ -406,8 +414,14 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
   if (timed) mark(c, 1, s);
   const int64_t cap = std::max<int64_t>(cap_vis, 1);
   CS_CUDA(cudaMemsetAsync(c->st_proj.p, 0, 8 * ((cap + 255) / 256 + 1), s));
-  launch_project(clouds, c->segs.as<Seg>(), stats, *cam, *st, c->st_proj.as<uint64_t>(), cap,
-                 c->keysA.as<uint64_t>(), c->valsA.as<uint32_t>(), c->recs.as<ProjRec>(), list, s);
+  const bool debug = (flags & (CS_RENDER_DEBUG | CS_RENDER_PROJECT_ONLY)) != 0;
+  if (debug && c->recs.ensure(sizeof(ProjRec) * c->cap_vis)) return fail(CS_ENOMEM, "debug records");
+  ProjOutputs po{c->keysA.as<uint64_t>(), c->valsA.as<uint32_t>(), c->hot.as<HotRec>(),
+                 c->cold.as<ColdRec>(), c->rects.as<int4>(), c->src.as<int64_t>(),
+                 debug ? c->recs.as<ProjRec>() : nullptr};
+  launch_project(clouds, c->segs.as<Seg>(), stats, *cam, *st, c->st_proj.as<uint64_t>(), cap, po,
+                 list, s);
+  c->last_debug = debug;
   CS_CHECK_LAUNCH();
   if (timed) mark(c, 2, s);
   // K4: global depth order (stable => ties keep assembled order)
@@ -418,12 +432,10 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
   CS_CHECK_LAUNCH();
   const uint32_t* order = which ? c->valsB.as<uint32_t>() : c->valsA.as<uint32_t>();
   if (timed) mark(c, 3, s);
-  // K5: gather by rank, rects, pair-count scan
+  // K5: pair counts in depth order, scanned
   CS_CUDA(cudaMemsetAsync(c->st_gather.p, 0, 8 * ((cap + 255) / 256 + 1), s));
-  launch_gather_count(order, c->recs.as<ProjRec>(), stats, ts, cam->width, cam->height,
-                      st->alpha_floor, c->cap_pairs, cap, c->st_gather.as<uint64_t>(),
-                      c->hot.as<HotRec>(), c->cold.as<ColdRec>(), c->rects.as<int4>(),
-                      c->src_sorted.as<int64_t>(), c->pair_off.as<int64_t>(), s);
+  launch_pair_count(order, c->rects.as<int4>(), stats, c->cap_pairs, cap,
+                    c->st_gather.as<uint64_t>(), c->pair_off.as<int64_t>(), s);
   CS_CHECK_LAUNCH();
   if (timed) mark(c, 4, s);
   if (flags & CS_RENDER_PROJECT_ONLY) {
@@ -432,8 +444,8 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
     return CS_OK;
   }
   // K6: duplicate
-  launch_duplicate(c->pair_off.as<int64_t>(), c->rects.as<int4>(), stats, ntx, c->cap_pairs,
-                   c->pkA.as<uint32_t>(), c->pvA.as<uint32_t>(), s);
+  launch_duplicate(c->pair_off.as<int64_t>(), order, c->rects.as<int4>(), stats, ntx,
+                   c->cap_pairs, c->pkA.as<uint32_t>(), c->pvA.as<uint32_t>(), s);
   CS_CHECK_LAUNCH();
   mark(c, 5, s);
   // K7: stable sort by tile id only (ceil(log2 T) bits)
@@ -464,9 +476,9 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
   BlendState keep{nullptr, nullptr, nullptr};
   const int64_t npx = (int64_t)cam->width * cam->height;
   if (flags & CS_RENDER_KEEP_STATE) {
-    if (c->st_t.ensure(4 * npx) || c->st_last.ensure(4 * npx) || c->st_acc.ensure(12 * npx))
+    if (c->st_t.ensure(8 * npx) || c->st_last.ensure(4 * npx) || c->st_acc.ensure(24 * npx))
       return fail(CS_ENOMEM, "blend state");
-    keep = BlendState{c->st_t.as<float>(), c->st_last.as<int32_t>(), c->st_acc.as<float>()};
+    keep = BlendState{c->st_t.as<double>(), c->st_last.as<int32_t>(), c->st_acc.as<double>()};
   }
   launch_blend(n_tiles, tvals, c->ranges.as<uint2>(), c->hot.as<HotRec>(), c->cold.as<ColdRec>(),
                bp, out, (flags & CS_RENDER_F64_OUT) != 0, c->frag_tile.as<int32_t>(), stats,
@@ -521,6 +533,42 @@ int cs_render(cs_ctx* c, const cs_source* src, const cs_camera* cam, const cs_se
   return fail(CS_ECUDA, "pair buffer did not converge");
 }
 
+int cs_render_backward(cs_ctx* c, const cs_source* src, const cs_camera* cam,
+                       const cs_settings* st, const float* dl_dimg, const cs_grads* out,
+                       void* stream) {
+  if (!c || !src || !out || !dl_dimg) return fail(CS_EINVAL, "NULL argument");
+  int rc = validate(cam, st);
+  if (rc) return rc;
+  if (src->kind != CS_SRC_CLOUD) return fail(CS_EINVAL, "backward needs a single-cloud source");
+  if (!c->last_list || c->last_width != cam->width || c->last_height != cam->height ||
+      !c->st_t.p)
+    return fail(CS_EINVAL, "no kept forward state for this camera (render with KEEP_STATE first)");
+  std::lock_guard<std::mutex> lock(c->mu);
+  CS_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const cs_cloud& cl = src->cloud;
+  const int64_t cap = c->cap_vis;
+  if (c->gacc.ensure(sizeof(float) * 9 * cap)) return fail(CS_ENOMEM, "gradient partials");
+  CS_CUDA(cudaMemsetAsync(c->gacc.p, 0, sizeof(float) * 9 * cap, s));
+  const int ts = st->tile_size;
+  const int ntx = (cam->width + ts - 1) / ts;
+  BlendState state{c->st_t.as<double>(), c->st_last.as<int32_t>(), c->st_acc.as<double>()};
+  launch_blend_bwd(c->last_tiles, c->last_list, c->last_ranges, c->hot.as<HotRec>(),
+                   c->cold.as<ColdRec>(), *st, cam->width, cam->height, ntx, dl_dimg, state,
+                   c->gacc.as<float>(), cap, s);
+  CS_CHECK_LAUNCH();
+  const int64_t K = cl.count;
+  CS_CUDA(cudaMemsetAsync(out->positions, 0, 12 * K, s));
+  CS_CUDA(cudaMemsetAsync(out->scales, 0, 12 * K, s));
+  CS_CUDA(cudaMemsetAsync(out->rotations, 0, 16 * K, s));
+  CS_CUDA(cudaMemsetAsync(out->opacities, 0, 4 * K, s));
+  CS_CUDA(cudaMemsetAsync(out->sh, 0, 12 * (size_t)cl.sh_coeffs * K, s));
+  launch_project_bwd(cl, c->src.as<int64_t>(), c->stats.as<DevStats>(), *cam, *st,
+                     c->gacc.as<float>(), cap, *out, s);
+  CS_CHECK_LAUNCH();
+  return CS_OK;
+}
+
 int cs_timing_begin(cs_ctx* c, int32_t max_frames) {
   if (!c || max_frames <= 0) return fail(CS_EINVAL, "bad argument");
   CS_CUDA(cudaSetDevice(c->device));
@@ -567,6 +615,7 @@ int cs_dump_projected(cs_ctx* c, double* means, double* conics, double* covs, do
                       double* colors, double* opacities, double* radii, int64_t* source,
                       void* stream) {
   if (!c || !c->last_order) return fail(CS_EINVAL, "no frame rendered");
+  if (!c->last_debug) return fail(CS_EINVAL, "last frame was not rendered in debug mode");
   CS_CUDA(cudaSetDevice(c->device));
   cudaStream_t s = (cudaStream_t)stream;
   int rc = fetch_stats(c, s);
@@ -598,10 +647,13 @@ int cs_dump_tiles(cs_ctx* c, int64_t* tile_ids, int64_t* offsets, void* stream) 
   int rc = fetch_stats(c, s);
   if (rc) return rc;
   const int64_t P = c->h_stats->pairs;
-  if (c->scratch2.ensure(8 * (P + c->last_tiles + 1))) return fail(CS_ENOMEM, "dump");
+  const int64_t M = c->h_stats->visible;
+  if (c->scratch2.ensure(8 * (P + c->last_tiles + 1 + M))) return fail(CS_ENOMEM, "dump");
   int64_t* dt = c->scratch2.as<int64_t>();
   int64_t* doff = dt + P;
-  launch_dump_tiles(c->last_list, c->last_ranges, c->stats.as<DevStats>(), c->last_tiles, dt, doff, s);
+  int64_t* rank_of = doff + c->last_tiles + 1;
+  launch_dump_tiles(c->last_order, c->last_list, c->last_ranges, c->stats.as<DevStats>(),
+                    c->last_tiles, rank_of, dt, doff, s);
   CS_CHECK_LAUNCH();
   if (tile_ids && P) CS_CUDA(cudaMemcpyAsync(tile_ids, dt, 8 * P, cudaMemcpyDeviceToHost, s));
   if (offsets) CS_CUDA(cudaMemcpyAsync(offsets, doff, 8 * (c->last_tiles + 1), cudaMemcpyDeviceToHost, s));

@@ -1,0 +1,345 @@
+// cs_backward.cu -- K10/K11: backward of the forward in cs_project.cu +
+// cs_blend.cu, used by per-block training (absent in the reference,
+// SPEC.md:76; semantics from SURVEY.md Appendix A "backward-relevant forward
+// semantics").
+//
+// K10 blend backward: one CTA per tile, one thread per pixel, the same
+// batched shared-memory walk over the tile list as the forward, front to
+// back up to the pixel's last accepted fragment (kept by the forward).  The
+// forward's float64 decisions are re-evaluated identically, so exactly the
+// accepted fragments receive gradient; skipped / dropped fragments get none.
+// With T_k the transmittance before fragment k, P_k the colour accumulated
+// through k and S_k = (C_acc - P_k) + T_end*bg the light arriving from behind,
+//     dC/dc_k = T_k a_k,   dC/da_k = T_k c_k - S_k / (1 - a_k)
+// and a = min(0.99, o*exp(power)) passes gradient only when unclamped.
+// Per-splat partials (mean2d, conic, opacity, colour) are warp-reduced and
+// accumulated with one atomicAdd per warp into buffers indexed by compact id.
+//
+// K11 projection backward: one thread per visible splat; recomputes the
+// float64 forward (t, J, V, cov2d) and chains the partials to position,
+// scale, rotation (the unnormalised quaternion polynomial of core.py:74-82),
+// opacity and SH, including the view-direction term of the colour.
+#include <algorithm>
+
+#include "cs_internal.cuh"
+
+namespace cs {
+
+constexpr int kBwdThreads = 256;
+constexpr int kBwdBatch = 256;
+constexpr int kGradFields = 9;  // mx, my, c0, c1, c2, opacity, r, g, b
+
+struct BwdParams {
+  double bg[3];
+  double alpha_floor;
+  int tile_size, width, height, ntx;
+};
+
+__global__ void __launch_bounds__(kBwdThreads)
+k_blend_bwd(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
+            const HotRec* __restrict__ hot, const ColdRec* __restrict__ cold, BwdParams bp,
+            const float* __restrict__ dl_dimg, BlendState state, float* __restrict__ grads /* [kGradFields][cap] */, int64_t cap) {
+  __shared__ __align__(16) HotRec buf[kBwdBatch];
+  __shared__ int s_any;
+  const int t = blockIdx.x;
+  const int tx = t % bp.ntx, ty = t / bp.ntx;
+  const int ts = bp.tile_size;
+  const uint2 rg = ranges[t];
+  const int64_t s0 = rg.x, s1 = rg.y;
+  const int li = threadIdx.x;
+  const int px = tx * ts + li % ts, py = ty * ts + li / ts;
+  const bool valid = li < ts * ts && px < bp.width && py < bp.height;
+  double sx = (double)px + 0.5, sy = (double)py + 0.5;
+  int64_t last = s0;
+  double g[3] = {0.0, 0.0, 0.0}, acc[3] = {0.0, 0.0, 0.0}, Tend = 1.0;
+  if (valid) {
+    const int64_t pix = (int64_t)py * bp.width + px;
+    last = state.last[pix];
+    Tend = state.final_t[pix];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      acc[c] = state.color_acc[3 * pix + c];
+      const double o = acc[c] + Tend * bp.bg[c];  // unclipped pixel value
+      // clip to [0, 1] (render.py:273): gradient passes where 0 <= C <= 1
+      g[c] = (o >= 0.0 && o <= 1.0) ? (double)dl_dimg[3 * pix + c] : 0.0;
+    }
+  }
+  double T = 1.0, P[3] = {0.0, 0.0, 0.0};
+  int64_t my_end = valid ? last : s0;
+  for (int64_t bstart = s0; bstart < s1; bstart += kBwdBatch) {
+    if (threadIdx.x == 0) s_any = 0;
+    __syncthreads();
+    if (my_end > bstart) s_any = 1;
+    __syncthreads();
+    if (!s_any) break;
+    const int64_t k = bstart + threadIdx.x;
+    if (k < s1) buf[threadIdx.x] = hot[__ldg(list + k)];
+    __syncthreads();
+    const int nb = (int)min((int64_t)kBwdBatch, s1 - bstart);
+    for (int j = 0; j < nb; ++j) {
+      const HotRec h = buf[j];
+      float gr[kGradFields];
+      bool contrib = false;
+      if (bstart + j < my_end) {
+        const double dx = dsub(sx, h.mx), dy = dsub(sy, h.my);
+        const double power =
+            dsub(dmul(-0.5, dadd(dmul(dmul(h.c0, dx), dx), dmul(dmul(h.c2, dy), dy))),
+                 dmul(dmul(h.c1, dx), dy));
+        if (power >= (double)h.lthr) {
+          const ColdRec cr = cold[h.id];
+          const double G = exp(power);
+          double alpha = dmul(cr.opacity, G);
+          const bool clamped = alpha > 0.99;
+          if (clamped) alpha = 0.99;
+          if (alpha >= bp.alpha_floor) {
+            contrib = true;
+            const double col[3] = {cr.r, cr.g, cr.b};
+            const double w = T * alpha;
+            double dl_da = 0.0;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              P[c] += w * col[c];
+              const double S = (acc[c] - P[c]) + Tend * bp.bg[c];
+              dl_da += g[c] * (T * col[c] - S / (1.0 - alpha));
+              gr[6 + c] = (float)(w * g[c]);
+            }
+            const double dl_dpow = clamped ? 0.0 : dl_da * alpha;
+            gr[5] = clamped ? 0.f : (float)(dl_da * G);
+            gr[0] = (float)(dl_dpow * (h.c0 * dx + h.c1 * dy));
+            gr[1] = (float)(dl_dpow * (h.c2 * dy + h.c1 * dx));
+            gr[2] = (float)(dl_dpow * (-0.5 * dx * dx));
+            gr[3] = (float)(dl_dpow * (-dx * dy));
+            gr[4] = (float)(dl_dpow * (-0.5 * dy * dy));
+            T = T * (1.0 - alpha);
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, contrib)) {
+#pragma unroll
+        for (int f = 0; f < kGradFields; ++f) {
+          float v = contrib ? gr[f] : 0.f;
+          v = warp_sum(v);
+          if (lane_id() == 0 && v != 0.f) atomicAdd(&grads[(int64_t)f * cap + h.id], v);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__constant__ double kB0 = 0.28209479177387814;
+__constant__ double kB1 = 0.4886025119029199;
+__constant__ double kB2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
+                              -1.0925484305920792, 0.5462742152960396};
+__constant__ double kB3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658,
+                              0.3731763325901154, -0.4570457994644658, 1.445305721320277,
+                              -0.5900435899266435};
+
+// SH basis values and their gradients w.r.t. the unit direction (x, y, z).
+__device__ void sh_basis_grad(double x, double y, double z, int degree, double Y[16],
+                              double dY[16][3]) {
+  for (int n = 0; n < 16; ++n) { Y[n] = 0.0; dY[n][0] = dY[n][1] = dY[n][2] = 0.0; }
+  Y[0] = kB0;
+  if (degree >= 1) {
+    Y[1] = -kB1 * y; dY[1][1] = -kB1;
+    Y[2] = kB1 * z;  dY[2][2] = kB1;
+    Y[3] = -kB1 * x; dY[3][0] = -kB1;
+  }
+  if (degree >= 2) {
+    const double xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    Y[4] = kB2[0] * xy;  dY[4][0] = kB2[0] * y; dY[4][1] = kB2[0] * x;
+    Y[5] = kB2[1] * yz;  dY[5][1] = kB2[1] * z; dY[5][2] = kB2[1] * y;
+    Y[6] = kB2[2] * (2.0 * zz - xx - yy);
+    dY[6][0] = -2.0 * kB2[2] * x; dY[6][1] = -2.0 * kB2[2] * y; dY[6][2] = 4.0 * kB2[2] * z;
+    Y[7] = kB2[3] * xz;  dY[7][0] = kB2[3] * z; dY[7][2] = kB2[3] * x;
+    Y[8] = kB2[4] * (xx - yy); dY[8][0] = 2.0 * kB2[4] * x; dY[8][1] = -2.0 * kB2[4] * y;
+    if (degree >= 3) {
+      Y[9] = kB3[0] * y * (3.0 * xx - yy);
+      dY[9][0] = 6.0 * kB3[0] * xy; dY[9][1] = kB3[0] * (3.0 * xx - 3.0 * yy);
+      Y[10] = kB3[1] * xy * z;
+      dY[10][0] = kB3[1] * yz; dY[10][1] = kB3[1] * xz; dY[10][2] = kB3[1] * xy;
+      Y[11] = kB3[2] * y * (4.0 * zz - xx - yy);
+      dY[11][0] = -2.0 * kB3[2] * xy; dY[11][1] = kB3[2] * (4.0 * zz - xx - 3.0 * yy);
+      dY[11][2] = 8.0 * kB3[2] * yz;
+      Y[12] = kB3[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+      dY[12][0] = -6.0 * kB3[3] * xz; dY[12][1] = -6.0 * kB3[3] * yz;
+      dY[12][2] = kB3[3] * (6.0 * zz - 3.0 * xx - 3.0 * yy);
+      Y[13] = kB3[4] * x * (4.0 * zz - xx - yy);
+      dY[13][0] = kB3[4] * (4.0 * zz - 3.0 * xx - yy); dY[13][1] = -2.0 * kB3[4] * xy;
+      dY[13][2] = 8.0 * kB3[4] * xz;
+      Y[14] = kB3[5] * z * (xx - yy);
+      dY[14][0] = 2.0 * kB3[5] * xz; dY[14][1] = -2.0 * kB3[5] * yz; dY[14][2] = kB3[5] * (xx - yy);
+      Y[15] = kB3[6] * x * (xx - 3.0 * yy);
+      dY[15][0] = kB3[6] * (3.0 * xx - 3.0 * yy); dY[15][1] = -6.0 * kB3[6] * xy;
+    }
+  }
+}
+
+__device__ __forceinline__ int deg_of(int c) { return c >= 16 ? 3 : c >= 9 ? 2 : c >= 4 ? 1 : 0; }
+
+// K11: per visible splat (compact id v) -> parameter gradients of its source row.
+__global__ void __launch_bounds__(128)
+k_project_bwd(const cs_cloud cl, const int64_t* __restrict__ src, const DevStats* __restrict__ stats,
+              cs_camera cam, cs_settings st, const float* __restrict__ grads, int64_t cap,
+              cs_grads out) {
+  const int64_t M = stats->visible;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < M;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = src[r];
+    const Geom gm = load_geom(cl, k);
+    float gin[kGradFields];
+#pragma unroll
+    for (int f = 0; f < kGradFields; ++f) gin[f] = grads[(int64_t)f * cap + r];
+    const double* W = cam.R;
+    // camera-space position
+    double tcam[3];
+    for (int i = 0; i < 3; ++i)
+      tcam[i] = W[3 * i] * gm.px + W[3 * i + 1] * gm.py + W[3 * i + 2] * gm.pz + cam.t[i];
+    const double z = tcam[2], iz = 1.0 / z, iz2 = iz * iz, iz3 = iz2 * iz;
+    // rotation and covariance
+    const double w = gm.qw, x = gm.qx, y = gm.qy, q = gm.qz;
+    double R[9] = {1.0 - 2.0 * (y * y + q * q), 2.0 * (x * y - w * q), 2.0 * (x * q + w * y),
+                   2.0 * (x * y + w * q), 1.0 - 2.0 * (x * x + q * q), 2.0 * (y * q - w * x),
+                   2.0 * (x * q - w * y), 2.0 * (y * q + w * x), 1.0 - 2.0 * (x * x + y * y)};
+    const double s[3] = {gm.sx, gm.sy, gm.sz};
+    double Mm[9];  // M = R diag(s)
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) Mm[3 * i + j] = R[3 * i + j] * s[j];
+    double Sig[9];
+    for (int i = 0; i < 3; ++i)
+      for (int l = 0; l < 3; ++l)
+        Sig[3 * i + l] = Mm[3 * i] * Mm[3 * l] + Mm[3 * i + 1] * Mm[3 * l + 1] + Mm[3 * i + 2] * Mm[3 * l + 2];
+    double V[9], WS[9];
+    for (int i = 0; i < 3; ++i)
+      for (int l = 0; l < 3; ++l)
+        WS[3 * i + l] = W[3 * i] * Sig[l] + W[3 * i + 1] * Sig[3 + l] + W[3 * i + 2] * Sig[6 + l];
+    for (int i = 0; i < 3; ++i)
+      for (int m = 0; m < 3; ++m)
+        V[3 * i + m] = WS[3 * i] * W[3 * m] + WS[3 * i + 1] * W[3 * m + 1] + WS[3 * i + 2] * W[3 * m + 2];
+    const double J[6] = {cam.fx * iz, 0.0, -cam.fx * tcam[0] * iz2,
+                         0.0, cam.fy * iz, -cam.fy * tcam[1] * iz2};
+    // cov2d + low pass
+    double JV[6];
+    for (int i = 0; i < 2; ++i)
+      for (int l = 0; l < 3; ++l)
+        JV[3 * i + l] = J[3 * i] * V[l] + J[3 * i + 1] * V[3 + l] + J[3 * i + 2] * V[6 + l];
+    const double a = JV[0] * J[0] + JV[1] * J[1] + JV[2] * J[2] + st.low_pass;
+    const double b = JV[0] * J[3] + JV[1] * J[4] + JV[2] * J[5];
+    const double c = JV[3] * J[3] + JV[4] * J[4] + JV[5] * J[5] + st.low_pass;
+    const double det = a * c - b * b, id2 = 1.0 / (det * det);
+    // conic -> (a, b, c)
+    const double g0 = gin[2], g1 = gin[3], g2 = gin[4];
+    const double dA = g0 * (-c * c * id2) + g1 * (b * c * id2) + g2 * (1.0 / det - a * c * id2);
+    const double dB = g0 * (2.0 * b * c * id2) + g1 * (-1.0 / det - 2.0 * b * b * id2) +
+                      g2 * (2.0 * a * b * id2);
+    const double dC = g0 * (1.0 / det - a * c * id2) + g1 * (a * b * id2) + g2 * (-a * a * id2);
+    const double G[4] = {dA, 0.5 * dB, 0.5 * dB, dC};  // symmetric dL/dcov2d
+    // dL/dV = J^T G J ; dL/dJ = 2 G J V
+    double GJ[6];
+    for (int i = 0; i < 2; ++i)
+      for (int l = 0; l < 3; ++l) GJ[3 * i + l] = G[2 * i] * J[l] + G[2 * i + 1] * J[3 + l];
+    double dV[9];
+    for (int j = 0; j < 3; ++j)
+      for (int l = 0; l < 3; ++l) dV[3 * j + l] = J[j] * GJ[l] + J[3 + j] * GJ[3 + l];
+    double dJ[6];
+    for (int i = 0; i < 2; ++i)
+      for (int l = 0; l < 3; ++l)
+        dJ[3 * i + l] = 2.0 * (GJ[3 * i] * V[l] + GJ[3 * i + 1] * V[3 + l] + GJ[3 * i + 2] * V[6 + l]);
+    // dL/dt from J and mean2d
+    const double gmx = gin[0], gmy = gin[1];
+    double dt[3];
+    dt[0] = dJ[2] * (-cam.fx * iz2) + gmx * cam.fx * iz;
+    dt[1] = dJ[5] * (-cam.fy * iz2) + gmy * cam.fy * iz;
+    dt[2] = dJ[0] * (-cam.fx * iz2) + dJ[2] * (2.0 * cam.fx * tcam[0] * iz3) +
+            dJ[4] * (-cam.fy * iz2) + dJ[5] * (2.0 * cam.fy * tcam[1] * iz3) -
+            gmx * cam.fx * tcam[0] * iz2 - gmy * cam.fy * tcam[1] * iz2;
+    double dp[3];
+    for (int i = 0; i < 3; ++i) dp[i] = W[i] * dt[0] + W[3 + i] * dt[1] + W[6 + i] * dt[2];
+    // dL/dSigma = W^T dV W (symmetrised)
+    double tmp[9], dS[9];
+    for (int j = 0; j < 3; ++j)
+      for (int m = 0; m < 3; ++m) tmp[3 * j + m] = W[j] * dV[m] + W[3 + j] * dV[3 + m] + W[6 + j] * dV[6 + m];
+    for (int j = 0; j < 3; ++j)
+      for (int l = 0; l < 3; ++l)
+        dS[3 * j + l] = tmp[3 * j] * W[l] + tmp[3 * j + 1] * W[3 + l] + tmp[3 * j + 2] * W[6 + l];
+    double dSs[9];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) dSs[3 * i + j] = dS[3 * i + j] + dS[3 * j + i];
+    // Sigma = M M^T: dL/dM = (dS + dS^T) M
+    double dM[9];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j)
+        dM[3 * i + j] = dSs[3 * i] * Mm[j] + dSs[3 * i + 1] * Mm[3 + j] + dSs[3 * i + 2] * Mm[6 + j];
+    double ds[3] = {0.0, 0.0, 0.0}, dR[9];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        ds[j] += dM[3 * i + j] * R[3 * i + j];
+        dR[3 * i + j] = dM[3 * i + j] * s[j];
+      }
+    double dq[4];
+    dq[0] = 2.0 * (-q * dR[1] + y * dR[2] + q * dR[3] - x * dR[5] - y * dR[6] + x * dR[7]);
+    dq[1] = 2.0 * (y * dR[1] + q * dR[2] + y * dR[3] - 2.0 * x * dR[4] - w * dR[5] + q * dR[6] +
+                   w * dR[7] - 2.0 * x * dR[8]);
+    dq[2] = 2.0 * (-2.0 * y * dR[0] + x * dR[1] + w * dR[2] + x * dR[3] + q * dR[5] - w * dR[6] +
+                   q * dR[7] - 2.0 * y * dR[8]);
+    dq[3] = 2.0 * (-2.0 * q * dR[0] - w * dR[1] + x * dR[2] + w * dR[3] - 2.0 * q * dR[4] +
+                   y * dR[5] + x * dR[6] + y * dR[7]);
+    // colour: SH coefficients and the view direction
+    const int C = cl.sh_coeffs;
+    const int degree = min((int)st.sh_degree, deg_of(C));
+    const int nb = (degree + 1) * (degree + 1);
+    double v[3] = {gm.px - cam.center[0], gm.py - cam.center[1], gm.pz - cam.center[2]};
+    const double nv = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+    const double d[3] = {v[0] / nv, v[1] / nv, v[2] / nv};
+    double Y[16], dY[16][3];
+    sh_basis_grad(d[0], d[1], d[2], degree, Y, dY);
+    const float* row = cl.sh + k * cl.sh_stride;
+    double dd[3] = {0.0, 0.0, 0.0};
+    for (int ch = 0; ch < 3; ++ch) {
+      double val = 0.5;
+      for (int n = 0; n < nb; ++n) val += (double)row[ch * C + n] * Y[n];
+      const double gc = (val >= 0.0 && val <= 1.0) ? (double)gin[6 + ch] : 0.0;
+      float* gsh = out.sh + k * (int64_t)(3 * C) + ch * C;
+      for (int n = 0; n < nb; ++n) {
+        gsh[n] = (float)(gc * Y[n]);
+        const double ws = gc * (double)row[ch * C + n];
+        dd[0] += ws * dY[n][0];
+        dd[1] += ws * dY[n][1];
+        dd[2] += ws * dY[n][2];
+      }
+    }
+    const double ddot = dd[0] * d[0] + dd[1] * d[1] + dd[2] * d[2];
+    for (int i = 0; i < 3; ++i) dp[i] += (dd[i] - d[i] * ddot) / nv;
+    for (int i = 0; i < 3; ++i) {
+      out.positions[3 * k + i] = (float)dp[i];
+      out.scales[3 * k + i] = (float)ds[i];
+    }
+    for (int i = 0; i < 4; ++i) out.rotations[4 * k + i] = (float)dq[i];
+    out.opacities[k] = gin[5];
+  }
+}
+
+void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint2* ranges, const HotRec* hot,
+                      const ColdRec* cold, const cs_settings& st, int width, int height, int ntx,
+                      const float* dl_dimg, const BlendState& state,
+                      float* grads, int64_t cap, cudaStream_t s) {
+  BwdParams bp;
+  for (int i = 0; i < 3; ++i) bp.bg[i] = st.background[i];
+  bp.alpha_floor = st.alpha_floor;
+  bp.tile_size = st.tile_size;
+  bp.width = width;
+  bp.height = height;
+  bp.ntx = ntx;
+  k_blend_bwd<<<n_tiles, kBwdThreads, 0, s>>>(list, ranges, hot, cold, bp, dl_dimg, state, grads,
+                                              cap);
+}
+
+void launch_project_bwd(const cs_cloud& cl, const int64_t* src,
+                        const DevStats* stats, const cs_camera& cam, const cs_settings& st,
+                        const float* grads, int64_t cap, const cs_grads& out, cudaStream_t s) {
+  const int64_t blocks = std::min<int64_t>((cap + 127) / 128, 148 * 16);
+  if (blocks <= 0) return;
+  k_project_bwd<<<(unsigned)blocks, 128, 0, s>>>(cl, src, stats, cam, st, grads, cap, out);
+}
+
+}  // namespace cs

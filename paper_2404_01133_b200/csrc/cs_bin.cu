@@ -1,61 +1,37 @@
-// cs_bin.cu -- K5/K6/K8: depth-rank gather, tile-count scan, pair
-// duplication and tile ranges.  Replaces render._bin_tiles (render.py:217-249)
-// together with the depth-order gather at the end of _project_cloud
-// (render.py:178-188).
+// cs_bin.cu -- K5/K6/K8: pair-count scan in depth order, pair duplication and
+// tile ranges.  Replaces render._bin_tiles (render.py:217-249).
+//
+// The tile rectangles were computed by the projection (render.py:226-231);
+// here only the depth permutation is applied: pairs are emitted in depth-rank
+// order (row-major over each rect, render.py:233-243) carrying the splat's
+// compact index, so after the stable tile sort every tile's list is in
+// (depth, assembled index) order (render.py:245) and the blend reads the
+// splat records directly by compact index -- no gather pass.
 #include "cs_internal.cuh"
 
 namespace cs {
 
-constexpr int kGatherThreads = 256;
+constexpr int kCountThreads = 256;
 
-// For every depth rank r (0..M-1): gather the projected record of the r-th
-// splat in depth order, compute its tile rectangle exactly as numpy does
-// (render.py:226-231, astype(int64) then clip), emit the blend records and
-// scan the pair counts (render.py:233-236) with a decoupled look-back.
-__global__ void __launch_bounds__(kGatherThreads)
-k_gather_count(const uint32_t* __restrict__ order, const ProjRec* __restrict__ recs,
-               DevStats* __restrict__ stats, int tile_size, int width, int height,
-               double alpha_floor, int64_t pair_cap, uint64_t* __restrict__ status,
-               HotRec* __restrict__ hot, ColdRec* __restrict__ cold, int4* __restrict__ rects,
-               int64_t* __restrict__ src_sorted, int64_t* __restrict__ pair_off) {
+// pair_off[r] = sum of pair counts of depth ranks < r (decoupled look-back).
+__global__ void __launch_bounds__(kCountThreads)
+k_pair_count(const uint32_t* __restrict__ order, const int4* __restrict__ rects,
+             DevStats* __restrict__ stats, int64_t pair_cap, uint64_t* __restrict__ status,
+             int64_t* __restrict__ pair_off) {
   __shared__ int64_t s_chunk;
-  __shared__ uint64_t s_scan[kGatherThreads / 32 + 1];
+  __shared__ uint64_t s_scan[kCountThreads / 32 + 1];
   __shared__ uint64_t s_prefix;
   const int64_t M = stats->visible;
   if (threadIdx.x == 0) s_chunk = atomicAdd(&stats->tickets[2], 1u);
   __syncthreads();
   const int64_t chunk = s_chunk;
-  const int64_t base = chunk * kGatherThreads;
+  const int64_t base = chunk * kCountThreads;
   if (base >= M) return;
   const int64_t r = base + threadIdx.x;
   uint64_t cnt = 0;
-  int4 rect = make_int4(0, 0, 0, 0);
   if (r < M) {
-    const ProjRec rec = recs[order[r]];
-    const int64_t ntx = (width + tile_size - 1) / tile_size;
-    const int64_t nty = (height + tile_size - 1) / tile_size;
-    const double ts = (double)tile_size;
-    const int64_t tx0 = clip_i64(np_to_i64(floor(ddiv(dsub(dsub(rec.mx, rec.rx), 0.5), ts))), 0, ntx - 1);
-    const int64_t tx1 = clip_i64(np_to_i64(floor(ddiv(dsub(dadd(rec.mx, rec.rx), 0.5), ts))), 0, ntx - 1);
-    const int64_t ty0 = clip_i64(np_to_i64(floor(ddiv(dsub(dsub(rec.my, rec.ry), 0.5), ts))), 0, nty - 1);
-    const int64_t ty1 = clip_i64(np_to_i64(floor(ddiv(dsub(dadd(rec.my, rec.ry), 0.5), ts))), 0, nty - 1);
-    rect = make_int4((int)tx0, (int)tx1, (int)ty0, (int)ty1);
-    cnt = (uint64_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
-    HotRec h;
-    h.mx = rec.mx; h.my = rec.my; h.c0 = rec.c0; h.c1 = rec.c1; h.c2 = rec.c2;
-    // fast-reject threshold: alpha = o*exp(power) < alpha_floor whenever
-    // power < log(alpha_floor/o) - 1e-6 (margin >> exp/log rounding).
-    const double lt = rec.opacity > 0.0 ? log(alpha_floor / rec.opacity) - 1e-6
-                                        : __longlong_as_double(0x7ff0000000000000ll);
-    h.lthr = __double2float_rd(lt);
-    h.rank = (uint32_t)r;
-    hot[r] = h;
-    ColdRec c;
-    c.opacity = rec.opacity;
-    c.r = rec.r; c.g = rec.g; c.b = rec.bl; c.pad = 0.f; c.pad2 = 0.0;
-    cold[r] = c;
-    rects[r] = rect;
-    src_sorted[r] = rec.src;
+    const int4 rc = __ldg(rects + __ldg(order + r));
+    cnt = (uint64_t)((int64_t)(rc.y - rc.x + 1) * (int64_t)(rc.w - rc.z + 1));
   }
   uint64_t total;
   const uint64_t excl = block_excl_scan<uint64_t>(cnt, s_scan, total);
@@ -63,7 +39,7 @@ k_gather_count(const uint32_t* __restrict__ order, const ProjRec* __restrict__ r
     const uint64_t pre = lookback_exclusive(status, chunk, total);
     if (threadIdx.x == 0) {
       s_prefix = pre;
-      if (base + kGatherThreads >= M) {
+      if (base + kCountThreads >= M) {
         const int64_t P = (int64_t)(pre + total);
         stats->pairs = P;
         stats->pairs_eff = P <= pair_cap ? P : 0;
@@ -78,16 +54,16 @@ k_gather_count(const uint32_t* __restrict__ order, const ProjRec* __restrict__ r
 constexpr int kDupThreads = 256;
 constexpr int kDupTile = 1024;
 
-// Load-balanced duplication (render.py:233-243): each CTA owns kDupTile
-// consecutive output pairs; the splats whose pair ranges intersect it are
-// found by binary search and staged in shared memory.  Pairs are emitted
-// row-major over each rect in depth-rank order: key = tile id, value = rank.
+// Load-balanced duplication: each CTA owns kDupTile consecutive output pairs;
+// the depth ranks whose pair ranges intersect it are found by binary search
+// and staged in shared memory.  key = tile id, value = compact index.
 __global__ void __launch_bounds__(kDupThreads)
-k_duplicate(const int64_t* __restrict__ pair_off, const int4* __restrict__ rects,
-            const DevStats* __restrict__ stats, int ntx, uint32_t* __restrict__ keys,
-            uint32_t* __restrict__ vals) {
+k_duplicate(const int64_t* __restrict__ pair_off, const uint32_t* __restrict__ order,
+            const int4* __restrict__ rects, const DevStats* __restrict__ stats, int ntx,
+            uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
   __shared__ int64_t s_off[kDupTile + 1];
   __shared__ int4 s_rect[kDupTile + 1];
+  __shared__ uint32_t s_id[kDupTile + 1];
   __shared__ int64_t s_rlo, s_rhi;
   const int64_t P = stats->pairs_eff;
   const int64_t M = stats->visible;
@@ -107,8 +83,10 @@ k_duplicate(const int64_t* __restrict__ pair_off, const int4* __restrict__ rects
   const int64_t rlo = s_rlo;
   const int nr = (int)(s_rhi - rlo + 1);
   for (int i = threadIdx.x; i < nr; i += kDupThreads) {
+    const uint32_t v = __ldg(order + rlo + i);
     s_off[i] = pair_off[rlo + i];
-    s_rect[i] = rects[rlo + i];
+    s_rect[i] = __ldg(rects + v);
+    s_id[i] = v;
   }
   __syncthreads();
   for (int64_t p = p0 + threadIdx.x; p < p1; p += kDupThreads) {
@@ -122,7 +100,7 @@ k_duplicate(const int64_t* __restrict__ pair_off, const int4* __restrict__ rects
     const int w = rc.y - rc.x + 1;
     const int ly = (int)(local / w), lx = (int)(local - (int64_t)ly * w);
     keys[p] = (uint32_t)((rc.z + ly) * ntx + (rc.x + lx));
-    vals[p] = (uint32_t)(rlo + lo);
+    vals[p] = s_id[lo];
   }
 }
 
@@ -138,23 +116,21 @@ __global__ void k_tile_ranges(const uint32_t* __restrict__ keys, const DevStats*
   }
 }
 
-void launch_gather_count(const uint32_t* order, const ProjRec* recs, DevStats* stats,
-                         int tile_size, int width, int height, double alpha_floor,
-                         int64_t pair_cap, int64_t capacity, uint64_t* status, HotRec* hot,
-                         ColdRec* cold, int4* rects, int64_t* src_sorted, int64_t* pair_off,
-                         cudaStream_t s) {
-  const int64_t chunks = (capacity + kGatherThreads - 1) / kGatherThreads;
+void launch_pair_count(const uint32_t* order, const int4* rects, DevStats* stats, int64_t pair_cap,
+                       int64_t capacity, uint64_t* status, int64_t* pair_off, cudaStream_t s) {
+  const int64_t chunks = (capacity + kCountThreads - 1) / kCountThreads;
   if (chunks == 0) return;
-  k_gather_count<<<(unsigned)chunks, kGatherThreads, 0, s>>>(order, recs, stats, tile_size, width,
-                                                             height, alpha_floor, pair_cap, status,
-                                                             hot, cold, rects, src_sorted, pair_off);
+  k_pair_count<<<(unsigned)chunks, kCountThreads, 0, s>>>(order, rects, stats, pair_cap, status,
+                                                          pair_off);
 }
 
-void launch_duplicate(const int64_t* pair_off, const int4* rects, const DevStats* stats, int ntx,
-                      int64_t pair_cap, uint32_t* keys, uint32_t* vals, cudaStream_t s) {
+void launch_duplicate(const int64_t* pair_off, const uint32_t* order, const int4* rects,
+                      const DevStats* stats, int ntx, int64_t pair_cap, uint32_t* keys,
+                      uint32_t* vals, cudaStream_t s) {
   const int64_t blocks = (pair_cap + kDupTile - 1) / kDupTile;
   if (blocks == 0) return;
-  k_duplicate<<<(unsigned)blocks, kDupThreads, 0, s>>>(pair_off, rects, stats, ntx, keys, vals);
+  k_duplicate<<<(unsigned)blocks, kDupThreads, 0, s>>>(pair_off, order, rects, stats, ntx, keys,
+                                                       vals);
 }
 
 void launch_tile_ranges(const uint32_t* keys, const DevStats* stats, uint2* ranges,
@@ -184,14 +160,22 @@ __global__ void k_dump_projected(const uint32_t* order, const ProjRec* recs,
   }
 }
 
+__global__ void k_rank_of(const uint32_t* order, const DevStats* stats, int64_t* rank_of) {
+  const int64_t M = stats->visible;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < M;
+       r += (int64_t)gridDim.x * blockDim.x)
+    rank_of[order[r]] = r;
+}
+
+// tile_ids as render._bin_tiles returns them: indices into the depth-sorted splats
 __global__ void k_dump_tiles(const uint32_t* vals, const uint2* ranges, const DevStats* stats,
-                             int n_tiles, int64_t* tile_ids, int64_t* offsets) {
+                             const int64_t* rank_of, int n_tiles, int64_t* tile_ids,
+                             int64_t* offsets) {
   const int64_t P = stats->pairs_eff;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P; p += stride)
-    tile_ids[p] = vals[p];
+    tile_ids[p] = rank_of[vals[p]];
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= n_tiles; t += stride) {
-    // offsets[t] = start of tile t; empty tiles take the next non-empty start
     if (t == n_tiles) { offsets[t] = P; continue; }
     int64_t tt = t;
     while (tt < n_tiles && ranges[tt].y == ranges[tt].x) ++tt;
@@ -206,9 +190,11 @@ void launch_dump_projected(const uint32_t* order, const ProjRec* recs, const Dev
   k_dump_projected<<<148 * 4, 256, 0, s>>>(order, recs, stats, means, conics, covs, depths,
                                            colors, opac, radii, src);
 }
-void launch_dump_tiles(const uint32_t* vals, const uint2* ranges, const DevStats* stats,
-                       int n_tiles, int64_t* tile_ids, int64_t* offsets, cudaStream_t s) {
-  k_dump_tiles<<<148 * 4, 256, 0, s>>>(vals, ranges, stats, n_tiles, tile_ids, offsets);
+void launch_dump_tiles(const uint32_t* order, const uint32_t* vals, const uint2* ranges,
+                       const DevStats* stats, int n_tiles, int64_t* rank_of, int64_t* tile_ids,
+                       int64_t* offsets, cudaStream_t s) {
+  k_rank_of<<<148 * 4, 256, 0, s>>>(order, stats, rank_of);
+  k_dump_tiles<<<148 * 4, 256, 0, s>>>(vals, ranges, stats, rank_of, n_tiles, tile_ids, offsets);
 }
 
 }  // namespace cs

@@ -2,11 +2,17 @@
 //
 // Replaces _kernels.blend_tiles (_kernels.py:17-76), the reference's only
 // native kernel.  One CTA per tile, one thread per pixel (tile_size <= 16;
-// 4 or 16 pixels per thread for 32/64).  The tile's splat list (depth-rank
-// order) is streamed through shared memory in batches of 256 HotRec records
-// (48 B each) with cp.async double buffering; each thread walks the batch for
-// its pixel and the CTA leaves as soon as every pixel has terminated
-// (__syncthreads_count).
+// 4 or 16 pixels per thread for 32/64).  For 16x16 tiles each warp owns an
+// 8x4 pixel box.
+//
+// The tile's splat list (depth order) is streamed through shared memory in
+// batches of 256 HotRec records (64 B: mean, conic, fast-reject threshold,
+// support AABB) with cp.async double buffering.  Per batch every warp first
+// tests 32 splats at a time against its pixel box (one AABB test per lane,
+// __ballot_sync) and then walks only the hits, so a splat whose alpha-floor
+// support misses the warp's 32 pixels costs 1/32 of an AABB test instead of
+// 32 float64 quadratic forms.  The CTA leaves as soon as every pixel has
+// terminated (__syncthreads_count).
 //
 // Precision: the quadratic form is float64 in the
 // reference's exact op order (no FMA).  A float64 power below
@@ -14,7 +20,8 @@
 // other fragment takes the reference path exactly: alpha = min(0.99,
 // o * exp(power)) in float64, float64 alpha/transmittance decisions, so the
 // accepted-fragment set equals the reference's.  Colour accumulates in
-// float64 from float32 splat colours.
+// float64 from float32 splat colours.  The AABB cull never drops a fragment
+// the exact path could accept: it bounds {power >= threshold} (cs_project.cu).
 #include "cs_internal.cuh"
 
 namespace cs {
@@ -30,6 +37,27 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+__device__ __forceinline__ void stage_batch(HotRec* dst, const uint32_t* list, const HotRec* hot,
+                                            int64_t k, int64_t s1) {
+  if (k < s1) {
+    const char* g = reinterpret_cast<const char*>(hot + __ldg(list + k));
+    char* d = reinterpret_cast<char*>(dst + threadIdx.x);
+    cp_async16(d, g);
+    cp_async16(d + 16, g + 16);
+    cp_async16(d + 32, g + 32);
+    cp_async16(d + 48, g + 48);
+  }
+}
+
+// local pixel index (0..ts*ts-1) of thread `tid`, pixel slot q
+__device__ __forceinline__ int local_pixel(int tid, int q, int ts) {
+  if (ts == 16) {  // 8x4 box per warp: warp w -> origin ((w & 1) * 8, (w >> 1) * 4)
+    const int w = tid >> 5, l = tid & 31;
+    return ((w >> 1) * 4 + (l >> 3)) * 16 + (w & 1) * 8 + (l & 7);
+  }
+  return tid + q * kBlendThreads;
+}
+
 template <int PPT, typename OutT, bool KEEP>
 __global__ void __launch_bounds__(kBlendThreads)
 k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
@@ -38,51 +66,49 @@ k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
         BlendState state) {
   __shared__ __align__(16) HotRec buf[2][kBatch];
   __shared__ int s_red[kBlendThreads / 32];
-  __shared__ int s_ev[kBlendThreads / 32];
+  __shared__ long long s_ev[kBlendThreads / 32];
   const int t = blockIdx.x;
   const int tx = t % bp.ntx, ty = t / bp.ntx;
   const int ts = bp.tile_size;
   const uint2 rg = ranges[t];
   const int64_t s0 = rg.x, s1 = rg.y;
+  const uint32_t lane = lane_id();
 
   double sx[PPT], sy[PPT], T[PPT], cr[PPT], cg[PPT], cb[PPT];
+  float wx0[PPT], wx1[PPT], wy0[PPT], wy1[PPT];  // warp's pixel-centre box per slot
   int cnt[PPT], last[PPT];
-  int evals = 0;
   bool done[PPT], valid[PPT];
+  long long evals = 0;
 #pragma unroll
   for (int q = 0; q < PPT; ++q) {
-    const int li = threadIdx.x + q * kBlendThreads;
-    const int lx = li % ts, ly = li / ts;
-    const int px = tx * ts + lx, py = ty * ts + ly;
+    const int li = local_pixel(threadIdx.x, q, ts);
+    const int px = tx * ts + li % ts, py = ty * ts + li / ts;
     valid[q] = li < ts * ts && px < bp.width && py < bp.height;
     sx[q] = (double)px + 0.5;  // pixel centres (_kernels.py:43-45)
     sy[q] = (double)py + 0.5;
     T[q] = 1.0; cr[q] = 0.0; cg[q] = 0.0; cb[q] = 0.0;
     cnt[q] = 0; last[q] = (int)s0;
     done[q] = !valid[q];
+    const float inf = __int_as_float(0x7f800000);
+    float x0 = valid[q] ? (float)sx[q] : inf, x1 = valid[q] ? (float)sx[q] : -inf;
+    float y0 = valid[q] ? (float)sy[q] : inf, y1 = valid[q] ? (float)sy[q] : -inf;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      x0 = fminf(x0, __shfl_xor_sync(0xffffffffu, x0, o));
+      x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+      y0 = fminf(y0, __shfl_xor_sync(0xffffffffu, y0, o));
+      y1 = fmaxf(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+    }
+    wx0[q] = x0; wx1[q] = x1; wy0[q] = y0; wy1[q] = y1;
   }
 
   const int64_t n = s1 - s0;
   const int nbatches = (int)((n + kBatch - 1) / kBatch);
-  // prefetch batch 0
-  if (nbatches > 0 && threadIdx.x < n) {
-    const uint32_t rk = __ldg(list + s0 + threadIdx.x);
-    const char* g = reinterpret_cast<const char*>(hot + rk);
-    char* d = reinterpret_cast<char*>(&buf[0][threadIdx.x]);
-    cp_async16(d, g); cp_async16(d + 16, g + 16); cp_async16(d + 32, g + 32);
-  }
+  if (nbatches > 0) stage_batch(buf[0], list, hot, s0 + threadIdx.x, s1);
   cp_async_commit();
   for (int b = 0; b < nbatches; ++b) {
     const int64_t bstart = s0 + (int64_t)b * kBatch;
-    if (b + 1 < nbatches) {
-      const int64_t k = bstart + kBatch + threadIdx.x;
-      if (k < s1) {
-        const uint32_t rk = __ldg(list + k);
-        const char* g = reinterpret_cast<const char*>(hot + rk);
-        char* d = reinterpret_cast<char*>(&buf[(b + 1) & 1][threadIdx.x]);
-        cp_async16(d, g); cp_async16(d + 16, g + 16); cp_async16(d + 32, g + 32);
-      }
-    }
+    if (b + 1 < nbatches) stage_batch(buf[(b + 1) & 1], list, hot, bstart + kBatch + threadIdx.x, s1);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
@@ -90,33 +116,45 @@ k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
     const int nb = (int)min((int64_t)kBatch, s1 - bstart);
 #pragma unroll
     for (int q = 0; q < PPT; ++q) {
-      if (done[q]) continue;
+      if (__all_sync(0xffffffffu, done[q])) continue;
       double Tq = T[q];
-      int j = 0;
-      for (; j < nb; ++j) {
-        const HotRec h = hb[j];
-        const double dx = dsub(sx[q], h.mx);
-        const double dy = dsub(sy[q], h.my);
-        // -0.5 * (c0*dx*dx + c2*dy*dy) - c1*dx*dy   (_kernels.py:54-57)
-        const double power =
-            dsub(dmul(-0.5, dadd(dmul(dmul(h.c0, dx), dx), dmul(dmul(h.c2, dy), dy))),
-                 dmul(dmul(h.c1, dx), dy));
-        if (power < (double)h.lthr) continue;  // alpha < alpha_floor guaranteed
-        const ColdRec c = cold[h.rank];
-        double alpha = dmul(c.opacity, exp(power));  // _kernels.py:58
-        if (alpha > 0.99) alpha = 0.99;              // _kernels.py:59-60
-        if (alpha < bp.alpha_floor) continue;        // _kernels.py:61-62
-        const double nt = dmul(Tq, dsub(1.0, alpha));
-        if (nt < bp.t_floor) { done[q] = true; ++j; break; }  // _kernels.py:63-66
-        const double w = dmul(Tq, alpha);
-        cr[q] += w * (double)c.r;
-        cg[q] += w * (double)c.g;
-        cb[q] += w * (double)c.b;
-        Tq = nt;
-        cnt[q] += 1;
-        last[q] = (int)(bstart + j + 1);
+      for (int base = 0; base < nb; base += 32) {
+        const int jl = base + (int)lane;
+        bool hit = false;
+        if (jl < nb) {
+          const float4 bx = *reinterpret_cast<const float4*>(&hb[jl].bx0);
+          hit = !(bx.x > wx1[q] || bx.y < wx0[q] || bx.z > wy1[q] || bx.w < wy0[q]);
+        }
+        uint32_t mask = __ballot_sync(0xffffffffu, hit);
+        while (mask) {
+          const int j = base + __ffs(mask) - 1;
+          mask &= mask - 1;
+          if (done[q]) continue;
+          ++evals;
+          const HotRec& h = hb[j];
+          const double dx = dsub(sx[q], h.mx);
+          const double dy = dsub(sy[q], h.my);
+          // -0.5 * (c0*dx*dx + c2*dy*dy) - c1*dx*dy   (_kernels.py:54-57)
+          const double power =
+              dsub(dmul(-0.5, dadd(dmul(dmul(h.c0, dx), dx), dmul(dmul(h.c2, dy), dy))),
+                   dmul(dmul(h.c1, dx), dy));
+          if (power < (double)h.lthr) continue;  // alpha < alpha_floor guaranteed
+          const ColdRec c = cold[h.id];
+          double alpha = dmul(c.opacity, exp(power));  // _kernels.py:58
+          if (alpha > 0.99) alpha = 0.99;              // _kernels.py:59-60
+          if (alpha < bp.alpha_floor) continue;        // _kernels.py:61-62
+          const double nt = dmul(Tq, dsub(1.0, alpha));
+          if (nt < bp.t_floor) { done[q] = true; continue; }  // _kernels.py:63-66
+          const double w = dmul(Tq, alpha);
+          cr[q] += w * (double)c.r;
+          cg[q] += w * (double)c.g;
+          cb[q] += w * (double)c.b;
+          Tq = nt;
+          cnt[q] += 1;
+          last[q] = (int)(bstart + j + 1);
+        }
+        if (__all_sync(0xffffffffu, done[q])) break;
       }
-      evals += j;
       T[q] = Tq;
     }
     int alive = 0;
@@ -130,7 +168,7 @@ k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
   for (int q = 0; q < PPT; ++q) {
     if (!valid[q]) continue;
     my += cnt[q];
-    const int li = threadIdx.x + q * kBlendThreads;
+    const int li = local_pixel(threadIdx.x, q, ts);
     const int px = tx * ts + li % ts, py = ty * ts + li / ts;
     const int64_t pix = (int64_t)py * bp.width + px;
     double o[3] = {cr[q] + T[q] * bp.bg[0], cg[q] + T[q] * bp.bg[1], cb[q] + T[q] * bp.bg[2]};
@@ -142,16 +180,16 @@ k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
     out[3 * pix + 1] = (OutT)o[1];
     out[3 * pix + 2] = (OutT)o[2];
     if (KEEP) {
-      state.final_t[pix] = (float)T[q];
+      state.final_t[pix] = T[q];
       state.last[pix] = last[q];
-      state.color_acc[3 * pix] = (float)cr[q];
-      state.color_acc[3 * pix + 1] = (float)cg[q];
-      state.color_acc[3 * pix + 2] = (float)cb[q];
+      state.color_acc[3 * pix] = cr[q];
+      state.color_acc[3 * pix + 1] = cg[q];
+      state.color_acc[3 * pix + 2] = cb[q];
     }
   }
   my = warp_sum(my);
   evals = warp_sum(evals);
-  if (lane_id() == 0) {
+  if (lane == 0) {
     s_red[threadIdx.x >> 5] = my;
     s_ev[threadIdx.x >> 5] = evals;
   }
@@ -207,8 +245,9 @@ void launch_blend(int n_tiles, const uint32_t* list, const uint2* ranges, const 
 
 // ---------------------------------------------------------------------------
 // cs_blend_tiles: the numba kernel's exact interface (_kernels.py:18-30).
-// Packs the caller's float64 arrays into HotRec/ColdRec and the int64 CSR
-// into (list, ranges); then runs the same blend kernel.
+// Packs the caller's float64 arrays into HotRec/ColdRec and the int64 CSR into
+// (list, ranges); then runs the same blend kernel.  The caller's conics need
+// not come from our projection, so no cull box is assumed (infinite AABB).
 
 __global__ void k_pack_records(int64_t m, const double* means, const double* conics,
                                const double* colors, const double* opac, double alpha_floor,
@@ -222,7 +261,9 @@ __global__ void k_pack_records(int64_t m, const double* means, const double* con
     const double lt = o > 0.0 ? log(alpha_floor / o) - 1e-6
                               : __longlong_as_double(0x7ff0000000000000ll);
     h.lthr = __double2float_rd(lt);
-    h.rank = (uint32_t)s;
+    h.id = (uint32_t)s;
+    const float inf = __int_as_float(0x7f800000);
+    h.bx0 = -inf; h.bx1 = inf; h.by0 = -inf; h.by1 = inf;
     hot[s] = h;
     ColdRec c;
     c.opacity = o;

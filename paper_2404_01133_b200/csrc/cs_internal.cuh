@@ -1,10 +1,14 @@
 // cs_internal.cuh -- shared device-side types and primitives for libcsgpu.
 //
-// Layouts in HBM:
-//   ProjRec   : 128 B per visible splat, compact (assembled-index) order
-//   HotRec    :  48 B per visible splat, depth-rank order -- staged in smem by the blend
-//   ColdRec   :  32 B per visible splat, depth-rank order -- read only for accepted fragments
-//   pairs     :  u32 tile key + u32 depth rank, sorted stably by tile
+// Layouts in HBM; every per-splat array is in
+// compact (ascending assembled-index) order, written once by the projection:
+//   HotRec    :  64 B -- staged in smem by the blend (quadratic form + cull box)
+//   ColdRec   :  32 B -- read only for fragments that may be accepted
+//   rect      :  16 B -- tile rectangle (render.py:226-231)
+//   src       :   8 B -- assembled index (depth tie-break, gradient scatter)
+//   keys/vals :  8+4 B -- depth key, compact index (sorted -> depth order)
+//   ProjRec   : 128 B -- full _Projected record, written only in debug/dump mode
+//   pairs     :  u32 tile key + u32 compact index, sorted stably by tile
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -45,9 +49,10 @@ static_assert(sizeof(ProjRec) == 128, "ProjRec layout");
 struct __align__(16) HotRec {   // what every (pixel, splat) evaluation reads
   double mx, my, c0, c1, c2;
   float lthr;                    // fast-reject threshold on power (<= log(alpha_floor/o) - margin)
-  uint32_t rank;                 // depth rank, index into ColdRec
+  uint32_t id;                   // compact index: ColdRec slot and gradient slot
+  float bx0, bx1, by0, by1;      // pixel-space AABB of {power >= lthr} (outward rounded)
 };
-static_assert(sizeof(HotRec) == 48, "HotRec layout");
+static_assert(sizeof(HotRec) == 64, "HotRec layout");
 
 struct __align__(16) ColdRec {  // read only when a fragment may be accepted
   double opacity;
@@ -70,6 +75,17 @@ struct DevStats {     // device mirror of cs_frame_stats + scratch counters
 };
 
 
+// Per-visible-splat outputs of the projection kernel (compact order).
+struct ProjOutputs {
+  uint64_t* keys;    // depth bits
+  uint32_t* vals;    // compact index
+  HotRec* hot;
+  ColdRec* cold;
+  int4* rects;
+  int64_t* src;
+  ProjRec* recs;     // optional (debug / dumps)
+};
+
 // LoD scene tables on device (cs_lod.cu)
 struct LodTables {
   const cs_cloud* clouds;      // [L*J] level-major
@@ -91,9 +107,9 @@ struct BlendParams {
 };
 
 struct BlendState {  // per-pixel state kept for the backward pass
-  float* final_t;       // (H*W) final transmittance
+  double* final_t;      // (H*W) final transmittance
   int32_t* last;        // (H*W) list position one past the last accepted fragment
-  float* color_acc;     // (H*W*3) sum of w*c (before the background term)
+  double* color_acc;    // (H*W*3) sum of w*c (before the background term)
 };
 
 // ---------------------------------------------------------------------------

@@ -182,13 +182,13 @@ __device__ __forceinline__ ProjOut project_one(const Geom& g, const cs_camera& c
 
 constexpr int kProjThreads = 256;
 
-// Single-pass projection + stable compaction.
+// Single-pass projection + stable compaction.  Every output array is written
+// once, in compact (ascending assembled-index) order; the depth sort then
+// only permutes (key, compact index) pairs and nothing is gathered again.
 __global__ void __launch_bounds__(kProjThreads)
 k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
           DevStats* __restrict__ stats, cs_camera cam, cs_settings st,
-          uint64_t* __restrict__ status, uint64_t* __restrict__ keys_out,
-          uint32_t* __restrict__ vals_out, ProjRec* __restrict__ recs,
-          const uint64_t* __restrict__ list) {
+          uint64_t* __restrict__ status, ProjOutputs po_out, const uint64_t* __restrict__ list) {
   __shared__ int64_t s_chunk;
   __shared__ uint32_t s_scan[kProjThreads / 32 + 1];
   __shared__ uint32_t s_skip[kProjThreads / 32];
@@ -245,28 +245,61 @@ k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
   int degree = min((int)st.sh_degree, degree_of(cd.sh_coeffs));
   double col[3];
   sh_colour(cd.sh + local * cd.sh_stride, cd.sh_coeffs, degree, dx / nrm, dy / nrm, dz / nrm, col);
-  ProjRec rec;
-  rec.mx = po.mx;
-  rec.my = po.my;
-  rec.c0 = ddiv(po.c, po.det);    // render.py:172
-  rec.c1 = ddiv(-po.b, po.det);
-  rec.c2 = ddiv(po.a, po.det);
-  rec.a = po.a;
-  rec.b = po.b;
-  rec.c = po.c;
-  rec.rx = po.rx;
-  rec.ry = po.ry;
-  rec.opacity = g.op;
-  rec.depth = po.z;
-  rec.r = (float)col[0];
-  rec.g = (float)col[1];
-  rec.bl = (float)col[2];
-  rec.pad = 0;
-  rec.src = i;
-  rec.pad2 = 0;
-  recs[idx] = rec;
-  keys_out[idx] = (uint64_t)__double_as_longlong(po.z);  // z > near > 0: bits are monotone
-  vals_out[idx] = (uint32_t)idx;
+  const double c0 = ddiv(po.c, po.det);   // render.py:172
+  const double c1 = ddiv(-po.b, po.det);
+  const double c2 = ddiv(po.a, po.det);
+  // blend fast-reject threshold: alpha = o*exp(power) < alpha_floor whenever
+  // power < log(alpha_floor / o) - 1e-6 (margin >> exp/log rounding)
+  const double lt = g.op > 0.0 ? log(st.alpha_floor / g.op) - 1e-6
+                               : __longlong_as_double(0x7ff0000000000000ll);
+  const float lthr = __double2float_rd(lt);
+  HotRec h;
+  h.mx = po.mx; h.my = po.my; h.c0 = c0; h.c1 = c1; h.c2 = c2;
+  h.lthr = lthr;
+  h.id = (uint32_t)idx;
+  // AABB of {d : power(d) >= lthr} = {d^T Q d <= 2L}, L = -lthr: half-extents
+  // sqrt(2 L a), sqrt(2 L c) with (a, b, c) = Q^-1 = cov2d + low pass;
+  // inflated (1e-4 relative + 1e-3 px) to cover rounding of the float64 power.
+  const double L = -(double)lthr;
+  if (L > 0.0) {
+    const double hx = sqrt(2.0 * L * po.a) * (1.0 + 1e-4) + 1e-3;
+    const double hy = sqrt(2.0 * L * po.c) * (1.0 + 1e-4) + 1e-3;
+    h.bx0 = __double2float_rd(po.mx - hx);
+    h.bx1 = __double2float_ru(po.mx + hx);
+    h.by0 = __double2float_rd(po.my - hy);
+    h.by1 = __double2float_ru(po.my + hy);
+  } else {
+    h.bx0 = h.by0 = __int_as_float(0x7f800000);   // empty: never intersects
+    h.bx1 = h.by1 = -__int_as_float(0x7f800000);
+  }
+  po_out.hot[idx] = h;
+  ColdRec cr;
+  cr.opacity = g.op;
+  cr.r = (float)col[0]; cr.g = (float)col[1]; cr.b = (float)col[2]; cr.pad = 0.f; cr.pad2 = 0.0;
+  po_out.cold[idx] = cr;
+  // tile rectangle exactly as numpy (render.py:226-231): floor, astype(int64), clip
+  {
+    const int64_t ntx = (cam.width + st.tile_size - 1) / st.tile_size;
+    const int64_t nty = (cam.height + st.tile_size - 1) / st.tile_size;
+    const double ts = (double)st.tile_size;
+    const int64_t tx0 = clip_i64(np_to_i64(floor(ddiv(dsub(dsub(po.mx, po.rx), 0.5), ts))), 0, ntx - 1);
+    const int64_t tx1 = clip_i64(np_to_i64(floor(ddiv(dsub(dadd(po.mx, po.rx), 0.5), ts))), 0, ntx - 1);
+    const int64_t ty0 = clip_i64(np_to_i64(floor(ddiv(dsub(dsub(po.my, po.ry), 0.5), ts))), 0, nty - 1);
+    const int64_t ty1 = clip_i64(np_to_i64(floor(ddiv(dsub(dadd(po.my, po.ry), 0.5), ts))), 0, nty - 1);
+    po_out.rects[idx] = make_int4((int)tx0, (int)tx1, (int)ty0, (int)ty1);
+  }
+  po_out.src[idx] = i;
+  po_out.keys[idx] = (uint64_t)__double_as_longlong(po.z);  // z > near > 0: bits are monotone
+  po_out.vals[idx] = (uint32_t)idx;
+  if (po_out.recs) {  // debug / dump mode: the full _Projected record (render.py:89-108)
+    ProjRec rec;
+    rec.mx = po.mx; rec.my = po.my; rec.c0 = c0; rec.c1 = c1; rec.c2 = c2;
+    rec.a = po.a; rec.b = po.b; rec.c = po.c; rec.rx = po.rx; rec.ry = po.ry;
+    rec.opacity = g.op; rec.depth = po.z;
+    rec.r = (float)col[0]; rec.g = (float)col[1]; rec.bl = (float)col[2]; rec.pad = 0;
+    rec.src = i; rec.pad2 = 0;
+    po_out.recs[idx] = rec;
+  }
 }
 
 // Single-cloud source: one segment covering the whole cloud.
@@ -282,12 +315,11 @@ __global__ void k_setup_cloud(cs_cloud c, cs_cloud* clouds, Seg* segs, DevStats*
 
 void launch_project(const cs_cloud* d_clouds, const Seg* d_segs, DevStats* d_stats,
                     const cs_camera& cam, const cs_settings& st, uint64_t* status,
-                    int64_t capacity, uint64_t* keys, uint32_t* vals, ProjRec* recs,
-                    const uint64_t* list, cudaStream_t s) {
+                    int64_t capacity, const ProjOutputs& out, const uint64_t* list, cudaStream_t s) {
   const int64_t chunks = (capacity + kProjThreads - 1) / kProjThreads;
   if (chunks == 0) return;
   k_project<<<(unsigned)chunks, kProjThreads, 0, s>>>(d_clouds, d_segs, d_stats, cam, st, status,
-                                                      keys, vals, recs, list);
+                                                      out, list);
 }
 
 void launch_setup_cloud(const cs_cloud& c, cs_cloud* d_clouds, Seg* d_segs, DevStats* d_stats,
