@@ -37,7 +37,7 @@ struct BwdParams {
 
 __global__ void __launch_bounds__(kBwdThreads)
 k_blend_bwd(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
-            const HotRec* __restrict__ hot, const ColdRec* __restrict__ cold, BwdParams bp,
+            const HotRec* __restrict__ hot, BwdParams bp,
             const float* __restrict__ dl_dimg, BlendState state, float* __restrict__ grads /* [kGradFields][cap] */, int64_t cap) {
   __shared__ __align__(16) HotRec buf[kBwdBatch];
   __shared__ int s_any;
@@ -86,14 +86,13 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
             dsub(dmul(-0.5, dadd(dmul(dmul(h.c0, dx), dx), dmul(dmul(h.c2, dy), dy))),
                  dmul(dmul(h.c1, dx), dy));
         if (power >= (double)h.lthr) {
-          const ColdRec cr = cold[h.id];
           const double G = exp(power);
-          double alpha = dmul(cr.opacity, G);
+          double alpha = dmul(h.opacity, G);
           const bool clamped = alpha > 0.99;
           if (clamped) alpha = 0.99;
           if (alpha >= bp.alpha_floor) {
             contrib = true;
-            const double col[3] = {cr.r, cr.g, cr.b};
+            const double col[3] = {h.r, h.g, h.b};
             const double w = T * alpha;
             double dl_da = 0.0;
 #pragma unroll
@@ -320,7 +319,7 @@ k_project_bwd(const cs_cloud cl, const int64_t* __restrict__ src, const DevStats
 }
 
 void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint2* ranges, const HotRec* hot,
-                      const ColdRec* cold, const cs_settings& st, int width, int height, int ntx,
+                      const cs_settings& st, int width, int height, int ntx,
                       const float* dl_dimg, const BlendState& state,
                       float* grads, int64_t cap, cudaStream_t s) {
   BwdParams bp;
@@ -330,7 +329,7 @@ void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint2* ranges, co
   bp.width = width;
   bp.height = height;
   bp.ntx = ntx;
-  k_blend_bwd<<<n_tiles, kBwdThreads, 0, s>>>(list, ranges, hot, cold, bp, dl_dimg, state, grads,
+  k_blend_bwd<<<n_tiles, kBwdThreads, 0, s>>>(list, ranges, hot, bp, dl_dimg, state, grads,
                                               cap);
 }
 

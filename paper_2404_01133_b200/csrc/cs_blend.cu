@@ -6,8 +6,10 @@
 // 8x4 pixel box.
 //
 // The tile's splat list (depth order) is streamed through shared memory in
-// batches of 256 HotRec records (64 B: mean, conic, fast-reject threshold,
-// support AABB) with cp.async double buffering.  Per batch every warp first
+// batches of 256 HotRec records (80 B: mean, conic, opacity, colour,
+// fast-reject threshold, support box) with cp.async double buffering.  Tiles
+// are launched heaviest list first (K8b), so the long hot-tile lists start in
+// the first wave instead of forming the tail.  Per batch every warp first
 // tests 32 splats at a time against its pixel box (one AABB test per lane,
 // __ballot_sync) and then walks only the hits, so a splat whose alpha-floor
 // support misses the warp's 32 pixels costs 1/32 of an AABB test instead of
@@ -46,6 +48,7 @@ __device__ __forceinline__ void stage_batch(HotRec* dst, const uint32_t* list, c
     cp_async16(d + 16, g + 16);
     cp_async16(d + 32, g + 32);
     cp_async16(d + 48, g + 48);
+    cp_async16(d + 64, g + 64);
   }
 }
 
@@ -61,13 +64,13 @@ __device__ __forceinline__ int local_pixel(int tid, int q, int ts) {
 template <int PPT, typename OutT, bool KEEP>
 __global__ void __launch_bounds__(kBlendThreads)
 k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
-        const HotRec* __restrict__ hot, const ColdRec* __restrict__ cold, BlendParams bp,
+        const HotRec* __restrict__ hot, const uint32_t* __restrict__ tile_order, BlendParams bp,
         OutT* __restrict__ out, int32_t* __restrict__ frag_tile, DevStats* __restrict__ stats,
         BlendState state) {
   __shared__ __align__(16) HotRec buf[2][kBatch];
   __shared__ int s_red[kBlendThreads / 32];
   __shared__ long long s_ev[kBlendThreads / 32];
-  const int t = blockIdx.x;
+  const int t = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
   const int tx = t % bp.ntx, ty = t / bp.ntx;
   const int ts = bp.tile_size;
   const uint2 rg = ranges[t];
@@ -75,7 +78,7 @@ k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
   const uint32_t lane = lane_id();
 
   double sx[PPT], sy[PPT], T[PPT], cr[PPT], cg[PPT], cb[PPT];
-  float wx0[PPT], wx1[PPT], wy0[PPT], wy1[PPT];  // warp's pixel-centre box per slot
+  int wx0[PPT], wx1[PPT], wy0[PPT], wy1[PPT];  // warp's pixel-index box per slot
   int cnt[PPT], last[PPT];
   bool done[PPT], valid[PPT];
   long long evals = 0;
@@ -89,15 +92,14 @@ k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
     T[q] = 1.0; cr[q] = 0.0; cg[q] = 0.0; cb[q] = 0.0;
     cnt[q] = 0; last[q] = (int)s0;
     done[q] = !valid[q];
-    const float inf = __int_as_float(0x7f800000);
-    float x0 = valid[q] ? (float)sx[q] : inf, x1 = valid[q] ? (float)sx[q] : -inf;
-    float y0 = valid[q] ? (float)sy[q] : inf, y1 = valid[q] ? (float)sy[q] : -inf;
+    int x0 = valid[q] ? px : 1 << 20, x1 = valid[q] ? px : -(1 << 20);
+    int y0 = valid[q] ? py : 1 << 20, y1 = valid[q] ? py : -(1 << 20);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      x0 = fminf(x0, __shfl_xor_sync(0xffffffffu, x0, o));
-      x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, o));
-      y0 = fminf(y0, __shfl_xor_sync(0xffffffffu, y0, o));
-      y1 = fmaxf(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+      x0 = min(x0, __shfl_xor_sync(0xffffffffu, x0, o));
+      x1 = max(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+      y0 = min(y0, __shfl_xor_sync(0xffffffffu, y0, o));
+      y1 = max(y1, __shfl_xor_sync(0xffffffffu, y1, o));
     }
     wx0[q] = x0; wx1[q] = x1; wy0[q] = y0; wy1[q] = y1;
   }
@@ -122,7 +124,7 @@ k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
         const int jl = base + (int)lane;
         bool hit = false;
         if (jl < nb) {
-          const float4 bx = *reinterpret_cast<const float4*>(&hb[jl].bx0);
+          const short4 bx = *reinterpret_cast<const short4*>(&hb[jl].bx0);
           hit = !(bx.x > wx1[q] || bx.y < wx0[q] || bx.z > wy1[q] || bx.w < wy0[q]);
         }
         uint32_t mask = __ballot_sync(0xffffffffu, hit);
@@ -139,16 +141,15 @@ k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
               dsub(dmul(-0.5, dadd(dmul(dmul(h.c0, dx), dx), dmul(dmul(h.c2, dy), dy))),
                    dmul(dmul(h.c1, dx), dy));
           if (power < (double)h.lthr) continue;  // alpha < alpha_floor guaranteed
-          const ColdRec c = cold[h.id];
-          double alpha = dmul(c.opacity, exp(power));  // _kernels.py:58
+          double alpha = dmul(h.opacity, exp(power));  // _kernels.py:58
           if (alpha > 0.99) alpha = 0.99;              // _kernels.py:59-60
           if (alpha < bp.alpha_floor) continue;        // _kernels.py:61-62
           const double nt = dmul(Tq, dsub(1.0, alpha));
           if (nt < bp.t_floor) { done[q] = true; continue; }  // _kernels.py:63-66
           const double w = dmul(Tq, alpha);
-          cr[q] += w * (double)c.r;
-          cg[q] += w * (double)c.g;
-          cb[q] += w * (double)c.b;
+          cr[q] += w * (double)h.r;
+          cg[q] += w * (double)h.g;
+          cb[q] += w * (double)h.b;
           Tq = nt;
           cnt[q] += 1;
           last[q] = (int)(bstart + j + 1);
@@ -207,18 +208,48 @@ k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
 
 template <typename OutT, bool KEEP>
 static void launch_blend_t(int ppt, int n_tiles, const uint32_t* list, const uint2* ranges,
-                           const HotRec* hot, const ColdRec* cold, const BlendParams& bp,
+                           const HotRec* hot, const uint32_t* order, const BlendParams& bp,
                            OutT* out, int32_t* frag_tile, DevStats* stats, BlendState st,
                            cudaStream_t s) {
   if (ppt == 1)
-    k_blend<1, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, ranges, hot, cold, bp, out,
+    k_blend<1, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, ranges, hot, order, bp, out,
                                                             frag_tile, stats, st);
   else if (ppt == 4)
-    k_blend<4, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, ranges, hot, cold, bp, out,
+    k_blend<4, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, ranges, hot, order, bp, out,
                                                             frag_tile, stats, st);
   else
-    k_blend<16, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, ranges, hot, cold, bp, out,
+    k_blend<16, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, ranges, hot, order, bp, out,
                                                              frag_tile, stats, st);
+}
+
+// K8b: heaviest-first tile order.  Tiles are bucketed by floor(log2(list
+// length)) and emitted bucket-descending (order inside a bucket is arbitrary;
+// tiles are independent, so the image does not depend on it).
+__global__ void k_tile_order(const uint2* __restrict__ ranges, int n_tiles, uint32_t* __restrict__ order) {
+  __shared__ int hist[34];
+  __shared__ int cursor[34];
+  if (threadIdx.x < 34) hist[threadIdx.x] = 0;
+  __syncthreads();
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+    const uint2 r = ranges[t];
+    const uint32_t c = r.y - r.x;
+    atomicAdd(&hist[c ? 32 - __clz(c) : 0], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int b = 33; b >= 0; --b) { cursor[b] = acc; acc += hist[b]; }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+    const uint2 r = ranges[t];
+    const uint32_t c = r.y - r.x;
+    order[atomicAdd(&cursor[c ? 32 - __clz(c) : 0], 1)] = (uint32_t)t;
+  }
+}
+
+void launch_tile_order(const uint2* ranges, int n_tiles, uint32_t* order, cudaStream_t s) {
+  k_tile_order<<<1, 1024, 0, s>>>(ranges, n_tiles, order);
 }
 
 int blend_ppt(int tile_size) {
@@ -230,46 +261,44 @@ int blend_ppt(int tile_size) {
 }
 
 void launch_blend(int n_tiles, const uint32_t* list, const uint2* ranges, const HotRec* hot,
-                  const ColdRec* cold, const BlendParams& bp, void* out, bool f64_out,
+                  const uint32_t* order, const BlendParams& bp, void* out, bool f64_out,
                   int32_t* frag_tile, DevStats* stats, const BlendState* keep, cudaStream_t s) {
   const int ppt = blend_ppt(bp.tile_size);
   BlendState st = keep ? *keep : BlendState{nullptr, nullptr, nullptr};
   if (f64_out) {
-    if (keep) launch_blend_t<double, true>(ppt, n_tiles, list, ranges, hot, cold, bp, (double*)out, frag_tile, stats, st, s);
-    else launch_blend_t<double, false>(ppt, n_tiles, list, ranges, hot, cold, bp, (double*)out, frag_tile, stats, st, s);
+    if (keep) launch_blend_t<double, true>(ppt, n_tiles, list, ranges, hot, order, bp, (double*)out, frag_tile, stats, st, s);
+    else launch_blend_t<double, false>(ppt, n_tiles, list, ranges, hot, order, bp, (double*)out, frag_tile, stats, st, s);
   } else {
-    if (keep) launch_blend_t<float, true>(ppt, n_tiles, list, ranges, hot, cold, bp, (float*)out, frag_tile, stats, st, s);
-    else launch_blend_t<float, false>(ppt, n_tiles, list, ranges, hot, cold, bp, (float*)out, frag_tile, stats, st, s);
+    if (keep) launch_blend_t<float, true>(ppt, n_tiles, list, ranges, hot, order, bp, (float*)out, frag_tile, stats, st, s);
+    else launch_blend_t<float, false>(ppt, n_tiles, list, ranges, hot, order, bp, (float*)out, frag_tile, stats, st, s);
   }
 }
 
 // ---------------------------------------------------------------------------
 // cs_blend_tiles: the numba kernel's exact interface (_kernels.py:18-30).
-// Packs the caller's float64 arrays into HotRec/ColdRec and the int64 CSR into
+// Packs the caller's float64 arrays into HotRec records and the int64 CSR into
 // (list, ranges); then runs the same blend kernel.  The caller's conics need
 // not come from our projection, so no cull box is assumed (infinite AABB).
 
 __global__ void k_pack_records(int64_t m, const double* means, const double* conics,
                                const double* colors, const double* opac, double alpha_floor,
-                               HotRec* hot, ColdRec* cold) {
+                               HotRec* hot) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m;
        s += (int64_t)gridDim.x * blockDim.x) {
     HotRec h;
     h.mx = means[2 * s]; h.my = means[2 * s + 1];
     h.c0 = conics[3 * s]; h.c1 = conics[3 * s + 1]; h.c2 = conics[3 * s + 2];
     const double o = opac[s];
+    h.opacity = o;
+    h.r = (float)colors[3 * s]; h.g = (float)colors[3 * s + 1]; h.b = (float)colors[3 * s + 2];
     const double lt = o > 0.0 ? log(alpha_floor / o) - 1e-6
                               : __longlong_as_double(0x7ff0000000000000ll);
     h.lthr = __double2float_rd(lt);
     h.id = (uint32_t)s;
-    const float inf = __int_as_float(0x7f800000);
-    h.bx0 = -inf; h.bx1 = inf; h.by0 = -inf; h.by1 = inf;
+    h.pad = 0;
+    h.bx0 = h.by0 = -1;     // full-image box
+    h.bx1 = h.by1 = 32000;
     hot[s] = h;
-    ColdRec c;
-    c.opacity = o;
-    c.r = (float)colors[3 * s]; c.g = (float)colors[3 * s + 1]; c.b = (float)colors[3 * s + 2];
-    c.pad = 0.f; c.pad2 = 0.0;
-    cold[s] = c;
   }
 }
 
@@ -283,11 +312,11 @@ __global__ void k_pack_tiles(int64_t p, const int64_t* tile_ids, int64_t n_tiles
 }
 
 void launch_pack(int64_t m, const double* means, const double* conics, const double* colors,
-                 const double* opac, double alpha_floor, HotRec* hot, ColdRec* cold, int64_t p,
+                 const double* opac, double alpha_floor, HotRec* hot, int64_t p,
                  const int64_t* tile_ids, int64_t n_tiles, const int64_t* offsets, uint32_t* list,
                  uint2* ranges, cudaStream_t s) {
   if (m > 0)
-    k_pack_records<<<148 * 4, 256, 0, s>>>(m, means, conics, colors, opac, alpha_floor, hot, cold);
+    k_pack_records<<<148 * 4, 256, 0, s>>>(m, means, conics, colors, opac, alpha_floor, hot);
   k_pack_tiles<<<148 * 4, 256, 0, s>>>(p, tile_ids, n_tiles, offsets, list, ranges);
 }
 

@@ -2,8 +2,8 @@
 //
 // Layouts in HBM; every per-splat array is in
 // compact (ascending assembled-index) order, written once by the projection:
-//   HotRec    :  64 B -- staged in smem by the blend (quadratic form + cull box)
-//   ColdRec   :  32 B -- read only for fragments that may be accepted
+//   HotRec    :  80 B -- staged in smem by the blend (quadratic form, opacity,
+//                        colour, fast-reject threshold, cull box)
 //   rect      :  16 B -- tile rectangle (render.py:226-231)
 //   src       :   8 B -- assembled index (depth tie-break, gradient scatter)
 //   keys/vals :  8+4 B -- depth key, compact index (sorted -> depth order)
@@ -46,20 +46,16 @@ struct __align__(16) ProjRec {
 };
 static_assert(sizeof(ProjRec) == 128, "ProjRec layout");
 
-struct __align__(16) HotRec {   // what every (pixel, splat) evaluation reads
-  double mx, my, c0, c1, c2;
-  float lthr;                    // fast-reject threshold on power (<= log(alpha_floor/o) - margin)
-  uint32_t id;                   // compact index: ColdRec slot and gradient slot
-  float bx0, bx1, by0, by1;      // pixel-space AABB of {power >= lthr} (outward rounded)
-};
-static_assert(sizeof(HotRec) == 64, "HotRec layout");
-
-struct __align__(16) ColdRec {  // read only when a fragment may be accepted
+struct __align__(16) HotRec {   // everything the blend reads per splat (80 B)
+  double mx, my, c0, c1, c2;     // mean2d, conic (render.py:128-129, 172)
   double opacity;
-  float r, g, b, pad;
-  double pad2;
+  float r, g, b;                 // SH colour (fp32 of the float64 value)
+  float lthr;                    // fast-reject threshold on power (<= log(alpha_floor/o) - margin)
+  int16_t bx0, bx1, by0, by1;    // inclusive pixel-index box of {power >= lthr}
+  uint32_t id;                   // compact index (gradient slot)
+  uint32_t pad;
 };
-static_assert(sizeof(ColdRec) == 32, "ColdRec layout");
+static_assert(sizeof(HotRec) == 80, "HotRec layout");
 
 struct DevStats {     // device mirror of cs_frame_stats + scratch counters
   int64_t assembled;
@@ -80,7 +76,6 @@ struct ProjOutputs {
   uint64_t* keys;    // depth bits
   uint32_t* vals;    // compact index
   HotRec* hot;
-  ColdRec* cold;
   int4* rects;
   int64_t* src;
   ProjRec* recs;     // optional (debug / dumps)

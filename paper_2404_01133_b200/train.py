@@ -49,16 +49,17 @@ class RasterizeFn(torch.autograd.Function):
         src.cloud = dc.desc()
         ccam = device.camera_struct(cam)
         cset = device.settings_struct(settings)
-        check(_lib.load().cs_render(device.context(dev.index), ctypes.byref(src), ctypes.byref(ccam),
+        h = device.context(dev.index)  # backward may run on autograd's device thread: reuse h
+        check(_lib.load().cs_render(h, ctypes.byref(src), ctypes.byref(ccam),
                                     ctypes.byref(cset), out.data_ptr(), _lib.CS_RENDER_KEEP_STATE, None,
                                     device.stream_handle(dev)), "cs_render")
-        ctx.keep = (dc, src, ccam, cset)
+        ctx.keep = (dc, src, ccam, cset, h)
         ctx.sh_shape = sh.shape
         return out
 
     @staticmethod
     def backward(ctx, grad_out):
-        dc, src, ccam, cset = ctx.keep
+        dc, src, ccam, cset, h = ctx.keep
         dev = grad_out.device
         k = dc.count
         g = grad_out.contiguous().float()
@@ -68,7 +69,7 @@ class RasterizeFn(torch.autograd.Function):
         go = torch.empty((k,), dtype=torch.float32, device=dev)
         gsh = torch.empty(ctx.sh_shape, dtype=torch.float32, device=dev)
         grads = CsGrads(gp.data_ptr(), gs.data_ptr(), gq.data_ptr(), go.data_ptr(), gsh.data_ptr())
-        check(_lib.load().cs_render_backward(device.context(dev.index), ctypes.byref(src), ctypes.byref(ccam),
+        check(_lib.load().cs_render_backward(h, ctypes.byref(src), ctypes.byref(ccam),
                                              ctypes.byref(cset), g.data_ptr(), ctypes.byref(grads),
                                              device.stream_handle(dev)), "cs_render_backward")
         return gp, gs, gq, go, gsh, None, None
