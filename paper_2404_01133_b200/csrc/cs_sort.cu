@@ -72,6 +72,7 @@ k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
   constexpr int kItems = SortCfg<K>::kItems;
   constexpr int kTile = kSortThreads * kItems;
   __shared__ uint32_t warp_hist[kSortWarps][256];
+  __shared__ uint32_t chunk_hist[256];
   __shared__ uint32_t digit_off[256];
   __shared__ int64_t gbase[256];
   __shared__ uint32_t scratch[kSortWarps + 1];
@@ -83,6 +84,7 @@ k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
   if (threadIdx.x == 0) s_chunk = atomicAdd(ticket, 1u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int d = lane; d < 256; d += 32) warp_hist[warp][d] = 0;
+  chunk_hist[threadIdx.x] = 0;
   __syncthreads();
   const int64_t chunk = s_chunk;
   const int64_t base = chunk * kTile;
@@ -101,24 +103,34 @@ k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
       val[r] = vals_in[idx];
     }
   }
+  // 1) chunk histogram first, published immediately so successors' look-back
+  //    finds this chunk's aggregate while it is still ranking
+#pragma unroll
+  for (int r = 0; r < kItems; ++r)
+    if (wbase + r * 32 + lane < n) atomicAdd(&chunk_hist[(uint32_t)((key[r] >> shift) & 255)], 1u);
+  __syncthreads();
+  const int d = threadIdx.x;  // 256 threads == 256 digits
+  const uint32_t my_count = chunk_hist[d];
+  uint32_t* my_status = status + chunk * 256 + d;
+  atomicExch(my_status, (chunk == 0 ? kStFlagPre : kStFlagAgg) | my_count);
+  // 2) stable in-warp ranks (warp order == input order)
   const uint32_t lt = lanemask_lt();
 #pragma unroll
   for (int r = 0; r < kItems; ++r) {
     const int64_t idx = wbase + r * 32 + lane;
     const bool valid = idx < n;
-    const uint32_t d = valid ? (uint32_t)((key[r] >> shift) & 255) : 256u + lane;
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t dg = valid ? (uint32_t)((key[r] >> shift) & 255) : 256u + lane;
+    const uint32_t peers = __match_any_sync(0xffffffffu, dg);
     const uint32_t pr = __popc(peers & lt);
     uint32_t old = 0;
-    if (valid) old = warp_hist[warp][d];
+    if (valid) old = warp_hist[warp][dg];
     __syncwarp();
-    if (valid && pr == 0) warp_hist[warp][d] = old + __popc(peers);
+    if (valid && pr == 0) warp_hist[warp][dg] = old + __popc(peers);
     __syncwarp();
     rank[r] = old + pr;
   }
   __syncthreads();
-  // combine warps (warp order == input order) -> per-digit chunk counts
-  const int d = threadIdx.x;  // 256 threads == 256 digits
+  // 3) combine warps and the chunk-local digit starts
   uint32_t sum = 0;
 #pragma unroll
   for (int w = 0; w < kSortWarps; ++w) {
@@ -126,32 +138,11 @@ k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     warp_hist[w][d] = sum;
     sum += c;
   }
-  uint32_t* my_status = status + chunk * 256 + d;
-  if (chunk == 0) {
-    atomicExch(my_status, kStFlagPre | sum);
-  } else {
-    atomicExch(my_status, kStFlagAgg | sum);
-  }
   uint32_t total;
   const uint32_t local_start = block_excl_scan<uint32_t>(sum, scratch, total);
   digit_off[d] = local_start;
-  // decoupled look-back for this digit
-  int64_t excl = 0;
-  if (chunk > 0) {
-    int64_t p = chunk - 1;
-    while (p >= 0) {
-      uint32_t s = ld_volatile_u32(status + p * 256 + d);
-      const uint32_t flag = s >> 30;
-      if (flag == 0) continue;
-      excl += s & kStMask;
-      if (flag == 2) break;
-      --p;
-    }
-    atomicExch(my_status, kStFlagPre | (uint32_t)(excl + sum));
-  }
-  gbase[d] = (int64_t)digit_base[d] + excl - (int64_t)local_start;
   __syncthreads();
-  // scatter into shared memory in chunk-local sorted order
+  // 4) scatter into shared memory in chunk-local sorted order
 #pragma unroll
   for (int r = 0; r < kItems; ++r) {
     const int64_t idx = wbase + r * 32 + lane;
@@ -162,7 +153,31 @@ k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
       vals_s[pos] = val[r];
     }
   }
+  // 5) decoupled look-back for this digit, four predecessors per round trip
+  int64_t excl = 0;
+  if (chunk > 0) {
+    int64_t p = chunk - 1;
+    bool found = false;
+    while (!found) {
+      uint32_t st[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        st[k] = p - k >= 0 ? ld_volatile_u32(status + (p - k) * 256 + d) : (kStFlagPre | 0u);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (found) break;
+        const uint32_t flag = st[k] >> 30;
+        if (flag == 0) break;          // not published yet: re-read from here
+        excl += st[k] & kStMask;
+        --p;
+        if (flag == 2) found = true;
+      }
+    }
+    atomicExch(my_status, kStFlagPre | (uint32_t)(excl + my_count));
+  }
+  gbase[d] = (int64_t)digit_base[d] + excl - (int64_t)local_start;
   __syncthreads();
+  // 6) coalesced write-out: consecutive threads store consecutive addresses of one digit run
   for (int i = threadIdx.x; i < valid_count; i += kSortThreads) {
     const K k = keys_s[i];
     const uint32_t dg = (uint32_t)((k >> shift) & 255);
