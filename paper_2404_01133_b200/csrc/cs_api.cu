@@ -66,10 +66,11 @@ void launch_dump_tiles(const uint32_t* order, const uint32_t* vals, const uint2*
 int blend_ppt(int tile_size);
 void launch_tile_order(const uint2* ranges, int n_tiles, uint32_t* order, cudaStream_t s);
 void launch_blend(int n_tiles, const uint32_t* list, const uint2* ranges, const HotRec* hot,
-                  const uint32_t* order, const BlendParams& bp, void* out, bool f64_out,
+                  const short4* boxes, const uint32_t* order, const BlendParams& bp, void* out,
+                  bool f64_out,
                   int32_t* frag_tile, DevStats* stats, const BlendState* keep, cudaStream_t s);
 void launch_pack(int64_t m, const double* means, const double* conics, const double* colors,
-                 const double* opac, double alpha_floor, HotRec* hot, int64_t p,
+                 const double* opac, double alpha_floor, HotRec* hot, short4* boxes, int64_t p,
                  const int64_t* tile_ids, int64_t n_tiles, const int64_t* offsets, uint32_t* list,
                  uint2* ranges, cudaStream_t s);
 // cs_fuse.cu
@@ -167,7 +168,7 @@ struct cs_ctx {
   DBuf stats, clouds1, segs, dec;
   DBuf st_proj, st_gather, st_pw, st_fuse, st_sort, hist, sort_tickets, fuse_ticket;
   DBuf keysA, valsA, keysB, valsB, recs;
-  DBuf hot, rects, src, pair_off, tile_order;
+  DBuf hot, boxes, rects, src, pair_off, tile_order;
   DBuf pkA, pvA, pkB, pvB, ranges, frag_tile, pw_list;
   DBuf st_t, st_last, st_acc;
   DBuf scratch1, scratch2, scratch3, scratch4;  // API utilities
@@ -229,7 +230,7 @@ void cs_destroy(cs_ctx* c) {
   DBuf* all[] = {&c->stats, &c->clouds1, &c->segs, &c->dec, &c->st_proj, &c->st_gather,
                  &c->st_pw, &c->st_fuse, &c->st_sort, &c->hist, &c->sort_tickets,
                  &c->fuse_ticket, &c->keysA, &c->valsA, &c->keysB, &c->valsB, &c->recs, &c->hot,
-                 &c->tile_order, &c->rects, &c->src, &c->pair_off, &c->pkA, &c->pvA, &c->pkB,
+                 &c->tile_order, &c->boxes, &c->rects, &c->src, &c->pair_off, &c->pkA, &c->pvA, &c->pkB,
                  &c->pvB, &c->ranges, &c->frag_tile, &c->pw_list, &c->st_t, &c->st_last,
                  &c->st_acc, &c->gacc, &c->scratch1, &c->scratch2, &c->scratch3, &c->scratch4};
   for (DBuf* b : all) b->release();
@@ -312,7 +313,7 @@ static int ensure_frame_buffers(cs_ctx* c, int64_t cap_vis, int n_segs, int n_bl
     if (c->st_proj.ensure(8 * chunks) || c->st_gather.ensure(8 * chunks) ||
         c->keysA.ensure(8 * cap) || c->keysB.ensure(8 * cap) || c->valsA.ensure(4 * cap) ||
         c->valsB.ensure(4 * cap) || c->hot.ensure(sizeof(HotRec) * cap) ||
-        c->rects.ensure(16 * cap) ||
+        c->rects.ensure(16 * cap) || c->boxes.ensure(8 * cap) ||
         c->src.ensure(8 * cap) || c->pair_off.ensure(8 * cap))
       return fail(CS_ENOMEM, "visible-splat buffers (%lld)", (long long)cap);
     c->cap_vis = cap;
@@ -420,7 +421,7 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
   const bool debug = (flags & (CS_RENDER_DEBUG | CS_RENDER_PROJECT_ONLY)) != 0;
   if (debug && c->recs.ensure(sizeof(ProjRec) * c->cap_vis)) return fail(CS_ENOMEM, "debug records");
   ProjOutputs po{c->keysA.as<uint64_t>(), c->valsA.as<uint32_t>(), c->hot.as<HotRec>(),
-                 c->rects.as<int4>(), c->src.as<int64_t>(),
+                 c->rects.as<int4>(), c->boxes.as<short4>(), c->src.as<int64_t>(),
                  debug ? c->recs.as<ProjRec>() : nullptr};
   launch_project(clouds, c->segs.as<Seg>(), stats, *cam, *st, c->st_proj.as<uint64_t>(), cap, po,
                  list, s);
@@ -485,7 +486,8 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
   }
   launch_tile_order(c->ranges.as<uint2>(), n_tiles, c->tile_order.as<uint32_t>(), s);
   CS_CHECK_LAUNCH();
-  launch_blend(n_tiles, tvals, c->ranges.as<uint2>(), c->hot.as<HotRec>(), c->tile_order.as<uint32_t>(),
+  launch_blend(n_tiles, tvals, c->ranges.as<uint2>(), c->hot.as<HotRec>(), c->boxes.as<short4>(),
+               c->tile_order.as<uint32_t>(),
                bp, out, (flags & CS_RENDER_F64_OUT) != 0, c->frag_tile.as<int32_t>(), stats,
                (flags & CS_RENDER_KEEP_STATE) ? &keep : nullptr, s);
   CS_CHECK_LAUNCH();
@@ -791,7 +793,7 @@ int cs_blend_tiles(cs_ctx* c, const int64_t* tile_ids, const int64_t* tile_offse
   CS_CUDA(cudaMemcpyAsync(bg, background, 24, cudaMemcpyDeviceToHost, s));
   CS_CUDA(cudaStreamSynchronize(s));
   const int64_t m = std::max<int64_t>(n_splats, 1);
-  if (c->scratch1.ensure(sizeof(HotRec) * m) ||
+  if (c->scratch1.ensure((sizeof(HotRec) + 8) * m) ||
       c->scratch2.ensure(4 * std::max<int64_t>(P, 1) + sizeof(uint2) * n_tiles + 4 * n_tiles) ||
       c->stats.ensure(sizeof(DevStats)))
     return fail(CS_ENOMEM, "blend scratch");
@@ -801,7 +803,8 @@ int cs_blend_tiles(cs_ctx* c, const int64_t* tile_ids, const int64_t* tile_offse
   // keep uint2 8-byte aligned
   ranges = reinterpret_cast<uint2*>((reinterpret_cast<uintptr_t>(ranges) + 7) & ~uintptr_t(7));
   int32_t* ftile = reinterpret_cast<int32_t*>(ranges + n_tiles);
-  launch_pack(n_splats, means, conics, colors, opacities, alpha_floor, hot, P, tile_ids,
+  short4* pboxes = reinterpret_cast<short4*>(hot + m);
+  launch_pack(n_splats, means, conics, colors, opacities, alpha_floor, hot, pboxes, P, tile_ids,
               n_tiles, tile_offsets, list, ranges, s);
   CS_CHECK_LAUNCH();
   CS_CUDA(cudaMemsetAsync(c->stats.p, 0, sizeof(DevStats), s));
@@ -814,7 +817,7 @@ int cs_blend_tiles(cs_ctx* c, const int64_t* tile_ids, const int64_t* tile_offse
   bp.height = height;
   bp.ntx = n_tiles_x;
   bp.flags = CS_RENDER_NO_CLIP;
-  launch_blend((int)n_tiles, list, ranges, hot, nullptr, bp, out, true, ftile, c->stats.as<DevStats>(),
+  launch_blend((int)n_tiles, list, ranges, hot, pboxes, nullptr, bp, out, true, ftile, c->stats.as<DevStats>(),
                nullptr, s);
   CS_CHECK_LAUNCH();
   // fragments: int32 per tile -> int64

@@ -5,16 +5,14 @@
 // 4 or 16 pixels per thread for 32/64).  For 16x16 tiles each warp owns an
 // 8x4 pixel box.
 //
-// The tile's splat list (depth order) is streamed through shared memory in
-// batches of 256 HotRec records (80 B: mean, conic, opacity, colour,
-// fast-reject threshold, support box) with cp.async double buffering.  Tiles
-// are launched heaviest list first (K8b), so the long hot-tile lists start in
-// the first wave instead of forming the tail.  Per batch every warp first
-// tests 32 splats at a time against its pixel box (one AABB test per lane,
-// __ballot_sync) and then walks only the hits, so a splat whose alpha-floor
-// support misses the warp's 32 pixels costs 1/32 of an AABB test instead of
-// 32 float64 quadratic forms.  The CTA leaves as soon as every pixel has
-// terminated (__syncthreads_count).
+// Every warp walks the tile's splat list (depth order) independently, 32
+// entries per round: each lane tests one splat's 8-byte alpha-floor support
+// box against the warp's pixel box, __ballot_sync compacts the hits, and the
+// warp evaluates only those (80-byte HotRec: mean, conic, opacity, colour,
+// fast-reject threshold), so a splat whose support misses the warp's 32
+// pixels costs 1/32 of a box test instead of 32 float64 quadratic forms, and
+// no warp ever waits at a block barrier for another.  Tiles are launched
+// heaviest list first (K8b) so hot-tile lists start in the first wave.
 //
 // Precision: the quadratic form is float64 in the
 // reference's exact op order (no FMA).  A float64 power below
@@ -31,43 +29,31 @@ namespace cs {
 constexpr int kBlendThreads = 256;
 constexpr int kBatch = 256;
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-__device__ __forceinline__ void stage_batch(HotRec* dst, const uint32_t* list, const HotRec* hot,
-                                            int64_t k, int64_t s1) {
-  if (k < s1) {
-    const char* g = reinterpret_cast<const char*>(hot + __ldg(list + k));
-    char* d = reinterpret_cast<char*>(dst + threadIdx.x);
-    cp_async16(d, g);
-    cp_async16(d + 16, g + 16);
-    cp_async16(d + 32, g + 32);
-    cp_async16(d + 48, g + 48);
-    cp_async16(d + 64, g + 64);
-  }
-}
-
-// local pixel index (0..ts*ts-1) of thread `tid`, pixel slot q
+// local pixel index (0..ts*ts-1) of thread `tid`, pixel slot q.  When the
+// tile side is a multiple of 8, warps own 8x4 pixel boxes (box index
+// warp + 8q, row-major over the tile's (ts/8) x (ts/4) boxes).
 __device__ __forceinline__ int local_pixel(int tid, int q, int ts) {
-  if (ts == 16) {  // 8x4 box per warp: warp w -> origin ((w & 1) * 8, (w >> 1) * 4)
-    const int w = tid >> 5, l = tid & 31;
-    return ((w >> 1) * 4 + (l >> 3)) * 16 + (w & 1) * 8 + (l & 7);
+  if ((ts & 7) == 0) {
+    const int b = (tid >> 5) + 8 * q, l = tid & 31, nbx = ts >> 3;
+    const int bx = b % nbx, by = b / nbx;
+    return (by * 4 + (l >> 3)) * ts + bx * 8 + (l & 7);
   }
   return tid + q * kBlendThreads;
 }
 
+// Warp-independent blend: each warp walks the tile's depth-ordered list on
+// its own (no block barriers).  Per round of 32 list entries each lane
+// fetches one splat's 8-byte cull box (dense array, L2-resident) and tests it
+// against the warp's pixel box; __ballot_sync compacts the hits and the warp
+// then evaluates each hit for its 32 pixels, reading the 80-byte HotRec with a
+// warp-uniform (broadcast) load.  A warp stops as soon as its 32 pixels have
+// terminated.
 template <int PPT, typename OutT, bool KEEP>
 __global__ void __launch_bounds__(kBlendThreads)
 k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
-        const HotRec* __restrict__ hot, const uint32_t* __restrict__ tile_order, BlendParams bp,
-        OutT* __restrict__ out, int32_t* __restrict__ frag_tile, DevStats* __restrict__ stats,
-        BlendState state) {
-  __shared__ __align__(16) HotRec buf[2][kBatch];
+        const HotRec* __restrict__ hot, const short4* __restrict__ boxes,
+        const uint32_t* __restrict__ tile_order, BlendParams bp, OutT* __restrict__ out,
+        int32_t* __restrict__ frag_tile, DevStats* __restrict__ stats, BlendState state) {
   __shared__ int s_red[kBlendThreads / 32];
   __shared__ long long s_ev[kBlendThreads / 32];
   const int t = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
@@ -76,24 +62,15 @@ k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
   const uint2 rg = ranges[t];
   const int64_t s0 = rg.x, s1 = rg.y;
   const uint32_t lane = lane_id();
-
-  double sx[PPT], sy[PPT], T[PPT], cr[PPT], cg[PPT], cb[PPT];
-  int wx0[PPT], wx1[PPT], wy0[PPT], wy1[PPT];  // warp's pixel-index box per slot
-  int cnt[PPT], last[PPT];
-  bool done[PPT], valid[PPT];
+  int my_frag = 0;
   long long evals = 0;
-#pragma unroll
+#pragma unroll 1
   for (int q = 0; q < PPT; ++q) {
     const int li = local_pixel(threadIdx.x, q, ts);
     const int px = tx * ts + li % ts, py = ty * ts + li / ts;
-    valid[q] = li < ts * ts && px < bp.width && py < bp.height;
-    sx[q] = (double)px + 0.5;  // pixel centres (_kernels.py:43-45)
-    sy[q] = (double)py + 0.5;
-    T[q] = 1.0; cr[q] = 0.0; cg[q] = 0.0; cb[q] = 0.0;
-    cnt[q] = 0; last[q] = (int)s0;
-    done[q] = !valid[q];
-    int x0 = valid[q] ? px : 1 << 20, x1 = valid[q] ? px : -(1 << 20);
-    int y0 = valid[q] ? py : 1 << 20, y1 = valid[q] ? py : -(1 << 20);
+    const bool valid = li < ts * ts && px < bp.width && py < bp.height;
+    int x0 = valid ? px : 1 << 20, x1 = valid ? px : -(1 << 20);
+    int y0 = valid ? py : 1 << 20, y1 = valid ? py : -(1 << 20);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       x0 = min(x0, __shfl_xor_sync(0xffffffffu, x0, o));
@@ -101,97 +78,81 @@ k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
       y0 = min(y0, __shfl_xor_sync(0xffffffffu, y0, o));
       y1 = max(y1, __shfl_xor_sync(0xffffffffu, y1, o));
     }
-    wx0[q] = x0; wx1[q] = x1; wy0[q] = y0; wy1[q] = y1;
-  }
-
-  const int64_t n = s1 - s0;
-  const int nbatches = (int)((n + kBatch - 1) / kBatch);
-  if (nbatches > 0) stage_batch(buf[0], list, hot, s0 + threadIdx.x, s1);
-  cp_async_commit();
-  for (int b = 0; b < nbatches; ++b) {
-    const int64_t bstart = s0 + (int64_t)b * kBatch;
-    if (b + 1 < nbatches) stage_batch(buf[(b + 1) & 1], list, hot, bstart + kBatch + threadIdx.x, s1);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    const HotRec* hb = buf[b & 1];
-    const int nb = (int)min((int64_t)kBatch, s1 - bstart);
-#pragma unroll
-    for (int q = 0; q < PPT; ++q) {
-      if (__all_sync(0xffffffffu, done[q])) continue;
-      double Tq = T[q];
-      for (int base = 0; base < nb; base += 32) {
-        const int jl = base + (int)lane;
-        bool hit = false;
-        if (jl < nb) {
-          const short4 bx = *reinterpret_cast<const short4*>(&hb[jl].bx0);
-          hit = !(bx.x > wx1[q] || bx.y < wx0[q] || bx.z > wy1[q] || bx.w < wy0[q]);
-        }
-        uint32_t mask = __ballot_sync(0xffffffffu, hit);
-        while (mask) {
-          const int j = base + __ffs(mask) - 1;
-          mask &= mask - 1;
-          if (done[q]) continue;
-          ++evals;
-          const HotRec& h = hb[j];
-          const double dx = dsub(sx[q], h.mx);
-          const double dy = dsub(sy[q], h.my);
-          // -0.5 * (c0*dx*dx + c2*dy*dy) - c1*dx*dy   (_kernels.py:54-57)
-          const double power =
-              dsub(dmul(-0.5, dadd(dmul(dmul(h.c0, dx), dx), dmul(dmul(h.c2, dy), dy))),
-                   dmul(dmul(h.c1, dx), dy));
-          if (power < (double)h.lthr) continue;  // alpha < alpha_floor guaranteed
-          double alpha = dmul(h.opacity, exp(power));  // _kernels.py:58
-          if (alpha > 0.99) alpha = 0.99;              // _kernels.py:59-60
-          if (alpha < bp.alpha_floor) continue;        // _kernels.py:61-62
-          const double nt = dmul(Tq, dsub(1.0, alpha));
-          if (nt < bp.t_floor) { done[q] = true; continue; }  // _kernels.py:63-66
-          const double w = dmul(Tq, alpha);
-          cr[q] += w * (double)h.r;
-          cg[q] += w * (double)h.g;
-          cb[q] += w * (double)h.b;
-          Tq = nt;
-          cnt[q] += 1;
-          last[q] = (int)(bstart + j + 1);
-        }
-        if (__all_sync(0xffffffffu, done[q])) break;
+    if (x0 > x1) continue;  // no pixel of this slot in the image (warp-uniform)
+    const double sx = (double)px + 0.5, sy = (double)py + 0.5;  // _kernels.py:43-45
+    double T = 1.0, cr = 0.0, cg = 0.0, cb = 0.0;
+    int cnt = 0;
+    int64_t last = s0;
+    bool done = !valid;
+    // software-pipelined fetch of (id, box) for the next round of 32 entries
+    uint32_t nid = 0;
+    short4 nbx = make_short4(32000, -1, 32000, -1);
+    if (s0 + lane < s1) {
+      nid = __ldg(list + s0 + lane);
+      nbx = __ldg(boxes + nid);
+    }
+    for (int64_t k0 = s0; k0 < s1; k0 += 32) {
+      const uint32_t id = nid;
+      const short4 bx = nbx;
+      if (k0 + 32 + lane < s1) {
+        nid = __ldg(list + k0 + 32 + lane);
+        nbx = __ldg(boxes + nid);
       }
-      T[q] = Tq;
+      const bool hit = !(bx.x > x1 || bx.y < x0 || bx.z > y1 || bx.w < y0);
+      uint32_t mask = __ballot_sync(0xffffffffu, hit);
+      while (mask) {
+        const int src = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const uint32_t jid = __shfl_sync(0xffffffffu, id, src);
+        if (done) continue;
+        ++evals;
+        const HotRec h = hot[jid];
+        const double dx = dsub(sx, h.mx);
+        const double dy = dsub(sy, h.my);
+        // -0.5 * (c0*dx*dx + c2*dy*dy) - c1*dx*dy   (_kernels.py:54-57)
+        const double power =
+            dsub(dmul(-0.5, dadd(dmul(dmul(h.c0, dx), dx), dmul(dmul(h.c2, dy), dy))),
+                 dmul(dmul(h.c1, dx), dy));
+        if (power < (double)h.lthr) continue;  // alpha < alpha_floor guaranteed
+        double alpha = dmul(h.opacity, exp(power));  // _kernels.py:58
+        if (alpha > 0.99) alpha = 0.99;              // _kernels.py:59-60
+        if (alpha < bp.alpha_floor) continue;        // _kernels.py:61-62
+        const double nt = dmul(T, dsub(1.0, alpha));
+        if (nt < bp.t_floor) { done = true; continue; }  // _kernels.py:63-66
+        const double w = dmul(T, alpha);
+        cr += w * (double)h.r;
+        cg += w * (double)h.g;
+        cb += w * (double)h.b;
+        T = nt;
+        cnt += 1;
+        last = k0 + src + 1;
+      }
+      if (__all_sync(0xffffffffu, done)) break;
     }
-    int alive = 0;
+    if (valid) {
+      my_frag += cnt;
+      const int64_t pix = (int64_t)py * bp.width + px;
+      double o[3] = {cr + T * bp.bg[0], cg + T * bp.bg[1], cb + T * bp.bg[2]};
+      if (!(bp.flags & CS_RENDER_NO_CLIP)) {
 #pragma unroll
-    for (int q = 0; q < PPT; ++q) alive |= done[q] ? 0 : 1;
-    if (__syncthreads_count(alive) == 0) break;
+        for (int c = 0; c < 3; ++c) o[c] = o[c] < 0.0 ? 0.0 : (o[c] > 1.0 ? 1.0 : o[c]);
+      }
+      out[3 * pix] = (OutT)o[0];
+      out[3 * pix + 1] = (OutT)o[1];
+      out[3 * pix + 2] = (OutT)o[2];
+      if (KEEP) {
+        state.final_t[pix] = T;
+        state.last[pix] = (int32_t)last;
+        state.color_acc[3 * pix] = cr;
+        state.color_acc[3 * pix + 1] = cg;
+        state.color_acc[3 * pix + 2] = cb;
+      }
+    }
   }
-  cp_async_wait<0>();
-  int my = 0;
-#pragma unroll
-  for (int q = 0; q < PPT; ++q) {
-    if (!valid[q]) continue;
-    my += cnt[q];
-    const int li = local_pixel(threadIdx.x, q, ts);
-    const int px = tx * ts + li % ts, py = ty * ts + li / ts;
-    const int64_t pix = (int64_t)py * bp.width + px;
-    double o[3] = {cr[q] + T[q] * bp.bg[0], cg[q] + T[q] * bp.bg[1], cb[q] + T[q] * bp.bg[2]};
-    if (!(bp.flags & CS_RENDER_NO_CLIP)) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) o[c] = o[c] < 0.0 ? 0.0 : (o[c] > 1.0 ? 1.0 : o[c]);
-    }
-    out[3 * pix] = (OutT)o[0];
-    out[3 * pix + 1] = (OutT)o[1];
-    out[3 * pix + 2] = (OutT)o[2];
-    if (KEEP) {
-      state.final_t[pix] = T[q];
-      state.last[pix] = last[q];
-      state.color_acc[3 * pix] = cr[q];
-      state.color_acc[3 * pix + 1] = cg[q];
-      state.color_acc[3 * pix + 2] = cb[q];
-    }
-  }
-  my = warp_sum(my);
+  my_frag = warp_sum(my_frag);
   evals = warp_sum(evals);
   if (lane == 0) {
-    s_red[threadIdx.x >> 5] = my;
+    s_red[threadIdx.x >> 5] = my_frag;
     s_ev[threadIdx.x >> 5] = evals;
   }
   __syncthreads();
@@ -208,17 +169,18 @@ k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
 
 template <typename OutT, bool KEEP>
 static void launch_blend_t(int ppt, int n_tiles, const uint32_t* list, const uint2* ranges,
-                           const HotRec* hot, const uint32_t* order, const BlendParams& bp,
+                           const HotRec* hot, const short4* boxes, const uint32_t* order,
+                           const BlendParams& bp,
                            OutT* out, int32_t* frag_tile, DevStats* stats, BlendState st,
                            cudaStream_t s) {
   if (ppt == 1)
-    k_blend<1, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, ranges, hot, order, bp, out,
+    k_blend<1, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, ranges, hot, boxes, order, bp, out,
                                                             frag_tile, stats, st);
   else if (ppt == 4)
-    k_blend<4, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, ranges, hot, order, bp, out,
+    k_blend<4, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, ranges, hot, boxes, order, bp, out,
                                                             frag_tile, stats, st);
   else
-    k_blend<16, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, ranges, hot, order, bp, out,
+    k_blend<16, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, ranges, hot, boxes, order, bp, out,
                                                              frag_tile, stats, st);
 }
 
@@ -261,16 +223,17 @@ int blend_ppt(int tile_size) {
 }
 
 void launch_blend(int n_tiles, const uint32_t* list, const uint2* ranges, const HotRec* hot,
-                  const uint32_t* order, const BlendParams& bp, void* out, bool f64_out,
+                  const short4* boxes, const uint32_t* order, const BlendParams& bp, void* out,
+                  bool f64_out,
                   int32_t* frag_tile, DevStats* stats, const BlendState* keep, cudaStream_t s) {
   const int ppt = blend_ppt(bp.tile_size);
   BlendState st = keep ? *keep : BlendState{nullptr, nullptr, nullptr};
   if (f64_out) {
-    if (keep) launch_blend_t<double, true>(ppt, n_tiles, list, ranges, hot, order, bp, (double*)out, frag_tile, stats, st, s);
-    else launch_blend_t<double, false>(ppt, n_tiles, list, ranges, hot, order, bp, (double*)out, frag_tile, stats, st, s);
+    if (keep) launch_blend_t<double, true>(ppt, n_tiles, list, ranges, hot, boxes, order, bp, (double*)out, frag_tile, stats, st, s);
+    else launch_blend_t<double, false>(ppt, n_tiles, list, ranges, hot, boxes, order, bp, (double*)out, frag_tile, stats, st, s);
   } else {
-    if (keep) launch_blend_t<float, true>(ppt, n_tiles, list, ranges, hot, order, bp, (float*)out, frag_tile, stats, st, s);
-    else launch_blend_t<float, false>(ppt, n_tiles, list, ranges, hot, order, bp, (float*)out, frag_tile, stats, st, s);
+    if (keep) launch_blend_t<float, true>(ppt, n_tiles, list, ranges, hot, boxes, order, bp, (float*)out, frag_tile, stats, st, s);
+    else launch_blend_t<float, false>(ppt, n_tiles, list, ranges, hot, boxes, order, bp, (float*)out, frag_tile, stats, st, s);
   }
 }
 
@@ -282,7 +245,7 @@ void launch_blend(int n_tiles, const uint32_t* list, const uint2* ranges, const 
 
 __global__ void k_pack_records(int64_t m, const double* means, const double* conics,
                                const double* colors, const double* opac, double alpha_floor,
-                               HotRec* hot) {
+                               HotRec* hot, short4* boxes) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m;
        s += (int64_t)gridDim.x * blockDim.x) {
     HotRec h;
@@ -299,6 +262,7 @@ __global__ void k_pack_records(int64_t m, const double* means, const double* con
     h.bx0 = h.by0 = -1;     // full-image box
     h.bx1 = h.by1 = 32000;
     hot[s] = h;
+    boxes[s] = make_short4(h.bx0, h.bx1, h.by0, h.by1);
   }
 }
 
@@ -312,11 +276,11 @@ __global__ void k_pack_tiles(int64_t p, const int64_t* tile_ids, int64_t n_tiles
 }
 
 void launch_pack(int64_t m, const double* means, const double* conics, const double* colors,
-                 const double* opac, double alpha_floor, HotRec* hot, int64_t p,
+                 const double* opac, double alpha_floor, HotRec* hot, short4* boxes, int64_t p,
                  const int64_t* tile_ids, int64_t n_tiles, const int64_t* offsets, uint32_t* list,
                  uint2* ranges, cudaStream_t s) {
   if (m > 0)
-    k_pack_records<<<148 * 4, 256, 0, s>>>(m, means, conics, colors, opac, alpha_floor, hot);
+    k_pack_records<<<148 * 4, 256, 0, s>>>(m, means, conics, colors, opac, alpha_floor, hot, boxes);
   k_pack_tiles<<<148 * 4, 256, 0, s>>>(p, tile_ids, n_tiles, offsets, list, ranges);
 }
 

@@ -77,6 +77,7 @@ struct ProjOutputs {
   uint32_t* vals;    // compact index
   HotRec* hot;
   int4* rects;
+  short4* boxes;     // copy of HotRec's cull box, dense (8 B) for the blend's warp tests
   int64_t* src;
   ProjRec* recs;     // optional (debug / dumps)
 };

@@ -27,40 +27,63 @@ __device__ __forceinline__ int degree_of(int c) { return c >= 16 ? 3 : c >= 9 ? 
 // eval_sh_basis (core.py:114-146) fused with sh_to_colors (core.py:166-172):
 // colour = clip(0.5 + sum_n sh[c, n] * Y_n(dir), 0, 1).  Tolerance-only
 // quantity (the reference sums through numpy einsum), evaluated in float64.
-__device__ void sh_colour(const float* row, int C, int degree, double x, double y, double z,
-                          double out[3]) {
-  double basis[16];
-  basis[0] = kShC0;
-  if (degree >= 1) {
-    basis[1] = -kShC1 * y;
-    basis[2] = kShC1 * z;
-    basis[3] = -kShC1 * x;
+// The row (3*C floats, 16-byte aligned, stride % 4 == 0) is fetched with
+// float4 loads; C is a template parameter so basis and coefficients stay in
+// registers.
+template <int C>
+__device__ __forceinline__ void sh_colour_t(const float* row, int degree, double x, double y,
+                                            double z, double out[3]) {
+  constexpr int kVec = (3 * C + 3) / 4;
+  float co[kVec * 4];
+  const float4* r4 = reinterpret_cast<const float4*>(row);
+#pragma unroll
+  for (int i = 0; i < kVec; ++i) {
+    const float4 v = __ldg(r4 + i);
+    co[4 * i] = v.x; co[4 * i + 1] = v.y; co[4 * i + 2] = v.z; co[4 * i + 3] = v.w;
   }
-  if (degree >= 2) {
-    double xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
-    basis[4] = kShC2[0] * xy;
-    basis[5] = kShC2[1] * yz;
-    basis[6] = kShC2[2] * (2.0 * zz - xx - yy);
-    basis[7] = kShC2[3] * xz;
-    basis[8] = kShC2[4] * (xx - yy);
-    if (degree >= 3) {
-      basis[9] = kShC3[0] * y * (3.0 * xx - yy);
-      basis[10] = kShC3[1] * xy * z;
-      basis[11] = kShC3[2] * y * (4.0 * zz - xx - yy);
-      basis[12] = kShC3[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
-      basis[13] = kShC3[4] * x * (4.0 * zz - xx - yy);
-      basis[14] = kShC3[5] * z * (xx - yy);
-      basis[15] = kShC3[6] * x * (xx - 3.0 * yy);
+  double basis[C];
+  basis[0] = kShC0;
+  if (C >= 4) {
+    basis[1] = degree >= 1 ? -kShC1 * y : 0.0;
+    basis[2] = degree >= 1 ? kShC1 * z : 0.0;
+    basis[3] = degree >= 1 ? -kShC1 * x : 0.0;
+  }
+  if (C >= 9) {
+    const double xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    const bool on = degree >= 2;
+    basis[4] = on ? kShC2[0] * xy : 0.0;
+    basis[5] = on ? kShC2[1] * yz : 0.0;
+    basis[6] = on ? kShC2[2] * (2.0 * zz - xx - yy) : 0.0;
+    basis[7] = on ? kShC2[3] * xz : 0.0;
+    basis[8] = on ? kShC2[4] * (xx - yy) : 0.0;
+    if (C >= 16) {
+      const bool on3 = degree >= 3;
+      basis[9] = on3 ? kShC3[0] * y * (3.0 * xx - yy) : 0.0;
+      basis[10] = on3 ? kShC3[1] * xy * z : 0.0;
+      basis[11] = on3 ? kShC3[2] * y * (4.0 * zz - xx - yy) : 0.0;
+      basis[12] = on3 ? kShC3[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy) : 0.0;
+      basis[13] = on3 ? kShC3[4] * x * (4.0 * zz - xx - yy) : 0.0;
+      basis[14] = on3 ? kShC3[5] * z * (xx - yy) : 0.0;
+      basis[15] = on3 ? kShC3[6] * x * (xx - 3.0 * yy) : 0.0;
     }
   }
-  const int nb = (degree + 1) * (degree + 1);
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) {
     double acc = 0.0;
-    const float* cr = row + ch * C;
-    for (int n = 0; n < nb; ++n) acc += (double)__ldg(cr + n) * basis[n];
-    double v = 0.5 + acc;
+#pragma unroll
+    for (int n = 0; n < C; ++n) acc += (double)co[ch * C + n] * basis[n];
+    const double v = 0.5 + acc;
     out[ch] = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+  }
+}
+
+__device__ __forceinline__ void sh_colour(const float* row, int C, int degree, double x, double y,
+                                          double z, double out[3]) {
+  switch (C) {
+    case 16: sh_colour_t<16>(row, degree, x, y, z, out); break;
+    case 9: sh_colour_t<9>(row, degree, x, y, z, out); break;
+    case 4: sh_colour_t<4>(row, degree, x, y, z, out); break;
+    default: sh_colour_t<1>(row, degree, x, y, z, out); break;
   }
 }
 
@@ -185,7 +208,7 @@ constexpr int kProjThreads = 256;
 // Single-pass projection + stable compaction.  Every output array is written
 // once, in compact (ascending assembled-index) order; the depth sort then
 // only permutes (key, compact index) pairs and nothing is gathered again.
-__global__ void __launch_bounds__(kProjThreads)
+__global__ void __launch_bounds__(kProjThreads, 3)
 k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
           DevStats* __restrict__ stats, cs_camera cam, cs_settings st,
           uint64_t* __restrict__ status, ProjOutputs po_out, const uint64_t* __restrict__ list) {
@@ -279,6 +302,7 @@ k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
     h.bx1 = h.by1 = -1;
   }
   po_out.hot[idx] = h;
+  po_out.boxes[idx] = make_short4(h.bx0, h.bx1, h.by0, h.by1);
   // tile rectangle exactly as numpy (render.py:226-231): floor, astype(int64), clip
   {
     const int64_t ntx = (cam.width + st.tile_size - 1) / st.tile_size;
