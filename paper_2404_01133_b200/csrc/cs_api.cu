@@ -53,7 +53,8 @@ void launch_pair_count(const uint32_t* order, const int4* rects, DevStats* stats
 void launch_duplicate(const int64_t* pair_off, const uint32_t* order, const int4* rects,
                       const DevStats* stats, int ntx, int64_t pair_cap, uint32_t* keys,
                       uint32_t* vals, cudaStream_t s);
-void launch_tile_ranges(const uint32_t* keys, const DevStats* stats, uint2* ranges,
+void launch_tile_ranges(const uint32_t* keys, const uint32_t* vals, const short4* boxes,
+                        const DevStats* stats, uint2* ranges, uint32_t* bxs, uint32_t* bys,
                         cudaStream_t s);
 void launch_dump_projected(const uint32_t* order, const ProjRec* recs, const DevStats* stats,
                            double* means, double* conics, double* covs, double* depths,
@@ -65,14 +66,14 @@ void launch_dump_tiles(const uint32_t* order, const uint32_t* vals, const uint2*
 // cs_blend.cu
 int blend_ppt(int tile_size);
 void launch_tile_order(const uint2* ranges, int n_tiles, uint32_t* order, cudaStream_t s);
-void launch_blend(int n_tiles, const uint32_t* list, const uint2* ranges, const HotRec* hot,
-                  const short4* boxes, const uint32_t* order, const BlendParams& bp, void* out,
-                  bool f64_out,
-                  int32_t* frag_tile, DevStats* stats, const BlendState* keep, cudaStream_t s);
+void launch_blend(int n_tiles, const uint32_t* list, const uint32_t* bxs, const uint32_t* bys,
+                  const uint2* ranges, const HotRec* hot, const uint32_t* order,
+                  const BlendParams& bp, void* out, bool f64_out, int32_t* frag_tile,
+                  DevStats* stats, const BlendState* keep, cudaStream_t s);
 void launch_pack(int64_t m, const double* means, const double* conics, const double* colors,
-                 const double* opac, double alpha_floor, HotRec* hot, short4* boxes, int64_t p,
+                 const double* opac, double alpha_floor, HotRec* hot, int64_t p,
                  const int64_t* tile_ids, int64_t n_tiles, const int64_t* offsets, uint32_t* list,
-                 uint2* ranges, cudaStream_t s);
+                 uint32_t* bxs, uint32_t* bys, uint2* ranges, cudaStream_t s);
 // cs_fuse.cu
 void launch_block_of_points(int64_t n, const void* pos, int f32, const double* pmin,
                             const double* pmax, int nx, int ny, int nz, int32_t* out,
@@ -464,7 +465,10 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
   mark(c, 6, s);
   // K8: tile ranges
   CS_CUDA(cudaMemsetAsync(c->ranges.p, 0, sizeof(uint2) * n_tiles, s));
-  launch_tile_ranges(tkeys, stats, c->ranges.as<uint2>(), s);
+  // the sort's other (key, value) buffers are free now: they take the pair-major boxes
+  uint32_t* bxs = which2 ? c->pkA.as<uint32_t>() : c->pkB.as<uint32_t>();
+  uint32_t* bys = which2 ? c->pvA.as<uint32_t>() : c->pvB.as<uint32_t>();
+  launch_tile_ranges(tkeys, tvals, c->boxes.as<short4>(), stats, c->ranges.as<uint2>(), bxs, bys, s);
   CS_CHECK_LAUNCH();
   mark(c, 7, s);
   // K9: blend
@@ -486,7 +490,7 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
   }
   launch_tile_order(c->ranges.as<uint2>(), n_tiles, c->tile_order.as<uint32_t>(), s);
   CS_CHECK_LAUNCH();
-  launch_blend(n_tiles, tvals, c->ranges.as<uint2>(), c->hot.as<HotRec>(), c->boxes.as<short4>(),
+  launch_blend(n_tiles, tvals, bxs, bys, c->ranges.as<uint2>(), c->hot.as<HotRec>(),
                c->tile_order.as<uint32_t>(),
                bp, out, (flags & CS_RENDER_F64_OUT) != 0, c->frag_tile.as<int32_t>(), stats,
                (flags & CS_RENDER_KEEP_STATE) ? &keep : nullptr, s);
@@ -793,19 +797,20 @@ int cs_blend_tiles(cs_ctx* c, const int64_t* tile_ids, const int64_t* tile_offse
   CS_CUDA(cudaMemcpyAsync(bg, background, 24, cudaMemcpyDeviceToHost, s));
   CS_CUDA(cudaStreamSynchronize(s));
   const int64_t m = std::max<int64_t>(n_splats, 1);
-  if (c->scratch1.ensure((sizeof(HotRec) + 8) * m) ||
-      c->scratch2.ensure(4 * std::max<int64_t>(P, 1) + sizeof(uint2) * n_tiles + 4 * n_tiles) ||
+  if (c->scratch1.ensure(sizeof(HotRec) * m) ||
+      c->scratch2.ensure(12 * std::max<int64_t>(P, 1) + sizeof(uint2) * n_tiles + 4 * n_tiles + 8) ||
       c->stats.ensure(sizeof(DevStats)))
     return fail(CS_ENOMEM, "blend scratch");
   HotRec* hot = c->scratch1.as<HotRec>();
   uint32_t* list = c->scratch2.as<uint32_t>();
-  uint2* ranges = reinterpret_cast<uint2*>(list + std::max<int64_t>(P, 1) + (P & 1 ? 0 : 0));
+  uint32_t* pbx = list + std::max<int64_t>(P, 1);
+  uint32_t* pby = pbx + std::max<int64_t>(P, 1);
+  uint2* ranges = reinterpret_cast<uint2*>(pby + std::max<int64_t>(P, 1));
   // keep uint2 8-byte aligned
   ranges = reinterpret_cast<uint2*>((reinterpret_cast<uintptr_t>(ranges) + 7) & ~uintptr_t(7));
   int32_t* ftile = reinterpret_cast<int32_t*>(ranges + n_tiles);
-  short4* pboxes = reinterpret_cast<short4*>(hot + m);
-  launch_pack(n_splats, means, conics, colors, opacities, alpha_floor, hot, pboxes, P, tile_ids,
-              n_tiles, tile_offsets, list, ranges, s);
+  launch_pack(n_splats, means, conics, colors, opacities, alpha_floor, hot, P, tile_ids,
+              n_tiles, tile_offsets, list, pbx, pby, ranges, s);
   CS_CHECK_LAUNCH();
   CS_CUDA(cudaMemsetAsync(c->stats.p, 0, sizeof(DevStats), s));
   BlendParams bp;
@@ -817,7 +822,7 @@ int cs_blend_tiles(cs_ctx* c, const int64_t* tile_ids, const int64_t* tile_offse
   bp.height = height;
   bp.ntx = n_tiles_x;
   bp.flags = CS_RENDER_NO_CLIP;
-  launch_blend((int)n_tiles, list, ranges, hot, pboxes, nullptr, bp, out, true, ftile, c->stats.as<DevStats>(),
+  launch_blend((int)n_tiles, list, pbx, pby, ranges, hot, nullptr, bp, out, true, ftile, c->stats.as<DevStats>(),
                nullptr, s);
   CS_CHECK_LAUNCH();
   // fragments: int32 per tile -> int64

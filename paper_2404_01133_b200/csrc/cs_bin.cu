@@ -104,15 +104,22 @@ k_duplicate(const int64_t* __restrict__ pair_off, const uint32_t* __restrict__ o
   }
 }
 
-// CSR tile ranges from the tile-sorted keys (render.py:247-248).
-__global__ void k_tile_ranges(const uint32_t* __restrict__ keys, const DevStats* __restrict__ stats,
-                              uint2* __restrict__ ranges) {
+// CSR tile ranges from the tile-sorted keys (render.py:247-248), and the
+// pair-major cull boxes the blend tests (boxes[vals[p]] split into one u32 per
+// axis, so a warp's 32 box reads are two coalesced 128-byte loads).
+__global__ void k_tile_ranges(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                              const uint2* __restrict__ boxes, const DevStats* __restrict__ stats,
+                              uint2* __restrict__ ranges, uint32_t* __restrict__ bxs,
+                              uint32_t* __restrict__ bys) {
   const int64_t P = stats->pairs_eff;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P; p += stride) {
     const uint32_t t = keys[p];
     if (p == 0 || keys[p - 1] != t) ranges[t].x = (uint32_t)p;
     if (p == P - 1 || keys[p + 1] != t) ranges[t].y = (uint32_t)(p + 1);
+    const uint2 b = __ldg(boxes + __ldg(vals + p));  // short4 (x0, x1, y0, y1)
+    bxs[p] = b.x;
+    bys[p] = b.y;
   }
 }
 
@@ -133,9 +140,11 @@ void launch_duplicate(const int64_t* pair_off, const uint32_t* order, const int4
                                                        vals);
 }
 
-void launch_tile_ranges(const uint32_t* keys, const DevStats* stats, uint2* ranges,
+void launch_tile_ranges(const uint32_t* keys, const uint32_t* vals, const short4* boxes,
+                        const DevStats* stats, uint2* ranges, uint32_t* bxs, uint32_t* bys,
                         cudaStream_t s) {
-  k_tile_ranges<<<148 * 8, 256, 0, s>>>(keys, stats, ranges);
+  k_tile_ranges<<<148 * 8, 256, 0, s>>>(keys, vals, reinterpret_cast<const uint2*>(boxes), stats,
+                                        ranges, bxs, bys);
 }
 
 // ---------------------------------------------------------------------------

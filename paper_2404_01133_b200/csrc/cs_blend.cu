@@ -29,6 +29,14 @@ namespace cs {
 constexpr int kBlendThreads = 256;
 constexpr int kBatch = 256;
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // local pixel index (0..ts*ts-1) of thread `tid`, pixel slot q.  When the
 // tile side is a multiple of 8, warps own 8x4 pixel boxes (box index
 // warp + 8q, row-major over the tile's (ts/8) x (ts/4) boxes).
@@ -42,18 +50,23 @@ __device__ __forceinline__ int local_pixel(int tid, int q, int ts) {
 }
 
 // Warp-independent blend: each warp walks the tile's depth-ordered list on
-// its own (no block barriers).  Per round of 32 list entries each lane
-// fetches one splat's 8-byte cull box (dense array, L2-resident) and tests it
-// against the warp's pixel box; __ballot_sync compacts the hits and the warp
-// then evaluates each hit for its 32 pixels, reading the 80-byte HotRec with a
-// warp-uniform (broadcast) load.  A warp stops as soon as its 32 pixels have
-// terminated.
+// its own (no block barriers).  Per round of 32 list entries each lane reads
+// one entry's compact id and packed cull box -- pair-major arrays written by
+// K8, so the reads are coalesced and shared by the CTA's 8 warps through L1 --
+// and tests the box against the warp's pixel box; __ballot_sync compacts the
+// hits and each hitting lane cp.async-copies its splat's 80-byte HotRec into
+// the warp's shared-memory slot.  The copies of round r are in flight while
+// the warp evaluates round r-1 (two stages per warp), so HotRec latency is
+// paid once per 32 entries, not once per evaluation.  A warp stops as soon as
+// its 32 pixels have terminated.
 template <int PPT, typename OutT, bool KEEP>
 __global__ void __launch_bounds__(kBlendThreads)
-k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
-        const HotRec* __restrict__ hot, const short4* __restrict__ boxes,
-        const uint32_t* __restrict__ tile_order, BlendParams bp, OutT* __restrict__ out,
-        int32_t* __restrict__ frag_tile, DevStats* __restrict__ stats, BlendState state) {
+k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
+        const uint32_t* __restrict__ bys, const uint2* __restrict__ ranges,
+        const HotRec* __restrict__ hot, const uint32_t* __restrict__ tile_order, BlendParams bp,
+        OutT* __restrict__ out, int32_t* __restrict__ frag_tile, DevStats* __restrict__ stats,
+        BlendState state) {
+  __shared__ __align__(16) HotRec s_hot[kBlendThreads / 32][2][32];
   __shared__ int s_red[kBlendThreads / 32];
   __shared__ long long s_ev[kBlendThreads / 32];
   const int t = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
@@ -62,6 +75,8 @@ k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
   const uint2 rg = ranges[t];
   const int64_t s0 = rg.x, s1 = rg.y;
   const uint32_t lane = lane_id();
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  HotRec (*wbuf)[32] = s_hot[threadIdx.x >> 5];
   int my_frag = 0;
   long long evals = 0;
 #pragma unroll 1
@@ -84,29 +99,16 @@ k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
     int cnt = 0;
     int64_t last = s0;
     bool done = !valid;
-    // software-pipelined fetch of (id, box) for the next round of 32 entries
-    uint32_t nid = 0;
-    short4 nbx = make_short4(32000, -1, 32000, -1);
-    if (s0 + lane < s1) {
-      nid = __ldg(list + s0 + lane);
-      nbx = __ldg(boxes + nid);
-    }
-    for (int64_t k0 = s0; k0 < s1; k0 += 32) {
-      const uint32_t id = nid;
-      const short4 bx = nbx;
-      if (k0 + 32 + lane < s1) {
-        nid = __ldg(list + k0 + 32 + lane);
-        nbx = __ldg(boxes + nid);
-      }
-      const bool hit = !(bx.x > x1 || bx.y < x0 || bx.z > y1 || bx.w < y0);
-      uint32_t mask = __ballot_sync(0xffffffffu, hit);
+
+    // one staged round: evaluate its hits (slots 0..popc-1) for this lane's pixel
+    auto eval_round = [&](const HotRec* buf, uint32_t mask, int64_t k0) {
+      int slot = 0;
       while (mask) {
         const int src = __ffs(mask) - 1;
         mask &= mask - 1;
-        const uint32_t jid = __shfl_sync(0xffffffffu, id, src);
+        const HotRec& h = buf[slot++];
         if (done) continue;
         ++evals;
-        const HotRec h = hot[jid];
         const double dx = dsub(sx, h.mx);
         const double dy = dsub(sy, h.my);
         // -0.5 * (c0*dx*dx + c2*dy*dy) - c1*dx*dy   (_kernels.py:54-57)
@@ -127,8 +129,55 @@ k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
         cnt += 1;
         last = k0 + src + 1;
       }
-      if (__all_sync(0xffffffffu, done)) break;
+    };
+
+    // software-pipelined (id, box) for the next round of 32 entries
+    uint32_t nid = 0, nbx = kEmptyBox, nby = kEmptyBox;
+    if (s0 + lane < s1) {
+      nid = __ldg(list + s0 + lane);
+      nbx = __ldg(bxs + s0 + lane);
+      nby = __ldg(bys + s0 + lane);
     }
+    uint32_t pmask = 0;
+    int64_t pk0 = 0;
+    int stage = 0;
+    bool alldone = false;
+    for (int64_t k0 = s0; k0 < s1; k0 += 32) {
+      const uint32_t id = nid, bx = nbx, by = nby;
+      if (k0 + 32 + lane < s1) {
+        nid = __ldg(list + k0 + 32 + lane);
+        nbx = __ldg(bxs + k0 + 32 + lane);
+        nby = __ldg(bys + k0 + 32 + lane);
+      } else {
+        nbx = nby = kEmptyBox;
+      }
+      const int bx0 = (int)(int16_t)(bx & 0xffffu), bx1 = (int)(int16_t)(bx >> 16);
+      const int by0 = (int)(int16_t)(by & 0xffffu), by1 = (int)(int16_t)(by >> 16);
+      const bool hit = !(bx0 > x1 || bx1 < x0 || by0 > y1 || by1 < y0);
+      const uint32_t mask = __ballot_sync(0xffffffffu, hit);
+      if (!mask) continue;
+      if (hit) {
+        const char* g = reinterpret_cast<const char*>(hot + id);
+        char* d = reinterpret_cast<char*>(&wbuf[stage][__popc(mask & lt_mask)]);
+#pragma unroll
+        for (int c = 0; c < 5; ++c) cp_async16(d + 16 * c, g + 16 * c);
+      }
+      cp_async_commit();
+      if (pmask) {
+        cp_async_wait<1>();
+        __syncwarp();
+        eval_round(wbuf[stage ^ 1], pmask, pk0);
+        __syncwarp();
+        if (__all_sync(0xffffffffu, done)) { alldone = true; break; }
+      }
+      pmask = mask;
+      pk0 = k0;
+      stage ^= 1;
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+    if (pmask && !alldone) eval_round(wbuf[stage ^ 1], pmask, pk0);
+    __syncwarp();
     if (valid) {
       my_frag += cnt;
       const int64_t pix = (int64_t)py * bp.width + px;
@@ -168,20 +217,19 @@ k_blend(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
 }
 
 template <typename OutT, bool KEEP>
-static void launch_blend_t(int ppt, int n_tiles, const uint32_t* list, const uint2* ranges,
-                           const HotRec* hot, const short4* boxes, const uint32_t* order,
-                           const BlendParams& bp,
-                           OutT* out, int32_t* frag_tile, DevStats* stats, BlendState st,
-                           cudaStream_t s) {
+static void launch_blend_t(int ppt, int n_tiles, const uint32_t* list, const uint32_t* bxs,
+                           const uint32_t* bys, const uint2* ranges, const HotRec* hot,
+                           const uint32_t* order, const BlendParams& bp, OutT* out,
+                           int32_t* frag_tile, DevStats* stats, BlendState st, cudaStream_t s) {
   if (ppt == 1)
-    k_blend<1, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, ranges, hot, boxes, order, bp, out,
-                                                            frag_tile, stats, st);
+    k_blend<1, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, bxs, bys, ranges, hot, order, bp,
+                                                            out, frag_tile, stats, st);
   else if (ppt == 4)
-    k_blend<4, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, ranges, hot, boxes, order, bp, out,
-                                                            frag_tile, stats, st);
+    k_blend<4, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, bxs, bys, ranges, hot, order, bp,
+                                                            out, frag_tile, stats, st);
   else
-    k_blend<16, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, ranges, hot, boxes, order, bp, out,
-                                                             frag_tile, stats, st);
+    k_blend<16, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, bxs, bys, ranges, hot, order, bp,
+                                                             out, frag_tile, stats, st);
 }
 
 // K8b: heaviest-first tile order.  Tiles are bucketed by floor(log2(list
@@ -222,18 +270,18 @@ int blend_ppt(int tile_size) {
   return 0;
 }
 
-void launch_blend(int n_tiles, const uint32_t* list, const uint2* ranges, const HotRec* hot,
-                  const short4* boxes, const uint32_t* order, const BlendParams& bp, void* out,
-                  bool f64_out,
-                  int32_t* frag_tile, DevStats* stats, const BlendState* keep, cudaStream_t s) {
+void launch_blend(int n_tiles, const uint32_t* list, const uint32_t* bxs, const uint32_t* bys,
+                  const uint2* ranges, const HotRec* hot, const uint32_t* order,
+                  const BlendParams& bp, void* out, bool f64_out, int32_t* frag_tile,
+                  DevStats* stats, const BlendState* keep, cudaStream_t s) {
   const int ppt = blend_ppt(bp.tile_size);
   BlendState st = keep ? *keep : BlendState{nullptr, nullptr, nullptr};
   if (f64_out) {
-    if (keep) launch_blend_t<double, true>(ppt, n_tiles, list, ranges, hot, boxes, order, bp, (double*)out, frag_tile, stats, st, s);
-    else launch_blend_t<double, false>(ppt, n_tiles, list, ranges, hot, boxes, order, bp, (double*)out, frag_tile, stats, st, s);
+    if (keep) launch_blend_t<double, true>(ppt, n_tiles, list, bxs, bys, ranges, hot, order, bp, (double*)out, frag_tile, stats, st, s);
+    else launch_blend_t<double, false>(ppt, n_tiles, list, bxs, bys, ranges, hot, order, bp, (double*)out, frag_tile, stats, st, s);
   } else {
-    if (keep) launch_blend_t<float, true>(ppt, n_tiles, list, ranges, hot, boxes, order, bp, (float*)out, frag_tile, stats, st, s);
-    else launch_blend_t<float, false>(ppt, n_tiles, list, ranges, hot, boxes, order, bp, (float*)out, frag_tile, stats, st, s);
+    if (keep) launch_blend_t<float, true>(ppt, n_tiles, list, bxs, bys, ranges, hot, order, bp, (float*)out, frag_tile, stats, st, s);
+    else launch_blend_t<float, false>(ppt, n_tiles, list, bxs, bys, ranges, hot, order, bp, (float*)out, frag_tile, stats, st, s);
   }
 }
 
@@ -245,7 +293,7 @@ void launch_blend(int n_tiles, const uint32_t* list, const uint2* ranges, const 
 
 __global__ void k_pack_records(int64_t m, const double* means, const double* conics,
                                const double* colors, const double* opac, double alpha_floor,
-                               HotRec* hot, short4* boxes) {
+                               HotRec* hot) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m;
        s += (int64_t)gridDim.x * blockDim.x) {
     HotRec h;
@@ -262,26 +310,30 @@ __global__ void k_pack_records(int64_t m, const double* means, const double* con
     h.bx0 = h.by0 = -1;     // full-image box
     h.bx1 = h.by1 = 32000;
     hot[s] = h;
-    boxes[s] = make_short4(h.bx0, h.bx1, h.by0, h.by1);
   }
 }
 
 __global__ void k_pack_tiles(int64_t p, const int64_t* tile_ids, int64_t n_tiles,
-                             const int64_t* offsets, uint32_t* list, uint2* ranges) {
+                             const int64_t* offsets, uint32_t* list, uint32_t* bxs, uint32_t* bys,
+                             uint2* ranges) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p; i += stride)
+  const uint32_t full = pack_box(-1, 32000);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p; i += stride) {
     list[i] = (uint32_t)tile_ids[i];
+    bxs[i] = full;
+    bys[i] = full;
+  }
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_tiles; t += stride)
     ranges[t] = make_uint2((uint32_t)offsets[t], (uint32_t)offsets[t + 1]);
 }
 
 void launch_pack(int64_t m, const double* means, const double* conics, const double* colors,
-                 const double* opac, double alpha_floor, HotRec* hot, short4* boxes, int64_t p,
+                 const double* opac, double alpha_floor, HotRec* hot, int64_t p,
                  const int64_t* tile_ids, int64_t n_tiles, const int64_t* offsets, uint32_t* list,
-                 uint2* ranges, cudaStream_t s) {
+                 uint32_t* bxs, uint32_t* bys, uint2* ranges, cudaStream_t s) {
   if (m > 0)
-    k_pack_records<<<148 * 4, 256, 0, s>>>(m, means, conics, colors, opac, alpha_floor, hot, boxes);
-  k_pack_tiles<<<148 * 4, 256, 0, s>>>(p, tile_ids, n_tiles, offsets, list, ranges);
+    k_pack_records<<<148 * 4, 256, 0, s>>>(m, means, conics, colors, opac, alpha_floor, hot);
+  k_pack_tiles<<<148 * 4, 256, 0, s>>>(p, tile_ids, n_tiles, offsets, list, bxs, bys, ranges);
 }
 
 }  // namespace cs

@@ -57,6 +57,13 @@ struct __align__(16) HotRec {   // everything the blend reads per splat (80 B)
 };
 static_assert(sizeof(HotRec) == 80, "HotRec layout");
 
+// pair-major cull boxes for the blend: (lo | hi << 16) as two int16, one word
+// per axis; kEmptyBox = (32767, -32768) never intersects
+__host__ __device__ __forceinline__ uint32_t pack_box(int lo, int hi) {
+  return (uint32_t)(uint16_t)(int16_t)lo | ((uint32_t)(uint16_t)(int16_t)hi << 16);
+}
+constexpr uint32_t kEmptyBox = 0x7fffu | (0x8000u << 16);
+
 struct DevStats {     // device mirror of cs_frame_stats + scratch counters
   int64_t assembled;
   int64_t visible;
