@@ -59,6 +59,10 @@ def parse():
     ap.add_argument("--frames-per-altitude", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-train", action="store_true", help="skip the block-training leg (C4)")
+    ap.add_argument("--train-steps", type=int, default=72, help="timed block iterations per rank")
+    ap.add_argument("--train-warmup", type=int, default=36)
+    ap.add_argument("--train-views", type=int, default=4)
     ap.add_argument("--seed", type=int, default=0)
     return ap.parse_args()
 
@@ -67,7 +71,7 @@ def parse():
 # scene
 
 
-def build_scene(name: str, seed: int, dev):
+def build_scene(name: str, seed: int, dev, keep_raw: bool = False):
     import torch
     from paper_2404_01133_b200 import lodgen
     from paper_2404_01133_b200.synth import city_cameras, generate_city_torch, orbit_cameras
@@ -84,9 +88,10 @@ def build_scene(name: str, seed: int, dev):
     hi = pos.double().max(dim=0).values.cpu().numpy()
     center = 0.5 * (lo + hi)
     radius = 0.5 * max(hi[0] - lo[0], hi[1] - lo[1])
+    raw = (pos, op, sc, q, sh, mem, int(np.prod(dims))) if keep_raw else None
     del pos, op, sc, q, sh, mem
     torch.cuda.empty_cache()
-    return scene, center, radius, alts, (W, H), time.perf_counter() - t0
+    return scene, center, radius, alts, (W, H), time.perf_counter() - t0, raw
 
 
 def flythrough(center, radius, alts, wh, per_alt):
@@ -187,7 +192,8 @@ def main():
     from paper_2404_01133_b200 import _lib, device
     from paper_2404_01133_b200._lib import CsFrameStats, CsSource
 
-    scene, center, radius, alts, wh, build_s = build_scene(args.scene, args.seed, dev)
+    scene, center, radius, alts, wh, build_s, raw = build_scene(args.scene, args.seed, dev,
+                                                                keep_raw=not args.no_train)
     cams_all = flythrough(center, radius, alts, wh, args.frames_per_altitude)
     # view split: rank r renders its contiguous share of the flythrough, cycling
     share = [cams_all[i] for i in range(len(cams_all)) if i * world // len(cams_all) == rank] or cams_all
@@ -309,6 +315,13 @@ def main():
                 "peak_source": "nominal 148 SM x 64 DFMA/clk at the sampled SM clock"}
     roof["stage_bytes_per_frame"] = {k: v / K for k, v in bytes_.items()}
 
+    train = None
+    if not args.no_train:
+        del scene
+        torch.cuda.empty_cache()
+        train = train_leg(args, raw, wh, rank, world, dev)
+        raw = None
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(scene, cams_all, settings, n_frames=1)
@@ -331,12 +344,94 @@ def main():
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "train": train,
             "gpu_launches": K * launches_per_frame(),
             "clocks": clocks,
         }
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def train_leg(args, raw, wh, rank, world, dev):
+    """C4: block-parallel training iterations/s (+ the NCCL fusion all-gather).
+
+    Every rank builds the same scene, takes its LPT share of the 36 blocks and
+    runs them round-robin; one step = one block iteration (fwd + loss + bwd +
+    Adam on one 1080p view).  value = all ranks' iterations / max rank time.
+    """
+    import torch
+    import torch.distributed as dist
+    from paper_2404_01133_b200 import blocktrain, fusion
+    from paper_2404_01133_b200.lodgen import central_third
+    pos, op, sc, q, sh, mem, n_blocks = raw
+    counts = blocktrain.block_counts(mem, n_blocks)
+    owner = blocktrain.assign_blocks(mem, n_blocks, world)
+    owned = [j for j in range(n_blocks) if owner[j] == rank and counts[j] > 0]
+    t0 = time.perf_counter()
+    jobs = blocktrain.setup_blocks(pos, op, sc, q, sh, mem, owned, wh[0], wh[1],
+                                   n_views=args.train_views, seed=args.seed)
+    pmin, pmax = central_third(pos)
+    dims = SCENES[args.scene][3]
+    del pos, op, sc, q, sh
+    torch.cuda.empty_cache()
+    setup_s = time.perf_counter() - t0
+    order = [jobs[j] for j in owned if j in jobs]
+    stream = torch.cuda.current_stream(dev)
+    for i in range(args.train_warmup):
+        order[i % len(order)].step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    K = args.train_steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(K)]
+    losses = []
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(K):
+        job = order[i % len(order)]
+        v = job.iters % len(job.cams)
+        job.iters += 1
+        losses.append(job.trainer.step(job.cams[v], job.targets[v], events=ev[i]))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    phases = {"forward": 0.0, "loss": 0.0, "backward": 0.0, "adam": 0.0}
+    for e in ev:
+        for k, (a, b) in zip(phases, ((0, 1), (1, 2), (2, 3), (3, 4))):
+            phases[k] += e[a].elapsed_time(e[b]) / K
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    # fusion: every rank filters its blocks; NCCL all-gather-v in block order
+    local = {j: jb.fusion_inputs() for j, jb in jobs.items()}
+    fuse_ms = None
+    fused_n = None
+    if world > 1:
+        dist.barrier()
+        torch.cuda.synchronize()
+        f0 = time.perf_counter()
+        fused = fusion.fuse_all_gather(local, n_blocks, owner, pmin, pmax, dims, sh_coeffs=16)
+        torch.cuda.synchronize()
+        fuse_ms = 1000 * (time.perf_counter() - f0)
+        fused_n = int(fused.shape[0])
+    sizes = [jobs[j].count for j in jobs]
+    return {
+        "metric": "block-train iters/s (C4)", "value": world * K / (ms_max / 1000.0), "unit": "iters/s",
+        "ms_per_iter": ms_max / K, "steps": K, "warmup": args.train_warmup, "n_gpus": world,
+        "scaling": "weak", "phases_ms": phases,
+        "loss_first_last": [float(losses[0]), float(losses[-1])],
+        "config": {"workload": f"{n_blocks} blocks of the {args.scene} scene (LPT over ranks), "
+                               f"{args.train_views} orbit views/block at {wh[0]}x{wh[1]}",
+                   "blocks_this_rank": len(order),
+                   "gaussians_per_block_min_med_max": [min(sizes), int(np.median(sizes)), max(sizes)]
+                   if sizes else None,
+                   "setup_s": round(setup_s, 1)},
+        "fusion_all_gather_ms": fuse_ms, "fused_gaussians": fused_n,
+    }
 
 
 def launches_per_frame() -> int:
@@ -392,7 +487,7 @@ def run_reference(args, rank, world):
     import torch
     torch.cuda.set_device(0)
     import paper_2404_01133_b200 as cs
-    scene, center, radius, alts, wh, build_s = build_scene(args.scene, args.seed, torch.device("cuda", 0))
+    scene, center, radius, alts, wh, build_s, _ = build_scene(args.scene, args.seed, torch.device("cuda", 0))
     cams = flythrough(center, radius, alts, wh, args.frames_per_altitude)
     from oracle import oracle as O
     hs = host_scene(scene)

@@ -229,6 +229,36 @@ int cs_build_covariances(cs_ctx* ctx, int64_t n, const double* scales, const dou
 int cs_sh_to_colors(cs_ctx* ctx, int64_t n, const double* sh, int32_t coeffs,
                     const double* dirs, int32_t degree, double* out, void* stream);
 
+/* ---- block training (the reference has no backward) ---
+ * Training loss of metrics.py:121-125, (1-lam)*L1 + lam*(1-SSIM) with the
+ * valid-region 11x11 Gaussian-window SSIM of metrics.py:70-95, and its
+ * gradient.  img, ref, grad_out: device (H,W,3) float32; loss_out: device
+ * double[1].  H, W >= 11 (metrics.py:80-81), else CS_EINVAL. */
+int cs_training_loss(cs_ctx* ctx, const float* img, const float* ref, int32_t height,
+                     int32_t width, double lam, double* loss_out, float* grad_out, void* stream);
+/* Adam hyper-parameters (torch.optim.Adam semantics, bias-corrected; step is
+ * the 1-based step count after this update).  Learning rates per parameter
+ * group; the manifest scales (partition.py:45-50) are applied by the caller. */
+typedef struct cs_adam_hparams {
+  float lr_position, lr_scale, lr_rotation, lr_opacity, lr_sh;
+  float beta1, beta2, eps;
+  int32_t step;
+  int32_t reserved;
+} cs_adam_hparams;
+/* One Adam step of a block's raw parameters with the PLY activations
+ * (ply.py:108-123: exp scale, sigmoid opacity, normalised quaternion).
+ * geom: device (K,11) float32 rows [x,y,z, log s0..2, q w,x,y,z (raw), logit o];
+ * geom_m/geom_v its Adam moments; sh (K,3C) float32 and its moments.
+ * grads: cs_render_backward's output for the activated parameters.
+ * Writes the activated (K,4) float32 quads pos_op/scale/quat that a cs_cloud
+ * with sh_stride = 3C (C = 4 or 16) reads for the next forward. */
+int cs_block_adam(cs_ctx* ctx, int64_t K, int32_t sh_coeffs, float* geom, float* geom_m,
+                  float* geom_v, float* sh, float* sh_m, float* sh_v, const cs_grads* grads,
+                  const cs_adam_hparams* hp, float* pos_op, float* scale, float* quat,
+                  void* stream);
+/* The activated quads of geom without an update (first forward). */
+int cs_block_activate(cs_ctx* ctx, int64_t K, const float* geom, float* pos_op, float* scale,
+                      float* quat, void* stream);
 /* ---- fusion (partition.py:570-587) ---------------------------------------
  * Block membership of n positions: normalize_position (partition.py:110-114)
  * -> contract (partition.py:117-126) -> block_of_points (partition.py:161-169).

@@ -65,6 +65,13 @@ class CsGrads(ctypes.Structure):
     _fields_ = [("positions", vp), ("scales", vp), ("rotations", vp), ("opacities", vp), ("sh", vp)]
 
 
+class CsAdamHparams(ctypes.Structure):
+    _fields_ = [("lr_position", ctypes.c_float), ("lr_scale", ctypes.c_float),
+                ("lr_rotation", ctypes.c_float), ("lr_opacity", ctypes.c_float),
+                ("lr_sh", ctypes.c_float), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float),
+                ("eps", ctypes.c_float), ("step", i32), ("reserved", i32)]
+
+
 class CsSource(ctypes.Structure):
     _fields_ = [("kind", i32), ("force_level", i32), ("cloud", CsCloud), ("lod", vp)]
 
@@ -96,6 +103,10 @@ _SIGS = {
                                       i32, ctypes.c_double, ctypes.c_double, vp, vp, vp]),
     "cs_build_covariances": (ctypes.c_int, [vp, i64, vp, vp, vp, vp]),
     "cs_sh_to_colors": (ctypes.c_int, [vp, i64, vp, i32, vp, i32, vp, vp]),
+    "cs_training_loss": (ctypes.c_int, [vp, vp, vp, i32, i32, ctypes.c_double, vp, vp, vp]),
+    "cs_block_adam": (ctypes.c_int, [vp, i64, i32, vp, vp, vp, vp, vp, vp, ctypes.POINTER(CsGrads),
+                                     ctypes.POINTER(CsAdamHparams), vp, vp, vp, vp]),
+    "cs_block_activate": (ctypes.c_int, [vp, i64, vp, vp, vp, vp, vp]),
     "cs_block_of_points": (ctypes.c_int, [vp, i64, vp, i32, vp, vp, i32, i32, i32, vp, vp]),
     "cs_fuse_filter": (ctypes.c_int, [vp, i64, vp, i32, vp, vp, i32, i32, i32, i32, vp, vp, vp]),
 }

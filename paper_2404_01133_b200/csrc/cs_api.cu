@@ -47,6 +47,14 @@ template <typename K>
 int radix_sort(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_dev, int64_t capacity,
                int begin_bit, int end_bit, uint32_t* hist, uint32_t* status, uint32_t* tickets,
                cudaStream_t s);
+// cs_train.cu
+void launch_training_loss(const float* img, const float* ref, int H, int W, double lam,
+                          float* maps, double* acc, double* loss, float* grad, cudaStream_t s);
+void launch_block_adam(int64_t K, int C, float* geom, float* gm, float* gv, float* sh, float* shm,
+                       float* shv, const cs_grads& g, const cs_adam_hparams& h, float4* pos_op,
+                       float4* scale, float4* quat, cudaStream_t s);
+void launch_activate_geom(int64_t K, const float* geom, float4* pos_op, float4* scale, float4* quat,
+                          cudaStream_t s);
 // cs_bin.cu
 void launch_pair_count(const uint32_t* order, const int4* rects, DevStats* stats, int64_t pair_cap,
                        int64_t capacity, uint64_t* status, int64_t* pair_off, cudaStream_t s);
@@ -82,10 +90,10 @@ void launch_fuse_filter(int64_t n, const void* pos, int f32, const double* pmin,
                         int nx, int ny, int nz, int block, uint64_t* status, uint32_t* ticket,
                         int64_t* kept, int64_t* kept_count, cudaStream_t s);
 // cs_backward.cu
-void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint2* ranges, const HotRec* hot,
-                      const cs_settings& st, int width, int height, int ntx,
-                      const float* dl_dimg, const BlendState& state, float* grads, int64_t cap,
-                      cudaStream_t s);
+void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint32_t* bxs, const uint32_t* bys,
+                      const uint2* ranges, const HotRec* hot, const cs_settings& st, int width,
+                      int height, int ntx, const float* dl_dimg, const BlendState& state,
+                      float* grads, int64_t cap, cudaStream_t s);
 void launch_project_bwd(const cs_cloud& cl, const int64_t* src,
                         const DevStats* stats, const cs_camera& cam, const cs_settings& st,
                         const float* grads, int64_t cap, const cs_grads& out, cudaStream_t s);
@@ -174,12 +182,15 @@ struct cs_ctx {
   DBuf st_t, st_last, st_acc;
   DBuf scratch1, scratch2, scratch3, scratch4;  // API utilities
   DBuf gacc;                                    // per-rank blend-backward partials
+  DBuf loss_maps, loss_acc;                     // cs_training_loss workspace
   cs_frame_stats* h_stats = nullptr;            // pinned
   int64_t cap_vis = 0, cap_pairs = 0, cap_pw = 0, cap_tiles = 0;
   // last frame bookkeeping (for dumps / backward)
   const uint32_t* last_order = nullptr;
   bool last_debug = false;
   const uint32_t* last_list = nullptr;
+  const uint32_t* last_bxs = nullptr;  // pair-major cull boxes of the last frame
+  const uint32_t* last_bys = nullptr;
   const uint2* last_ranges = nullptr;
   int last_tiles = 0;
   int last_width = 0, last_height = 0;
@@ -233,7 +244,7 @@ void cs_destroy(cs_ctx* c) {
                  &c->fuse_ticket, &c->keysA, &c->valsA, &c->keysB, &c->valsB, &c->recs, &c->hot,
                  &c->tile_order, &c->boxes, &c->rects, &c->src, &c->pair_off, &c->pkA, &c->pvA, &c->pkB,
                  &c->pvB, &c->ranges, &c->frag_tile, &c->pw_list, &c->st_t, &c->st_last,
-                 &c->st_acc, &c->gacc, &c->scratch1, &c->scratch2, &c->scratch3, &c->scratch4};
+                 &c->st_acc, &c->gacc, &c->loss_maps, &c->loss_acc, &c->scratch1, &c->scratch2, &c->scratch3, &c->scratch4};
   for (DBuf* b : all) b->release();
   if (c->h_stats) cudaFreeHost(c->h_stats);
   for (cudaEvent_t e : c->tev) cudaEventDestroy(e);
@@ -499,6 +510,8 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
   if (c->timing_on && c->timing_frame < c->timing_max) ++c->timing_frame;
   c->last_order = order;
   c->last_list = tvals;
+  c->last_bxs = bxs;
+  c->last_bys = bys;
   c->last_ranges = c->ranges.as<uint2>();
   c->last_tiles = n_tiles;
   c->last_width = cam->width;
@@ -564,7 +577,8 @@ int cs_render_backward(cs_ctx* c, const cs_source* src, const cs_camera* cam,
   const int ts = st->tile_size;
   const int ntx = (cam->width + ts - 1) / ts;
   BlendState state{c->st_t.as<double>(), c->st_last.as<int32_t>(), c->st_acc.as<double>()};
-  launch_blend_bwd(c->last_tiles, c->last_list, c->last_ranges, c->hot.as<HotRec>(),
+  launch_blend_bwd(c->last_tiles, c->last_list, c->last_bxs, c->last_bys, c->last_ranges,
+                   c->hot.as<HotRec>(),
                    *st, cam->width, cam->height, ntx, dl_dimg, state,
                    c->gacc.as<float>(), cap, s);
   CS_CHECK_LAUNCH();
@@ -576,6 +590,50 @@ int cs_render_backward(cs_ctx* c, const cs_source* src, const cs_camera* cam,
   CS_CUDA(cudaMemsetAsync(out->sh, 0, 12 * (size_t)cl.sh_coeffs * K, s));
   launch_project_bwd(cl, c->src.as<int64_t>(), c->stats.as<DevStats>(), *cam, *st,
                      c->gacc.as<float>(), cap, *out, s);
+  CS_CHECK_LAUNCH();
+  return CS_OK;
+}
+
+int cs_training_loss(cs_ctx* c, const float* img, const float* ref, int32_t height, int32_t width,
+                     double lam, double* loss_out, float* grad_out, void* stream) {
+  if (!c || !img || !ref || !loss_out || !grad_out) return fail(CS_EINVAL, "NULL argument");
+  if (height < 11 || width < 11) return fail(CS_EINVAL, "images must be at least 11x11 for ssim");
+  if (!(lam >= 0.0 && lam <= 1.0)) return fail(CS_EINVAL, "lam must be in [0, 1]");
+  std::lock_guard<std::mutex> lock(c->mu);
+  CS_CUDA(cudaSetDevice(c->device));
+  const size_t maps = (size_t)9 * (height - 10) * (width - 10);
+  if (c->loss_maps.ensure(4 * maps) || c->loss_acc.ensure(16)) return fail(CS_ENOMEM, "loss maps");
+  launch_training_loss(img, ref, height, width, lam, c->loss_maps.as<float>(),
+                       c->loss_acc.as<double>(), loss_out, grad_out, (cudaStream_t)stream);
+  CS_CHECK_LAUNCH();
+  return CS_OK;
+}
+
+int cs_block_adam(cs_ctx* c, int64_t K, int32_t sh_coeffs, float* geom, float* geom_m,
+                  float* geom_v, float* sh, float* sh_m, float* sh_v, const cs_grads* grads,
+                  const cs_adam_hparams* hp, float* pos_op, float* scale, float* quat,
+                  void* stream) {
+  if (!c || !grads || !hp || K < 0) return fail(CS_EINVAL, "bad argument");
+  if (K > 0 && (!geom || !geom_m || !geom_v || !sh || !sh_m || !sh_v || !pos_op || !scale || !quat))
+    return fail(CS_EINVAL, "NULL buffer");
+  if (sh_coeffs != 1 && sh_coeffs != 4 && sh_coeffs != 9 && sh_coeffs != 16)
+    return fail(CS_EINVAL, "sh_coeffs must be 1, 4, 9 or 16");
+  if (hp->step < 1) return fail(CS_EINVAL, "step must be >= 1");
+  CS_CUDA(cudaSetDevice(c->device));
+  launch_block_adam(K, sh_coeffs, geom, geom_m, geom_v, sh, sh_m, sh_v, *grads, *hp,
+                    reinterpret_cast<float4*>(pos_op), reinterpret_cast<float4*>(scale),
+                    reinterpret_cast<float4*>(quat), (cudaStream_t)stream);
+  CS_CHECK_LAUNCH();
+  return CS_OK;
+}
+
+int cs_block_activate(cs_ctx* c, int64_t K, const float* geom, float* pos_op, float* scale,
+                      float* quat, void* stream) {
+  if (!c || K < 0 || (K > 0 && (!geom || !pos_op || !scale || !quat)))
+    return fail(CS_EINVAL, "bad argument");
+  CS_CUDA(cudaSetDevice(c->device));
+  launch_activate_geom(K, geom, reinterpret_cast<float4*>(pos_op), reinterpret_cast<float4*>(scale),
+                       reinterpret_cast<float4*>(quat), (cudaStream_t)stream);
   CS_CHECK_LAUNCH();
   return CS_OK;
 }

@@ -26,7 +26,6 @@
 namespace cs {
 
 constexpr int kBwdThreads = 256;
-constexpr int kBwdBatch = 256;
 constexpr int kGradFields = 9;  // mx, my, c0, c1, c2, opacity, r, g, b
 
 struct BwdParams {
@@ -35,94 +34,160 @@ struct BwdParams {
   int tile_size, width, height, ntx;
 };
 
+// Same warp-independent walk as the forward (cs_blend.cu): per round of 32
+// list entries a coalesced read of (id, packed box), a ballot of the hits
+// against the warp's pixel box, cp.async staging of the hits' HotRecs into
+// the warp's two-stage shared buffer.  A warp walks only up to the largest
+// `last` of its pixels.  Per evaluated hit each lane re-derives the forward's
+// float64 decisions for its pixel; when any lane contributes, the nine
+// partials are warp-reduced and lane 0 adds them with one atomic each.
+template <int PPT>
 __global__ void __launch_bounds__(kBwdThreads)
-k_blend_bwd(const uint32_t* __restrict__ list, const uint2* __restrict__ ranges,
-            const HotRec* __restrict__ hot, BwdParams bp,
-            const float* __restrict__ dl_dimg, BlendState state, float* __restrict__ grads /* [kGradFields][cap] */, int64_t cap) {
-  __shared__ __align__(16) HotRec buf[kBwdBatch];
-  __shared__ int s_any;
+k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
+            const uint32_t* __restrict__ bys, const uint2* __restrict__ ranges,
+            const HotRec* __restrict__ hot, BwdParams bp, const float* __restrict__ dl_dimg,
+            BlendState state, float* __restrict__ grads /* [kGradFields][cap] */, int64_t cap) {
+  __shared__ __align__(16) HotRec s_hot[kBwdThreads / 32][2][32];
   const int t = blockIdx.x;
   const int tx = t % bp.ntx, ty = t / bp.ntx;
   const int ts = bp.tile_size;
   const uint2 rg = ranges[t];
   const int64_t s0 = rg.x, s1 = rg.y;
-  const int li = threadIdx.x;
-  const int px = tx * ts + li % ts, py = ty * ts + li / ts;
-  const bool valid = li < ts * ts && px < bp.width && py < bp.height;
-  double sx = (double)px + 0.5, sy = (double)py + 0.5;
-  int64_t last = s0;
-  double g[3] = {0.0, 0.0, 0.0}, acc[3] = {0.0, 0.0, 0.0}, Tend = 1.0;
-  if (valid) {
-    const int64_t pix = (int64_t)py * bp.width + px;
-    last = state.last[pix];
-    Tend = state.final_t[pix];
+  const uint32_t lane = lane_id();
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  HotRec (*wbuf)[32] = s_hot[threadIdx.x >> 5];
+#pragma unroll 1
+  for (int q = 0; q < PPT; ++q) {
+    const int li = local_pixel(threadIdx.x, q, ts);
+    const int px = tx * ts + li % ts, py = ty * ts + li / ts;
+    const bool valid = li < ts * ts && px < bp.width && py < bp.height;
+    int x0 = valid ? px : 1 << 20, x1 = valid ? px : -(1 << 20);
+    int y0 = valid ? py : 1 << 20, y1 = valid ? py : -(1 << 20);
+    int64_t my_end = s0;
+    double g[3] = {0.0, 0.0, 0.0}, acc[3] = {0.0, 0.0, 0.0}, Tend = 1.0;
+    if (valid) {
+      const int64_t pix = (int64_t)py * bp.width + px;
+      my_end = state.last[pix];
+      Tend = state.final_t[pix];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      acc[c] = state.color_acc[3 * pix + c];
-      const double o = acc[c] + Tend * bp.bg[c];  // unclipped pixel value
-      // clip to [0, 1] (render.py:273): gradient passes where 0 <= C <= 1
-      g[c] = (o >= 0.0 && o <= 1.0) ? (double)dl_dimg[3 * pix + c] : 0.0;
+      for (int c = 0; c < 3; ++c) {
+        acc[c] = state.color_acc[3 * pix + c];
+        const double o = acc[c] + Tend * bp.bg[c];  // unclipped pixel value
+        // clip to [0, 1] (render.py:273): gradient passes where 0 <= C <= 1
+        g[c] = (o >= 0.0 && o <= 1.0) ? (double)dl_dimg[3 * pix + c] : 0.0;
+      }
     }
-  }
-  double T = 1.0, P[3] = {0.0, 0.0, 0.0};
-  int64_t my_end = valid ? last : s0;
-  for (int64_t bstart = s0; bstart < s1; bstart += kBwdBatch) {
-    if (threadIdx.x == 0) s_any = 0;
-    __syncthreads();
-    if (my_end > bstart) s_any = 1;
-    __syncthreads();
-    if (!s_any) break;
-    const int64_t k = bstart + threadIdx.x;
-    if (k < s1) buf[threadIdx.x] = hot[__ldg(list + k)];
-    __syncthreads();
-    const int nb = (int)min((int64_t)kBwdBatch, s1 - bstart);
-    for (int j = 0; j < nb; ++j) {
-      const HotRec h = buf[j];
-      float gr[kGradFields];
-      bool contrib = false;
-      if (bstart + j < my_end) {
-        const double dx = dsub(sx, h.mx), dy = dsub(sy, h.my);
-        const double power =
-            dsub(dmul(-0.5, dadd(dmul(dmul(h.c0, dx), dx), dmul(dmul(h.c2, dy), dy))),
-                 dmul(dmul(h.c1, dx), dy));
-        if (power >= (double)h.lthr) {
-          const double G = exp(power);
-          double alpha = dmul(h.opacity, G);
-          const bool clamped = alpha > 0.99;
-          if (clamped) alpha = 0.99;
-          if (alpha >= bp.alpha_floor) {
-            contrib = true;
-            const double col[3] = {h.r, h.g, h.b};
-            const double w = T * alpha;
-            double dl_da = 0.0;
+    int wend = (int)my_end;
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              P[c] += w * col[c];
-              const double S = (acc[c] - P[c]) + Tend * bp.bg[c];
-              dl_da += g[c] * (T * col[c] - S / (1.0 - alpha));
-              gr[6 + c] = (float)(w * g[c]);
+    for (int o = 16; o > 0; o >>= 1) {
+      x0 = min(x0, __shfl_xor_sync(0xffffffffu, x0, o));
+      x1 = max(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+      y0 = min(y0, __shfl_xor_sync(0xffffffffu, y0, o));
+      y1 = max(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+      wend = max(wend, __shfl_xor_sync(0xffffffffu, wend, o));
+    }
+    if (x0 > x1) continue;  // warp-uniform
+    const int64_t e1 = min((int64_t)wend, s1);
+    const double sx = (double)px + 0.5, sy = (double)py + 0.5;
+    double T = 1.0, P[3] = {0.0, 0.0, 0.0};
+
+    auto eval_round = [&](const HotRec* buf, uint32_t mask, int64_t k0) {
+      int slot = 0;
+      while (mask) {
+        const int src = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const HotRec& h = buf[slot++];
+        float gr[kGradFields];
+        bool contrib = false;
+        if (k0 + src < my_end) {
+          const double dx = dsub(sx, h.mx), dy = dsub(sy, h.my);
+          const double power =
+              dsub(dmul(-0.5, dadd(dmul(dmul(h.c0, dx), dx), dmul(dmul(h.c2, dy), dy))),
+                   dmul(dmul(h.c1, dx), dy));
+          if (power >= (double)h.lthr) {
+            const double G = exp(power);
+            double alpha = dmul(h.opacity, G);
+            const bool clamped = alpha > 0.99;
+            if (clamped) alpha = 0.99;
+            if (alpha >= bp.alpha_floor) {
+              contrib = true;
+              const double col[3] = {h.r, h.g, h.b};
+              const double w = T * alpha;
+              double dl_da = 0.0;
+#pragma unroll
+              for (int c = 0; c < 3; ++c) {
+                P[c] += w * col[c];
+                const double S = (acc[c] - P[c]) + Tend * bp.bg[c];
+                dl_da += g[c] * (T * col[c] - S / (1.0 - alpha));
+                gr[6 + c] = (float)(w * g[c]);
+              }
+              const float dl_dpow = clamped ? 0.f : (float)(dl_da * alpha);
+              const float fdx = (float)dx, fdy = (float)dy;
+              gr[5] = clamped ? 0.f : (float)(dl_da * G);
+              gr[0] = dl_dpow * ((float)h.c0 * fdx + (float)h.c1 * fdy);
+              gr[1] = dl_dpow * ((float)h.c2 * fdy + (float)h.c1 * fdx);
+              gr[2] = dl_dpow * (-0.5f * fdx * fdx);
+              gr[3] = dl_dpow * (-fdx * fdy);
+              gr[4] = dl_dpow * (-0.5f * fdy * fdy);
+              T = T * (1.0 - alpha);
             }
-            const double dl_dpow = clamped ? 0.0 : dl_da * alpha;
-            gr[5] = clamped ? 0.f : (float)(dl_da * G);
-            gr[0] = (float)(dl_dpow * (h.c0 * dx + h.c1 * dy));
-            gr[1] = (float)(dl_dpow * (h.c2 * dy + h.c1 * dx));
-            gr[2] = (float)(dl_dpow * (-0.5 * dx * dx));
-            gr[3] = (float)(dl_dpow * (-dx * dy));
-            gr[4] = (float)(dl_dpow * (-0.5 * dy * dy));
-            T = T * (1.0 - alpha);
+          }
+        }
+        if (__any_sync(0xffffffffu, contrib)) {
+#pragma unroll
+          for (int f = 0; f < kGradFields; ++f) {
+            float v = contrib ? gr[f] : 0.f;
+            v = warp_sum(v);
+            if (lane == 0 && v != 0.f) atomicAdd(&grads[(int64_t)f * cap + h.id], v);
           }
         }
       }
-      if (__any_sync(0xffffffffu, contrib)) {
-#pragma unroll
-        for (int f = 0; f < kGradFields; ++f) {
-          float v = contrib ? gr[f] : 0.f;
-          v = warp_sum(v);
-          if (lane_id() == 0 && v != 0.f) atomicAdd(&grads[(int64_t)f * cap + h.id], v);
-        }
-      }
+    };
+
+    uint32_t nid = 0, nbx = kEmptyBox, nby = kEmptyBox;
+    if (s0 + lane < e1) {
+      nid = __ldg(list + s0 + lane);
+      nbx = __ldg(bxs + s0 + lane);
+      nby = __ldg(bys + s0 + lane);
     }
-    __syncthreads();
+    uint32_t pmask = 0;
+    int64_t pk0 = 0;
+    int stage = 0;
+    for (int64_t k0 = s0; k0 < e1; k0 += 32) {
+      const uint32_t id = nid, bx = nbx, by = nby;
+      if (k0 + 32 + lane < e1) {
+        nid = __ldg(list + k0 + 32 + lane);
+        nbx = __ldg(bxs + k0 + 32 + lane);
+        nby = __ldg(bys + k0 + 32 + lane);
+      } else {
+        nbx = nby = kEmptyBox;
+      }
+      const int bx0 = (int)(int16_t)(bx & 0xffffu), bx1 = (int)(int16_t)(bx >> 16);
+      const int by0 = (int)(int16_t)(by & 0xffffu), by1 = (int)(int16_t)(by >> 16);
+      const bool hit = !(bx0 > x1 || bx1 < x0 || by0 > y1 || by1 < y0);
+      const uint32_t mask = __ballot_sync(0xffffffffu, hit);
+      if (!mask) continue;
+      if (hit) {
+        const char* gp = reinterpret_cast<const char*>(hot + id);
+        char* d = reinterpret_cast<char*>(&wbuf[stage][__popc(mask & lt_mask)]);
+#pragma unroll
+        for (int c = 0; c < 5; ++c) cp_async16(d + 16 * c, gp + 16 * c);
+      }
+      cp_async_commit();
+      if (pmask) {
+        cp_async_wait<1>();
+        __syncwarp();
+        eval_round(wbuf[stage ^ 1], pmask, pk0);
+        __syncwarp();
+      }
+      pmask = mask;
+      pk0 = k0;
+      stage ^= 1;
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+    if (pmask) eval_round(wbuf[stage ^ 1], pmask, pk0);
+    __syncwarp();
   }
 }
 
@@ -318,9 +383,9 @@ k_project_bwd(const cs_cloud cl, const int64_t* __restrict__ src, const DevStats
   }
 }
 
-void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint2* ranges, const HotRec* hot,
-                      const cs_settings& st, int width, int height, int ntx,
-                      const float* dl_dimg, const BlendState& state,
+void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint32_t* bxs, const uint32_t* bys,
+                      const uint2* ranges, const HotRec* hot, const cs_settings& st, int width,
+                      int height, int ntx, const float* dl_dimg, const BlendState& state,
                       float* grads, int64_t cap, cudaStream_t s) {
   BwdParams bp;
   for (int i = 0; i < 3; ++i) bp.bg[i] = st.background[i];
@@ -329,8 +394,16 @@ void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint2* ranges, co
   bp.width = width;
   bp.height = height;
   bp.ntx = ntx;
-  k_blend_bwd<<<n_tiles, kBwdThreads, 0, s>>>(list, ranges, hot, bp, dl_dimg, state, grads,
-                                              cap);
+  const int px = st.tile_size * st.tile_size;
+  if (px <= 256)
+    k_blend_bwd<1><<<n_tiles, kBwdThreads, 0, s>>>(list, bxs, bys, ranges, hot, bp, dl_dimg, state,
+                                                   grads, cap);
+  else if (px <= 1024)
+    k_blend_bwd<4><<<n_tiles, kBwdThreads, 0, s>>>(list, bxs, bys, ranges, hot, bp, dl_dimg, state,
+                                                   grads, cap);
+  else
+    k_blend_bwd<16><<<n_tiles, kBwdThreads, 0, s>>>(list, bxs, bys, ranges, hot, bp, dl_dimg,
+                                                    state, grads, cap);
 }
 
 void launch_project_bwd(const cs_cloud& cl, const int64_t* src,

@@ -29,26 +29,6 @@ namespace cs {
 constexpr int kBlendThreads = 256;
 constexpr int kBatch = 256;
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// local pixel index (0..ts*ts-1) of thread `tid`, pixel slot q.  When the
-// tile side is a multiple of 8, warps own 8x4 pixel boxes (box index
-// warp + 8q, row-major over the tile's (ts/8) x (ts/4) boxes).
-__device__ __forceinline__ int local_pixel(int tid, int q, int ts) {
-  if ((ts & 7) == 0) {
-    const int b = (tid >> 5) + 8 * q, l = tid & 31, nbx = ts >> 3;
-    const int bx = b % nbx, by = b / nbx;
-    return (by * 4 + (l >> 3)) * ts + bx * 8 + (l & 7);
-  }
-  return tid + q * kBlendThreads;
-}
-
 // Warp-independent blend: each warp walks the tile's depth-ordered list on
 // its own (no block barriers).  Per round of 32 list entries each lane reads
 // one entry's compact id and packed cull box -- pair-major arrays written by

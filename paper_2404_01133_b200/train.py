@@ -129,18 +129,26 @@ class BlockTrainer:
             {"params": [self.quat], "lr": 1e-3},
             {"params": [self.logit_op], "lr": 5e-2},
             {"params": [self.sh], "lr": 2.5e-3},
-        ], eps=1e-15)
+        ], eps=1e-15, fused=self.pos.is_cuda)
 
     def activated(self):
         q = self.quat / self.quat.norm(dim=1, keepdim=True)
         return (self.pos, torch.exp(self.log_scale), q, torch.sigmoid(self.logit_op), self.sh)
 
-    def step(self, cam, target: torch.Tensor) -> torch.Tensor:
+    def step(self, cam, target: torch.Tensor, events=None) -> torch.Tensor:
+        """One iteration; `events` (5 CUDA events) brackets forward, loss,
+        backward and the optimizer step for per-phase timing."""
+        rec = (lambda i: events[i].record()) if events is not None else (lambda i: None)
         self.opt.zero_grad(set_to_none=True)
+        rec(0)
         img = rasterize_train(*self.activated(), cam, self.settings)
+        rec(1)
         loss = training_loss(img, target)
+        rec(2)
         loss.backward()
+        rec(3)
         self.opt.step()
+        rec(4)
         return loss.detach()
 
 
@@ -153,3 +161,104 @@ def lpt_assign(sizes: Sequence[int], n_ranks: int) -> List[int]:
         owner[j] = r
         load[r] += sizes[j]
     return owner
+
+
+class DeviceBlockTrainer:
+    """The block iteration on the C ABI end to end (no autograd graph):
+
+        cs_render(KEEP_STATE) -> cs_training_loss (K13) -> cs_render_backward
+        (K10/K11) -> cs_block_adam (K14: activation chain + Adam + the
+        activated quads of the next forward)
+
+    Same loss, activations, learning rates and Adam semantics as
+    ``BlockTrainer`` (its torch restatement, used as the reference in tests).
+    Raw parameters: geom (K, 11) = [xyz, log scale, raw quaternion wxyz,
+    logit opacity] and sh (K, 3C); the sh array doubles as the render's SH
+    row table, so C must be 4 or 16 (3C a multiple of 4).
+    """
+
+    def __init__(self, positions, scales, rotations, opacities, sh, lr=1.6e-4, settings=None,
+                 betas=(0.9, 0.999), eps=1e-15):
+        from .render import RenderSettings
+        self.settings = settings or RenderSettings()
+        dev = positions.device
+        k = int(positions.shape[0])
+        C = int(sh.shape[2])
+        if C not in (4, 16):
+            raise ValueError("DeviceBlockTrainer needs 4 or 16 SH coefficients (row stride 3C % 4 == 0)")
+        self.K, self.C, self.dev = k, C, dev
+        f = lambda t: t.detach().to(device=dev, dtype=torch.float32)
+        o = f(opacities).reshape(k).clamp(1e-6, 1 - 1e-6)
+        self.geom = torch.cat([f(positions).reshape(k, 3), torch.log(f(scales).clamp_min(1e-8)).reshape(k, 3),
+                               f(rotations).reshape(k, 4), torch.log(o / (1 - o)).reshape(k, 1)],
+                              dim=1).contiguous()
+        self.sh = f(sh).reshape(k, 3 * C).contiguous()
+        self.geom_m = torch.zeros_like(self.geom)
+        self.geom_v = torch.zeros_like(self.geom)
+        self.sh_m = torch.zeros_like(self.sh)
+        self.sh_v = torch.zeros_like(self.sh)
+        self.quads = torch.empty((3, k, 4), dtype=torch.float32, device=dev)
+        self.g_pos = torch.empty((k, 3), dtype=torch.float32, device=dev)
+        self.g_scale = torch.empty((k, 3), dtype=torch.float32, device=dev)
+        self.g_rot = torch.empty((k, 4), dtype=torch.float32, device=dev)
+        self.g_op = torch.empty((k,), dtype=torch.float32, device=dev)
+        self.g_sh = torch.empty((k, 3 * C), dtype=torch.float32, device=dev)
+        self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.hp = _lib.CsAdamHparams(lr * POSITION_LR_SCALE, 5e-3 * SCALE_LR_SCALE, 1e-3, 5e-2, 2.5e-3,
+                                     betas[0], betas[1], eps, 0, 0)
+        self.grads = CsGrads(self.g_pos.data_ptr(), self.g_scale.data_ptr(), self.g_rot.data_ptr(),
+                             self.g_op.data_ptr(), self.g_sh.data_ptr())
+        self.src = CsSource()
+        self.src.kind = _lib.CS_SRC_CLOUD
+        self.src.force_level = -1
+        self.src.cloud = _lib.CsCloud(self.quads[0].data_ptr(), self.quads[1].data_ptr(),
+                                      self.quads[2].data_ptr(), self.sh.data_ptr(), k, C, 3 * C, 0, 0)
+        self.cset = device.settings_struct(self.settings)
+        self._bufs = {}
+        self.lib = _lib.load()
+        self.h = device.context(dev.index)
+        check(self.lib.cs_block_activate(self.h, k, self.geom.data_ptr(), self.quads[0].data_ptr(),
+                                         self.quads[1].data_ptr(), self.quads[2].data_ptr(),
+                                         device.stream_handle(dev)), "cs_block_activate")
+
+    @property
+    def step_count(self) -> int:
+        return int(self.hp.step)
+
+    def activated(self):
+        """(positions, scales, rotations, opacities, sh) as the renderer sees them."""
+        q = self.quads
+        return (q[0, :, :3], q[1, :, :3], q[2], q[0, :, 3], self.sh.reshape(self.K, 3, self.C))
+
+    def _images(self, H: int, W: int):
+        b = self._bufs.get((H, W))
+        if b is None:
+            b = self._bufs[(H, W)] = (torch.empty((H, W, 3), dtype=torch.float32, device=self.dev),
+                                      torch.empty((H, W, 3), dtype=torch.float32, device=self.dev))
+        return b
+
+    def step(self, cam, target: torch.Tensor, events=None) -> torch.Tensor:
+        rec = (lambda i: events[i].record()) if events is not None else (lambda i: None)
+        lib, h = self.lib, self.h
+        s = device.stream_handle(self.dev)
+        H, W = int(cam.height), int(cam.width)
+        img, dimg = self._images(H, W)
+        ccam = device.camera_struct(cam)
+        rec(0)
+        check(lib.cs_render(h, ctypes.byref(self.src), ctypes.byref(ccam), ctypes.byref(self.cset),
+                            img.data_ptr(), _lib.CS_RENDER_KEEP_STATE, None, s), "cs_render")
+        rec(1)
+        check(lib.cs_training_loss(h, img.data_ptr(), target.data_ptr(), H, W, LOSS_LAMBDA,
+                                   self.loss.data_ptr(), dimg.data_ptr(), s), "cs_training_loss")
+        rec(2)
+        check(lib.cs_render_backward(h, ctypes.byref(self.src), ctypes.byref(ccam), ctypes.byref(self.cset),
+                                     dimg.data_ptr(), ctypes.byref(self.grads), s), "cs_render_backward")
+        rec(3)
+        self.hp.step += 1
+        check(lib.cs_block_adam(h, self.K, self.C, self.geom.data_ptr(), self.geom_m.data_ptr(),
+                                self.geom_v.data_ptr(), self.sh.data_ptr(), self.sh_m.data_ptr(),
+                                self.sh_v.data_ptr(), ctypes.byref(self.grads), ctypes.byref(self.hp),
+                                self.quads[0].data_ptr(), self.quads[1].data_ptr(), self.quads[2].data_ptr(),
+                                s), "cs_block_adam")
+        rec(4)
+        return self.loss
