@@ -91,9 +91,10 @@ void launch_fuse_filter(int64_t n, const void* pos, int f32, const double* pmin,
                         int64_t* kept, int64_t* kept_count, cudaStream_t s);
 // cs_backward.cu
 void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint32_t* bxs, const uint32_t* bys,
-                      const uint2* ranges, const HotRec* hot, const cs_settings& st, int width,
-                      int height, int ntx, const float* dl_dimg, const BlendState& state,
-                      float* grads, int64_t cap, cudaStream_t s);
+                      const uint2* ranges, const HotRec* hot, const uint32_t* order,
+                      const cs_settings& st, int width, int height, int ntx, const float* dl_dimg,
+                      const BlendState& state, uint32_t* ticket, float* grads, int64_t cap,
+                      cudaStream_t s);
 void launch_project_bwd(const cs_cloud& cl, const int64_t* src,
                         const DevStats* stats, const cs_camera& cam, const cs_settings& st,
                         const float* grads, int64_t cap, const cs_grads& out, cudaStream_t s);
@@ -578,8 +579,8 @@ int cs_render_backward(cs_ctx* c, const cs_source* src, const cs_camera* cam,
   const int ntx = (cam->width + ts - 1) / ts;
   BlendState state{c->st_t.as<double>(), c->st_last.as<int32_t>(), c->st_acc.as<double>()};
   launch_blend_bwd(c->last_tiles, c->last_list, c->last_bxs, c->last_bys, c->last_ranges,
-                   c->hot.as<HotRec>(),
-                   *st, cam->width, cam->height, ntx, dl_dimg, state,
+                   c->hot.as<HotRec>(), c->tile_order.as<uint32_t>(), *st, cam->width,
+                   cam->height, ntx, dl_dimg, state, &c->stats.as<DevStats>()->tickets[5],
                    c->gacc.as<float>(), cap, s);
   CS_CHECK_LAUNCH();
   const int64_t K = cl.count;

@@ -34,31 +34,58 @@ struct BwdParams {
   int tile_size, width, height, ntx;
 };
 
-// Same warp-independent walk as the forward (cs_blend.cu): per round of 32
+// Sums the 9 per-lane partials over the warp with a recursive-halving
+// transpose (8 + 4 + 2 + 1 + 1 shuffles for 16 slots instead of 5 per value):
+// on return lane l holds the warp total of slot (l >> 1) & 15 (slots >= 9 are
+// zero padding), so nine lanes can issue their atomics in one instruction.
+__device__ __forceinline__ float warp_transpose_sum9(const float (&in)[kGradFields], uint32_t lane) {
+  float v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = i < kGradFields ? in[i] : 0.f;
+#pragma unroll
+  for (int o = 16, n = 16; o >= 2; o >>= 1, n >>= 1) {
+    const bool upper = (lane & o) != 0;
+    const int h = n >> 1;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const float send = upper ? v[i] : v[i + h];
+      const float keep = upper ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+
+// Same persistent warp-item walk as the forward (cs_blend.cu): per round of 32
 // list entries a coalesced read of (id, packed box), a ballot of the hits
 // against the warp's pixel box, cp.async staging of the hits' HotRecs into
 // the warp's two-stage shared buffer.  A warp walks only up to the largest
 // `last` of its pixels.  Per evaluated hit each lane re-derives the forward's
 // float64 decisions for its pixel; when any lane contributes, the nine
 // partials are warp-reduced and lane 0 adds them with one atomic each.
-template <int PPT>
 __global__ void __launch_bounds__(kBwdThreads)
 k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
             const uint32_t* __restrict__ bys, const uint2* __restrict__ ranges,
-            const HotRec* __restrict__ hot, BwdParams bp, const float* __restrict__ dl_dimg,
-            BlendState state, float* __restrict__ grads /* [kGradFields][cap] */, int64_t cap) {
+            const HotRec* __restrict__ hot, const uint32_t* __restrict__ tile_order, int n_items,
+            int nboxes, BwdParams bp, const float* __restrict__ dl_dimg, BlendState state,
+            uint32_t* __restrict__ ticket, float* __restrict__ grads /* [kGradFields][cap] */,
+            int64_t cap) {
   __shared__ __align__(16) HotRec s_hot[kBwdThreads / 32][2][32];
-  const int t = blockIdx.x;
-  const int tx = t % bp.ntx, ty = t / bp.ntx;
   const int ts = bp.tile_size;
-  const uint2 rg = ranges[t];
-  const int64_t s0 = rg.x, s1 = rg.y;
   const uint32_t lane = lane_id();
   const uint32_t lt_mask = (1u << lane) - 1u;
   HotRec (*wbuf)[32] = s_hot[threadIdx.x >> 5];
-#pragma unroll 1
-  for (int q = 0; q < PPT; ++q) {
-    const int li = local_pixel(threadIdx.x, q, ts);
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = (int)atomicAdd(ticket, 1u);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= n_items) break;
+    const int tr = item / nboxes, b = item - tr * nboxes;
+    const int t = tile_order ? (int)tile_order[tr] : tr;
+    const int tx = t % bp.ntx, ty = t / bp.ntx;
+    const uint2 rg = ranges[t];
+    const int64_t s0 = rg.x, s1 = rg.y;
+    const int li = box_pixel(b, lane, ts);
     const int px = tx * ts + li % ts, py = ty * ts + li / ts;
     const bool valid = li < ts * ts && px < bp.width && py < bp.height;
     int x0 = valid ? px : 1 << 20, x1 = valid ? px : -(1 << 20);
@@ -114,11 +141,12 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
               const double col[3] = {h.r, h.g, h.b};
               const double w = T * alpha;
               double dl_da = 0.0;
+              const double inv = 1.0 / (1.0 - alpha);
 #pragma unroll
               for (int c = 0; c < 3; ++c) {
                 P[c] += w * col[c];
                 const double S = (acc[c] - P[c]) + Tend * bp.bg[c];
-                dl_da += g[c] * (T * col[c] - S / (1.0 - alpha));
+                dl_da += g[c] * (T * col[c] - S * inv);
                 gr[6 + c] = (float)(w * g[c]);
               }
               const float dl_dpow = clamped ? 0.f : (float)(dl_da * alpha);
@@ -134,12 +162,13 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
           }
         }
         if (__any_sync(0xffffffffu, contrib)) {
+          if (!contrib) {
 #pragma unroll
-          for (int f = 0; f < kGradFields; ++f) {
-            float v = contrib ? gr[f] : 0.f;
-            v = warp_sum(v);
-            if (lane == 0 && v != 0.f) atomicAdd(&grads[(int64_t)f * cap + h.id], v);
+            for (int f = 0; f < kGradFields; ++f) gr[f] = 0.f;
           }
+          const float v = warp_transpose_sum9(gr, lane);
+          const uint32_t f = (lane >> 1) & 15;
+          if (!(lane & 1) && f < kGradFields && v != 0.f) atomicAdd(&grads[(int64_t)f * cap + h.id], v);
         }
       }
     };
@@ -384,9 +413,10 @@ k_project_bwd(const cs_cloud cl, const int64_t* __restrict__ src, const DevStats
 }
 
 void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint32_t* bxs, const uint32_t* bys,
-                      const uint2* ranges, const HotRec* hot, const cs_settings& st, int width,
-                      int height, int ntx, const float* dl_dimg, const BlendState& state,
-                      float* grads, int64_t cap, cudaStream_t s) {
+                      const uint2* ranges, const HotRec* hot, const uint32_t* order,
+                      const cs_settings& st, int width, int height, int ntx, const float* dl_dimg,
+                      const BlendState& state, uint32_t* ticket, float* grads, int64_t cap,
+                      cudaStream_t s) {
   BwdParams bp;
   for (int i = 0; i < 3; ++i) bp.bg[i] = st.background[i];
   bp.alpha_floor = st.alpha_floor;
@@ -394,16 +424,12 @@ void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint32_t* bxs, co
   bp.width = width;
   bp.height = height;
   bp.ntx = ntx;
-  const int px = st.tile_size * st.tile_size;
-  if (px <= 256)
-    k_blend_bwd<1><<<n_tiles, kBwdThreads, 0, s>>>(list, bxs, bys, ranges, hot, bp, dl_dimg, state,
-                                                   grads, cap);
-  else if (px <= 1024)
-    k_blend_bwd<4><<<n_tiles, kBwdThreads, 0, s>>>(list, bxs, bys, ranges, hot, bp, dl_dimg, state,
-                                                   grads, cap);
-  else
-    k_blend_bwd<16><<<n_tiles, kBwdThreads, 0, s>>>(list, bxs, bys, ranges, hot, bp, dl_dimg,
-                                                    state, grads, cap);
+  static int grid = 0;
+  if (grid == 0) grid = persistent_grid(k_blend_bwd, kBwdThreads);
+  const int nboxes = boxes_per_tile(st.tile_size);
+  cudaMemsetAsync(ticket, 0, sizeof(uint32_t), s);
+  k_blend_bwd<<<grid, kBwdThreads, 0, s>>>(list, bxs, bys, ranges, hot, order, n_tiles * nboxes,
+                                           nboxes, bp, dl_dimg, state, ticket, grads, cap);
 }
 
 void launch_project_bwd(const cs_cloud& cl, const int64_t* src,

@@ -27,41 +27,43 @@
 namespace cs {
 
 constexpr int kBlendThreads = 256;
-constexpr int kBatch = 256;
 
-// Warp-independent blend: each warp walks the tile's depth-ordered list on
-// its own (no block barriers).  Per round of 32 list entries each lane reads
-// one entry's compact id and packed cull box -- pair-major arrays written by
-// K8, so the reads are coalesced and shared by the CTA's 8 warps through L1 --
-// and tests the box against the warp's pixel box; __ballot_sync compacts the
-// hits and each hitting lane cp.async-copies its splat's 80-byte HotRec into
-// the warp's shared-memory slot.  The copies of round r are in flight while
-// the warp evaluates round r-1 (two stages per warp), so HotRec latency is
-// paid once per 32 entries, not once per evaluation.  A warp stops as soon as
-// its 32 pixels have terminated.
-template <int PPT, typename OutT, bool KEEP>
+// Warp-independent blend, persistent: every warp repeatedly takes the next
+// work item -- one 8x4 pixel box of one tile, tiles in heaviest-list-first
+// order -- from a device-wide ticket, so no warp ever waits for another and a
+// CTA's slots are never held by finished warps.  For its box a warp walks the
+// tile's depth-ordered list 32 entries per round: each lane reads one entry's
+// compact id and packed cull box (pair-major arrays written by K8: coalesced,
+// and the 8 boxes of a tile run concurrently so the list stays in L1/L2), a
+// __ballot_sync compacts the entries whose alpha-floor box meets the warp's
+// pixel box, and each hitting lane cp.async-copies its splat's 80-byte HotRec
+// into the warp's shared-memory slot.  The copies of round r are in flight
+// while the warp evaluates round r-1 (two stages per warp).  The walk stops
+// as soon as the box's 32 pixels have terminated.
+template <typename OutT, bool KEEP>
 __global__ void __launch_bounds__(kBlendThreads)
 k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
         const uint32_t* __restrict__ bys, const uint2* __restrict__ ranges,
-        const HotRec* __restrict__ hot, const uint32_t* __restrict__ tile_order, BlendParams bp,
-        OutT* __restrict__ out, int32_t* __restrict__ frag_tile, DevStats* __restrict__ stats,
-        BlendState state) {
+        const HotRec* __restrict__ hot, const uint32_t* __restrict__ tile_order, int n_items,
+        int nboxes, BlendParams bp, OutT* __restrict__ out, int32_t* __restrict__ frag_tile,
+        DevStats* __restrict__ stats, BlendState state) {
   __shared__ __align__(16) HotRec s_hot[kBlendThreads / 32][2][32];
-  __shared__ int s_red[kBlendThreads / 32];
-  __shared__ long long s_ev[kBlendThreads / 32];
-  const int t = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
-  const int tx = t % bp.ntx, ty = t / bp.ntx;
   const int ts = bp.tile_size;
-  const uint2 rg = ranges[t];
-  const int64_t s0 = rg.x, s1 = rg.y;
   const uint32_t lane = lane_id();
   const uint32_t lt_mask = (1u << lane) - 1u;
   HotRec (*wbuf)[32] = s_hot[threadIdx.x >> 5];
-  int my_frag = 0;
-  long long evals = 0;
-#pragma unroll 1
-  for (int q = 0; q < PPT; ++q) {
-    const int li = local_pixel(threadIdx.x, q, ts);
+  long long frags = 0, evals = 0;
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = (int)atomicAdd(&stats->tickets[4], 1u);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= n_items) break;
+    const int tr = item / nboxes, b = item - tr * nboxes;
+    const int t = tile_order ? (int)tile_order[tr] : tr;
+    const int tx = t % bp.ntx, ty = t / bp.ntx;
+    const uint2 rg = ranges[t];
+    const int64_t s0 = rg.x, s1 = rg.y;
+    const int li = box_pixel(b, lane, ts);
     const int px = tx * ts + li % ts, py = ty * ts + li / ts;
     const bool valid = li < ts * ts && px < bp.width && py < bp.height;
     int x0 = valid ? px : 1 << 20, x1 = valid ? px : -(1 << 20);
@@ -73,7 +75,7 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
       y0 = min(y0, __shfl_xor_sync(0xffffffffu, y0, o));
       y1 = max(y1, __shfl_xor_sync(0xffffffffu, y1, o));
     }
-    if (x0 > x1) continue;  // no pixel of this slot in the image (warp-uniform)
+    if (x0 > x1) continue;  // no pixel of this box in the image (warp-uniform)
     const double sx = (double)px + 0.5, sy = (double)py + 0.5;  // _kernels.py:43-45
     double T = 1.0, cr = 0.0, cg = 0.0, cb = 0.0;
     int cnt = 0;
@@ -159,7 +161,6 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
     if (pmask && !alldone) eval_round(wbuf[stage ^ 1], pmask, pk0);
     __syncwarp();
     if (valid) {
-      my_frag += cnt;
       const int64_t pix = (int64_t)py * bp.width + px;
       double o[3] = {cr + T * bp.bg[0], cg + T * bp.bg[1], cb + T * bp.bg[2]};
       if (!(bp.flags & CS_RENDER_NO_CLIP)) {
@@ -177,39 +178,28 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
         state.color_acc[3 * pix + 2] = cb;
       }
     }
+    const int box_frags = warp_sum(valid ? cnt : 0);
+    frags += box_frags;
+    if (lane == 0 && box_frags) atomicAdd(frag_tile + t, box_frags);
   }
-  my_frag = warp_sum(my_frag);
   evals = warp_sum(evals);
   if (lane == 0) {
-    s_red[threadIdx.x >> 5] = my_frag;
-    s_ev[threadIdx.x >> 5] = evals;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int tot = 0;
-    long long ev = 0;
-    for (int w = 0; w < kBlendThreads / 32; ++w) { tot += s_red[w]; ev += s_ev[w]; }
-    frag_tile[t] = tot;
-    if (tot) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->fragments),
-                       (unsigned long long)tot);
-    if (ev) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->evals), (unsigned long long)ev);
+    if (frags) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->fragments), (unsigned long long)frags);
+    if (evals) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->evals), (unsigned long long)evals);
   }
 }
 
 template <typename OutT, bool KEEP>
-static void launch_blend_t(int ppt, int n_tiles, const uint32_t* list, const uint32_t* bxs,
+static void launch_blend_t(int n_tiles, const uint32_t* list, const uint32_t* bxs,
                            const uint32_t* bys, const uint2* ranges, const HotRec* hot,
                            const uint32_t* order, const BlendParams& bp, OutT* out,
                            int32_t* frag_tile, DevStats* stats, BlendState st, cudaStream_t s) {
-  if (ppt == 1)
-    k_blend<1, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, bxs, bys, ranges, hot, order, bp,
-                                                            out, frag_tile, stats, st);
-  else if (ppt == 4)
-    k_blend<4, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, bxs, bys, ranges, hot, order, bp,
-                                                            out, frag_tile, stats, st);
-  else
-    k_blend<16, OutT, KEEP><<<n_tiles, kBlendThreads, 0, s>>>(list, bxs, bys, ranges, hot, order, bp,
-                                                             out, frag_tile, stats, st);
+  static int grid = 0;  // persistent: one wave of resident CTAs
+  if (grid == 0) grid = persistent_grid(k_blend<OutT, KEEP>, kBlendThreads);
+  const int nboxes = boxes_per_tile(bp.tile_size);
+  k_blend<OutT, KEEP><<<grid, kBlendThreads, 0, s>>>(list, bxs, bys, ranges, hot, order,
+                                                     n_tiles * nboxes, nboxes, bp, out, frag_tile,
+                                                     stats, st);
 }
 
 // K8b: heaviest-first tile order.  Tiles are bucketed by floor(log2(list
@@ -242,26 +232,23 @@ void launch_tile_order(const uint2* ranges, int n_tiles, uint32_t* order, cudaSt
   k_tile_order<<<1, 1024, 0, s>>>(ranges, n_tiles, order);
 }
 
-int blend_ppt(int tile_size) {
-  const int px = tile_size * tile_size;
-  if (px <= 256) return 1;
-  if (px <= 1024) return 4;
-  if (px <= 4096) return 16;
-  return 0;
+int blend_ppt(int tile_size) {  // 0 = unsupported tile size
+  return tile_size * tile_size <= 4096 ? 1 : 0;
 }
 
 void launch_blend(int n_tiles, const uint32_t* list, const uint32_t* bxs, const uint32_t* bys,
                   const uint2* ranges, const HotRec* hot, const uint32_t* order,
                   const BlendParams& bp, void* out, bool f64_out, int32_t* frag_tile,
                   DevStats* stats, const BlendState* keep, cudaStream_t s) {
-  const int ppt = blend_ppt(bp.tile_size);
   BlendState st = keep ? *keep : BlendState{nullptr, nullptr, nullptr};
+  cudaMemsetAsync(frag_tile, 0, sizeof(int32_t) * n_tiles, s);
+  cudaMemsetAsync(&stats->tickets[4], 0, sizeof(uint32_t), s);
   if (f64_out) {
-    if (keep) launch_blend_t<double, true>(ppt, n_tiles, list, bxs, bys, ranges, hot, order, bp, (double*)out, frag_tile, stats, st, s);
-    else launch_blend_t<double, false>(ppt, n_tiles, list, bxs, bys, ranges, hot, order, bp, (double*)out, frag_tile, stats, st, s);
+    if (keep) launch_blend_t<double, true>(n_tiles, list, bxs, bys, ranges, hot, order, bp, (double*)out, frag_tile, stats, st, s);
+    else launch_blend_t<double, false>(n_tiles, list, bxs, bys, ranges, hot, order, bp, (double*)out, frag_tile, stats, st, s);
   } else {
-    if (keep) launch_blend_t<float, true>(ppt, n_tiles, list, bxs, bys, ranges, hot, order, bp, (float*)out, frag_tile, stats, st, s);
-    else launch_blend_t<float, false>(ppt, n_tiles, list, bxs, bys, ranges, hot, order, bp, (float*)out, frag_tile, stats, st, s);
+    if (keep) launch_blend_t<float, true>(n_tiles, list, bxs, bys, ranges, hot, order, bp, (float*)out, frag_tile, stats, st, s);
+    else launch_blend_t<float, false>(n_tiles, list, bxs, bys, ranges, hot, order, bp, (float*)out, frag_tile, stats, st, s);
   }
 }
 

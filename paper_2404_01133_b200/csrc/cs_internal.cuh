@@ -11,6 +11,8 @@
 //   pairs     :  u32 tile key + u32 compact index, sorted stably by tile
 #pragma once
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <stdint.h>
 
 #include "../../include/cs_api.h"
@@ -135,6 +137,30 @@ __device__ __forceinline__ int local_pixel(int tid, int q, int ts) {
     return (by * 4 + (l >> 3)) * ts + bx * 8 + (l & 7);
   }
   return tid + q * 256;
+}
+
+// Blend work items are (tile, box) pairs: a box is 32 pixels of a tile --
+// an 8x4 block when the tile side is a multiple of 8, else 32 consecutive
+// row-major pixels.  box_pixel -> local pixel index (>= ts*ts: no pixel).
+__host__ __device__ __forceinline__ int boxes_per_tile(int ts) {
+  return (ts & 7) == 0 ? (ts >> 3) * (ts >> 2) : (ts * ts + 31) / 32;
+}
+__device__ __forceinline__ int box_pixel(int b, int lane, int ts) {
+  if ((ts & 7) == 0) {
+    const int nbx = ts >> 3, bx = b % nbx, by = b / nbx;
+    return (by * 4 + (lane >> 3)) * ts + bx * 8 + (lane & 7);
+  }
+  return b * 32 + lane;
+}
+
+// grid of a persistent kernel: as many CTAs as are co-resident on all SMs
+template <typename K>
+static int persistent_grid(K kernel, int threads) {
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
+  return std::max(1, sms * std::max(1, per_sm));
 }
 
 // ---------------------------------------------------------------------------
