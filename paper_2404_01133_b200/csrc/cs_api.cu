@@ -2,7 +2,7 @@
 // pipeline K1..K9 on one stream with no host round trip.
 //
 //   K1  lod_select / pointwise      (lod.py:330-401)            cs_lod.cu
-//   K3  project + compaction        (render.py:111-172)         cs_project.cu
+//   K3  project + cull              (render.py:111-172)         cs_project.cu
 //   K4  depth radix sort, 64-bit    (render.py:176-177)         cs_sort.cu
 //   K5  rank gather + pair scan     (render.py:178-188,226-236) cs_bin.cu
 //   K6  pair duplication            (render.py:237-243)         cs_bin.cu
@@ -24,8 +24,8 @@
 namespace cs {
 // cs_project.cu
 void launch_project(const cs_cloud* d_clouds, const Seg* d_segs, DevStats* d_stats,
-                    const cs_camera& cam, const cs_settings& st, uint64_t* status,
-                    int64_t capacity, const ProjOutputs& out, const uint64_t* list, cudaStream_t s);
+                    const cs_camera& cam, const cs_settings& st, int64_t capacity,
+                    const ProjOutputs& out, const uint64_t* list, cudaStream_t s);
 void launch_setup_cloud(const cs_cloud& c, cs_cloud* d_clouds, Seg* d_segs, DevStats* d_stats,
                         cudaStream_t s);
 void launch_build_covariances(int64_t n, const double* scales, const double* quats, double* out,
@@ -56,11 +56,14 @@ void launch_block_adam(int64_t K, int C, float* geom, float* gm, float* gv, floa
 void launch_activate_geom(int64_t K, const float* geom, float4* pos_op, float4* scale, float4* quat,
                           cudaStream_t s);
 // cs_bin.cu
+int64_t pair_count_chunks(int64_t capacity);
+int64_t dup_blocks(int64_t pair_cap);
 void launch_pair_count(const uint32_t* order, const int4* rects, DevStats* stats, int64_t pair_cap,
-                       int64_t capacity, uint64_t* status, int64_t* pair_off, cudaStream_t s);
+                       int64_t capacity, uint64_t* status, int64_t* pair_off, uint32_t* dup_start,
+                       cudaStream_t s);
 void launch_duplicate(const int64_t* pair_off, const uint32_t* order, const int4* rects,
-                      const DevStats* stats, int ntx, int64_t pair_cap, uint32_t* keys,
-                      uint32_t* vals, cudaStream_t s);
+                      const uint32_t* dup_start, const DevStats* stats, int ntx, int64_t pair_cap,
+                      uint32_t* keys, uint32_t* vals, cudaStream_t s);
 void launch_tile_ranges(const uint32_t* keys, const uint32_t* vals, const short4* boxes,
                         const DevStats* stats, uint2* ranges, uint32_t* bxs, uint32_t* bys,
                         cudaStream_t s);
@@ -95,7 +98,7 @@ void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint32_t* bxs, co
                       const cs_settings& st, int width, int height, int ntx, const float* dl_dimg,
                       const BlendState& state, uint32_t* ticket, float* grads, int64_t cap,
                       cudaStream_t s);
-void launch_project_bwd(const cs_cloud& cl, const int64_t* src,
+void launch_project_bwd(const cs_cloud& cl, const uint32_t* order,
                         const DevStats* stats, const cs_camera& cam, const cs_settings& st,
                         const float* grads, int64_t cap, const cs_grads& out, cudaStream_t s);
 }  // namespace cs
@@ -176,13 +179,14 @@ struct cs_ctx {
   int device = 0;
   std::mutex mu;  // one frame at a time per context (contexts are per thread/stream)
   DBuf stats, clouds1, segs, dec;
-  DBuf st_proj, st_gather, st_pw, st_fuse, st_sort, hist, sort_tickets, fuse_ticket;
+  DBuf st_gather, st_pw, st_fuse, st_sort, hist, sort_tickets, fuse_ticket;
   DBuf keysA, valsA, keysB, valsB, recs;
-  DBuf hot, boxes, rects, src, pair_off, tile_order;
+  DBuf hot, boxes, rects, pair_off, tile_order;
   DBuf pkA, pvA, pkB, pvB, ranges, frag_tile, pw_list;
   DBuf st_t, st_last, st_acc;
   DBuf scratch1, scratch2, scratch3, scratch4;  // API utilities
   DBuf gacc;                                    // per-rank blend-backward partials
+  DBuf dup_start;                               // K5 -> K6: first depth rank of each duplication CTA
   DBuf loss_maps, loss_acc;                     // cs_training_loss workspace
   cs_frame_stats* h_stats = nullptr;            // pinned
   int64_t cap_vis = 0, cap_pairs = 0, cap_pw = 0, cap_tiles = 0;
@@ -240,12 +244,12 @@ void cs_destroy(cs_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
-  DBuf* all[] = {&c->stats, &c->clouds1, &c->segs, &c->dec, &c->st_proj, &c->st_gather,
+  DBuf* all[] = {&c->stats, &c->clouds1, &c->segs, &c->dec, &c->st_gather,
                  &c->st_pw, &c->st_fuse, &c->st_sort, &c->hist, &c->sort_tickets,
                  &c->fuse_ticket, &c->keysA, &c->valsA, &c->keysB, &c->valsB, &c->recs, &c->hot,
-                 &c->tile_order, &c->boxes, &c->rects, &c->src, &c->pair_off, &c->pkA, &c->pvA, &c->pkB,
+                 &c->tile_order, &c->boxes, &c->rects, &c->pair_off, &c->pkA, &c->pvA, &c->pkB,
                  &c->pvB, &c->ranges, &c->frag_tile, &c->pw_list, &c->st_t, &c->st_last,
-                 &c->st_acc, &c->gacc, &c->loss_maps, &c->loss_acc, &c->scratch1, &c->scratch2, &c->scratch3, &c->scratch4};
+                 &c->st_acc, &c->gacc, &c->dup_start, &c->loss_maps, &c->loss_acc, &c->scratch1, &c->scratch2, &c->scratch3, &c->scratch4};
   for (DBuf* b : all) b->release();
   if (c->h_stats) cudaFreeHost(c->h_stats);
   for (cudaEvent_t e : c->tev) cudaEventDestroy(e);
@@ -323,18 +327,19 @@ static int ensure_frame_buffers(cs_ctx* c, int64_t cap_vis, int n_segs, int n_bl
     int64_t cap = std::max<int64_t>(cap_vis, c->cap_vis + c->cap_vis / 2);
     if (cap >= (1ll << 30)) return fail(CS_EINVAL, "more than 2^30 assembled Gaussians");
     const int64_t chunks = (cap + 255) / 256 + 1;
-    if (c->st_proj.ensure(8 * chunks) || c->st_gather.ensure(8 * chunks) ||
+    if (c->st_gather.ensure(8 * chunks) ||
         c->keysA.ensure(8 * cap) || c->keysB.ensure(8 * cap) || c->valsA.ensure(4 * cap) ||
         c->valsB.ensure(4 * cap) || c->hot.ensure(sizeof(HotRec) * cap) ||
         c->rects.ensure(16 * cap) || c->boxes.ensure(8 * cap) ||
-        c->src.ensure(8 * cap) || c->pair_off.ensure(8 * cap))
+        c->pair_off.ensure(8 * cap))
       return fail(CS_ENOMEM, "visible-splat buffers (%lld)", (long long)cap);
     c->cap_vis = cap;
   }
   if (c->cap_pairs == 0) c->cap_pairs = std::max<int64_t>(1 << 20, 8 * c->cap_vis);
   if (c->cap_pairs >= (1ll << 30)) c->cap_pairs = (1ll << 30) - 1;
   if (c->pkA.ensure(4 * c->cap_pairs) || c->pvA.ensure(4 * c->cap_pairs) ||
-      c->pkB.ensure(4 * c->cap_pairs) || c->pvB.ensure(4 * c->cap_pairs))
+      c->pkB.ensure(4 * c->cap_pairs) || c->pvB.ensure(4 * c->cap_pairs) ||
+      c->dup_start.ensure(4 * (dup_blocks(c->cap_pairs) + 1)))
     return fail(CS_ENOMEM, "pair buffers (%lld)", (long long)c->cap_pairs);
   const size_t sw = std::max(radix_status_words(c->cap_vis, 8), radix_status_words(c->cap_pairs, 4));
   if (c->st_sort.ensure(4 * sw)) return fail(CS_ENOMEM, "sort status");
@@ -430,29 +435,29 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
   CS_CHECK_LAUNCH();
   if (timed) mark(c, 1, s);
   const int64_t cap = std::max<int64_t>(cap_vis, 1);
-  CS_CUDA(cudaMemsetAsync(c->st_proj.p, 0, 8 * ((cap + 255) / 256 + 1), s));
   const bool debug = (flags & (CS_RENDER_DEBUG | CS_RENDER_PROJECT_ONLY)) != 0;
   if (debug && c->recs.ensure(sizeof(ProjRec) * c->cap_vis)) return fail(CS_ENOMEM, "debug records");
   ProjOutputs po{c->keysA.as<uint64_t>(), c->valsA.as<uint32_t>(), c->hot.as<HotRec>(),
-                 c->rects.as<int4>(), c->boxes.as<short4>(), c->src.as<int64_t>(),
+                 c->rects.as<int4>(), c->boxes.as<short4>(),
                  debug ? c->recs.as<ProjRec>() : nullptr};
-  launch_project(clouds, c->segs.as<Seg>(), stats, *cam, *st, c->st_proj.as<uint64_t>(), cap, po,
-                 list, s);
+  launch_project(clouds, c->segs.as<Seg>(), stats, *cam, *st, cap, po, list, s);
   c->last_debug = debug;
   CS_CHECK_LAUNCH();
   if (timed) mark(c, 2, s);
-  // K4: global depth order (stable => ties keep assembled order)
+  // K4: global depth order over the assembled set (stable => ties keep assembled
+  // order; culled Gaussians carry key ~0 and land behind the M visible ones)
   const int which = radix_sort<uint64_t>(c->keysA.as<uint64_t>(), c->valsA.as<uint32_t>(),
                                          c->keysB.as<uint64_t>(), c->valsB.as<uint32_t>(),
-                                         &stats->visible, cap, 0, 64, c->hist.as<uint32_t>(),
+                                         &stats->assembled, cap, 0, 64, c->hist.as<uint32_t>(),
                                          c->st_sort.as<uint32_t>(), c->sort_tickets.as<uint32_t>(), s);
   CS_CHECK_LAUNCH();
   const uint32_t* order = which ? c->valsB.as<uint32_t>() : c->valsA.as<uint32_t>();
   if (timed) mark(c, 3, s);
   // K5: pair counts in depth order, scanned
-  CS_CUDA(cudaMemsetAsync(c->st_gather.p, 0, 8 * ((cap + 255) / 256 + 1), s));
+  CS_CUDA(cudaMemsetAsync(c->st_gather.p, 0, 8 * (pair_count_chunks(cap) + 1), s));
   launch_pair_count(order, c->rects.as<int4>(), stats, c->cap_pairs, cap,
-                    c->st_gather.as<uint64_t>(), c->pair_off.as<int64_t>(), s);
+                    c->st_gather.as<uint64_t>(), c->pair_off.as<int64_t>(),
+                    c->dup_start.as<uint32_t>(), s);
   CS_CHECK_LAUNCH();
   if (timed) mark(c, 4, s);
   if (flags & CS_RENDER_PROJECT_ONLY) {
@@ -461,7 +466,8 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
     return CS_OK;
   }
   // K6: duplicate
-  launch_duplicate(c->pair_off.as<int64_t>(), order, c->rects.as<int4>(), stats, ntx,
+  launch_duplicate(c->pair_off.as<int64_t>(), order, c->rects.as<int4>(),
+                   c->dup_start.as<uint32_t>(), stats, ntx,
                    c->cap_pairs, c->pkA.as<uint32_t>(), c->pvA.as<uint32_t>(), s);
   CS_CHECK_LAUNCH();
   mark(c, 5, s);
@@ -589,7 +595,7 @@ int cs_render_backward(cs_ctx* c, const cs_source* src, const cs_camera* cam,
   CS_CUDA(cudaMemsetAsync(out->rotations, 0, 16 * K, s));
   CS_CUDA(cudaMemsetAsync(out->opacities, 0, 4 * K, s));
   CS_CUDA(cudaMemsetAsync(out->sh, 0, 12 * (size_t)cl.sh_coeffs * K, s));
-  launch_project_bwd(cl, c->src.as<int64_t>(), c->stats.as<DevStats>(), *cam, *st,
+  launch_project_bwd(cl, c->last_order, c->stats.as<DevStats>(), *cam, *st,
                      c->gacc.as<float>(), cap, *out, s);
   CS_CHECK_LAUNCH();
   return CS_OK;
@@ -717,8 +723,8 @@ int cs_dump_tiles(cs_ctx* c, int64_t* tile_ids, int64_t* offsets, void* stream) 
   int rc = fetch_stats(c, s);
   if (rc) return rc;
   const int64_t P = c->h_stats->pairs;
-  const int64_t M = c->h_stats->visible;
-  if (c->scratch2.ensure(8 * (P + c->last_tiles + 1 + M))) return fail(CS_ENOMEM, "dump");
+  const int64_t NA = c->h_stats->assembled;  // rank_of is indexed by splat id (assembled index)
+  if (c->scratch2.ensure(8 * (P + c->last_tiles + 1 + NA))) return fail(CS_ENOMEM, "dump");
   int64_t* dt = c->scratch2.as<int64_t>();
   int64_t* doff = dt + P;
   int64_t* rank_of = doff + c->last_tiles + 1;

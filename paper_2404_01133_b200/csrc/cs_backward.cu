@@ -3,9 +3,9 @@
 // SPEC.md:76; semantics from SURVEY.md Appendix A "backward-relevant forward
 // semantics").
 //
-// K10 blend backward: one CTA per tile, one thread per pixel, the same
-// batched shared-memory walk over the tile list as the forward, front to
-// back up to the pixel's last accepted fragment (kept by the forward).  The
+// K10 blend backward: the forward's persistent warp-item walk (one 8x4 pixel
+// box of one tile per item, lane = pixel), front to back up to the pixel's
+// last accepted fragment (kept by the forward).  The
 // forward's float64 decisions are re-evaluated identically, so exactly the
 // accepted fragments receive gradient; skipped / dropped fragments get none.
 // With T_k the transmittance before fragment k, P_k the colour accumulated
@@ -13,7 +13,7 @@
 //     dC/dc_k = T_k a_k,   dC/da_k = T_k c_k - S_k / (1 - a_k)
 // and a = min(0.99, o*exp(power)) passes gradient only when unclamped.
 // Per-splat partials (mean2d, conic, opacity, colour) are warp-reduced and
-// accumulated with one atomicAdd per warp into buffers indexed by compact id.
+// accumulated with one atomicAdd per warp into buffers indexed by splat id.
 //
 // K11 projection backward: one thread per visible splat; recomputes the
 // float64 forward (t, J, V, cov2d) and chains the partials to position,
@@ -270,19 +270,19 @@ __device__ void sh_basis_grad(double x, double y, double z, int degree, double Y
 
 __device__ __forceinline__ int deg_of(int c) { return c >= 16 ? 3 : c >= 9 ? 2 : c >= 4 ? 1 : 0; }
 
-// K11: per visible splat (compact id v) -> parameter gradients of its source row.
+// K11: per visible splat (depth rank r -> splat id = cloud row) -> parameter gradients.
 __global__ void __launch_bounds__(128)
-k_project_bwd(const cs_cloud cl, const int64_t* __restrict__ src, const DevStats* __restrict__ stats,
+k_project_bwd(const cs_cloud cl, const uint32_t* __restrict__ order, const DevStats* __restrict__ stats,
               cs_camera cam, cs_settings st, const float* __restrict__ grads, int64_t cap,
               cs_grads out) {
   const int64_t M = stats->visible;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < M;
        r += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = src[r];
+    const int64_t k = order[r];
     const Geom gm = load_geom(cl, k);
     float gin[kGradFields];
 #pragma unroll
-    for (int f = 0; f < kGradFields; ++f) gin[f] = grads[(int64_t)f * cap + r];
+    for (int f = 0; f < kGradFields; ++f) gin[f] = grads[(int64_t)f * cap + k];
     const double* W = cam.R;
     // camera-space position
     double tcam[3];
@@ -432,12 +432,12 @@ void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint32_t* bxs, co
                                            nboxes, bp, dl_dimg, state, ticket, grads, cap);
 }
 
-void launch_project_bwd(const cs_cloud& cl, const int64_t* src,
+void launch_project_bwd(const cs_cloud& cl, const uint32_t* order,
                         const DevStats* stats, const cs_camera& cam, const cs_settings& st,
                         const float* grads, int64_t cap, const cs_grads& out, cudaStream_t s) {
   const int64_t blocks = std::min<int64_t>((cap + 127) / 128, 148 * 16);
   if (blocks <= 0) return;
-  k_project_bwd<<<(unsigned)blocks, 128, 0, s>>>(cl, src, stats, cam, st, grads, cap, out);
+  k_project_bwd<<<(unsigned)blocks, 128, 0, s>>>(cl, order, stats, cam, st, grads, cap, out);
 }
 
 }  // namespace cs

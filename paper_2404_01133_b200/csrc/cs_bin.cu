@@ -12,12 +12,18 @@
 namespace cs {
 
 constexpr int kCountThreads = 256;
+constexpr int kCountItems = 16;                        // ranks per thread
+constexpr int kCountTile = kCountThreads * kCountItems;  // ranks per chunk
+constexpr int kDupTile = 1024;                         // pairs per duplication CTA
 
-// pair_off[r] = sum of pair counts of depth ranks < r (decoupled look-back).
+// pair_off[r] = sum of pair counts of depth ranks < r (single pass: chunks of
+// 4096 ranks, warp-striped so every load is coalesced, decoupled look-back
+// across chunks).  Also records, for every duplication CTA b, the depth rank
+// owning pair b*kDupTile (dup_start[b]), so K6 needs no global binary search.
 __global__ void __launch_bounds__(kCountThreads)
 k_pair_count(const uint32_t* __restrict__ order, const int4* __restrict__ rects,
              DevStats* __restrict__ stats, int64_t pair_cap, uint64_t* __restrict__ status,
-             int64_t* __restrict__ pair_off) {
+             int64_t* __restrict__ pair_off, uint32_t* __restrict__ dup_start) {
   __shared__ int64_t s_chunk;
   __shared__ uint64_t s_scan[kCountThreads / 32 + 1];
   __shared__ uint64_t s_prefix;
@@ -25,21 +31,47 @@ k_pair_count(const uint32_t* __restrict__ order, const int4* __restrict__ rects,
   if (threadIdx.x == 0) s_chunk = atomicAdd(&stats->tickets[2], 1u);
   __syncthreads();
   const int64_t chunk = s_chunk;
-  const int64_t base = chunk * kCountThreads;
+  const int64_t base = chunk * kCountTile;
   if (base >= M) return;
-  const int64_t r = base + threadIdx.x;
-  uint64_t cnt = 0;
-  if (r < M) {
-    const int4 rc = __ldg(rects + __ldg(order + r));
-    cnt = (uint64_t)((int64_t)(rc.y - rc.x + 1) * (int64_t)(rc.w - rc.z + 1));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t wbase = base + (int64_t)warp * (32 * kCountItems);
+  uint64_t cnt[kCountItems];
+  uint32_t c32[kCountItems];  // pair count of each rank (<= n_tiles)
+#pragma unroll
+  for (int i = 0; i < kCountItems; ++i) {
+    const int64_t r = wbase + i * 32 + lane;
+    c32[i] = 0;
+    if (r < M) {
+      const int4 rc = __ldg(rects + __ldg(order + r));
+      c32[i] = (uint32_t)((rc.y - rc.x + 1) * (rc.w - rc.z + 1));
+    }
+    cnt[i] = c32[i];
   }
-  uint64_t total;
-  const uint64_t excl = block_excl_scan<uint64_t>(cnt, s_scan, total);
+  // warp-local exclusive offsets over the warp's 512 consecutive ranks
+  uint64_t run = 0;
+#pragma unroll
+  for (int i = 0; i < kCountItems; ++i) {
+    const uint64_t incl = warp_incl_scan(cnt[i]);
+    const uint64_t c = cnt[i];
+    cnt[i] = run + incl - c;  // now: exclusive offset within the warp
+    run += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  // warp totals -> block-exclusive warp offsets
+  if (lane == 0) s_scan[warp] = run;
+  __syncthreads();
+  if (warp == 0) {
+    const uint64_t w = lane < kCountThreads / 32 ? s_scan[lane] : 0ull;
+    const uint64_t wi = warp_incl_scan(w);
+    if (lane < kCountThreads / 32) s_scan[lane] = wi - w;
+    if (lane == 31) s_scan[kCountThreads / 32] = wi;
+  }
+  __syncthreads();
+  const uint64_t total = s_scan[kCountThreads / 32];
   if (threadIdx.x < 32) {
     const uint64_t pre = lookback_exclusive(status, chunk, total);
     if (threadIdx.x == 0) {
       s_prefix = pre;
-      if (base + kCountThreads >= M) {
+      if (base + kCountTile >= M) {
         const int64_t P = (int64_t)(pre + total);
         stats->pairs = P;
         stats->pairs_eff = P <= pair_cap ? P : 0;
@@ -48,40 +80,43 @@ k_pair_count(const uint32_t* __restrict__ order, const int4* __restrict__ rects,
     }
   }
   __syncthreads();
-  if (r < M) pair_off[r] = (int64_t)(s_prefix + excl);
+  const uint64_t off0 = s_prefix + s_scan[warp];
+#pragma unroll
+  for (int i = 0; i < kCountItems; ++i) {
+    const int64_t r = wbase + i * 32 + lane;
+    if (r >= M) break;
+    const int64_t o = (int64_t)(off0 + cnt[i]);
+    pair_off[r] = o;
+    // duplication CTAs whose first pair lies in [o, o + count)
+    const int64_t c = c32[i];
+    if (o + c <= pair_cap) {
+      for (int64_t b = (o + kDupTile - 1) / kDupTile; b * kDupTile < o + c; ++b) dup_start[b] = (uint32_t)r;
+    }
+  }
 }
 
 constexpr int kDupThreads = 256;
-constexpr int kDupTile = 1024;
 
 // Load-balanced duplication: each CTA owns kDupTile consecutive output pairs;
-// the depth ranks whose pair ranges intersect it are found by binary search
-// and staged in shared memory.  key = tile id, value = compact index.
+// the depth ranks whose pair ranges intersect it (dup_start[b] ..
+// dup_start[b+1], from K5) are staged in shared memory and every pair finds
+// its rank by a binary search there.  key = tile id, value = compact index.
 __global__ void __launch_bounds__(kDupThreads)
 k_duplicate(const int64_t* __restrict__ pair_off, const uint32_t* __restrict__ order,
-            const int4* __restrict__ rects, const DevStats* __restrict__ stats, int ntx,
-            uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+            const int4* __restrict__ rects, const uint32_t* __restrict__ dup_start,
+            const DevStats* __restrict__ stats, int ntx, uint32_t* __restrict__ keys,
+            uint32_t* __restrict__ vals) {
   __shared__ int64_t s_off[kDupTile + 1];
   __shared__ int4 s_rect[kDupTile + 1];
   __shared__ uint32_t s_id[kDupTile + 1];
-  __shared__ int64_t s_rlo, s_rhi;
   const int64_t P = stats->pairs_eff;
   const int64_t M = stats->visible;
   const int64_t p0 = (int64_t)blockIdx.x * kDupTile;
   if (p0 >= P) return;
   const int64_t p1 = min(p0 + kDupTile, P);
-  if (threadIdx.x < 2) {
-    const int64_t target = threadIdx.x == 0 ? p0 : p1 - 1;
-    int64_t lo = 0, hi = M - 1;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi + 1) >> 1;
-      if (pair_off[mid] <= target) lo = mid; else hi = mid - 1;
-    }
-    if (threadIdx.x == 0) s_rlo = lo; else s_rhi = lo;
-  }
-  __syncthreads();
-  const int64_t rlo = s_rlo;
-  const int nr = (int)(s_rhi - rlo + 1);
+  const int64_t rlo = dup_start[blockIdx.x];
+  const int64_t rhi = p1 < P ? (int64_t)dup_start[blockIdx.x + 1] : M - 1;  // owner of pair p1 (>= owner of p1-1)
+  const int nr = (int)(rhi - rlo + 1);
   for (int i = threadIdx.x; i < nr; i += kDupThreads) {
     const uint32_t v = __ldg(order + rlo + i);
     s_off[i] = pair_off[rlo + i];
@@ -123,21 +158,25 @@ __global__ void k_tile_ranges(const uint32_t* __restrict__ keys, const uint32_t*
   }
 }
 
+int64_t pair_count_chunks(int64_t capacity) { return (capacity + kCountTile - 1) / kCountTile; }
+int64_t dup_blocks(int64_t pair_cap) { return (pair_cap + kDupTile - 1) / kDupTile; }
+
 void launch_pair_count(const uint32_t* order, const int4* rects, DevStats* stats, int64_t pair_cap,
-                       int64_t capacity, uint64_t* status, int64_t* pair_off, cudaStream_t s) {
-  const int64_t chunks = (capacity + kCountThreads - 1) / kCountThreads;
+                       int64_t capacity, uint64_t* status, int64_t* pair_off, uint32_t* dup_start,
+                       cudaStream_t s) {
+  const int64_t chunks = pair_count_chunks(capacity);
   if (chunks == 0) return;
   k_pair_count<<<(unsigned)chunks, kCountThreads, 0, s>>>(order, rects, stats, pair_cap, status,
-                                                          pair_off);
+                                                          pair_off, dup_start);
 }
 
 void launch_duplicate(const int64_t* pair_off, const uint32_t* order, const int4* rects,
-                      const DevStats* stats, int ntx, int64_t pair_cap, uint32_t* keys,
-                      uint32_t* vals, cudaStream_t s) {
-  const int64_t blocks = (pair_cap + kDupTile - 1) / kDupTile;
+                      const uint32_t* dup_start, const DevStats* stats, int ntx, int64_t pair_cap,
+                      uint32_t* keys, uint32_t* vals, cudaStream_t s) {
+  const int64_t blocks = dup_blocks(pair_cap);
   if (blocks == 0) return;
-  k_duplicate<<<(unsigned)blocks, kDupThreads, 0, s>>>(pair_off, order, rects, stats, ntx, keys,
-                                                       vals);
+  k_duplicate<<<(unsigned)blocks, kDupThreads, 0, s>>>(pair_off, order, rects, dup_start, stats,
+                                                       ntx, keys, vals);
 }
 
 void launch_tile_ranges(const uint32_t* keys, const uint32_t* vals, const short4* boxes,

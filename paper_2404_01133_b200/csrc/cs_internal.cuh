@@ -1,14 +1,13 @@
 // cs_internal.cuh -- shared device-side types and primitives for libcsgpu.
 //
-// Layouts in HBM; every per-splat array is in
-// compact (ascending assembled-index) order, written once by the projection:
+// Layouts in HBM; every per-splat array is
+// indexed by assembled index (the splat id), written once by the projection:
 //   HotRec    :  80 B -- staged in smem by the blend (quadratic form, opacity,
 //                        colour, fast-reject threshold, cull box)
 //   rect      :  16 B -- tile rectangle (render.py:226-231)
-//   src       :   8 B -- assembled index (depth tie-break, gradient scatter)
-//   keys/vals :  8+4 B -- depth key, compact index (sorted -> depth order)
+//   keys/vals :  8+4 B -- depth key (~0 if culled), splat id (sorted -> depth order)
 //   ProjRec   : 128 B -- full _Projected record, written only in debug/dump mode
-//   pairs     :  u32 tile key + u32 compact index, sorted stably by tile
+//   pairs     :  u32 tile key + u32 splat id, sorted stably by tile
 #pragma once
 #include <cuda_runtime.h>
 
@@ -80,14 +79,14 @@ struct DevStats {     // device mirror of cs_frame_stats + scratch counters
 };
 
 
-// Per-visible-splat outputs of the projection kernel (compact order).
+// Outputs of the projection kernel, indexed by assembled index (splat id);
+// hot/rects/boxes/recs are written for visible splats only.
 struct ProjOutputs {
-  uint64_t* keys;    // depth bits
-  uint32_t* vals;    // compact index
+  uint64_t* keys;    // depth bits (~0 for culled Gaussians)
+  uint32_t* vals;    // splat id
   HotRec* hot;
   int4* rects;
-  short4* boxes;     // copy of HotRec's cull box, dense (8 B) for the blend's warp tests
-  int64_t* src;
+  short4* boxes;     // copy of HotRec's cull box, dense (8 B)
   ProjRec* recs;     // optional (debug / dumps)
 };
 

@@ -1,10 +1,11 @@
-// cs_project.cu -- K3: EWA projection + SH colour + visible-set compaction.
+// cs_project.cu -- K3: EWA projection + SH colour + cull.
 //
 // Replaces render._project_cloud (render.py:111-188) up to the depth sort.
-// One thread per assembled Gaussian; chunks of 256 assembled indices are
-// handed out in launch order and compacted with a decoupled look-back scan, so
-// visible splats land in ascending assembled order (the np.nonzero order of
-// render.py:121/163) in a single pass over HBM.
+// One thread per assembled Gaussian, outputs at its assembled index; culled
+// Gaussians get the depth key ~0, so the stable depth sort (K4) yields the
+// visible set in (depth, assembled index) order -- the np.nonzero order of
+// render.py:121/163 followed by the stable argsort of render.py:176-177 --
+// with no compaction pass.
 //
 // All decision math (cull, mean, covariance, conic, radii, on-image test) is
 // float64 written with explicit round-to-nearest intrinsics in numpy's
@@ -205,24 +206,20 @@ __device__ __forceinline__ ProjOut project_one(const Geom& g, const cs_camera& c
 
 constexpr int kProjThreads = 256;
 
-// Single-pass projection + stable compaction.  Every output array is written
-// once, in compact (ascending assembled-index) order; the depth sort then
-// only permutes (key, compact index) pairs and nothing is gathered again.
+// Projection, one thread per assembled Gaussian, no compaction: every
+// per-splat output is written at the Gaussian's assembled index i (its
+// "splat id"), and a culled Gaussian gets the depth key ~0, which the stable
+// depth sort (K4) moves behind every visible one.  So the sort's first M
+// values are the visible splat ids in (depth, assembled index) order, and the
+// kernel needs no block scan or cross-CTA look-back (LoD assembly already
+// drops invisible blocks: ~97% of the assembled set is visible on C3).
 __global__ void __launch_bounds__(kProjThreads, 3)
 k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
           DevStats* __restrict__ stats, cs_camera cam, cs_settings st,
-          uint64_t* __restrict__ status, ProjOutputs po_out, const uint64_t* __restrict__ list) {
-  __shared__ int64_t s_chunk;
-  __shared__ uint32_t s_scan[kProjThreads / 32 + 1];
-  __shared__ uint32_t s_skip[kProjThreads / 32];
-  __shared__ uint64_t s_prefix;
+          ProjOutputs po_out, const uint64_t* __restrict__ list) {
   const int64_t n = stats->assembled;
-  if (threadIdx.x == 0) s_chunk = atomicAdd(&stats->tickets[0], 1u);
-  __syncthreads();
-  const int64_t chunk = s_chunk;
-  const int64_t base = chunk * kProjThreads;
-  if (base >= n) return;
-  const int64_t i = base + threadIdx.x;
+  const int64_t i = blockIdx.x * (int64_t)kProjThreads + threadIdx.x;
+  if (blockIdx.x * (int64_t)kProjThreads >= n) return;  // CTA-uniform
   ProjOut po;
   po.in_front = po.ok = po.keep = false;
   Geom g;
@@ -242,25 +239,18 @@ k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
     po = project_one(g, cam, st);
   }
   // skipped_singular: in front but det <= 1e-12 (render.py:146-148)
-  uint32_t skip = (po.in_front && !po.ok) ? 1u : 0u;
-  uint32_t wskip = warp_sum(skip);
-  if (lane_id() == 0) s_skip[threadIdx.x >> 5] = wskip;
-  uint32_t total;
-  uint32_t excl = block_excl_scan<uint32_t>(po.keep ? 1u : 0u, s_scan, total);
-  if (threadIdx.x < 32) {
-    uint32_t ws = threadIdx.x < kProjThreads / 32 ? s_skip[threadIdx.x] : 0u;
-    ws = warp_sum(ws);
-    uint64_t pre = lookback_exclusive(status, chunk, total);
-    if (threadIdx.x == 0) {
-      s_prefix = pre;
-      if (ws) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->skipped),
-                        (unsigned long long)ws);
-      if (base + kProjThreads >= n) stats->visible = (int64_t)(pre + total);
-    }
+  const uint32_t kb = __ballot_sync(0xffffffffu, po.keep);
+  const uint32_t sb = __ballot_sync(0xffffffffu, po.in_front && !po.ok);
+  if (lane_id() == 0) {
+    if (kb) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->visible), (unsigned long long)__popc(kb));
+    if (sb) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->skipped), (unsigned long long)__popc(sb));
   }
-  __syncthreads();
+  if (i >= n) return;
+  // z > near > 0: the float64 bits are monotone; culled -> ~0 (sorts last)
+  po_out.keys[i] = po.keep ? (uint64_t)__double_as_longlong(po.z) : ~0ull;
+  po_out.vals[i] = (uint32_t)i;
   if (!po.keep) return;
-  const uint64_t idx = s_prefix + excl;
+  const int64_t idx = i;
   const cs_cloud& cd = clouds[cloud_id];
   // view direction and SH colour (render.py:167-169, core.py:166-172)
   double dx = g.px - cam.center[0], dy = g.py - cam.center[1], dz = g.pz - cam.center[2];
@@ -314,9 +304,6 @@ k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
     const int64_t ty1 = clip_i64(np_to_i64(floor(ddiv(dsub(dadd(po.my, po.ry), 0.5), ts))), 0, nty - 1);
     po_out.rects[idx] = make_int4((int)tx0, (int)tx1, (int)ty0, (int)ty1);
   }
-  po_out.src[idx] = i;
-  po_out.keys[idx] = (uint64_t)__double_as_longlong(po.z);  // z > near > 0: bits are monotone
-  po_out.vals[idx] = (uint32_t)idx;
   if (po_out.recs) {  // debug / dump mode: the full _Projected record (render.py:89-108)
     ProjRec rec;
     rec.mx = po.mx; rec.my = po.my; rec.c0 = c0; rec.c1 = c1; rec.c2 = c2;
@@ -340,12 +327,11 @@ __global__ void k_setup_cloud(cs_cloud c, cs_cloud* clouds, Seg* segs, DevStats*
 }
 
 void launch_project(const cs_cloud* d_clouds, const Seg* d_segs, DevStats* d_stats,
-                    const cs_camera& cam, const cs_settings& st, uint64_t* status,
-                    int64_t capacity, const ProjOutputs& out, const uint64_t* list, cudaStream_t s) {
-  const int64_t chunks = (capacity + kProjThreads - 1) / kProjThreads;
-  if (chunks == 0) return;
-  k_project<<<(unsigned)chunks, kProjThreads, 0, s>>>(d_clouds, d_segs, d_stats, cam, st, status,
-                                                      out, list);
+                    const cs_camera& cam, const cs_settings& st, int64_t capacity,
+                    const ProjOutputs& out, const uint64_t* list, cudaStream_t s) {
+  const int64_t blocks = (capacity + kProjThreads - 1) / kProjThreads;
+  if (blocks == 0) return;
+  k_project<<<(unsigned)blocks, kProjThreads, 0, s>>>(d_clouds, d_segs, d_stats, cam, st, out, list);
 }
 
 void launch_setup_cloud(const cs_cloud& c, cs_cloud* d_clouds, Seg* d_segs, DevStats* d_stats,
