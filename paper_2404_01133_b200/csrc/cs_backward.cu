@@ -71,6 +71,9 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
             uint32_t* __restrict__ ticket, float* __restrict__ grads /* [kGradFields][cap] */,
             int64_t cap) {
   __shared__ __align__(16) HotRec s_hot[kBwdThreads / 32][2][32];
+  __shared__ double s_exp[64];
+  load_exp_table(s_exp);
+  __syncthreads();
   const int ts = bp.tile_size;
   const uint32_t lane = lane_id();
   const uint32_t lt_mask = (1u << lane) - 1u;
@@ -132,7 +135,7 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
               dsub(dmul(-0.5, dadd(dmul(dmul(h.c0, dx), dx), dmul(dmul(h.c2, dy), dy))),
                    dmul(dmul(h.c1, dx), dy));
           if (power >= (double)h.lthr) {
-            const double G = exp(power);
+            const double G = exp_le0(power, s_exp);
             double alpha = dmul(h.opacity, G);
             const bool clamped = alpha > 0.99;
             if (clamped) alpha = 0.99;

@@ -48,6 +48,9 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
         int nboxes, BlendParams bp, OutT* __restrict__ out, int32_t* __restrict__ frag_tile,
         DevStats* __restrict__ stats, BlendState state) {
   __shared__ __align__(16) HotRec s_hot[kBlendThreads / 32][2][32];
+  __shared__ double s_exp[64];
+  load_exp_table(s_exp);
+  __syncthreads();
   const int ts = bp.tile_size;
   const uint32_t lane = lane_id();
   const uint32_t lt_mask = (1u << lane) - 1u;
@@ -98,7 +101,7 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
             dsub(dmul(-0.5, dadd(dmul(dmul(h.c0, dx), dx), dmul(dmul(h.c2, dy), dy))),
                  dmul(dmul(h.c1, dx), dy));
         if (power < (double)h.lthr) continue;  // alpha < alpha_floor guaranteed
-        double alpha = dmul(h.opacity, exp(power));  // _kernels.py:58
+        double alpha = dmul(h.opacity, exp_le0(power, s_exp));  // _kernels.py:58
         if (alpha > 0.99) alpha = 0.99;              // _kernels.py:59-60
         if (alpha < bp.alpha_floor) continue;        // _kernels.py:61-62
         const double nt = dmul(T, dsub(1.0, alpha));

@@ -152,6 +152,50 @@ __device__ __forceinline__ int box_pixel(int b, int lane, int ts) {
   return b * 32 + lane;
 }
 
+// ---------------------------------------------------------------------------
+// exp(x) for the blend's x = power in [lthr, 0] (lthr >= log(alpha_floor) - 1e-6
+// > -745): x = (64 m + j) ln2/64 + r, |r| <= ln2/128, exp(x) = 2^m 2^(j/64) p(r)
+// with p the degree-6 Taylor polynomial (truncation < 2e-20) and 2^(j/64)
+// from a 64-entry table kept in shared memory.  ~1 ulp like CUDA's exp(),
+// which is itself not bit-identical to the reference's libm exp: both only
+// matter at exact alpha-floor / transmittance knife-edges.
+__constant__ double c_exp2_64[64] = {
+    1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284,
+    1.0442737824274138, 1.0556451783605572, 1.0671404006768237, 1.0787607977571199,
+    1.0905077326652577, 1.102382583307841, 1.1143867425958924, 1.1265216186082418,
+    1.1387886347566916, 1.1511892299529827, 1.1637248587775775, 1.1763969916502812,
+    1.189207115002721, 1.202156731452703, 1.215247359980469, 1.22848053610687,
+    1.241857812073484, 1.255380757024691, 1.2690509571917332, 1.2828700160787783,
+    1.2968395546510096, 1.3109612115247644, 1.3252366431597413, 1.339667524053303,
+    1.3542555469368927, 1.3690024229745905, 1.383909881963832, 1.3989796725383112,
+    1.4142135623730951, 1.42961333839197, 1.4451808069770467, 1.460917794180647,
+    1.4768261459394993, 1.4929077282912648, 1.5091644275934228, 1.5255981507445384,
+    1.5422108254079407, 1.559004400237837, 1.5759808451078865, 1.593142151342267,
+    1.6104903319492543, 1.6280274218573478, 1.645755478153965, 1.6636765803267364,
+    1.681792830507429, 1.7001063537185235, 1.718619298122478, 1.7373338352737062,
+    1.7562521603732995, 1.7753764925265212, 1.7947090750031072, 1.8142521755003989,
+    1.8340080864093424, 1.8539791250833855, 1.8741676341103, 1.8945759815869656,
+    1.9152065613971474, 1.9360617934922943, 1.9571441241754002, 1.978456026387951};
+
+__device__ __forceinline__ void load_exp_table(double* s_tab) {
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) s_tab[i] = c_exp2_64[i];
+}
+
+__device__ __forceinline__ double exp_le0(double x, const double* s_tab) {
+  const double kd = rint(x * 92.33248261689366);          // 64 / ln2
+  double r = fma(kd, -0.010830424696905538, x);           // ln2/64, high 33 bits
+  r = fma(kd, 6.563929801064195e-13, r);                  // ln2/64, low part
+  double p = fma(r, 1.0 / 720.0, 1.0 / 120.0);
+  p = fma(p, r, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const int k = (int)kd;
+  const double scale = __longlong_as_double((long long)((k >> 6) + 1023) << 52);  // 2^m, m = floor(k/64)
+  return (s_tab[k & 63] * p) * scale;
+}
+
 // grid of a persistent kernel: as many CTAs as are co-resident on all SMs
 template <typename K>
 static int persistent_grid(K kernel, int threads) {

@@ -113,14 +113,28 @@ k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
   const uint32_t my_count = chunk_hist[d];
   uint32_t* my_status = status + chunk * 256 + d;
   atomicExch(my_status, (chunk == 0 ? kStFlagPre : kStFlagAgg) | my_count);
-  // 2) stable in-warp ranks (warp order == input order)
+  // 2) stable in-warp ranks (warp order == input order).  The lanes holding
+  //    the same digit: 8 ballots (one per digit bit) for 64-bit keys, where
+  //    __match_any_sync (a multi-cycle MIO op) measured ~10% slower;
+  //    __match_any_sync for 32-bit keys, where it measured faster.
   const uint32_t lt = lanemask_lt();
 #pragma unroll
   for (int r = 0; r < kItems; ++r) {
     const int64_t idx = wbase + r * 32 + lane;
     const bool valid = idx < n;
-    const uint32_t dg = valid ? (uint32_t)((key[r] >> shift) & 255) : 256u + lane;
-    const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+    const uint32_t dg = (uint32_t)((key[r] >> shift) & 255);
+    uint32_t peers;
+    if (sizeof(K) == 8) {
+      peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const bool bit = (dg >> b) & 1u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? bal : ~bal;
+      }
+    } else {
+      peers = __match_any_sync(0xffffffffu, valid ? dg : 256u + lane);
+    }
     const uint32_t pr = __popc(peers & lt);
     uint32_t old = 0;
     if (valid) old = warp_hist[warp][dg];
