@@ -47,6 +47,13 @@ template <typename K>
 int radix_sort(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_dev, int64_t capacity,
                int begin_bit, int end_bit, uint32_t* hist, uint32_t* status, uint32_t* tickets,
                cudaStream_t s);
+// cs_depth.cu
+void launch_fix_depth_runs(const uint32_t* k32_sorted, uint32_t* order, const uint64_t* k64,
+                           const DevStats* stats, int64_t capacity, void* ctl_mem,
+                           uint32_t* long_runs, uint32_t long_cap, uint32_t* scratch,
+                           cudaStream_t s);
+size_t fix_ctl_bytes();
+int64_t fix_long_cap(int64_t capacity);
 // cs_train.cu
 void launch_training_loss(const float* img, const float* ref, int H, int W, double lam,
                           float* maps, double* acc, double* loss, float* grad, cudaStream_t s);
@@ -181,6 +188,7 @@ struct cs_ctx {
   DBuf stats, clouds1, segs, dec;
   DBuf st_gather, st_pw, st_fuse, st_sort, hist, sort_tickets, fuse_ticket;
   DBuf keysA, valsA, keysB, valsB, recs;
+  DBuf k32A, k32B, long_runs, fix_ctl;          // K4 32-bit depth sort + K4b run fix-up
   DBuf hot, boxes, rects, pair_off, tile_order;
   DBuf pkA, pvA, pkB, pvB, ranges, frag_tile, pw_list;
   DBuf st_t, st_last, st_acc;
@@ -246,7 +254,8 @@ void cs_destroy(cs_ctx* c) {
   cudaDeviceSynchronize();
   DBuf* all[] = {&c->stats, &c->clouds1, &c->segs, &c->dec, &c->st_gather,
                  &c->st_pw, &c->st_fuse, &c->st_sort, &c->hist, &c->sort_tickets,
-                 &c->fuse_ticket, &c->keysA, &c->valsA, &c->keysB, &c->valsB, &c->recs, &c->hot,
+                 &c->fuse_ticket, &c->keysA, &c->valsA, &c->keysB, &c->valsB, &c->recs, &c->k32A, &c->k32B,
+                 &c->long_runs, &c->fix_ctl, &c->hot,
                  &c->tile_order, &c->boxes, &c->rects, &c->pair_off, &c->pkA, &c->pvA, &c->pkB,
                  &c->pvB, &c->ranges, &c->frag_tile, &c->pw_list, &c->st_t, &c->st_last,
                  &c->st_acc, &c->gacc, &c->dup_start, &c->loss_maps, &c->loss_acc, &c->scratch1, &c->scratch2, &c->scratch3, &c->scratch4};
@@ -329,6 +338,8 @@ static int ensure_frame_buffers(cs_ctx* c, int64_t cap_vis, int n_segs, int n_bl
     const int64_t chunks = (cap + 255) / 256 + 1;
     if (c->st_gather.ensure(8 * chunks) ||
         c->keysA.ensure(8 * cap) || c->keysB.ensure(8 * cap) || c->valsA.ensure(4 * cap) ||
+        c->k32A.ensure(4 * cap) || c->k32B.ensure(4 * cap) ||
+        c->long_runs.ensure(4 * fix_long_cap(cap)) || c->fix_ctl.ensure(fix_ctl_bytes()) ||
         c->valsB.ensure(4 * cap) || c->hot.ensure(sizeof(HotRec) * cap) ||
         c->rects.ensure(16 * cap) || c->boxes.ensure(8 * cap) ||
         c->pair_off.ensure(8 * cap))
@@ -437,21 +448,29 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
   const int64_t cap = std::max<int64_t>(cap_vis, 1);
   const bool debug = (flags & (CS_RENDER_DEBUG | CS_RENDER_PROJECT_ONLY)) != 0;
   if (debug && c->recs.ensure(sizeof(ProjRec) * c->cap_vis)) return fail(CS_ENOMEM, "debug records");
-  ProjOutputs po{c->keysA.as<uint64_t>(), c->valsA.as<uint32_t>(), c->hot.as<HotRec>(),
+  ProjOutputs po{c->keysA.as<uint64_t>(), c->k32A.as<uint32_t>(), c->valsA.as<uint32_t>(),
+                 c->hot.as<HotRec>(),
                  c->rects.as<int4>(), c->boxes.as<short4>(),
                  debug ? c->recs.as<ProjRec>() : nullptr};
   launch_project(clouds, c->segs.as<Seg>(), stats, *cam, *st, cap, po, list, s);
   c->last_debug = debug;
   CS_CHECK_LAUNCH();
   if (timed) mark(c, 2, s);
-  // K4: global depth order over the assembled set (stable => ties keep assembled
-  // order; culled Gaussians carry key ~0 and land behind the M visible ones)
-  const int which = radix_sort<uint64_t>(c->keysA.as<uint64_t>(), c->valsA.as<uint32_t>(),
-                                         c->keysB.as<uint64_t>(), c->valsB.as<uint32_t>(),
-                                         &stats->assembled, cap, 0, 64, c->hist.as<uint32_t>(),
+  // K4: global depth order over the assembled set: stable 32-bit radix sort of
+  // the float32-rounded depth (culled Gaussians carry ~0 and land behind the M
+  // visible ones), then K4b re-sorts runs of equal float32 depth by (float64
+  // depth, splat id) -- the exact stable argsort of render.py:176-177.
+  const int which = radix_sort<uint32_t>(c->k32A.as<uint32_t>(), c->valsA.as<uint32_t>(),
+                                         c->k32B.as<uint32_t>(), c->valsB.as<uint32_t>(),
+                                         &stats->assembled, cap, 0, 32, c->hist.as<uint32_t>(),
                                          c->st_sort.as<uint32_t>(), c->sort_tickets.as<uint32_t>(), s);
   CS_CHECK_LAUNCH();
-  const uint32_t* order = which ? c->valsB.as<uint32_t>() : c->valsA.as<uint32_t>();
+  uint32_t* order = which ? c->valsB.as<uint32_t>() : c->valsA.as<uint32_t>();
+  const uint32_t* k32s = which ? c->k32B.as<uint32_t>() : c->k32A.as<uint32_t>();
+  launch_fix_depth_runs(k32s, order, c->keysA.as<uint64_t>(), stats, cap, c->fix_ctl.p,
+                        c->long_runs.as<uint32_t>(), (uint32_t)fix_long_cap(cap),
+                        c->keysB.as<uint32_t>(), s);
+  CS_CHECK_LAUNCH();
   if (timed) mark(c, 3, s);
   // K5: pair counts in depth order, scanned
   CS_CUDA(cudaMemsetAsync(c->st_gather.p, 0, 8 * (pair_count_chunks(cap) + 1), s));

@@ -71,7 +71,7 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
             uint32_t* __restrict__ ticket, float* __restrict__ grads /* [kGradFields][cap] */,
             int64_t cap) {
   __shared__ __align__(16) HotRec s_hot[kBwdThreads / 32][2][32];
-  __shared__ double s_exp[64];
+  __shared__ double2 s_exp[64];
   load_exp_table(s_exp);
   __syncthreads();
   const int ts = bp.tile_size;

@@ -48,7 +48,7 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
         int nboxes, BlendParams bp, OutT* __restrict__ out, int32_t* __restrict__ frag_tile,
         DevStats* __restrict__ stats, BlendState state) {
   __shared__ __align__(16) HotRec s_hot[kBlendThreads / 32][2][32];
-  __shared__ double s_exp[64];
+  __shared__ double2 s_exp[64];
   load_exp_table(s_exp);
   __syncthreads();
   const int ts = bp.tile_size;

@@ -5,7 +5,8 @@
 //   HotRec    :  80 B -- staged in smem by the blend (quadratic form, opacity,
 //                        colour, fast-reject threshold, cull box)
 //   rect      :  16 B -- tile rectangle (render.py:226-231)
-//   keys/vals :  8+4 B -- depth key (~0 if culled), splat id (sorted -> depth order)
+//   keys      :  8 B  -- float64 depth bits (~0 if culled), exact tie-break of K4b
+//   keys32/vals: 4+4 B -- float32-rounded depth, splat id (radix-sorted, K4)
 //   ProjRec   : 128 B -- full _Projected record, written only in debug/dump mode
 //   pairs     :  u32 tile key + u32 splat id, sorted stably by tile
 #pragma once
@@ -82,7 +83,8 @@ struct DevStats {     // device mirror of cs_frame_stats + scratch counters
 // Outputs of the projection kernel, indexed by assembled index (splat id);
 // hot/rects/boxes/recs are written for visible splats only.
 struct ProjOutputs {
-  uint64_t* keys;    // depth bits (~0 for culled Gaussians)
+  uint64_t* keys;    // float64 depth bits (~0 for culled Gaussians), for the exact run fix-up
+  uint32_t* keys32;  // float32-rounded depth bits (~0 for culled): the radix-sorted key
   uint32_t* vals;    // splat id
   HotRec* hot;
   int4* rects;
@@ -154,46 +156,66 @@ __device__ __forceinline__ int box_pixel(int b, int lane, int ts) {
 
 // ---------------------------------------------------------------------------
 // exp(x) for the blend's x = power in [lthr, 0] (lthr >= log(alpha_floor) - 1e-6
-// > -745): x = (64 m + j) ln2/64 + r, |r| <= ln2/128, exp(x) = 2^m 2^(j/64) p(r)
-// with p the degree-6 Taylor polynomial (truncation < 2e-20) and 2^(j/64)
-// from a 64-entry table kept in shared memory.  ~1 ulp like CUDA's exp(),
-// which is itself not bit-identical to the reference's libm exp: both only
-// matter at exact alpha-floor / transmittance knife-edges.
-__constant__ double c_exp2_64[64] = {
-    1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284,
-    1.0442737824274138, 1.0556451783605572, 1.0671404006768237, 1.0787607977571199,
-    1.0905077326652577, 1.102382583307841, 1.1143867425958924, 1.1265216186082418,
-    1.1387886347566916, 1.1511892299529827, 1.1637248587775775, 1.1763969916502812,
-    1.189207115002721, 1.202156731452703, 1.215247359980469, 1.22848053610687,
-    1.241857812073484, 1.255380757024691, 1.2690509571917332, 1.2828700160787783,
-    1.2968395546510096, 1.3109612115247644, 1.3252366431597413, 1.339667524053303,
-    1.3542555469368927, 1.3690024229745905, 1.383909881963832, 1.3989796725383112,
-    1.4142135623730951, 1.42961333839197, 1.4451808069770467, 1.460917794180647,
-    1.4768261459394993, 1.4929077282912648, 1.5091644275934228, 1.5255981507445384,
-    1.5422108254079407, 1.559004400237837, 1.5759808451078865, 1.593142151342267,
-    1.6104903319492543, 1.6280274218573478, 1.645755478153965, 1.6636765803267364,
-    1.681792830507429, 1.7001063537185235, 1.718619298122478, 1.7373338352737062,
-    1.7562521603732995, 1.7753764925265212, 1.7947090750031072, 1.8142521755003989,
-    1.8340080864093424, 1.8539791250833855, 1.8741676341103, 1.8945759815869656,
-    1.9152065613971474, 1.9360617934922943, 1.9571441241754002, 1.978456026387951};
+// > -745): x = (64 m + j) ln2/64 + r, |r| <= ln2/128, exp(x) = 2^m 2^(j/64) (1 + q(r))
+// with q the degree-6 Taylor polynomial minus 1 (truncation < 2e-20) and
+// 2^(j/64) = hi + lo from a 64-entry table kept in shared memory; the result
+// is formed as hi + (hi q + lo), ~0.5 ulp like a libm exp (measured max 0.5x
+// ulp over [-6, 0], tools/exp_check.cu).  Neither this, CUDA's exp() nor the
+// reference's libm exp are bit-identical to each other: they differ only at
+// exact alpha-floor / transmittance knife-edges.
+__constant__ double2 c_exp2_64[64] = {
+    {1.0, 0.0}, {1.0108892860517005, -1.5234778603368577e-17},
+    {1.0218971486541166, 5.109225028973444e-17}, {1.0330248790212284, 7.600838874027088e-18},
+    {1.0442737824274138, 8.551889705537965e-17}, {1.0556451783605572, 1.759325738772092e-18},
+    {1.0671404006768237, -7.899853966841582e-17}, {1.0787607977571199, -6.656660436056593e-17},
+    {1.0905077326652577, -3.046782079812471e-17}, {1.102382583307841, 5.2660368715706944e-17},
+    {1.1143867425958924, 1.0410278456845571e-16}, {1.1265216186082418, 5.165856758795457e-17},
+    {1.1387886347566916, 8.912812676025408e-17}, {1.1511892299529827, 3.250710218863827e-17},
+    {1.1637248587775775, 3.8292048369240935e-17}, {1.1763969916502812, 5.554203254218079e-17},
+    {1.189207115002721, 3.982015231465646e-17}, {1.202156731452703, 6.644981499252301e-17},
+    {1.215247359980469, -7.712630692681488e-17}, {1.22848053610687, -1.89878163130253e-17},
+    {1.241857812073484, 4.658027591836937e-17}, {1.255380757024691, -6.7113898212968784e-18},
+    {1.2690509571917332, 2.667932131342186e-18}, {1.2828700160787783, 1.713594918243561e-17},
+    {1.2968395546510096, 2.5382502794888315e-17}, {1.3109612115247644, -7.181536135519454e-17},
+    {1.3252366431597413, -2.8587312100388614e-17}, {1.339667524053303, 8.927282594831732e-17},
+    {1.3542555469368927, 7.70094837980299e-17}, {1.3690024229745905, 9.593797919118849e-17},
+    {1.383909881963832, -6.770511658794786e-17}, {1.3989796725383112, -9.614213209051323e-17},
+    {1.4142135623730951, -9.667293313452913e-17}, {1.42961333839197, -1.2031642489053655e-17},
+    {1.4451808069770467, -3.0237581349939873e-17}, {1.460917794180647, -5.600377186075216e-17},
+    {1.4768261459394993, -3.483994556892796e-17}, {1.4929077282912648, 1.4192920154284036e-17},
+    {1.5091644275934228, -1.016455327754295e-16}, {1.5255981507445384, -1.1024941712342561e-16},
+    {1.5422108254079407, 7.949834809697621e-17}, {1.559004400237837, 3.7812070533575275e-17},
+    {1.5759808451078865, -1.0136916471278304e-17}, {1.593142151342267, -1.0094406542311964e-16},
+    {1.6104903319492543, 2.4707192569797888e-17}, {1.6280274218573478, -6.712955084707084e-17},
+    {1.645755478153965, -1.0125679913674773e-16}, {1.6636765803267364, 5.8909926967131e-17},
+    {1.681792830507429, 8.199010020581497e-17}, {1.7001063537185235, -8.0237193703977e-18},
+    {1.718619298122478, -1.851380418263111e-17}, {1.7373338352737062, 3.164389299292957e-17},
+    {1.7562521603732995, 2.960140695448873e-17}, {1.7753764925265212, 6.429731796556572e-17},
+    {1.7947090750031072, 1.8227458427912087e-17}, {1.8142521755003989, -9.969531538920349e-17},
+    {1.8340080864093424, 3.283107224245627e-17}, {1.8539791250833855, 9.761887490727594e-17},
+    {1.8741676341103, -6.122763413004143e-17}, {1.8945759815869656, 3.4034035352165297e-17},
+    {1.9152065613971474, -1.0619946056195963e-16}, {1.9360617934922943, 1.0332385960676326e-16},
+    {1.9571441241754002, 8.960767791036668e-17}, {1.978456026387951, 4.0388753109278167e-17}
+};
 
-__device__ __forceinline__ void load_exp_table(double* s_tab) {
+__device__ __forceinline__ void load_exp_table(double2* s_tab) {
   for (int i = threadIdx.x; i < 64; i += blockDim.x) s_tab[i] = c_exp2_64[i];
 }
 
-__device__ __forceinline__ double exp_le0(double x, const double* s_tab) {
+__device__ __forceinline__ double exp_le0(double x, const double2* s_tab) {
   const double kd = rint(x * 92.33248261689366);          // 64 / ln2
   double r = fma(kd, -0.010830424696905538, x);           // ln2/64, high 33 bits
   r = fma(kd, 6.563929801064195e-13, r);                  // ln2/64, low part
-  double p = fma(r, 1.0 / 720.0, 1.0 / 120.0);
-  p = fma(p, r, 1.0 / 24.0);
-  p = fma(p, r, 1.0 / 6.0);
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
+  double q = fma(r, 1.0 / 720.0, 1.0 / 120.0);
+  q = fma(q, r, 1.0 / 24.0);
+  q = fma(q, r, 1.0 / 6.0);
+  q = fma(q, r, 0.5);
+  q = fma(q, r, 1.0);
+  q = q * r;                                              // exp(r) - 1
   const int k = (int)kd;
+  const double2 t = s_tab[k & 63];
   const double scale = __longlong_as_double((long long)((k >> 6) + 1023) << 52);  // 2^m, m = floor(k/64)
-  return (s_tab[k & 63] * p) * scale;
+  return (t.x + fma(t.x, q, t.y)) * scale;
 }
 
 // grid of a persistent kernel: as many CTAs as are co-resident on all SMs

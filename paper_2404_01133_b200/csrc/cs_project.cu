@@ -248,6 +248,8 @@ k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
   if (i >= n) return;
   // z > near > 0: the float64 bits are monotone; culled -> ~0 (sorts last)
   po_out.keys[i] = po.keep ? (uint64_t)__double_as_longlong(po.z) : ~0ull;
+  // float32 rounding is monotone: the 32-bit sort is a coarsening of the exact order
+  po_out.keys32[i] = po.keep ? __float_as_uint(__double2float_rn(po.z)) : 0xffffffffu;
   po_out.vals[i] = (uint32_t)i;
   if (!po.keep) return;
   const int64_t idx = i;

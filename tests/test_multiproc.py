@@ -1,0 +1,117 @@
+"""World-size-2 CPU (gloo) tests of the multi-GPU host logic.
+
+* fusion.fuse_all_gather: each rank filters the blocks it owns (membership
+  from the C oracle here, the CUDA kernel on the box), the kept rows are
+  exchanged block-ordered; every rank must end with rows byte-identical to
+  the CPU fuse() of all blocks (partition.py:570-587), for the golden 9-block
+  fusion fixture and LPT and round-robin ownership.
+* lpt_assign / the bench's view split: deterministic, balanced, complete.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, owner, result_q):
+    import sys
+    sys.path.insert(0, os.path.dirname(HERE))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as O
+        from paper_2404_01133_b200 import fusion
+        g = np.load(os.path.join(HERE, "golden", "fuse.npz"))
+        pmin, pmax, dims = g["p_min"], g["p_max"], tuple(int(d) for d in g["dims"])
+        n_blocks = int(np.prod(dims))
+        local = {}
+        C = 0
+        for j in range(n_blocks):
+            if owner[j] != rank or f"block{j}/positions" not in g:
+                continue
+            t = lambda k: torch.from_numpy(np.ascontiguousarray(g[f"block{j}/{k}"]))
+            local[j] = (t("positions"), t("opacities"), t("scales"), t("rotations"), t("sh"))
+            C = int(g[f"block{j}/sh"].shape[2])
+        Cs = [0] * world
+        dist.all_gather_object(Cs, C)
+        C = max(Cs)
+        filt = lambda pos, j: torch.from_numpy(
+            np.nonzero(O.block_of_points(pos.numpy(), pmin, pmax, dims) == j)[0])
+        fused = fusion.fuse_all_gather(local, n_blocks, owner, pmin, pmax, dims, sh_coeffs=C, filter_fn=filt)
+        result_q.put((rank, fused.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def _expected():
+    from oracle import oracle as O
+    from paper_2404_01133_b200 import fusion
+    g = np.load(os.path.join(HERE, "golden", "fuse.npz"))
+    pmin, pmax, dims = g["p_min"], g["p_max"], tuple(int(d) for d in g["dims"])
+    from types import SimpleNamespace
+    blocks = []
+    for j in range(int(np.prod(dims))):
+        if f"block{j}/positions" in g:
+            blocks.append((SimpleNamespace(**{k: g[f"block{j}/{k}"] for k in
+                                              ("positions", "opacities", "scales", "rotations", "sh")}), j))
+    ref = O.fuse(blocks, pmin, pmax, dims)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a))
+    return fusion.pack_rows(t(ref.positions), t(ref.opacities), t(ref.scales), t(ref.rotations), t(ref.sh)).numpy()
+
+
+@pytest.mark.parametrize("policy", ["lpt", "round_robin"])
+def test_fuse_all_gather_gloo_world2(policy):
+    from paper_2404_01133_b200.train import lpt_assign
+    g = np.load(os.path.join(HERE, "golden", "fuse.npz"))
+    n_blocks = int(np.prod(g["dims"]))
+    sizes = [int(g[f"block{j}/positions"].shape[0]) if f"block{j}/positions" in g else 0 for j in range(n_blocks)]
+    owner = lpt_assign(sizes, 2) if policy == "lpt" else [j % 2 for j in range(n_blocks)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, owner, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = _expected()
+    for r in range(2):
+        assert got[r].shape == want.shape
+        assert got[r].tobytes() == want.tobytes(), r
+
+
+def test_lpt_assign_balanced_and_deterministic():
+    from paper_2404_01133_b200.train import lpt_assign
+    rng = np.random.default_rng(0)
+    sizes = rng.integers(300_000, 1_000_000, 36).tolist()
+    for n in (1, 2, 4, 8):
+        own = lpt_assign(sizes, n)
+        assert own == lpt_assign(sizes, n) and set(own) <= set(range(n)) and len(own) == 36
+        loads = [sum(s for s, o in zip(sizes, own) if o == r) for r in range(n)]
+        assert max(loads) <= sum(sizes) / n + max(sizes)   # LPT bound
+        if n == 8:
+            assert max(loads) / (sum(sizes) / n) < 1.15
+
+
+def test_view_split_covers_flythrough():
+    # bench.py: rank r renders frames i with i * world // n == r (contiguous, complete, disjoint)
+    for n_frames in (60, 740):
+        for world in (1, 2, 4, 8):
+            shares = [[i for i in range(n_frames) if i * world // n_frames == r] for r in range(world)]
+            assert sorted(sum(shares, [])) == list(range(n_frames))
+            assert max(map(len, shares)) - min(map(len, shares)) <= 1

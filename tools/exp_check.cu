@@ -8,7 +8,7 @@
 #include "../paper_2404_01133_b200/csrc/cs_internal.cuh"
 
 __global__ void k_probe(int n, const double* x, double* mine, double* cuda) {
-  __shared__ double tab[64];
+  __shared__ double2 tab[64];
   cs::load_exp_table(tab);
   __syncthreads();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
