@@ -160,17 +160,46 @@ class ClockSampler:
 
 
 def stage_bytes(st: dict) -> dict:
-    """Algorithmic HBM bytes of each stage summed over the measured frames."""
+    """Algorithmic HBM bytes of each stage summed over the measured frames
+    (every array read or written once per pass)."""
     na, m, p = st["assembled"], st["visible"], st["pairs"]
-    sh_bytes = st["sh_bytes_visible"]
     return {
-        "project": na * 48 + sh_bytes + m * (128 + 8 + 4),
-        "depth_sort": m * 8 + 8 * 2 * m * 12,                 # histogram read + 8 passes r/w
-        "gather_scan": m * (4 + 128 + 48 + 32 + 16 + 8 + 8),
-        "duplicate": m * 24 + p * 8,
-        "tile_sort": p * 4 + 2 * 2 * p * 8,                   # histogram read + 2 passes r/w
-        "ranges": p * 4,
+        # per assembled: 3 fp32 quads (48 B) + depth keys (8 + 4) + id (4);
+        # per visible: its SH row (level width) + HotRec 80 + rect 16 + cull box 8
+        "project": na * (48 + 16) + st["sh_bytes_visible"] + m * (80 + 16 + 8),
+        # 4 LSD passes over (u32 key, u32 id) + one histogram read + run check
+        "depth_sort": na * 4 + 4 * 2 * na * 8 + m * 4,
+        # per visible: id + rect gather + pair offset write
+        "gather_scan": m * (4 + 16 + 8),
+        # per pair: (tile, id) written; per visible: offset, id, rect staged
+        "duplicate": p * 8 + m * 28,
+        # 2 LSD passes over (u32 tile, u32 id) + one histogram read
+        "tile_sort": p * 4 + 2 * 2 * p * 8,
+        # per pair: key + id read, cull box gathered (8) and written pair-major (8)
+        "ranges": p * (4 + 4 + 8 + 8),
     }
+
+
+def blend_flops(st: dict) -> float:
+    """Algorithmic float64 flops of the blend: per
+    evaluated (pixel, splat) the quadratic form (2 sub + 7 mul + 2 add = 11);
+    per accepted fragment exp (3 mul/add + 9 FMA = 21) and alpha/T/colour
+    (4 mul/add + 3 FMA = 10)."""
+    return 11.0 * st["evals"] + 31.0 * st["fragments"]
+
+
+def ncu_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full
+    capture (profiles/*_frame_traffic.json, newest), or None."""
+    files = sorted((ROOT / "profiles").glob("*_frame_traffic.json"))
+    if not files:
+        return None, None
+    data = json.loads(files[-1].read_text())
+    hits = [v for k, v in data.items() if k.startswith(kernel)]
+    if not hits:
+        return None, files[-1].name
+    launches = [x for lst in hits for x in lst]
+    return sum(x["dram_bytes"] for x in launches) / len(launches), files[-1].name
 
 
 def main():
@@ -222,6 +251,11 @@ def main():
     for i in range(min(len(ccams), max(K, 1))):
         s = CsFrameStats()
         frame(i, _lib.CS_RENDER_SYNC, s)
+    from paper_2404_01133_b200.device import sh_stride
+    row_bytes = [4 * sh_stride(lc.sh_coeffs) for lc in scene.level_clouds]
+    seg_idx = (ctypes.c_int32 * 4096)()
+    seg_cnt = (ctypes.c_int64 * 4096)()
+    n_seg = ctypes.c_int32(0)
     for i in range(K):
         s = CsFrameStats()
         frame(i, _lib.CS_RENDER_SYNC, s)
@@ -230,9 +264,11 @@ def main():
         counts["pairs"] += s.pairs
         counts["evals"] += s.evals
         counts["fragments"] += s.fragments
-    # SH bytes read per visible splat depend on its level (C = 16/9/4 -> 192/108/48 B);
-    # bounded by the finest width, estimated from the assembled level mix
-    counts["sh_bytes_visible"] = counts["visible"] * 12 * 9
+        # SH rows are read for visible splats; their width depends on the level
+        # (C = 16/9/4 -> 192/112/48 B): weight by this frame's assembled level mix
+        _lib.check(lib.cs_dump_segments(ctx, seg_idx, seg_cnt, 4096, ctypes.byref(n_seg), sh))
+        sh_assembled = sum(seg_cnt[q] * row_bytes[seg_idx[q] // scene.n_blocks] for q in range(n_seg.value))
+        counts["sh_bytes_visible"] += sh_assembled * (s.visible / max(s.assembled, 1))
     for i in range(args.warmup):
         frame(i)
     torch.cuda.synchronize()
@@ -295,25 +331,40 @@ def main():
 
     clocks = clk.summary()
     value = world * K / (ms_max / 1000.0)
-    # roofline of the dominant kernel
+    # roofline of the dominant kernel (+ every HBM-bound stage)
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_peak = peaks.get("hbm_gbs", 6450.0)
     bytes_ = stage_bytes(counts)
     dom = max(STAGES, key=lambda k: stages_ms[k])
-    roof = {}
+    stage_roof = {k: {"bytes_per_frame": v / K, "ms": stages_ms[k],
+                      "achieved_gbs": (v / K) / (stages_ms[k] / 1000.0) / 1e9 if stages_ms[k] else None}
+                  for k, v in bytes_.items()}
+    for v in stage_roof.values():
+        v["frac"] = v["achieved_gbs"] / hbm_peak if v["achieved_gbs"] else None
     if dom in bytes_:
-        achieved = (bytes_[dom] / K) / (stages_ms[dom] / 1000.0) / 1e9
+        achieved = stage_roof[dom]["achieved_gbs"]
+        traffic, tsrc = ncu_traffic({"project": "k_project", "depth_sort": "k_onesweep",
+                                     "tile_sort": "k_onesweep", "duplicate": "k_duplicate",
+                                     "gather_scan": "k_pair_count", "ranges": "k_tile_ranges"}[dom])
         roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None,
-                "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback"}
-    else:  # blend: float64 pipe (quadratic form per evaluation, exact path per fragment)
-        fp64_peak = 148 * 64 * 2 * (clocks.get("sm_mhz") or 1965.0) * 1e6 / 1e12  # TFLOP/s at observed clock
-        flops = (22.0 * counts["evals"] + 60.0 * counts["fragments"]) / K
-        achieved = flops / (stages_ms[dom] / 1000.0) / 1e12
-        roof = {"kernel": dom, "bound": "fp64", "achieved": achieved, "peak": fp64_peak,
-                "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": None,
-                "peak_source": "nominal 148 SM x 64 DFMA/clk at the sampled SM clock"}
-    roof["stage_bytes_per_frame"] = {k: v / K for k, v in bytes_.items()}
+                "frac": achieved / hbm_peak, "traffic": traffic,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "B200_PROFILING.md fallback"}
+    else:  # blend: float64-pipe bound (quadratic form per evaluation, exp + alpha/T per fragment)
+        sm_mhz = clocks.get("sm_mhz") or 1965.0
+        fp64_peak = 148 * 64 * 2 * sm_mhz * 1e6 / 1e12  # TFLOP/s: 148 SM x 64 DFMA/clk x 2 at the sampled clock
+        achieved = blend_flops(counts) / K / (stages_ms[dom] / 1000.0) / 1e12
+        traffic, tsrc = ncu_traffic("k_blend")
+        roof = {"kernel": "k_blend", "bound": "fp64", "achieved": achieved, "peak": fp64_peak,
+                "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": traffic,
+                "peak_source": "148 SM x 64 FP64 FMA/clk x 2 at the sampled SM clock (no FP64 entry in "
+                               "MEASURED_PEAKS.json)",
+                "flops_per_frame": blend_flops(counts) / K}
+    roof["traffic_source"] = f"profiles/{tsrc} (ncu --set full, dram__bytes_read+write per launch)" if tsrc else None
+    roof["stages_hbm"] = stage_roof
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(scene, cams_all, settings, n_frames=1)
 
     train = None
     if not args.no_train:
@@ -321,10 +372,6 @@ def main():
         torch.cuda.empty_cache()
         train = train_leg(args, raw, wh, rank, world, dev)
         raw = None
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(scene, cams_all, settings, n_frames=1)
 
     if rank == 0:
         line = {
@@ -378,8 +425,10 @@ def train_leg(args, raw, wh, rank, world, dev):
     setup_s = time.perf_counter() - t0
     order = [jobs[j] for j in owned if j in jobs]
     stream = torch.cuda.current_stream(dev)
+    per_block = {jb.j: [] for jb in order}
     for i in range(args.train_warmup):
-        order[i % len(order)].step()
+        jb = order[i % len(order)]
+        per_block[jb.j].append(jb.step().clone())
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -394,7 +443,8 @@ def train_leg(args, raw, wh, rank, world, dev):
         job = order[i % len(order)]
         v = job.iters % len(job.cams)
         job.iters += 1
-        losses.append(job.trainer.step(job.cams[v], job.targets[v], events=ev[i]))
+        losses.append(job.trainer.step(job.cams[v], job.targets[v], events=ev[i]).clone())
+        per_block[job.j].append(losses[-1])
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
@@ -423,7 +473,10 @@ def train_leg(args, raw, wh, rank, world, dev):
         "metric": "block-train iters/s (C4)", "value": world * K / (ms_max / 1000.0), "unit": "iters/s",
         "ms_per_iter": ms_max / K, "steps": K, "warmup": args.train_warmup, "n_gpus": world,
         "scaling": "weak", "phases_ms": phases,
-        "loss_first_last": [float(losses[0]), float(losses[-1])],
+        # mean over blocks of each block's first / last training loss (same view cycle)
+        "loss_first_last_mean": [float(np.mean([float(v[0]) for v in per_block.values() if v])),
+                                 float(np.mean([float(v[-1]) for v in per_block.values() if v]))],
+        "iters_per_block": float(np.mean([len(v) for v in per_block.values()])),
         "config": {"workload": f"{n_blocks} blocks of the {args.scene} scene (LPT over ranks), "
                                f"{args.train_views} orbit views/block at {wh[0]}x{wh[1]}",
                    "blocks_this_rank": len(order),

@@ -71,8 +71,8 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
             uint32_t* __restrict__ ticket, float* __restrict__ grads /* [kGradFields][cap] */,
             int64_t cap) {
   __shared__ __align__(16) HotRec s_hot[kBwdThreads / 32][2][32];
-  __shared__ double2 s_exp[64];
-  load_exp_table(s_exp);
+  __shared__ ExpTable s_exp;
+  const ExpCoef ec = load_exp_table(&s_exp);
   __syncthreads();
   const int ts = bp.tile_size;
   const uint32_t lane = lane_id();
@@ -134,8 +134,8 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
           const double power =
               dsub(dmul(-0.5, dadd(dmul(dmul(h.c0, dx), dx), dmul(dmul(h.c2, dy), dy))),
                    dmul(dmul(h.c1, dx), dy));
-          if (power >= (double)h.lthr) {
-            const double G = exp_le0(power, s_exp);
+          if (power >= h.lthr) {
+            const double G = exp_le0(power, s_exp, ec);
             double alpha = dmul(h.opacity, G);
             const bool clamped = alpha > 0.99;
             if (clamped) alpha = 0.99;

@@ -48,8 +48,8 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
         int nboxes, BlendParams bp, OutT* __restrict__ out, int32_t* __restrict__ frag_tile,
         DevStats* __restrict__ stats, BlendState state) {
   __shared__ __align__(16) HotRec s_hot[kBlendThreads / 32][2][32];
-  __shared__ double2 s_exp[64];
-  load_exp_table(s_exp);
+  __shared__ ExpTable s_exp;
+  const ExpCoef ec = load_exp_table(&s_exp);
   __syncthreads();
   const int ts = bp.tile_size;
   const uint32_t lane = lane_id();
@@ -80,7 +80,8 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
     }
     if (x0 > x1) continue;  // no pixel of this box in the image (warp-uniform)
     const double sx = (double)px + 0.5, sy = (double)py + 0.5;  // _kernels.py:43-45
-    double T = 1.0, cr = 0.0, cg = 0.0, cb = 0.0;
+    double T = 1.0;
+    float cr = 0.f, cg = 0.f, cb = 0.f;  // colour accumulates in float32 (SURVEY.md H2 recipe m3)
     int cnt = 0;
     int64_t last = s0;
     bool done = !valid;
@@ -100,16 +101,16 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
         const double power =
             dsub(dmul(-0.5, dadd(dmul(dmul(h.c0, dx), dx), dmul(dmul(h.c2, dy), dy))),
                  dmul(dmul(h.c1, dx), dy));
-        if (power < (double)h.lthr) continue;  // alpha < alpha_floor guaranteed
-        double alpha = dmul(h.opacity, exp_le0(power, s_exp));  // _kernels.py:58
+        if (power < h.lthr) continue;  // alpha < alpha_floor guaranteed
+        double alpha = dmul(h.opacity, exp_le0(power, s_exp, ec));  // _kernels.py:58
         if (alpha > 0.99) alpha = 0.99;              // _kernels.py:59-60
         if (alpha < bp.alpha_floor) continue;        // _kernels.py:61-62
         const double nt = dmul(T, dsub(1.0, alpha));
         if (nt < bp.t_floor) { done = true; continue; }  // _kernels.py:63-66
-        const double w = dmul(T, alpha);
-        cr += w * (double)h.r;
-        cg += w * (double)h.g;
-        cb += w * (double)h.b;
+        const float w = (float)dmul(T, alpha);
+        cr = fmaf(w, h.r, cr);
+        cg = fmaf(w, h.g, cg);
+        cb = fmaf(w, h.b, cb);
         T = nt;
         cnt += 1;
         last = k0 + src + 1;
@@ -165,7 +166,7 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
     __syncwarp();
     if (valid) {
       const int64_t pix = (int64_t)py * bp.width + px;
-      double o[3] = {cr + T * bp.bg[0], cg + T * bp.bg[1], cb + T * bp.bg[2]};
+      double o[3] = {(double)cr + T * bp.bg[0], (double)cg + T * bp.bg[1], (double)cb + T * bp.bg[2]};
       if (!(bp.flags & CS_RENDER_NO_CLIP)) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) o[c] = o[c] < 0.0 ? 0.0 : (o[c] > 1.0 ? 1.0 : o[c]);
@@ -176,9 +177,9 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
       if (KEEP) {
         state.final_t[pix] = T;
         state.last[pix] = (int32_t)last;
-        state.color_acc[3 * pix] = cr;
-        state.color_acc[3 * pix + 1] = cg;
-        state.color_acc[3 * pix + 2] = cb;
+        state.color_acc[3 * pix] = (double)cr;
+        state.color_acc[3 * pix + 1] = (double)cg;
+        state.color_acc[3 * pix + 2] = (double)cb;
       }
     }
     const int box_frags = warp_sum(valid ? cnt : 0);
@@ -274,11 +275,9 @@ __global__ void k_pack_records(int64_t m, const double* means, const double* con
     h.r = (float)colors[3 * s]; h.g = (float)colors[3 * s + 1]; h.b = (float)colors[3 * s + 2];
     const double lt = o > 0.0 ? log(alpha_floor / o) - 1e-6
                               : __longlong_as_double(0x7ff0000000000000ll);
-    h.lthr = __double2float_rd(lt);
+    h.lthr = (double)__double2float_rd(lt);
     h.id = (uint32_t)s;
-    h.pad = 0;
-    h.bx0 = h.by0 = -1;     // full-image box
-    h.bx1 = h.by1 = 32000;
+    h.pad[0] = h.pad[1] = 0;
     hot[s] = h;
   }
 }

@@ -272,29 +272,27 @@ k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
   h.mx = po.mx; h.my = po.my; h.c0 = c0; h.c1 = c1; h.c2 = c2;
   h.opacity = g.op;
   h.r = (float)col[0]; h.g = (float)col[1]; h.b = (float)col[2];
-  h.lthr = lthr;
+  h.lthr = (double)lthr;
   h.id = (uint32_t)idx;
-  h.pad = 0;
+  h.pad[0] = h.pad[1] = 0;
   // Pixel box of {d : power(d) >= lthr} = {d^T Q d <= 2L}, L = -lthr: the
   // ellipse's AABB half-extents are sqrt(2 L a), sqrt(2 L c) with
   // (a, b, c) = Q^-1 = cov2d + low pass; inflated (1e-4 relative + 1e-3 px)
   // to cover rounding of the float64 power.  Pixel px is inside when its
   // centre px + 0.5 lies in [mx - hx, mx + hx].
   const double L = -(double)lthr;
+  short4 box = make_short4(32000, -1, 32000, -1);  // empty: never intersects
   if (L > 0.0) {
     const double hx = sqrt(2.0 * L * po.a) * (1.0 + 1e-4) + 1e-3;
     const double hy = sqrt(2.0 * L * po.c) * (1.0 + 1e-4) + 1e-3;
     const double lim = 32000.0;
-    h.bx0 = (int16_t)fmin(fmax(ceil(po.mx - hx - 0.5), -1.0), lim);
-    h.bx1 = (int16_t)fmin(fmax(floor(po.mx + hx - 0.5), -1.0), lim);
-    h.by0 = (int16_t)fmin(fmax(ceil(po.my - hy - 0.5), -1.0), lim);
-    h.by1 = (int16_t)fmin(fmax(floor(po.my + hy - 0.5), -1.0), lim);
-  } else {  // empty: never intersects
-    h.bx0 = h.by0 = 32000;
-    h.bx1 = h.by1 = -1;
+    box.x = (int16_t)fmin(fmax(ceil(po.mx - hx - 0.5), -1.0), lim);
+    box.y = (int16_t)fmin(fmax(floor(po.mx + hx - 0.5), -1.0), lim);
+    box.z = (int16_t)fmin(fmax(ceil(po.my - hy - 0.5), -1.0), lim);
+    box.w = (int16_t)fmin(fmax(floor(po.my + hy - 0.5), -1.0), lim);
   }
   po_out.hot[idx] = h;
-  po_out.boxes[idx] = make_short4(h.bx0, h.bx1, h.by0, h.by1);
+  po_out.boxes[idx] = box;
   // tile rectangle exactly as numpy (render.py:226-231): floor, astype(int64), clip
   {
     const int64_t ntx = (cam.width + st.tile_size - 1) / st.tile_size;

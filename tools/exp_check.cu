@@ -8,11 +8,11 @@
 #include "../paper_2404_01133_b200/csrc/cs_internal.cuh"
 
 __global__ void k_probe(int n, const double* x, double* mine, double* cuda) {
-  __shared__ double2 tab[64];
-  cs::load_exp_table(tab);
+  __shared__ cs::ExpTable tab;
+  const cs::ExpCoef ec = cs::load_exp_table(&tab);
   __syncthreads();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    mine[i] = cs::exp_le0(x[i], tab);
+    mine[i] = cs::exp_le0(x[i], tab, ec);
     cuda[i] = exp(x[i]);
   }
 }
