@@ -247,7 +247,8 @@ def main():
 
     # sizing pass (synchronous, grows pair buffers) + per-frame counts for the roofline
     K = args.steps
-    counts = dict(assembled=0, visible=0, pairs=0, evals=0, fragments=0, sh_bytes_visible=0)
+    counts = dict(assembled=0, visible=0, pairs=0, evals=0, fragments=0, sh_bytes_visible=0, warp_hits=0,
+                  warp_hits_empty=0)
     for i in range(min(len(ccams), max(K, 1))):
         s = CsFrameStats()
         frame(i, _lib.CS_RENDER_SYNC, s)
@@ -264,6 +265,8 @@ def main():
         counts["pairs"] += s.pairs
         counts["evals"] += s.evals
         counts["fragments"] += s.fragments
+        counts["warp_hits"] += s.warp_hits
+        counts["warp_hits_empty"] += s.warp_hits_empty
         # SH rows are read for visible splats; their width depends on the level
         # (C = 16/9/4 -> 192/112/48 B): weight by this frame's assembled level mix
         _lib.check(lib.cs_dump_segments(ctx, seg_idx, seg_cnt, 4096, ctypes.byref(n_seg), sh))

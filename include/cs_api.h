@@ -82,6 +82,8 @@ typedef struct cs_frame_stats {
   int32_t n_segments;       /* (level, block) pieces concatenated */
   int32_t status;           /* bit0 pair-buffer overflow, bit1 CS_ERANGE */
   int64_t evals;            /* blend evaluations E (pixel x splat pairs walked) */
+  int64_t warp_hits;        /* blend (8x4 pixel box, splat) pairs evaluated by a warp */
+  int64_t warp_hits_empty;  /* ... of which no live pixel passed the alpha-floor test */
 } cs_frame_stats;
 
 /* One block decision, VisibilityDecision (lod.py:255-264). level -1 = None. */

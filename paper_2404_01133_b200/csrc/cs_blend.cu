@@ -55,7 +55,7 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
   const uint32_t lane = lane_id();
   const uint32_t lt_mask = (1u << lane) - 1u;
   HotRec (*wbuf)[32] = s_hot[threadIdx.x >> 5];
-  long long frags = 0, evals = 0;
+  long long frags = 0, evals = 0, whits = 0, whits_empty = 0;
   for (;;) {
     int item = 0;
     if (lane == 0) item = (int)atomicAdd(&stats->tickets[4], 1u);
@@ -93,15 +93,19 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
         const int src = __ffs(mask) - 1;
         mask &= mask - 1;
         const HotRec& h = buf[slot++];
-        if (done) continue;
-        ++evals;
-        const double dx = dsub(sx, h.mx);
-        const double dy = dsub(sy, h.my);
-        // -0.5 * (c0*dx*dx + c2*dy*dy) - c1*dx*dy   (_kernels.py:54-57)
-        const double power =
-            dsub(dmul(-0.5, dadd(dmul(dmul(h.c0, dx), dx), dmul(dmul(h.c2, dy), dy))),
-                 dmul(dmul(h.c1, dx), dy));
-        if (power < h.lthr) continue;  // alpha < alpha_floor guaranteed
+        ++whits;
+        double power = -1e300;
+        if (!done) {
+          ++evals;
+          const double dx = dsub(sx, h.mx);
+          const double dy = dsub(sy, h.my);
+          // -0.5 * (c0*dx*dx + c2*dy*dy) - c1*dx*dy   (_kernels.py:54-57)
+          power = dsub(dmul(-0.5, dadd(dmul(dmul(h.c0, dx), dx), dmul(dmul(h.c2, dy), dy))),
+                       dmul(dmul(h.c1, dx), dy));
+        }
+        const bool pass = power >= h.lthr;  // else alpha < alpha_floor guaranteed
+        if (!__any_sync(0xffffffffu, pass)) ++whits_empty;
+        if (!pass) continue;
         double alpha = dmul(h.opacity, exp_le0(power, s_exp, ec));  // _kernels.py:58
         if (alpha > 0.99) alpha = 0.99;              // _kernels.py:59-60
         if (alpha < bp.alpha_floor) continue;        // _kernels.py:61-62
@@ -188,6 +192,9 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
   }
   evals = warp_sum(evals);
   if (lane == 0) {
+    if (whits) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->warp_hits), (unsigned long long)whits);
+    if (whits_empty)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&stats->warp_hits_empty), (unsigned long long)whits_empty);
     if (frags) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->fragments), (unsigned long long)frags);
     if (evals) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->evals), (unsigned long long)evals);
   }

@@ -74,6 +74,8 @@ struct DevStats {     // device mirror of cs_frame_stats + scratch counters
   int32_t n_segs;
   int32_t status;
   int64_t evals;         // blend (pixel, splat) evaluations executed (E)
+  int64_t warp_hits;     // blend (box, splat) warp evaluations
+  int64_t warp_hits_empty;  // ... where no live pixel passed the fast reject
   int64_t pairs_eff;     // pairs actually processed (0 when the pair buffer overflowed)
   uint32_t tickets[16];  // chunk tickets for single-pass kernels, zeroed per frame
 };
