@@ -63,13 +63,13 @@ __global__ void k_radix_hist_scan(uint32_t* hist, int n_passes) {
   }
 }
 
-template <typename K>
+template <typename K, int ITEMS = SortCfg<K>::kItems>
 __global__ void __launch_bounds__(kSortThreads)
 k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
            K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
            const int64_t* __restrict__ n_ptr, int shift, const uint32_t* __restrict__ digit_base,
            uint32_t* __restrict__ status, uint32_t* __restrict__ ticket) {
-  constexpr int kItems = SortCfg<K>::kItems;
+  constexpr int kItems = ITEMS;
   constexpr int kTile = kSortThreads * kItems;
   __shared__ uint32_t warp_hist[kSortWarps][256];
   __shared__ uint32_t chunk_hist[256];
@@ -211,13 +211,13 @@ size_t radix_status_words(int64_t capacity, int key_bytes) {
 // Sorts (keys, vals) of length *n_dev (<= capacity) by bits [begin_bit, end_bit).
 // Ping-pongs between (k0,v0) and (k1,v1); returns 1 when the result is in
 // (k1,v1), 0 when in (k0,v0).
-template <typename K>
+template <typename K, int ITEMS = SortCfg<K>::kItems>
 int radix_sort(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_dev, int64_t capacity,
                int begin_bit, int end_bit, uint32_t* hist, uint32_t* status, uint32_t* tickets,
                cudaStream_t s) {
   const int n_passes = (end_bit - begin_bit + 7) / 8;
   if (n_passes <= 0 || capacity <= 0) return 0;
-  constexpr int kTile = kSortThreads * SortCfg<K>::kItems;
+  constexpr int kTile = kSortThreads * ITEMS;
   const int64_t chunks = (capacity + kTile - 1) / kTile;
   cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 256 * n_passes, s);
   cudaMemsetAsync(tickets, 0, sizeof(uint32_t) * n_passes, s);
@@ -228,7 +228,7 @@ int radix_sort(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_dev, i
   uint32_t* vin = v0; uint32_t* vout = v1;
   for (int p = 0; p < n_passes; ++p) {
     cudaMemsetAsync(status, 0, sizeof(uint32_t) * 256 * chunks, s);
-    k_onesweep<K><<<(unsigned)chunks, kSortThreads, 0, s>>>(kin, vin, kout, vout, n_dev,
+    k_onesweep<K, ITEMS><<<(unsigned)chunks, kSortThreads, 0, s>>>(kin, vin, kout, vout, n_dev,
                                                            begin_bit + 8 * p, hist + 256 * p,
                                                            status, tickets + p);
     K* tk = kin; kin = kout; kout = tk;
