@@ -211,10 +211,10 @@ size_t radix_status_words(int64_t capacity, int key_bytes) {
 // Sorts (keys, vals) of length *n_dev (<= capacity) by bits [begin_bit, end_bit).
 // Ping-pongs between (k0,v0) and (k1,v1); returns 1 when the result is in
 // (k1,v1), 0 when in (k0,v0).
-template <typename K, int ITEMS = SortCfg<K>::kItems>
-int radix_sort(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_dev, int64_t capacity,
-               int begin_bit, int end_bit, uint32_t* hist, uint32_t* status, uint32_t* tickets,
-               cudaStream_t s) {
+template <typename K, int ITEMS>
+int radix_sort_items(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_dev,
+                     int64_t capacity, int begin_bit, int end_bit, uint32_t* hist,
+                     uint32_t* status, uint32_t* tickets, cudaStream_t s) {
   const int n_passes = (end_bit - begin_bit + 7) / 8;
   if (n_passes <= 0 || capacity <= 0) return 0;
   constexpr int kTile = kSortThreads * ITEMS;
@@ -235,6 +235,14 @@ int radix_sort(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_dev, i
     uint32_t* tv = vin; vin = vout; vout = tv;
   }
   return (n_passes & 1) ? 1 : 0;
+}
+
+template <typename K>
+int radix_sort(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_dev, int64_t capacity,
+               int begin_bit, int end_bit, uint32_t* hist, uint32_t* status, uint32_t* tickets,
+               cudaStream_t s) {
+  return radix_sort_items<K, SortCfg<K>::kItems>(k0, v0, k1, v1, n_dev, capacity, begin_bit,
+                                                 end_bit, hist, status, tickets, s);
 }
 
 template int radix_sort<uint64_t>(uint64_t*, uint32_t*, uint64_t*, uint32_t*, const int64_t*,

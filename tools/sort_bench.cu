@@ -38,7 +38,7 @@ static void run(const char* name, std::vector<K> keys, int bits, int reps) {
     cudaMemcpy(v0, idx.data(), 4 * n, cudaMemcpyHostToDevice);
     cudaDeviceSynchronize();
     cudaEventRecord(e0);
-    which = cs::radix_sort<K, V>(k0, v0, k1, v1, dn, n, 0, bits, hist, status, tickets, 0);
+    which = cs::radix_sort_items<K, V>(k0, v0, k1, v1, dn, n, 0, bits, hist, status, tickets, 0);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
