@@ -1,6 +1,7 @@
 """Build libcsgpu.so (sm_100a only) in-tree with nvcc.
 
-    python -m paper_2404_01133_b200._build [--force]
+    python paper_2404_01133_b200/_build.py [--force]
+    (not ``python -m``: importing the package loads the library first)
 
 Each .cu in csrc/ is compiled with
 ``-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo`` and the objects are
