@@ -66,3 +66,32 @@ def test_depth_runs_exact(seed):
     rimg, rstats = O.rasterize_stats(cloud, cam, st)
     assert stats.blended_fragments == rstats["blended_fragments"]
     assert np.abs(img.pixels - rimg).max() <= 1e-4
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_needle_splats_box_masks(seed):
+    """Thin, long, randomly rotated splats stress K8's exact ellipse-vs-box
+    mask: a box the alpha-floor ellipse reaches must never be skipped, so the
+    accepted-fragment count and image must still equal the oracle's."""
+    import paper_2404_01133_b200 as cs
+    from oracle import oracle as O
+    from paper_2404_01133_b200.core import CameraView, GaussianCloud
+    rng = np.random.default_rng(100 + seed)
+    W, H = 256, 192
+    f = 0.9 * W
+    cam = CameraView(W, H, f, f, W / 2.0 + 0.37, H / 2.0 - 0.21, np.eye(3), np.zeros(3))
+    k = 3000
+    z = rng.uniform(2.0, 30.0, k)
+    u = rng.uniform(-0.1 * W, 1.1 * W, k)
+    v = rng.uniform(-0.1 * H, 1.1 * H, k)
+    pos = np.stack([(u - cam.cx) / f * z, (v - cam.cy) / f * z, z], axis=1)
+    q = rng.normal(size=(k, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    sc = np.stack([rng.uniform(0.001, 0.01, k), rng.uniform(0.2, 3.0, k), rng.uniform(0.001, 0.01, k)], axis=1)
+    cloud = GaussianCloud(pos, rng.uniform(0.05, 1.0, k), sc, q, rng.normal(0.0, 0.3, (k, 3, 4)))
+    st = cs.RenderSettings()
+    img, stats = cs.rasterize_stats(cloud, cam, st)
+    rimg, rstats = O.rasterize_stats(cloud, cam, st)
+    assert stats.visible_splats == rstats["visible_splats"]
+    assert stats.blended_fragments == rstats["blended_fragments"]
+    assert np.abs(img.pixels - rimg).max() <= 1e-4
