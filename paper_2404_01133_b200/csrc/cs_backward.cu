@@ -63,7 +63,7 @@ __device__ __forceinline__ float warp_transpose_sum9(const float (&in)[kGradFiel
 // `last` of its pixels.  Per evaluated hit each lane re-derives the forward's
 // float64 decisions for its pixel; when any lane contributes, the nine
 // partials are warp-reduced and lane 0 adds them with one atomic each.
-__global__ void __launch_bounds__(kBwdThreads)
+__global__ void __launch_bounds__(kBwdThreads, 3)
 k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
             const uint32_t* __restrict__ bys, const uint2* __restrict__ ranges,
             const HotRec* __restrict__ hot, const uint32_t* __restrict__ tile_order, int n_items,
@@ -94,17 +94,21 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
     int x0 = valid ? px : 1 << 20, x1 = valid ? px : -(1 << 20);
     int y0 = valid ? py : 1 << 20, y1 = valid ? py : -(1 << 20);
     int64_t my_end = s0;
-    double g[3] = {0.0, 0.0, 0.0}, acc[3] = {0.0, 0.0, 0.0}, Tend = 1.0;
+    // Only the accept decision (power, exp, alpha floor) must replay the
+    // forward's float64 arithmetic; the partials themselves are float32.
+    float g[3] = {0.f, 0.f, 0.f}, acc[3] = {0.f, 0.f, 0.f}, Tend = 1.f;
     if (valid) {
       const int64_t pix = (int64_t)py * bp.width + px;
       my_end = state.last[pix];
-      Tend = state.final_t[pix];
+      const double te = state.final_t[pix];
+      Tend = (float)te;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        acc[c] = state.color_acc[3 * pix + c];
-        const double o = acc[c] + Tend * bp.bg[c];  // unclipped pixel value
+        const double a = state.color_acc[3 * pix + c];
+        acc[c] = (float)a;
+        const double o = a + te * bp.bg[c];  // unclipped pixel value
         // clip to [0, 1] (render.py:273): gradient passes where 0 <= C <= 1
-        g[c] = (o >= 0.0 && o <= 1.0) ? (double)dl_dimg[3 * pix + c] : 0.0;
+        g[c] = (o >= 0.0 && o <= 1.0) ? dl_dimg[3 * pix + c] : 0.f;
       }
     }
     int wend = (int)my_end;
@@ -119,7 +123,8 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
     if (x0 > x1) continue;  // warp-uniform
     const int64_t e1 = min((int64_t)wend, s1);
     const double sx = (double)px + 0.5, sy = (double)py + 0.5;
-    double T = 1.0, P[3] = {0.0, 0.0, 0.0};
+    const float bg[3] = {(float)bp.bg[0], (float)bp.bg[1], (float)bp.bg[2]};
+    float T = 1.f, P[3] = {0.f, 0.f, 0.f};
 
     auto eval_round = [&](const HotRec* buf, uint32_t mask, int64_t k0) {
       int slot = 0;
@@ -141,26 +146,27 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
             if (clamped) alpha = 0.99;
             if (alpha >= bp.alpha_floor) {
               contrib = true;
-              const double col[3] = {h.r, h.g, h.b};
-              const double w = T * alpha;
-              double dl_da = 0.0;
-              const double inv = 1.0 / (1.0 - alpha);
+              const float a = (float)alpha;
+              const float w = T * a;
+              const float inv = 1.f / (1.f - a);
+              const float col[3] = {h.r, h.g, h.b};
+              float dl_da = 0.f;
 #pragma unroll
               for (int c = 0; c < 3; ++c) {
-                P[c] += w * col[c];
-                const double S = (acc[c] - P[c]) + Tend * bp.bg[c];
+                P[c] = fmaf(w, col[c], P[c]);
+                const float S = (acc[c] - P[c]) + Tend * bg[c];
                 dl_da += g[c] * (T * col[c] - S * inv);
-                gr[6 + c] = (float)(w * g[c]);
+                gr[6 + c] = w * g[c];
               }
-              const float dl_dpow = clamped ? 0.f : (float)(dl_da * alpha);
+              const float dl_dpow = clamped ? 0.f : dl_da * a;
               const float fdx = (float)dx, fdy = (float)dy;
-              gr[5] = clamped ? 0.f : (float)(dl_da * G);
+              gr[5] = clamped ? 0.f : dl_da * (float)G;
               gr[0] = dl_dpow * ((float)h.c0 * fdx + (float)h.c1 * fdy);
               gr[1] = dl_dpow * ((float)h.c2 * fdy + (float)h.c1 * fdx);
               gr[2] = dl_dpow * (-0.5f * fdx * fdx);
               gr[3] = dl_dpow * (-fdx * fdy);
               gr[4] = dl_dpow * (-0.5f * fdy * fdy);
-              T = T * (1.0 - alpha);
+              T *= 1.f - a;
             }
           }
         }
@@ -231,44 +237,34 @@ __constant__ double kB3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457
                               0.3731763325901154, -0.4570457994644658, 1.445305721320277,
                               -0.5900435899266435};
 
-// SH basis values and their gradients w.r.t. the unit direction (x, y, z).
-__device__ void sh_basis_grad(double x, double y, double z, int degree, double Y[16],
-                              double dY[16][3]) {
-  for (int n = 0; n < 16; ++n) { Y[n] = 0.0; dY[n][0] = dY[n][1] = dY[n][2] = 0.0; }
-  Y[0] = kB0;
-  if (degree >= 1) {
-    Y[1] = -kB1 * y; dY[1][1] = -kB1;
-    Y[2] = kB1 * z;  dY[2][2] = kB1;
-    Y[3] = -kB1 * x; dY[3][0] = -kB1;
-  }
-  if (degree >= 2) {
-    const double xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
-    Y[4] = kB2[0] * xy;  dY[4][0] = kB2[0] * y; dY[4][1] = kB2[0] * x;
-    Y[5] = kB2[1] * yz;  dY[5][1] = kB2[1] * z; dY[5][2] = kB2[1] * y;
-    Y[6] = kB2[2] * (2.0 * zz - xx - yy);
-    dY[6][0] = -2.0 * kB2[2] * x; dY[6][1] = -2.0 * kB2[2] * y; dY[6][2] = 4.0 * kB2[2] * z;
-    Y[7] = kB2[3] * xz;  dY[7][0] = kB2[3] * z; dY[7][2] = kB2[3] * x;
-    Y[8] = kB2[4] * (xx - yy); dY[8][0] = 2.0 * kB2[4] * x; dY[8][1] = -2.0 * kB2[4] * y;
-    if (degree >= 3) {
-      Y[9] = kB3[0] * y * (3.0 * xx - yy);
-      dY[9][0] = 6.0 * kB3[0] * xy; dY[9][1] = kB3[0] * (3.0 * xx - 3.0 * yy);
-      Y[10] = kB3[1] * xy * z;
-      dY[10][0] = kB3[1] * yz; dY[10][1] = kB3[1] * xz; dY[10][2] = kB3[1] * xy;
-      Y[11] = kB3[2] * y * (4.0 * zz - xx - yy);
-      dY[11][0] = -2.0 * kB3[2] * xy; dY[11][1] = kB3[2] * (4.0 * zz - xx - 3.0 * yy);
-      dY[11][2] = 8.0 * kB3[2] * yz;
-      Y[12] = kB3[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
-      dY[12][0] = -6.0 * kB3[3] * xz; dY[12][1] = -6.0 * kB3[3] * yz;
-      dY[12][2] = kB3[3] * (6.0 * zz - 3.0 * xx - 3.0 * yy);
-      Y[13] = kB3[4] * x * (4.0 * zz - xx - yy);
-      dY[13][0] = kB3[4] * (4.0 * zz - 3.0 * xx - yy); dY[13][1] = -2.0 * kB3[4] * xy;
-      dY[13][2] = 8.0 * kB3[4] * xz;
-      Y[14] = kB3[5] * z * (xx - yy);
-      dY[14][0] = 2.0 * kB3[5] * xz; dY[14][1] = -2.0 * kB3[5] * yz; dY[14][2] = kB3[5] * (xx - yy);
-      Y[15] = kB3[6] * x * (xx - 3.0 * yy);
-      dY[15][0] = kB3[6] * (3.0 * xx - 3.0 * yy); dY[15][1] = -6.0 * kB3[6] * xy;
-    }
-  }
+// Visits every SH basis function n <= degree with its value Y_n and its
+// gradient (gx, gy, gz) w.r.t. the unit direction (core.py:114-146), without
+// materialising 16 x 4 arrays (the previous form spilled 512 B per thread).
+template <typename F>
+__device__ __forceinline__ void for_sh_basis(double x, double y, double z, int degree, F&& f) {
+  f(0, kB0, 0.0, 0.0, 0.0);
+  if (degree < 1) return;
+  f(1, -kB1 * y, 0.0, -kB1, 0.0);
+  f(2, kB1 * z, 0.0, 0.0, kB1);
+  f(3, -kB1 * x, -kB1, 0.0, 0.0);
+  if (degree < 2) return;
+  const double xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+  f(4, kB2[0] * xy, kB2[0] * y, kB2[0] * x, 0.0);
+  f(5, kB2[1] * yz, 0.0, kB2[1] * z, kB2[1] * y);
+  f(6, kB2[2] * (2.0 * zz - xx - yy), -2.0 * kB2[2] * x, -2.0 * kB2[2] * y, 4.0 * kB2[2] * z);
+  f(7, kB2[3] * xz, kB2[3] * z, 0.0, kB2[3] * x);
+  f(8, kB2[4] * (xx - yy), 2.0 * kB2[4] * x, -2.0 * kB2[4] * y, 0.0);
+  if (degree < 3) return;
+  f(9, kB3[0] * y * (3.0 * xx - yy), 6.0 * kB3[0] * xy, kB3[0] * (3.0 * xx - 3.0 * yy), 0.0);
+  f(10, kB3[1] * xy * z, kB3[1] * yz, kB3[1] * xz, kB3[1] * xy);
+  f(11, kB3[2] * y * (4.0 * zz - xx - yy), -2.0 * kB3[2] * xy, kB3[2] * (4.0 * zz - xx - 3.0 * yy),
+    8.0 * kB3[2] * yz);
+  f(12, kB3[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy), -6.0 * kB3[3] * xz, -6.0 * kB3[3] * yz,
+    kB3[3] * (6.0 * zz - 3.0 * xx - 3.0 * yy));
+  f(13, kB3[4] * x * (4.0 * zz - xx - yy), kB3[4] * (4.0 * zz - 3.0 * xx - yy), -2.0 * kB3[4] * xy,
+    8.0 * kB3[4] * xz);
+  f(14, kB3[5] * z * (xx - yy), 2.0 * kB3[5] * xz, -2.0 * kB3[5] * yz, kB3[5] * (xx - yy));
+  f(15, kB3[6] * x * (xx - 3.0 * yy), kB3[6] * (3.0 * xx - 3.0 * yy), -6.0 * kB3[6] * xy, 0.0);
 }
 
 __device__ __forceinline__ int deg_of(int c) { return c >= 16 ? 3 : c >= 9 ? 2 : c >= 4 ? 1 : 0; }
@@ -383,27 +379,34 @@ k_project_bwd(const cs_cloud cl, const uint32_t* __restrict__ order, const DevSt
     // colour: SH coefficients and the view direction
     const int C = cl.sh_coeffs;
     const int degree = min((int)st.sh_degree, deg_of(C));
-    const int nb = (degree + 1) * (degree + 1);
     double v[3] = {gm.px - cam.center[0], gm.py - cam.center[1], gm.pz - cam.center[2]};
     const double nv = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
     const double d[3] = {v[0] / nv, v[1] / nv, v[2] / nv};
-    double Y[16], dY[16][3];
-    sh_basis_grad(d[0], d[1], d[2], degree, Y, dY);
     const float* row = cl.sh + k * cl.sh_stride;
+    // pass 1: colour before the clip (core.py:169-172) -> which channels pass gradient
+    double val[3] = {0.5, 0.5, 0.5};
+    for_sh_basis(d[0], d[1], d[2], degree, [&](int n, double Yn, double, double, double) {
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) val[ch] += (double)row[ch * C + n] * Yn;
+    });
+    double gc[3];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch)
+      gc[ch] = (val[ch] >= 0.0 && val[ch] <= 1.0) ? (double)gin[6 + ch] : 0.0;
+    // pass 2: dL/dsh = gc * Y_n, dL/ddir = sum gc * sh * dY_n
+    float* gsh = out.sh + k * (int64_t)(3 * C);
     double dd[3] = {0.0, 0.0, 0.0};
-    for (int ch = 0; ch < 3; ++ch) {
-      double val = 0.5;
-      for (int n = 0; n < nb; ++n) val += (double)row[ch * C + n] * Y[n];
-      const double gc = (val >= 0.0 && val <= 1.0) ? (double)gin[6 + ch] : 0.0;
-      float* gsh = out.sh + k * (int64_t)(3 * C) + ch * C;
-      for (int n = 0; n < nb; ++n) {
-        gsh[n] = (float)(gc * Y[n]);
-        const double ws = gc * (double)row[ch * C + n];
-        dd[0] += ws * dY[n][0];
-        dd[1] += ws * dY[n][1];
-        dd[2] += ws * dY[n][2];
+    for_sh_basis(d[0], d[1], d[2], degree, [&](int n, double Yn, double gx, double gy, double gz) {
+      double ws = 0.0;
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        gsh[ch * C + n] = (float)(gc[ch] * Yn);
+        ws += gc[ch] * (double)row[ch * C + n];
       }
-    }
+      dd[0] += ws * gx;
+      dd[1] += ws * gy;
+      dd[2] += ws * gz;
+    });
     const double ddot = dd[0] * d[0] + dd[1] * d[1] + dd[2] * d[2];
     for (int i = 0; i < 3; ++i) dp[i] += (dd[i] - d[i] * ddot) / nv;
     for (int i = 0; i < 3; ++i) {
