@@ -96,17 +96,22 @@ k_pair_count(const uint32_t* __restrict__ order, const int4* __restrict__ rects,
 }
 
 constexpr int kDupThreads = 256;
+static_assert(kDupTile == 4 * kDupThreads, "k_duplicate emits 4 pairs per thread");
 
 // Load-balanced duplication: each CTA owns kDupTile consecutive output pairs;
 // the depth ranks whose pair ranges intersect it (dup_start[b] ..
-// dup_start[b+1], from K5) are staged in shared memory and every pair finds
-// its rank by a binary search there.  key = tile id, value = compact index.
+// dup_start[b+1], from K5) are staged in shared memory.  Each thread emits 4
+// consecutive pairs: one binary search for its first pair's rank, then a
+// sequential walk over the rect row-major (render.py:233-243) and on to the
+// next rank, and two 16-byte stores.  key = tile id, value = splat id.
+constexpr int kDupItems = kDupTile / kDupThreads;  // 4
+
 __global__ void __launch_bounds__(kDupThreads)
 k_duplicate(const int64_t* __restrict__ pair_off, const uint32_t* __restrict__ order,
             const int4* __restrict__ rects, const uint32_t* __restrict__ dup_start,
             const DevStats* __restrict__ stats, int ntx, uint32_t* __restrict__ keys,
             uint32_t* __restrict__ vals) {
-  __shared__ int64_t s_off[kDupTile + 1];
+  __shared__ int64_t s_off[kDupTile + 2];
   __shared__ int4 s_rect[kDupTile + 1];
   __shared__ uint32_t s_id[kDupTile + 1];
   const int64_t P = stats->pairs_eff;
@@ -123,19 +128,43 @@ k_duplicate(const int64_t* __restrict__ pair_off, const uint32_t* __restrict__ o
     s_rect[i] = __ldg(rects + v);
     s_id[i] = v;
   }
+  if (threadIdx.x == 0) s_off[nr] = INT64_MAX;  // sentinel: every rank owns >= 1 pair
   __syncthreads();
-  for (int64_t p = p0 + threadIdx.x; p < p1; p += kDupThreads) {
-    int lo = 0, hi = nr - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (s_off[mid] <= p) lo = mid; else hi = mid - 1;
+  const int64_t p = p0 + (int64_t)threadIdx.x * kDupItems;
+  if (p >= p1) return;
+  int lo = 0, hi = nr - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (s_off[mid] <= p) lo = mid; else hi = mid - 1;
+  }
+  int4 rc = s_rect[lo];
+  int w = rc.y - rc.x + 1;
+  const int64_t local = p - s_off[lo];
+  int ly = (int)(local / w), lx = (int)(local - (int64_t)ly * w);
+  int64_t next = s_off[lo + 1];
+  uint32_t k[kDupItems], v[kDupItems];
+#pragma unroll
+  for (int j = 0; j < kDupItems; ++j) {
+    k[j] = (uint32_t)((rc.z + ly) * ntx + (rc.x + lx));
+    v[j] = s_id[lo];
+    if (p + j + 1 == next) {  // next rank starts at its first tile
+      ++lo;
+      rc = s_rect[lo];
+      w = rc.y - rc.x + 1;
+      lx = ly = 0;
+      next = s_off[lo + 1];
+    } else if (++lx == w) {
+      lx = 0;
+      ++ly;
     }
-    const int4 rc = s_rect[lo];
-    const int64_t local = p - s_off[lo];
-    const int w = rc.y - rc.x + 1;
-    const int ly = (int)(local / w), lx = (int)(local - (int64_t)ly * w);
-    keys[p] = (uint32_t)((rc.z + ly) * ntx + (rc.x + lx));
-    vals[p] = s_id[lo];
+  }
+  if (p + kDupItems <= p1) {
+    *reinterpret_cast<uint4*>(keys + p) = make_uint4(k[0], k[1], k[2], k[3]);
+    *reinterpret_cast<uint4*>(vals + p) = make_uint4(v[0], v[1], v[2], v[3]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < kDupItems; ++j)
+      if (p + j < p1) { keys[p + j] = k[j]; vals[p + j] = v[j]; }
   }
 }
 
