@@ -259,7 +259,7 @@ def main():
     n_seg = ctypes.c_int32(0)
     for i in range(K):
         s = CsFrameStats()
-        frame(i, _lib.CS_RENDER_SYNC, s)
+        frame(i, _lib.CS_RENDER_SYNC | _lib.CS_RENDER_DIAG, s)
         counts["assembled"] += s.assembled
         counts["visible"] += s.visible
         counts["pairs"] += s.pairs

@@ -17,6 +17,7 @@ CS_SRC_CLOUD, CS_SRC_LOD_BLOCK, CS_SRC_LOD_POINT = 0, 1, 2
 CS_RENDER_SYNC, CS_RENDER_F64_OUT, CS_RENDER_NO_CLIP, CS_RENDER_KEEP_STATE = 1, 2, 4, 8
 CS_RENDER_PROJECT_ONLY = 16
 CS_RENDER_DEBUG = 32
+CS_RENDER_DIAG = 64
 
 c_double_p = ctypes.POINTER(ctypes.c_double)
 vp = ctypes.c_void_p

@@ -40,7 +40,7 @@ constexpr int kBlendThreads = 256;
 // into the warp's shared-memory slot.  The copies of round r are in flight
 // while the warp evaluates round r-1 (two stages per warp).  The walk stops
 // as soon as the box's 32 pixels have terminated.
-template <typename OutT, bool KEEP>
+template <typename OutT, bool KEEP, bool DIAG>
 __global__ void __launch_bounds__(kBlendThreads)
 k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
         const uint32_t* __restrict__ bys, const uint2* __restrict__ ranges,
@@ -55,7 +55,8 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
   const uint32_t lane = lane_id();
   const uint32_t lt_mask = (1u << lane) - 1u;
   HotRec (*wbuf)[32] = s_hot[threadIdx.x >> 5];
-  long long frags = 0, evals = 0, whits = 0, whits_empty = 0;
+  long long frags = 0, whits = 0;
+  uint32_t evals = 0, whits_empty = 0;  // per lane: well below 2^32 per launch
   for (;;) {
     int item = 0;
     if (lane == 0) item = (int)atomicAdd(&stats->tickets[4], 1u);
@@ -87,24 +88,23 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
     bool done = !valid;
 
     // one staged round: evaluate its hits (slots 0..popc-1) for this lane's pixel
+    // (the quadratic form is computed by terminated lanes too: a branch around
+    // it costs more issue slots than the idle lanes' share of the DP pipe)
     auto eval_round = [&](const HotRec* buf, uint32_t mask, int64_t k0) {
       int slot = 0;
+      whits += __popc(mask);
       while (mask) {
         const int src = __ffs(mask) - 1;
         mask &= mask - 1;
         const HotRec& h = buf[slot++];
-        ++whits;
-        double power = -1e300;
-        if (!done) {
-          ++evals;
-          const double dx = dsub(sx, h.mx);
-          const double dy = dsub(sy, h.my);
-          // -0.5 * (c0*dx*dx + c2*dy*dy) - c1*dx*dy   (_kernels.py:54-57)
-          power = dsub(dmul(-0.5, dadd(dmul(dmul(h.c0, dx), dx), dmul(dmul(h.c2, dy), dy))),
-                       dmul(dmul(h.c1, dx), dy));
-        }
-        const bool pass = power >= h.lthr;  // else alpha < alpha_floor guaranteed
-        if (!__any_sync(0xffffffffu, pass)) ++whits_empty;
+        evals += done ? 0u : 1u;
+        const double dx = dsub(sx, h.mx);
+        const double dy = dsub(sy, h.my);
+        // -0.5 * (c0*dx*dx + c2*dy*dy) - c1*dx*dy   (_kernels.py:54-57)
+        const double power = dsub(dmul(-0.5, dadd(dmul(dmul(h.c0, dx), dx), dmul(dmul(h.c2, dy), dy))),
+                                  dmul(dmul(h.c1, dx), dy));
+        const bool pass = !done && power >= h.lthr;  // else alpha < alpha_floor guaranteed
+        if (DIAG && !__any_sync(0xffffffffu, pass)) ++whits_empty;
         if (!pass) continue;
         double alpha = dmul(h.opacity, exp_le0(power, s_exp, ec));  // _kernels.py:58
         if (alpha > 0.99) alpha = 0.99;              // _kernels.py:59-60
@@ -190,14 +190,27 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
     frags += box_frags;
     if (lane == 0 && box_frags) atomicAdd(frag_tile + t, box_frags);
   }
-  evals = warp_sum(evals);
+  const long long wevals = warp_sum((long long)evals);
   if (lane == 0) {
     if (whits) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->warp_hits), (unsigned long long)whits);
-    if (whits_empty)
+    if (DIAG && whits_empty)
       atomicAdd(reinterpret_cast<unsigned long long*>(&stats->warp_hits_empty), (unsigned long long)whits_empty);
     if (frags) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->fragments), (unsigned long long)frags);
-    if (evals) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->evals), (unsigned long long)evals);
+    if (wevals) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->evals), (unsigned long long)wevals);
   }
+}
+
+template <typename OutT, bool KEEP, bool DIAG>
+static void launch_blend_d(int n_tiles, const uint32_t* list, const uint32_t* bxs,
+                           const uint32_t* bys, const uint2* ranges, const HotRec* hot,
+                           const uint32_t* order, const BlendParams& bp, OutT* out,
+                           int32_t* frag_tile, DevStats* stats, BlendState st, cudaStream_t s) {
+  static int grid = 0;  // persistent: one wave of resident CTAs
+  if (grid == 0) grid = persistent_grid(k_blend<OutT, KEEP, DIAG>, kBlendThreads);
+  const int nboxes = boxes_per_tile(bp.tile_size);
+  k_blend<OutT, KEEP, DIAG><<<grid, kBlendThreads, 0, s>>>(list, bxs, bys, ranges, hot, order,
+                                                           n_tiles * nboxes, nboxes, bp, out,
+                                                           frag_tile, stats, st);
 }
 
 template <typename OutT, bool KEEP>
@@ -205,12 +218,10 @@ static void launch_blend_t(int n_tiles, const uint32_t* list, const uint32_t* bx
                            const uint32_t* bys, const uint2* ranges, const HotRec* hot,
                            const uint32_t* order, const BlendParams& bp, OutT* out,
                            int32_t* frag_tile, DevStats* stats, BlendState st, cudaStream_t s) {
-  static int grid = 0;  // persistent: one wave of resident CTAs
-  if (grid == 0) grid = persistent_grid(k_blend<OutT, KEEP>, kBlendThreads);
-  const int nboxes = boxes_per_tile(bp.tile_size);
-  k_blend<OutT, KEEP><<<grid, kBlendThreads, 0, s>>>(list, bxs, bys, ranges, hot, order,
-                                                     n_tiles * nboxes, nboxes, bp, out, frag_tile,
-                                                     stats, st);
+  if (bp.flags & CS_RENDER_DIAG)
+    launch_blend_d<OutT, KEEP, true>(n_tiles, list, bxs, bys, ranges, hot, order, bp, out, frag_tile, stats, st, s);
+  else
+    launch_blend_d<OutT, KEEP, false>(n_tiles, list, bxs, bys, ranges, hot, order, bp, out, frag_tile, stats, st, s);
 }
 
 // K8b: heaviest-first tile order.  Tiles are bucketed by floor(log2(list

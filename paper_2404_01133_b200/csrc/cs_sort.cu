@@ -30,13 +30,13 @@ constexpr uint32_t kStFlagPre = 2u << 30;
 constexpr uint32_t kStMask = (1u << 30) - 1;
 
 template <typename K> struct SortCfg;
-template <> struct SortCfg<uint64_t> { static constexpr int kItems = 8; };
-template <> struct SortCfg<uint32_t> { static constexpr int kItems = 12; };
+template <> struct SortCfg<uint64_t> { static constexpr int kItems = 8, kMinBlocks = 1; };
+template <> struct SortCfg<uint32_t> { static constexpr int kItems = 12, kMinBlocks = 3; };
 
 template <typename K>
 __global__ void __launch_bounds__(kSortThreads)
 k_radix_hist(const K* __restrict__ keys, const int64_t* __restrict__ n_ptr, int begin_bit,
-             int n_passes, uint32_t* __restrict__ hist) {
+             int n_passes, int width, int end_bit, uint32_t* __restrict__ hist) {
   __shared__ uint32_t sh[8 * 256];
   for (int i = threadIdx.x; i < n_passes * 256; i += blockDim.x) sh[i] = 0;
   __syncthreads();
@@ -44,8 +44,11 @@ k_radix_hist(const K* __restrict__ keys, const int64_t* __restrict__ n_ptr, int 
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
     const K k = keys[i];
-    for (int p = 0; p < n_passes; ++p)
-      atomicAdd(&sh[p * 256 + (uint32_t)((k >> (begin_bit + 8 * p)) & 255)], 1u);
+    for (int p = 0; p < n_passes; ++p) {
+      const int sh_p = begin_bit + width * p;
+      const uint32_t m = (1u << min(width, end_bit - sh_p)) - 1u;
+      atomicAdd(&sh[p * 256 + ((uint32_t)(k >> sh_p) & m)], 1u);
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < n_passes * 256; i += blockDim.x)
@@ -63,12 +66,14 @@ __global__ void k_radix_hist_scan(uint32_t* hist, int n_passes) {
   }
 }
 
-template <typename K, int ITEMS = SortCfg<K>::kItems>
-__global__ void __launch_bounds__(kSortThreads)
+template <typename K, int ITEMS = SortCfg<K>::kItems, int MINB = 1, bool MATCH = false,
+          bool EARLY = true>
+__global__ void __launch_bounds__(kSortThreads, MINB)
 k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
            K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
-           const int64_t* __restrict__ n_ptr, int shift, const uint32_t* __restrict__ digit_base,
-           uint32_t* __restrict__ status, uint32_t* __restrict__ ticket) {
+           const int64_t* __restrict__ n_ptr, int shift, int nbits,
+           const uint32_t* __restrict__ digit_base, uint32_t* __restrict__ status,
+           uint32_t* __restrict__ ticket) {
   constexpr int kItems = ITEMS;
   constexpr int kTile = kSortThreads * kItems;
   __shared__ uint32_t warp_hist[kSortWarps][256];
@@ -81,6 +86,7 @@ k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
   __shared__ uint32_t vals_s[kTile];
 
   const int64_t n = *n_ptr;
+  const uint32_t dmask = (1u << nbits) - 1u;  // this pass's digit: bits [shift, shift + nbits), nbits <= 8
   if (threadIdx.x == 0) s_chunk = atomicAdd(ticket, 1u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int d = lane; d < 256; d += 32) warp_hist[warp][d] = 0;
@@ -103,47 +109,69 @@ k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
       val[r] = vals_in[idx];
     }
   }
-  // 1) chunk histogram first, published immediately so successors' look-back
-  //    finds this chunk's aggregate while it is still ranking
-#pragma unroll
-  for (int r = 0; r < kItems; ++r)
-    if (wbase + r * 32 + lane < n) atomicAdd(&chunk_hist[(uint32_t)((key[r] >> shift) & 255)], 1u);
-  __syncthreads();
+  // 1) EARLY: chunk histogram first, published immediately so successors'
+  //    look-back finds this chunk's aggregate while it is still ranking.
+  //    Otherwise the ranking's group leaders also count the chunk histogram
+  //    (one atomic per digit group instead of one per key) and it is
+  //    published right after the ranking.
   const int d = threadIdx.x;  // 256 threads == 256 digits
-  const uint32_t my_count = chunk_hist[d];
   uint32_t* my_status = status + chunk * 256 + d;
-  atomicExch(my_status, (chunk == 0 ? kStFlagPre : kStFlagAgg) | my_count);
-  // 2) stable in-warp ranks (warp order == input order).  The lanes holding
-  //    the same digit: 8 ballots (one per digit bit) for 64-bit keys, where
-  //    __match_any_sync (a multi-cycle MIO op) measured ~10% slower;
-  //    __match_any_sync for 32-bit keys, where it measured faster.
+  uint32_t my_count = 0;
+  if (EARLY) {
+#pragma unroll
+    for (int r = 0; r < kItems; ++r)
+      if (wbase + r * 32 + lane < n) atomicAdd(&chunk_hist[(uint32_t)(key[r] >> shift) & dmask], 1u);
+    __syncthreads();
+    my_count = chunk_hist[d];
+    atomicExch(my_status, (chunk == 0 ? kStFlagPre : kStFlagAgg) | my_count);
+  }
+  // 2) stable in-warp ranks (warp order == input order).  All peer masks are
+  //    computed first (the MATCH/VOTE latencies overlap instead of serialising
+  //    behind each item's counter update), then per item the leader lane of
+  //    each digit group bumps the warp's counter with one shared atomic and
+  //    broadcasts the old value.  A warp's atomics to one address execute in
+  //    issue order, so items keep their input order.  64-bit keys: 8 ballots
+  //    per item (measured faster there than __match_any_sync).
   const uint32_t lt = lanemask_lt();
+  uint32_t peers[kItems];
 #pragma unroll
   for (int r = 0; r < kItems; ++r) {
-    const int64_t idx = wbase + r * 32 + lane;
-    const bool valid = idx < n;
-    const uint32_t dg = (uint32_t)((key[r] >> shift) & 255);
-    uint32_t peers;
-    if (sizeof(K) == 8) {
-      peers = __ballot_sync(0xffffffffu, valid);
+    const bool valid = wbase + r * 32 + lane < n;
+    const uint32_t dg = (uint32_t)(key[r] >> shift) & dmask;
+    if (!MATCH) {
+      uint32_t pm = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
       for (int b = 0; b < 8; ++b) {
-        const bool bit = (dg >> b) & 1u;
-        const uint32_t bal = __ballot_sync(0xffffffffu, bit);
-        peers &= bit ? bal : ~bal;
+        if (b < nbits) {  // warp-uniform
+          const bool bit = (dg >> b) & 1u;
+          const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+          pm &= bit ? bal : ~bal;
+        }
       }
+      peers[r] = valid ? pm : 0u;
     } else {
-      peers = __match_any_sync(0xffffffffu, valid ? dg : 256u + lane);
+      const uint32_t pm = __match_any_sync(0xffffffffu, valid ? dg : 256u + lane);
+      peers[r] = valid ? pm : 0u;
     }
-    const uint32_t pr = __popc(peers & lt);
+  }
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    const uint32_t pm = peers[r];
+    const uint32_t dg = (uint32_t)(key[r] >> shift) & dmask;
+    const int leader = pm ? __ffs(pm) - 1 : (int)lane;
     uint32_t old = 0;
-    if (valid) old = warp_hist[warp][dg];
-    __syncwarp();
-    if (valid && pr == 0) warp_hist[warp][dg] = old + __popc(peers);
-    __syncwarp();
-    rank[r] = old + pr;
+    if (pm && (int)lane == leader) {
+      old = atomicAdd(&warp_hist[warp][dg], (uint32_t)__popc(pm));
+      if (!EARLY) atomicAdd(&chunk_hist[dg], (uint32_t)__popc(pm));
+    }
+    old = __shfl_sync(0xffffffffu, old, leader);
+    rank[r] = old + __popc(pm & lt);
   }
   __syncthreads();
+  if (!EARLY) {
+    my_count = chunk_hist[d];
+    atomicExch(my_status, (chunk == 0 ? kStFlagPre : kStFlagAgg) | my_count);
+  }
   // 3) combine warps and the chunk-local digit starts
   uint32_t sum = 0;
 #pragma unroll
@@ -161,7 +189,7 @@ k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
   for (int r = 0; r < kItems; ++r) {
     const int64_t idx = wbase + r * 32 + lane;
     if (idx < n) {
-      const uint32_t dg = (uint32_t)((key[r] >> shift) & 255);
+      const uint32_t dg = (uint32_t)(key[r] >> shift) & dmask;
       const uint32_t pos = digit_off[dg] + warp_hist[warp][dg] + rank[r];
       keys_s[pos] = key[r];
       vals_s[pos] = val[r];
@@ -194,7 +222,7 @@ k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
   // 6) coalesced write-out: consecutive threads store consecutive addresses of one digit run
   for (int i = threadIdx.x; i < valid_count; i += kSortThreads) {
     const K k = keys_s[i];
-    const uint32_t dg = (uint32_t)((k >> shift) & 255);
+    const uint32_t dg = (uint32_t)(k >> shift) & dmask;
     const int64_t o = gbase[dg] + i;
     keys_out[o] = k;
     vals_out[o] = vals_s[i];
@@ -211,26 +239,34 @@ size_t radix_status_words(int64_t capacity, int key_bytes) {
 // Sorts (keys, vals) of length *n_dev (<= capacity) by bits [begin_bit, end_bit).
 // Ping-pongs between (k0,v0) and (k1,v1); returns 1 when the result is in
 // (k1,v1), 0 when in (k0,v0).
-template <typename K, int ITEMS>
+template <typename K, int ITEMS, int MINB = SortCfg<K>::kMinBlocks, bool MATCH = false,
+          bool EARLY = true>
 int radix_sort_items(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_dev,
                      int64_t capacity, int begin_bit, int end_bit, uint32_t* hist,
                      uint32_t* status, uint32_t* tickets, cudaStream_t s) {
+  // equal-width digits of <= 8 bits (13 tile bits -> 7 + 6: fewer ballots per key)
   const int n_passes = (end_bit - begin_bit + 7) / 8;
   if (n_passes <= 0 || capacity <= 0) return 0;
+  const int width = (end_bit - begin_bit + n_passes - 1) / n_passes;
   constexpr int kTile = kSortThreads * ITEMS;
   const int64_t chunks = (capacity + kTile - 1) / kTile;
+  static bool carveout = false;  // shared memory is the occupancy limit: take all of it
+  if (!carveout) {
+    cudaFuncSetAttribute(k_onesweep<K, ITEMS, MINB, MATCH, EARLY>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    carveout = true;
+  }
   cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 256 * n_passes, s);
   cudaMemsetAsync(tickets, 0, sizeof(uint32_t) * n_passes, s);
   int hist_grid = (int)std::min<int64_t>(148 * 4, (capacity + kSortThreads - 1) / kSortThreads);
-  k_radix_hist<K><<<hist_grid, kSortThreads, 0, s>>>(k0, n_dev, begin_bit, n_passes, hist);
+  k_radix_hist<K><<<hist_grid, kSortThreads, 0, s>>>(k0, n_dev, begin_bit, n_passes, width, end_bit, hist);
   k_radix_hist_scan<<<1, 256, 0, s>>>(hist, n_passes);
   K* kin = k0; K* kout = k1;
   uint32_t* vin = v0; uint32_t* vout = v1;
   for (int p = 0; p < n_passes; ++p) {
     cudaMemsetAsync(status, 0, sizeof(uint32_t) * 256 * chunks, s);
-    k_onesweep<K, ITEMS><<<(unsigned)chunks, kSortThreads, 0, s>>>(kin, vin, kout, vout, n_dev,
-                                                           begin_bit + 8 * p, hist + 256 * p,
-                                                           status, tickets + p);
+    k_onesweep<K, ITEMS, MINB, MATCH, EARLY><<<(unsigned)chunks, kSortThreads, 0, s>>>(kin, vin, kout, vout, n_dev,
+        begin_bit + width * p, std::min(width, end_bit - begin_bit - width * p), hist + 256 * p,
+        status, tickets + p);
     K* tk = kin; kin = kout; kout = tk;
     uint32_t* tv = vin; vin = vout; vout = tv;
   }
