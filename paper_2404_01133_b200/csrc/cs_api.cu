@@ -105,9 +105,9 @@ void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint32_t* bxs, co
                       const cs_settings& st, int width, int height, int ntx, const float* dl_dimg,
                       const BlendState& state, uint32_t* ticket, float* grads, int64_t cap,
                       cudaStream_t s);
-void launch_project_bwd(const cs_cloud& cl, const uint32_t* order,
-                        const DevStats* stats, const cs_camera& cam, const cs_settings& st,
-                        const float* grads, int64_t cap, const cs_grads& out, cudaStream_t s);
+void launch_project_bwd(const cs_cloud& cl, const uint64_t* depth_keys, const cs_camera& cam,
+                        const cs_settings& st, const float* grads, int64_t cap, const cs_grads& out,
+                        cudaStream_t s);
 }  // namespace cs
 
 using namespace cs;
@@ -608,14 +608,9 @@ int cs_render_backward(cs_ctx* c, const cs_source* src, const cs_camera* cam,
                    cam->height, ntx, dl_dimg, state, &c->stats.as<DevStats>()->tickets[5],
                    c->gacc.as<float>(), cap, s);
   CS_CHECK_LAUNCH();
-  const int64_t K = cl.count;
-  CS_CUDA(cudaMemsetAsync(out->positions, 0, 12 * K, s));
-  CS_CUDA(cudaMemsetAsync(out->scales, 0, 12 * K, s));
-  CS_CUDA(cudaMemsetAsync(out->rotations, 0, 16 * K, s));
-  CS_CUDA(cudaMemsetAsync(out->opacities, 0, 4 * K, s));
-  CS_CUDA(cudaMemsetAsync(out->sh, 0, 12 * (size_t)cl.sh_coeffs * K, s));
-  launch_project_bwd(cl, c->last_order, c->stats.as<DevStats>(), *cam, *st,
-                     c->gacc.as<float>(), cap, *out, s);
+  // K11 writes every row (zeros for the culled ones): no clear of the outputs.
+  // The forward's per-splat float64 depth keys (~0 = culled) are still in keysA.
+  launch_project_bwd(cl, c->keysA.as<uint64_t>(), *cam, *st, c->gacc.as<float>(), cap, *out, s);
   CS_CHECK_LAUNCH();
   return CS_OK;
 }

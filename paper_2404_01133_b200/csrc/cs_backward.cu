@@ -189,6 +189,7 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
       nby = __ldg(bys + s0 + lane);
     }
     uint32_t pmask = 0;
+    uint32_t live = __ballot_sync(0xffffffffu, valid && my_end > s0);
     int64_t pk0 = 0;
     int stage = 0;
     for (int64_t k0 = s0; k0 < e1; k0 += 32) {
@@ -217,6 +218,23 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
         __syncwarp();
         eval_round(wbuf[stage ^ 1], pmask, pk0);
         __syncwarp();
+      }
+      // shrink the cull box to the pixels whose last fragment lies beyond
+      // this round (as in the forward: entries that only meet finished
+      // pixels are neither staged nor evaluated)
+      const uint32_t live_now = __ballot_sync(0xffffffffu, valid && my_end > k0 + 32);
+      if (live_now != live) {
+        live = live_now;
+        const bool on = valid && my_end > k0 + 32;
+        x0 = on ? px : 1 << 20; x1 = on ? px : -(1 << 20);
+        y0 = on ? py : 1 << 20; y1 = on ? py : -(1 << 20);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          x0 = min(x0, __shfl_xor_sync(0xffffffffu, x0, o));
+          x1 = max(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+          y0 = min(y0, __shfl_xor_sync(0xffffffffu, y0, o));
+          y1 = max(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+        }
       }
       pmask = mask;
       pk0 = k0;
@@ -269,15 +287,25 @@ __device__ __forceinline__ void for_sh_basis(double x, double y, double z, int d
 
 __device__ __forceinline__ int deg_of(int c) { return c >= 16 ? 3 : c >= 9 ? 2 : c >= 4 ? 1 : 0; }
 
-// K11: per visible splat (depth rank r -> splat id = cloud row) -> parameter gradients.
+// K11: one thread per cloud row k (= splat id of the single-cloud source), in
+// row order so every parameter, partial and gradient access is coalesced;
+// rows the forward culled (depth key ~0) get zero gradients, so the output
+// buffers need no separate clear.
 __global__ void __launch_bounds__(128)
-k_project_bwd(const cs_cloud cl, const uint32_t* __restrict__ order, const DevStats* __restrict__ stats,
-              cs_camera cam, cs_settings st, const float* __restrict__ grads, int64_t cap,
-              cs_grads out) {
-  const int64_t M = stats->visible;
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < M;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = order[r];
+k_project_bwd(const cs_cloud cl, const uint64_t* __restrict__ depth_keys, cs_camera cam,
+              cs_settings st, const float* __restrict__ grads, int64_t cap, cs_grads out) {
+  const int64_t K = cl.count;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    if (depth_keys[k] == ~0ull) {  // culled by the forward projection: no gradient
+      const int C3 = 3 * cl.sh_coeffs;
+      float* gsh0 = out.sh + k * (int64_t)C3;
+      for (int i = 0; i < C3; ++i) gsh0[i] = 0.f;
+      for (int i = 0; i < 3; ++i) out.positions[3 * k + i] = out.scales[3 * k + i] = 0.f;
+      for (int i = 0; i < 4; ++i) out.rotations[4 * k + i] = 0.f;
+      out.opacities[k] = 0.f;
+      continue;
+    }
     const Geom gm = load_geom(cl, k);
     float gin[kGradFields];
 #pragma unroll
@@ -438,12 +466,12 @@ void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint32_t* bxs, co
                                            nboxes, bp, dl_dimg, state, ticket, grads, cap);
 }
 
-void launch_project_bwd(const cs_cloud& cl, const uint32_t* order,
-                        const DevStats* stats, const cs_camera& cam, const cs_settings& st,
-                        const float* grads, int64_t cap, const cs_grads& out, cudaStream_t s) {
-  const int64_t blocks = std::min<int64_t>((cap + 127) / 128, 148 * 16);
+void launch_project_bwd(const cs_cloud& cl, const uint64_t* depth_keys, const cs_camera& cam,
+                        const cs_settings& st, const float* grads, int64_t cap, const cs_grads& out,
+                        cudaStream_t s) {
+  const int64_t blocks = std::min<int64_t>((cl.count + 127) / 128, 148 * 16);
   if (blocks <= 0) return;
-  k_project_bwd<<<(unsigned)blocks, 128, 0, s>>>(cl, order, stats, cam, st, grads, cap, out);
+  k_project_bwd<<<(unsigned)blocks, 128, 0, s>>>(cl, depth_keys, cam, st, grads, cap, out);
 }
 
 }  // namespace cs

@@ -129,6 +129,7 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
       nby = __ldg(bys + s0 + lane);
     }
     uint32_t pmask = 0;
+    uint32_t live = __ballot_sync(0xffffffffu, !done);
     int64_t pk0 = 0;
     int stage = 0;
     bool alldone = false;
@@ -158,7 +159,22 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
         __syncwarp();
         eval_round(wbuf[stage ^ 1], pmask, pk0);
         __syncwarp();
-        if (__all_sync(0xffffffffu, done)) { alldone = true; break; }
+        const uint32_t live_now = __ballot_sync(0xffffffffu, !done);
+        if (!live_now) { alldone = true; break; }
+        if (live_now != live) {
+          // shrink the warp's cull box to its still-live pixels: a splat that
+          // only meets terminated pixels is no longer staged or evaluated
+          live = live_now;
+          x0 = !done ? px : 1 << 20; x1 = !done ? px : -(1 << 20);
+          y0 = !done ? py : 1 << 20; y1 = !done ? py : -(1 << 20);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            x0 = min(x0, __shfl_xor_sync(0xffffffffu, x0, o));
+            x1 = max(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+            y0 = min(y0, __shfl_xor_sync(0xffffffffu, y0, o));
+            y1 = max(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+          }
+        }
       }
       pmask = mask;
       pk0 = k0;
