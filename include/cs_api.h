@@ -276,6 +276,34 @@ int cs_fuse_filter(cs_ctx* ctx, int64_t n, const void* positions, int32_t f32,
                    const double* p_min, const double* p_max, int32_t nx, int32_t ny, int32_t nz,
                    int32_t block, int64_t* kept_idx, int64_t* kept_count, void* stream);
 
+/* ---- LoD generation (lod.py:54-248) -------------------
+ * significance_scores (lod.py:54-101): per-Gaussian training-view hit count x
+ * opacity x percentile-clamped volume^0.1.  cams: HOST array of n_cams views.
+ * scores: device double[count]; hits: device int32[count] or NULL. */
+int cs_significance(cs_ctx* ctx, const cs_cloud* cloud, const cs_camera* cams, int32_t n_cams,
+                    const cs_settings* st, double* scores, int32_t* hits, void* stream);
+/* _priority (lod.py:114-116): indices by descending score, ties -> lower index.
+ * scores: device double[n]; order: device int32[n]. */
+int cs_priority(cs_ctx* ctx, int64_t n, const double* scores, int32_t* order, void* stream);
+/* build_lod's kept rows (lod.py:222-234): level L (rates coarsest first, HOST)
+ * keeps the top _keep_count(rate_L, n) of `order`, grouped by block in
+ * ascending block id, ascending row inside a block.  rows: device
+ * int32[n_levels * n] (level L at offset L*n); counts: HOST int64
+ * [n_levels * n_blocks].  Synchronises `stream`. */
+int cs_lod_rows(cs_ctx* ctx, int64_t n, const int32_t* order, const int32_t* membership,
+                int32_t n_blocks, const double* rates, int32_t n_levels, int32_t* rows,
+                int64_t* counts, void* stream);
+/* mad_bounds (lod.py:130-147) of every block's members (membership: device
+ * int32[count]); blocks without members get zero bounds (lod.py:236-240).
+ * bmin/bmax: HOST double[n_blocks * 3].  Synchronises `stream`. */
+int cs_mad_bounds(cs_ctx* ctx, const cs_cloud* cloud, const int32_t* membership, int32_t n_blocks,
+                  double n_mad, double* bmin, double* bmax, void* stream);
+/* GaussianCloud.take(rows).with_sh_degree (core.py): copies the geometry quads
+ * of `rows` and the first dst->sh_coeffs SH coefficients per channel into the
+ * caller-allocated dst (same fp64 flag; dst->count is ignored, n rows written). */
+int cs_gather_cloud(cs_ctx* ctx, const cs_cloud* src, const int32_t* rows, int64_t n,
+                    const cs_cloud* dst, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

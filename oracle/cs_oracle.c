@@ -551,6 +551,102 @@ void or_pointwise_keep(int64_t K, const void* pos, int f32, const double* center
   }
 }
 
+/*
+ * significance_scores hit counts, lod.py:54-101 (the per-view loop of
+ * lod.py:71-95).  A view hits Gaussian k when its centre is in front of the
+ * near plane (lod.py:74), projects inside [0, W] x [0, H] inclusive
+ * (lod.py:81-83) and its support radius support_sigmas * sqrt(lambda_max of
+ * cov2d + LOW_PASS) is >= MIN_FOOTPRINT_RADIUS = 0.5 px (lod.py:92-95).  The
+ * covariance chain is the same numpy op order as _project_cloud (the einsums
+ * of lod.py:85 / lod.py:91 are those of render.py:133 / render.py:141).
+ * hits[k] counts views (the reference accumulates them in float64, exactly).
+ */
+void or_significance_hits(int64_t K, const void* pos, const void* scl, const void* rot,
+                          int geom_f32, int64_t n_cams, const or_camera* cams,
+                          const or_settings* st, int64_t* hits, int nthreads) {
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < K; ++k) {
+    double p0 = ld(pos, geom_f32, 3 * k), p1 = ld(pos, geom_f32, 3 * k + 1),
+           p2 = ld(pos, geom_f32, 3 * k + 2);
+    double w = ld(rot, geom_f32, 4 * k), x = ld(rot, geom_f32, 4 * k + 1),
+           y = ld(rot, geom_f32, 4 * k + 2), zq = ld(rot, geom_f32, 4 * k + 3);
+    double r[9];
+    r[0] = 1.0 - 2.0 * (y * y + zq * zq);
+    r[1] = 2.0 * (x * y - w * zq);
+    r[2] = 2.0 * (x * zq + w * y);
+    r[3] = 2.0 * (x * y + w * zq);
+    r[4] = 1.0 - 2.0 * (x * x + zq * zq);
+    r[5] = 2.0 * (y * zq - w * x);
+    r[6] = 2.0 * (x * zq - w * y);
+    r[7] = 2.0 * (y * zq + w * x);
+    r[8] = 1.0 - 2.0 * (x * x + y * y);
+    double s0 = ld(scl, geom_f32, 3 * k), s1 = ld(scl, geom_f32, 3 * k + 1),
+           s2 = ld(scl, geom_f32, 3 * k + 2);
+    double q0 = s0 * s0, q1 = s1 * s1, q2 = s2 * s2;
+    double rs[9], sig[9];
+    for (int i = 0; i < 3; ++i) {
+      rs[3 * i + 0] = r[3 * i + 0] * q0;
+      rs[3 * i + 1] = r[3 * i + 1] * q1;
+      rs[3 * i + 2] = r[3 * i + 2] * q2;
+    }
+    for (int i = 0; i < 3; ++i)
+      for (int l = 0; l < 3; ++l)
+        sig[3 * i + l] = (rs[3 * i + 0] * r[3 * l + 0] + rs[3 * i + 2] * r[3 * l + 2]) +
+                         rs[3 * i + 1] * r[3 * l + 1];
+    int64_t h = 0;
+    for (int64_t ci = 0; ci < n_cams; ++ci) {
+      const or_camera* cam = &cams[ci];
+      const double* R = cam->R;
+      const double* T = cam->t;
+      double t0 = ((p0 * R[0] + p1 * R[1]) + p2 * R[2]) + T[0];
+      double t1 = ((p0 * R[3] + p1 * R[4]) + p2 * R[5]) + T[1];
+      double z = ((p0 * R[6] + p1 * R[7]) + p2 * R[8]) + T[2];
+      if (!(z > st->near_plane)) continue;                 /* lod.py:74 */
+      double u = cam->fx * t0 / z + cam->cx;                /* lod.py:79-80 */
+      double v = cam->fy * t1 / z + cam->cy;
+      int on_image = (u >= 0.0) && (u <= (double)cam->width) && (v >= 0.0) &&
+                     (v <= (double)cam->height);            /* lod.py:81 */
+      if (!on_image) continue;
+      double V[9];
+      for (int i = 0; i < 3; ++i)
+        for (int m = 0; m < 3; ++m) {
+          double acc = 0.0;
+          int first = 1;
+          for (int j = 0; j < 3; ++j)
+            for (int l = 0; l < 3; ++l) {
+              double term = (R[3 * i + j] * sig[3 * j + l]) * R[3 * m + l];
+              if (first) { acc = term; first = 0; } else acc = acc + term;
+            }
+          V[3 * i + m] = acc;
+        }
+      double J[6] = {cam->fx / z, 0.0, -cam->fx * t0 / (z * z),
+                     0.0, cam->fy / z, -cam->fy * t1 / (z * z)};
+      double cv[4];
+      for (int i = 0; i < 2; ++i)
+        for (int m = 0; m < 2; ++m) {
+          double acc = 0.0;
+          int first = 1;
+          for (int j = 0; j < 3; ++j)
+            for (int l = 0; l < 3; ++l) {
+              double term = (J[3 * i + j] * V[3 * j + l]) * J[3 * m + l];
+              if (first) { acc = term; first = 0; } else acc = acc + term;
+            }
+          cv[2 * i + m] = acc;
+        }
+      double a = cv[0] + st->low_pass, b = cv[1], c = cv[3] + st->low_pass; /* lod.py:87-89 */
+      double mid = 0.5 * (a + c);
+      double disc = mid * mid - (a * c - b * b);
+      double lam = mid + sqrt(disc > 0.0 ? disc : 0.0);    /* np.maximum(..., 0.0) */
+      double radius = st->support_sigmas * sqrt(lam);
+      if (radius >= 0.5) h += 1;                            /* MIN_FOOTPRINT_RADIUS */
+    }
+    hits[k] = h;
+  }
+}
+
 /* normalize_position + contract + block_of_points, partition.py:110-169. */
 void or_block_of_points(int64_t K, const void* pos, int f32, const double* pmin,
                         const double* pmax, int64_t nx, int64_t ny, int64_t nz, int64_t* out) {

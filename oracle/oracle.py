@@ -87,6 +87,7 @@ def lib():
         _lib.or_decide_visibility.argtypes = [i64, P, P, P, i64, P, P, i64, P, P, P, P, P]
         _lib.or_pointwise_keep.argtypes = [i64, P, ctypes.c_int, P, i64, P, i64, P]
         _lib.or_block_of_points.argtypes = [i64, P, ctypes.c_int, P, P, i64, i64, i64, P]
+        _lib.or_significance_hits.argtypes = [i64, P, P, P, ctypes.c_int, i64, P, P, P, ctypes.c_int]
         _lib.or_rasterize.restype = ctypes.c_int
         _lib.or_rasterize.argtypes = [i64, P, P, P, P, ctypes.c_int, P, ctypes.c_int, i64, P, P,
                                       P, P, P, ctypes.c_int]
@@ -390,3 +391,75 @@ def fuse(block_clouds, p_min, p_max, dims):
                                  np.asarray(cloud.scales)[idx], np.asarray(cloud.rotations)[idx],
                                  np.asarray(cloud.sh)[idx]))
     return concat(pieces)
+
+
+def significance_scores(cloud, cameras, settings=None, nthreads: int = 0):
+    """lod.significance_scores (lod.py:54-101): C hit counts (or_significance_hits)
+    times opacity times the percentile-clamped volume^0.1, the last two in numpy
+    exactly as the reference writes them (lod.py:97-100).  Returns (scores, hits)."""
+    settings = settings or DefaultSettings()
+    k = int(np.asarray(cloud.positions).shape[0])
+    if k == 0:
+        return np.zeros(0), np.zeros(0, dtype=np.int64)
+    geo = [_geom(a) for a in (cloud.positions, cloud.scales, cloud.rotations)]
+    f32 = int(all(f for _, f in geo))
+    pos, scl, rot = (g if f32 else _f64(g) for g, _ in geo)
+    cams = list(cameras)
+    arr = (_Cam * max(len(cams), 1))()
+    for i, c in enumerate(cams):
+        arr[i] = camera_struct(c)
+    ss = settings_struct(settings)
+    hits = np.zeros(k, dtype=np.int64)
+    lib().or_significance_hits(k, _ptr(pos), _ptr(scl), _ptr(rot), f32, len(cams),
+                               ctypes.cast(arr, ctypes.c_void_p), ctypes.byref(ss), _ptr(hits),
+                               nthreads)
+    scales = np.asarray(cloud.scales, dtype=np.float64)
+    volume = np.prod(scales, axis=1)
+    cap = np.percentile(volume, 90.0)
+    clamped = np.minimum(volume, cap)
+    scores = hits.astype(np.float64) * np.asarray(cloud.opacities, dtype=np.float64) * clamped ** 0.1
+    return scores, hits
+
+
+def priority(scores):
+    """lod._priority (lod.py:114-116): descending score, ties -> lower index."""
+    return np.argsort(-np.asarray(scores, dtype=np.float64), kind="stable")
+
+
+def keep_count(rate: float, k: int) -> int:
+    """lod._keep_count (lod.py:104-111)."""
+    import math
+    if not 0.0 < rate <= 1.0:
+        raise ValueError("compression rate must be in (0, 1]")
+    if k == 0:
+        return 0
+    return min(k, max(1, math.ceil(rate * k - 1e-9 * k)))
+
+
+def level_rows(order, membership, n_blocks, rates_finest_first):
+    """build_lod's kept rows (lod.py:222-234): [L][j] ascending indices, L coarsest first."""
+    k = len(order)
+    out = []
+    membership = np.asarray(membership)
+    for rate in reversed(tuple(rates_finest_first)):
+        mask = np.zeros(k, dtype=bool)
+        mask[np.asarray(order)[:keep_count(rate, k)]] = True
+        out.append([np.nonzero(mask & (membership == j))[0] for j in range(n_blocks)])
+    return out
+
+
+def mad_bounds(positions, n_mad):
+    """lod.mad_bounds (lod.py:130-147) restated with numpy."""
+    import math
+    p = np.asarray(positions, dtype=np.float64)
+    if p.shape[0] == 0:
+        raise ValueError("bounds of an empty block are undefined")
+    lo = p.min(axis=0).copy()
+    hi = p.max(axis=0).copy()
+    med = np.median(p, axis=0)
+    mad = np.median(np.abs(p - med), axis=0)
+    for axis in range(3):
+        if mad[axis] > 0.0 and math.isfinite(n_mad):
+            lo[axis] = max(lo[axis], med[axis] - n_mad * mad[axis])
+            hi[axis] = min(hi[axis], med[axis] + n_mad * mad[axis])
+    return lo, hi

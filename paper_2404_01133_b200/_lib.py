@@ -110,6 +110,12 @@ _SIGS = {
     "cs_block_activate": (ctypes.c_int, [vp, i64, vp, vp, vp, vp, vp]),
     "cs_block_of_points": (ctypes.c_int, [vp, i64, vp, i32, vp, vp, i32, i32, i32, vp, vp]),
     "cs_fuse_filter": (ctypes.c_int, [vp, i64, vp, i32, vp, vp, i32, i32, i32, i32, vp, vp, vp]),
+    "cs_significance": (ctypes.c_int, [vp, ctypes.POINTER(CsCloud), vp, i32, ctypes.POINTER(CsSettings),
+                                       vp, vp, vp]),
+    "cs_priority": (ctypes.c_int, [vp, i64, vp, vp, vp]),
+    "cs_lod_rows": (ctypes.c_int, [vp, i64, vp, vp, i32, vp, i32, vp, vp, vp]),
+    "cs_mad_bounds": (ctypes.c_int, [vp, ctypes.POINTER(CsCloud), vp, i32, ctypes.c_double, vp, vp, vp]),
+    "cs_gather_cloud": (ctypes.c_int, [vp, ctypes.POINTER(CsCloud), vp, i64, ctypes.POINTER(CsCloud), vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -108,6 +108,18 @@ void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint32_t* bxs, co
 void launch_project_bwd(const cs_cloud& cl, const uint64_t* depth_keys, const cs_camera& cam,
                         const cs_settings& st, const float* grads, int64_t cap, const cs_grads& out,
                         cudaStream_t s);
+cudaError_t significance_run(const cs_cloud& cl, const cs_camera* cams_host, int n_cams,
+                             const cs_settings& st, double* scores, int32_t* hits_out,
+                             cudaStream_t s);
+cudaError_t priority_run(int64_t K, const double* scores, int32_t* order, cudaStream_t s);
+cudaError_t lod_rows_run(int64_t K, const int32_t* order, const int32_t* membership, int n_blocks,
+                         const int64_t* keep, int n_levels, int32_t* rows_out, int64_t* counts_dev,
+                         cudaStream_t s);
+cudaError_t mad_bounds_run(const cs_cloud& cl, const int32_t* membership, int n_blocks,
+                           double n_mad, double* bmin_dev, double* bmax_dev, int64_t* cnt_host,
+                           cudaStream_t s);
+void launch_gather_cloud(const cs_cloud& src, const int32_t* rows, int64_t n, const cs_cloud& dst,
+                         cudaStream_t s);
 }  // namespace cs
 
 using namespace cs;
@@ -957,6 +969,98 @@ int cs_fuse_filter(cs_ctx* c, int64_t n, const void* positions, int32_t f32, con
   CS_CUDA(cudaMemsetAsync(c->fuse_ticket.p, 0, 4, s));
   launch_fuse_filter(n, positions, f32, p_min, p_max, nx, ny, nz, block, c->st_fuse.as<uint64_t>(),
                      c->fuse_ticket.as<uint32_t>(), kept_idx, kept_count, s);
+  CS_CHECK_LAUNCH();
+  return CS_OK;
+}
+
+// ---- LoD generation (lod.py:54-248) ------------------------------------------
+
+static int check_cloud(const cs_cloud* cl) {
+  if (!cl || cl->count < 0) return fail(CS_EINVAL, "bad cloud descriptor");
+  if (cl->count > 0 && (!cl->pos_op || !cl->scale || !cl->quat))
+    return fail(CS_EINVAL, "bad cloud descriptor");
+  if (cl->count >= (1ll << 32)) return fail(CS_EINVAL, "more than 2^32 Gaussians");
+  return CS_OK;
+}
+
+int cs_significance(cs_ctx* c, const cs_cloud* cloud, const cs_camera* cams, int32_t n_cams,
+                    const cs_settings* st, double* scores, int32_t* hits, void* stream) {
+  if (!c || !st || !scores || n_cams < 0 || (n_cams > 0 && !cams)) return fail(CS_EINVAL, "bad argument");
+  int rc = check_cloud(cloud);
+  if (rc) return rc;
+  CS_CUDA(cudaSetDevice(c->device));
+  CS_CUDA(significance_run(*cloud, cams, n_cams, *st, scores, hits, (cudaStream_t)stream));
+  return CS_OK;
+}
+
+int cs_priority(cs_ctx* c, int64_t n, const double* scores, int32_t* order, void* stream) {
+  if (!c || n < 0 || (n > 0 && (!scores || !order))) return fail(CS_EINVAL, "bad argument");
+  if (n >= (1ll << 32)) return fail(CS_EINVAL, "more than 2^32 scores");
+  CS_CUDA(cudaSetDevice(c->device));
+  CS_CUDA(priority_run(n, scores, order, (cudaStream_t)stream));
+  return CS_OK;
+}
+
+int cs_lod_rows(cs_ctx* c, int64_t n, const int32_t* order, const int32_t* membership,
+                int32_t n_blocks, const double* rates, int32_t n_levels, int32_t* rows,
+                int64_t* counts, void* stream) {
+  if (!c || n < 0 || n_blocks < 1 || n_blocks > 4096 || n_levels < 1 || !rates || !counts)
+    return fail(CS_EINVAL, "bad argument");
+  if (n > 0 && (!order || !membership || !rows)) return fail(CS_EINVAL, "bad argument");
+  if (n >= (1ll << 32)) return fail(CS_EINVAL, "more than 2^32 Gaussians");
+  std::vector<int64_t> keep(n_levels);
+  for (int L = 0; L < n_levels; ++L) {  // _keep_count, lod.py:104-111
+    const double r = rates[L];
+    if (!(r > 0.0 && r <= 1.0)) return fail(CS_EINVAL, "compression rate must be in (0, 1]");
+    const double k = (double)n;
+    keep[L] = n == 0 ? 0 : std::min<int64_t>(n, std::max<int64_t>(1, (int64_t)std::ceil(r * k - 1e-9 * k)));
+  }
+  CS_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t* dcounts = nullptr;
+  CS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dcounts), sizeof(int64_t) * n_levels * n_blocks, s));
+  CS_CUDA(cudaMemsetAsync(dcounts, 0, sizeof(int64_t) * n_levels * n_blocks, s));
+  CS_CUDA(lod_rows_run(n, order, membership, n_blocks, keep.data(), n_levels, rows, dcounts, s));
+  CS_CUDA(cudaMemcpyAsync(counts, dcounts, sizeof(int64_t) * n_levels * n_blocks,
+                          cudaMemcpyDeviceToHost, s));
+  CS_CUDA(cudaFreeAsync(dcounts, s));
+  CS_CUDA(cudaStreamSynchronize(s));
+  return CS_OK;
+}
+
+int cs_mad_bounds(cs_ctx* c, const cs_cloud* cloud, const int32_t* membership, int32_t n_blocks,
+                  double n_mad, double* bmin, double* bmax, void* stream) {
+  if (!c || n_blocks < 1 || n_blocks > 4096 || !bmin || !bmax) return fail(CS_EINVAL, "bad argument");
+  if (!(n_mad > 0)) return fail(CS_EINVAL, "n_mad must be positive");
+  int rc = check_cloud(cloud);
+  if (rc) return rc;
+  if (cloud->count > 0 && !membership) return fail(CS_EINVAL, "bad argument");
+  CS_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  double *db = nullptr;
+  CS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&db), sizeof(double) * 6 * n_blocks, s));
+  CS_CUDA(cudaMemsetAsync(db, 0, sizeof(double) * 6 * n_blocks, s));
+  std::vector<int64_t> cnt(n_blocks, 0);
+  if (cloud->count > 0)
+    CS_CUDA(mad_bounds_run(*cloud, membership, n_blocks, n_mad, db, db + 3 * n_blocks, cnt.data(), s));
+  CS_CUDA(cudaMemcpyAsync(bmin, db, sizeof(double) * 3 * n_blocks, cudaMemcpyDeviceToHost, s));
+  CS_CUDA(cudaMemcpyAsync(bmax, db + 3 * n_blocks, sizeof(double) * 3 * n_blocks, cudaMemcpyDeviceToHost, s));
+  CS_CUDA(cudaFreeAsync(db, s));
+  CS_CUDA(cudaStreamSynchronize(s));
+  return CS_OK;
+}
+
+int cs_gather_cloud(cs_ctx* c, const cs_cloud* src, const int32_t* rows, int64_t n,
+                    const cs_cloud* dst, void* stream) {
+  if (!c || !dst || n < 0 || (n > 0 && !rows)) return fail(CS_EINVAL, "bad argument");
+  int rc = check_cloud(src);
+  if (rc) return rc;
+  if (dst->fp64 != src->fp64) return fail(CS_EINVAL, "source and destination precision differ");
+  if (n > 0 && (!dst->pos_op || !dst->scale || !dst->quat || !dst->sh || !src->sh))
+    return fail(CS_EINVAL, "bad destination descriptor");
+  if (dst->sh_coeffs < 1 || dst->sh_stride < 3 * dst->sh_coeffs) return fail(CS_EINVAL, "bad sh layout");
+  CS_CUDA(cudaSetDevice(c->device));
+  launch_gather_cloud(*src, rows, n, *dst, (cudaStream_t)stream);
   CS_CHECK_LAUNCH();
   return CS_OK;
 }

@@ -88,26 +88,9 @@ __device__ __forceinline__ void sh_colour(const float* row, int C, int degree, d
   }
 }
 
-struct ProjOut {
-  bool in_front, ok, keep;
-  double z, mx, my, a, b, c, det, rx, ry;
-};
-
-// Decision math of render.py:118-160 for one Gaussian, numpy op order.
-__device__ __forceinline__ ProjOut project_one(const Geom& g, const cs_camera& cam,
-                                               const cs_settings& st) {
-  ProjOut o;
-  const double* R = cam.R;
-  double t0 = dadd(dadd(dadd(dmul(g.px, R[0]), dmul(g.py, R[1])), dmul(g.pz, R[2])), cam.t[0]);
-  double t1 = dadd(dadd(dadd(dmul(g.px, R[3]), dmul(g.py, R[4])), dmul(g.pz, R[5])), cam.t[1]);
-  double z = dadd(dadd(dadd(dmul(g.px, R[6]), dmul(g.py, R[7])), dmul(g.pz, R[8])), cam.t[2]);
-  o.z = z;
-  o.in_front = z > st.near_plane;            // render.py:120
-  o.ok = false;
-  o.keep = false;
-  if (!o.in_front) return o;
-  o.mx = dadd(ddiv(dmul(cam.fx, t0), z), cam.cx);   // render.py:128
-  o.my = dadd(ddiv(dmul(cam.fy, t1), z), cam.cy);   // render.py:129
+// Sigma = R diag(s^2) R^T of one Gaussian (core.py:74-82, core.py:107-111),
+// numpy's op order.
+__device__ __forceinline__ void sigma_of(const Geom& g, double sig[9]) {
   // quat_to_rotmat, core.py:74-82
   const double w = g.qw, x = g.qx, y = g.qy, q = g.qz;
   double r[9];
@@ -128,13 +111,20 @@ __device__ __forceinline__ ProjOut project_one(const Geom& g, const cs_camera& c
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j) rs[3 * i + j] = dmul(r[3 * i + j], s2[j]);
-  double sig[9];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int l = 0; l < 3; ++l)
       sig[3 * i + l] = dadd(dadd(dmul(rs[3 * i + 0], r[3 * l + 0]), dmul(rs[3 * i + 2], r[3 * l + 2])),
                             dmul(rs[3 * i + 1], r[3 * l + 1]));
+}
+
+// cov2d = J (W Sigma W^T) J^T entries (0,0), (0,1), (1,1) for camera-space
+// position (t0, t1, z) (render.py:133-141 / lod.py:85-91), numpy's op order.
+__device__ __forceinline__ void cov2d_of(const double sig[9], const cs_camera& cam, double t0,
+                                         double t1, double z, double& c00_o, double& c01_o,
+                                         double& c11_o) {
+  const double* R = cam.R;
   // V = W Sigma W^T, einsum ij,kjl,ml->kim: ((W_ij * S_jl) * W_ml), j-major l-minor (render.py:133)
   double V[9];
 #pragma unroll
@@ -191,6 +181,35 @@ __device__ __forceinline__ ProjOut project_one(const Geom& g, const cs_camera& c
   c11 = dadd(c11, dmul(dmul(j11, V12), j12));
   c11 = dadd(c11, dmul(dmul(j12, V21), j11));
   c11 = dadd(c11, dmul(dmul(j12, V22), j12));
+  c00_o = c00;
+  c01_o = c01;
+  c11_o = c11;
+}
+
+struct ProjOut {
+  bool in_front, ok, keep;
+  double z, mx, my, a, b, c, det, rx, ry;
+};
+
+// Decision math of render.py:118-160 for one Gaussian, numpy op order.
+__device__ __forceinline__ ProjOut project_one(const Geom& g, const cs_camera& cam,
+                                               const cs_settings& st) {
+  ProjOut o;
+  const double* R = cam.R;
+  double t0 = dadd(dadd(dadd(dmul(g.px, R[0]), dmul(g.py, R[1])), dmul(g.pz, R[2])), cam.t[0]);
+  double t1 = dadd(dadd(dadd(dmul(g.px, R[3]), dmul(g.py, R[4])), dmul(g.pz, R[5])), cam.t[1]);
+  double z = dadd(dadd(dadd(dmul(g.px, R[6]), dmul(g.py, R[7])), dmul(g.pz, R[8])), cam.t[2]);
+  o.z = z;
+  o.in_front = z > st.near_plane;            // render.py:120
+  o.ok = false;
+  o.keep = false;
+  if (!o.in_front) return o;
+  o.mx = dadd(ddiv(dmul(cam.fx, t0), z), cam.cx);   // render.py:128
+  o.my = dadd(ddiv(dmul(cam.fy, t1), z), cam.cy);   // render.py:129
+  double sig[9];
+  sigma_of(g, sig);
+  double c00, c01, c11;
+  cov2d_of(sig, cam, t0, t1, z, c00, c01, c11);
   o.a = dadd(c00, st.low_pass);                // render.py:142-144
   o.b = c01;
   o.c = dadd(c11, st.low_pass);
@@ -202,6 +221,57 @@ __device__ __forceinline__ ProjOut project_one(const Geom& g, const cs_camera& c
                         (dadd(o.my, o.ry) > 0.0) && (dsub(o.my, o.ry) < (double)cam.height);
   o.keep = o.ok && on_image;                   // render.py:156-161
   return o;
+}
+
+// K15: significance_scores hit counts (lod.py:54-101).  One thread per
+// Gaussian; Sigma once, then per training view the reference's tests in its
+// order: in front of the near plane (lod.py:74), centre inside [0, W] x [0, H]
+// inclusive (lod.py:79-83), support radius support_sigmas * sqrt(lambda_max)
+// of cov2d + LOW_PASS >= MIN_FOOTPRINT_RADIUS (lod.py:84-95).  Same float64
+// op order as the projection (the einsums of lod.py:85/91 are render.py's).
+// Also writes the volume key (np.prod(scales, axis=1), lod.py:97; positive, so
+// its IEEE bits sort like the value) for the percentile sort.
+__global__ void __launch_bounds__(256)
+k_significance(const cs_cloud cl, const cs_camera* __restrict__ cams, int n_cams, cs_settings st,
+               int32_t* __restrict__ hits, uint64_t* __restrict__ vol_keys,
+               uint32_t* __restrict__ vals) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < cl.count;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const Geom g = load_geom(cl, k);
+    double sig[9];
+    sigma_of(g, sig);
+    int h = 0;
+    for (int ci = 0; ci < n_cams; ++ci) {
+      const cs_camera& cam = cams[ci];
+      const double* R = cam.R;
+      const double t0 = dadd(dadd(dadd(dmul(g.px, R[0]), dmul(g.py, R[1])), dmul(g.pz, R[2])), cam.t[0]);
+      const double t1 = dadd(dadd(dadd(dmul(g.px, R[3]), dmul(g.py, R[4])), dmul(g.pz, R[5])), cam.t[1]);
+      const double z = dadd(dadd(dadd(dmul(g.px, R[6]), dmul(g.py, R[7])), dmul(g.pz, R[8])), cam.t[2]);
+      if (!(z > st.near_plane)) continue;                      // lod.py:74
+      const double u = dadd(ddiv(dmul(cam.fx, t0), z), cam.cx); // lod.py:79
+      const double v = dadd(ddiv(dmul(cam.fy, t1), z), cam.cy); // lod.py:80
+      if (!(u >= 0.0 && u <= (double)cam.width && v >= 0.0 && v <= (double)cam.height)) continue;
+      double c00, c01, c11;
+      cov2d_of(sig, cam, t0, t1, z, c00, c01, c11);
+      const double a = dadd(c00, st.low_pass), b = c01, c = dadd(c11, st.low_pass);
+      const double mid = dmul(0.5, dadd(a, c));                 // lod.py:90
+      const double disc = dsub(dmul(mid, mid), dsub(dmul(a, c), dmul(b, b)));
+      const double lam = dadd(mid, __dsqrt_rn(disc > 0.0 ? disc : 0.0));  // lod.py:91
+      const double radius = dmul(st.support_sigmas, __dsqrt_rn(lam));     // lod.py:92
+      if (radius >= 0.5) ++h;                                   // MIN_FOOTPRINT_RADIUS, lod.py:45
+    }
+    hits[k] = h;
+    vol_keys[k] = (uint64_t)__double_as_longlong(dmul(dmul(g.sx, g.sy), g.sz));
+    vals[k] = (uint32_t)k;
+  }
+}
+
+void launch_significance(const cs_cloud& cl, const cs_camera* cams, int n_cams,
+                         const cs_settings& st, int32_t* hits, uint64_t* vol_keys, uint32_t* vals,
+                         cudaStream_t s) {
+  const int64_t blocks = std::min<int64_t>((cl.count + 255) / 256, 148 * 16);
+  if (blocks <= 0) return;
+  k_significance<<<(unsigned)blocks, 256, 0, s>>>(cl, cams, n_cams, st, hits, vol_keys, vals);
 }
 
 constexpr int kProjThreads = 256;

@@ -355,6 +355,15 @@ def _host_arrays(lc: DeviceCloud, o: int, n: int):
                 rotations=q(lc.quat), sh=sh)
 
 
+def prime_lod_cache(scene, dscene: DeviceLodScene) -> None:
+    """Register an already-built DeviceLodScene for the host LodScene `scene`."""
+    _cached(scene, ("lod", dscene.device_index), lambda: dscene)
+
+
+def default_device() -> torch.device:
+    return torch.device("cuda", _device_index(None))
+
+
 def device_lod_scene(scene, device=None) -> DeviceLodScene:
     if isinstance(scene, DeviceLodScene):
         return scene

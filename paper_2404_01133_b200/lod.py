@@ -13,6 +13,13 @@
   column arrays, materialised on access) and that ``rasterize_stats``
   recognises and renders straight from the scene in HBM.
 
+Builder half (lod.py:54-248), on the CUDA LoD generator (lodgen.py, cs_lodgen.cu):
+
+* ``significance_scores`` (lod.py:54-101), ``compress`` (lod.py:119-127),
+  ``mad_bounds`` (lod.py:130-147), ``build_lod`` (lod.py:211-248) -- same
+  signatures and exceptions; ``build_lod`` also leaves the device scene in the
+  upload cache, so rendering the returned LodScene does not re-upload it.
+
 Accepts the reference's own LodScene objects as well (duck-typed fields).
 """
 
@@ -31,8 +38,79 @@ from . import _lib, device
 from ._lib import CsDecision, CsFrameStats, check
 from .core import GaussianCloud, pad_sh
 
-__all__ = ["LodScene", "VisibilityDecision", "AssembledSet", "AssembledCloud", "block_visible",
+__all__ = ["significance_scores", "compress", "mad_bounds", "build_lod",
+           "LodScene", "VisibilityDecision", "AssembledSet", "AssembledCloud", "block_visible",
            "select_level", "decide_visibility", "assemble_render_set"]
+
+
+def _device_settings(settings):
+    from .render import RenderSettings
+    return settings or RenderSettings()
+
+
+def significance_scores(cloud, cameras: Sequence, settings=None) -> np.ndarray:
+    """lod.significance_scores (lod.py:54-101) on the device; float64 (K,)."""
+    from . import lodgen
+    if _count(cloud) == 0:
+        return np.zeros(0)
+    dc = device.device_cloud(cloud)
+    return lodgen.significance_scores(dc, cameras, _device_settings(settings)).cpu().numpy()
+
+
+def compress(cloud, rate: float, sh_degree: int = 3, cameras: Sequence = (), *,
+             scores: Optional[np.ndarray] = None):
+    """lod.compress (lod.py:119-127): the ceil(rate*K) highest-significance
+    Gaussians in their original order, SH bands above sh_degree dropped."""
+    from . import lodgen
+    k = _count(cloud)
+    keep = lodgen.keep_count(rate, k)
+    if scores is None:
+        sc = lodgen.significance_scores(device.device_cloud(cloud), cameras) if k else None
+    else:
+        sc = torch.as_tensor(np.asarray(scores, dtype=np.float64), device=device.default_device())
+    if k == 0:
+        return cloud.take(np.zeros(0, dtype=np.int64)).with_sh_degree(sh_degree)
+    order = lodgen.priority(sc)
+    kept = torch.sort(order[:keep].long()).values.cpu().numpy()
+    return cloud.take(kept).with_sh_degree(sh_degree)
+
+
+def mad_bounds(block_cloud, n_mad: float) -> Tuple[np.ndarray, np.ndarray]:
+    """lod.mad_bounds (lod.py:130-147) on the device."""
+    from . import lodgen
+    if _count(block_cloud) == 0:
+        raise ValueError("bounds of an empty block are undefined")
+    if not n_mad > 0:
+        raise ValueError("n_mad must be positive")
+    dc = device.device_cloud(block_cloud)
+    mem = torch.zeros(dc.count, dtype=torch.int32, device=dc.device)
+    lo, hi = lodgen.block_bounds(dc, mem, 1, n_mad)
+    return lo[0], hi[0]
+
+
+def build_lod(cloud, grid, cameras: Sequence, config) -> "LodScene":
+    """lod.build_lod (lod.py:211-248): every detail level of a partitioned scene."""
+    from . import lodgen
+    from .core import GaussianCloud
+    dc = device.device_cloud(cloud)
+    n_blocks = int(grid.n_blocks)
+    mem = torch.as_tensor(np.asarray(grid.membership).astype(np.int32), device=dc.device)
+    dscene = lodgen.build_lod_cloud(dc, mem, n_blocks, cameras, config.distance_intervals,
+                                    config.compression_rates, config.lod_sh_degrees,
+                                    float(config.n_mad))
+    levels = []
+    for L in range(dscene.n_levels):
+        blocks = []
+        for j in range(n_blocks):
+            a = dscene.block_cloud_host(L, j)
+            blocks.append(GaussianCloud(a["positions"], a["opacities"], a["scales"],
+                                        a["rotations"], a["sh"]))
+        levels.append(tuple(blocks))
+    scene = LodScene(levels=tuple(levels), bounds_min=dscene.bounds_min,
+                     bounds_max=dscene.bounds_max, distance_intervals=config.distance_intervals,
+                     sh_degrees=dscene.sh_degrees, n_mad=float(config.n_mad), full=cloud)
+    device.prime_lod_cache(scene, dscene)
+    return scene
 
 
 @dataclass(frozen=True)

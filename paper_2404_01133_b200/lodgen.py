@@ -1,20 +1,20 @@
-"""Offline LoD generation on the GPU.
+"""LoD generation on the GPU, hand-written kernels.
 
 Builds the per-block detail levels of a partitioned scene the way
-citysplat.lod.build_lod does (lod.py:211-248):
+citysplat.lod.build_lod does (lod.py:211-248), entirely through libcsgpu:
 
-* ``significance_scores`` (lod.py:54-101): training-view hit count x opacity x
-  percentile-clamped volume^0.1 -- a view hits a Gaussian whose centre is in
-  front of the near plane, projects inside the image and whose support radius
-  (from the largest eigenvalue of cov2d + 0.3) is at least half a pixel;
-* a stable descending ranking (ties -> lower index, lod.py:114-116);
-* level L keeps the top ceil(rate_L K - 1e-9 K) globally (lod.py:104-111) and
-  splits them by block in ascending index order, SH truncated per level;
-* MAD-clipped world bounds per block from the full membership (lod.py:130-147).
+* ``significance_scores`` (lod.py:54-101) -> ``cs_significance`` (K15 hit
+  counts in the projection's float64 op order, volume percentile, scores);
+* ``priority``  (lod.py:114-116)          -> ``cs_priority`` (stable 64-bit
+  radix sort of the complemented score bits: descending, ties -> lower index);
+* level rows    (lod.py:222-234)          -> ``cs_lod_rows`` (level L keeps the
+  top ceil(rate_L K - 1e-9 K), grouped by block, ascending index);
+* ``mad_bounds`` (lod.py:130-147)         -> ``cs_mad_bounds`` (per-block
+  medians / MADs from stable sorts, clipping as the reference);
+* ``cloud.take(rows).with_sh_degree(d)``  -> ``cs_gather_cloud``.
 
-Membership comes from the CUDA contraction/binning kernel (cs_block_of_points).
-This is the offline scene build feeding the benchmark, not the timed path; it
-runs as float64 torch ops on the device.
+Membership comes from the contraction/binning kernel (cs_block_of_points).
+Host-facing mirrors with the reference signatures live in ``lod.py``.
 """
 
 from __future__ import annotations
@@ -64,57 +64,45 @@ def block_membership(positions: torch.Tensor, p_min, p_max, dims) -> torch.Tenso
     return out
 
 
-def _rotmats(q: torch.Tensor) -> torch.Tensor:
-    w, x, y, z = q.unbind(1)
-    r = torch.stack([
-        1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
-        2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
-        2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)], dim=1)
-    return r.view(-1, 3, 3)
+def _cams(cameras):
+    views = [c if hasattr(c, "rotation_w2c") else c.view for c in cameras]
+    arr = (_lib.CsCamera * max(len(views), 1))()
+    for i, v in enumerate(views):
+        arr[i] = device.camera_struct(v)
+    return arr, len(views)
 
 
-def significance_scores(positions, opacities, scales, rotations, cameras, near=0.2,
-                        alpha_floor=1.0 / 255.0, chunk=1 << 22) -> torch.Tensor:
-    k = positions.shape[0]
-    dev = positions.device
-    hits = torch.zeros(k, dtype=torch.float64, device=dev)
-    ss = math.sqrt(2.0 * math.log(1.0 / alpha_floor))
-    for s in range(0, k, chunk):
-        e = min(k, s + chunk)
-        p = positions[s:e].double()
-        r = _rotmats(rotations[s:e].double())
-        sc2 = scales[s:e].double() ** 2
-        sigma = torch.einsum("kij,kj,klj->kil", r, sc2, r)
-        for cam in cameras:
-            R = torch.from_numpy(np.asarray(cam.rotation_w2c, dtype=np.float64)).to(dev)
-            T = torch.from_numpy(np.asarray(cam.translation_w2c, dtype=np.float64)).to(dev)
-            t = p @ R.T + T
-            z = t[:, 2]
-            front = z > near
-            zs = torch.where(front, z, torch.ones_like(z))
-            u = cam.fx * t[:, 0] / zs + cam.cx
-            v = cam.fy * t[:, 1] / zs + cam.cy
-            on = front & (u >= 0) & (u <= cam.width) & (v >= 0) & (v <= cam.height)
-            V = torch.einsum("ij,kjl,ml->kim", R, sigma, R)
-            J = torch.zeros((e - s, 2, 3), dtype=torch.float64, device=dev)
-            J[:, 0, 0] = cam.fx / zs
-            J[:, 0, 2] = -cam.fx * t[:, 0] / (zs * zs)
-            J[:, 1, 1] = cam.fy / zs
-            J[:, 1, 2] = -cam.fy * t[:, 1] / (zs * zs)
-            cov = J @ V @ J.transpose(1, 2)
-            a = cov[:, 0, 0] + 0.3
-            b = cov[:, 0, 1]
-            c = cov[:, 1, 1] + 0.3
-            mid = 0.5 * (a + c)
-            lam = mid + torch.sqrt(torch.clamp(mid * mid - (a * c - b * b), min=0.0))
-            radius = ss * torch.sqrt(lam)
-            hits[s:e] += (on & (radius >= MIN_FOOTPRINT_RADIUS)).double()
-    volume = scales.double().prod(dim=1)
-    cap = float(np.percentile(volume.cpu().numpy(), VOLUME_PERCENTILE))
-    return hits * opacities.double() * torch.clamp(volume, max=cap) ** VOLUME_EXPONENT
+def significance_scores(cloud: "device.DeviceCloud", cameras: Sequence, settings=None,
+                        return_hits: bool = False):
+    """lod.significance_scores (lod.py:54-101) of a DeviceCloud -> float64 device tensor."""
+    from .render import RenderSettings
+    settings = settings or RenderSettings()
+    k = cloud.count
+    dev = cloud.device
+    scores = torch.empty(k, dtype=torch.float64, device=dev)
+    hits = torch.empty(k, dtype=torch.int32, device=dev)
+    arr, n = _cams(cameras)
+    desc = cloud.desc()
+    cset = device.settings_struct(settings)
+    check(_lib.load().cs_significance(device.context(dev.index), ctypes.byref(desc),
+                                      ctypes.cast(arr, ctypes.c_void_p), n, ctypes.byref(cset),
+                                      scores.data_ptr(), hits.data_ptr(), device.stream_handle(dev)),
+          "cs_significance")
+    return (scores, hits) if return_hits else scores
+
+
+def priority(scores: torch.Tensor) -> torch.Tensor:
+    """lod._priority (lod.py:114-116): int32 indices, descending score, ties -> lower index."""
+    scores = scores.to(torch.float64).contiguous()
+    order = torch.empty(scores.shape[0], dtype=torch.int32, device=scores.device)
+    check(_lib.load().cs_priority(device.context(scores.device.index), scores.shape[0],
+                                  scores.data_ptr(), order.data_ptr(),
+                                  device.stream_handle(scores.device)), "cs_priority")
+    return order
 
 
 def keep_count(rate: float, k: int) -> int:
+    """lod._keep_count (lod.py:104-111)."""
     if not 0.0 < rate <= 1.0:
         raise ValueError("compression rate must be in (0, 1]")
     if k == 0:
@@ -122,26 +110,73 @@ def keep_count(rate: float, k: int) -> int:
     return min(k, max(1, math.ceil(rate * k - 1e-9 * k)))
 
 
-def _median(x: torch.Tensor) -> torch.Tensor:
-    """np.median along dim 0 (mean of the two middle values for even n)."""
-    n = x.shape[0]
-    s = torch.sort(x, dim=0).values
-    if n % 2:
-        return s[n // 2]
-    return 0.5 * (s[n // 2 - 1] + s[n // 2])
+def level_rows(order: torch.Tensor, membership: torch.Tensor, n_blocks: int, rates_coarsest_first):
+    """Kept rows of every level (lod.py:222-234) -> (rows int32 device (L, K), counts (L, J))."""
+    k = order.shape[0]
+    n_levels = len(rates_coarsest_first)
+    rows = torch.empty((n_levels, max(k, 1)), dtype=torch.int32, device=order.device)
+    counts = np.zeros((n_levels, n_blocks), dtype=np.int64)
+    rates = np.ascontiguousarray(rates_coarsest_first, dtype=np.float64)
+    mem = membership.to(torch.int32).contiguous()
+    check(_lib.load().cs_lod_rows(device.context(order.device.index), k, order.data_ptr(),
+                                  mem.data_ptr(), n_blocks, rates.ctypes.data, n_levels,
+                                  rows.data_ptr(), counts.ctypes.data,
+                                  device.stream_handle(order.device)), "cs_lod_rows")
+    return rows, counts
 
 
-def mad_bounds(p: torch.Tensor, n_mad: float):
-    p = p.double()
-    lo = p.min(dim=0).values
-    hi = p.max(dim=0).values
-    med = _median(p)
-    mad = _median((p - med).abs())
-    if math.isfinite(n_mad):
-        ok = mad > 0
-        lo = torch.where(ok, torch.maximum(lo, med - n_mad * mad), lo)
-        hi = torch.where(ok, torch.minimum(hi, med + n_mad * mad), hi)
-    return lo.cpu().numpy(), hi.cpu().numpy()
+def block_bounds(cloud: "device.DeviceCloud", membership: torch.Tensor, n_blocks: int, n_mad: float):
+    """mad_bounds (lod.py:130-147) of every block's members -> (bmin, bmax) (J, 3) float64."""
+    bmin = np.zeros((n_blocks, 3))
+    bmax = np.zeros((n_blocks, 3))
+    mem = membership.to(torch.int32).contiguous()
+    desc = cloud.desc()
+    check(_lib.load().cs_mad_bounds(device.context(cloud.device.index), ctypes.byref(desc),
+                                    mem.data_ptr(), n_blocks, float(n_mad), bmin.ctypes.data,
+                                    bmax.ctypes.data, device.stream_handle(cloud.device)),
+          "cs_mad_bounds")
+    return bmin, bmax
+
+
+def gather(cloud: "device.DeviceCloud", rows: torch.Tensor, sh_coeffs: int) -> "device.DeviceCloud":
+    """cloud.take(rows).with_sh_degree(...) on the device (rows: int32 device)."""
+    n = int(rows.shape[0])
+    dev = cloud.device
+    dt = cloud.pos_op.dtype
+    quads = torch.empty((3, n, 4), dtype=dt, device=dev)
+    stride = device.sh_stride(sh_coeffs)
+    sh = torch.empty((n, stride), dtype=torch.float32, device=dev)
+    out = device.DeviceCloud(quads[0], quads[1], quads[2], sh, sh_coeffs, n)
+    src = cloud.desc()
+    dst = out.desc()
+    rows = rows.to(torch.int32).contiguous()
+    check(_lib.load().cs_gather_cloud(device.context(dev.index), ctypes.byref(src), rows.data_ptr(),
+                                      n, ctypes.byref(dst), device.stream_handle(dev)),
+          "cs_gather_cloud")
+    return out
+
+
+def build_lod_cloud(full: "device.DeviceCloud", membership: torch.Tensor, n_blocks: int,
+                    cameras: Sequence,
+                    distance_intervals=((0.0, 200.0), (200.0, 400.0), (400.0, math.inf)),
+                    compression_rates=(0.5, 0.34, 0.25), lod_sh_degrees=(3, 2, 1), n_mad=4.0,
+                    scores=None, settings=None) -> device.DeviceLodScene:
+    """build_lod (lod.py:211-248) of a DeviceCloud into a DeviceLodScene.
+
+    Rates / SH degrees are finest-first as in RunConfig and reversed here."""
+    if scores is None:
+        scores = significance_scores(full, cameras, settings)
+    order = priority(scores)
+    rates = tuple(reversed(compression_rates))
+    degrees = tuple(reversed(lod_sh_degrees))
+    rows, counts = level_rows(order, membership, n_blocks, rates)
+    level_clouds = []
+    for L, deg in enumerate(degrees):
+        C = min((deg + 1) ** 2, full.sh_coeffs)
+        level_clouds.append(gather(full, rows[L, :int(counts[L].sum())], C))
+    bmin, bmax = block_bounds(full, membership, n_blocks, n_mad)
+    return device.DeviceLodScene.from_device_levels(level_clouds, counts, bmin, bmax,
+                                                    distance_intervals, degrees, full.device.index)
 
 
 def build_lod_device(positions, opacities, scales, rotations, sh, membership: torch.Tensor,
@@ -149,34 +184,7 @@ def build_lod_device(positions, opacities, scales, rotations, sh, membership: to
                                                                            (400.0, math.inf)),
                      compression_rates=(0.5, 0.34, 0.25), lod_sh_degrees=(3, 2, 1), n_mad=4.0,
                      scores=None) -> device.DeviceLodScene:
-    """build_lod (lod.py:211-248) into a DeviceLodScene; rates/degrees finest-first."""
-    k = positions.shape[0]
-    dev = positions.device
-    if scores is None:
-        scores = significance_scores(positions, opacities, scales, rotations, cameras)
-    order = torch.sort(-scores, stable=True).indices
-    rates = tuple(reversed(compression_rates))
-    degrees = tuple(reversed(lod_sh_degrees))
-    mem = membership.long()
-    level_clouds = []
-    counts = np.zeros((len(rates), n_blocks), dtype=np.int64)
-    for L, (rate, deg) in enumerate(zip(rates, degrees)):
-        keep = keep_count(rate, k)
-        mask = torch.zeros(k, dtype=torch.bool, device=dev)
-        mask[order[:keep]] = True
-        idx = torch.nonzero(mask).squeeze(1)            # ascending original index
-        blk = mem[idx]
-        perm = torch.sort(blk, stable=True).indices     # group by block, keep index order
-        rows = idx[perm]
-        counts[L] = torch.bincount(blk, minlength=n_blocks).cpu().numpy()
-        C = (deg + 1) ** 2
-        level_clouds.append(device.DeviceCloud.from_torch(
-            positions[rows], opacities[rows], scales[rows], rotations[rows], sh[rows][:, :, :C]))
-    bmin = np.zeros((n_blocks, 3))
-    bmax = np.zeros((n_blocks, 3))
-    for j in range(n_blocks):
-        m = torch.nonzero(mem == j).squeeze(1)
-        if m.numel():
-            bmin[j], bmax[j] = mad_bounds(positions[m], n_mad)
-    return device.DeviceLodScene.from_device_levels(level_clouds, counts, bmin, bmax,
-                                                    distance_intervals, degrees, dev.index)
+    """build_lod from device tensors (K,3),(K,),(K,3),(K,4),(K,3,C)."""
+    full = device.DeviceCloud.from_torch(positions, opacities, scales, rotations, sh)
+    return build_lod_cloud(full, membership, n_blocks, cameras, distance_intervals,
+                           compression_rates, lod_sh_degrees, n_mad, scores)

@@ -97,3 +97,19 @@ def golden_city():
 @pytest.fixture(scope="session")
 def golden_fuse():
     return Golden("fuse.npz")
+
+
+@pytest.fixture(scope="session")
+def golden_lodgen():
+    return Golden("lodgen.npz")
+
+
+def lodgen_inputs(g):
+    """(cloud, cameras, membership, n_blocks) of tests/golden/lodgen.npz."""
+    k = int(g["positions"].shape[0])
+    rng = np.random.default_rng(1)
+    cloud = SimpleNamespace(positions=g["positions"], opacities=g["opacities"], scales=g["scales"],
+                            rotations=g["rotations"],
+                            sh=rng.normal(0.0, 0.2, (k, 3, 16)).astype(np.float32), count=k)
+    cams = [g.camera(f"cam{i:02d}") for i in range(int(g["n_cams"]))]
+    return cloud, cams, g["membership"], int(g["n_blocks"])

@@ -15,6 +15,11 @@ the reference's own outputs of the hot-path functions:
                assemble_render_set (block, forced, pointwise) and the render of
                the assembled cloud, for several cameras
   fuse.npz     partition.fuse (partition.py:570-587) of perturbed block clouds
+  lodgen.npz   LoD generation: significance_scores
+               (lod.py:54-101), the stable priority order (lod.py:114-116),
+               build_lod's per-level / per-block kept rows (lod.py:211-248) and
+               mad_bounds (lod.py:130-147), on a 3x3-block city with exact
+               duplicate Gaussians (score ties)
 
 OPENBLAS_CORETYPE=Sandybridge pins numpy's dgemm to the no-FMA kernel
 (SURVEY.md Appendix B.1); the script refuses to run without it.
@@ -38,7 +43,8 @@ sys.path.insert(0, str(REF / "tests"))
 
 from citysplat.config import RunConfig  # noqa: E402
 from citysplat.core import CameraView, Gaussian, GaussianCloud, SH_C0  # noqa: E402
-from citysplat.lod import assemble_render_set, build_lod, decide_visibility  # noqa: E402
+from citysplat.lod import (_keep_count, _priority, assemble_render_set, build_lod,  # noqa: E402
+                           decide_visibility, mad_bounds, significance_scores)
 from citysplat.partition import ContractionMap, fuse, grid_partition  # noqa: E402
 from citysplat.render import RenderSettings, _bin_tiles, _project_cloud, rasterize_stats  # noqa: E402
 from citysplat.synthetic import generate_synthetic_city, look_at  # noqa: E402
@@ -223,9 +229,59 @@ def make_fuse():
     print("fuse.npz", fused.count, "fused of", sum(b.count for b, _ in blocks))
 
 
+def make_lodgen():
+    bundle = generate_synthetic_city(seed=11, extent=120.0, n_buildings=30, n_cameras=24,
+                                     target_gaussians=20_000, image_size=(320, 240))
+    c = quantize(bundle.cloud)
+    # append exact duplicates of 500 Gaussians: identical scores, ties broken by index
+    dup = np.arange(0, 20_000, 40)
+    cloud = GaussianCloud(positions=np.concatenate([c.positions, c.positions[dup]]),
+                          opacities=np.concatenate([c.opacities, c.opacities[dup]]),
+                          scales=np.concatenate([c.scales, c.scales[dup]]),
+                          rotations=np.concatenate([c.rotations, c.rotations[dup]]),
+                          sh=np.concatenate([c.sh, c.sh[dup]]))
+    cmap = ContractionMap.central_third(cloud)
+    grid = grid_partition(cloud, cmap, (3, 3))
+    config = RunConfig(block_dims=(3, 3), n_mad=2.5)
+    cams = [r.view for r in bundle.train_cameras()]
+    scores = significance_scores(cloud, cams)
+    order = _priority(scores)
+    lod = build_lod(cloud, grid, cams, config)
+    store = dict(positions=cloud.positions.astype(np.float32), opacities=cloud.opacities.astype(np.float32),
+                 scales=cloud.scales.astype(np.float32), rotations=cloud.rotations.astype(np.float32),
+                 membership=grid.membership.astype(np.int32), n_blocks=np.int64(grid.n_blocks),
+                 rates=np.array(config.compression_rates), sh_degrees=np.array(config.lod_sh_degrees),
+                 n_mad=np.float64(config.n_mad), scores=scores, order=order.astype(np.int32),
+                 bounds_min=lod.bounds_min, bounds_max=lod.bounds_max,
+                 n_cams=np.int64(len(cams)))
+    assert np.array_equal(store["positions"].astype(np.float64), cloud.positions)
+    for i, cam in enumerate(cams):
+        put(store, f"cam{i:02d}", cam_dict(cam))
+    rates = tuple(reversed(config.compression_rates))
+    for L, rate in enumerate(rates):
+        keep = _keep_count(rate, cloud.count)
+        mask = np.zeros(cloud.count, dtype=bool)
+        mask[order[:keep]] = True
+        for j in range(grid.n_blocks):
+            idx = np.nonzero(mask & (grid.membership == j))[0]
+            assert np.array_equal(lod.levels[L][j].positions, cloud.positions[idx])
+            store[f"level{L}/block{j}"] = idx.astype(np.int32)
+    # mad_bounds with clipping disabled (n_mad = inf) for one block
+    lo, hi = mad_bounds(cloud.take(grid.members(4)), math.inf)
+    store["block4_inf_lo"], store["block4_inf_hi"] = lo, hi
+    np.savez_compressed(OUT / "lodgen.npz", **store)
+    print("lodgen.npz", cloud.count, "Gaussians,", len(cams), "views, ties:", len(dup),
+          "zero scores:", int((scores == 0).sum()))
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()["make_" + name]()
+        sys.exit(0)
     make_render()
     make_city()
     make_fuse()
+    make_lodgen()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size // 1024, "KiB")
