@@ -37,6 +37,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+LOD_BUILD = None
 STAGES = ("select", "project", "depth_sort", "gather_scan", "duplicate", "tile_sort", "ranges", "blend")
 SCENES = {
     # name: (gaussians, extent, buildings, blocks, intervals, altitudes, W, H)
@@ -82,8 +83,16 @@ def build_scene(name: str, seed: int, dev, keep_raw: bool = False):
     mem = lodgen.block_membership(pos, pmin, pmax, dims)
     cams = city_cameras(64, extent, W, H, seed=seed)
     train = [c for i, c in enumerate(cams) if i % 8 != 0]   # every 8th is test (colmap.py:152-156)
+    torch.cuda.synchronize()
+    t_lod = time.perf_counter()
     scene = lodgen.build_lod_device(pos, op, sc, q, sh, mem, int(np.prod(dims)), train,
                                     distance_intervals=ints)
+    torch.cuda.synchronize()
+    global LOD_BUILD
+    LOD_BUILD = {"s": round(time.perf_counter() - t_lod, 3), "gaussians": int(pos.shape[0]),
+                 "views": len(train), "blocks": int(np.prod(dims)),
+                 "what": "significance (K15) + priority sort + level rows + MAD bounds + gather "
+                         "(lodgen.build_lod_device, build_lod lod.py:211-248), wall clock after sync"}
     lo = pos.double().min(dim=0).values.cpu().numpy()
     hi = pos.double().max(dim=0).values.cpu().numpy()
     center = 0.5 * (lo + hi)
@@ -395,6 +404,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "train": train,
+            "lod_build": LOD_BUILD,
             "gpu_launches": K * launches_per_frame(),
             "clocks": clocks,
         }

@@ -57,6 +57,16 @@ def significance_scores(cloud, cameras: Sequence, settings=None) -> np.ndarray:
     return lodgen.significance_scores(dc, cameras, _device_settings(settings)).cpu().numpy()
 
 
+def _host_cloud(cloud):
+    if hasattr(cloud, "take") and hasattr(cloud, "with_sh_degree"):
+        return cloud
+    return GaussianCloud(np.asarray(cloud.positions, dtype=np.float64),
+                         np.asarray(cloud.opacities, dtype=np.float64),
+                         np.asarray(cloud.scales, dtype=np.float64),
+                         np.asarray(cloud.rotations, dtype=np.float64),
+                         np.asarray(cloud.sh, dtype=np.float64))
+
+
 def compress(cloud, rate: float, sh_degree: int = 3, cameras: Sequence = (), *,
              scores: Optional[np.ndarray] = None):
     """lod.compress (lod.py:119-127): the ceil(rate*K) highest-significance
@@ -69,10 +79,10 @@ def compress(cloud, rate: float, sh_degree: int = 3, cameras: Sequence = (), *,
     else:
         sc = torch.as_tensor(np.asarray(scores, dtype=np.float64), device=device.default_device())
     if k == 0:
-        return cloud.take(np.zeros(0, dtype=np.int64)).with_sh_degree(sh_degree)
+        return _host_cloud(cloud).take(np.zeros(0, dtype=np.int64)).with_sh_degree(sh_degree)
     order = lodgen.priority(sc)
     kept = torch.sort(order[:keep].long()).values.cpu().numpy()
-    return cloud.take(kept).with_sh_degree(sh_degree)
+    return _host_cloud(cloud).take(kept).with_sh_degree(sh_degree)
 
 
 def mad_bounds(block_cloud, n_mad: float) -> Tuple[np.ndarray, np.ndarray]:
