@@ -14,7 +14,8 @@ _lib.load()  # fail loudly without the CUDA extension
 
 from .core import CameraView, Gaussian, GaussianCloud, Image  # noqa: E402
 from .lod import (AssembledSet, LodScene, VisibilityDecision, assemble_render_set,  # noqa: E402
-                  block_visible, decide_visibility, select_level)
+                  block_visible, build_lod, compress, decide_visibility, mad_bounds, select_level,
+                  significance_scores)
 from .render import (FrameStats, RenderSettings, SplatPrimitive, project_gaussian,  # noqa: E402
                      rasterize, rasterize_stats, render)
 
@@ -22,6 +23,7 @@ __version__ = "0.1.0"
 __all__ = [
     "CameraView", "Gaussian", "GaussianCloud", "Image", "LodScene", "VisibilityDecision",
     "AssembledSet", "assemble_render_set", "block_visible", "decide_visibility", "select_level",
+    "significance_scores", "compress", "mad_bounds", "build_lod",
     "FrameStats", "RenderSettings", "SplatPrimitive", "project_gaussian", "rasterize",
     "rasterize_stats", "render",
 ]
