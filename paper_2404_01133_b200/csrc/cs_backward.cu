@@ -287,20 +287,19 @@ __device__ __forceinline__ void for_sh_basis(double x, double y, double z, int d
 
 __device__ __forceinline__ int deg_of(int c) { return c >= 16 ? 3 : c >= 9 ? 2 : c >= 4 ? 1 : 0; }
 
-// K11: one thread per cloud row k (= splat id of the single-cloud source), in
-// row order so every parameter, partial and gradient access is coalesced;
-// rows the forward culled (depth key ~0) get zero gradients, so the output
-// buffers need no separate clear.
+// K11a: geometry.  One thread per cloud row k (= splat id of the single-cloud
+// source), in row order so every parameter, partial and gradient access is
+// coalesced; rows the forward culled (depth key ~0) get zero gradients, so the
+// output buffers need no separate clear.  Writes dL/d{position (without the
+// view-direction term of the colour, added by K11b), scale, rotation,
+// opacity}.
 __global__ void __launch_bounds__(128)
-k_project_bwd(const cs_cloud cl, const uint64_t* __restrict__ depth_keys, cs_camera cam,
+k_project_bwd_geom(const cs_cloud cl, const uint64_t* __restrict__ depth_keys, cs_camera cam,
               cs_settings st, const float* __restrict__ grads, int64_t cap, cs_grads out) {
   const int64_t K = cl.count;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K;
        k += (int64_t)gridDim.x * blockDim.x) {
     if (depth_keys[k] == ~0ull) {  // culled by the forward projection: no gradient
-      const int C3 = 3 * cl.sh_coeffs;
-      float* gsh0 = out.sh + k * (int64_t)C3;
-      for (int i = 0; i < C3; ++i) gsh0[i] = 0.f;
       for (int i = 0; i < 3; ++i) out.positions[3 * k + i] = out.scales[3 * k + i] = 0.f;
       for (int i = 0; i < 4; ++i) out.rotations[4 * k + i] = 0.f;
       out.opacities[k] = 0.f;
@@ -404,45 +403,99 @@ k_project_bwd(const cs_cloud cl, const uint64_t* __restrict__ depth_keys, cs_cam
                    q * dR[7] - 2.0 * y * dR[8]);
     dq[3] = 2.0 * (-2.0 * q * dR[0] - w * dR[1] + x * dR[2] + w * dR[3] - 2.0 * q * dR[4] +
                    y * dR[5] + x * dR[6] + y * dR[7]);
-    // colour: SH coefficients and the view direction
-    const int C = cl.sh_coeffs;
-    const int degree = min((int)st.sh_degree, deg_of(C));
-    double v[3] = {gm.px - cam.center[0], gm.py - cam.center[1], gm.pz - cam.center[2]};
-    const double nv = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
-    const double d[3] = {v[0] / nv, v[1] / nv, v[2] / nv};
-    const float* row = cl.sh + k * cl.sh_stride;
-    // pass 1: colour before the clip (core.py:169-172) -> which channels pass gradient
-    double val[3] = {0.5, 0.5, 0.5};
-    for_sh_basis(d[0], d[1], d[2], degree, [&](int n, double Yn, double, double, double) {
-#pragma unroll
-      for (int ch = 0; ch < 3; ++ch) val[ch] += (double)row[ch * C + n] * Yn;
-    });
-    double gc[3];
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch)
-      gc[ch] = (val[ch] >= 0.0 && val[ch] <= 1.0) ? (double)gin[6 + ch] : 0.0;
-    // pass 2: dL/dsh = gc * Y_n, dL/ddir = sum gc * sh * dY_n
-    float* gsh = out.sh + k * (int64_t)(3 * C);
-    double dd[3] = {0.0, 0.0, 0.0};
-    for_sh_basis(d[0], d[1], d[2], degree, [&](int n, double Yn, double gx, double gy, double gz) {
-      double ws = 0.0;
-#pragma unroll
-      for (int ch = 0; ch < 3; ++ch) {
-        gsh[ch * C + n] = (float)(gc[ch] * Yn);
-        ws += gc[ch] * (double)row[ch * C + n];
-      }
-      dd[0] += ws * gx;
-      dd[1] += ws * gy;
-      dd[2] += ws * gz;
-    });
-    const double ddot = dd[0] * d[0] + dd[1] * d[1] + dd[2] * d[2];
-    for (int i = 0; i < 3; ++i) dp[i] += (dd[i] - d[i] * ddot) / nv;
     for (int i = 0; i < 3; ++i) {
       out.positions[3 * k + i] = (float)dp[i];
       out.scales[3 * k + i] = (float)ds[i];
     }
     for (int i = 0; i < 4; ++i) out.rotations[4 * k + i] = (float)dq[i];
     out.opacities[k] = gin[5];
+  }
+}
+
+// K11b: colour.  dL/dsh = gc * Y_n for the channels the forward's clip passed
+// (core.py:169-172), and the view-direction term of the colour added to
+// K11a's position gradient.  A warp owns 32 consecutive rows: their SH rows
+// (contiguous in HBM) are staged into shared memory with coalesced float4
+// loads (row pitch padded to an odd word count: conflict-free per-lane
+// access), each lane evaluates its row and overwrites it with the gradient in
+// place, and the warp stores the 32 gradient rows coalesced.
+constexpr int kShBwdThreads = 256;
+
+__global__ void __launch_bounds__(kShBwdThreads)
+k_project_bwd_sh(const cs_cloud cl, const uint64_t* __restrict__ depth_keys, cs_camera cam,
+                 cs_settings st, const float* __restrict__ grads, int64_t cap, cs_grads out,
+                 int pitch) {
+  extern __shared__ float s_rows[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* buf = s_rows + (size_t)warp * 32 * pitch;
+  const int64_t K = cl.count;
+  const int C = cl.sh_coeffs, C3 = 3 * C, stride = cl.sh_stride;
+  const int degree = min((int)st.sh_degree, deg_of(C));
+  const int nb = (degree + 1) * (degree + 1);
+  for (int64_t base = ((int64_t)blockIdx.x * (kShBwdThreads / 32) + warp) * 32; base < K;
+       base += (int64_t)gridDim.x * (kShBwdThreads / 32) * 32) {
+    const int n_rows = (int)min((int64_t)32, K - base);
+    {  // stage the rows (stride % 4 == 0: float4 loads)
+      const float4* src = reinterpret_cast<const float4*>(cl.sh + base * stride);
+      const int n4 = n_rows * stride / 4;
+      for (int i = lane; i < n4; i += 32) {
+        const float4 v = __ldg(src + i);
+        const int e = 4 * i, r = e / stride, c = e - r * stride;
+        float* d = buf + r * pitch + c;
+        d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+      }
+    }
+    __syncwarp();
+    const int64_t k = base + lane;
+    float* row = buf + lane * pitch;
+    if (lane < n_rows) {
+      if (depth_keys[k] == ~0ull) {
+        for (int i = 0; i < C3; ++i) row[i] = 0.f;
+      } else {
+        const Geom gm = load_geom(cl, k);
+        double gin[3];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) gin[ch] = (double)grads[(int64_t)(6 + ch) * cap + k];
+        const double v[3] = {gm.px - cam.center[0], gm.py - cam.center[1], gm.pz - cam.center[2]};
+        const double nv = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+        const double d[3] = {v[0] / nv, v[1] / nv, v[2] / nv};
+        // pass 1: colour before the clip (core.py:169-172) -> which channels pass gradient
+        double val[3] = {0.5, 0.5, 0.5};
+        for_sh_basis(d[0], d[1], d[2], degree, [&](int n, double Yn, double, double, double) {
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) val[ch] += (double)row[ch * C + n] * Yn;
+        });
+        double gc[3];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) gc[ch] = (val[ch] >= 0.0 && val[ch] <= 1.0) ? gin[ch] : 0.0;
+        // pass 2: dL/dsh = gc * Y_n (in place), dL/ddir = sum gc * sh * dY_n
+        double dd[3] = {0.0, 0.0, 0.0};
+        for_sh_basis(d[0], d[1], d[2], degree, [&](int n, double Yn, double gx, double gy, double gz) {
+          double ws = 0.0;
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            ws += gc[ch] * (double)row[ch * C + n];
+            row[ch * C + n] = (float)(gc[ch] * Yn);
+          }
+          dd[0] += ws * gx;
+          dd[1] += ws * gy;
+          dd[2] += ws * gz;
+        });
+        // stored bands above the evaluated degree get no gradient
+        for (int n = nb; n < C; ++n)
+          for (int ch = 0; ch < 3; ++ch) row[ch * C + n] = 0.f;
+        const double ddot = dd[0] * d[0] + dd[1] * d[1] + dd[2] * d[2];
+        for (int i = 0; i < 3; ++i) out.positions[3 * k + i] += (float)((dd[i] - d[i] * ddot) / nv);
+      }
+    }
+    __syncwarp();
+    // gradient rows are packed (3C floats per row): coalesced scalar stores
+    float* dst = out.sh + base * C3;
+    for (int e = lane; e < n_rows * C3; e += 32) {
+      const int r = e / C3, c = e - r * C3;
+      dst[e] = buf[r * pitch + c];
+    }
+    __syncwarp();
   }
 }
 
@@ -471,7 +524,17 @@ void launch_project_bwd(const cs_cloud& cl, const uint64_t* depth_keys, const cs
                         cudaStream_t s) {
   const int64_t blocks = std::min<int64_t>((cl.count + 127) / 128, 148 * 16);
   if (blocks <= 0) return;
-  k_project_bwd<<<(unsigned)blocks, 128, 0, s>>>(cl, depth_keys, cam, st, grads, cap, out);
+  k_project_bwd_geom<<<(unsigned)blocks, 128, 0, s>>>(cl, depth_keys, cam, st, grads, cap, out);
+  const int pitch = cl.sh_stride | 1;  // odd word pitch: lane rows hit distinct banks
+  const size_t smem = sizeof(float) * (kShBwdThreads / 32) * 32 * pitch;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_project_bwd_sh, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  const int64_t blocks_sh = std::min<int64_t>((cl.count + kShBwdThreads - 1) / kShBwdThreads, 148 * 4);
+  k_project_bwd_sh<<<(unsigned)blocks_sh, kShBwdThreads, smem, s>>>(cl, depth_keys, cam, st, grads,
+                                                                    cap, out, pitch);
 }
 
 }  // namespace cs
