@@ -242,55 +242,91 @@ __device__ __forceinline__ void adam1(float& p, float& m, float& v, float g, flo
   p -= (lr / bc1) * (m / denom);
 }
 
-__global__ void k_adam_geom(int64_t K, float* __restrict__ geom, float* __restrict__ gm,
-                            float* __restrict__ gv, cs_grads g, cs_adam_hparams h, float bc1,
-                            float bc2s, float4* __restrict__ pos_op, float4* __restrict__ scale,
-                            float4* __restrict__ quat) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    float p[11], m[11], v[11], gr[11];
+// One warp per 32 consecutive Gaussians: their (K, 11) rows of parameters and
+// both moments are contiguous, so they are staged through shared memory with
+// coalesced float4 copies (odd row pitch 11: conflict-free per-lane access),
+// updated per lane, and written back the same way.
+constexpr int kAdamThreads = 256;
+
+__global__ void __launch_bounds__(kAdamThreads)
+k_adam_geom(int64_t K, float* __restrict__ geom, float* __restrict__ gm,
+            float* __restrict__ gv, cs_grads g, cs_adam_hparams h, float bc1,
+            float bc2s, float4* __restrict__ pos_op, float4* __restrict__ scale,
+            float4* __restrict__ quat) {
+  __shared__ __align__(16) float s_buf[kAdamThreads / 32][3][32 * 11];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* arrs[3] = {geom, gm, gv};
+  for (int64_t base = ((int64_t)blockIdx.x * (kAdamThreads / 32) + warp) * 32; base < K;
+       base += (int64_t)gridDim.x * (kAdamThreads / 32) * 32) {
+    const int n_rows = (int)min((int64_t)32, K - base);
+    const int nf = n_rows * 11;
 #pragma unroll
-    for (int i = 0; i < 11; ++i) {
-      p[i] = geom[11 * k + i];
-      m[i] = gm[11 * k + i];
-      v[i] = gv[11 * k + i];
+    for (int a = 0; a < 3; ++a) {
+      const float* src = arrs[a] + base * 11;
+      if (n_rows == 32) {
+        const float4* s4 = reinterpret_cast<const float4*>(src);
+        float4* d4 = reinterpret_cast<float4*>(s_buf[warp][a]);
+        for (int i = lane; i < 88; i += 32) d4[i] = s4[i];
+      } else {
+        for (int i = lane; i < nf; i += 32) s_buf[warp][a][i] = src[i];
+      }
     }
-    // chain the activated-parameter gradients to the raw parameters
+    __syncwarp();
+    const int64_t k = base + lane;
+    if (lane < n_rows) {
+      float* p = &s_buf[warp][0][lane * 11];
+      float* m = &s_buf[warp][1][lane * 11];
+      float* v = &s_buf[warp][2][lane * 11];
+      float gr[11];
+      // chain the activated-parameter gradients to the raw parameters
 #pragma unroll
-    for (int i = 0; i < 3; ++i) gr[i] = g.positions[3 * k + i];
+      for (int i = 0; i < 3; ++i) gr[i] = g.positions[3 * k + i];
 #pragma unroll
-    for (int i = 0; i < 3; ++i) gr[3 + i] = g.scales[3 * k + i] * expf(p[3 + i]);  // d exp
-    {
-      const float q0 = p[6], q1 = p[7], q2 = p[8], q3 = p[9];
-      const float n = sqrtf(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
-      const float inv = 1.f / n;
-      const float u[4] = {q0 * inv, q1 * inv, q2 * inv, q3 * inv};
-      const float gq[4] = {g.rotations[4 * k], g.rotations[4 * k + 1], g.rotations[4 * k + 2],
-                           g.rotations[4 * k + 3]};
-      const float dot = u[0] * gq[0] + u[1] * gq[1] + u[2] * gq[2] + u[3] * gq[3];
+      for (int i = 0; i < 3; ++i) gr[3 + i] = g.scales[3 * k + i] * expf(p[3 + i]);  // d exp
+      {
+        const float q0 = p[6], q1 = p[7], q2 = p[8], q3 = p[9];
+        const float n = sqrtf(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+        const float inv = 1.f / n;
+        const float u[4] = {q0 * inv, q1 * inv, q2 * inv, q3 * inv};
+        const float4 gq4 = reinterpret_cast<const float4*>(g.rotations)[k];
+        const float gq[4] = {gq4.x, gq4.y, gq4.z, gq4.w};
+        const float dot = u[0] * gq[0] + u[1] * gq[1] + u[2] * gq[2] + u[3] * gq[3];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) gr[6 + i] = (gq[i] - u[i] * dot) * inv;  // d (q / |q|)
+        for (int i = 0; i < 4; ++i) gr[6 + i] = (gq[i] - u[i] * dot) * inv;  // d (q / |q|)
+      }
+      {
+        const float sg = 1.f / (1.f + expf(-p[10]));
+        gr[10] = g.opacities[k] * sg * (1.f - sg);  // d sigmoid
+      }
+      const float lrs[11] = {h.lr_position, h.lr_position, h.lr_position, h.lr_scale, h.lr_scale,
+                             h.lr_scale, h.lr_rotation, h.lr_rotation, h.lr_rotation,
+                             h.lr_rotation, h.lr_opacity};
+      float pr[11], mr[11], vr[11];
+#pragma unroll
+      for (int i = 0; i < 11; ++i) {
+        pr[i] = p[i]; mr[i] = m[i]; vr[i] = v[i];
+        adam1(pr[i], mr[i], vr[i], gr[i], lrs[i], h, bc1, bc2s);
+        p[i] = pr[i]; m[i] = mr[i]; v[i] = vr[i];
+      }
+      // activated quads for the next forward
+      const float n = sqrtf(pr[6] * pr[6] + pr[7] * pr[7] + pr[8] * pr[8] + pr[9] * pr[9]);
+      pos_op[k] = make_float4(pr[0], pr[1], pr[2], 1.f / (1.f + expf(-pr[10])));
+      scale[k] = make_float4(expf(pr[3]), expf(pr[4]), expf(pr[5]), 0.f);
+      quat[k] = make_float4(pr[6] / n, pr[7] / n, pr[8] / n, pr[9] / n);
     }
-    {
-      const float sg = 1.f / (1.f + expf(-p[10]));
-      gr[10] = g.opacities[k] * sg * (1.f - sg);  // d sigmoid
-    }
-    const float lrs[11] = {h.lr_position, h.lr_position, h.lr_position, h.lr_scale, h.lr_scale,
-                           h.lr_scale, h.lr_rotation, h.lr_rotation, h.lr_rotation,
-                           h.lr_rotation, h.lr_opacity};
+    __syncwarp();
 #pragma unroll
-    for (int i = 0; i < 11; ++i) adam1(p[i], m[i], v[i], gr[i], lrs[i], h, bc1, bc2s);
-#pragma unroll
-    for (int i = 0; i < 11; ++i) {
-      geom[11 * k + i] = p[i];
-      gm[11 * k + i] = m[i];
-      gv[11 * k + i] = v[i];
+    for (int a = 0; a < 3; ++a) {
+      float* dst = arrs[a] + base * 11;
+      if (n_rows == 32) {
+        float4* d4 = reinterpret_cast<float4*>(dst);
+        const float4* s4 = reinterpret_cast<const float4*>(s_buf[warp][a]);
+        for (int i = lane; i < 88; i += 32) d4[i] = s4[i];
+      } else {
+        for (int i = lane; i < nf; i += 32) dst[i] = s_buf[warp][a][i];
+      }
     }
-    // activated quads for the next forward
-    const float n = sqrtf(p[6] * p[6] + p[7] * p[7] + p[8] * p[8] + p[9] * p[9]);
-    pos_op[k] = make_float4(p[0], p[1], p[2], 1.f / (1.f + expf(-p[10])));
-    scale[k] = make_float4(expf(p[3]), expf(p[4]), expf(p[5]), 0.f);
-    quat[k] = make_float4(p[6] / n, p[7] / n, p[8] / n, p[9] / n);
+    __syncwarp();
   }
 }
 
@@ -335,8 +371,9 @@ void launch_block_adam(int64_t K, int C, float* geom, float* gm, float* gv, floa
   const double bc2 = 1.0 - pow((double)h.beta2, (double)h.step);
   const float bc2s = (float)sqrt(bc2);
   if (K <= 0) return;
-  const int grid = (int)std::min<int64_t>(148 * 8, (K + 255) / 256);
-  k_adam_geom<<<grid, 256, 0, s>>>(K, geom, gm, gv, g, h, (float)bc1, bc2s, pos_op, scale, quat);
+  const int grid = (int)std::min<int64_t>(148 * 8, (K + kAdamThreads - 1) / kAdamThreads);
+  k_adam_geom<<<grid, kAdamThreads, 0, s>>>(K, geom, gm, gv, g, h, (float)bc1, bc2s, pos_op, scale,
+                                            quat);
   const int64_t n = K * 3 * C;
   const int grid2 = (int)std::min<int64_t>(148 * 8, (n / 4 + 255) / 256 + 1);
   k_adam_flat<<<grid2, 256, 0, s>>>(n, sh, shm, shv, g.sh, h.lr_sh, h, (float)bc1, bc2s);
