@@ -40,8 +40,20 @@ constexpr int kBlendThreads = 256;
 // into the warp's shared-memory slot.  The copies of round r are in flight
 // while the warp evaluates round r-1 (two stages per warp).  The walk stops
 // as soon as the box's 32 pixels have terminated.
-template <typename OutT, bool KEEP, bool DIAG>
-__global__ void __launch_bounds__(kBlendThreads)
+template <int PX>
+__device__ __forceinline__ int blend_box_pixel(int b, int lane, int ts, int j) {
+  return PX == 1 ? box_pixel(b, lane, ts) : box_pixel2(b, lane, ts, j);
+}
+
+// PX pixels per lane (1: 8x4 boxes, 2: 8x8 boxes).  With two pixels a lane
+// reads each staged record once for both, and a tile is walked by half as
+// many warps.
+#ifndef CS_BLEND_MINB
+#define CS_BLEND_MINB 1
+#endif
+
+template <typename OutT, bool KEEP, bool DIAG, int PX>
+__global__ void __launch_bounds__(kBlendThreads, CS_BLEND_MINB)
 k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
         const uint32_t* __restrict__ bys, const uint2* __restrict__ ranges,
         const HotRec* __restrict__ hot, const uint32_t* __restrict__ tile_order, int n_items,
@@ -67,11 +79,31 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
     const int tx = t % bp.ntx, ty = t / bp.ntx;
     const uint2 rg = ranges[t];
     const int64_t s0 = rg.x, s1 = rg.y;
-    const int li = box_pixel(b, lane, ts);
-    const int px = tx * ts + li % ts, py = ty * ts + li / ts;
-    const bool valid = li < ts * ts && px < bp.width && py < bp.height;
-    int x0 = valid ? px : 1 << 20, x1 = valid ? px : -(1 << 20);
-    int y0 = valid ? py : 1 << 20, y1 = valid ? py : -(1 << 20);
+    int px[PX], py[PX];
+    bool valid[PX], done[PX];
+    double sx[PX], sy[PX], T[PX];
+    float cr[PX], cg[PX], cb[PX];  // colour accumulates in float32 (SURVEY.md H2 recipe m3)
+    int cnt[PX];
+    int64_t last[PX];
+    int x0 = 1 << 20, x1 = -(1 << 20), y0 = 1 << 20, y1 = -(1 << 20);
+#pragma unroll
+    for (int j = 0; j < PX; ++j) {
+      const int li = blend_box_pixel<PX>(b, lane, ts, j);
+      px[j] = tx * ts + li % ts;
+      py[j] = ty * ts + li / ts;
+      valid[j] = li < ts * ts && px[j] < bp.width && py[j] < bp.height;
+      if (valid[j]) {
+        x0 = min(x0, px[j]); x1 = max(x1, px[j]);
+        y0 = min(y0, py[j]); y1 = max(y1, py[j]);
+      }
+      sx[j] = (double)px[j] + 0.5;  // _kernels.py:43-45
+      sy[j] = (double)py[j] + 0.5;
+      T[j] = 1.0;
+      cr[j] = cg[j] = cb[j] = 0.f;
+      cnt[j] = 0;
+      last[j] = s0;
+      done[j] = !valid[j];
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       x0 = min(x0, __shfl_xor_sync(0xffffffffu, x0, o));
@@ -80,15 +112,9 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
       y1 = max(y1, __shfl_xor_sync(0xffffffffu, y1, o));
     }
     if (x0 > x1) continue;  // no pixel of this box in the image (warp-uniform)
-    const double sx = (double)px + 0.5, sy = (double)py + 0.5;  // _kernels.py:43-45
-    double T = 1.0;
-    float cr = 0.f, cg = 0.f, cb = 0.f;  // colour accumulates in float32 (SURVEY.md H2 recipe m3)
-    int cnt = 0;
-    int64_t last = s0;
-    bool done = !valid;
 
-    // one staged round: evaluate its hits (slots 0..popc-1) for this lane's pixel
-    // (the quadratic form is computed by terminated lanes too: a branch around
+    // one staged round: evaluate its hits (slots 0..popc-1) for this lane's pixels
+    // (the quadratic form is computed by terminated pixels too: a branch around
     // it costs more issue slots than the idle lanes' share of the DP pipe)
     auto eval_round = [&](const HotRec* buf, uint32_t mask, int64_t k0) {
       int slot = 0;
@@ -97,27 +123,41 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
         const int src = __ffs(mask) - 1;
         mask &= mask - 1;
         const HotRec& h = buf[slot++];
-        evals += done ? 0u : 1u;
-        const double dx = dsub(sx, h.mx);
-        const double dy = dsub(sy, h.my);
-        // -0.5 * (c0*dx*dx + c2*dy*dy) - c1*dx*dy   (_kernels.py:54-57)
-        const double power = dsub(dmul(-0.5, dadd(dmul(dmul(h.c0, dx), dx), dmul(dmul(h.c2, dy), dy))),
-                                  dmul(dmul(h.c1, dx), dy));
-        const bool pass = !done && power >= h.lthr;  // else alpha < alpha_floor guaranteed
-        if (DIAG && !__any_sync(0xffffffffu, pass)) ++whits_empty;
-        if (!pass) continue;
-        double alpha = dmul(h.opacity, exp_le0(power, s_exp, ec));  // _kernels.py:58
-        if (alpha > 0.99) alpha = 0.99;              // _kernels.py:59-60
-        if (alpha < bp.alpha_floor) continue;        // _kernels.py:61-62
-        const double nt = dmul(T, dsub(1.0, alpha));
-        if (nt < bp.t_floor) { done = true; continue; }  // _kernels.py:63-66
-        const float w = (float)dmul(T, alpha);
-        cr = fmaf(w, h.r, cr);
-        cg = fmaf(w, h.g, cg);
-        cb = fmaf(w, h.b, cb);
-        T = nt;
-        cnt += 1;
-        last = k0 + src + 1;
+        const double mx = h.mx, my = h.my, c0 = h.c0, c1 = h.c1, c2 = h.c2, lthr = h.lthr;
+        double power[PX];
+        bool pass[PX];
+#pragma unroll
+        for (int j = 0; j < PX; ++j) {
+          evals += done[j] ? 0u : 1u;
+          const double dx = dsub(sx[j], mx);
+          const double dy = dsub(sy[j], my);
+          // -0.5 * (c0*dx*dx + c2*dy*dy) - c1*dx*dy   (_kernels.py:54-57)
+          power[j] = dsub(dmul(-0.5, dadd(dmul(dmul(c0, dx), dx), dmul(dmul(c2, dy), dy))),
+                          dmul(dmul(c1, dx), dy));
+          pass[j] = !done[j] && power[j] >= lthr;  // else alpha < alpha_floor guaranteed
+        }
+        if (DIAG) {
+          bool any = false;
+#pragma unroll
+          for (int j = 0; j < PX; ++j) any |= pass[j];
+          if (!__any_sync(0xffffffffu, any)) ++whits_empty;
+        }
+#pragma unroll
+        for (int j = 0; j < PX; ++j) {
+          if (!pass[j]) continue;
+          double alpha = dmul(h.opacity, exp_le0(power[j], s_exp, ec));  // _kernels.py:58
+          if (alpha > 0.99) alpha = 0.99;              // _kernels.py:59-60
+          if (alpha < bp.alpha_floor) continue;        // _kernels.py:61-62
+          const double nt = dmul(T[j], dsub(1.0, alpha));
+          if (nt < bp.t_floor) { done[j] = true; continue; }  // _kernels.py:63-66
+          const float w = (float)dmul(T[j], alpha);
+          cr[j] = fmaf(w, h.r, cr[j]);
+          cg[j] = fmaf(w, h.g, cg[j]);
+          cb[j] = fmaf(w, h.b, cb[j]);
+          T[j] = nt;
+          cnt[j] += 1;
+          last[j] = k0 + src + 1;
+        }
       }
     };
 
@@ -129,7 +169,13 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
       nby = __ldg(bys + s0 + lane);
     }
     uint32_t pmask = 0;
-    uint32_t live = __ballot_sync(0xffffffffu, !done);
+    bool live_lane = false;
+#pragma unroll
+    for (int j = 0; j < PX; ++j) live_lane |= !done[j];
+    uint32_t live = __ballot_sync(0xffffffffu, live_lane);
+    uint32_t live_px = 0;  // per-lane bitmask of live pixels (box recomputed when it changes)
+#pragma unroll
+    for (int j = 0; j < PX; ++j) live_px |= (done[j] ? 0u : 1u) << j;
     int64_t pk0 = 0;
     int stage = 0;
     bool alldone = false;
@@ -159,14 +205,23 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
         __syncwarp();
         eval_round(wbuf[stage ^ 1], pmask, pk0);
         __syncwarp();
-        const uint32_t live_now = __ballot_sync(0xffffffffu, !done);
+        uint32_t lp = 0;
+#pragma unroll
+        for (int j = 0; j < PX; ++j) lp |= (done[j] ? 0u : 1u) << j;
+        const uint32_t live_now = __ballot_sync(0xffffffffu, lp != 0);
         if (!live_now) { alldone = true; break; }
-        if (live_now != live) {
+        if (__any_sync(0xffffffffu, lp != live_px)) {
           // shrink the warp's cull box to its still-live pixels: a splat that
           // only meets terminated pixels is no longer staged or evaluated
+          live_px = lp;
           live = live_now;
-          x0 = !done ? px : 1 << 20; x1 = !done ? px : -(1 << 20);
-          y0 = !done ? py : 1 << 20; y1 = !done ? py : -(1 << 20);
+          x0 = 1 << 20; x1 = -(1 << 20); y0 = 1 << 20; y1 = -(1 << 20);
+#pragma unroll
+          for (int j = 0; j < PX; ++j)
+            if (!done[j]) {
+              x0 = min(x0, px[j]); x1 = max(x1, px[j]);
+              y0 = min(y0, py[j]); y1 = max(y1, py[j]);
+            }
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) {
             x0 = min(x0, __shfl_xor_sync(0xffffffffu, x0, o));
@@ -180,13 +235,19 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
       pk0 = k0;
       stage ^= 1;
     }
+    (void)live;
     cp_async_wait<0>();
     __syncwarp();
     if (pmask && !alldone) eval_round(wbuf[stage ^ 1], pmask, pk0);
     __syncwarp();
-    if (valid) {
-      const int64_t pix = (int64_t)py * bp.width + px;
-      double o[3] = {(double)cr + T * bp.bg[0], (double)cg + T * bp.bg[1], (double)cb + T * bp.bg[2]};
+    int box_cnt = 0;
+#pragma unroll
+    for (int j = 0; j < PX; ++j) {
+      if (!valid[j]) continue;
+      box_cnt += cnt[j];
+      const int64_t pix = (int64_t)py[j] * bp.width + px[j];
+      double o[3] = {(double)cr[j] + T[j] * bp.bg[0], (double)cg[j] + T[j] * bp.bg[1],
+                     (double)cb[j] + T[j] * bp.bg[2]};
       if (!(bp.flags & CS_RENDER_NO_CLIP)) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) o[c] = o[c] < 0.0 ? 0.0 : (o[c] > 1.0 ? 1.0 : o[c]);
@@ -195,14 +256,14 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
       out[3 * pix + 1] = (OutT)o[1];
       out[3 * pix + 2] = (OutT)o[2];
       if (KEEP) {
-        state.final_t[pix] = T;
-        state.last[pix] = (int32_t)last;
-        state.color_acc[3 * pix] = (double)cr;
-        state.color_acc[3 * pix + 1] = (double)cg;
-        state.color_acc[3 * pix + 2] = (double)cb;
+        state.final_t[pix] = T[j];
+        state.last[pix] = (int32_t)last[j];
+        state.color_acc[3 * pix] = (double)cr[j];
+        state.color_acc[3 * pix + 1] = (double)cg[j];
+        state.color_acc[3 * pix + 2] = (double)cb[j];
       }
     }
-    const int box_frags = warp_sum(valid ? cnt : 0);
+    const int box_frags = warp_sum(box_cnt);
     frags += box_frags;
     if (lane == 0 && box_frags) atomicAdd(frag_tile + t, box_frags);
   }
@@ -216,17 +277,22 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
   }
 }
 
+#ifndef CS_BLEND_PX
+#define CS_BLEND_PX 1
+#endif
+
 template <typename OutT, bool KEEP, bool DIAG>
 static void launch_blend_d(int n_tiles, const uint32_t* list, const uint32_t* bxs,
                            const uint32_t* bys, const uint2* ranges, const HotRec* hot,
                            const uint32_t* order, const BlendParams& bp, OutT* out,
                            int32_t* frag_tile, DevStats* stats, BlendState st, cudaStream_t s) {
+  constexpr int PX = CS_BLEND_PX;
   static int grid = 0;  // persistent: one wave of resident CTAs
-  if (grid == 0) grid = persistent_grid(k_blend<OutT, KEEP, DIAG>, kBlendThreads);
-  const int nboxes = boxes_per_tile(bp.tile_size);
-  k_blend<OutT, KEEP, DIAG><<<grid, kBlendThreads, 0, s>>>(list, bxs, bys, ranges, hot, order,
-                                                           n_tiles * nboxes, nboxes, bp, out,
-                                                           frag_tile, stats, st);
+  if (grid == 0) grid = persistent_grid(k_blend<OutT, KEEP, DIAG, PX>, kBlendThreads);
+  const int nboxes = PX == 1 ? boxes_per_tile(bp.tile_size) : boxes_per_tile2(bp.tile_size);
+  k_blend<OutT, KEEP, DIAG, PX><<<grid, kBlendThreads, 0, s>>>(list, bxs, bys, ranges, hot, order,
+                                                               n_tiles * nboxes, nboxes, bp, out,
+                                                               frag_tile, stats, st);
 }
 
 template <typename OutT, bool KEEP>

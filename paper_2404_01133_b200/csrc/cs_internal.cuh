@@ -154,6 +154,19 @@ __device__ __forceinline__ int box_pixel(int b, int lane, int ts) {
   }
   return b * 32 + lane;
 }
+// Two pixels per lane: 8x8 boxes, lane (x, y) of the upper 8x4 half and
+// (x, y + 4) of the lower; tile sizes that are not multiples of 8 use
+// row-major 64-pixel chunks (pixel j of the lane at 32 j + lane).
+__host__ __device__ __forceinline__ int boxes_per_tile2(int ts) {
+  return (ts & 7) == 0 ? (ts >> 3) * (ts >> 3) : (ts * ts + 63) / 64;
+}
+__device__ __forceinline__ int box_pixel2(int b, int lane, int ts, int j) {
+  if ((ts & 7) == 0) {
+    const int nbx = ts >> 3, bx = b % nbx, by = b / nbx;
+    return (by * 8 + (lane >> 3) + 4 * j) * ts + bx * 8 + (lane & 7);
+  }
+  return b * 64 + 32 * j + lane;
+}
 
 // ---------------------------------------------------------------------------
 // exp(x) for the blend's x = power in [lthr, 0] (lthr >= log(alpha_floor) - 1e-6
