@@ -81,7 +81,7 @@ typedef struct cs_frame_stats {
   int64_t fragments;        /* FrameStats.blended_fragments */
   int32_t n_segments;       /* (level, block) pieces concatenated */
   int32_t status;           /* bit0 pair-buffer overflow, bit1 CS_ERANGE */
-  int64_t evals;            /* blend evaluations E (pixel x splat pairs walked) */
+  int64_t evals;            /* blend evaluations E (pixel x splat pairs walked; CS_RENDER_DIAG only) */
   int64_t warp_hits;        /* blend (8x4 pixel box, splat) pairs evaluated by a warp */
   int64_t warp_hits_empty;  /* ... of which no live pixel passed the alpha-floor test (CS_RENDER_DIAG only) */
 } cs_frame_stats;
@@ -129,7 +129,7 @@ typedef struct cs_source {
 #define CS_RENDER_KEEP_STATE 8u  /* keep per-pixel state for cs_render_backward */
 #define CS_RENDER_PROJECT_ONLY 16u /* stop after projection + depth order (cs_dump_projected) */
 #define CS_RENDER_DEBUG 32u        /* also keep the full projected records (cs_dump_projected) */
-#define CS_RENDER_DIAG 64u         /* also count warp_hits_empty (blend diagnostic, slower) */
+#define CS_RENDER_DIAG 64u         /* also count evals and warp_hits_empty (blend diagnostics, slower) */
 
 /* ---- context ----------------------------------------------------------- */
 int cs_create(int device, cs_ctx** out);

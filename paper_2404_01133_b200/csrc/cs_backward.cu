@@ -63,7 +63,10 @@ __device__ __forceinline__ float warp_transpose_sum9(const float (&in)[kGradFiel
 // `last` of its pixels.  Per evaluated hit each lane re-derives the forward's
 // float64 decisions for its pixel; when any lane contributes, the nine
 // partials are warp-reduced and lane 0 adds them with one atomic each.
-__global__ void __launch_bounds__(kBwdThreads, 3)
+#ifndef CS_BWD_MINB
+#define CS_BWD_MINB 3
+#endif
+__global__ void __launch_bounds__(kBwdThreads, CS_BWD_MINB)
 k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
             const uint32_t* __restrict__ bys, const uint2* __restrict__ ranges,
             const HotRec* __restrict__ hot, const uint32_t* __restrict__ tile_order, int n_items,
@@ -132,14 +135,15 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
         const int src = __ffs(mask) - 1;
         mask &= mask - 1;
         const HotRec& h = buf[slot++];
+        const double mx = h.mx, my = h.my, c0 = h.c0, c1 = h.c1, c2 = h.c2, lthr = h.lthr;
         float gr[kGradFields];
         bool contrib = false;
-        if (k0 + src < my_end) {
-          const double dx = dsub(sx, h.mx), dy = dsub(sy, h.my);
-          const double power =
-              dsub(dmul(-0.5, dadd(dmul(dmul(h.c0, dx), dx), dmul(dmul(h.c2, dy), dy))),
-                   dmul(dmul(h.c1, dx), dy));
-          if (power >= h.lthr) {
+        // the quadratic form for every lane (as in the forward: cheaper than a branch)
+        const double dx = dsub(sx, mx), dy = dsub(sy, my);
+        const double power = dsub(dmul(-0.5, dadd(dmul(dmul(c0, dx), dx), dmul(dmul(c2, dy), dy))),
+                                  dmul(dmul(c1, dx), dy));
+        {
+          if (k0 + src < my_end && power >= lthr) {
             const double G = exp_le0(power, s_exp, ec);
             double alpha = dmul(h.opacity, G);
             const bool clamped = alpha > 0.99;
@@ -161,8 +165,8 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
               const float dl_dpow = clamped ? 0.f : dl_da * a;
               const float fdx = (float)dx, fdy = (float)dy;
               gr[5] = clamped ? 0.f : dl_da * (float)G;
-              gr[0] = dl_dpow * ((float)h.c0 * fdx + (float)h.c1 * fdy);
-              gr[1] = dl_dpow * ((float)h.c2 * fdy + (float)h.c1 * fdx);
+              gr[0] = dl_dpow * ((float)c0 * fdx + (float)c1 * fdy);
+              gr[1] = dl_dpow * ((float)c2 * fdy + (float)c1 * fdx);
               gr[2] = dl_dpow * (-0.5f * fdx * fdx);
               gr[3] = dl_dpow * (-fdx * fdy);
               gr[4] = dl_dpow * (-0.5f * fdy * fdy);

@@ -128,7 +128,7 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
         bool pass[PX];
 #pragma unroll
         for (int j = 0; j < PX; ++j) {
-          evals += done[j] ? 0u : 1u;
+          if (DIAG) evals += done[j] ? 0u : 1u;
           const double dx = dsub(sx[j], mx);
           const double dy = dsub(sy[j], my);
           // -0.5 * (c0*dx*dx + c2*dy*dy) - c1*dx*dy   (_kernels.py:54-57)
