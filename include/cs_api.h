@@ -120,6 +120,11 @@ typedef struct cs_source {
   int32_t force_level; /* -1 = None */
   cs_cloud cloud;      /* CS_SRC_CLOUD */
   const cs_lod* lod;   /* CS_SRC_LOD_* */
+  /* CS_SRC_CLOUD only, optional (NULL): device uint8[cloud.count]; rows with a
+   * nonzero byte are rendered as if absent -- the image of
+   * cloud.take(nonzero(mask == 0)), the "rest" cloud of assign_b1
+   * (partition.py:332-333), without materialising it */
+  const uint8_t* exclude;
 } cs_source;
 
 /* cs_render flags */
@@ -303,6 +308,21 @@ int cs_mad_bounds(cs_ctx* ctx, const cs_cloud* cloud, const int32_t* membership,
  * caller-allocated dst (same fp64 flag; dst->count is ignored, n rows written). */
 int cs_gather_cloud(cs_ctx* ctx, const cs_cloud* src, const int32_t* rows, int64_t n,
                     const cs_cloud* dst, void* stream);
+
+/* ---- training-data assignment (partition.py:172-439) ----
+ * bounds_contain(contract(normalize_position(p)), lo, hi) (partition.py:110-126,
+ * 172-181) for n points (device xyz, fp32 or fp64, stride 3 floats or 4 = the
+ * pos_op quads of a cs_cloud); p_min = p_max = NULL: the points are already
+ * contracted (BlockGrid.contracted).  mask: device uint8[n] or NULL; count:
+ * HOST int64 (synchronises `stream`) or NULL. */
+int cs_bounds_contain(cs_ctx* ctx, int64_t n, const void* positions, int32_t f32, int32_t stride,
+                      const double* p_min, const double* p_max, const double* lo, const double* hi,
+                      uint8_t* mask, int64_t* count, void* stream);
+/* metrics.ssim (metrics.py:70-96) of two device (H, W, 3) float32 images with
+ * the reference's 11x11 window (HOST double[121]).  acc4: device double[4];
+ * acc4[3] receives the SSIM (acc4[0..2] per-channel sums).  Asynchronous. */
+int cs_ssim(cs_ctx* ctx, const float* img_a, const float* img_b, int32_t height, int32_t width,
+            const double* window, double* acc4, void* stream);
 
 #ifdef __cplusplus
 }

@@ -463,3 +463,129 @@ def mad_bounds(positions, n_mad):
             lo[axis] = max(lo[axis], med[axis] - n_mad * mad[axis])
             hi[axis] = min(hi[axis], med[axis] + n_mad * mad[axis])
     return lo, hi
+
+
+# ---------------------------------------------------------------------------
+# training-data assignment (partition.py:172-439, metrics.py:61-101)
+
+def ssim(a, b):
+    """metrics.ssim (metrics.py:70-96), restated with scipy.signal.convolve as the reference."""
+    from scipy.signal import convolve
+    g = np.exp(-((np.arange(11) - 5) ** 2) / (2.0 * 1.5 ** 2))
+    w = np.outer(g, g)
+    w = w / w.sum()
+    pa, pb = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    vals = []
+    for ch in range(3):
+        x, y = pa[:, :, ch], pb[:, :, ch]
+        mu_x = convolve(x, w, mode="valid")
+        mu_y = convolve(y, w, mode="valid")
+        e_xx = convolve(x * x, w, mode="valid")
+        e_yy = convolve(y * y, w, mode="valid")
+        e_xy = convolve(x * y, w, mode="valid")
+        var_x = e_xx - mu_x ** 2
+        var_y = e_yy - mu_y ** 2
+        cov = e_xy - mu_x * mu_y
+        num = (2 * mu_x * mu_y + 0.01 ** 2) * (2 * cov + 0.03 ** 2)
+        den = (mu_x ** 2 + mu_y ** 2 + 0.01 ** 2) * (var_x + var_y + 0.03 ** 2)
+        vals.append(np.mean(num / den))
+    return float(np.mean(vals))
+
+
+def bounds_contain(points, bounds_min, bounds_max):
+    """partition.bounds_contain (partition.py:172-181)."""
+    p = np.asarray(points, dtype=np.float64).reshape(-1, 3)
+    lo = np.asarray(bounds_min, dtype=np.float64)
+    hi = np.asarray(bounds_max, dtype=np.float64)
+    below = np.where(hi == 2.0, p <= hi, p < hi)
+    return ((p >= lo) & below).all(axis=1)
+
+
+def contract_normalized(p, p_min, p_max):
+    """contract(normalize_position(p)) (partition.py:110-126)."""
+    p = np.asarray(p, dtype=np.float64)
+    ph = 2.0 * (p - np.asarray(p_min)) / (np.asarray(p_max) - np.asarray(p_min)) - 1.0
+    m = np.abs(ph).max(axis=-1, keepdims=True)
+    safe = np.maximum(m, 1.0)
+    return np.where(m <= 1.0, ph, (2.0 - 1.0 / safe) * ph / safe)
+
+
+def enlarge_bounds(j, bounds_min, bounds_max, contracted, min_count, factor=1.2):
+    """partition.enlarge_bounds (partition.py:234-259)."""
+    lo = np.asarray(bounds_min[j], dtype=np.float64).copy()
+    hi = np.asarray(bounds_max[j], dtype=np.float64).copy()
+    if contracted.shape[0] < min_count:
+        return np.full(3, -2.0), np.full(3, 2.0)
+    while bounds_contain(contracted, lo, hi).sum() < min_count:
+        if (lo == -2.0).all() and (hi == 2.0).all():
+            break
+        center = 0.5 * (lo + hi)
+        half = 0.5 * (hi - lo) * factor
+        lo = np.maximum(center - half, -2.0)
+        hi = np.minimum(center + half, 2.0)
+    return lo, hi
+
+
+def scaled_camera(cam, scale):
+    """partition._scaled_camera (partition.py:300-310) as a plain namespace."""
+    from types import SimpleNamespace
+    if scale == 1.0:
+        return cam
+    return SimpleNamespace(width=max(1, int(round(cam.width * scale))),
+                           height=max(1, int(round(cam.height * scale))),
+                           fx=cam.fx * scale, fy=cam.fy * scale, cx=cam.cx * scale, cy=cam.cy * scale,
+                           rotation_w2c=cam.rotation_w2c, translation_w2c=cam.translation_w2c,
+                           camera_center=cam.camera_center)
+
+
+def take(cloud, idx):
+    return Arrays(np.asarray(cloud.positions)[idx], np.asarray(cloud.opacities)[idx],
+                  np.asarray(cloud.scales)[idx], np.asarray(cloud.rotations)[idx],
+                  np.asarray(cloud.sh)[idx])
+
+
+def assign(views, grid, cloud, epsilon, settings=None, assignment_scale=0.25, enlarge_min_count=25_000):
+    """partition.assign (partition.py:348-439) -> (entries, provenance, bmin_used, bmax_used, l_ssim)."""
+    settings = settings or DefaultSettings()
+    J = np.asarray(grid.bounds_min).shape[0]
+    P = len(views)
+    entries = np.zeros((P, J), dtype=bool)
+    prov = np.full((P, J), "", dtype="<U5")
+    bmin = np.asarray(grid.bounds_min, dtype=np.float64).copy()
+    bmax = np.asarray(grid.bounds_max, dtype=np.float64).copy()
+    scaled = [scaled_camera(v, assignment_scale) for v in views]
+    fulls = [rasterize_stats(cloud, s, settings)[0] for s in scaled]
+    centers = contract_normalized(np.stack([np.asarray(v.camera_center, dtype=np.float64) for v in views]),
+                                  grid.map.p_min, grid.map.p_max)
+    lmat = np.full((P, J), np.nan)
+
+    def evaluate(j, rest, lo, hi, record):
+        b2 = bounds_contain(centers, lo, hi)
+        for i in range(P):
+            b1 = False
+            if rest is not None:
+                l = 1.0 - ssim(fulls[i], rasterize_stats(rest, scaled[i], settings)[0])
+                if record:
+                    lmat[i, j] = l
+                b1 = l > epsilon
+            if b1 or b2[i]:
+                entries[i, j] = True
+                prov[i, j] = "B1+B2" if (b1 and b2[i]) else ("B1" if b1 else "B2")
+            else:
+                entries[i, j] = False
+                prov[i, j] = ""
+
+    mem = np.asarray(grid.membership)
+    for j in range(J):
+        rest = take(cloud, np.nonzero(mem != j)[0]) if np.asarray(grid.counts)[j] > 0 else None
+        evaluate(j, rest, grid.bounds_min[j], grid.bounds_max[j], True)
+    for j in range(J):
+        if entries[:, j].any():
+            continue
+        lo, hi = enlarge_bounds(j, grid.bounds_min, grid.bounds_max, np.asarray(grid.contracted),
+                                enlarge_min_count)
+        bmin[j], bmax[j] = lo, hi
+        m = bounds_contain(grid.contracted, lo, hi)
+        rest = take(cloud, np.nonzero(~m)[0]) if m.any() else None
+        evaluate(j, rest, lo, hi, False)
+    return entries, prov, bmin, bmax, lmat

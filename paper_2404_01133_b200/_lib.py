@@ -74,7 +74,7 @@ class CsAdamHparams(ctypes.Structure):
 
 
 class CsSource(ctypes.Structure):
-    _fields_ = [("kind", i32), ("force_level", i32), ("cloud", CsCloud), ("lod", vp)]
+    _fields_ = [("kind", i32), ("force_level", i32), ("cloud", CsCloud), ("lod", vp), ("exclude", vp)]
 
 
 _SIGS = {
@@ -116,6 +116,8 @@ _SIGS = {
     "cs_lod_rows": (ctypes.c_int, [vp, i64, vp, vp, i32, vp, i32, vp, vp, vp]),
     "cs_mad_bounds": (ctypes.c_int, [vp, ctypes.POINTER(CsCloud), vp, i32, ctypes.c_double, vp, vp, vp]),
     "cs_gather_cloud": (ctypes.c_int, [vp, ctypes.POINTER(CsCloud), vp, i64, ctypes.POINTER(CsCloud), vp]),
+    "cs_bounds_contain": (ctypes.c_int, [vp, i64, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp]),
+    "cs_ssim": (ctypes.c_int, [vp, vp, vp, i32, i32, vp, vp, vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -120,6 +120,11 @@ cudaError_t mad_bounds_run(const cs_cloud& cl, const int32_t* membership, int n_
                            cudaStream_t s);
 void launch_gather_cloud(const cs_cloud& src, const int32_t* rows, int64_t n, const cs_cloud& dst,
                          cudaStream_t s);
+void launch_bounds_contain(int64_t n, const void* pos, int f32, int stride, const double* pmin,
+                           const double* pmax, const double* lo, const double* hi, uint8_t* mask,
+                           unsigned long long* count, cudaStream_t s);
+cudaError_t ssim_run(const float* a, const float* b, int H, int W, const double* window,
+                     double* acc4, cudaStream_t s);
 }  // namespace cs
 
 using namespace cs;
@@ -418,6 +423,7 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
     cap_vis = cl.count;
   } else {
     if (!L) return fail(CS_EINVAL, "LoD source without scene");
+    if (src->exclude) return fail(CS_EINVAL, "exclude masks apply to single-cloud sources only");
     n_segs = L->n_levels * L->n_blocks;
     n_blocks = L->n_blocks;
     if (src->kind == CS_SRC_LOD_BLOCK) {
@@ -463,7 +469,8 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
   ProjOutputs po{c->keysA.as<uint64_t>(), c->k32A.as<uint32_t>(), c->valsA.as<uint32_t>(),
                  c->hot.as<HotRec>(),
                  c->rects.as<int4>(), c->boxes.as<short4>(),
-                 debug ? c->recs.as<ProjRec>() : nullptr};
+                 debug ? c->recs.as<ProjRec>() : nullptr,
+                 src->kind == CS_SRC_CLOUD ? src->exclude : nullptr};
   launch_project(clouds, c->segs.as<Seg>(), stats, *cam, *st, cap, po, list, s);
   c->last_debug = debug;
   CS_CHECK_LAUNCH();
@@ -1066,6 +1073,39 @@ int cs_gather_cloud(cs_ctx* c, const cs_cloud* src, const int32_t* rows, int64_t
   CS_CUDA(cudaSetDevice(c->device));
   launch_gather_cloud(*src, rows, n, *dst, (cudaStream_t)stream);
   CS_CHECK_LAUNCH();
+  return CS_OK;
+}
+
+// ---- training-data assignment (partition.py:172-439) -------------------------
+
+int cs_bounds_contain(cs_ctx* c, int64_t n, const void* positions, int32_t f32, int32_t stride,
+                      const double* p_min, const double* p_max, const double* lo, const double* hi,
+                      uint8_t* mask, int64_t* count, void* stream) {
+  if (!c || n < 0 || !lo || !hi || (stride != 3 && stride != 4) || (n > 0 && !positions) ||
+      (!p_min) != (!p_max))
+    return fail(CS_EINVAL, "bad argument");
+  CS_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  std::lock_guard<std::mutex> lock(c->mu);
+  if (c->scratch4.ensure(sizeof(unsigned long long))) return fail(CS_ENOMEM, "count");
+  launch_bounds_contain(n, positions, f32, stride, p_min, p_max, lo, hi, mask,
+                        c->scratch4.as<unsigned long long>(), s);
+  CS_CHECK_LAUNCH();
+  if (count) {
+    unsigned long long h = 0;
+    CS_CUDA(cudaMemcpyAsync(&h, c->scratch4.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CS_CUDA(cudaStreamSynchronize(s));
+    *count = (int64_t)h;
+  }
+  return CS_OK;
+}
+
+int cs_ssim(cs_ctx* c, const float* img_a, const float* img_b, int32_t height, int32_t width,
+            const double* window, double* acc4, void* stream) {
+  if (!c || !img_a || !img_b || !window || !acc4) return fail(CS_EINVAL, "NULL argument");
+  if (height < 11 || width < 11) return fail(CS_EINVAL, "images must be at least 11x11 for ssim");
+  CS_CUDA(cudaSetDevice(c->device));
+  CS_CUDA(ssim_run(img_a, img_b, height, width, window, acc4, (cudaStream_t)stream));
   return CS_OK;
 }
 

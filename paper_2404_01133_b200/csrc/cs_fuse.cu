@@ -15,7 +15,9 @@ struct FuseMap {
   int nx, ny, nz;
 };
 
-__device__ __forceinline__ int block_of(double x, double y, double z, const FuseMap& m) {
+// contract(normalize_position(p)) (partition.py:110-126), numpy op order
+__device__ __forceinline__ void contract_point(double x, double y, double z, const FuseMap& m,
+                                               double c[3]) {
   double p[3] = {x, y, z};
   double ph[3];
 #pragma unroll
@@ -23,29 +25,60 @@ __device__ __forceinline__ int block_of(double x, double y, double z, const Fuse
     ph[a] = dsub(ddiv(dmul(2.0, dsub(p[a], m.pmin[a])), dsub(m.pmax[a], m.pmin[a])), 1.0);
   const double mx = fmax(fmax(fabs(ph[0]), fabs(ph[1])), fabs(ph[2]));
   const double safe = fmax(mx, 1.0);
+#pragma unroll
+  for (int a = 0; a < 3; ++a)  // identity inside the unit cube, (2 - 1/m) * p / m outside
+    c[a] = mx <= 1.0 ? ph[a] : ddiv(dmul(dsub(2.0, ddiv(1.0, safe)), ph[a]), safe);
+}
+
+__device__ __forceinline__ int block_of(double x, double y, double z, const FuseMap& m) {
+  double c[3];
+  contract_point(x, y, z, m, c);
   const int dims[3] = {m.nx, m.ny, m.nz};
   int64_t ib[3];
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    // contract: identity inside the unit cube, (2 - 1/m) * p / m outside
-    const double c = mx <= 1.0 ? ph[a] : ddiv(dmul(dsub(2.0, ddiv(1.0, safe)), ph[a]), safe);
-    // _bin: floor((c + 2) / 4 * n), astype(int64), clip
-    ib[a] = clip_i64(np_to_i64(floor(dmul(ddiv(dadd(c, 2.0), 4.0), (double)dims[a]))), 0,
+  for (int a = 0; a < 3; ++a)  // _bin: floor((c + 2) / 4 * n), astype(int64), clip
+    ib[a] = clip_i64(np_to_i64(floor(dmul(ddiv(dadd(c[a], 2.0), 4.0), (double)dims[a]))), 0,
                      dims[a] - 1);
-  }
   if (m.nz <= 1) ib[2] = 0;
   return (int)(ib[0] + (int64_t)m.nx * (ib[1] + (int64_t)m.ny * ib[2]));
 }
 
 __device__ __forceinline__ void load_xyz(const void* pos, int f32, int64_t k, double& x, double& y,
-                                         double& z) {
+                                         double& z, int stride = 3) {
   if (f32) {
-    const float* p = reinterpret_cast<const float*>(pos) + 3 * k;
+    const float* p = reinterpret_cast<const float*>(pos) + stride * k;
     x = p[0]; y = p[1]; z = p[2];
   } else {
-    const double* p = reinterpret_cast<const double*>(pos) + 3 * k;
+    const double* p = reinterpret_cast<const double*>(pos) + stride * k;
     x = p[0]; y = p[1]; z = p[2];
   }
+}
+
+// bounds_contain(contract(normalize_position(p)), lo, hi) (partition.py:172-181):
+// lower-inclusive, upper-exclusive, an upper bound on the cube surface (== 2)
+// inclusive.  mask (optional) per point; count of contained points.
+__global__ void k_bounds_contain(int64_t n, const void* pos, int f32, int stride, FuseMap m,
+                                 double lo0, double lo1, double lo2, double hi0, double hi1,
+                                 double hi2, uint8_t* mask, unsigned long long* count) {
+  const double lo[3] = {lo0, lo1, lo2}, hi[3] = {hi0, hi1, hi2};
+  unsigned long long local = 0;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += gstride) {
+    double x, y, z, c[3];
+    load_xyz(pos, f32, k, x, y, z, stride);
+    if (m.nx) {
+      contract_point(x, y, z, m, c);
+    } else {  // points already contracted
+      c[0] = x; c[1] = y; c[2] = z;
+    }
+    bool in = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) in = in && c[a] >= lo[a] && (hi[a] == 2.0 ? c[a] <= hi[a] : c[a] < hi[a]);
+    if (mask) mask[k] = in ? 1 : 0;
+    local += in ? 1ull : 0ull;
+  }
+  local = warp_sum(local);
+  if (lane_id() == 0 && local) atomicAdd(count, local);
 }
 
 __global__ void k_block_of_points(int64_t n, const void* pos, int f32, FuseMap m, int32_t* out) {
@@ -96,6 +129,18 @@ void launch_block_of_points(int64_t n, const void* pos, int f32, const double* p
   for (int a = 0; a < 3; ++a) { m.pmin[a] = pmin[a]; m.pmax[a] = pmax[a]; }
   m.nx = nx; m.ny = ny; m.nz = nz;
   if (n > 0) k_block_of_points<<<148 * 8, 256, 0, s>>>(n, pos, f32, m, out);
+}
+
+void launch_bounds_contain(int64_t n, const void* pos, int f32, int stride, const double* pmin,
+                           const double* pmax, const double* lo, const double* hi, uint8_t* mask,
+                           unsigned long long* count, cudaStream_t s) {
+  FuseMap m;
+  for (int a = 0; a < 3; ++a) { m.pmin[a] = pmin ? pmin[a] : 0.0; m.pmax[a] = pmax ? pmax[a] : 1.0; }
+  m.nx = m.ny = m.nz = pmin ? 1 : 0;  // 0: the points are contracted already
+  cudaMemsetAsync(count, 0, sizeof(unsigned long long), s);
+  if (n > 0)
+    k_bounds_contain<<<148 * 8, 256, 0, s>>>(n, pos, f32, stride, m, lo[0], lo[1], lo[2], hi[0], hi[1],
+                                             hi[2], mask, count);
 }
 
 void launch_fuse_filter(int64_t n, const void* pos, int f32, const double* pmin, const double* pmax,

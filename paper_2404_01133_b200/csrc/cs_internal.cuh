@@ -91,6 +91,7 @@ struct ProjOutputs {
   int4* rects;
   short4* boxes;     // copy of HotRec's cull box, dense (8 B)
   ProjRec* recs;     // optional (debug / dumps)
+  const uint8_t* exclude;  // input, optional: rows culled as if absent (assignment renders)
 };
 
 // LoD scene tables on device (cs_lod.cu)

@@ -307,6 +307,10 @@ k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
     }
     g = load_geom(clouds[cloud_id], local);
     po = project_one(g, cam, st);
+    // a row of the "rest" cloud of assign_b1 (partition.py:332-333): rendering
+    // the full cloud with the excluded rows culled equals rendering
+    // cloud.take(~mask) -- the kept rows keep their relative (index) order
+    if (po_out.exclude && po_out.exclude[i]) po.in_front = po.ok = po.keep = false;
   }
   // skipped_singular: in front but det <= 1e-12 (render.py:146-148)
   const uint32_t kb = __ballot_sync(0xffffffffu, po.keep);

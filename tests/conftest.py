@@ -113,3 +113,22 @@ def lodgen_inputs(g):
                             sh=rng.normal(0.0, 0.2, (k, 3, 16)).astype(np.float32), count=k)
     cams = [g.camera(f"cam{i:02d}") for i in range(int(g["n_cams"]))]
     return cloud, cams, g["membership"], int(g["n_blocks"])
+
+
+@pytest.fixture(scope="session")
+def golden_assign():
+    return Golden("assign.npz")
+
+
+def assign_inputs(g):
+    """(cloud, views, grid, settings) of tests/golden/assign.npz (duck-typed)."""
+    cloud = SimpleNamespace(positions=g["positions"], opacities=g["opacities"], scales=g["scales"],
+                            rotations=g["rotations"], sh=g["sh"], count=int(g["positions"].shape[0]))
+    views = [g.camera(f"pose{i:02d}") for i in range(int(g["n_poses"]))]
+    grid = SimpleNamespace(map=SimpleNamespace(p_min=g["p_min"], p_max=g["p_max"]),
+                           dims=tuple(int(d) for d in g["dims"]), bounds_min=g["bounds_min"],
+                           bounds_max=g["bounds_max"], membership=g["membership"], counts=g["counts"],
+                           contracted=g["contracted"], n_blocks=int(g["bounds_min"].shape[0]))
+    settings = SimpleNamespace(background=(0.0, 0.0, 0.0), sh_degree=3, tile_size=16,
+                               alpha_floor=1.0 / 255.0, transmittance_floor=1e-4, near_plane=0.2)
+    return cloud, views, grid, settings

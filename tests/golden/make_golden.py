@@ -15,6 +15,10 @@ the reference's own outputs of the hot-path functions:
                assemble_render_set (block, forced, pointwise) and the render of
                the assembled cloud, for several cameras
   fuse.npz     partition.fuse (partition.py:570-587) of perturbed block clouds
+  assign.npz   training-data assignment (partition.assign, partition.py:348-439)
+               with the per-(pose, block) l_ssim of the contribution test
+               (partition.py:318-334, metrics.py:70-101); a 5x5 grid with
+               sparse / unassigned blocks (enlarged-bounds retry)
   lodgen.npz   LoD generation: significance_scores
                (lod.py:54-101), the stable priority order (lod.py:114-116),
                build_lod's per-level / per-block kept rows (lod.py:211-248) and
@@ -45,7 +49,10 @@ from citysplat.config import RunConfig  # noqa: E402
 from citysplat.core import CameraView, Gaussian, GaussianCloud, SH_C0  # noqa: E402
 from citysplat.lod import (_keep_count, _priority, assemble_render_set, build_lod,  # noqa: E402
                            decide_visibility, mad_bounds, significance_scores)
-from citysplat.partition import ContractionMap, fuse, grid_partition  # noqa: E402
+from citysplat.metrics import l_ssim  # noqa: E402
+from citysplat.partition import (ContractionMap, _scaled_camera, assign, fuse,  # noqa: E402
+                                 grid_partition)
+from citysplat.render import rasterize  # noqa: E402
 from citysplat.render import RenderSettings, _bin_tiles, _project_cloud, rasterize_stats  # noqa: E402
 from citysplat.synthetic import generate_synthetic_city, look_at  # noqa: E402
 from conftest import cloud_in_view, identity_camera, random_camera  # noqa: E402
@@ -229,6 +236,59 @@ def make_fuse():
     print("fuse.npz", fused.count, "fused of", sum(b.count for b, _ in blocks))
 
 
+def make_assign():
+    bundle = generate_synthetic_city(seed=21, extent=80.0, n_buildings=12, n_cameras=12,
+                                     target_gaussians=6000, image_size=(160, 120))
+    cloud = quantize(bundle.cloud)
+    # foreground box over the x-y centre third; a 5x5 grid leaves corner
+    # blocks empty or sparse so the enlarged-bounds retry runs
+    cmap = ContractionMap.central_third(cloud)
+    grid = grid_partition(cloud, cmap, (5, 5))
+    poses = bundle.train_cameras()
+    scale = 0.5
+    settings = RenderSettings()
+    views = [p.view for p in poses]
+    scaled = [_scaled_camera(v, scale) for v in views]
+    P, J = len(poses), grid.n_blocks
+    l = np.full((P, J), np.nan)
+    fulls = [rasterize(cloud, s, settings) for s in scaled]
+    for j in range(J):
+        if grid.counts[j] == 0:
+            continue
+        rest = cloud.take(np.nonzero(grid.membership != j)[0])
+        for i in range(P):
+            l[i, j] = l_ssim(fulls[i], rasterize(rest, scaled[i], settings))
+    # epsilon in the widest gap of the middle half of the finite values: no
+    # decision sits on a knife edge
+    v = np.sort(l[np.isfinite(l)])
+    lo_i, hi_i = len(v) // 4, 3 * len(v) // 4
+    gaps = np.diff(v[lo_i:hi_i + 1])
+    g = int(np.argmax(gaps))
+    eps = float(0.5 * (v[lo_i + g] + v[lo_i + g + 1]))
+    min_count = 900
+    res = assign(poses, grid, cloud, eps, settings=settings, assignment_scale=scale,
+                 enlarge_min_count=min_count)
+    store = dict(positions=cloud.positions.astype(np.float32), opacities=cloud.opacities.astype(np.float32),
+                 scales=cloud.scales.astype(np.float32), rotations=cloud.rotations.astype(np.float32),
+                 sh=cloud.sh.astype(np.float32), membership=grid.membership, counts=grid.counts,
+                 contracted=grid.contracted, bounds_min=grid.bounds_min, bounds_max=grid.bounds_max,
+                 p_min=cmap.p_min, p_max=cmap.p_max, dims=np.array(grid.dims),
+                 epsilon=np.float64(eps), scale=np.float64(scale), min_count=np.int64(min_count),
+                 l_ssim=l, entries=res.entries, provenance=res.provenance.astype("U5"),
+                 bounds_min_used=res.bounds_min_used, bounds_max_used=res.bounds_max_used,
+                 image_ids=np.array(res.image_ids), n_poses=np.int64(P))
+    assert np.array_equal(store["positions"].astype(np.float64), cloud.positions)
+    assert np.array_equal(store["sh"].astype(np.float64), cloud.sh)
+    for i, vw in enumerate(views):
+        put(store, f"pose{i:02d}", cam_dict(vw))
+    np.savez_compressed(OUT / "assign.npz", **store)
+    enlarged = int((~np.all(res.bounds_min_used == grid.bounds_min, axis=1)).sum())
+    print("assign.npz", P, "poses", J, "blocks; counts", grid.counts.tolist(), "eps", eps,
+          "gap", float(gaps[g]), "B1", int((res.provenance == "B1").sum()),
+          "B2", int((res.provenance == "B2").sum()), "B1+B2", int((res.provenance == "B1+B2").sum()),
+          "enlarged", enlarged)
+
+
 def make_lodgen():
     bundle = generate_synthetic_city(seed=11, extent=120.0, n_buildings=30, n_cameras=24,
                                      target_gaussians=20_000, image_size=(320, 240))
@@ -283,5 +343,6 @@ if __name__ == "__main__":
     make_city()
     make_fuse()
     make_lodgen()
+    make_assign()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size // 1024, "KiB")
