@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-train", action="store_true", help="skip the block-training leg (C4)")
+    ap.add_argument("--no-assign", action="store_true", help="skip the data-assignment leg (f2)")
+    ap.add_argument("--assign-poses", type=int, default=4)
     ap.add_argument("--train-steps", type=int, default=72, help="timed block iterations per rank")
     ap.add_argument("--train-warmup", type=int, default=36)
     ap.add_argument("--train-views", type=int, default=4)
@@ -231,7 +233,7 @@ def main():
     from paper_2404_01133_b200._lib import CsFrameStats, CsSource
 
     scene, center, radius, alts, wh, build_s, raw = build_scene(args.scene, args.seed, dev,
-                                                                keep_raw=not args.no_train)
+                                                                keep_raw=not (args.no_train and args.no_assign))
     cams_all = flythrough(center, radius, alts, wh, args.frames_per_altitude)
     # view split: rank r renders its contiguous share of the flythrough, cycling
     share = [cams_all[i] for i in range(len(cams_all)) if i * world // len(cams_all) == rank] or cams_all
@@ -378,9 +380,15 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(scene, cams_all, settings, n_frames=1)
 
+    assign = None
+    if raw is not None and not args.no_assign and rank == 0:
+        del scene
+        scene = None
+        torch.cuda.empty_cache()
+        assign = assign_leg(args, raw, wh, dev)
     train = None
     if not args.no_train:
-        del scene
+        scene = None
         torch.cuda.empty_cache()
         train = train_leg(args, raw, wh, rank, world, dev)
         raw = None
@@ -405,12 +413,52 @@ def main():
             "e2e": e2e,
             "train": train,
             "lod_build": LOD_BUILD,
+            "assign": assign,
             "gpu_launches": K * launches_per_frame(),
             "clocks": clocks,
         }
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def assign_leg(args, raw, wh, dev):
+    """f2: training-data assignment contribution tests (assign_b1, partition.py:318-334)
+    on the full 23M-Gaussian cloud: per (pose, block) one masked render at the
+    assignment scale (0.25) + SSIM, as partition.assign runs them."""
+    import torch
+    from paper_2404_01133_b200 import device, partition
+    from paper_2404_01133_b200.synth import city_cameras
+    pos, op, sc, q, sh, mem, n_blocks = raw
+    full = device.DeviceCloud.from_torch(pos, op, sc, q, sh)
+    extent = SCENES[args.scene][1]
+    cams = city_cameras(64, extent, wh[0], wh[1], seed=args.seed)
+    poses = [c for i, c in enumerate(cams) if i % 8 != 0][:: max(1, 56 // max(args.assign_poses, 1))]
+    poses = poses[:args.assign_poses]
+    scaled = [partition._scaled_camera(c, 0.25) for c in poses]
+    r = partition._Renderer(full, None)
+    counts = torch.bincount(mem.long(), minlength=n_blocks).cpu().numpy()
+    blocks = [j for j in range(n_blocks) if counts[j] > 0]
+    masks = {j: (mem == j).to(torch.uint8) for j in blocks}
+    acc = torch.zeros((len(poses), n_blocks, 4), dtype=torch.float64, device=dev)
+    fulls = [r(c) for c in scaled]  # warm-up + the full images
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i, c in enumerate(scaled):
+        for j in blocks:
+            partition._ssim_into(fulls[i], r(c, masks[j]), acc[i, j])
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    l = 1.0 - acc[:, blocks, 3].cpu().numpy()
+    del full, masks, fulls
+    torch.cuda.empty_cache()
+    n = len(poses) * len(blocks)
+    return {"metric": "assign_b1 contribution tests/s (f2)", "value": n / dt, "unit": "tests/s",
+            "tests": n, "s": round(dt, 3), "poses": len(poses), "blocks": len(blocks),
+            "resolution": f"{scaled[0].width}x{scaled[0].height}", "gaussians": int(pos.shape[0]),
+            "l_ssim_min_med_max": [float(l.min()), float(np.median(l)), float(l.max())],
+            "what": "masked cs_render (exclude = block j) + cs_ssim per (pose, block), synchronous "
+                    "renders as partition.assign issues them; wall clock after sync"}
 
 
 def train_leg(args, raw, wh, rank, world, dev):
