@@ -74,7 +74,7 @@ def parse():
 # scene
 
 
-def build_scene(name: str, seed: int, dev, keep_raw: bool = False):
+def build_scene(name: str, seed: int, dev, keep_raw: bool = False, build_lod: bool = True):
     import torch
     from paper_2404_01133_b200 import lodgen
     from paper_2404_01133_b200.synth import city_cameras, generate_city_torch, orbit_cameras
@@ -88,10 +88,10 @@ def build_scene(name: str, seed: int, dev, keep_raw: bool = False):
     torch.cuda.synchronize()
     t_lod = time.perf_counter()
     scene = lodgen.build_lod_device(pos, op, sc, q, sh, mem, int(np.prod(dims)), train,
-                                    distance_intervals=ints)
+                                    distance_intervals=ints) if build_lod else None
     torch.cuda.synchronize()
     global LOD_BUILD
-    LOD_BUILD = {"s": round(time.perf_counter() - t_lod, 3), "gaussians": int(pos.shape[0]),
+    LOD_BUILD = None if not build_lod else {"s": round(time.perf_counter() - t_lod, 3), "gaussians": int(pos.shape[0]),
                  "views": len(train), "blocks": int(np.prod(dims)),
                  "what": "significance (K15) + priority sort + level rows + MAD bounds + gather "
                          "(lodgen.build_lod_device, build_lod lod.py:211-248), wall clock after sync"}
@@ -243,8 +243,20 @@ def main():
     from paper_2404_01133_b200 import _lib, device
     from paper_2404_01133_b200._lib import CsFrameStats, CsSource
 
+    # N > 1: rank 0 runs the LoD build, the levels and table reach the other
+    # ranks by NCCL broadcast (fusion.broadcast_device_lod_scene)
     scene, center, radius, alts, wh, build_s, raw = build_scene(args.scene, args.seed, dev,
-                                                                keep_raw=not (args.no_train and args.no_assign))
+                                                                keep_raw=not (args.no_train and args.no_assign),
+                                                                build_lod=(rank == 0))
+    lod_bcast_ms = None
+    if world > 1:
+        from paper_2404_01133_b200 import fusion
+        torch.cuda.synchronize()
+        dist.barrier()
+        tb = time.perf_counter()
+        scene = fusion.broadcast_device_lod_scene(scene if rank == 0 else None, src=0)
+        torch.cuda.synchronize()
+        lod_bcast_ms = 1000.0 * (time.perf_counter() - tb)
     cams_all = flythrough(center, radius, alts, wh, args.frames_per_altitude)
     # view split: rank r renders its contiguous share of the flythrough, cycling
     share = [cams_all[i] for i in range(len(cams_all)) if i * world // len(cams_all) == rank] or cams_all
@@ -426,6 +438,7 @@ def main():
             "e2e": e2e,
             "train": train,
             "lod_build": LOD_BUILD,
+            "lod_broadcast_ms": lod_bcast_ms,
             "assign": assign,
             "gpu_launches": K * launches_per_frame(),
             "clocks": clocks,

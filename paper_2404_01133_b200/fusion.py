@@ -144,3 +144,85 @@ def fuse_all_gather(local_blocks: Dict[int, Tuple[torch.Tensor, ...]], n_blocks:
             view.copy_(kept_rows[j])
         dist.broadcast(view, src=owner[j], group=group)
     return fused
+
+
+# ---------------------------------------------------------------------------
+# LoD table broadcast (SURVEY.md 8e "LoD table"): the source rank's detail
+# levels and table reach every rank through one broadcast per tensor, so a
+# single rank runs the LoD build (lodgen.build_lod_cloud) for the whole box.
+
+_HDR = 4  # n_levels, n_blocks, fp64, reserved
+
+
+def broadcast_lod(levels, table, src: int = 0, group=None, device=None):
+    """Broadcast LoD level tensors and table from ``src``.
+
+    levels: on src, a list of (quads (3, K_L, 4), sh rows (K_L, stride_L),
+    sh_coeffs) per level; table: on src, dict(counts (L, J) int64,
+    bounds_min/bounds_max (J, 3), intervals (L, 2), sh_degrees (L,)).  Other
+    ranks pass None and receive both (tensors on ``device``).
+    """
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    dev = torch.device(device) if device is not None else (
+        levels[0][0].device if levels else torch.device("cpu"))
+    hdr = torch.zeros(_HDR, dtype=torch.int64, device=dev)
+    if rank == src:
+        hdr[0], hdr[1] = len(levels), int(np.asarray(table["counts"]).shape[1])
+        hdr[2] = 1 if levels[0][0].dtype == torch.float64 else 0
+    dist.broadcast(hdr, src=src, group=group)
+    L, J, fp64 = int(hdr[0]), int(hdr[1]), bool(hdr[2])
+    # the table: per level (count, sh_coeffs, stride) + counts, then the float64 part
+    itab = torch.zeros(L * 3 + L * J, dtype=torch.int64, device=dev)
+    ftab = torch.zeros(J * 6 + L * 3, dtype=torch.float64, device=dev)
+    if rank == src:
+        for i, (q, sh, C) in enumerate(levels):
+            itab[3 * i], itab[3 * i + 1], itab[3 * i + 2] = q.shape[1], int(C), sh.shape[1]
+        itab[3 * L:] = torch.as_tensor(np.asarray(table["counts"], dtype=np.int64).reshape(-1))
+        f = np.concatenate([np.asarray(table["bounds_min"], dtype=np.float64).reshape(-1),
+                            np.asarray(table["bounds_max"], dtype=np.float64).reshape(-1),
+                            np.asarray(table["intervals"], dtype=np.float64).reshape(-1),
+                            np.asarray(table["sh_degrees"], dtype=np.float64).reshape(-1)])
+        ftab.copy_(torch.as_tensor(f))
+    dist.broadcast(itab, src=src, group=group)
+    dist.broadcast(ftab, src=src, group=group)
+    it = itab.cpu().numpy()
+    ft = ftab.cpu().numpy()
+    out_levels = []
+    for i in range(L):
+        K, C, stride = int(it[3 * i]), int(it[3 * i + 1]), int(it[3 * i + 2])
+        if rank == src:
+            q, sh = levels[i][0].contiguous(), levels[i][1].contiguous()
+        else:
+            q = torch.empty((3, K, 4), dtype=torch.float64 if fp64 else torch.float32, device=dev)
+            sh = torch.empty((K, stride), dtype=torch.float32, device=dev)
+        if K:
+            dist.broadcast(q, src=src, group=group)
+            dist.broadcast(sh, src=src, group=group)
+        out_levels.append((q, sh, C))
+    out_table = dict(counts=it[3 * L:].reshape(L, J),
+                     bounds_min=ft[:3 * J].reshape(J, 3), bounds_max=ft[3 * J:6 * J].reshape(J, 3),
+                     intervals=ft[6 * J:6 * J + 2 * L].reshape(L, 2),
+                     sh_degrees=ft[6 * J + 2 * L:].astype(np.int64))
+    return out_levels, out_table
+
+
+def broadcast_device_lod_scene(dscene, src: int = 0, group=None):
+    """A DeviceLodScene on every rank from the one built on ``src`` (others pass None)."""
+    import torch.distributed as dist
+    from . import device as _device
+    rank = dist.get_rank(group)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if rank == src:
+        levels = [(torch.stack([lc.pos_op, lc.scale, lc.quat]), lc.sh, lc.sh_coeffs)
+                  for lc in dscene.level_clouds]
+        table = dict(counts=dscene.counts, bounds_min=dscene.bounds_min, bounds_max=dscene.bounds_max,
+                     intervals=np.array(dscene.distance_intervals, dtype=np.float64),
+                     sh_degrees=np.array(dscene.sh_degrees))
+        broadcast_lod(levels, table, src, group, dev)
+        return dscene
+    levels, table = broadcast_lod(None, None, src, group, dev)
+    clouds = [_device.DeviceCloud(q[0], q[1], q[2], sh, C, q.shape[1]) for q, sh, C in levels]
+    return _device.DeviceLodScene.from_device_levels(
+        clouds, table["counts"], table["bounds_min"], table["bounds_max"],
+        [tuple(r) for r in table["intervals"]], tuple(int(d) for d in table["sh_degrees"]), dev.index)

@@ -115,3 +115,74 @@ def test_view_split_covers_flythrough():
             shares = [[i for i in range(n_frames) if i * world // n_frames == r] for r in range(world)]
             assert sorted(sum(shares, [])) == list(range(n_frames))
             assert max(map(len, shares)) - min(map(len, shares)) <= 1
+
+
+def _lod_levels_from_golden():
+    """(levels, table) of the golden 2x2x3 LoD city in the device layout, on CPU."""
+    g = np.load(os.path.join(HERE, "golden", "city.npz"))
+    L, J = int(g["n_levels"]), int(g["n_blocks"])
+    levels, counts = [], np.zeros((L, J), dtype=np.int64)
+    for lvl in range(L):
+        pos, op, sc, rot, sh = [], [], [], [], []
+        for j in range(J):
+            p = f"level{lvl}/block{j}/"
+            pos.append(g[p + "positions"]); op.append(g[p + "opacities"]); sc.append(g[p + "scales"])
+            rot.append(g[p + "rotations"]); sh.append(g[p + "sh"])
+            counts[lvl, j] = g[p + "positions"].shape[0]
+        K = int(counts[lvl].sum())
+        q = np.zeros((3, K, 4), dtype=np.float32)
+        q[0, :, :3] = np.concatenate(pos); q[0, :, 3] = np.concatenate(op)
+        q[1, :, :3] = np.concatenate(sc); q[2] = np.concatenate(rot)
+        shc = np.concatenate(sh).astype(np.float32)
+        C = shc.shape[2]
+        stride = (3 * C + 3) // 4 * 4
+        rows = np.zeros((K, stride), dtype=np.float32)
+        rows[:, :3 * C] = shc.reshape(K, 3 * C)
+        levels.append((torch.from_numpy(q), torch.from_numpy(rows), C))
+    table = dict(counts=counts, bounds_min=g["bounds_min"], bounds_max=g["bounds_max"],
+                 intervals=np.array(g["intervals"], dtype=np.float64), sh_degrees=g["sh_degrees"])
+    return levels, table
+
+
+def _lod_worker(rank, world, port, result_q):
+    import sys
+    sys.path.insert(0, os.path.dirname(HERE))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2404_01133_b200 import fusion
+        if rank == 0:
+            levels, table = _lod_levels_from_golden()
+            out = fusion.broadcast_lod(levels, table, src=0, device="cpu")
+        else:
+            out = fusion.broadcast_lod(None, None, src=0, device="cpu")
+        levels, table = out
+        result_q.put((rank, [(q.numpy(), sh.numpy(), C) for q, sh, C in levels],
+                      {k: np.asarray(v) for k, v in table.items()}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_lod_table_broadcast_gloo_world2():
+    """fusion.broadcast_lod: the LoD levels + table built on rank 0 arrive byte-identical on rank 1."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_lod_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in range(2):
+        r, lv, tb = q.get(timeout=120)
+        got[r] = (lv, tb)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want_levels, want_table = _lod_levels_from_golden()
+    for r in range(2):
+        lv, tb = got[r]
+        assert len(lv) == len(want_levels)
+        for (q_, sh, C), (wq, wsh, wC) in zip(lv, want_levels):
+            assert C == wC and q_.tobytes() == wq.numpy().tobytes() and sh.tobytes() == wsh.numpy().tobytes()
+        for k, v in want_table.items():
+            assert np.array_equal(tb[k], np.asarray(v)), k
