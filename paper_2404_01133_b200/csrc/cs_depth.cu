@@ -2,12 +2,12 @@
 //
 // The reference orders visible splats by np.argsort(depths, kind="stable")
 // (render.py:176-177): float64 depth, ties by assembled index.  K4 sorts only
-// the float32-rounded depth (round-to-nearest is monotone, so this is a
-// coarsening of the exact order: 4 radix passes over 8-byte (key, id) pairs
-// instead of 8 over 12-byte ones).  Splats whose float64 depths round to the
-// same float32 form runs that are contiguous after the sort and already in
-// ascending id order (the sort is stable); this kernel re-sorts every run by
-// (float64 depth bits, id), which restores the reference order exactly.
+// a 32-bit monotone coarsening of the float64 depth (the top bits of
+// bits(z) - bits(near), cs_project.cu: 4 radix passes over 8-byte (key, id)
+// pairs instead of 8 over 12-byte ones).  Splats with equal 32-bit keys
+// form runs that are contiguous after the sort and already in ascending id
+// order (the sort is stable); this kernel re-sorts every run by (float64
+// depth bits, id), which restores the reference order exactly.
 //   * runs of <= 8 (nearly all; 1-ulp float32 buckets at city scale hold a
 //     few splats at most): one thread, insertion sort in registers;
 //   * longer runs (e.g. many splats at exactly equal depth): queued and

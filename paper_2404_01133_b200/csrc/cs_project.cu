@@ -322,8 +322,18 @@ k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
   if (i >= n) return;
   // z > near > 0: the float64 bits are monotone; culled -> ~0 (sorts last)
   po_out.keys[i] = po.keep ? (uint64_t)__double_as_longlong(po.z) : ~0ull;
-  // float32 rounding is monotone: the 32-bit sort is a coarsening of the exact order
-  po_out.keys32[i] = po.keep ? __float_as_uint(__double2float_rn(po.z)) : 0xffffffffu;
+  // 32-bit sort key: a monotone coarsening of the float64 depth, so K4b only
+  // has to re-sort runs of equal keys.  For z > near the float64 bit patterns
+  // increase with z; (bits(z) - bits(near)) >> 24 keeps 2^28 steps per octave
+  // over the 16 octaves above the near plane (32x finer than the float32
+  // rounding, so far fewer equal-key runs), saturating beyond (~0.2 * 2^16 m
+  // at the default near plane); ~0 marks culled Gaussians.
+  {
+    const uint64_t zb = (uint64_t)__double_as_longlong(po.z);
+    const uint64_t nb = (uint64_t)__double_as_longlong(st.near_plane > 0.0 ? st.near_plane : 0.0);
+    const uint64_t code = (zb - nb) >> 24;
+    po_out.keys32[i] = po.keep ? (uint32_t)min(code, (uint64_t)0xfffffffeu) : 0xffffffffu;
+  }
   po_out.vals[i] = (uint32_t)i;
   if (!po.keep) return;
   const int64_t idx = i;

@@ -1,7 +1,8 @@
 """Exact depth order through the 32-bit depth sort + run fix-up (K4/K4b), needs a B200.
 
-Splats whose float64 depths round to the same float32 form runs after the
-32-bit radix sort; K4b re-sorts each run by (float64 depth, assembled index).
+Splats whose float64 depths share a 32-bit sort key (the top bits of
+bits(z) - bits(near), ~2^28 steps per octave) form runs after the 32-bit radix
+sort; K4b re-sorts each run by (float64 depth, assembled index).
 These scenes force every fix-up path -- short runs (<= 8, one thread), runs
 handled by one CTA in shared memory (<= 2048) and longer runs merged through
 global scratch -- with shuffled sub-ulp depth offsets and exact ties, and
@@ -47,10 +48,10 @@ def test_depth_runs_exact(seed):
     from paper_2404_01133_b200.render import bin_tiles_last, project_cloud
     groups = [
         (5.0, 600, 1e-2, False),     # spread out: mostly singleton runs, some short runs
-        (7.0, 24, 1e-7, True),       # one float32 bucket at 7: a 24-run (CTA path) with ties
-        (10.0, 1500, 4e-7, True),    # one float32 bucket at 10: 1500-run (CTA bitonic)
+        (7.0, 24, 1e-7, True),       # ~7 keys at 7: short runs with ties
+        (10.0, 1500, 4e-7, True),    # ~13 keys at 10: runs of ~100 (CTA bitonic)
         (30.0, 5000, 0.0, False),    # 5000 exactly equal depths (merge path, order by index)
-        (40.0, 4500, 1.5e-6, True),  # one bucket at 40: 4500-run, shuffled (merge path)
+        (40.0, 4500, 1.5e-6, True),  # ~12 keys at 40: runs of ~400, shuffled, with ties
     ]
     cloud, cam = _scene(seed, groups)
     st = cs.RenderSettings()
