@@ -46,7 +46,7 @@ size_t radix_status_words(int64_t capacity, int key_bytes);
 template <typename K>
 int radix_sort(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_dev, int64_t capacity,
                int begin_bit, int end_bit, uint32_t* hist, uint32_t* status, uint32_t* tickets,
-               cudaStream_t s);
+               cudaStream_t s, bool hist_ready = false);
 // cs_depth.cu
 void launch_fix_depth_runs(const uint32_t* k32_sorted, uint32_t* order, const uint64_t* k64,
                            const DevStats* stats, int64_t capacity, void* ctl_mem,
@@ -70,7 +70,7 @@ void launch_pair_count(const uint32_t* order, const int4* rects, DevStats* stats
                        cudaStream_t s);
 void launch_duplicate(const int64_t* pair_off, const uint32_t* order, const int4* rects,
                       const uint32_t* dup_start, const DevStats* stats, int ntx, int64_t pair_cap,
-                      uint32_t* keys, uint32_t* vals, cudaStream_t s);
+                      uint32_t* keys, uint32_t* vals, uint32_t* hist, int key_bits, cudaStream_t s);
 void launch_tile_ranges(const uint32_t* keys, const uint32_t* vals, const short4* boxes,
                         const DevStats* stats, uint2* ranges, uint32_t* bxs, uint32_t* bys,
                         cudaStream_t s);
@@ -504,9 +504,11 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
     return CS_OK;
   }
   // K6: duplicate
+  // (also counts the tile sort's digit histograms, so K7 skips its counting pass)
   launch_duplicate(c->pair_off.as<int64_t>(), order, c->rects.as<int4>(),
                    c->dup_start.as<uint32_t>(), stats, ntx,
-                   c->cap_pairs, c->pkA.as<uint32_t>(), c->pvA.as<uint32_t>(), s);
+                   c->cap_pairs, c->pkA.as<uint32_t>(), c->pvA.as<uint32_t>(),
+                   bits_for(n_tiles) <= 24 ? c->hist.as<uint32_t>() : nullptr, bits_for(n_tiles), s);
   CS_CHECK_LAUNCH();
   mark(c, 5, s);
   // K7: stable sort by tile id only (ceil(log2 T) bits)
@@ -514,7 +516,8 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
                                           c->pkB.as<uint32_t>(), c->pvB.as<uint32_t>(),
                                           &stats->pairs_eff, c->cap_pairs, 0, bits_for(n_tiles),
                                           c->hist.as<uint32_t>(), c->st_sort.as<uint32_t>(),
-                                          c->sort_tickets.as<uint32_t>() + 8, s);
+                                          c->sort_tickets.as<uint32_t>() + 8, s,
+                                          /*hist_ready=*/bits_for(n_tiles) <= 24);
   CS_CHECK_LAUNCH();
   const uint32_t* tkeys = which2 ? c->pkB.as<uint32_t>() : c->pkA.as<uint32_t>();
   const uint32_t* tvals = which2 ? c->pvB.as<uint32_t>() : c->pvA.as<uint32_t>();

@@ -105,33 +105,19 @@ static_assert(kDupTile == 4 * kDupThreads, "k_duplicate emits 4 pairs per thread
 // sequential walk over the rect row-major (render.py:233-243) and on to the
 // next rank, and two 16-byte stores.  key = tile id, value = splat id.
 constexpr int kDupItems = kDupTile / kDupThreads;  // 4
+constexpr int kMaxHistPasses = 3;
 
-__global__ void __launch_bounds__(kDupThreads)
-k_duplicate(const int64_t* __restrict__ pair_off, const uint32_t* __restrict__ order,
-            const int4* __restrict__ rects, const uint32_t* __restrict__ dup_start,
-            const DevStats* __restrict__ stats, int ntx, uint32_t* __restrict__ keys,
-            uint32_t* __restrict__ vals) {
-  __shared__ int64_t s_off[kDupTile + 2];
-  __shared__ int4 s_rect[kDupTile + 1];
-  __shared__ uint32_t s_id[kDupTile + 1];
-  const int64_t P = stats->pairs_eff;
-  const int64_t M = stats->visible;
-  const int64_t p0 = (int64_t)blockIdx.x * kDupTile;
-  if (p0 >= P) return;
-  const int64_t p1 = min(p0 + kDupTile, P);
-  const int64_t rlo = dup_start[blockIdx.x];
-  const int64_t rhi = p1 < P ? (int64_t)dup_start[blockIdx.x + 1] : M - 1;  // owner of pair p1 (>= owner of p1-1)
-  const int nr = (int)(rhi - rlo + 1);
-  for (int i = threadIdx.x; i < nr; i += kDupThreads) {
-    const uint32_t v = __ldg(order + rlo + i);
-    s_off[i] = pair_off[rlo + i];
-    s_rect[i] = __ldg(rects + v);
-    s_id[i] = v;
-  }
-  if (threadIdx.x == 0) s_off[nr] = INT64_MAX;  // sentinel: every rank owns >= 1 pair
-  __syncthreads();
-  const int64_t p = p0 + (int64_t)threadIdx.x * kDupItems;
-  if (p >= p1) return;
+// Digit histograms of the tile sort that follows (equal-width digits, as
+// radix_sort_items splits end_bit): counted here from the pair keys.
+struct DigitHist {
+  uint32_t* hist;  // [n_passes][256], zeroed by the caller
+  int n_passes, width, end_bit;
+};
+
+__device__ __forceinline__ void emit_pairs(int64_t p, int64_t p1, int nr, const int64_t* s_off,
+                                           const int4* s_rect, const uint32_t* s_id, int ntx,
+                                           uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                           const DigitHist& dh, uint32_t (*s_hist)[256]) {
   int lo = 0, hi = nr - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -166,7 +152,49 @@ k_duplicate(const int64_t* __restrict__ pair_off, const uint32_t* __restrict__ o
     for (int j = 0; j < kDupItems; ++j)
       if (p + j < p1) { keys[p + j] = k[j]; vals[p + j] = v[j]; }
   }
+#pragma unroll
+  for (int j = 0; j < kDupItems; ++j)
+    if (p + j < p1)
+      for (int q = 0; q < dh.n_passes; ++q)
+        atomicAdd(&s_hist[q][(k[j] >> (dh.width * q)) & ((1u << min(dh.width, dh.end_bit - dh.width * q)) - 1u)], 1u);
 }
+
+__global__ void __launch_bounds__(kDupThreads)
+k_duplicate(const int64_t* __restrict__ pair_off, const uint32_t* __restrict__ order,
+            const int4* __restrict__ rects, const uint32_t* __restrict__ dup_start,
+            const DevStats* __restrict__ stats, int ntx, uint32_t* __restrict__ keys,
+            uint32_t* __restrict__ vals, DigitHist dh) {
+  __shared__ int64_t s_off[kDupTile + 2];
+  __shared__ int4 s_rect[kDupTile + 1];
+  __shared__ uint32_t s_id[kDupTile + 1];
+  __shared__ uint32_t s_hist[kMaxHistPasses][256];
+  const int64_t P = stats->pairs_eff;
+  const int64_t M = stats->visible;
+  const int64_t p0 = (int64_t)blockIdx.x * kDupTile;
+  if (p0 >= P) return;  // CTA-uniform
+  for (int i = threadIdx.x; i < dh.n_passes * 256; i += kDupThreads) s_hist[i >> 8][i & 255] = 0;
+  const int64_t p1 = min(p0 + kDupTile, P);
+  const int64_t rlo = dup_start[blockIdx.x];
+  const int64_t rhi = p1 < P ? (int64_t)dup_start[blockIdx.x + 1] : M - 1;  // owner of pair p1 (>= owner of p1-1)
+  const int nr = (int)(rhi - rlo + 1);
+  for (int i = threadIdx.x; i < nr; i += kDupThreads) {
+    const uint32_t v = __ldg(order + rlo + i);
+    s_off[i] = pair_off[rlo + i];
+    s_rect[i] = __ldg(rects + v);
+    s_id[i] = v;
+  }
+  if (threadIdx.x == 0) s_off[nr] = INT64_MAX;  // sentinel: every rank owns >= 1 pair
+  __syncthreads();
+  const int64_t p = p0 + (int64_t)threadIdx.x * kDupItems;
+  if (p < p1) emit_pairs(p, p1, nr, s_off, s_rect, s_id, ntx, keys, vals, dh, s_hist);
+  __syncthreads();
+  // the tile sort's digit histograms (K7 skips its counting pass)
+  for (int i = threadIdx.x; i < dh.n_passes * 256; i += kDupThreads) {
+    const uint32_t c = s_hist[i >> 8][i & 255];
+    if (c) atomicAdd(dh.hist + i, c);
+  }
+}
+
 
 // CSR tile ranges from the tile-sorted keys (render.py:247-248), and the
 // pair-major cull boxes the blend tests (boxes[vals[p]] split into one u32 per
@@ -201,11 +229,17 @@ void launch_pair_count(const uint32_t* order, const int4* rects, DevStats* stats
 
 void launch_duplicate(const int64_t* pair_off, const uint32_t* order, const int4* rects,
                       const uint32_t* dup_start, const DevStats* stats, int ntx, int64_t pair_cap,
-                      uint32_t* keys, uint32_t* vals, cudaStream_t s) {
+                      uint32_t* keys, uint32_t* vals, uint32_t* hist, int key_bits, cudaStream_t s) {
   const int64_t blocks = dup_blocks(pair_cap);
   if (blocks == 0) return;
+  DigitHist dh;  // hist == nullptr (keys wider than kMaxHistPasses digits): no counting
+  dh.hist = hist;
+  dh.n_passes = hist ? (key_bits + 7) / 8 : 0;
+  dh.width = dh.n_passes ? (key_bits + dh.n_passes - 1) / dh.n_passes : 8;
+  dh.end_bit = key_bits;
+  if (hist) cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 256 * dh.n_passes, s);
   k_duplicate<<<(unsigned)blocks, kDupThreads, 0, s>>>(pair_off, order, rects, dup_start, stats,
-                                                       ntx, keys, vals);
+                                                       ntx, keys, vals, dh);
 }
 
 void launch_tile_ranges(const uint32_t* keys, const uint32_t* vals, const short4* boxes,

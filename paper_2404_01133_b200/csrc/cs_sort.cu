@@ -243,7 +243,7 @@ template <typename K, int ITEMS, int MINB = SortCfg<K>::kMinBlocks, bool MATCH =
           bool EARLY = true>
 int radix_sort_items(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_dev,
                      int64_t capacity, int begin_bit, int end_bit, uint32_t* hist,
-                     uint32_t* status, uint32_t* tickets, cudaStream_t s) {
+                     uint32_t* status, uint32_t* tickets, cudaStream_t s, bool hist_ready = false) {
   // equal-width digits of <= 8 bits (13 tile bits -> 7 + 6: fewer ballots per key)
   const int n_passes = (end_bit - begin_bit + 7) / 8;
   if (n_passes <= 0 || capacity <= 0) return 0;
@@ -255,10 +255,12 @@ int radix_sort_items(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_
     cudaFuncSetAttribute(k_onesweep<K, ITEMS, MINB, MATCH, EARLY>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     carveout = true;
   }
-  cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 256 * n_passes, s);
   cudaMemsetAsync(tickets, 0, sizeof(uint32_t) * n_passes, s);
-  int hist_grid = (int)std::min<int64_t>(148 * 4, (capacity + kSortThreads - 1) / kSortThreads);
-  k_radix_hist<K><<<hist_grid, kSortThreads, 0, s>>>(k0, n_dev, begin_bit, n_passes, width, end_bit, hist);
+  if (!hist_ready) {  // else the producer counted the digits (K6 for the tile sort)
+    cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 256 * n_passes, s);
+    int hist_grid = (int)std::min<int64_t>(148 * 4, (capacity + kSortThreads - 1) / kSortThreads);
+    k_radix_hist<K><<<hist_grid, kSortThreads, 0, s>>>(k0, n_dev, begin_bit, n_passes, width, end_bit, hist);
+  }
   k_radix_hist_scan<<<1, 256, 0, s>>>(hist, n_passes);
   K* kin = k0; K* kout = k1;
   uint32_t* vin = v0; uint32_t* vout = v1;
@@ -276,14 +278,16 @@ int radix_sort_items(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_
 template <typename K>
 int radix_sort(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_dev, int64_t capacity,
                int begin_bit, int end_bit, uint32_t* hist, uint32_t* status, uint32_t* tickets,
-               cudaStream_t s) {
+               cudaStream_t s, bool hist_ready) {
   return radix_sort_items<K, SortCfg<K>::kItems>(k0, v0, k1, v1, n_dev, capacity, begin_bit,
-                                                 end_bit, hist, status, tickets, s);
+                                                 end_bit, hist, status, tickets, s, hist_ready);
 }
 
 template int radix_sort<uint64_t>(uint64_t*, uint32_t*, uint64_t*, uint32_t*, const int64_t*,
-                                  int64_t, int, int, uint32_t*, uint32_t*, uint32_t*, cudaStream_t);
+                                  int64_t, int, int, uint32_t*, uint32_t*, uint32_t*, cudaStream_t,
+                                  bool);
 template int radix_sort<uint32_t>(uint32_t*, uint32_t*, uint32_t*, uint32_t*, const int64_t*,
-                                  int64_t, int, int, uint32_t*, uint32_t*, uint32_t*, cudaStream_t);
+                                  int64_t, int, int, uint32_t*, uint32_t*, uint32_t*, cudaStream_t,
+                                  bool);
 
 }  // namespace cs
