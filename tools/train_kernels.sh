@@ -4,7 +4,7 @@ TAG=${1:-tk}
 python -c "import __graft_entry__ as g; g.build()" >/dev/null 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none \
   -k regex:"k_project_bwd|k_blend_bwd|k_adam|k_ssim|k_blend<float, 1" \
-  --launch-skip 100 -c 60 --csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e \
+  --launch-skip 100 -c 60 --csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-assign \
   --train-steps 8 --train-warmup 36 > gpurun_out/${TAG}_train_launches.csv 2>&1
 python - "$TAG" <<'PY'
 import csv, collections, sys
