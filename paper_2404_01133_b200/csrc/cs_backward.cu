@@ -64,8 +64,20 @@ __device__ __forceinline__ float warp_transpose_sum9(const float (&in)[kGradFiel
 // float64 decisions for its pixel; when any lane contributes, the nine
 // partials are warp-reduced and lane 0 adds them with one atomic each.
 #ifndef CS_BWD_MINB
-#define CS_BWD_MINB 3
+#define CS_BWD_MINB 2
 #endif
+#ifndef CS_BWD_PX
+#define CS_BWD_PX 2
+#endif
+
+template <int PX>
+__device__ __forceinline__ int bwd_box_pixel(int b, int lane, int ts, int j) {
+  return PX == 1 ? box_pixel(b, lane, ts) : box_pixel2(b, lane, ts, j);
+}
+
+// PX pixels per lane (1: 8x4 boxes, 2: 8x8 boxes): with two, a lane sums its
+// pixels' partials before the warp reduction, halving reductions and atomics.
+template <int PX>
 __global__ void __launch_bounds__(kBwdThreads, CS_BWD_MINB)
 k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
             const uint32_t* __restrict__ bys, const uint2* __restrict__ ranges,
@@ -81,6 +93,7 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
   const uint32_t lane = lane_id();
   const uint32_t lt_mask = (1u << lane) - 1u;
   HotRec (*wbuf)[32] = s_hot[threadIdx.x >> 5];
+  const float bg[3] = {(float)bp.bg[0], (float)bp.bg[1], (float)bp.bg[2]};
   for (;;) {
     int item = 0;
     if (lane == 0) item = (int)atomicAdd(ticket, 1u);
@@ -91,30 +104,45 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
     const int tx = t % bp.ntx, ty = t / bp.ntx;
     const uint2 rg = ranges[t];
     const int64_t s0 = rg.x, s1 = rg.y;
-    const int li = box_pixel(b, lane, ts);
-    const int px = tx * ts + li % ts, py = ty * ts + li / ts;
-    const bool valid = li < ts * ts && px < bp.width && py < bp.height;
-    int x0 = valid ? px : 1 << 20, x1 = valid ? px : -(1 << 20);
-    int y0 = valid ? py : 1 << 20, y1 = valid ? py : -(1 << 20);
-    int64_t my_end = s0;
+    int px[PX], py[PX];
+    bool valid[PX];
+    int64_t my_end[PX];
     // Only the accept decision (power, exp, alpha floor) must replay the
     // forward's float64 arithmetic; the partials themselves are float32.
-    float g[3] = {0.f, 0.f, 0.f}, acc[3] = {0.f, 0.f, 0.f}, Tend = 1.f;
-    if (valid) {
-      const int64_t pix = (int64_t)py * bp.width + px;
-      my_end = state.last[pix];
-      const double te = state.final_t[pix];
-      Tend = (float)te;
+    float g[PX][3], acc[PX][3], Tend[PX], T[PX], P[PX][3];
+    double sx[PX], sy[PX];
+    int x0 = 1 << 20, x1 = -(1 << 20), y0 = 1 << 20, y1 = -(1 << 20), wend = (int)s0;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const double a = state.color_acc[3 * pix + c];
-        acc[c] = (float)a;
-        const double o = a + te * bp.bg[c];  // unclipped pixel value
-        // clip to [0, 1] (render.py:273): gradient passes where 0 <= C <= 1
-        g[c] = (o >= 0.0 && o <= 1.0) ? dl_dimg[3 * pix + c] : 0.f;
+    for (int j = 0; j < PX; ++j) {
+      const int li = bwd_box_pixel<PX>(b, lane, ts, j);
+      px[j] = tx * ts + li % ts;
+      py[j] = ty * ts + li / ts;
+      valid[j] = li < ts * ts && px[j] < bp.width && py[j] < bp.height;
+      my_end[j] = s0;
+      Tend[j] = 1.f;
+      T[j] = 1.f;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) g[j][c] = acc[j][c] = P[j][c] = 0.f;
+      if (valid[j]) {
+        const int64_t pix = (int64_t)py[j] * bp.width + px[j];
+        my_end[j] = state.last[pix];
+        const double te = state.final_t[pix];
+        Tend[j] = (float)te;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double a = state.color_acc[3 * pix + c];
+          acc[j][c] = (float)a;
+          const double o = a + te * bp.bg[c];  // unclipped pixel value
+          // clip to [0, 1] (render.py:273): gradient passes where 0 <= C <= 1
+          g[j][c] = (o >= 0.0 && o <= 1.0) ? dl_dimg[3 * pix + c] : 0.f;
+        }
+        x0 = min(x0, px[j]); x1 = max(x1, px[j]);
+        y0 = min(y0, py[j]); y1 = max(y1, py[j]);
+        wend = max(wend, (int)my_end[j]);
       }
+      sx[j] = (double)px[j] + 0.5;
+      sy[j] = (double)py[j] + 0.5;
     }
-    int wend = (int)my_end;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       x0 = min(x0, __shfl_xor_sync(0xffffffffu, x0, o));
@@ -125,9 +153,6 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
     }
     if (x0 > x1) continue;  // warp-uniform
     const int64_t e1 = min((int64_t)wend, s1);
-    const double sx = (double)px + 0.5, sy = (double)py + 0.5;
-    const float bg[3] = {(float)bp.bg[0], (float)bp.bg[1], (float)bp.bg[2]};
-    float T = 1.f, P[3] = {0.f, 0.f, 0.f};
 
     auto eval_round = [&](const HotRec* buf, uint32_t mask, int64_t k0) {
       int slot = 0;
@@ -137,13 +162,16 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
         const HotRec& h = buf[slot++];
         const double mx = h.mx, my = h.my, c0 = h.c0, c1 = h.c1, c2 = h.c2, lthr = h.lthr;
         float gr[kGradFields];
+#pragma unroll
+        for (int f = 0; f < kGradFields; ++f) gr[f] = 0.f;
         bool contrib = false;
-        // the quadratic form for every lane (as in the forward: cheaper than a branch)
-        const double dx = dsub(sx, mx), dy = dsub(sy, my);
-        const double power = dsub(dmul(-0.5, dadd(dmul(dmul(c0, dx), dx), dmul(dmul(c2, dy), dy))),
-                                  dmul(dmul(c1, dx), dy));
-        {
-          if (k0 + src < my_end && power >= lthr) {
+#pragma unroll
+        for (int j = 0; j < PX; ++j) {
+          // the quadratic form for every lane (as in the forward: cheaper than a branch)
+          const double dx = dsub(sx[j], mx), dy = dsub(sy[j], my);
+          const double power = dsub(dmul(-0.5, dadd(dmul(dmul(c0, dx), dx), dmul(dmul(c2, dy), dy))),
+                                    dmul(dmul(c1, dx), dy));
+          if (k0 + src < my_end[j] && power >= lthr) {
             const double G = exp_le0(power, s_exp, ec);
             double alpha = dmul(h.opacity, G);
             const bool clamped = alpha > 0.99;
@@ -151,34 +179,30 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
             if (alpha >= bp.alpha_floor) {
               contrib = true;
               const float a = (float)alpha;
-              const float w = T * a;
+              const float w = T[j] * a;
               const float inv = 1.f / (1.f - a);
               const float col[3] = {h.r, h.g, h.b};
               float dl_da = 0.f;
 #pragma unroll
               for (int c = 0; c < 3; ++c) {
-                P[c] = fmaf(w, col[c], P[c]);
-                const float S = (acc[c] - P[c]) + Tend * bg[c];
-                dl_da += g[c] * (T * col[c] - S * inv);
-                gr[6 + c] = w * g[c];
+                P[j][c] = fmaf(w, col[c], P[j][c]);
+                const float S = (acc[j][c] - P[j][c]) + Tend[j] * bg[c];
+                dl_da += g[j][c] * (T[j] * col[c] - S * inv);
+                gr[6 + c] += w * g[j][c];
               }
               const float dl_dpow = clamped ? 0.f : dl_da * a;
               const float fdx = (float)dx, fdy = (float)dy;
-              gr[5] = clamped ? 0.f : dl_da * (float)G;
-              gr[0] = dl_dpow * ((float)c0 * fdx + (float)c1 * fdy);
-              gr[1] = dl_dpow * ((float)c2 * fdy + (float)c1 * fdx);
-              gr[2] = dl_dpow * (-0.5f * fdx * fdx);
-              gr[3] = dl_dpow * (-fdx * fdy);
-              gr[4] = dl_dpow * (-0.5f * fdy * fdy);
-              T *= 1.f - a;
+              gr[5] += clamped ? 0.f : dl_da * (float)G;
+              gr[0] += dl_dpow * ((float)c0 * fdx + (float)c1 * fdy);
+              gr[1] += dl_dpow * ((float)c2 * fdy + (float)c1 * fdx);
+              gr[2] += dl_dpow * (-0.5f * fdx * fdx);
+              gr[3] += dl_dpow * (-fdx * fdy);
+              gr[4] += dl_dpow * (-0.5f * fdy * fdy);
+              T[j] *= 1.f - a;
             }
           }
         }
         if (__any_sync(0xffffffffu, contrib)) {
-          if (!contrib) {
-#pragma unroll
-            for (int f = 0; f < kGradFields; ++f) gr[f] = 0.f;
-          }
           const float v = warp_transpose_sum9(gr, lane);
           const uint32_t f = (lane >> 1) & 15;
           if (!(lane & 1) && f < kGradFields && v != 0.f) atomicAdd(&grads[(int64_t)f * cap + h.id], v);
@@ -193,7 +217,9 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
       nby = __ldg(bys + s0 + lane);
     }
     uint32_t pmask = 0;
-    uint32_t live = __ballot_sync(0xffffffffu, valid && my_end > s0);
+    uint32_t live_px = 0;  // per-lane bitmask of pixels still needing entries
+#pragma unroll
+    for (int j = 0; j < PX; ++j) live_px |= (valid[j] && my_end[j] > s0 ? 1u : 0u) << j;
     int64_t pk0 = 0;
     int stage = 0;
     for (int64_t k0 = s0; k0 < e1; k0 += 32) {
@@ -226,12 +252,18 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
       // shrink the cull box to the pixels whose last fragment lies beyond
       // this round (as in the forward: entries that only meet finished
       // pixels are neither staged nor evaluated)
-      const uint32_t live_now = __ballot_sync(0xffffffffu, valid && my_end > k0 + 32);
-      if (live_now != live) {
-        live = live_now;
-        const bool on = valid && my_end > k0 + 32;
-        x0 = on ? px : 1 << 20; x1 = on ? px : -(1 << 20);
-        y0 = on ? py : 1 << 20; y1 = on ? py : -(1 << 20);
+      uint32_t lp = 0;
+#pragma unroll
+      for (int j = 0; j < PX; ++j) lp |= (valid[j] && my_end[j] > k0 + 32 ? 1u : 0u) << j;
+      if (__any_sync(0xffffffffu, lp != live_px)) {
+        live_px = lp;
+        x0 = 1 << 20; x1 = -(1 << 20); y0 = 1 << 20; y1 = -(1 << 20);
+#pragma unroll
+        for (int j = 0; j < PX; ++j)
+          if (lp & (1u << j)) {
+            x0 = min(x0, px[j]); x1 = max(x1, px[j]);
+            y0 = min(y0, py[j]); y1 = max(y1, py[j]);
+          }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           x0 = min(x0, __shfl_xor_sync(0xffffffffu, x0, o));
@@ -515,12 +547,13 @@ void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint32_t* bxs, co
   bp.width = width;
   bp.height = height;
   bp.ntx = ntx;
+  constexpr int PX = CS_BWD_PX;
   static int grid = 0;
-  if (grid == 0) grid = persistent_grid(k_blend_bwd, kBwdThreads);
-  const int nboxes = boxes_per_tile(st.tile_size);
+  if (grid == 0) grid = persistent_grid(k_blend_bwd<PX>, kBwdThreads);
+  const int nboxes = PX == 1 ? boxes_per_tile(st.tile_size) : boxes_per_tile2(st.tile_size);
   cudaMemsetAsync(ticket, 0, sizeof(uint32_t), s);
-  k_blend_bwd<<<grid, kBwdThreads, 0, s>>>(list, bxs, bys, ranges, hot, order, n_tiles * nboxes,
-                                           nboxes, bp, dl_dimg, state, ticket, grads, cap);
+  k_blend_bwd<PX><<<grid, kBwdThreads, 0, s>>>(list, bxs, bys, ranges, hot, order, n_tiles * nboxes,
+                                               nboxes, bp, dl_dimg, state, ticket, grads, cap);
 }
 
 void launch_project_bwd(const cs_cloud& cl, const uint64_t* depth_keys, const cs_camera& cam,
