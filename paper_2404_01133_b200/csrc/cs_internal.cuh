@@ -516,8 +516,8 @@ __device__ __forceinline__ void load_pos(const cs_cloud& c, int64_t k, double& x
 }
 
 // Upper-bound binary search over segment starts: last s with seg[s].start <= i.
-__device__ __forceinline__ int find_seg(const Seg* segs, int n, int64_t i) {
-  int lo = 0, hi = n - 1;
+__device__ __forceinline__ int find_seg(const Seg* segs, int n, int64_t i, int lo = 0, int hi = -1) {
+  if (hi < 0) hi = n - 1;
   while (lo < hi) {
     int mid = (lo + hi + 1) >> 1;
     if (segs[mid].start <= i) lo = mid; else hi = mid - 1;

@@ -274,7 +274,13 @@ void launch_significance(const cs_cloud& cl, const cs_camera* cams, int n_cams,
   k_significance<<<(unsigned)blocks, 256, 0, s>>>(cl, cams, n_cams, st, hits, vol_keys, vals);
 }
 
-constexpr int kProjThreads = 256;
+#ifndef CS_PROJ_THREADS
+#define CS_PROJ_THREADS 256
+#endif
+#ifndef CS_PROJ_MINB
+#define CS_PROJ_MINB 3
+#endif
+constexpr int kProjThreads = CS_PROJ_THREADS;
 
 // Projection, one thread per assembled Gaussian, no compaction: every
 // per-splat output is written at the Gaussian's assembled index i (its
@@ -283,20 +289,28 @@ constexpr int kProjThreads = 256;
 // values are the visible splat ids in (depth, assembled index) order, and the
 // kernel needs no block scan or cross-CTA look-back (LoD assembly already
 // drops invisible blocks: ~97% of the assembled set is visible on C3).
-__global__ void __launch_bounds__(kProjThreads, 3)
+__global__ void __launch_bounds__(kProjThreads, CS_PROJ_MINB)
 k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
           DevStats* __restrict__ stats, cs_camera cam, cs_settings st,
           ProjOutputs po_out, const uint64_t* __restrict__ list) {
   const int64_t n = stats->assembled;
   const int64_t i = blockIdx.x * (int64_t)kProjThreads + threadIdx.x;
-  if (blockIdx.x * (int64_t)kProjThreads >= n) return;  // CTA-uniform
+  const int64_t cta0 = blockIdx.x * (int64_t)kProjThreads;
+  if (cta0 >= n) return;  // CTA-uniform
+  // the segments of the CTA's first and last index bound every thread's
+  // search (a CTA's 256 indices nearly always fall in one or two pieces)
+  __shared__ int s_seg[2];
+  const int n_segs = stats->n_segs;
+  if (threadIdx.x < 2)
+    s_seg[threadIdx.x] = find_seg(segs, n_segs, threadIdx.x ? min(cta0 + kProjThreads, n) - 1 : cta0);
+  __syncthreads();
   ProjOut po;
   po.in_front = po.ok = po.keep = false;
   Geom g;
   int64_t local = 0;
   int cloud_id = 0;
   if (i < n) {
-    const int si = find_seg(segs, stats->n_segs, i);
+    const int si = find_seg(segs, n_segs, i, s_seg[0], s_seg[1]);
     const Seg sg = segs[si];
     cloud_id = sg.cloud;
     local = i - sg.start;

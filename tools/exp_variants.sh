@@ -10,7 +10,7 @@ for V in "$@"; do
 import json,sys
 d=json.loads(sys.stdin.read())
 t=d.get('train')
-print('$V', 'fps', round(d['value'],1), 'blend', round(d['stages_ms']['blend'],3), 'train', t and round(t['value'],1), t and {k: round(v,3) for k,v in t['phases_ms'].items()})"
+print('$V', 'fps', round(d['value'],1), 'stages', {k: round(v,3) for k,v in d['stages_ms'].items()}, 'train', t and round(t['value'],1), t and {k: round(v,3) for k,v in t['phases_ms'].items()})"
 done
 touch paper_2404_01133_b200/csrc/${FILE}.cu
 python paper_2404_01133_b200/_build.py > /dev/null 2>&1
