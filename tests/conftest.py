@@ -132,3 +132,8 @@ def assign_inputs(g):
     settings = SimpleNamespace(background=(0.0, 0.0, 0.0), sh_degree=3, tile_size=16,
                                alpha_floor=1.0 / 255.0, transmittance_floor=1e-4, near_plane=0.2)
     return cloud, views, grid, settings
+
+
+@pytest.fixture(scope="session")
+def golden_bundle():
+    return Golden("bundle.npz")

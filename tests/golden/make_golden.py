@@ -19,6 +19,8 @@ the reference's own outputs of the hot-path functions:
                with the per-(pose, block) l_ssim of the contribution test
                (partition.py:318-334, metrics.py:70-101); a 5x5 grid with
                sparse / unassigned blocks (enlarged-bounds retry)
+  bundle/      an on-disk LoD bundle written by lod.save_lod (lod.py:405-429)
+  bundle.npz   the reference's lod.load_lod (lod.py:432-455) of it
   lodgen.npz   LoD generation: significance_scores
                (lod.py:54-101), the stable priority order (lod.py:114-116),
                build_lod's per-level / per-block kept rows (lod.py:211-248) and
@@ -48,7 +50,7 @@ sys.path.insert(0, str(REF / "tests"))
 from citysplat.config import RunConfig  # noqa: E402
 from citysplat.core import CameraView, Gaussian, GaussianCloud, SH_C0  # noqa: E402
 from citysplat.lod import (_keep_count, _priority, assemble_render_set, build_lod,  # noqa: E402
-                           decide_visibility, mad_bounds, significance_scores)
+                           decide_visibility, load_lod, mad_bounds, save_lod, significance_scores)
 from citysplat.metrics import l_ssim  # noqa: E402
 from citysplat.partition import (ContractionMap, _scaled_camera, assign, fuse,  # noqa: E402
                                  grid_partition)
@@ -289,6 +291,35 @@ def make_assign():
           "enlarged", enlarged)
 
 
+def make_bundle():
+    import shutil
+    bundle = generate_synthetic_city(seed=5, extent=50.0, n_buildings=6, n_cameras=8,
+                                     target_gaussians=1500, image_size=(64, 48))
+    cloud = bundle.cloud
+    cmap = ContractionMap.central_third(cloud)
+    grid = grid_partition(cloud, cmap, (2, 2))
+    config = RunConfig(block_dims=(2, 2), distance_intervals=((0.0, 15.0), (15.0, 35.0), (35.0, math.inf)))
+    lod = build_lod(cloud, grid, [r.view for r in bundle.train_cameras()], config)
+    out = OUT / "bundle"
+    shutil.rmtree(out, ignore_errors=True)
+    save_lod(lod, out)
+    back = load_lod(out)
+    store = {"n_levels": np.int64(back.n_levels), "n_blocks": np.int64(back.n_blocks),
+             "bounds_min": back.bounds_min, "bounds_max": back.bounds_max,
+             "intervals": np.array(back.distance_intervals), "sh_degrees": np.array(back.sh_degrees),
+             "n_mad": np.float64(back.n_mad)}
+    put(store, "full", cloud_dict(back.full))
+    for l in range(back.n_levels):
+        for j in range(back.n_blocks):
+            put(store, f"level{l}/block{j}", cloud_dict(back.levels[l][j]))
+    cam = bundle.cameras[3].view
+    put(store, "cam", cam_dict(cam))
+    a = assemble_render_set(back, cam)
+    put(store, "render", render_record(a.cloud, cam, RenderSettings()))
+    np.savez_compressed(OUT / "bundle.npz", **store)
+    print("bundle/", sum(f.stat().st_size for f in out.rglob("*") if f.is_file()) // 1024, "KiB")
+
+
 def make_lodgen():
     bundle = generate_synthetic_city(seed=11, extent=120.0, n_buildings=30, n_cameras=24,
                                      target_gaussians=20_000, image_size=(320, 240))
@@ -344,5 +375,6 @@ if __name__ == "__main__":
     make_fuse()
     make_lodgen()
     make_assign()
+    make_bundle()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size // 1024, "KiB")
