@@ -213,7 +213,9 @@ def blend_flops(st: dict) -> float:
 def ncu_traffic(kernel: str):
     """DRAM bytes per launch of `kernel` from the committed ncu --set full
     capture (profiles/*_frame_traffic.json, newest), or None."""
-    files = sorted((ROOT / "profiles").glob("*_frame_traffic.json"))
+    # capture tags run r1a .. r1z, r1aa ..: newest = longest, then greatest
+    tag = lambda f: f.name[: -len("_frame_traffic.json")]
+    files = sorted((ROOT / "profiles").glob("*_frame_traffic.json"), key=lambda f: (len(tag(f)), tag(f)))
     if not files:
         return None, None
     data = json.loads(files[-1].read_text())
@@ -222,6 +224,21 @@ def ncu_traffic(kernel: str):
         return None, files[-1].name
     launches = [x for lst in hits for x in lst]
     return sum(x["dram_bytes"] for x in launches) / len(launches), files[-1].name
+
+
+def ncu_pipes(kernel: str):
+    """Issue-slot / FP64 / FMA pipe / shared-memory utilisation of `kernel` from
+    the same committed capture (percent), or None."""
+    tag = lambda f: f.name[: -len("_frame_traffic.json")]
+    files = sorted((ROOT / "profiles").glob("*_frame_traffic.json"), key=lambda f: (len(tag(f)), tag(f)))
+    if not files:
+        return None
+    data = json.loads(files[-1].read_text())
+    hits = [x for k, v in data.items() if k.startswith(kernel) for x in v]
+    keys = ("issue_active_pct", "fp64_pipe_pct", "fma_pipe_pct", "smem_pct", "threads_per_inst")
+    if not hits or any(k not in hits[0] for k in keys):
+        return None
+    return {k: round(sum(x[k] or 0.0 for x in hits) / len(hits), 1) for k in keys}
 
 
 def main():
@@ -399,6 +416,9 @@ def main():
                                "MEASURED_PEAKS.json)",
                 "flops_per_frame": blend_flops(counts) / K}
     roof["traffic_source"] = f"profiles/{tsrc} (ncu --set full, dram__bytes_read+write per launch)" if tsrc else None
+    # the blend is issue-bound (divergent per-pixel termination), not FP64-pipe-bound:
+    # the ncu pipe utilisations of the same capture explain the flop fraction
+    roof["ncu_pipes_pct"] = ncu_pipes("k_blend")
     roof["stages_hbm"] = stage_roof
 
     cpu = None

@@ -21,7 +21,7 @@ constexpr int kDupTile = 1024;                         // pairs per duplication 
 // across chunks).  Also records, for every duplication CTA b, the depth rank
 // owning pair b*kDupTile (dup_start[b]), so K6 needs no global binary search.
 __global__ void __launch_bounds__(kCountThreads)
-k_pair_count(const uint32_t* __restrict__ order, const int4* __restrict__ rects,
+k_pair_count(const uint32_t* __restrict__ order, const uint2* __restrict__ rects,
              DevStats* __restrict__ stats, int64_t pair_cap, uint64_t* __restrict__ status,
              int64_t* __restrict__ pair_off, uint32_t* __restrict__ dup_start) {
   __shared__ int64_t s_chunk;
@@ -42,7 +42,7 @@ k_pair_count(const uint32_t* __restrict__ order, const int4* __restrict__ rects,
     const int64_t r = wbase + i * 32 + lane;
     c32[i] = 0;
     if (r < M) {
-      const int4 rc = __ldg(rects + __ldg(order + r));
+      const int4 rc = unpack_rect(__ldg(rects + __ldg(order + r)));
       c32[i] = (uint32_t)((rc.y - rc.x + 1) * (rc.w - rc.z + 1));
     }
     cnt[i] = c32[i];
@@ -161,7 +161,7 @@ __device__ __forceinline__ void emit_pairs(int64_t p, int64_t p1, int nr, const 
 
 __global__ void __launch_bounds__(kDupThreads)
 k_duplicate(const int64_t* __restrict__ pair_off, const uint32_t* __restrict__ order,
-            const int4* __restrict__ rects, const uint32_t* __restrict__ dup_start,
+            const uint2* __restrict__ rects, const uint32_t* __restrict__ dup_start,
             const DevStats* __restrict__ stats, int ntx, uint32_t* __restrict__ keys,
             uint32_t* __restrict__ vals, DigitHist dh) {
   __shared__ int64_t s_off[kDupTile + 2];
@@ -180,7 +180,7 @@ k_duplicate(const int64_t* __restrict__ pair_off, const uint32_t* __restrict__ o
   for (int i = threadIdx.x; i < nr; i += kDupThreads) {
     const uint32_t v = __ldg(order + rlo + i);
     s_off[i] = pair_off[rlo + i];
-    s_rect[i] = __ldg(rects + v);
+    s_rect[i] = unpack_rect(__ldg(rects + v));
     s_id[i] = v;
   }
   if (threadIdx.x == 0) s_off[nr] = INT64_MAX;  // sentinel: every rank owns >= 1 pair
@@ -218,7 +218,7 @@ __global__ void k_tile_ranges(const uint32_t* __restrict__ keys, const uint32_t*
 int64_t pair_count_chunks(int64_t capacity) { return (capacity + kCountTile - 1) / kCountTile; }
 int64_t dup_blocks(int64_t pair_cap) { return (pair_cap + kDupTile - 1) / kDupTile; }
 
-void launch_pair_count(const uint32_t* order, const int4* rects, DevStats* stats, int64_t pair_cap,
+void launch_pair_count(const uint32_t* order, const uint2* rects, DevStats* stats, int64_t pair_cap,
                        int64_t capacity, uint64_t* status, int64_t* pair_off, uint32_t* dup_start,
                        cudaStream_t s) {
   const int64_t chunks = pair_count_chunks(capacity);
@@ -227,7 +227,7 @@ void launch_pair_count(const uint32_t* order, const int4* rects, DevStats* stats
                                                           pair_off, dup_start);
 }
 
-void launch_duplicate(const int64_t* pair_off, const uint32_t* order, const int4* rects,
+void launch_duplicate(const int64_t* pair_off, const uint32_t* order, const uint2* rects,
                       const uint32_t* dup_start, const DevStats* stats, int ntx, int64_t pair_cap,
                       uint32_t* keys, uint32_t* vals, uint32_t* hist, int key_bits, cudaStream_t s) {
   const int64_t blocks = dup_blocks(pair_cap);

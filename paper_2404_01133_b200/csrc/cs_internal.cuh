@@ -83,12 +83,21 @@ struct DevStats {     // device mirror of cs_frame_stats + scratch counters
 
 // Outputs of the projection kernel, indexed by assembled index (splat id);
 // hot/rects/boxes/recs are written for visible splats only.
+// 8-byte tile rectangle (tile coordinates < 2^16): K5/K6 gather it in depth
+// order, so half the bytes of an int4 means half the gathered sectors' footprint.
+__device__ __forceinline__ uint2 pack_rect(int x0, int x1, int y0, int y1) {
+  return make_uint2((uint32_t)x0 | ((uint32_t)x1 << 16), (uint32_t)y0 | ((uint32_t)y1 << 16));
+}
+__device__ __forceinline__ int4 unpack_rect(uint2 r) {
+  return make_int4((int)(r.x & 0xffffu), (int)(r.x >> 16), (int)(r.y & 0xffffu), (int)(r.y >> 16));
+}
+
 struct ProjOutputs {
   uint64_t* keys;    // float64 depth bits (~0 for culled Gaussians), for the exact run fix-up
   uint32_t* keys32;  // float32-rounded depth bits (~0 for culled): the radix-sorted key
   uint32_t* vals;    // splat id
   HotRec* hot;
-  int4* rects;
+  uint2* rects;      // tile rectangle, 16-bit packed: (x0 | x1 << 16, y0 | y1 << 16)
   short4* boxes;     // copy of HotRec's cull box, dense (8 B)
   ProjRec* recs;     // optional (debug / dumps)
   const uint8_t* exclude;  // input, optional: rows culled as if absent (assignment renders)

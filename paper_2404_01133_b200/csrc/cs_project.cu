@@ -400,7 +400,7 @@ k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
     const int64_t tx1 = clip_i64(np_to_i64(floor(ddiv(dsub(dadd(po.mx, po.rx), 0.5), ts))), 0, ntx - 1);
     const int64_t ty0 = clip_i64(np_to_i64(floor(ddiv(dsub(dsub(po.my, po.ry), 0.5), ts))), 0, nty - 1);
     const int64_t ty1 = clip_i64(np_to_i64(floor(ddiv(dsub(dadd(po.my, po.ry), 0.5), ts))), 0, nty - 1);
-    po_out.rects[idx] = make_int4((int)tx0, (int)tx1, (int)ty0, (int)ty1);
+    po_out.rects[idx] = pack_rect((int)tx0, (int)tx1, (int)ty0, (int)ty1);
   }
   if (po_out.recs) {  // debug / dump mode: the full _Projected record (render.py:89-108)
     ProjRec rec;

@@ -21,7 +21,7 @@ METRICS = [
     "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
     "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
-    "l1tex__data_pipe_lsu_wavefronts_mem_shared.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
     "smsp__thread_inst_executed_per_inst_executed.ratio",
     "smsp__issue_active.avg.pct_of_peak_sustained_active",
 ]
@@ -68,7 +68,12 @@ def main():
         lines.append(f"| `{name}` | {t:.1f} | {rd / 1e6:.1f} | {wr / 1e6:.1f} | {bw:.0f} | {100 * bw / hbm:.1f} | "
                      f"{fmt(f(METRICS[3]))} | {fmt(f(METRICS[4]))} | {fmt(f(METRICS[5]))} | {fmt(f(METRICS[7]))} | "
                      f"{fmt(f(METRICS[8]))} | {fmt(f(METRICS[9]))} | {fmt(f(METRICS[10]))} | {fmt(f(METRICS[11]))} |")
-        traffic.setdefault(name, []).append({"us": t, "dram_bytes": rd + wr})
+        traffic.setdefault(name, []).append({"us": t, "dram_bytes": rd + wr,
+                                             "issue_active_pct": f(METRICS[11]),
+                                             "fp64_pipe_pct": f(METRICS[7]),
+                                             "fma_pipe_pct": f(METRICS[8]),
+                                             "smem_pct": f(METRICS[9]),
+                                             "threads_per_inst": f(METRICS[10])})
     Path(out_md).write_text("\n".join(lines) + "\n")
     if out_json:
         Path(out_json).write_text(json.dumps(traffic, indent=1))
