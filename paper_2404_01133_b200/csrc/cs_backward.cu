@@ -154,13 +154,16 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
     if (x0 > x1) continue;  // warp-uniform
     const int64_t e1 = min((int64_t)wend, s1);
 
-    auto eval_round = [&](const HotRec* buf, uint32_t mask, int64_t k0) {
+    // ids: each lane's list entry of the staged round (the hit's splat id is
+    // the entry of lane src, the gradient slot of its atomics)
+    auto eval_round = [&](const HotRec* buf, uint32_t mask, int64_t k0, uint32_t ids) {
       int slot = 0;
       while (mask) {
         const int src = __ffs(mask) - 1;
         mask &= mask - 1;
         const HotRec& h = buf[slot++];
-        const double mx = h.mx, my = h.my, c0 = h.c0, c1 = h.c1, c2 = h.c2, lthr = h.lthr;
+        const uint32_t hid = __shfl_sync(0xffffffffu, ids, src);
+        const double mx = h.mx, my = h.my, c0 = h.c0, c1 = h.c1, c2 = h.c2, lthr = (double)h.lthr;
         float gr[kGradFields];
 #pragma unroll
         for (int f = 0; f < kGradFields; ++f) gr[f] = 0.f;
@@ -205,7 +208,7 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
         if (__any_sync(0xffffffffu, contrib)) {
           const float v = warp_transpose_sum9(gr, lane);
           const uint32_t f = (lane >> 1) & 15;
-          if (!(lane & 1) && f < kGradFields && v != 0.f) atomicAdd(&grads[(int64_t)f * cap + h.id], v);
+          if (!(lane & 1) && f < kGradFields && v != 0.f) atomicAdd(&grads[(int64_t)f * cap + hid], v);
         }
       }
     };
@@ -216,7 +219,7 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
       nbx = __ldg(bxs + s0 + lane);
       nby = __ldg(bys + s0 + lane);
     }
-    uint32_t pmask = 0;
+    uint32_t pmask = 0, pid = 0;
     uint32_t live_px = 0;  // per-lane bitmask of pixels still needing entries
 #pragma unroll
     for (int j = 0; j < PX; ++j) live_px |= (valid[j] && my_end[j] > s0 ? 1u : 0u) << j;
@@ -240,13 +243,13 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
         const char* gp = reinterpret_cast<const char*>(hot + id);
         char* d = reinterpret_cast<char*>(&wbuf[stage][__popc(mask & lt_mask)]);
 #pragma unroll
-        for (int c = 0; c < 5; ++c) cp_async16(d + 16 * c, gp + 16 * c);
+        for (int c = 0; c < kHotChunks; ++c) cp_async16(d + 16 * c, gp + 16 * c);
       }
       cp_async_commit();
       if (pmask) {
         cp_async_wait<1>();
         __syncwarp();
-        eval_round(wbuf[stage ^ 1], pmask, pk0);
+        eval_round(wbuf[stage ^ 1], pmask, pk0, pid);
         __syncwarp();
       }
       // shrink the cull box to the pixels whose last fragment lies beyond
@@ -274,11 +277,12 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
       }
       pmask = mask;
       pk0 = k0;
+      pid = id;
       stage ^= 1;
     }
     cp_async_wait<0>();
     __syncwarp();
-    if (pmask) eval_round(wbuf[stage ^ 1], pmask, pk0);
+    if (pmask) eval_round(wbuf[stage ^ 1], pmask, pk0, pid);
     __syncwarp();
   }
 }

@@ -8,7 +8,7 @@
 // Every warp walks the tile's splat list (depth order) independently, 32
 // entries per round: each lane tests one splat's 8-byte alpha-floor support
 // box against the warp's pixel box, __ballot_sync compacts the hits, and the
-// warp evaluates only those (80-byte HotRec: mean, conic, opacity, colour,
+// warp evaluates only those (64-byte HotRec: mean, conic, opacity, colour,
 // fast-reject threshold), so a splat whose support misses the warp's 32
 // pixels costs 1/32 of a box test instead of 32 float64 quadratic forms, and
 // no warp ever waits at a block barrier for another.  Tiles are launched
@@ -36,7 +36,7 @@ constexpr int kBlendThreads = 256;
 // compact id and packed cull box (pair-major arrays written by K8: coalesced,
 // and the 8 boxes of a tile run concurrently so the list stays in L1/L2), a
 // __ballot_sync compacts the entries whose alpha-floor box meets the warp's
-// pixel box, and each hitting lane cp.async-copies its splat's 80-byte HotRec
+// pixel box, and each hitting lane cp.async-copies its splat's 64-byte HotRec
 // into the warp's shared-memory slot.  The copies of round r are in flight
 // while the warp evaluates round r-1 (two stages per warp).  The walk stops
 // as soon as the box's 32 pixels have terminated.
@@ -123,7 +123,7 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
         const int src = __ffs(mask) - 1;
         mask &= mask - 1;
         const HotRec& h = buf[slot++];
-        const double mx = h.mx, my = h.my, c0 = h.c0, c1 = h.c1, c2 = h.c2, lthr = h.lthr;
+        const double mx = h.mx, my = h.my, c0 = h.c0, c1 = h.c1, c2 = h.c2, lthr = (double)h.lthr;
         double power[PX];
         bool pass[PX];
 #pragma unroll
@@ -197,7 +197,7 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
         const char* g = reinterpret_cast<const char*>(hot + id);
         char* d = reinterpret_cast<char*>(&wbuf[stage][__popc(mask & lt_mask)]);
 #pragma unroll
-        for (int c = 0; c < 5; ++c) cp_async16(d + 16 * c, g + 16 * c);
+        for (int c = 0; c < kHotChunks; ++c) cp_async16(d + 16 * c, g + 16 * c);
       }
       cp_async_commit();
       if (pmask) {
@@ -375,9 +375,7 @@ __global__ void k_pack_records(int64_t m, const double* means, const double* con
     h.r = (float)colors[3 * s]; h.g = (float)colors[3 * s + 1]; h.b = (float)colors[3 * s + 2];
     const double lt = o > 0.0 ? log(alpha_floor / o) - 1e-6
                               : __longlong_as_double(0x7ff0000000000000ll);
-    h.lthr = (double)__double2float_rd(lt);
-    h.id = (uint32_t)s;
-    h.pad[0] = h.pad[1] = 0;
+    h.lthr = __double2float_rd(lt);
     hot[s] = h;
   }
 }

@@ -48,15 +48,15 @@ struct __align__(16) ProjRec {
 };
 static_assert(sizeof(ProjRec) == 128, "ProjRec layout");
 
-struct __align__(16) HotRec {   // everything the blend reads per splat (80 B: 5 cp.async)
+struct __align__(16) HotRec {   // everything the blend reads per splat (64 B: 4 cp.async)
   double mx, my, c0, c1, c2;     // mean2d, conic (render.py:128-129, 172)
   double opacity;
-  double lthr;                   // fast-reject threshold on power (<= log(alpha_floor/o) - margin)
+  float lthr;                    // fast-reject threshold on power (<= log(alpha_floor/o) - margin,
+                                 // rounded down to float: exact as a double)
   float r, g, b;                 // SH colour (fp32 of the float64 value)
-  uint32_t id;                   // splat id (gradient slot)
-  uint32_t pad[2];
 };
-static_assert(sizeof(HotRec) == 80, "HotRec layout");
+static_assert(sizeof(HotRec) == 64, "HotRec layout");
+constexpr int kHotChunks = (int)(sizeof(HotRec) / 16);  // cp.async 16-byte copies per record
 
 // pair-major cull boxes for the blend: (lo | hi << 16) as two int16, one word
 // per axis; kEmptyBox = (32767, -32768) never intersects

@@ -370,9 +370,7 @@ k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
   h.mx = po.mx; h.my = po.my; h.c0 = c0; h.c1 = c1; h.c2 = c2;
   h.opacity = g.op;
   h.r = (float)col[0]; h.g = (float)col[1]; h.b = (float)col[2];
-  h.lthr = (double)lthr;
-  h.id = (uint32_t)idx;
-  h.pad[0] = h.pad[1] = 0;
+  h.lthr = lthr;
   // Pixel box of {d : power(d) >= lthr} = {d^T Q d <= 2L}, L = -lthr: the
   // ellipse's AABB half-extents are sqrt(2 L a), sqrt(2 L c) with
   // (a, b, c) = Q^-1 = cov2d + low pass; inflated (1e-4 relative + 1e-3 px)
