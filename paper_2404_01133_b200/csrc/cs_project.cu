@@ -31,9 +31,18 @@ __device__ __forceinline__ int degree_of(int c) { return c >= 16 ? 3 : c >= 9 ? 
 // The row (3*C floats, 16-byte aligned, stride % 4 == 0) is fetched with
 // float4 loads; C is a template parameter so basis and coefficients stay in
 // registers.
+// The colour is a tolerance-only quantity (clipped [0, 1] colours, image
+// parity 1e-4; the rows are float32 already), so it is evaluated in float32
+// (CS_SH_F64 restores float64): the FP64 pipe stays with the decision math.
+#ifdef CS_SH_F64
+typedef double sh_t;
+#else
+typedef float sh_t;
+#endif
+
 template <int C>
-__device__ __forceinline__ void sh_colour_t(const float* row, int degree, double x, double y,
-                                            double z, double out[3]) {
+__device__ __forceinline__ void sh_colour_t(const float* row, int degree, sh_t x, sh_t y, sh_t z,
+                                            double out[3]) {
   constexpr int kVec = (3 * C + 3) / 4;
   float co[kVec * 4];
   const float4* r4 = reinterpret_cast<const float4*>(row);
@@ -42,49 +51,50 @@ __device__ __forceinline__ void sh_colour_t(const float* row, int degree, double
     const float4 v = __ldg(r4 + i);
     co[4 * i] = v.x; co[4 * i + 1] = v.y; co[4 * i + 2] = v.z; co[4 * i + 3] = v.w;
   }
-  double basis[C];
-  basis[0] = kShC0;
+  sh_t basis[C];
+  basis[0] = (sh_t)kShC0;
   if (C >= 4) {
-    basis[1] = degree >= 1 ? -kShC1 * y : 0.0;
-    basis[2] = degree >= 1 ? kShC1 * z : 0.0;
-    basis[3] = degree >= 1 ? -kShC1 * x : 0.0;
+    basis[1] = degree >= 1 ? -(sh_t)kShC1 * y : (sh_t)0;
+    basis[2] = degree >= 1 ? (sh_t)kShC1 * z : (sh_t)0;
+    basis[3] = degree >= 1 ? -(sh_t)kShC1 * x : (sh_t)0;
   }
   if (C >= 9) {
-    const double xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    const sh_t xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
     const bool on = degree >= 2;
-    basis[4] = on ? kShC2[0] * xy : 0.0;
-    basis[5] = on ? kShC2[1] * yz : 0.0;
-    basis[6] = on ? kShC2[2] * (2.0 * zz - xx - yy) : 0.0;
-    basis[7] = on ? kShC2[3] * xz : 0.0;
-    basis[8] = on ? kShC2[4] * (xx - yy) : 0.0;
+    basis[4] = on ? (sh_t)kShC2[0] * xy : (sh_t)0;
+    basis[5] = on ? (sh_t)kShC2[1] * yz : (sh_t)0;
+    basis[6] = on ? (sh_t)kShC2[2] * ((sh_t)2 * zz - xx - yy) : (sh_t)0;
+    basis[7] = on ? (sh_t)kShC2[3] * xz : (sh_t)0;
+    basis[8] = on ? (sh_t)kShC2[4] * (xx - yy) : (sh_t)0;
     if (C >= 16) {
       const bool on3 = degree >= 3;
-      basis[9] = on3 ? kShC3[0] * y * (3.0 * xx - yy) : 0.0;
-      basis[10] = on3 ? kShC3[1] * xy * z : 0.0;
-      basis[11] = on3 ? kShC3[2] * y * (4.0 * zz - xx - yy) : 0.0;
-      basis[12] = on3 ? kShC3[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy) : 0.0;
-      basis[13] = on3 ? kShC3[4] * x * (4.0 * zz - xx - yy) : 0.0;
-      basis[14] = on3 ? kShC3[5] * z * (xx - yy) : 0.0;
-      basis[15] = on3 ? kShC3[6] * x * (xx - 3.0 * yy) : 0.0;
+      basis[9] = on3 ? (sh_t)kShC3[0] * y * ((sh_t)3 * xx - yy) : (sh_t)0;
+      basis[10] = on3 ? (sh_t)kShC3[1] * xy * z : (sh_t)0;
+      basis[11] = on3 ? (sh_t)kShC3[2] * y * ((sh_t)4 * zz - xx - yy) : (sh_t)0;
+      basis[12] = on3 ? (sh_t)kShC3[3] * z * ((sh_t)2 * zz - (sh_t)3 * xx - (sh_t)3 * yy) : (sh_t)0;
+      basis[13] = on3 ? (sh_t)kShC3[4] * x * ((sh_t)4 * zz - xx - yy) : (sh_t)0;
+      basis[14] = on3 ? (sh_t)kShC3[5] * z * (xx - yy) : (sh_t)0;
+      basis[15] = on3 ? (sh_t)kShC3[6] * x * (xx - (sh_t)3 * yy) : (sh_t)0;
     }
   }
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) {
-    double acc = 0.0;
+    sh_t acc = 0;
 #pragma unroll
-    for (int n = 0; n < C; ++n) acc += (double)co[ch * C + n] * basis[n];
-    const double v = 0.5 + acc;
+    for (int n = 0; n < C; ++n) acc += (sh_t)co[ch * C + n] * basis[n];
+    const double v = 0.5 + (double)acc;
     out[ch] = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
   }
 }
 
 __device__ __forceinline__ void sh_colour(const float* row, int C, int degree, double x, double y,
                                           double z, double out[3]) {
+  const sh_t fx = (sh_t)x, fy = (sh_t)y, fz = (sh_t)z;
   switch (C) {
-    case 16: sh_colour_t<16>(row, degree, x, y, z, out); break;
-    case 9: sh_colour_t<9>(row, degree, x, y, z, out); break;
-    case 4: sh_colour_t<4>(row, degree, x, y, z, out); break;
-    default: sh_colour_t<1>(row, degree, x, y, z, out); break;
+    case 16: sh_colour_t<16>(row, degree, fx, fy, fz, out); break;
+    case 9: sh_colour_t<9>(row, degree, fx, fy, fz, out); break;
+    case 4: sh_colour_t<4>(row, degree, fx, fy, fz, out); break;
+    default: sh_colour_t<1>(row, degree, fx, fy, fz, out); break;
   }
 }
 
