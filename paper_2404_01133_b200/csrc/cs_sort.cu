@@ -66,45 +66,30 @@ __global__ void k_radix_hist_scan(uint32_t* hist, int n_passes) {
   }
 }
 
-template <typename K, int ITEMS = SortCfg<K>::kItems, int MINB = 1, bool MATCH = false,
-          bool EARLY = true>
-__global__ void __launch_bounds__(kSortThreads, MINB)
-k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
-           K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
-           const int64_t* __restrict__ n_ptr, int shift, int nbits,
-           const uint32_t* __restrict__ digit_base, uint32_t* __restrict__ status,
-           uint32_t* __restrict__ ticket) {
+// The pass body, FULL = the chunk holds kTile keys (no bounds checks, the
+// common case), NB = digit width (ballot count known at compile time).
+// Indices are 32-bit (n < 2^31).
+template <typename K, int ITEMS, bool FULL, int NB, bool EARLY>
+__device__ __forceinline__ void onesweep_body(
+    const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, K* __restrict__ keys_out,
+    uint32_t* __restrict__ vals_out, uint32_t n, uint32_t chunk, int shift,
+    const uint32_t* __restrict__ digit_base, uint32_t* __restrict__ status,
+    uint32_t (*warp_hist)[256], uint32_t* chunk_hist, uint32_t* digit_off, uint32_t* gbase,
+    uint32_t* scratch, K* keys_s, uint32_t* vals_s) {
   constexpr int kItems = ITEMS;
   constexpr int kTile = kSortThreads * kItems;
-  __shared__ uint32_t warp_hist[kSortWarps][256];
-  __shared__ uint32_t chunk_hist[256];
-  __shared__ uint32_t digit_off[256];
-  __shared__ int64_t gbase[256];
-  __shared__ uint32_t scratch[kSortWarps + 1];
-  __shared__ int64_t s_chunk;
-  __shared__ K keys_s[kTile];
-  __shared__ uint32_t vals_s[kTile];
-
-  const int64_t n = *n_ptr;
-  const uint32_t dmask = (1u << nbits) - 1u;  // this pass's digit: bits [shift, shift + nbits), nbits <= 8
-  if (threadIdx.x == 0) s_chunk = atomicAdd(ticket, 1u);
+  constexpr uint32_t dmask = (1u << NB) - 1u;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int d = lane; d < 256; d += 32) warp_hist[warp][d] = 0;
-  chunk_hist[threadIdx.x] = 0;
-  __syncthreads();
-  const int64_t chunk = s_chunk;
-  const int64_t base = chunk * kTile;
-  if (base >= n) return;
-  const int64_t valid_count = min((int64_t)kTile, n - base);
-
+  const uint32_t base = chunk * kTile;
+  const uint32_t valid_count = FULL ? kTile : n - base;
   K key[kItems];
   uint32_t val[kItems];
   uint32_t rank[kItems];
-  const int64_t wbase = base + (int64_t)warp * 32 * kItems;
+  const uint32_t wbase = base + warp * 32 * kItems;
 #pragma unroll
   for (int r = 0; r < kItems; ++r) {
-    const int64_t idx = wbase + r * 32 + lane;
-    if (idx < n) {
+    const uint32_t idx = wbase + r * 32 + lane;
+    if (FULL || idx < n) {
       key[r] = keys_in[idx];
       val[r] = vals_in[idx];
     }
@@ -115,44 +100,36 @@ k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
   //    (one atomic per digit group instead of one per key) and it is
   //    published right after the ranking.
   const int d = threadIdx.x;  // 256 threads == 256 digits
-  uint32_t* my_status = status + chunk * 256 + d;
+  uint32_t* my_status = status + (size_t)chunk * 256 + d;
   uint32_t my_count = 0;
   if (EARLY) {
 #pragma unroll
     for (int r = 0; r < kItems; ++r)
-      if (wbase + r * 32 + lane < n) atomicAdd(&chunk_hist[(uint32_t)(key[r] >> shift) & dmask], 1u);
+      if (FULL || wbase + r * 32 + lane < n) atomicAdd(&chunk_hist[(uint32_t)(key[r] >> shift) & dmask], 1u);
     __syncthreads();
     my_count = chunk_hist[d];
     atomicExch(my_status, (chunk == 0 ? kStFlagPre : kStFlagAgg) | my_count);
   }
-  // 2) stable in-warp ranks (warp order == input order).  All peer masks are
-  //    computed first (the MATCH/VOTE latencies overlap instead of serialising
-  //    behind each item's counter update), then per item the leader lane of
-  //    each digit group bumps the warp's counter with one shared atomic and
-  //    broadcasts the old value.  A warp's atomics to one address execute in
-  //    issue order, so items keep their input order.  64-bit keys: 8 ballots
-  //    per item (measured faster there than __match_any_sync).
+  // 2) stable in-warp ranks (warp order == input order): the lanes holding
+  //    the same digit from NB ballots; all peer masks first (the vote
+  //    latencies overlap), then per item the leader lane of each digit group
+  //    bumps the warp's counter with one shared atomic and broadcasts the old
+  //    value.  A warp's atomics to one address execute in issue order, so
+  //    items keep their input order.
   const uint32_t lt = lanemask_lt();
   uint32_t peers[kItems];
 #pragma unroll
   for (int r = 0; r < kItems; ++r) {
-    const bool valid = wbase + r * 32 + lane < n;
+    const bool valid = FULL || wbase + r * 32 + lane < n;
     const uint32_t dg = (uint32_t)(key[r] >> shift) & dmask;
-    if (!MATCH) {
-      uint32_t pm = __ballot_sync(0xffffffffu, valid);
+    uint32_t pm = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
 #pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        if (b < nbits) {  // warp-uniform
-          const bool bit = (dg >> b) & 1u;
-          const uint32_t bal = __ballot_sync(0xffffffffu, bit);
-          pm &= bit ? bal : ~bal;
-        }
-      }
-      peers[r] = valid ? pm : 0u;
-    } else {
-      const uint32_t pm = __match_any_sync(0xffffffffu, valid ? dg : 256u + lane);
-      peers[r] = valid ? pm : 0u;
+    for (int bit = 0; bit < NB; ++bit) {
+      const bool on = (dg >> bit) & 1u;
+      const uint32_t bal = __ballot_sync(0xffffffffu, on);
+      pm &= on ? bal : ~bal;
     }
+    peers[r] = valid ? pm : 0u;
   }
 #pragma unroll
   for (int r = 0; r < kItems; ++r) {
@@ -187,8 +164,7 @@ k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
   // 4) scatter into shared memory in chunk-local sorted order
 #pragma unroll
   for (int r = 0; r < kItems; ++r) {
-    const int64_t idx = wbase + r * 32 + lane;
-    if (idx < n) {
+    if (FULL || wbase + r * 32 + lane < n) {
       const uint32_t dg = (uint32_t)(key[r] >> shift) & dmask;
       const uint32_t pos = digit_off[dg] + warp_hist[warp][dg] + rank[r];
       keys_s[pos] = key[r];
@@ -196,15 +172,15 @@ k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     }
   }
   // 5) decoupled look-back for this digit, four predecessors per round trip
-  int64_t excl = 0;
+  uint32_t excl = 0;
   if (chunk > 0) {
-    int64_t p = chunk - 1;
+    int p = (int)chunk - 1;
     bool found = false;
     while (!found) {
       uint32_t st[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        st[k] = p - k >= 0 ? ld_volatile_u32(status + (p - k) * 256 + d) : (kStFlagPre | 0u);
+        st[k] = p - k >= 0 ? ld_volatile_u32(status + (size_t)(p - k) * 256 + d) : (kStFlagPre | 0u);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         if (found) break;
@@ -215,18 +191,54 @@ k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
         if (flag == 2) found = true;
       }
     }
-    atomicExch(my_status, kStFlagPre | (uint32_t)(excl + my_count));
+    atomicExch(my_status, kStFlagPre | (excl + my_count));
   }
-  gbase[d] = (int64_t)digit_base[d] + excl - (int64_t)local_start;
+  gbase[d] = digit_base[d] + excl - local_start;
   __syncthreads();
   // 6) coalesced write-out: consecutive threads store consecutive addresses of one digit run
-  for (int i = threadIdx.x; i < valid_count; i += kSortThreads) {
+#pragma unroll 4
+  for (uint32_t i = threadIdx.x; i < valid_count; i += kSortThreads) {
     const K k = keys_s[i];
-    const uint32_t dg = (uint32_t)(k >> shift) & dmask;
-    const int64_t o = gbase[dg] + i;
+    const uint32_t o = gbase[(uint32_t)(k >> shift) & dmask] + i;
     keys_out[o] = k;
     vals_out[o] = vals_s[i];
   }
+}
+
+template <typename K, int ITEMS = SortCfg<K>::kItems, int MINB = 1, int NB = 8, bool EARLY = true>
+__global__ void __launch_bounds__(kSortThreads, MINB)
+k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
+           K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
+           const int64_t* __restrict__ n_ptr, int shift,
+           const uint32_t* __restrict__ digit_base, uint32_t* __restrict__ status,
+           uint32_t* __restrict__ ticket) {
+  constexpr int kTile = kSortThreads * ITEMS;
+  __shared__ uint32_t warp_hist[kSortWarps][256];
+  __shared__ uint32_t chunk_hist[256];
+  __shared__ uint32_t digit_off[256];
+  __shared__ uint32_t gbase[256];
+  __shared__ uint32_t scratch[kSortWarps + 1];
+  __shared__ uint32_t s_chunk;
+  __shared__ K keys_s[kTile];
+  __shared__ uint32_t vals_s[kTile];
+
+  const uint32_t n = (uint32_t)*n_ptr;
+  if (threadIdx.x == 0) s_chunk = atomicAdd(ticket, 1u);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int d = lane; d < 256; d += 32) warp_hist[warp][d] = 0;
+  chunk_hist[threadIdx.x] = 0;
+  __syncthreads();
+  const uint32_t chunk = s_chunk;
+  const uint64_t base = (uint64_t)chunk * kTile;
+  if (base >= n) return;
+  if (base + kTile <= n)
+    onesweep_body<K, ITEMS, true, NB, EARLY>(keys_in, vals_in, keys_out, vals_out, n, chunk, shift,
+                                             digit_base, status, warp_hist, chunk_hist, digit_off,
+                                             gbase, scratch, keys_s, vals_s);
+  else
+    onesweep_body<K, ITEMS, false, NB, EARLY>(keys_in, vals_in, keys_out, vals_out, n, chunk, shift,
+                                              digit_base, status, warp_hist, chunk_hist, digit_off,
+                                              gbase, scratch, keys_s, vals_s);
 }
 
 // Workspace: hist (8*256 u32), status (chunks*256 u32), tickets (8 u32).
@@ -239,8 +251,21 @@ size_t radix_status_words(int64_t capacity, int key_bytes) {
 // Sorts (keys, vals) of length *n_dev (<= capacity) by bits [begin_bit, end_bit).
 // Ping-pongs between (k0,v0) and (k1,v1); returns 1 when the result is in
 // (k1,v1), 0 when in (k0,v0).
-template <typename K, int ITEMS, int MINB = SortCfg<K>::kMinBlocks, bool MATCH = false,
-          bool EARLY = true>
+template <typename K, int ITEMS, int MINB, int NB, bool EARLY>
+static void launch_pass(unsigned chunks, cudaStream_t s, const K* kin, const uint32_t* vin, K* kout,
+                        uint32_t* vout, const int64_t* n_dev, int shift, const uint32_t* hist,
+                        uint32_t* status, uint32_t* ticket) {
+  static bool carveout = false;  // shared memory is the occupancy limit: take all of it
+  if (!carveout) {
+    cudaFuncSetAttribute(k_onesweep<K, ITEMS, MINB, NB, EARLY>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    carveout = true;
+  }
+  k_onesweep<K, ITEMS, MINB, NB, EARLY><<<chunks, kSortThreads, 0, s>>>(kin, vin, kout, vout, n_dev,
+                                                                      shift, hist, status, ticket);
+}
+
+template <typename K, int ITEMS, int MINB = SortCfg<K>::kMinBlocks, bool EARLY = true>
 int radix_sort_items(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_dev,
                      int64_t capacity, int begin_bit, int end_bit, uint32_t* hist,
                      uint32_t* status, uint32_t* tickets, cudaStream_t s, bool hist_ready = false) {
@@ -250,11 +275,6 @@ int radix_sort_items(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_
   const int width = (end_bit - begin_bit + n_passes - 1) / n_passes;
   constexpr int kTile = kSortThreads * ITEMS;
   const int64_t chunks = (capacity + kTile - 1) / kTile;
-  static bool carveout = false;  // shared memory is the occupancy limit: take all of it
-  if (!carveout) {
-    cudaFuncSetAttribute(k_onesweep<K, ITEMS, MINB, MATCH, EARLY>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    carveout = true;
-  }
   cudaMemsetAsync(tickets, 0, sizeof(uint32_t) * n_passes, s);
   if (!hist_ready) {  // else the producer counted the digits (K6 for the tile sort)
     cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 256 * n_passes, s);
@@ -266,11 +286,23 @@ int radix_sort_items(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_
   uint32_t* vin = v0; uint32_t* vout = v1;
   for (int p = 0; p < n_passes; ++p) {
     cudaMemsetAsync(status, 0, sizeof(uint32_t) * 256 * chunks, s);
-    k_onesweep<K, ITEMS, MINB, MATCH, EARLY><<<(unsigned)chunks, kSortThreads, 0, s>>>(kin, vin, kout, vout, n_dev,
-        begin_bit + width * p, std::min(width, end_bit - begin_bit - width * p), hist + 256 * p,
-        status, tickets + p);
-    K* tk = kin; kin = kout; kout = tk;
-    uint32_t* tv = vin; vin = vout; vout = tv;
+    const int shift = begin_bit + width * p;
+    const int nb = std::min(width, end_bit - shift);
+    const unsigned g = (unsigned)chunks;
+    uint32_t* tk = tickets + p;
+    const uint32_t* hp = hist + 256 * p;
+    switch (nb) {
+      case 8: launch_pass<K, ITEMS, MINB, 8, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, tk); break;
+      case 7: launch_pass<K, ITEMS, MINB, 7, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, tk); break;
+      case 6: launch_pass<K, ITEMS, MINB, 6, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, tk); break;
+      case 5: launch_pass<K, ITEMS, MINB, 5, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, tk); break;
+      case 4: launch_pass<K, ITEMS, MINB, 4, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, tk); break;
+      case 3: launch_pass<K, ITEMS, MINB, 3, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, tk); break;
+      case 2: launch_pass<K, ITEMS, MINB, 2, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, tk); break;
+      default: launch_pass<K, ITEMS, MINB, 1, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, tk); break;
+    }
+    K* t0 = kin; kin = kout; kout = t0;
+    uint32_t* t1 = vin; vin = vout; vout = t1;
   }
   return (n_passes & 1) ? 1 : 0;
 }

@@ -14,7 +14,7 @@
 
 #include "../paper_2404_01133_b200/csrc/cs_sort.cu"
 
-template <typename K, int V, int MB = 1, bool MT = false, bool EA = true>
+template <typename K, int V, int MB = 1, bool EA = true>
 static void run(const char* name, std::vector<K> keys, int bits, int reps) {
   const int64_t n = (int64_t)keys.size();
   K *k0, *k1;
@@ -38,7 +38,7 @@ static void run(const char* name, std::vector<K> keys, int bits, int reps) {
     cudaMemcpy(v0, idx.data(), 4 * n, cudaMemcpyHostToDevice);
     cudaDeviceSynchronize();
     cudaEventRecord(e0);
-    which = cs::radix_sort_items<K, V, MB, MT, EA>(k0, v0, k1, v1, dn, n, 0, bits, hist, status, tickets, 0);
+    which = cs::radix_sort_items<K, V, MB, EA>(k0, v0, k1, v1, dn, n, 0, bits, hist, status, tickets, 0);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
@@ -51,7 +51,7 @@ static void run(const char* name, std::vector<K> keys, int bits, int reps) {
   const K mask = bits >= (int)(8 * sizeof(K)) ? ~K(0) : (K(1) << bits) - 1;
   std::stable_sort(want.begin(), want.end(), [&](uint32_t a, uint32_t b) { return (keys[a] & mask) < (keys[b] & mask); });
   const bool ok = got == want;
-  printf("v%-2d/%d%s%s %-24s n=%lld bits=%d: %.1f us (%s), %.2f Gkeys/s\n", V, MB, MT ? "m" : "b", EA ? "e" : "l", name, (long long)n, bits, best * 1e3,
+  printf("v%-2d/%d%s %-24s n=%lld bits=%d: %.1f us (%s), %.2f Gkeys/s\n", V, MB, EA ? "e" : "l", name, (long long)n, bits, best * 1e3,
          ok ? "exact" : "MISMATCH", n / (best * 1e-3) / 1e9);
 }
 
@@ -66,8 +66,8 @@ int main(int argc, char** argv) {
     if (prof) { run<uint32_t, 12, 3>("depth f32 keys", k, 32, 1); goto tiles; }
     run<uint32_t, 12, 3>("depth f32 keys", k, 32, 5);
     run<uint32_t, 16, 2>("depth f32 keys", k, 32, 5);
-    run<uint32_t, 12, 3, false, false>("depth f32 keys", k, 32, 5);
-    run<uint32_t, 16, 2, false, false>("depth f32 keys", k, 32, 5);
+    run<uint32_t, 12, 3, false>("depth f32 keys", k, 32, 5);
+    run<uint32_t, 16, 2, false>("depth f32 keys", k, 32, 5);
   }
 tiles:
   {
@@ -77,8 +77,8 @@ tiles:
     if (prof) { run<uint32_t, 12, 3>("tile keys", k, 13, 1); return 0; }
     run<uint32_t, 12, 3>("tile keys", k, 13, 5);
     run<uint32_t, 16, 2>("tile keys", k, 13, 5);
-    run<uint32_t, 12, 3, false, false>("tile keys", k, 13, 5);
-    run<uint32_t, 16, 2, false, false>("tile keys", k, 13, 5);
+    run<uint32_t, 12, 3, false>("tile keys", k, 13, 5);
+    run<uint32_t, 16, 2, false>("tile keys", k, 13, 5);
   }
   return 0;
 }
