@@ -31,7 +31,7 @@ constexpr uint32_t kStMask = (1u << 30) - 1;
 
 template <typename K> struct SortCfg;
 template <> struct SortCfg<uint64_t> { static constexpr int kItems = 8, kMinBlocks = 1; };
-template <> struct SortCfg<uint32_t> { static constexpr int kItems = 12, kMinBlocks = 3; };
+template <> struct SortCfg<uint32_t> { static constexpr int kItems = 16, kMinBlocks = 3; };
 
 template <typename K>
 __global__ void __launch_bounds__(kSortThreads)

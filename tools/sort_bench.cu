@@ -64,10 +64,11 @@ int main(int argc, char** argv) {
     for (auto& x : k) { float f = d(rng); memcpy(&x, &f, 4); }
     for (size_t i = 0; i < k.size() / 33; ++i) k[i * 33] = 0xffffffffu;  // culled
     if (prof) { run<uint32_t, 12, 3>("depth f32 keys", k, 32, 1); goto tiles; }
+    run<uint32_t, 8, 4>("depth f32 keys", k, 32, 5);
+    run<uint32_t, 10, 3>("depth f32 keys", k, 32, 5);
     run<uint32_t, 12, 3>("depth f32 keys", k, 32, 5);
     run<uint32_t, 16, 2>("depth f32 keys", k, 32, 5);
-    run<uint32_t, 12, 3, false>("depth f32 keys", k, 32, 5);
-    run<uint32_t, 16, 2, false>("depth f32 keys", k, 32, 5);
+    run<uint32_t, 16, 3>("depth f32 keys", k, 32, 5);
   }
 tiles:
   {
@@ -75,10 +76,11 @@ tiles:
     std::uniform_int_distribution<uint32_t> d(0, 8159);
     for (auto& x : k) x = d(rng);
     if (prof) { run<uint32_t, 12, 3>("tile keys", k, 13, 1); return 0; }
+    run<uint32_t, 8, 4>("tile keys", k, 13, 5);
+    run<uint32_t, 10, 3>("tile keys", k, 13, 5);
     run<uint32_t, 12, 3>("tile keys", k, 13, 5);
     run<uint32_t, 16, 2>("tile keys", k, 13, 5);
-    run<uint32_t, 12, 3, false>("tile keys", k, 13, 5);
-    run<uint32_t, 16, 2, false>("tile keys", k, 13, 5);
+    run<uint32_t, 16, 3>("tile keys", k, 13, 5);
   }
   return 0;
 }
