@@ -12,7 +12,13 @@
 namespace cs {
 
 constexpr int kCountThreads = 256;
-constexpr int kCountItems = 16;                        // ranks per thread
+#ifndef CS_COUNT_ITEMS
+#define CS_COUNT_ITEMS 16
+#endif
+#ifndef CS_COUNT_MINB
+#define CS_COUNT_MINB 1
+#endif
+constexpr int kCountItems = CS_COUNT_ITEMS;            // ranks per thread
 constexpr int kCountTile = kCountThreads * kCountItems;  // ranks per chunk
 constexpr int kDupTile = 1024;                         // pairs per duplication CTA
 
@@ -20,7 +26,7 @@ constexpr int kDupTile = 1024;                         // pairs per duplication 
 // 4096 ranks, warp-striped so every load is coalesced, decoupled look-back
 // across chunks).  Also records, for every duplication CTA b, the depth rank
 // owning pair b*kDupTile (dup_start[b]), so K6 needs no global binary search.
-__global__ void __launch_bounds__(kCountThreads)
+__global__ void __launch_bounds__(kCountThreads, CS_COUNT_MINB)
 k_pair_count(const uint32_t* __restrict__ order, const uint2* __restrict__ rects,
              DevStats* __restrict__ stats, int64_t pair_cap, uint64_t* __restrict__ status,
              int64_t* __restrict__ pair_off, uint32_t* __restrict__ dup_start) {
@@ -35,25 +41,25 @@ k_pair_count(const uint32_t* __restrict__ order, const uint2* __restrict__ rects
   if (base >= M) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t wbase = base + (int64_t)warp * (32 * kCountItems);
-  uint64_t cnt[kCountItems];
-  uint32_t c32[kCountItems];  // pair count of each rank (<= n_tiles)
+  // per rank count (<= n_tiles) and its exclusive offset inside the chunk:
+  // 32-bit (a chunk holds <= 4096 x 2^16 pairs), 64-bit only across chunks
+  uint32_t cnt[kCountItems], c32[kCountItems];
+  const bool full = base + kCountTile <= M;  // CTA-uniform
 #pragma unroll
   for (int i = 0; i < kCountItems; ++i) {
     const int64_t r = wbase + i * 32 + lane;
     c32[i] = 0;
-    if (r < M) {
+    if (full || r < M) {
       const int4 rc = unpack_rect(__ldg(rects + __ldg(order + r)));
       c32[i] = (uint32_t)((rc.y - rc.x + 1) * (rc.w - rc.z + 1));
     }
-    cnt[i] = c32[i];
   }
   // warp-local exclusive offsets over the warp's 512 consecutive ranks
-  uint64_t run = 0;
+  uint32_t run = 0;
 #pragma unroll
   for (int i = 0; i < kCountItems; ++i) {
-    const uint64_t incl = warp_incl_scan(cnt[i]);
-    const uint64_t c = cnt[i];
-    cnt[i] = run + incl - c;  // now: exclusive offset within the warp
+    const uint32_t incl = warp_incl_scan(c32[i]);
+    cnt[i] = run + incl - c32[i];  // exclusive offset within the warp
     run += __shfl_sync(0xffffffffu, incl, 31);
   }
   // warp totals -> block-exclusive warp offsets
