@@ -66,9 +66,9 @@ void launch_activate_geom(int64_t K, const float* geom, float4* pos_op, float4* 
 int64_t pair_count_chunks(int64_t capacity);
 int64_t dup_blocks(int64_t pair_cap);
 void launch_pair_count(const uint32_t* order, const uint2* rects, DevStats* stats, int64_t pair_cap,
-                       int64_t capacity, uint64_t* status, int64_t* pair_off, uint32_t* dup_start,
+                       int64_t capacity, uint64_t* status, uint32_t* pair_off, uint32_t* dup_start,
                        cudaStream_t s);
-void launch_duplicate(const int64_t* pair_off, const uint32_t* order, const uint2* rects,
+void launch_duplicate(const uint32_t* pair_off, const uint32_t* order, const uint2* rects,
                       const uint32_t* dup_start, const DevStats* stats, int ntx, int64_t pair_cap,
                       uint32_t* keys, uint32_t* vals, uint32_t* hist, int key_bits, cudaStream_t s);
 void launch_tile_ranges(const uint32_t* keys, const uint32_t* vals, const short4* boxes,
@@ -359,7 +359,7 @@ static int ensure_frame_buffers(cs_ctx* c, int64_t cap_vis, int n_segs, int n_bl
         c->long_runs.ensure(4 * fix_long_cap(cap)) || c->fix_ctl.ensure(fix_ctl_bytes()) ||
         c->valsB.ensure(4 * cap) || c->hot.ensure(sizeof(HotRec) * cap) ||
         c->rects.ensure(8 * cap) || c->boxes.ensure(8 * cap) ||
-        c->pair_off.ensure(8 * cap))
+        c->pair_off.ensure(4 * cap))
       return fail(CS_ENOMEM, "visible-splat buffers (%lld)", (long long)cap);
     c->cap_vis = cap;
   }
@@ -494,7 +494,7 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
   // K5: pair counts in depth order, scanned
   CS_CUDA(cudaMemsetAsync(c->st_gather.p, 0, 8 * (pair_count_chunks(cap) + 1), s));
   launch_pair_count(order, c->rects.as<uint2>(), stats, c->cap_pairs, cap,
-                    c->st_gather.as<uint64_t>(), c->pair_off.as<int64_t>(),
+                    c->st_gather.as<uint64_t>(), c->pair_off.as<uint32_t>(),
                     c->dup_start.as<uint32_t>(), s);
   CS_CHECK_LAUNCH();
   if (timed) mark(c, 4, s);
@@ -505,7 +505,7 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
   }
   // K6: duplicate
   // (also counts the tile sort's digit histograms, so K7 skips its counting pass)
-  launch_duplicate(c->pair_off.as<int64_t>(), order, c->rects.as<uint2>(),
+  launch_duplicate(c->pair_off.as<uint32_t>(), order, c->rects.as<uint2>(),
                    c->dup_start.as<uint32_t>(), stats, ntx,
                    c->cap_pairs, c->pkA.as<uint32_t>(), c->pvA.as<uint32_t>(),
                    bits_for(n_tiles) <= 24 ? c->hist.as<uint32_t>() : nullptr, bits_for(n_tiles), s);

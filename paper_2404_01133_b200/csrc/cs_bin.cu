@@ -29,7 +29,7 @@ constexpr int kDupTile = 1024;                         // pairs per duplication 
 __global__ void __launch_bounds__(kCountThreads, CS_COUNT_MINB)
 k_pair_count(const uint32_t* __restrict__ order, const uint2* __restrict__ rects,
              DevStats* __restrict__ stats, int64_t pair_cap, uint64_t* __restrict__ status,
-             int64_t* __restrict__ pair_off, uint32_t* __restrict__ dup_start) {
+             uint32_t* __restrict__ pair_off, uint32_t* __restrict__ dup_start) {
   __shared__ int64_t s_chunk;
   __shared__ uint64_t s_scan[kCountThreads / 32 + 1];
   __shared__ uint64_t s_prefix;
@@ -92,7 +92,7 @@ k_pair_count(const uint32_t* __restrict__ order, const uint2* __restrict__ rects
     const int64_t r = wbase + i * 32 + lane;
     if (r >= M) break;
     const int64_t o = (int64_t)(off0 + cnt[i]);
-    pair_off[r] = o;
+    pair_off[r] = (uint32_t)o;  // read by K6 only when P <= pair_cap < 2^30
     // duplication CTAs whose first pair lies in [o, o + count)
     const int64_t c = c32[i];
     if (o + c <= pair_cap) {
@@ -120,7 +120,7 @@ struct DigitHist {
   int n_passes, width, end_bit;
 };
 
-__device__ __forceinline__ void emit_pairs(int64_t p, int64_t p1, int nr, const int64_t* s_off,
+__device__ __forceinline__ void emit_pairs(int64_t p, int64_t p1, int nr, const uint32_t* s_off,
                                            const int4* s_rect, const uint32_t* s_id, int ntx,
                                            uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
                                            const DigitHist& dh, uint32_t (*s_hist)[256]) {
@@ -133,7 +133,7 @@ __device__ __forceinline__ void emit_pairs(int64_t p, int64_t p1, int nr, const 
   int w = rc.y - rc.x + 1;
   const int64_t local = p - s_off[lo];
   int ly = (int)(local / w), lx = (int)(local - (int64_t)ly * w);
-  int64_t next = s_off[lo + 1];
+  int64_t next = s_off[lo + 1];  // sentinel 0xffffffff beyond the last rank
   uint32_t k[kDupItems], v[kDupItems];
 #pragma unroll
   for (int j = 0; j < kDupItems; ++j) {
@@ -166,11 +166,11 @@ __device__ __forceinline__ void emit_pairs(int64_t p, int64_t p1, int nr, const 
 }
 
 __global__ void __launch_bounds__(kDupThreads)
-k_duplicate(const int64_t* __restrict__ pair_off, const uint32_t* __restrict__ order,
+k_duplicate(const uint32_t* __restrict__ pair_off, const uint32_t* __restrict__ order,
             const uint2* __restrict__ rects, const uint32_t* __restrict__ dup_start,
             const DevStats* __restrict__ stats, int ntx, uint32_t* __restrict__ keys,
             uint32_t* __restrict__ vals, DigitHist dh) {
-  __shared__ int64_t s_off[kDupTile + 2];
+  __shared__ uint32_t s_off[kDupTile + 2];
   __shared__ int4 s_rect[kDupTile + 1];
   __shared__ uint32_t s_id[kDupTile + 1];
   __shared__ uint32_t s_hist[kMaxHistPasses][256];
@@ -189,7 +189,7 @@ k_duplicate(const int64_t* __restrict__ pair_off, const uint32_t* __restrict__ o
     s_rect[i] = unpack_rect(__ldg(rects + v));
     s_id[i] = v;
   }
-  if (threadIdx.x == 0) s_off[nr] = INT64_MAX;  // sentinel: every rank owns >= 1 pair
+  if (threadIdx.x == 0) s_off[nr] = 0xffffffffu;  // sentinel: every rank owns >= 1 pair
   __syncthreads();
   const int64_t p = p0 + (int64_t)threadIdx.x * kDupItems;
   if (p < p1) emit_pairs(p, p1, nr, s_off, s_rect, s_id, ntx, keys, vals, dh, s_hist);
@@ -225,7 +225,7 @@ int64_t pair_count_chunks(int64_t capacity) { return (capacity + kCountTile - 1)
 int64_t dup_blocks(int64_t pair_cap) { return (pair_cap + kDupTile - 1) / kDupTile; }
 
 void launch_pair_count(const uint32_t* order, const uint2* rects, DevStats* stats, int64_t pair_cap,
-                       int64_t capacity, uint64_t* status, int64_t* pair_off, uint32_t* dup_start,
+                       int64_t capacity, uint64_t* status, uint32_t* pair_off, uint32_t* dup_start,
                        cudaStream_t s) {
   const int64_t chunks = pair_count_chunks(capacity);
   if (chunks == 0) return;
@@ -233,7 +233,7 @@ void launch_pair_count(const uint32_t* order, const uint2* rects, DevStats* stat
                                                           pair_off, dup_start);
 }
 
-void launch_duplicate(const int64_t* pair_off, const uint32_t* order, const uint2* rects,
+void launch_duplicate(const uint32_t* pair_off, const uint32_t* order, const uint2* rects,
                       const uint32_t* dup_start, const DevStats* stats, int ntx, int64_t pair_cap,
                       uint32_t* keys, uint32_t* vals, uint32_t* hist, int key_bits, cudaStream_t s) {
   const int64_t blocks = dup_blocks(pair_cap);
