@@ -209,15 +209,48 @@ __global__ void k_tile_ranges(const uint32_t* __restrict__ keys, const uint32_t*
                               const uint2* __restrict__ boxes, const DevStats* __restrict__ stats,
                               uint2* __restrict__ ranges, uint32_t* __restrict__ bxs,
                               uint32_t* __restrict__ bys) {
-  const int64_t P = stats->pairs_eff;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P; p += stride) {
-    const uint32_t t = keys[p];
-    if (p == 0 || keys[p - 1] != t) ranges[t].x = (uint32_t)p;
-    if (p == P - 1 || keys[p + 1] != t) ranges[t].y = (uint32_t)(p + 1);
-    const uint2 b = __ldg(boxes + __ldg(vals + p));  // short4 (x0, x1, y0, y1)
-    bxs[p] = b.x;
-    bys[p] = b.y;
+  // four consecutive pairs per thread (16-byte loads / stores, four independent
+  // box gathers in flight); pairs < 2^30, so 32-bit indices
+  const uint32_t P = (uint32_t)stats->pairs_eff;
+  const uint32_t groups = (P + 3) / 4;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += stride) {
+    const uint32_t p = 4 * gi;
+    uint32_t k[4], v[4];
+    if (p + 4 <= P) {
+      const uint4 k4 = __ldg(reinterpret_cast<const uint4*>(keys) + gi);
+      const uint4 v4 = __ldg(reinterpret_cast<const uint4*>(vals) + gi);
+      k[0] = k4.x; k[1] = k4.y; k[2] = k4.z; k[3] = k4.w;
+      v[0] = v4.x; v[1] = v4.y; v[2] = v4.z; v[3] = v4.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        k[j] = p + j < P ? __ldg(keys + p + j) : 0xffffffffu;
+        v[j] = p + j < P ? __ldg(vals + p + j) : 0u;
+      }
+    }
+    uint2 b[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (p + j < P) b[j] = __ldg(boxes + v[j]);  // short4 (x0, x1, y0, y1)
+    const uint32_t prev = p == 0 ? 0xffffffffu : __ldg(keys + p - 1);
+    const uint32_t next = p + 4 < P ? __ldg(keys + p + 4) : 0xffffffffu;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (p + j >= P) break;
+      const uint32_t before = j == 0 ? prev : k[j - 1];
+      const uint32_t after = j == 3 ? next : (p + j + 1 < P ? k[j + 1] : 0xffffffffu);
+      if (p + j == 0 || before != k[j]) ranges[k[j]].x = p + j;
+      if (p + j + 1 == P || after != k[j]) ranges[k[j]].y = p + j + 1;
+    }
+    if (p + 4 <= P) {
+      reinterpret_cast<uint4*>(bxs)[gi] = make_uint4(b[0].x, b[1].x, b[2].x, b[3].x);
+      reinterpret_cast<uint4*>(bys)[gi] = make_uint4(b[0].y, b[1].y, b[2].y, b[3].y);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (p + j < P) { bxs[p + j] = b[j].x; bys[p + j] = b[j].y; }
+    }
   }
 }
 
