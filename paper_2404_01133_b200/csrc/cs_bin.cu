@@ -120,10 +120,11 @@ struct DigitHist {
   int n_passes, width, end_bit;
 };
 
-__device__ __forceinline__ void emit_pairs(int64_t p, int64_t p1, int nr, const uint32_t* s_off,
+__device__ __forceinline__ void emit_pairs(uint32_t p, uint32_t p1, int nr, const uint32_t* s_off,
                                            const int4* s_rect, const uint32_t* s_id, int ntx,
                                            uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
                                            const DigitHist& dh, uint32_t (*s_hist)[256]) {
+  // 32-bit throughout: pairs < 2^30 (pair_cap), a rank owns <= n_tiles pairs
   int lo = 0, hi = nr - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -131,9 +132,9 @@ __device__ __forceinline__ void emit_pairs(int64_t p, int64_t p1, int nr, const 
   }
   int4 rc = s_rect[lo];
   int w = rc.y - rc.x + 1;
-  const int64_t local = p - s_off[lo];
-  int ly = (int)(local / w), lx = (int)(local - (int64_t)ly * w);
-  int64_t next = s_off[lo + 1];  // sentinel 0xffffffff beyond the last rank
+  const int local = (int)(p - s_off[lo]);
+  int ly = local / w, lx = local - ly * w;
+  uint32_t next = s_off[lo + 1];  // sentinel 0xffffffff beyond the last rank
   uint32_t k[kDupItems], v[kDupItems];
 #pragma unroll
   for (int j = 0; j < kDupItems; ++j) {
@@ -191,8 +192,8 @@ k_duplicate(const uint32_t* __restrict__ pair_off, const uint32_t* __restrict__ 
   }
   if (threadIdx.x == 0) s_off[nr] = 0xffffffffu;  // sentinel: every rank owns >= 1 pair
   __syncthreads();
-  const int64_t p = p0 + (int64_t)threadIdx.x * kDupItems;
-  if (p < p1) emit_pairs(p, p1, nr, s_off, s_rect, s_id, ntx, keys, vals, dh, s_hist);
+  const uint32_t p = (uint32_t)p0 + threadIdx.x * kDupItems;
+  if (p < p1) emit_pairs(p, (uint32_t)p1, nr, s_off, s_rect, s_id, ntx, keys, vals, dh, s_hist);
   __syncthreads();
   // the tile sort's digit histograms (K7 skips its counting pass)
   for (int i = threadIdx.x; i < dh.n_passes * 256; i += kDupThreads) {
