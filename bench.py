@@ -250,10 +250,20 @@ def main():
         return run_reference(args, rank, world)
     import torch
     import torch.distributed as dist
+    # CS_BENCH_SHARED_GPU=1 (testing only): every rank on the visible GPU(s) modulo
+    # their count, with gloo carrying the collectives -- exercises the N > 1
+    # code path (view split, LoD broadcast, LPT training, fusion all-gather) on
+    # a one-GPU box.  Never set for a measured run.
+    shared = os.environ.get("CS_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     import ctypes
 
     import paper_2404_01133_b200 as cs
