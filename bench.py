@@ -607,10 +607,13 @@ def train_leg(args, raw, wh, rank, world, dev):
 
 
 def launches_per_frame() -> int:
-    # memset(stats), select, memset(status), project, [hist memset, ticket memset, hist, scan,
-    # 8 x (status memset + onesweep)], memset, gather, duplicate, [memset x2, hist, scan,
-    # 2 x (memset + onesweep)], memset, ranges, blend  -- kernels only:
-    return 1 + 1 + 2 + 8 + 1 + 1 + 2 + 2 + 1 + 1
+    """Kernels of one C3 frame (memsets excluded), as listed by the ncu launch
+    capture (profiles/r1ab_launches.csv: 72 launches over 4 frames):
+    k_lod_select, k_project, depth sort [k_radix_hist, k_radix_hist_scan,
+    4 x k_onesweep], k_fix_short_runs, k_fix_long_runs, k_pair_count,
+    k_duplicate (also counts the tile-sort digits), tile sort
+    [k_radix_hist_scan, 2 x k_onesweep], k_tile_ranges, k_tile_order, k_blend."""
+    return 1 + 1 + (1 + 1 + 4) + 2 + 1 + 1 + (1 + 2) + 1 + 1 + 1
 
 
 def host_scene(scene):
