@@ -416,14 +416,16 @@ def main():
                 "frac": achieved / hbm_peak, "traffic": traffic,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "B200_PROFILING.md fallback"}
     else:  # blend: float64-pipe bound (quadratic form per evaluation, exp + alpha/T per fragment)
-        sm_mhz = clocks.get("sm_mhz") or 1965.0
-        fp64_peak = 148 * 64 * 2 * sm_mhz * 1e6 / 1e12  # TFLOP/s: 148 SM x 64 DFMA/clk x 2 at the sampled clock
+        # measured on this box: DFMA chains on every SM (cs_measure_fp64_peak)
+        pk = ctypes.c_double(0.0)
+        _lib.check(lib.cs_measure_fp64_peak(ctx, ctypes.byref(pk), sh), "cs_measure_fp64_peak")
+        fp64_peak = pk.value
         achieved = blend_flops(counts) / K / (stages_ms[dom] / 1000.0) / 1e12
         traffic, tsrc = ncu_traffic("k_blend")
         roof = {"kernel": "k_blend", "bound": "fp64", "achieved": achieved, "peak": fp64_peak,
                 "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": traffic,
-                "peak_source": "148 SM x 64 FP64 FMA/clk x 2 at the sampled SM clock (no FP64 entry in "
-                               "MEASURED_PEAKS.json)",
+                "peak_source": "measured in this run: dense DFMA chains on every SM, CUDA events "
+                               "(cs_measure_fp64_peak; MEASURED_PEAKS.json has no FP64 entry)",
                 "flops_per_frame": blend_flops(counts) / K}
     roof["traffic_source"] = f"profiles/{tsrc} (ncu --set full, dram__bytes_read+write per launch)" if tsrc else None
     # the blend is issue-bound (divergent per-pixel termination), not FP64-pipe-bound:

@@ -324,6 +324,12 @@ int cs_bounds_contain(cs_ctx* ctx, int64_t n, const void* positions, int32_t f32
 int cs_ssim(cs_ctx* ctx, const float* img_a, const float* img_b, int32_t height, int32_t width,
             const double* window, double* acc4, void* stream);
 
+/* ---- measurement --------------------------------------------------------------
+ * Dense DFMA throughput of this device (TFLOP/s, 2 flops per DFMA), measured
+ * with CUDA events: the FP64 roofline denominator of the blend.
+ * Synchronises `stream`. */
+int cs_measure_fp64_peak(cs_ctx* ctx, double* tflops, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

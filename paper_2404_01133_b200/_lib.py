@@ -118,6 +118,7 @@ _SIGS = {
     "cs_gather_cloud": (ctypes.c_int, [vp, ctypes.POINTER(CsCloud), vp, i64, ctypes.POINTER(CsCloud), vp]),
     "cs_bounds_contain": (ctypes.c_int, [vp, i64, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp]),
     "cs_ssim": (ctypes.c_int, [vp, vp, vp, i32, i32, vp, vp, vp]),
+    "cs_measure_fp64_peak": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_double), vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -125,6 +125,7 @@ void launch_bounds_contain(int64_t n, const void* pos, int f32, int stride, cons
                            unsigned long long* count, cudaStream_t s);
 cudaError_t ssim_run(const float* a, const float* b, int H, int W, const double* window,
                      double* acc4, cudaStream_t s);
+cudaError_t fp64_peak_run(double* tflops, cudaStream_t s);
 }  // namespace cs
 
 using namespace cs;
@@ -1109,6 +1110,13 @@ int cs_ssim(cs_ctx* c, const float* img_a, const float* img_b, int32_t height, i
   if (height < 11 || width < 11) return fail(CS_EINVAL, "images must be at least 11x11 for ssim");
   CS_CUDA(cudaSetDevice(c->device));
   CS_CUDA(ssim_run(img_a, img_b, height, width, window, acc4, (cudaStream_t)stream));
+  return CS_OK;
+}
+
+int cs_measure_fp64_peak(cs_ctx* c, double* tflops, void* stream) {
+  if (!c || !tflops) return fail(CS_EINVAL, "NULL argument");
+  CS_CUDA(cudaSetDevice(c->device));
+  CS_CUDA(fp64_peak_run(tflops, (cudaStream_t)stream));
   return CS_OK;
 }
 

@@ -104,3 +104,48 @@ cudaError_t ssim_run(const float* a, const float* b, int H, int W, const double*
 }
 
 }  // namespace cs
+
+namespace cs {
+
+// FP64 peak microbenchmark (the blend's roofline denominator is
+// measured on the box): every thread runs 8 independent DFMA chains.
+__global__ void __launch_bounds__(256) k_dfma_peak(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = (double)(threadIdx.x + i) * 1e-9;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = fma(x[i], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+
+cudaError_t fp64_peak_run(double* tflops, cudaStream_t s) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* out = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&out), sizeof(double), s);
+  if (e) return e;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = sms * 8, iters = 4096;
+  k_dfma_peak<<<blocks, 256, 0, s>>>(out, 64, 1.0000001, 1e-12);  // warm-up
+  cudaEventRecord(e0, s);
+  k_dfma_peak<<<blocks, 256, 0, s>>>(out, iters, 1.0000001, 1e-12);
+  cudaEventRecord(e1, s);
+  e = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  *tflops = 2.0 * 8.0 * iters * (double)blocks * 256.0 / (ms * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFreeAsync(out, s);
+  return e ? e : cudaGetLastError();
+}
+
+}  // namespace cs
