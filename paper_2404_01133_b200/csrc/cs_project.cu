@@ -307,12 +307,14 @@ k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
   const int64_t i = blockIdx.x * (int64_t)kProjThreads + threadIdx.x;
   const int64_t cta0 = blockIdx.x * (int64_t)kProjThreads;
   if (cta0 >= n) return;  // CTA-uniform
-  // the segments of the CTA's first and last index bound every thread's
-  // search (a CTA's 256 indices nearly always fall in one or two pieces)
-  __shared__ int s_seg[2];
+  // segment starts staged in shared memory (one coalesced load; n_segs <= L*J
+  // is small), so the per-thread search costs no dependent global loads
+  constexpr int kSmemSegs = 512;
+  __shared__ int64_t s_start[kSmemSegs];
   const int n_segs = stats->n_segs;
-  if (threadIdx.x < 2)
-    s_seg[threadIdx.x] = find_seg(segs, n_segs, threadIdx.x ? min(cta0 + kProjThreads, n) - 1 : cta0);
+  const bool smem_segs = n_segs <= kSmemSegs;
+  if (smem_segs)
+    for (int q = threadIdx.x; q < n_segs; q += kProjThreads) s_start[q] = segs[q].start;
   __syncthreads();
   ProjOut po;
   po.in_front = po.ok = po.keep = false;
@@ -320,7 +322,16 @@ k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
   int64_t local = 0;
   int cloud_id = 0;
   if (i < n) {
-    const int si = find_seg(segs, n_segs, i, s_seg[0], s_seg[1]);
+    int si = 0;
+    if (smem_segs) {
+      int hi = n_segs - 1;
+      while (si < hi) {
+        const int mid = (si + hi + 1) >> 1;
+        if (s_start[mid] <= i) si = mid; else hi = mid - 1;
+      }
+    } else {
+      si = find_seg(segs, n_segs, i);
+    }
     const Seg sg = segs[si];
     cloud_id = sg.cloud;
     local = i - sg.start;
