@@ -63,6 +63,7 @@ def parse():
     ap.add_argument("--no-train", action="store_true", help="skip the block-training leg (C4)")
     ap.add_argument("--no-assign", action="store_true", help="skip the data-assignment leg (f2)")
     ap.add_argument("--assign-poses", type=int, default=4)
+    ap.add_argument("--no-c5", action="store_true", help="skip the 740-test-view batch render (C5)")
     ap.add_argument("--train-steps", type=int, default=72, help="timed block iterations per rank")
     ap.add_argument("--train-warmup", type=int, default=36)
     ap.add_argument("--train-views", type=int, default=4)
@@ -433,6 +434,41 @@ def main():
     roof["ncu_pipes_pct"] = ncu_pipes("k_blend")
     roof["stages_hbm"] = stage_roof
 
+    # C5: batch render of the 740 test views of a 5920-camera set (every 8th,
+    # colmap.py:152-156) on the same LoD scene, view-split across ranks
+    c5 = None
+    if not args.no_c5:
+        from paper_2404_01133_b200.synth import city_cameras
+        all5 = city_cameras(5920, SCENES[args.scene][1], wh[0], wh[1], seed=args.seed)
+        test5 = [c for i, c in enumerate(all5) if i % 8 == 0]
+        mine = [test5[i] for i in range(len(test5)) if i * world // len(test5) == rank]
+        c5cams = [device.camera_struct(c) for c in mine]
+
+        def frame5(c, flags=0):
+            _lib.check(lib.cs_render(ctx, ctypes.byref(src), ctypes.byref(c), ctypes.byref(cset),
+                                     out.data_ptr(), flags, None, sh), "cs_render")
+
+        for c in c5cams:  # sizing pass (synchronous: pair buffers grow to the largest view)
+            frame5(c, _lib.CS_RENDER_SYNC)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for c in c5cams:
+            frame5(c)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        t5 = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t5, op=dist.ReduceOp.MAX)
+        c5 = {"metric": "C5 batch render FPS (740 test views, 1080p, LoD, view-split)",
+              "value": len(test5) / (float(t5.item()) / 1000.0), "unit": "frames/s",
+              "views": len(test5), "views_this_rank": len(mine), "n_gpus": world,
+              "ms_max_rank": float(t5.item()), "scaling": "weak in views per rank" if world > 1 else "n/a"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(scene, cams_all, settings, n_frames=1)
@@ -470,6 +506,7 @@ def main():
             "e2e": e2e,
             "train": train,
             "lod_build": LOD_BUILD,
+            "c5": c5,
             "lod_broadcast_ms": lod_bcast_ms,
             "assign": assign,
             "gpu_launches": K * launches_per_frame(),
