@@ -188,14 +188,14 @@ def stage_bytes(st: dict) -> dict:
     na, m, p = st["assembled"], st["visible"], st["pairs"]
     return {
         # per assembled: 3 fp32 quads (48 B) + depth keys (8 + 4) + id (4);
-        # per visible: its SH row (level width) + HotRec 80 + rect 16 + cull box 8
-        "project": na * (48 + 16) + st["sh_bytes_visible"] + m * (80 + 16 + 8),
+        # per visible: its SH row (level width) + HotRec 64 + rect 8 + cull box 8
+        "project": na * (48 + 16) + st["sh_bytes_visible"] + m * (64 + 8 + 8),
         # 4 LSD passes over (u32 key, u32 id) + one histogram read + run check
         "depth_sort": na * 4 + 4 * 2 * na * 8 + m * 4,
-        # per visible: id + rect gather + pair offset write
-        "gather_scan": m * (4 + 16 + 8),
-        # per pair: (tile, id) written; per visible: offset, id, rect staged
-        "duplicate": p * 8 + m * 28,
+        # fused K5+K6: per visible id + rect gather (8); per pair (tile, id) written
+        "gather_scan": m * (4 + 8) + p * 8,
+        # (folded into gather_scan: the stage boundary remains, ~0 ms)
+        "duplicate": 0,
         # 2 LSD passes over (u32 tile, u32 id) + one histogram read
         "tile_sort": p * 4 + 2 * 2 * p * 8,
         # per pair: key + id read, cull box gathered (8) and written pair-major (8)
@@ -411,8 +411,8 @@ def main():
     if dom in bytes_:
         achieved = stage_roof[dom]["achieved_gbs"]
         traffic, tsrc = ncu_traffic({"project": "k_project", "depth_sort": "k_onesweep",
-                                     "tile_sort": "k_onesweep", "duplicate": "k_duplicate",
-                                     "gather_scan": "k_pair_count", "ranges": "k_tile_ranges"}[dom])
+                                     "tile_sort": "k_onesweep", "duplicate": "k_bin_pairs",
+                                     "gather_scan": "k_bin_pairs", "ranges": "k_tile_ranges"}[dom])
         roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": traffic,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "B200_PROFILING.md fallback"}
@@ -647,12 +647,11 @@ def train_leg(args, raw, wh, rank, world, dev):
 
 def launches_per_frame() -> int:
     """Kernels of one C3 frame (memsets excluded), as listed by the ncu launch
-    capture (profiles/r1ab_launches.csv: 72 launches over 4 frames):
-    k_lod_select, k_project, depth sort [k_radix_hist, k_radix_hist_scan,
-    4 x k_onesweep], k_fix_short_runs, k_fix_long_runs, k_pair_count,
-    k_duplicate (also counts the tile-sort digits), tile sort
+    capture: k_lod_select, k_project, depth sort [k_radix_hist,
+    k_radix_hist_scan, 4 x k_onesweep], k_fix_short_runs, k_fix_long_runs,
+    (fused) k_bin_pairs (also counts the tile-sort digits), tile sort
     [k_radix_hist_scan, 2 x k_onesweep], k_tile_ranges, k_tile_order, k_blend."""
-    return 1 + 1 + (1 + 1 + 4) + 2 + 1 + 1 + (1 + 2) + 1 + 1 + 1
+    return 1 + 1 + (1 + 1 + 4) + 2 + 1 + (1 + 2) + 1 + 1 + 1
 
 
 def host_scene(scene):

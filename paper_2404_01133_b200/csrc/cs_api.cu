@@ -63,14 +63,12 @@ void launch_block_adam(int64_t K, int C, float* geom, float* gm, float* gv, floa
 void launch_activate_geom(int64_t K, const float* geom, float4* pos_op, float4* scale, float4* quat,
                           cudaStream_t s);
 // cs_bin.cu
-int64_t pair_count_chunks(int64_t capacity);
-int64_t dup_blocks(int64_t pair_cap);
-void launch_pair_count(const uint32_t* order, const uint2* rects, DevStats* stats, int64_t pair_cap,
-                       int64_t capacity, uint64_t* status, uint32_t* pair_off, uint32_t* dup_start,
-                       cudaStream_t s);
-void launch_duplicate(const uint32_t* pair_off, const uint32_t* order, const uint2* rects,
-                      const uint32_t* dup_start, const DevStats* stats, int ntx, int64_t pair_cap,
-                      uint32_t* keys, uint32_t* vals, uint32_t* hist, int key_bits, cudaStream_t s);
+int64_t bin_chunks(int64_t capacity);
+void launch_bin_pairs(const uint32_t* order, const uint2* rects, DevStats* stats, int64_t pair_cap,
+                      int64_t capacity, uint64_t* status, int ntx, uint32_t* keys, uint32_t* vals,
+                      uint32_t* hist, int key_bits, bool emit, cudaStream_t s);
+
+
 void launch_tile_ranges(const uint32_t* keys, const uint32_t* vals, const short4* boxes,
                         const DevStats* stats, uint2* ranges, uint32_t* bxs, uint32_t* bys,
                         cudaStream_t s);
@@ -207,12 +205,11 @@ struct cs_ctx {
   DBuf st_gather, st_pw, st_fuse, st_sort, hist, sort_tickets, fuse_ticket;
   DBuf keysA, valsA, keysB, valsB, recs;
   DBuf k32A, k32B, long_runs, fix_ctl;          // K4 32-bit depth sort + K4b run fix-up
-  DBuf hot, boxes, rects, pair_off, tile_order;
+  DBuf hot, boxes, rects, tile_order;
   DBuf pkA, pvA, pkB, pvB, ranges, frag_tile, pw_list;
   DBuf st_t, st_last, st_acc;
   DBuf scratch1, scratch2, scratch3, scratch4;  // API utilities
   DBuf gacc;                                    // per-rank blend-backward partials
-  DBuf dup_start;                               // K5 -> K6: first depth rank of each duplication CTA
   DBuf loss_maps, loss_acc;                     // cs_training_loss workspace
   cs_frame_stats* h_stats = nullptr;            // pinned
   int64_t cap_vis = 0, cap_pairs = 0, cap_pw = 0, cap_tiles = 0;
@@ -274,9 +271,9 @@ void cs_destroy(cs_ctx* c) {
                  &c->st_pw, &c->st_fuse, &c->st_sort, &c->hist, &c->sort_tickets,
                  &c->fuse_ticket, &c->keysA, &c->valsA, &c->keysB, &c->valsB, &c->recs, &c->k32A, &c->k32B,
                  &c->long_runs, &c->fix_ctl, &c->hot,
-                 &c->tile_order, &c->boxes, &c->rects, &c->pair_off, &c->pkA, &c->pvA, &c->pkB,
+                 &c->tile_order, &c->boxes, &c->rects, &c->pkA, &c->pvA, &c->pkB,
                  &c->pvB, &c->ranges, &c->frag_tile, &c->pw_list, &c->st_t, &c->st_last,
-                 &c->st_acc, &c->gacc, &c->dup_start, &c->loss_maps, &c->loss_acc, &c->scratch1, &c->scratch2, &c->scratch3, &c->scratch4};
+                 &c->st_acc, &c->gacc, &c->loss_maps, &c->loss_acc, &c->scratch1, &c->scratch2, &c->scratch3, &c->scratch4};
   for (DBuf* b : all) b->release();
   if (c->h_stats) cudaFreeHost(c->h_stats);
   for (cudaEvent_t e : c->tev) cudaEventDestroy(e);
@@ -359,16 +356,14 @@ static int ensure_frame_buffers(cs_ctx* c, int64_t cap_vis, int n_segs, int n_bl
         c->k32A.ensure(4 * cap) || c->k32B.ensure(4 * cap) ||
         c->long_runs.ensure(4 * fix_long_cap(cap)) || c->fix_ctl.ensure(fix_ctl_bytes()) ||
         c->valsB.ensure(4 * cap) || c->hot.ensure(sizeof(HotRec) * cap) ||
-        c->rects.ensure(8 * cap) || c->boxes.ensure(8 * cap) ||
-        c->pair_off.ensure(4 * cap))
+        c->rects.ensure(8 * cap) || c->boxes.ensure(8 * cap))
       return fail(CS_ENOMEM, "visible-splat buffers (%lld)", (long long)cap);
     c->cap_vis = cap;
   }
   if (c->cap_pairs == 0) c->cap_pairs = std::max<int64_t>(1 << 20, 8 * c->cap_vis);
   if (c->cap_pairs >= (1ll << 30)) c->cap_pairs = (1ll << 30) - 1;
   if (c->pkA.ensure(4 * c->cap_pairs) || c->pvA.ensure(4 * c->cap_pairs) ||
-      c->pkB.ensure(4 * c->cap_pairs) || c->pvB.ensure(4 * c->cap_pairs) ||
-      c->dup_start.ensure(4 * (dup_blocks(c->cap_pairs) + 1)))
+      c->pkB.ensure(4 * c->cap_pairs) || c->pvB.ensure(4 * c->cap_pairs))
     return fail(CS_ENOMEM, "pair buffers (%lld)", (long long)c->cap_pairs);
   const size_t sw = std::max(radix_status_words(c->cap_vis, 8), radix_status_words(c->cap_pairs, 4));
   if (c->st_sort.ensure(4 * sw)) return fail(CS_ENOMEM, "sort status");
@@ -492,25 +487,22 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
                         c->keysB.as<uint32_t>(), s);
   CS_CHECK_LAUNCH();
   if (timed) mark(c, 3, s);
-  // K5: pair counts in depth order, scanned
-  CS_CUDA(cudaMemsetAsync(c->st_gather.p, 0, 8 * (pair_count_chunks(cap) + 1), s));
-  launch_pair_count(order, c->rects.as<uint2>(), stats, c->cap_pairs, cap,
-                    c->st_gather.as<uint64_t>(), c->pair_off.as<uint32_t>(),
-                    c->dup_start.as<uint32_t>(), s);
+  // K5+K6: pair counts in depth order, scanned, and the pairs emitted in one
+  // pass (also counts the tile sort's digit histograms, so K7 skips its
+  // counting pass)
+  CS_CUDA(cudaMemsetAsync(c->st_gather.p, 0, 8 * (bin_chunks(cap) + 1), s));
+  const bool project_only = (flags & CS_RENDER_PROJECT_ONLY) != 0;
+  launch_bin_pairs(order, c->rects.as<uint2>(), stats, c->cap_pairs, cap,
+                   c->st_gather.as<uint64_t>(), ntx, c->pkA.as<uint32_t>(), c->pvA.as<uint32_t>(),
+                   bits_for(n_tiles) <= 24 ? c->hist.as<uint32_t>() : nullptr, bits_for(n_tiles),
+                   !project_only, s);
   CS_CHECK_LAUNCH();
   if (timed) mark(c, 4, s);
-  if (flags & CS_RENDER_PROJECT_ONLY) {
+  if (project_only) {
     c->last_order = order;
     c->last_list = nullptr;
     return CS_OK;
   }
-  // K6: duplicate
-  // (also counts the tile sort's digit histograms, so K7 skips its counting pass)
-  launch_duplicate(c->pair_off.as<uint32_t>(), order, c->rects.as<uint2>(),
-                   c->dup_start.as<uint32_t>(), stats, ntx,
-                   c->cap_pairs, c->pkA.as<uint32_t>(), c->pvA.as<uint32_t>(),
-                   bits_for(n_tiles) <= 24 ? c->hist.as<uint32_t>() : nullptr, bits_for(n_tiles), s);
-  CS_CHECK_LAUNCH();
   mark(c, 5, s);
   // K7: stable sort by tile id only (ceil(log2 T) bits)
   const int which2 = radix_sort<uint32_t>(c->pkA.as<uint32_t>(), c->pvA.as<uint32_t>(),

@@ -1,5 +1,5 @@
-// cs_bin.cu -- K5/K6/K8: pair-count scan in depth order, pair duplication and
-// tile ranges.  Replaces render._bin_tiles (render.py:217-249).
+// cs_bin.cu -- K5/K6 (fused) and K8: pair counts in depth order, pair
+// duplication and tile ranges.  Replaces render._bin_tiles (render.py:217-249).
 //
 // The tile rectangles were computed by the projection (render.py:226-231);
 // here only the depth permutation is applied: pairs are emitted in depth-rank
@@ -11,106 +11,11 @@
 
 namespace cs {
 
-constexpr int kCountThreads = 256;
-#ifndef CS_COUNT_ITEMS
-#define CS_COUNT_ITEMS 16
-#endif
-#ifndef CS_COUNT_MINB
-#define CS_COUNT_MINB 1
-#endif
-constexpr int kCountItems = CS_COUNT_ITEMS;            // ranks per thread
-constexpr int kCountTile = kCountThreads * kCountItems;  // ranks per chunk
-constexpr int kDupTile = 1024;                         // pairs per duplication CTA
-
-// pair_off[r] = sum of pair counts of depth ranks < r (single pass: chunks of
-// 4096 ranks, warp-striped so every load is coalesced, decoupled look-back
-// across chunks).  Also records, for every duplication CTA b, the depth rank
-// owning pair b*kDupTile (dup_start[b]), so K6 needs no global binary search.
-__global__ void __launch_bounds__(kCountThreads, CS_COUNT_MINB)
-k_pair_count(const uint32_t* __restrict__ order, const uint2* __restrict__ rects,
-             DevStats* __restrict__ stats, int64_t pair_cap, uint64_t* __restrict__ status,
-             uint32_t* __restrict__ pair_off, uint32_t* __restrict__ dup_start) {
-  __shared__ int64_t s_chunk;
-  __shared__ uint64_t s_scan[kCountThreads / 32 + 1];
-  __shared__ uint64_t s_prefix;
-  const int64_t M = stats->visible;
-  if (threadIdx.x == 0) s_chunk = atomicAdd(&stats->tickets[2], 1u);
-  __syncthreads();
-  const int64_t chunk = s_chunk;
-  const int64_t base = chunk * kCountTile;
-  if (base >= M) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t wbase = base + (int64_t)warp * (32 * kCountItems);
-  // per rank count (<= n_tiles) and its exclusive offset inside the chunk:
-  // 32-bit (a chunk holds <= 4096 x 2^16 pairs), 64-bit only across chunks
-  uint32_t cnt[kCountItems], c32[kCountItems];
-  const bool full = base + kCountTile <= M;  // CTA-uniform
-#pragma unroll
-  for (int i = 0; i < kCountItems; ++i) {
-    const int64_t r = wbase + i * 32 + lane;
-    c32[i] = 0;
-    if (full || r < M) {
-      const int4 rc = unpack_rect(__ldg(rects + __ldg(order + r)));
-      c32[i] = (uint32_t)((rc.y - rc.x + 1) * (rc.w - rc.z + 1));
-    }
-  }
-  // warp-local exclusive offsets over the warp's 512 consecutive ranks
-  uint32_t run = 0;
-#pragma unroll
-  for (int i = 0; i < kCountItems; ++i) {
-    const uint32_t incl = warp_incl_scan(c32[i]);
-    cnt[i] = run + incl - c32[i];  // exclusive offset within the warp
-    run += __shfl_sync(0xffffffffu, incl, 31);
-  }
-  // warp totals -> block-exclusive warp offsets
-  if (lane == 0) s_scan[warp] = run;
-  __syncthreads();
-  if (warp == 0) {
-    const uint64_t w = lane < kCountThreads / 32 ? s_scan[lane] : 0ull;
-    const uint64_t wi = warp_incl_scan(w);
-    if (lane < kCountThreads / 32) s_scan[lane] = wi - w;
-    if (lane == 31) s_scan[kCountThreads / 32] = wi;
-  }
-  __syncthreads();
-  const uint64_t total = s_scan[kCountThreads / 32];
-  if (threadIdx.x < 32) {
-    const uint64_t pre = lookback_exclusive(status, chunk, total);
-    if (threadIdx.x == 0) {
-      s_prefix = pre;
-      if (base + kCountTile >= M) {
-        const int64_t P = (int64_t)(pre + total);
-        stats->pairs = P;
-        stats->pairs_eff = P <= pair_cap ? P : 0;
-        if (P > pair_cap) atomicOr(&stats->status, 1);
-      }
-    }
-  }
-  __syncthreads();
-  const uint64_t off0 = s_prefix + s_scan[warp];
-#pragma unroll
-  for (int i = 0; i < kCountItems; ++i) {
-    const int64_t r = wbase + i * 32 + lane;
-    if (r >= M) break;
-    const int64_t o = (int64_t)(off0 + cnt[i]);
-    pair_off[r] = (uint32_t)o;  // read by K6 only when P <= pair_cap < 2^30
-    // duplication CTAs whose first pair lies in [o, o + count)
-    const int64_t c = c32[i];
-    if (o + c <= pair_cap) {
-      for (int64_t b = (o + kDupTile - 1) / kDupTile; b * kDupTile < o + c; ++b) dup_start[b] = (uint32_t)r;
-    }
-  }
-}
-
-constexpr int kDupThreads = 256;
-static_assert(kDupTile == 4 * kDupThreads, "k_duplicate emits 4 pairs per thread");
-
-// Load-balanced duplication: each CTA owns kDupTile consecutive output pairs;
-// the depth ranks whose pair ranges intersect it (dup_start[b] ..
-// dup_start[b+1], from K5) are staged in shared memory.  Each thread emits 4
-// consecutive pairs: one binary search for its first pair's rank, then a
-// sequential walk over the rect row-major (render.py:233-243) and on to the
-// next rank, and two 16-byte stores.  key = tile id, value = splat id.
-constexpr int kDupItems = kDupTile / kDupThreads;  // 4
+// Each thread emits 4 consecutive pairs: one binary search in shared memory for
+// its first pair's rank, then a sequential walk over the rect row-major
+// (render.py:233-243) and on to the next rank, and two 16-byte stores.
+// key = tile id, value = splat id.
+constexpr int kDupItems = 4;
 constexpr int kMaxHistPasses = 3;
 
 // Digit histograms of the tile sort that follows (equal-width digits, as
@@ -121,16 +26,17 @@ struct DigitHist {
 };
 
 __device__ __forceinline__ void emit_pairs(uint32_t p, uint32_t p1, int nr, const uint32_t* s_off,
-                                           const int4* s_rect, const uint32_t* s_id, int ntx,
+                                           const uint2* s_rect, const uint32_t* s_id, int ntx,
                                            uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                                           const DigitHist& dh, uint32_t (*s_hist)[256]) {
+                                           const DigitHist& dh, uint32_t (*s_hist)[256],
+                                           uint64_t out_base = 0) {
   // 32-bit throughout: pairs < 2^30 (pair_cap), a rank owns <= n_tiles pairs
   int lo = 0, hi = nr - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
     if (s_off[mid] <= p) lo = mid; else hi = mid - 1;
   }
-  int4 rc = s_rect[lo];
+  int4 rc = unpack_rect(s_rect[lo]);
   int w = rc.y - rc.x + 1;
   const int local = (int)(p - s_off[lo]);
   int ly = local / w, lx = local - ly * w;
@@ -142,7 +48,7 @@ __device__ __forceinline__ void emit_pairs(uint32_t p, uint32_t p1, int nr, cons
     v[j] = s_id[lo];
     if (p + j + 1 == next) {  // next rank starts at its first tile
       ++lo;
-      rc = s_rect[lo];
+      rc = unpack_rect(s_rect[lo]);
       w = rc.y - rc.x + 1;
       lx = ly = 0;
       next = s_off[lo + 1];
@@ -151,13 +57,14 @@ __device__ __forceinline__ void emit_pairs(uint32_t p, uint32_t p1, int nr, cons
       ++ly;
     }
   }
-  if (p + kDupItems <= p1) {
-    *reinterpret_cast<uint4*>(keys + p) = make_uint4(k[0], k[1], k[2], k[3]);
-    *reinterpret_cast<uint4*>(vals + p) = make_uint4(v[0], v[1], v[2], v[3]);
+  const uint64_t o = out_base + p;
+  if (p + kDupItems <= p1 && (o & 3) == 0) {
+    *reinterpret_cast<uint4*>(keys + o) = make_uint4(k[0], k[1], k[2], k[3]);
+    *reinterpret_cast<uint4*>(vals + o) = make_uint4(v[0], v[1], v[2], v[3]);
   } else {
 #pragma unroll
     for (int j = 0; j < kDupItems; ++j)
-      if (p + j < p1) { keys[p + j] = k[j]; vals[p + j] = v[j]; }
+      if (p + j < p1) { keys[o + j] = k[j]; vals[o + j] = v[j]; }
   }
 #pragma unroll
   for (int j = 0; j < kDupItems; ++j)
@@ -166,42 +73,94 @@ __device__ __forceinline__ void emit_pairs(uint32_t p, uint32_t p1, int nr, cons
         atomicAdd(&s_hist[q][(k[j] >> (dh.width * q)) & ((1u << min(dh.width, dh.end_bit - dh.width * q)) - 1u)], 1u);
 }
 
-__global__ void __launch_bounds__(kDupThreads)
-k_duplicate(const uint32_t* __restrict__ pair_off, const uint32_t* __restrict__ order,
-            const uint2* __restrict__ rects, const uint32_t* __restrict__ dup_start,
-            const DevStats* __restrict__ stats, int ntx, uint32_t* __restrict__ keys,
-            uint32_t* __restrict__ vals, DigitHist dh) {
-  __shared__ uint32_t s_off[kDupTile + 2];
-  __shared__ int4 s_rect[kDupTile + 1];
-  __shared__ uint32_t s_id[kDupTile + 1];
+// K5+K6 fused: per chunk of 2048 depth ranks (warp-striped, coalesced), the
+// tile rectangles are gathered once into shared memory, the pair counts
+// scanned (block scan + decoupled look-back across chunks), and the chunk's
+// pairs emitted right away -- four per thread, owner rank by binary search in
+// shared memory, row-major over each rect (render.py:233-243) -- together
+// with the tile sort's digit histograms.  emit = false (projection-only
+// renders) stops after the count.
+constexpr int kBinThreads = 256;
+constexpr int kBinItems = 8;
+constexpr int kBinRanks = kBinThreads * kBinItems;
+
+__global__ void __launch_bounds__(kBinThreads)
+k_bin_pairs(const uint32_t* __restrict__ order, const uint2* __restrict__ rects,
+            DevStats* __restrict__ stats, int64_t pair_cap, uint64_t* __restrict__ status,
+            int ntx, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, DigitHist dh,
+            int emit) {
+  __shared__ uint32_t s_off[kBinRanks + 1];
+  __shared__ uint2 s_rect[kBinRanks];
+  __shared__ uint32_t s_id[kBinRanks];
   __shared__ uint32_t s_hist[kMaxHistPasses][256];
-  const int64_t P = stats->pairs_eff;
+  __shared__ uint32_t s_scan[kBinThreads / 32 + 1];
+  __shared__ uint64_t s_prefix;
+  __shared__ uint32_t s_chunk;
   const int64_t M = stats->visible;
-  const int64_t p0 = (int64_t)blockIdx.x * kDupTile;
-  if (p0 >= P) return;  // CTA-uniform
-  for (int i = threadIdx.x; i < dh.n_passes * 256; i += kDupThreads) s_hist[i >> 8][i & 255] = 0;
-  const int64_t p1 = min(p0 + kDupTile, P);
-  const int64_t rlo = dup_start[blockIdx.x];
-  const int64_t rhi = p1 < P ? (int64_t)dup_start[blockIdx.x + 1] : M - 1;  // owner of pair p1 (>= owner of p1-1)
-  const int nr = (int)(rhi - rlo + 1);
-  for (int i = threadIdx.x; i < nr; i += kDupThreads) {
-    const uint32_t v = __ldg(order + rlo + i);
-    s_off[i] = pair_off[rlo + i];
-    s_rect[i] = unpack_rect(__ldg(rects + v));
-    s_id[i] = v;
+  if (threadIdx.x == 0) s_chunk = atomicAdd(&stats->tickets[2], 1u);
+  for (int i = threadIdx.x; i < dh.n_passes * 256; i += kBinThreads) s_hist[i >> 8][i & 255] = 0;
+  __syncthreads();
+  const int64_t chunk = s_chunk;
+  const int64_t base = chunk * kBinRanks;
+  if (base >= M) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nr = (int)min((int64_t)kBinRanks, M - base);
+  uint32_t cnt[kBinItems], run = 0;
+#pragma unroll
+  for (int i = 0; i < kBinItems; ++i) {
+    const int li = warp * (32 * kBinItems) + i * 32 + lane;  // chunk-local rank
+    uint32_t c = 0;
+    if (li < nr) {
+      const uint32_t id = __ldg(order + base + li);
+      const uint2 pr = __ldg(rects + id);
+      const int4 rc = unpack_rect(pr);
+      s_rect[li] = pr;
+      s_id[li] = id;
+      c = (uint32_t)((rc.y - rc.x + 1) * (rc.w - rc.z + 1));
+    }
+    const uint32_t incl = warp_incl_scan(c);
+    cnt[i] = run + incl - c;  // exclusive offset inside the warp's 256 ranks
+    run += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (lane == 0) s_scan[warp] = run;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t w = lane < kBinThreads / 32 ? s_scan[lane] : 0u;
+    const uint32_t wi = warp_incl_scan(w);
+    if (lane < kBinThreads / 32) s_scan[lane] = wi - w;
+    if (lane == 31) s_scan[kBinThreads / 32] = wi;
+  }
+  __syncthreads();
+  const uint32_t total = s_scan[kBinThreads / 32];  // <= 2048 x 2^16 pairs
+  if (threadIdx.x < 32) {
+    const uint64_t pre = lookback_exclusive(status, chunk, total);
+    if (threadIdx.x == 0) {
+      s_prefix = pre;
+      if (base + kBinRanks >= M) {
+        const int64_t P = (int64_t)(pre + total);
+        stats->pairs = P;
+        stats->pairs_eff = P <= pair_cap ? P : 0;
+        if (P > pair_cap) atomicOr(&stats->status, 1);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kBinItems; ++i) {
+    const int li = warp * (32 * kBinItems) + i * 32 + lane;
+    if (li < nr) s_off[li] = s_scan[warp] + cnt[i];
   }
   if (threadIdx.x == 0) s_off[nr] = 0xffffffffu;  // sentinel: every rank owns >= 1 pair
   __syncthreads();
-  const uint32_t p = (uint32_t)p0 + threadIdx.x * kDupItems;
-  if (p < p1) emit_pairs(p, (uint32_t)p1, nr, s_off, s_rect, s_id, ntx, keys, vals, dh, s_hist);
+  const uint64_t prefix = s_prefix;
+  if (!emit || prefix + total > (uint64_t)pair_cap) return;  // overflow: the SYNC path re-renders
+  for (uint32_t q = threadIdx.x * kDupItems; q < total; q += kBinThreads * kDupItems)
+    emit_pairs(q, total, nr, s_off, s_rect, s_id, ntx, keys, vals, dh, s_hist, prefix);
   __syncthreads();
-  // the tile sort's digit histograms (K7 skips its counting pass)
-  for (int i = threadIdx.x; i < dh.n_passes * 256; i += kDupThreads) {
+  for (int i = threadIdx.x; i < dh.n_passes * 256; i += kBinThreads) {
     const uint32_t c = s_hist[i >> 8][i & 255];
     if (c) atomicAdd(dh.hist + i, c);
   }
 }
-
 
 // CSR tile ranges from the tile-sorted keys (render.py:247-248), and the
 // pair-major cull boxes the blend tests (boxes[vals[p]] split into one u32 per
@@ -255,31 +214,21 @@ __global__ void k_tile_ranges(const uint32_t* __restrict__ keys, const uint32_t*
   }
 }
 
-int64_t pair_count_chunks(int64_t capacity) { return (capacity + kCountTile - 1) / kCountTile; }
-int64_t dup_blocks(int64_t pair_cap) { return (pair_cap + kDupTile - 1) / kDupTile; }
+int64_t bin_chunks(int64_t capacity) { return (capacity + kBinRanks - 1) / kBinRanks; }
 
-void launch_pair_count(const uint32_t* order, const uint2* rects, DevStats* stats, int64_t pair_cap,
-                       int64_t capacity, uint64_t* status, uint32_t* pair_off, uint32_t* dup_start,
-                       cudaStream_t s) {
-  const int64_t chunks = pair_count_chunks(capacity);
+void launch_bin_pairs(const uint32_t* order, const uint2* rects, DevStats* stats, int64_t pair_cap,
+                      int64_t capacity, uint64_t* status, int ntx, uint32_t* keys, uint32_t* vals,
+                      uint32_t* hist, int key_bits, bool emit, cudaStream_t s) {
+  const int64_t chunks = bin_chunks(capacity);
   if (chunks == 0) return;
-  k_pair_count<<<(unsigned)chunks, kCountThreads, 0, s>>>(order, rects, stats, pair_cap, status,
-                                                          pair_off, dup_start);
-}
-
-void launch_duplicate(const uint32_t* pair_off, const uint32_t* order, const uint2* rects,
-                      const uint32_t* dup_start, const DevStats* stats, int ntx, int64_t pair_cap,
-                      uint32_t* keys, uint32_t* vals, uint32_t* hist, int key_bits, cudaStream_t s) {
-  const int64_t blocks = dup_blocks(pair_cap);
-  if (blocks == 0) return;
   DigitHist dh;  // hist == nullptr (keys wider than kMaxHistPasses digits): no counting
   dh.hist = hist;
   dh.n_passes = hist ? (key_bits + 7) / 8 : 0;
   dh.width = dh.n_passes ? (key_bits + dh.n_passes - 1) / dh.n_passes : 8;
   dh.end_bit = key_bits;
   if (hist) cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 256 * dh.n_passes, s);
-  k_duplicate<<<(unsigned)blocks, kDupThreads, 0, s>>>(pair_off, order, rects, dup_start, stats,
-                                                       ntx, keys, vals, dh);
+  k_bin_pairs<<<(unsigned)chunks, kBinThreads, 0, s>>>(order, rects, stats, pair_cap, status, ntx,
+                                                       keys, vals, dh, emit ? 1 : 0);
 }
 
 void launch_tile_ranges(const uint32_t* keys, const uint32_t* vals, const short4* boxes,
