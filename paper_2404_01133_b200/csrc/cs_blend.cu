@@ -51,6 +51,10 @@ __device__ __forceinline__ int blend_box_pixel(int b, int lane, int ts, int j) {
 #ifndef CS_BLEND_MINB
 #define CS_BLEND_MINB 1
 #endif
+#ifndef CS_BLEND_PAIR
+#define CS_BLEND_PAIR 0
+#endif
+constexpr bool kPairHits = CS_BLEND_PAIR != 0;  // evaluate hits two at a time
 
 template <typename OutT, bool KEEP, bool DIAG, int PX>
 __global__ void __launch_bounds__(kBlendThreads, CS_BLEND_MINB)
@@ -116,47 +120,71 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
     // one staged round: evaluate its hits (slots 0..popc-1) for this lane's pixels
     // (the quadratic form is computed by terminated pixels too: a branch around
     // it costs more issue slots than the idle lanes' share of the DP pipe)
+    // the quadratic form of one hit for this lane's pixels (pure)
+    auto quad = [&](const HotRec& h, double (&power)[PX]) {
+      const double mx = h.mx, my = h.my, c0 = h.c0, c1 = h.c1, c2 = h.c2;
+#pragma unroll
+      for (int j = 0; j < PX; ++j) {
+        const double dx = dsub(sx[j], mx);
+        const double dy = dsub(sy[j], my);
+        // -0.5 * (c0*dx*dx + c2*dy*dy) - c1*dx*dy   (_kernels.py:54-57)
+        power[j] = dsub(dmul(-0.5, dadd(dmul(dmul(c0, dx), dx), dmul(dmul(c2, dy), dy))),
+                        dmul(dmul(c1, dx), dy));
+      }
+    };
+    // the reference's sequential decisions for one hit (_kernels.py:58-72)
+    auto accept = [&](const HotRec& h, const double (&power)[PX], int src, int64_t k0) {
+      const double lthr = (double)h.lthr;
+      bool pass[PX];
+#pragma unroll
+      for (int j = 0; j < PX; ++j) {
+        if (DIAG) evals += done[j] ? 0u : 1u;
+        pass[j] = !done[j] && power[j] >= lthr;  // else alpha < alpha_floor guaranteed
+      }
+      if (DIAG) {
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < PX; ++j) any |= pass[j];
+        if (!__any_sync(0xffffffffu, any)) ++whits_empty;
+      }
+#pragma unroll
+      for (int j = 0; j < PX; ++j) {
+        if (!pass[j]) continue;
+        double alpha = dmul(h.opacity, exp_le0(power[j], s_exp, ec));  // _kernels.py:58
+        if (alpha > 0.99) alpha = 0.99;              // _kernels.py:59-60
+        if (alpha < bp.alpha_floor) continue;        // _kernels.py:61-62
+        const double nt = dmul(T[j], dsub(1.0, alpha));
+        if (nt < bp.t_floor) { done[j] = true; continue; }  // _kernels.py:63-66
+        const float w = (float)dmul(T[j], alpha);
+        cr[j] = fmaf(w, h.r, cr[j]);
+        cg[j] = fmaf(w, h.g, cg[j]);
+        cb[j] = fmaf(w, h.b, cb[j]);
+        T[j] = nt;
+        cnt[j] += 1;
+        last[j] = k0 + src + 1;
+      }
+    };
+    // one staged round: its hits (slots 0..popc-1), two at a time so the two
+    // independent quadratic-form chains overlap; the decisions stay in order
     auto eval_round = [&](const HotRec* buf, uint32_t mask, int64_t k0) {
       int slot = 0;
       whits += __popc(mask);
       while (mask) {
-        const int src = __ffs(mask) - 1;
+        const int src0 = __ffs(mask) - 1;
         mask &= mask - 1;
-        const HotRec& h = buf[slot++];
-        const double mx = h.mx, my = h.my, c0 = h.c0, c1 = h.c1, c2 = h.c2, lthr = (double)h.lthr;
-        double power[PX];
-        bool pass[PX];
-#pragma unroll
-        for (int j = 0; j < PX; ++j) {
-          if (DIAG) evals += done[j] ? 0u : 1u;
-          const double dx = dsub(sx[j], mx);
-          const double dy = dsub(sy[j], my);
-          // -0.5 * (c0*dx*dx + c2*dy*dy) - c1*dx*dy   (_kernels.py:54-57)
-          power[j] = dsub(dmul(-0.5, dadd(dmul(dmul(c0, dx), dx), dmul(dmul(c2, dy), dy))),
-                          dmul(dmul(c1, dx), dy));
-          pass[j] = !done[j] && power[j] >= lthr;  // else alpha < alpha_floor guaranteed
-        }
-        if (DIAG) {
-          bool any = false;
-#pragma unroll
-          for (int j = 0; j < PX; ++j) any |= pass[j];
-          if (!__any_sync(0xffffffffu, any)) ++whits_empty;
-        }
-#pragma unroll
-        for (int j = 0; j < PX; ++j) {
-          if (!pass[j]) continue;
-          double alpha = dmul(h.opacity, exp_le0(power[j], s_exp, ec));  // _kernels.py:58
-          if (alpha > 0.99) alpha = 0.99;              // _kernels.py:59-60
-          if (alpha < bp.alpha_floor) continue;        // _kernels.py:61-62
-          const double nt = dmul(T[j], dsub(1.0, alpha));
-          if (nt < bp.t_floor) { done[j] = true; continue; }  // _kernels.py:63-66
-          const float w = (float)dmul(T[j], alpha);
-          cr[j] = fmaf(w, h.r, cr[j]);
-          cg[j] = fmaf(w, h.g, cg[j]);
-          cb[j] = fmaf(w, h.b, cb[j]);
-          T[j] = nt;
-          cnt[j] += 1;
-          last[j] = k0 + src + 1;
+        const HotRec& h0 = buf[slot++];
+        double p0[PX];
+        quad(h0, p0);
+        if (kPairHits && mask) {  // warp-uniform
+          const int src1 = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const HotRec& h1 = buf[slot++];
+          double p1[PX];
+          quad(h1, p1);
+          accept(h0, p0, src0, k0);
+          accept(h1, p1, src1, k0);
+        } else {
+          accept(h0, p0, src0, k0);
         }
       }
     };
