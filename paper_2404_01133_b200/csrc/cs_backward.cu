@@ -177,8 +177,8 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
           if (k0 + src < my_end[j] && power >= lthr) {
             const double G = exp_le0(power, s_exp, ec);
             double alpha = dmul(h.opacity, G);
-            const bool clamped = alpha > 0.99;
-            if (clamped) alpha = 0.99;
+            const bool clamped = alpha > ec.clamp;  // 0.99
+            if (clamped) alpha = ec.clamp;
             if (alpha >= bp.alpha_floor) {
               contrib = true;
               const float a = (float)alpha;

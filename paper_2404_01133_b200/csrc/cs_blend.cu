@@ -151,7 +151,7 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
       for (int j = 0; j < PX; ++j) {
         if (!pass[j]) continue;
         double alpha = dmul(h.opacity, exp_le0(power[j], s_exp, ec));  // _kernels.py:58
-        if (alpha > 0.99) alpha = 0.99;              // _kernels.py:59-60
+        if (alpha > ec.clamp) alpha = ec.clamp;      // 0.99, _kernels.py:59-60
         if (alpha < bp.alpha_floor) continue;        // _kernels.py:61-62
         const double nt = dmul(T[j], dsub(1.0, alpha));
         if (nt < bp.t_floor) { done[j] = true; continue; }  // _kernels.py:63-66

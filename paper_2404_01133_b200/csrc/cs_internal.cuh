@@ -323,8 +323,19 @@ __constant__ double2 c_exp2_256[256] = {
 struct ExpTable {
   double2 t[256];
 };
+#ifndef CS_EXP_REGCONST
+#define CS_EXP_REGCONST 1
+#endif
+// The range-reduction constants and the 0.99 clamp, kept in registers (loaded
+// through a volatile pointer) instead of being re-materialised as 64-bit
+// immediates (two uniform moves each) at every use.
+__constant__ double c_exp_consts[4] = {369.3299304675746,        // 256 / ln2
+                                       -0.0027076061742263846,   // -(ln2/256), high 33 bits
+                                       1.6409824502660487e-13,   // ln2/256, low part
+                                       0.99};                    // alpha clamp (_kernels.py:59)
 struct ExpCoef {
   double c3, c4, c5;  // 1/6, 1/24, 1/120
+  double inv, hi, lo, clamp;
 };
 
 __device__ __forceinline__ ExpCoef load_exp_table(ExpTable* s_tab) {
@@ -337,13 +348,19 @@ __device__ __forceinline__ ExpCoef load_exp_table(ExpTable* s_tab) {
   c.c3 = one / 6.0;
   c.c4 = one / 24.0;
   c.c5 = one / 120.0;
+  if (CS_EXP_REGCONST) {
+    volatile const double* vk = c_exp_consts;
+    c.inv = vk[0]; c.hi = vk[1]; c.lo = vk[2]; c.clamp = vk[3];
+  } else {
+    c.inv = 369.3299304675746; c.hi = -0.0027076061742263846; c.lo = 1.6409824502660487e-13; c.clamp = 0.99;
+  }
   return c;
 }
 
 __device__ __forceinline__ double exp_le0(double x, const ExpTable& T, const ExpCoef& c) {
-  const double kd = rint(x * 369.3299304675746);           // 256 / ln2
-  double r = fma(kd, -0.0027076061742263846, x);           // ln2/256, high 33 bits
-  r = fma(kd, 1.6409824502660487e-13, r);                  // ln2/256, low part
+  const double kd = rint(x * c.inv);                        // 256 / ln2
+  double r = fma(kd, c.hi, x);                              // ln2/256, high 33 bits
+  r = fma(kd, c.lo, r);                                     // ln2/256, low part
   double q = fma(r, c.c5, c.c4);
   q = fma(q, r, c.c3);
   q = fma(q, r, 0.5);
