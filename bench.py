@@ -448,8 +448,14 @@ def main():
             _lib.check(lib.cs_render(ctx, ctypes.byref(src), ctypes.byref(c), ctypes.byref(cset),
                                      out.data_ptr(), flags, None, sh), "cs_render")
 
+        vis5, pairs5 = [], []
         for c in c5cams:  # sizing pass (synchronous: pair buffers grow to the largest view)
-            frame5(c, _lib.CS_RENDER_SYNC)
+            s5 = CsFrameStats()
+            _lib.check(lib.cs_render(ctx, ctypes.byref(src), ctypes.byref(c), ctypes.byref(cset),
+                                     out.data_ptr(), _lib.CS_RENDER_SYNC, ctypes.byref(s5), sh),
+                       "cs_render")
+            vis5.append(s5.visible)
+            pairs5.append(s5.pairs)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -464,10 +470,23 @@ def main():
         t5 = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t5, op=dist.ReduceOp.MAX)
+        # untimed second pass with the per-stage event marks
+        lib.cs_timing_begin(ctx, len(c5cams))
+        for c in c5cams:
+            frame5(c)
+        torch.cuda.synchronize()
+        st5 = (ctypes.c_double * 8)()
+        n5 = ctypes.c_int32(0)
+        _lib.check(lib.cs_timing_end(ctx, st5, ctypes.byref(n5)))
         c5 = {"metric": "C5 batch render FPS (740 test views, 1080p, LoD, view-split)",
               "value": len(test5) / (float(t5.item()) / 1000.0), "unit": "frames/s",
               "views": len(test5), "views_this_rank": len(mine), "n_gpus": world,
-              "ms_max_rank": float(t5.item()), "scaling": "weak in views per rank" if world > 1 else "n/a"}
+              "ms_max_rank": float(t5.item()), "scaling": "weak in views per rank" if world > 1 else "n/a",
+              "visible_M_min_med_max": [round(float(x) / 1e6, 3) for x in
+                                        (min(vis5), float(np.median(vis5)), max(vis5))] if vis5 else None,
+              "pairs_M_min_med_max": [round(float(x) / 1e6, 3) for x in
+                                      (min(pairs5), float(np.median(pairs5)), max(pairs5))] if pairs5 else None,
+              "stages_ms": {k: round(st5[i] / max(n5.value, 1), 4) for i, k in enumerate(STAGES)}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -649,9 +668,10 @@ def launches_per_frame() -> int:
     """Kernels of one C3 frame (memsets excluded), as listed by the ncu launch
     capture: k_lod_select, k_project, depth sort [k_radix_hist,
     k_radix_hist_scan, 4 x k_onesweep], k_fix_short_runs, k_fix_long_runs,
-    (fused) k_bin_pairs (also counts the tile-sort digits), tile sort
-    [k_radix_hist_scan, 2 x k_onesweep], k_tile_ranges, k_tile_order, k_blend."""
-    return 1 + 1 + (1 + 1 + 4) + 2 + 1 + (1 + 2) + 1 + 1 + 1
+    (fused) k_bin_pairs (also counts the tile-sort digits), k_emit_heavy
+    (pairs of chunks above kBinHeavy), tile sort [k_radix_hist_scan,
+    2 x k_onesweep], k_tile_ranges, k_tile_order, k_blend."""
+    return 1 + 1 + (1 + 1 + 4) + 2 + 2 + (1 + 2) + 1 + 1 + 1
 
 
 def host_scene(scene):

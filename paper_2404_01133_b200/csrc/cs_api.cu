@@ -64,6 +64,7 @@ void launch_activate_geom(int64_t K, const float* geom, float4* pos_op, float4* 
                           cudaStream_t s);
 // cs_bin.cu
 int64_t bin_chunks(int64_t capacity);
+int64_t bin_status_words(int64_t capacity);
 void launch_bin_pairs(const uint32_t* order, const uint2* rects, DevStats* stats, int64_t pair_cap,
                       int64_t capacity, uint64_t* status, int ntx, uint32_t* keys, uint32_t* vals,
                       uint32_t* hist, int key_bits, bool emit, cudaStream_t s);
@@ -351,7 +352,7 @@ static int ensure_frame_buffers(cs_ctx* c, int64_t cap_vis, int n_segs, int n_bl
     int64_t cap = std::max<int64_t>(cap_vis, c->cap_vis + c->cap_vis / 2);
     if (cap >= (1ll << 30)) return fail(CS_EINVAL, "more than 2^30 assembled Gaussians");
     const int64_t chunks = (cap + 255) / 256 + 1;
-    if (c->st_gather.ensure(8 * chunks) ||
+    if (c->st_gather.ensure(8 * std::max<int64_t>(chunks, bin_status_words(cap))) ||
         c->keysA.ensure(8 * cap) || c->keysB.ensure(8 * cap) || c->valsA.ensure(4 * cap) ||
         c->k32A.ensure(4 * cap) || c->k32B.ensure(4 * cap) ||
         c->long_runs.ensure(4 * fix_long_cap(cap)) || c->fix_ctl.ensure(fix_ctl_bytes()) ||

@@ -80,31 +80,41 @@ __device__ __forceinline__ void emit_pairs(uint32_t p, uint32_t p1, int nr, cons
 // shared memory, row-major over each rect (render.py:233-243) -- together
 // with the tile sort's digit histograms.  emit = false (projection-only
 // renders) stops after the count.
+//
+// A chunk of near, large splats can own far more pairs than the average
+// (a top-down or close-up view: one chunk with 10^5-10^6 pairs), and one CTA
+// emitting them would be the kernel's tail.  Chunks above kBinHeavy pairs are
+// therefore only registered (chunk, first slice, prefix, total) and their
+// pairs emitted by k_emit_heavy in kBinSlice-pair slices spread over the
+// whole GPU.  The output is the same: every pair lands at prefix + local.
 constexpr int kBinThreads = 256;
 constexpr int kBinItems = 8;
 constexpr int kBinRanks = kBinThreads * kBinItems;
+#ifndef CS_BIN_HEAVY
+#define CS_BIN_HEAVY 32768
+#endif
+#ifndef CS_BIN_SLICE
+#define CS_BIN_SLICE 8192
+#endif
+constexpr uint32_t kBinHeavy = CS_BIN_HEAVY;
+constexpr uint32_t kBinSlice = CS_BIN_SLICE;
+constexpr int kHeavyCtas = 148 * 4;
 
-__global__ void __launch_bounds__(kBinThreads)
-k_bin_pairs(const uint32_t* __restrict__ order, const uint2* __restrict__ rects,
-            DevStats* __restrict__ stats, int64_t pair_cap, uint64_t* __restrict__ status,
-            int ntx, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, DigitHist dh,
-            int emit) {
-  __shared__ uint32_t s_off[kBinRanks + 1];
-  __shared__ uint2 s_rect[kBinRanks];
-  __shared__ uint32_t s_id[kBinRanks];
-  __shared__ uint32_t s_hist[kMaxHistPasses][256];
-  __shared__ uint32_t s_scan[kBinThreads / 32 + 1];
-  __shared__ uint64_t s_prefix;
-  __shared__ uint32_t s_chunk;
-  const int64_t M = stats->visible;
-  if (threadIdx.x == 0) s_chunk = atomicAdd(&stats->tickets[2], 1u);
-  for (int i = threadIdx.x; i < dh.n_passes * 256; i += kBinThreads) s_hist[i >> 8][i & 255] = 0;
-  __syncthreads();
-  const int64_t chunk = s_chunk;
-  const int64_t base = chunk * kBinRanks;
-  if (base >= M) return;
+struct BinSmem {
+  uint32_t off[kBinRanks + 1];
+  uint2 rect[kBinRanks];
+  uint32_t id[kBinRanks];
+  uint32_t hist[kMaxHistPasses][256];
+  uint32_t scan[kBinThreads / 32 + 1];
+};
+
+// Gathers chunk [base, base + nr) of the depth order into shared memory and
+// writes each rank's exclusive pair offset inside the chunk (off[nr] = the
+// 0xffffffff sentinel: every rank owns >= 1 pair).  Returns the chunk total.
+__device__ __forceinline__ uint32_t gather_chunk(const uint32_t* __restrict__ order,
+                                                 const uint2* __restrict__ rects, int64_t base,
+                                                 int nr, BinSmem& sm) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nr = (int)min((int64_t)kBinRanks, M - base);
   uint32_t cnt[kBinItems], run = 0;
 #pragma unroll
   for (int i = 0; i < kBinItems; ++i) {
@@ -114,24 +124,56 @@ k_bin_pairs(const uint32_t* __restrict__ order, const uint2* __restrict__ rects,
       const uint32_t id = __ldg(order + base + li);
       const uint2 pr = __ldg(rects + id);
       const int4 rc = unpack_rect(pr);
-      s_rect[li] = pr;
-      s_id[li] = id;
+      sm.rect[li] = pr;
+      sm.id[li] = id;
       c = (uint32_t)((rc.y - rc.x + 1) * (rc.w - rc.z + 1));
     }
     const uint32_t incl = warp_incl_scan(c);
     cnt[i] = run + incl - c;  // exclusive offset inside the warp's 256 ranks
     run += __shfl_sync(0xffffffffu, incl, 31);
   }
-  if (lane == 0) s_scan[warp] = run;
+  if (lane == 0) sm.scan[warp] = run;
   __syncthreads();
   if (warp == 0) {
-    const uint32_t w = lane < kBinThreads / 32 ? s_scan[lane] : 0u;
+    const uint32_t w = lane < kBinThreads / 32 ? sm.scan[lane] : 0u;
     const uint32_t wi = warp_incl_scan(w);
-    if (lane < kBinThreads / 32) s_scan[lane] = wi - w;
-    if (lane == 31) s_scan[kBinThreads / 32] = wi;
+    if (lane < kBinThreads / 32) sm.scan[lane] = wi - w;
+    if (lane == 31) sm.scan[kBinThreads / 32] = wi;
   }
   __syncthreads();
-  const uint32_t total = s_scan[kBinThreads / 32];  // <= 2048 x 2^16 pairs
+#pragma unroll
+  for (int i = 0; i < kBinItems; ++i) {
+    const int li = warp * (32 * kBinItems) + i * 32 + lane;
+    if (li < nr) sm.off[li] = sm.scan[warp] + cnt[i];
+  }
+  if (threadIdx.x == 0) sm.off[nr] = 0xffffffffu;
+  return sm.scan[kBinThreads / 32];  // <= 2048 x 2^16 pairs
+}
+
+__device__ __forceinline__ void flush_hist(const DigitHist& dh, BinSmem& sm) {
+  for (int i = threadIdx.x; i < dh.n_passes * 256; i += kBinThreads) {
+    const uint32_t c = sm.hist[i >> 8][i & 255];
+    if (c) atomicAdd(dh.hist + i, c);
+  }
+}
+
+__global__ void __launch_bounds__(kBinThreads)
+k_bin_pairs(const uint32_t* __restrict__ order, const uint2* __restrict__ rects,
+            DevStats* __restrict__ stats, int64_t pair_cap, uint64_t* __restrict__ status,
+            uint4* __restrict__ heavy, int ntx, uint32_t* __restrict__ keys,
+            uint32_t* __restrict__ vals, DigitHist dh, int emit) {
+  __shared__ BinSmem sm;
+  __shared__ uint64_t s_prefix;
+  __shared__ uint32_t s_chunk;
+  const int64_t M = stats->visible;
+  if (threadIdx.x == 0) s_chunk = atomicAdd(&stats->tickets[2], 1u);
+  for (int i = threadIdx.x; i < dh.n_passes * 256; i += kBinThreads) sm.hist[i >> 8][i & 255] = 0;
+  __syncthreads();
+  const int64_t chunk = s_chunk;
+  const int64_t base = chunk * kBinRanks;
+  if (base >= M) return;
+  const int nr = (int)min((int64_t)kBinRanks, M - base);
+  const uint32_t total = gather_chunk(order, rects, base, nr, sm);
   if (threadIdx.x < 32) {
     const uint64_t pre = lookback_exclusive(status, chunk, total);
     if (threadIdx.x == 0) {
@@ -142,24 +184,66 @@ k_bin_pairs(const uint32_t* __restrict__ order, const uint2* __restrict__ rects,
         stats->pairs_eff = P <= pair_cap ? P : 0;
         if (P > pair_cap) atomicOr(&stats->status, 1);
       }
+      if (emit && total > kBinHeavy && pre + total <= (uint64_t)pair_cap) {
+        // register the chunk: entry index and first slice from one 64-bit
+        // atomic, so entries are ordered by first slice
+        const uint32_t ns = (total + kBinSlice - 1) / kBinSlice;
+        const unsigned long long old = atomicAdd(
+            reinterpret_cast<unsigned long long*>(&stats->tickets[8]), (1ull << 32) | ns);
+        heavy[old >> 32] = make_uint4((uint32_t)chunk, (uint32_t)old, (uint32_t)pre, total);
+      }
     }
   }
-#pragma unroll
-  for (int i = 0; i < kBinItems; ++i) {
-    const int li = warp * (32 * kBinItems) + i * 32 + lane;
-    if (li < nr) s_off[li] = s_scan[warp] + cnt[i];
-  }
-  if (threadIdx.x == 0) s_off[nr] = 0xffffffffu;  // sentinel: every rank owns >= 1 pair
   __syncthreads();
   const uint64_t prefix = s_prefix;
   if (!emit || prefix + total > (uint64_t)pair_cap) return;  // overflow: the SYNC path re-renders
+  if (total > kBinHeavy) return;                             // k_emit_heavy's
   for (uint32_t q = threadIdx.x * kDupItems; q < total; q += kBinThreads * kDupItems)
-    emit_pairs(q, total, nr, s_off, s_rect, s_id, ntx, keys, vals, dh, s_hist, prefix);
+    emit_pairs(q, total, nr, sm.off, sm.rect, sm.id, ntx, keys, vals, dh, sm.hist, prefix);
   __syncthreads();
-  for (int i = threadIdx.x; i < dh.n_passes * 256; i += kBinThreads) {
-    const uint32_t c = s_hist[i >> 8][i & 255];
-    if (c) atomicAdd(dh.hist + i, c);
+  flush_hist(dh, sm);
+}
+
+// Pairs of the registered heavy chunks, one kBinSlice slice per ticket; a CTA
+// re-gathers a chunk's offsets only when its slice moves to another chunk.
+__global__ void __launch_bounds__(kBinThreads)
+k_emit_heavy(const uint32_t* __restrict__ order, const uint2* __restrict__ rects,
+             DevStats* __restrict__ stats, const uint4* __restrict__ heavy, int ntx,
+             uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, DigitHist dh) {
+  __shared__ BinSmem sm;
+  __shared__ uint32_t s_t;
+  const unsigned long long hc = *reinterpret_cast<const unsigned long long*>(&stats->tickets[8]);
+  const uint32_t n_entries = (uint32_t)(hc >> 32), n_slices = (uint32_t)hc;
+  if (n_slices == 0) return;
+  const int64_t M = stats->visible;
+  for (int i = threadIdx.x; i < dh.n_passes * 256; i += kBinThreads) sm.hist[i >> 8][i & 255] = 0;
+  int64_t cur = -1;
+  int nr = 0;
+  while (true) {
+    if (threadIdx.x == 0) s_t = atomicAdd(&stats->tickets[10], 1u);
+    __syncthreads();
+    const uint32_t t = s_t;
+    if (t >= n_slices) break;
+    int lo = 0, hi = (int)n_entries - 1;  // last entry whose first slice <= t
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (__ldg(&heavy[mid].y) <= t) lo = mid; else hi = mid - 1;
+    }
+    const uint4 e = __ldg(heavy + lo);
+    if ((int64_t)e.x != cur) {
+      __syncthreads();  // the previous chunk's shared arrays are no longer read
+      cur = e.x;
+      const int64_t base = cur * kBinRanks;
+      nr = (int)min((int64_t)kBinRanks, M - base);
+      gather_chunk(order, rects, base, nr, sm);
+      __syncthreads();
+    }
+    const uint32_t q0 = (t - e.y) * kBinSlice, q1 = min(e.w, q0 + kBinSlice);
+    for (uint32_t q = q0 + threadIdx.x * kDupItems; q < q1; q += kBinThreads * kDupItems)
+      emit_pairs(q, q1, nr, sm.off, sm.rect, sm.id, ntx, keys, vals, dh, sm.hist, e.z);
   }
+  __syncthreads();
+  flush_hist(dh, sm);
 }
 
 // CSR tile ranges from the tile-sorted keys (render.py:247-248), and the
@@ -215,6 +299,11 @@ __global__ void k_tile_ranges(const uint32_t* __restrict__ keys, const uint32_t*
 }
 
 int64_t bin_chunks(int64_t capacity) { return (capacity + kBinRanks - 1) / kBinRanks; }
+// 8-byte words of the K5+K6 workspace: look-back status, then 16-byte heavy entries
+int64_t bin_status_words(int64_t capacity) {
+  const int64_t chunks = bin_chunks(capacity);
+  return chunks + 2 + 2 * chunks;
+}
 
 void launch_bin_pairs(const uint32_t* order, const uint2* rects, DevStats* stats, int64_t pair_cap,
                       int64_t capacity, uint64_t* status, int ntx, uint32_t* keys, uint32_t* vals,
@@ -227,8 +316,13 @@ void launch_bin_pairs(const uint32_t* order, const uint2* rects, DevStats* stats
   dh.width = dh.n_passes ? (key_bits + dh.n_passes - 1) / dh.n_passes : 8;
   dh.end_bit = key_bits;
   if (hist) cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 256 * dh.n_passes, s);
-  k_bin_pairs<<<(unsigned)chunks, kBinThreads, 0, s>>>(order, rects, stats, pair_cap, status, ntx,
-                                                       keys, vals, dh, emit ? 1 : 0);
+  // status: chunks + 1 look-back words, then the heavy-chunk entries
+  uint4* heavy = reinterpret_cast<uint4*>(status + chunks + 1 + ((chunks + 1) & 1));
+  k_bin_pairs<<<(unsigned)chunks, kBinThreads, 0, s>>>(order, rects, stats, pair_cap, status, heavy,
+                                                       ntx, keys, vals, dh, emit ? 1 : 0);
+  if (emit)
+    k_emit_heavy<<<(unsigned)std::min<int64_t>(kHeavyCtas, chunks), kBinThreads, 0, s>>>(
+        order, rects, stats, heavy, ntx, keys, vals, dh);
 }
 
 void launch_tile_ranges(const uint32_t* keys, const uint32_t* vals, const short4* boxes,

@@ -14,7 +14,10 @@
 //     digit gives the chunk's global offset (no separate scan pass);
 //   * keys are first scattered to shared memory in digit order, then written
 //     out so consecutive threads store consecutive addresses of one digit run.
-// A single histogram kernel computes the digit counts of every pass up front.
+// A single histogram kernel computes the digit counts of every pass up front;
+// the scan kernel after it also clears the look-back status of every pass for
+// the actual count, and each pass runs one wave of CTAs that loop over chunk
+// tickets, so a large pair capacity costs nothing when a view has few pairs.
 // The element count is read from device memory, so the whole frame runs
 // without a host round trip (and is CUDA-graph capturable).
 #include <algorithm>
@@ -55,15 +58,27 @@ k_radix_hist(const K* __restrict__ keys, const int64_t* __restrict__ n_ptr, int 
     if (sh[i]) atomicAdd(&hist[i], sh[i]);
 }
 
-// exclusive scan of each pass's 256-bin histogram, in place
-__global__ void k_radix_hist_scan(uint32_t* hist, int n_passes) {
+// exclusive scan of each pass's 256-bin histogram, in place (block 0), and
+// the look-back status of every pass zeroed for the ACTUAL element count (all
+// blocks; pass p's words start at p * ceil(n / tile) * 256), so neither the
+// status clear nor the pass grids scale with the buffer capacity
+__global__ void k_radix_hist_scan(uint32_t* hist, int n_passes, uint32_t* __restrict__ status,
+                                  const int64_t* __restrict__ n_ptr, int tile) {
   __shared__ uint32_t scratch[kSortWarps + 1];
-  for (int p = 0; p < n_passes; ++p) {
-    uint32_t v = hist[p * 256 + threadIdx.x];
-    uint32_t total;
-    uint32_t ex = block_excl_scan<uint32_t>(v, scratch, total);
-    hist[p * 256 + threadIdx.x] = ex;
+  if (blockIdx.x == 0) {
+    for (int p = 0; p < n_passes; ++p) {
+      uint32_t v = hist[p * 256 + threadIdx.x];
+      uint32_t total;
+      uint32_t ex = block_excl_scan<uint32_t>(v, scratch, total);
+      hist[p * 256 + threadIdx.x] = ex;
+    }
   }
+  const uint64_t chunks = ((uint64_t)*n_ptr + tile - 1) / tile;
+  const uint64_t n4 = chunks * 64 * n_passes;  // uint4 words
+  uint4* st4 = reinterpret_cast<uint4*>(status);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    st4[i] = make_uint4(0, 0, 0, 0);
 }
 
 // The pass body, FULL = the chunk holds kTile keys (no bounds checks, the
@@ -205,12 +220,16 @@ __device__ __forceinline__ void onesweep_body(
   }
 }
 
+#ifndef CS_SORT_PERSIST
+#define CS_SORT_PERSIST 1
+#endif
+
 template <typename K, int ITEMS = SortCfg<K>::kItems, int MINB = 1, int NB = 8, bool EARLY = true>
 __global__ void __launch_bounds__(kSortThreads, MINB)
 k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
            K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
            const int64_t* __restrict__ n_ptr, int shift,
-           const uint32_t* __restrict__ digit_base, uint32_t* __restrict__ status,
+           const uint32_t* __restrict__ digit_base, uint32_t* __restrict__ status, int pass,
            uint32_t* __restrict__ ticket) {
   constexpr int kTile = kSortThreads * ITEMS;
   __shared__ uint32_t warp_hist[kSortWarps][256];
@@ -223,29 +242,37 @@ k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
   __shared__ uint32_t vals_s[kTile];
 
   const uint32_t n = (uint32_t)*n_ptr;
-  if (threadIdx.x == 0) s_chunk = atomicAdd(ticket, 1u);
+  status += (size_t)pass * ((n + kTile - 1) / kTile) * 256;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int d = lane; d < 256; d += 32) warp_hist[warp][d] = 0;
-  chunk_hist[threadIdx.x] = 0;
-  __syncthreads();
-  const uint32_t chunk = s_chunk;
-  const uint64_t base = (uint64_t)chunk * kTile;
-  if (base >= n) return;
-  if (base + kTile <= n)
-    onesweep_body<K, ITEMS, true, NB, EARLY>(keys_in, vals_in, keys_out, vals_out, n, chunk, shift,
-                                             digit_base, status, warp_hist, chunk_hist, digit_off,
-                                             gbase, scratch, keys_s, vals_s);
-  else
-    onesweep_body<K, ITEMS, false, NB, EARLY>(keys_in, vals_in, keys_out, vals_out, n, chunk, shift,
-                                              digit_base, status, warp_hist, chunk_hist, digit_off,
-                                              gbase, scratch, keys_s, vals_s);
+  // CS_SORT_PERSIST: the grid is at most one wave and every CTA loops over
+  // chunk tickets until the actual count is covered (no capacity-sized grid
+  // of CTAs that only exit)
+  while (true) {
+    if (threadIdx.x == 0) s_chunk = atomicAdd(ticket, 1u);
+    for (int d = lane; d < 256; d += 32) warp_hist[warp][d] = 0;
+    chunk_hist[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t chunk = s_chunk;
+    const uint64_t base = (uint64_t)chunk * kTile;
+    if (base >= n) return;
+    if (base + kTile <= n)
+      onesweep_body<K, ITEMS, true, NB, EARLY>(keys_in, vals_in, keys_out, vals_out, n, chunk, shift,
+                                               digit_base, status, warp_hist, chunk_hist, digit_off,
+                                               gbase, scratch, keys_s, vals_s);
+    else
+      onesweep_body<K, ITEMS, false, NB, EARLY>(keys_in, vals_in, keys_out, vals_out, n, chunk, shift,
+                                                digit_base, status, warp_hist, chunk_hist, digit_off,
+                                                gbase, scratch, keys_s, vals_s);
+    if (!CS_SORT_PERSIST) return;
+    __syncthreads();  // shared arrays are reused by the next chunk
+  }
 }
 
-// Workspace: hist (8*256 u32), status (chunks*256 u32), tickets (8 u32).
+// Workspace: hist (8*256 u32), status (passes*chunks*256 u32), tickets (8 u32).
 size_t radix_status_words(int64_t capacity, int key_bytes) {
   const int items = key_bytes == 8 ? SortCfg<uint64_t>::kItems : SortCfg<uint32_t>::kItems;
   const int64_t tile = (int64_t)kSortThreads * items;
-  return (size_t)((capacity + tile - 1) / tile) * 256;
+  return (size_t)((capacity + tile - 1) / tile) * 256 * key_bytes;  // <= key_bytes 8-bit passes
 }
 
 // Sorts (keys, vals) of length *n_dev (<= capacity) by bits [begin_bit, end_bit).
@@ -254,15 +281,25 @@ size_t radix_status_words(int64_t capacity, int key_bytes) {
 template <typename K, int ITEMS, int MINB, int NB, bool EARLY>
 static void launch_pass(unsigned chunks, cudaStream_t s, const K* kin, const uint32_t* vin, K* kout,
                         uint32_t* vout, const int64_t* n_dev, int shift, const uint32_t* hist,
-                        uint32_t* status, uint32_t* ticket) {
+                        uint32_t* status, int pass, uint32_t* ticket) {
   static bool carveout = false;  // shared memory is the occupancy limit: take all of it
   if (!carveout) {
     cudaFuncSetAttribute(k_onesweep<K, ITEMS, MINB, NB, EARLY>,
                          cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     carveout = true;
   }
-  k_onesweep<K, ITEMS, MINB, NB, EARLY><<<chunks, kSortThreads, 0, s>>>(kin, vin, kout, vout, n_dev,
-                                                                      shift, hist, status, ticket);
+  static int wave = 0;  // resident CTAs of this instantiation on the whole GPU
+  if (!wave) {
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_onesweep<K, ITEMS, MINB, NB, EARLY>,
+                                                  kSortThreads, 0);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    wave = std::max(1, per_sm * sms);
+  }
+  const unsigned g = CS_SORT_PERSIST ? std::min<unsigned>(chunks, (unsigned)wave) : chunks;
+  k_onesweep<K, ITEMS, MINB, NB, EARLY><<<g, kSortThreads, 0, s>>>(kin, vin, kout, vout, n_dev,
+                                                                  shift, hist, status, pass, ticket);
 }
 
 template <typename K, int ITEMS, int MINB = SortCfg<K>::kMinBlocks, bool EARLY = true>
@@ -281,25 +318,25 @@ int radix_sort_items(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_
     int hist_grid = (int)std::min<int64_t>(148 * 4, (capacity + kSortThreads - 1) / kSortThreads);
     k_radix_hist<K><<<hist_grid, kSortThreads, 0, s>>>(k0, n_dev, begin_bit, n_passes, width, end_bit, hist);
   }
-  k_radix_hist_scan<<<1, 256, 0, s>>>(hist, n_passes);
+  k_radix_hist_scan<<<(unsigned)std::min<int64_t>(148 * 2, chunks), 256, 0, s>>>(hist, n_passes, status,
+                                                                                n_dev, kTile);
   K* kin = k0; K* kout = k1;
   uint32_t* vin = v0; uint32_t* vout = v1;
   for (int p = 0; p < n_passes; ++p) {
-    cudaMemsetAsync(status, 0, sizeof(uint32_t) * 256 * chunks, s);
     const int shift = begin_bit + width * p;
     const int nb = std::min(width, end_bit - shift);
     const unsigned g = (unsigned)chunks;
     uint32_t* tk = tickets + p;
     const uint32_t* hp = hist + 256 * p;
     switch (nb) {
-      case 8: launch_pass<K, ITEMS, MINB, 8, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, tk); break;
-      case 7: launch_pass<K, ITEMS, MINB, 7, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, tk); break;
-      case 6: launch_pass<K, ITEMS, MINB, 6, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, tk); break;
-      case 5: launch_pass<K, ITEMS, MINB, 5, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, tk); break;
-      case 4: launch_pass<K, ITEMS, MINB, 4, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, tk); break;
-      case 3: launch_pass<K, ITEMS, MINB, 3, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, tk); break;
-      case 2: launch_pass<K, ITEMS, MINB, 2, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, tk); break;
-      default: launch_pass<K, ITEMS, MINB, 1, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, tk); break;
+      case 8: launch_pass<K, ITEMS, MINB, 8, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, p, tk); break;
+      case 7: launch_pass<K, ITEMS, MINB, 7, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, p, tk); break;
+      case 6: launch_pass<K, ITEMS, MINB, 6, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, p, tk); break;
+      case 5: launch_pass<K, ITEMS, MINB, 5, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, p, tk); break;
+      case 4: launch_pass<K, ITEMS, MINB, 4, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, p, tk); break;
+      case 3: launch_pass<K, ITEMS, MINB, 3, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, p, tk); break;
+      case 2: launch_pass<K, ITEMS, MINB, 2, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, p, tk); break;
+      default: launch_pass<K, ITEMS, MINB, 1, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, p, tk); break;
     }
     K* t0 = kin; kin = kout; kout = t0;
     uint32_t* t1 = vin; vin = vout; vout = t1;

@@ -9,8 +9,9 @@ for V in "$@"; do
   tail -1 gpurun_out/${TAG}_var.log | python -c "
 import json,sys
 d=json.loads(sys.stdin.read())
-t=d.get('train')
-print('$V', 'fps', round(d['value'],1), 'stages', {k: round(v,3) for k,v in d['stages_ms'].items()}, 'train', t and round(t['value'],1), t and {k: round(v,3) for k,v in t['phases_ms'].items()})"
+t=d.get('train'); c5=d.get('c5')
+print('$V', 'fps', round(d['value'],1), 'stages', {k: round(v,3) for k,v in d['stages_ms'].items()}, 'train', t and round(t['value'],1), t and {k: round(v,3) for k,v in t['phases_ms'].items()})
+if c5: print('   c5', round(c5['value'],1), c5.get('stages_ms'))"
 done
 touch paper_2404_01133_b200/csrc/${FILE}.cu
 python paper_2404_01133_b200/_build.py > /dev/null 2>&1
