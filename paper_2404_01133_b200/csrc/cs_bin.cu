@@ -157,6 +157,10 @@ __device__ __forceinline__ void flush_hist(const DigitHist& dh, BinSmem& sm) {
   }
 }
 
+#ifndef CS_BIN_PERSIST
+#define CS_BIN_PERSIST 1
+#endif
+
 __global__ void __launch_bounds__(kBinThreads)
 k_bin_pairs(const uint32_t* __restrict__ order, const uint2* __restrict__ rects,
             DevStats* __restrict__ stats, int64_t pair_cap, uint64_t* __restrict__ status,
@@ -166,40 +170,46 @@ k_bin_pairs(const uint32_t* __restrict__ order, const uint2* __restrict__ rects,
   __shared__ uint64_t s_prefix;
   __shared__ uint32_t s_chunk;
   const int64_t M = stats->visible;
-  if (threadIdx.x == 0) s_chunk = atomicAdd(&stats->tickets[2], 1u);
   for (int i = threadIdx.x; i < dh.n_passes * 256; i += kBinThreads) sm.hist[i >> 8][i & 255] = 0;
-  __syncthreads();
-  const int64_t chunk = s_chunk;
-  const int64_t base = chunk * kBinRanks;
-  if (base >= M) return;
-  const int nr = (int)min((int64_t)kBinRanks, M - base);
-  const uint32_t total = gather_chunk(order, rects, base, nr, sm);
-  if (threadIdx.x < 32) {
-    const uint64_t pre = lookback_exclusive(status, chunk, total);
-    if (threadIdx.x == 0) {
-      s_prefix = pre;
-      if (base + kBinRanks >= M) {
-        const int64_t P = (int64_t)(pre + total);
-        stats->pairs = P;
-        stats->pairs_eff = P <= pair_cap ? P : 0;
-        if (P > pair_cap) atomicOr(&stats->status, 1);
-      }
-      if (emit && total > kBinHeavy && pre + total <= (uint64_t)pair_cap) {
-        // register the chunk: entry index and first slice from one 64-bit
-        // atomic, so entries are ordered by first slice
-        const uint32_t ns = (total + kBinSlice - 1) / kBinSlice;
-        const unsigned long long old = atomicAdd(
-            reinterpret_cast<unsigned long long*>(&stats->tickets[8]), (1ull << 32) | ns);
-        heavy[old >> 32] = make_uint4((uint32_t)chunk, (uint32_t)old, (uint32_t)pre, total);
+  // CS_BIN_PERSIST: one wave of CTAs looping over chunk tickets (the grid is
+  // not sized by the visible capacity); digit counts flushed once per CTA
+  while (true) {
+    if (threadIdx.x == 0) s_chunk = atomicAdd(&stats->tickets[2], 1u);
+    __syncthreads();
+    const int64_t chunk = s_chunk;
+    const int64_t base = chunk * kBinRanks;
+    if (base >= M) break;
+    const int nr = (int)min((int64_t)kBinRanks, M - base);
+    const uint32_t total = gather_chunk(order, rects, base, nr, sm);
+    if (threadIdx.x < 32) {
+      const uint64_t pre = lookback_exclusive(status, chunk, total);
+      if (threadIdx.x == 0) {
+        s_prefix = pre;
+        if (base + kBinRanks >= M) {
+          const int64_t P = (int64_t)(pre + total);
+          stats->pairs = P;
+          stats->pairs_eff = P <= pair_cap ? P : 0;
+          if (P > pair_cap) atomicOr(&stats->status, 1);
+        }
+        if (emit && total > kBinHeavy && pre + total <= (uint64_t)pair_cap) {
+          // register the chunk: entry index and first slice from one 64-bit
+          // atomic, so entries are ordered by first slice
+          const uint32_t ns = (total + kBinSlice - 1) / kBinSlice;
+          const unsigned long long old = atomicAdd(
+              reinterpret_cast<unsigned long long*>(&stats->tickets[8]), (1ull << 32) | ns);
+          heavy[old >> 32] = make_uint4((uint32_t)chunk, (uint32_t)old, (uint32_t)pre, total);
+        }
       }
     }
+    __syncthreads();
+    const uint64_t prefix = s_prefix;
+    // overflow: the SYNC path re-renders; heavy chunks: k_emit_heavy's
+    if (emit && prefix + total <= (uint64_t)pair_cap && total <= kBinHeavy)
+      for (uint32_t q = threadIdx.x * kDupItems; q < total; q += kBinThreads * kDupItems)
+        emit_pairs(q, total, nr, sm.off, sm.rect, sm.id, ntx, keys, vals, dh, sm.hist, prefix);
+    if (!CS_BIN_PERSIST) break;
+    __syncthreads();  // shared arrays are reused by the next chunk
   }
-  __syncthreads();
-  const uint64_t prefix = s_prefix;
-  if (!emit || prefix + total > (uint64_t)pair_cap) return;  // overflow: the SYNC path re-renders
-  if (total > kBinHeavy) return;                             // k_emit_heavy's
-  for (uint32_t q = threadIdx.x * kDupItems; q < total; q += kBinThreads * kDupItems)
-    emit_pairs(q, total, nr, sm.off, sm.rect, sm.id, ntx, keys, vals, dh, sm.hist, prefix);
   __syncthreads();
   flush_hist(dh, sm);
 }
@@ -318,8 +328,17 @@ void launch_bin_pairs(const uint32_t* order, const uint2* rects, DevStats* stats
   if (hist) cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 256 * dh.n_passes, s);
   // status: chunks + 1 look-back words, then the heavy-chunk entries
   uint4* heavy = reinterpret_cast<uint4*>(status + chunks + 1 + ((chunks + 1) & 1));
-  k_bin_pairs<<<(unsigned)chunks, kBinThreads, 0, s>>>(order, rects, stats, pair_cap, status, heavy,
-                                                       ntx, keys, vals, dh, emit ? 1 : 0);
+  static int wave = 0;  // resident CTAs on the whole GPU
+  if (!wave) {
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bin_pairs, kBinThreads, 0);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    wave = std::max(1, per_sm * sms);
+  }
+  const unsigned grid = CS_BIN_PERSIST ? (unsigned)std::min<int64_t>(chunks, wave) : (unsigned)chunks;
+  k_bin_pairs<<<grid, kBinThreads, 0, s>>>(order, rects, stats, pair_cap, status, heavy, ntx, keys,
+                                           vals, dh, emit ? 1 : 0);
   if (emit)
     k_emit_heavy<<<(unsigned)std::min<int64_t>(kHeavyCtas, chunks), kBinThreads, 0, s>>>(
         order, rects, stats, heavy, ntx, keys, vals, dh);
