@@ -375,18 +375,34 @@ k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
   const cs_cloud& cd = clouds[cloud_id];
   // view direction and SH colour (render.py:167-169, core.py:166-172)
   double dx = g.px - cam.center[0], dy = g.py - cam.center[1], dz = g.pz - cam.center[2];
-  double nrm = sqrt((dx * dx + dy * dy) + dz * dz);
   int degree = min((int)st.sh_degree, degree_of(cd.sh_coeffs));
   double col[3];
+#ifdef CS_SH_F64
+  double nrm = sqrt((dx * dx + dy * dy) + dz * dz);
   sh_colour(cd.sh + local * cd.sh_stride, cd.sh_coeffs, degree, dx / nrm, dy / nrm, dz / nrm, col);
+#else
+  {  // the colour is evaluated in float32: so is the unit view direction (no
+     // float64 divisions / sqrt for a tolerance-only quantity)
+    const float fx = (float)dx, fy = (float)dy, fz = (float)dz;
+    const float inv = rsqrtf(fmaf(fx, fx, fmaf(fy, fy, fz * fz)));
+    sh_colour(cd.sh + local * cd.sh_stride, cd.sh_coeffs, degree, fx * inv, fy * inv, fz * inv, col);
+  }
+#endif
   const double c0 = ddiv(po.c, po.det);   // render.py:172
   const double c1 = ddiv(-po.b, po.det);
   const double c2 = ddiv(po.a, po.det);
   // blend fast-reject threshold: alpha = o*exp(power) < alpha_floor whenever
-  // power < log(alpha_floor / o) - 1e-6 (margin >> exp/log rounding)
-  const double lt = g.op > 0.0 ? log(st.alpha_floor / g.op) - 1e-6
-                               : __longlong_as_double(0x7ff0000000000000ll);
-  const float lthr = __double2float_rd(lt);
+  // power < log(alpha_floor / o) - 1e-6 (margin >> exp rounding).  Evaluated
+  // in float32 with a 1e-5 margin, which covers the float32 logs (<= 2 ulp of
+  // |log| <= ~20, i.e. < 5e-6): the threshold stays conservative, only the
+  // exact float64 path decides a fragment.
+  float lthr;
+  if (g.op > 0.0) {
+    const float lf = __fsub_rn(logf((float)st.alpha_floor), logf((float)g.op));
+    lthr = __fsub_rd(lf, 1e-5f + 1e-6f * fabsf(lf));
+  } else {
+    lthr = __int_as_float(0x7f800000);
+  }
   HotRec h;
   h.mx = po.mx; h.my = po.my; h.c0 = c0; h.c1 = c1; h.c2 = c2;
   h.opacity = g.op;
@@ -400,8 +416,9 @@ k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
   const double L = -(double)lthr;
   short4 box = make_short4(32000, -1, 32000, -1);  // empty: never intersects
   if (L > 0.0) {
-    const double hx = sqrt(2.0 * L * po.a) * (1.0 + 1e-4) + 1e-3;
-    const double hy = sqrt(2.0 * L * po.c) * (1.0 + 1e-4) + 1e-3;
+    // float32 square roots (relative error ~1e-7, inside the 1e-4 inflation)
+    const double hx = (double)sqrtf((float)(2.0 * L * po.a)) * (1.0 + 1e-4) + 1e-3;
+    const double hy = (double)sqrtf((float)(2.0 * L * po.c)) * (1.0 + 1e-4) + 1e-3;
     const double lim = 32000.0;
     box.x = (int16_t)fmin(fmax(ceil(po.mx - hx - 0.5), -1.0), lim);
     box.y = (int16_t)fmin(fmax(floor(po.mx + hx - 0.5), -1.0), lim);
@@ -415,10 +432,15 @@ k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
     const int64_t ntx = (cam.width + st.tile_size - 1) / st.tile_size;
     const int64_t nty = (cam.height + st.tile_size - 1) / st.tile_size;
     const double ts = (double)st.tile_size;
-    const int64_t tx0 = clip_i64(np_to_i64(floor(ddiv(dsub(dsub(po.mx, po.rx), 0.5), ts))), 0, ntx - 1);
-    const int64_t tx1 = clip_i64(np_to_i64(floor(ddiv(dsub(dadd(po.mx, po.rx), 0.5), ts))), 0, ntx - 1);
-    const int64_t ty0 = clip_i64(np_to_i64(floor(ddiv(dsub(dsub(po.my, po.ry), 0.5), ts))), 0, nty - 1);
-    const int64_t ty1 = clip_i64(np_to_i64(floor(ddiv(dsub(dadd(po.my, po.ry), 0.5), ts))), 0, nty - 1);
+    // x / ts for a power-of-two tile size is x * (1 / ts) exactly (both are
+    // the correctly rounded x * 2^-k), so the division becomes a multiply
+    const bool pow2 = (st.tile_size & (st.tile_size - 1)) == 0;
+    const double its = pow2 ? __longlong_as_double((long long)(1024 - __ffs(st.tile_size)) << 52) : 0.0;
+    auto div_ts = [&](double x) { return pow2 ? dmul(x, its) : ddiv(x, ts); };
+    const int64_t tx0 = clip_i64(np_to_i64(floor(div_ts(dsub(dsub(po.mx, po.rx), 0.5)))), 0, ntx - 1);
+    const int64_t tx1 = clip_i64(np_to_i64(floor(div_ts(dsub(dadd(po.mx, po.rx), 0.5)))), 0, ntx - 1);
+    const int64_t ty0 = clip_i64(np_to_i64(floor(div_ts(dsub(dsub(po.my, po.ry), 0.5)))), 0, nty - 1);
+    const int64_t ty1 = clip_i64(np_to_i64(floor(div_ts(dsub(dadd(po.my, po.ry), 0.5)))), 0, nty - 1);
     po_out.rects[idx] = pack_rect((int)tx0, (int)tx1, (int)ty0, (int)ty1);
   }
   if (po_out.recs) {  // debug / dump mode: the full _Projected record (render.py:89-108)

@@ -31,6 +31,10 @@ constexpr int kSortWarps = kSortThreads / 32;
 constexpr uint32_t kStFlagAgg = 1u << 30;
 constexpr uint32_t kStFlagPre = 2u << 30;
 constexpr uint32_t kStMask = (1u << 30) - 1;
+#ifndef CS_SORT_LB
+#define CS_SORT_LB 8
+#endif
+constexpr int kLookback = CS_SORT_LB;
 
 template <typename K> struct SortCfg;
 template <> struct SortCfg<uint64_t> { static constexpr int kItems = 8, kMinBlocks = 1; };
@@ -186,18 +190,20 @@ __device__ __forceinline__ void onesweep_body(
       vals_s[pos] = val[r];
     }
   }
-  // 5) decoupled look-back for this digit, four predecessors per round trip
+  // 5) decoupled look-back for this digit, kLookback predecessors per round
+  //    trip (a chunk of the first wave may have to sum hundreds of
+  //    predecessors' aggregates before any inclusive prefix exists)
   uint32_t excl = 0;
   if (chunk > 0) {
     int p = (int)chunk - 1;
     bool found = false;
     while (!found) {
-      uint32_t st[4];
+      uint32_t st[kLookback];
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < kLookback; ++k)
         st[k] = p - k >= 0 ? ld_volatile_u32(status + (size_t)(p - k) * 256 + d) : (kStFlagPre | 0u);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < kLookback; ++k) {
         if (found) break;
         const uint32_t flag = st[k] >> 30;
         if (flag == 0) break;          // not published yet: re-read from here
