@@ -18,6 +18,7 @@ from .lod import (AssembledSet, LodScene, VisibilityDecision, assemble_render_se
                   significance_scores)
 from .render import (FrameStats, RenderSettings, SplatPrimitive, project_gaussian,  # noqa: E402
                      rasterize, rasterize_stats, render)
+from .service import RenderService  # noqa: E402
 
 __version__ = "0.1.0"
 __all__ = [
@@ -25,5 +26,5 @@ __all__ = [
     "AssembledSet", "assemble_render_set", "block_visible", "decide_visibility", "select_level",
     "significance_scores", "compress", "mad_bounds", "build_lod",
     "FrameStats", "RenderSettings", "SplatPrimitive", "project_gaussian", "rasterize",
-    "rasterize_stats", "render",
+    "rasterize_stats", "render", "RenderService",
 ]

@@ -26,7 +26,10 @@
 
 namespace cs {
 
-constexpr int kBlendThreads = 256;
+#ifndef CS_BLEND_THREADS
+#define CS_BLEND_THREADS 256
+#endif
+constexpr int kBlendThreads = CS_BLEND_THREADS;
 
 // Warp-independent blend, persistent: every warp repeatedly takes the next
 // work item -- one 8x4 pixel box of one tile, tiles in heaviest-list-first

@@ -137,3 +137,8 @@ def assign_inputs(g):
 @pytest.fixture(scope="session")
 def golden_bundle():
     return Golden("bundle.npz")
+
+
+@pytest.fixture(scope="session")
+def golden_service():
+    return Golden("service.npz")

@@ -365,6 +365,45 @@ def make_lodgen():
           "zero scores:", int((scores == 0).sum()))
 
 
+def make_service():
+    """RenderService.render (service.py:195-230) of the reference on the
+    bundle scene: request bodies, decoded PNG pixels and the stats payload
+    (render_ms / fps_estimate dropped: wall-clock)."""
+    import io
+    import json
+    from PIL import Image as PilImage
+    from citysplat.service import RenderService
+    from citysplat.lod import load_lod as ref_load_lod
+    bundle = generate_synthetic_city(seed=5, extent=50.0, n_buildings=6, n_cameras=8,
+                                     target_gaussians=1500, image_size=(64, 48))
+    scene = ref_load_lod(OUT / "bundle")
+    svc = RenderService(scene, max_dim=256)
+
+    def cam_json(cam):
+        return {"width": cam.width, "height": cam.height, "fx": cam.fx, "fy": cam.fy,
+                "cx": cam.cx, "cy": cam.cy, "rotation": cam.rotation_w2c.tolist(),
+                "translation": cam.translation_w2c.tolist()}
+
+    reqs = []
+    for i in range(8):
+        reqs.append({"camera": cam_json(bundle.cameras[i].view), "want_overlay": i % 2 == 1})
+    reqs.append({"camera": cam_json(bundle.cameras[3].view), "lod": {"enabled": False}})
+    reqs.append({"camera": cam_json(bundle.cameras[5].view),
+                 "lod": {"intervals": [[0, 5], [5, 10], [10, None]]}, "want_overlay": True})
+    store = {"n": np.int64(len(reqs))}
+    for k, body in enumerate(reqs):
+        png, stats = svc.render(body)
+        px = np.asarray(PilImage.open(io.BytesIO(png)).convert("RGB"))
+        stats = {key: v for key, v in stats.items() if key not in ("render_ms", "fps_estimate")}
+        store[f"req{k}/body"] = np.array(json.dumps(body))
+        store[f"req{k}/pixels"] = px
+        store[f"req{k}/png"] = np.frombuffer(png, dtype=np.uint8)
+        store[f"req{k}/stats"] = np.array(json.dumps(stats))
+    store["scene_info"] = np.array(json.dumps(svc.scene_info()))
+    store["blocks"] = np.array(json.dumps(svc.block_geometry()))
+    np.savez_compressed(OUT / "service.npz", **store)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -376,5 +415,6 @@ if __name__ == "__main__":
     make_lodgen()
     make_assign()
     make_bundle()
+    make_service()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size // 1024, "KiB")
