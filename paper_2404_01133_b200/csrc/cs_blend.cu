@@ -341,14 +341,24 @@ static void launch_blend_t(int n_tiles, const uint32_t* list, const uint32_t* bx
 // length)) and emitted bucket-descending (order inside a bucket is arbitrary;
 // tiles are independent, so the image does not depend on it).
 __global__ void k_tile_order(const uint2* __restrict__ ranges, int n_tiles, uint32_t* __restrict__ order) {
+  // warp-aggregated shared atomics: most tiles fall into a handful of
+  // buckets, and one atomic per (warp, bucket) instead of per tile keeps the
+  // single CTA from serialising on them
   __shared__ int hist[34];
   __shared__ int cursor[34];
   if (threadIdx.x < 34) hist[threadIdx.x] = 0;
   __syncthreads();
-  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
-    const uint2 r = ranges[t];
-    const uint32_t c = r.y - r.x;
-    atomicAdd(&hist[c ? 32 - __clz(c) : 0], 1);
+  const uint32_t lt = lanemask_lt();
+  const int span = (n_tiles + blockDim.x - 1) / blockDim.x * blockDim.x;  // whole warps iterate
+  for (int t = threadIdx.x; t < span; t += blockDim.x) {
+    int bk = -1;
+    if (t < n_tiles) {
+      const uint2 r = ranges[t];
+      const uint32_t c = r.y - r.x;
+      bk = c ? 32 - __clz(c) : 0;
+    }
+    const uint32_t peers = __match_any_sync(0xffffffffu, bk);
+    if (bk >= 0 && (peers & lt) == 0) atomicAdd(&hist[bk], __popc(peers));
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -356,10 +366,19 @@ __global__ void k_tile_order(const uint2* __restrict__ ranges, int n_tiles, uint
     for (int b = 33; b >= 0; --b) { cursor[b] = acc; acc += hist[b]; }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
-    const uint2 r = ranges[t];
-    const uint32_t c = r.y - r.x;
-    order[atomicAdd(&cursor[c ? 32 - __clz(c) : 0], 1)] = (uint32_t)t;
+  for (int t = threadIdx.x; t < span; t += blockDim.x) {
+    int bk = -1;
+    if (t < n_tiles) {
+      const uint2 r = ranges[t];
+      const uint32_t c = r.y - r.x;
+      bk = c ? 32 - __clz(c) : 0;
+    }
+    const uint32_t peers = __match_any_sync(0xffffffffu, bk);
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (bk >= 0 && (int)(threadIdx.x & 31) == leader) base = atomicAdd(&cursor[bk], __popc(peers));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (bk >= 0) order[base + __popc(peers & lt)] = (uint32_t)t;
   }
 }
 

@@ -31,46 +31,74 @@ __device__ __forceinline__ bool key_less(uint64_t ka, uint32_t ia, uint64_t kb, 
   return ka < kb || (ka == kb && ia < ib);
 }
 
+// One run of equal 32-bit keys starting at rank r (r + 1 < M, k32[r + 1] ==
+// k32[r]): short runs are re-sorted in registers, long ones queued.
+__device__ __forceinline__ void fix_run(const uint32_t* __restrict__ k32, uint32_t* __restrict__ order,
+                                        const uint64_t* __restrict__ k64, int64_t M, int64_t r,
+                                        RunCtl* __restrict__ ctl, uint32_t* __restrict__ long_runs,
+                                        uint32_t long_cap) {
+  const uint32_t k = k32[r];
+  int L = 2;
+  while (L <= kShortRun && r + L < M && k32[r + L] == k) ++L;
+  if (L > kShortRun) {  // long_cap >= M / (kShortRun + 1) + 1: the queue cannot overflow
+    const uint32_t slot = atomicAdd(&ctl->n_long, 1u);
+    if (slot < long_cap) long_runs[slot] = (uint32_t)r;
+    return;
+  }
+  uint32_t id[kShortRun];
+  uint64_t key[kShortRun];
+#pragma unroll
+  for (int j = 0; j < kShortRun; ++j) {
+    if (j < L) {
+      id[j] = order[r + j];
+      key[j] = k64[id[j]];
+    }
+  }
+  // insertion sort (ids arrive ascending, so equal depths keep their order)
+#pragma unroll
+  for (int j = 1; j < kShortRun; ++j) {
+    if (j >= L) break;
+#pragma unroll
+    for (int m = j; m > 0; --m) {
+      if (key_less(key[m], id[m], key[m - 1], id[m - 1])) {
+        const uint64_t tk = key[m]; key[m] = key[m - 1]; key[m - 1] = tk;
+        const uint32_t ti = id[m]; id[m] = id[m - 1]; id[m - 1] = ti;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kShortRun; ++j)
+    if (j < L) order[r + j] = id[j];
+}
+
+// Run starts, four ranks per thread (one 16-byte key load plus the two
+// neighbours): the scan is a streaming read, the rare runs branch off.
 __global__ void k_fix_short_runs(const uint32_t* __restrict__ k32, uint32_t* __restrict__ order,
                                  const uint64_t* __restrict__ k64, const DevStats* __restrict__ stats,
                                  RunCtl* __restrict__ ctl, uint32_t* __restrict__ long_runs,
                                  uint32_t long_cap) {
   const int64_t M = stats->visible;
+  const int64_t groups = (M + 3) / 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r + 1 < M; r += stride) {
-    const uint32_t k = k32[r];
-    if (k32[r + 1] != k || (r > 0 && k32[r - 1] == k)) continue;  // not the start of a run
-    int L = 2;
-    while (L <= kShortRun && r + L < M && k32[r + L] == k) ++L;
-    if (L > kShortRun) {  // long_cap >= M / (kShortRun + 1) + 1: the queue cannot overflow
-      const uint32_t slot = atomicAdd(&ctl->n_long, 1u);
-      if (slot < long_cap) long_runs[slot] = (uint32_t)r;
-      continue;
+  for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < groups; gi += stride) {
+    const int64_t r0 = 4 * gi;
+    uint32_t k[6];  // k[0] = rank r0 - 1, k[1..4] = r0..r0+3, k[5] = r0 + 4
+    if (r0 + 4 <= M) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(k32) + gi);
+      k[1] = v.x; k[2] = v.y; k[3] = v.z; k[4] = v.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) k[1 + j] = r0 + j < M ? __ldg(k32 + r0 + j) : 0xfffffffeu - j;
     }
-    uint32_t id[kShortRun];
-    uint64_t key[kShortRun];
+    k[0] = r0 > 0 ? __ldg(k32 + r0 - 1) : ~k[1];
+    k[5] = r0 + 4 < M ? __ldg(k32 + r0 + 4) : ~k[4];
 #pragma unroll
-    for (int j = 0; j < kShortRun; ++j) {
-      if (j < L) {
-        id[j] = order[r + j];
-        key[j] = k64[id[j]];
-      }
+    for (int j = 0; j < 4; ++j) {
+      const int64_t r = r0 + j;
+      // the start of a run: equal to the next key, different from the previous
+      if (r + 1 < M && k[j + 2] == k[j + 1] && k[j] != k[j + 1])
+        fix_run(k32, order, k64, M, r, ctl, long_runs, long_cap);
     }
-    // insertion sort (ids arrive ascending, so equal depths keep their order)
-#pragma unroll
-    for (int j = 1; j < kShortRun; ++j) {
-      if (j >= L) break;
-#pragma unroll
-      for (int m = j; m > 0; --m) {
-        if (key_less(key[m], id[m], key[m - 1], id[m - 1])) {
-          const uint64_t tk = key[m]; key[m] = key[m - 1]; key[m - 1] = tk;
-          const uint32_t ti = id[m]; id[m] = id[m - 1]; id[m - 1] = ti;
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < kShortRun; ++j)
-      if (j < L) order[r + j] = id[j];
   }
 }
 
