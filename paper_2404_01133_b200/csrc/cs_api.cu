@@ -370,7 +370,7 @@ static int ensure_frame_buffers(cs_ctx* c, int64_t cap_vis, int n_segs, int n_bl
   if (c->st_sort.ensure(4 * sw)) return fail(CS_ENOMEM, "sort status");
   if (n_tiles > c->cap_tiles) {
     if (c->ranges.ensure(sizeof(uint2) * n_tiles) || c->frag_tile.ensure(4 * n_tiles) ||
-        c->tile_order.ensure(4 * (n_tiles + 2 * 34)))  // + launch_tile_order's scratch
+        c->tile_order.ensure(4 * (n_tiles + 2 * 34 * 16)))  // + launch_tile_order's scratch
       return fail(CS_ENOMEM, "tile buffers");
     c->cap_tiles = n_tiles;
   }

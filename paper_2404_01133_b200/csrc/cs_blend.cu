@@ -343,13 +343,29 @@ static void launch_blend_t(int n_tiles, const uint32_t* list, const uint32_t* bx
 // ascending tile ids inside a bucket, which the blend measured faster (L2
 // locality of neighbouring tiles' records) than the two-kernel multi-CTA
 // form (CS_TILE_ORDER_MULTI=1: 0.934 vs 0.928 ms) despite its 11 us.
-constexpr int kOrderBuckets = 34;
+
+#ifndef CS_TILE_ORDER_SHIFT
+#define CS_TILE_ORDER_SHIFT 0   // bucket = floor(log2(len)) >> shift (coarser buckets keep more raster order)
+#endif
+#ifndef CS_TILE_ORDER_SUB
+#define CS_TILE_ORDER_SUB 1     // extra mantissa bits per octave (finer heaviest-first order)
+#endif
+#ifndef CS_TILE_ORDER_RASTER
+#define CS_TILE_ORDER_RASTER 0  // 1: no reordering at all
+#endif
+constexpr int kOrderBuckets = CS_TILE_ORDER_SUB ? (34 << CS_TILE_ORDER_SUB) : 34;
 
 __device__ __forceinline__ int tile_bucket(const uint2* __restrict__ ranges, int t, int n_tiles) {
   if (t >= n_tiles) return -1;
   const uint2 r = ranges[t];
   const uint32_t c = r.y - r.x;
-  return c ? 32 - __clz(c) : 0;
+  if (CS_TILE_ORDER_RASTER) return 0;
+  if (CS_TILE_ORDER_SUB == 0) return (c ? 32 - __clz(c) : 0) >> CS_TILE_ORDER_SHIFT;
+  // finer: floor(log2 c) plus the next CS_TILE_ORDER_SUB bits of c
+  if (c < (2u << CS_TILE_ORDER_SUB)) return (int)c;
+  const int e = 31 - __clz(c);  // >= SUB + 1
+  const int m = (int)((c >> (e - CS_TILE_ORDER_SUB)) & ((1u << CS_TILE_ORDER_SUB) - 1u));
+  return (2 << CS_TILE_ORDER_SUB) + ((e - CS_TILE_ORDER_SUB - 1) << CS_TILE_ORDER_SUB) + m;
 }
 
 __global__ void k_tile_hist(const uint2* __restrict__ ranges, int n_tiles, int* __restrict__ hist) {
