@@ -319,6 +319,8 @@ def main():
     seg_idx = (ctypes.c_int32 * 4096)()
     seg_cnt = (ctypes.c_int64 * 4096)()
     n_seg = ctypes.c_int32(0)
+    blend_item_max = []  # longest blend work item per frame, SM clocks (DIAG)
+    blend_item_sum = []  # sum over the frame's blend work items
     for i in range(K):
         s = CsFrameStats()
         frame(i, _lib.CS_RENDER_SYNC | _lib.CS_RENDER_DIAG, s)
@@ -329,6 +331,8 @@ def main():
         counts["fragments"] += s.fragments
         counts["warp_hits"] += s.warp_hits
         counts["warp_hits_empty"] += s.warp_hits_empty
+        blend_item_max.append(s.blend_max_item_cycles)
+        blend_item_sum.append(s.blend_item_cycles)
         # SH rows are read for visible splats; their width depends on the level
         # (C = 16/9/4 -> 192/112/48 B): weight by this frame's assembled level mix
         _lib.check(lib.cs_dump_segments(ctx, seg_idx, seg_cnt, 4096, ctypes.byref(n_seg), sh))
@@ -520,6 +524,10 @@ def main():
                        "scene_build_s": round(build_s, 1)},
             "stages_ms": stages_ms,
             "counts_per_frame": {k: v / K for k, v in counts.items()},
+            "blend_longest_item_us": (round(float(np.median(blend_item_max)) / ((clocks or {}).get("sm_mhz") or 1965.0), 1)
+                                      if blend_item_max else None),
+            "blend_item_us_sum_per_warp_slot": (round(float(np.median(blend_item_sum)) / ((clocks or {}).get("sm_mhz") or 1965.0)
+                                                      / lib_blend_slots(), 1) if blend_item_sum else None),
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -662,6 +670,12 @@ def train_leg(args, raw, wh, rank, world, dev):
                    "setup_s": round(setup_s, 1)},
         "fusion_all_gather_ms": fuse_ms, "fused_gaussians": fused_n,
     }
+
+
+def lib_blend_slots() -> int:
+    """Resident blend warps on the GPU (148 SMs x CTAs/SM x 8 warps)."""
+    import torch
+    return torch.cuda.get_device_properties(0).multi_processor_count * 3 * 8
 
 
 def launches_per_frame() -> int:

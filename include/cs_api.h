@@ -84,6 +84,8 @@ typedef struct cs_frame_stats {
   int64_t evals;            /* blend evaluations E (pixel x splat pairs walked; CS_RENDER_DIAG only) */
   int64_t warp_hits;        /* blend (8x4 pixel box, splat) pairs evaluated by a warp */
   int64_t warp_hits_empty;  /* ... of which no live pixel passed the alpha-floor test (CS_RENDER_DIAG only) */
+  int64_t blend_max_item_cycles; /* longest blend work item (one pixel box), SM clocks (CS_RENDER_DIAG only) */
+  int64_t blend_item_cycles;     /* sum over the blend's work items, SM clocks (CS_RENDER_DIAG only) */
 } cs_frame_stats;
 
 /* One block decision, VisibilityDecision (lod.py:255-264). level -1 = None. */

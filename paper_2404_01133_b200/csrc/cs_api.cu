@@ -561,6 +561,9 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
   return CS_OK;
 }
 
+static_assert(offsetof(DevStats, blend_max_item_cycles) == offsetof(cs_frame_stats, blend_max_item_cycles) &&
+                  sizeof(cs_frame_stats) <= offsetof(DevStats, pairs_eff) + sizeof(int64_t),
+              "DevStats must lead with the cs_frame_stats layout");
 static int fetch_stats(cs_ctx* c, cudaStream_t s) {
   // DevStats and cs_frame_stats share the leading layout
   CS_CUDA(cudaMemcpyAsync(c->h_stats, c->stats.p, sizeof(cs_frame_stats), cudaMemcpyDeviceToHost, s));

@@ -81,6 +81,7 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
     if (lane == 0) item = (int)atomicAdd(&stats->tickets[4], 1u);
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item >= n_items) break;
+    const long long item_t0 = DIAG ? clock64() : 0;
     const int tr = item / nboxes, b = item - tr * nboxes;
     const int t = tile_order ? (int)tile_order[tr] : tr;
     const int tx = t % bp.ntx, ty = t / bp.ntx;
@@ -297,6 +298,11 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
     const int box_frags = warp_sum(box_cnt);
     frags += box_frags;
     if (lane == 0 && box_frags) atomicAdd(frag_tile + t, box_frags);
+    if (DIAG && lane == 0) {
+      const unsigned long long dt = (unsigned long long)(clock64() - item_t0);
+      atomicMax(reinterpret_cast<unsigned long long*>(&stats->blend_max_item_cycles), dt);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&stats->blend_item_cycles), dt);
+    }
   }
   const long long wevals = warp_sum((long long)evals);
   if (lane == 0) {

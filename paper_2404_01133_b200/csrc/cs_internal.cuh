@@ -76,6 +76,8 @@ struct DevStats {     // device mirror of cs_frame_stats + scratch counters
   int64_t evals;         // blend (pixel, splat) evaluations executed (E)
   int64_t warp_hits;     // blend (box, splat) warp evaluations
   int64_t warp_hits_empty;  // ... where no live pixel passed the fast reject
+  int64_t blend_max_item_cycles;  // longest blend work item (DIAG)
+  int64_t blend_item_cycles;      // sum over blend work items (DIAG)
   int64_t pairs_eff;     // pairs actually processed (0 when the pair buffer overflowed)
   uint32_t tickets[16];  // chunk tickets for single-pass kernels, zeroed per frame
 };
