@@ -200,6 +200,14 @@ int cs_render_backward(cs_ctx* ctx, const cs_source* src, const cs_camera* cam,
 int cs_timing_begin(cs_ctx* ctx, int32_t max_frames);
 int cs_timing_end(cs_ctx* ctx, double* stage_ms, int32_t* frames);
 
+/* Frame graphs (no reference counterpart; B200 launch path): an asynchronous
+ * cs_render (no SYNC/DEBUG/DIAG/KEEP_STATE flag, no stats, no timing) whose
+ * source, settings, resolution, output, stream and buffer capacities repeat
+ * is captured once into a CUDA graph and replayed with only the camera
+ * parameters patched.  Returns the number of graphs cached by the context
+ * (diagnostics); set CS_NO_GRAPH in the environment to disable. */
+int cs_frame_graphs(cs_ctx* ctx);
+
 /* Stats of the last frame (synchronises the stream). */
 int cs_frame_stats_get(cs_ctx* ctx, cs_frame_stats* out, void* stream);
 

@@ -97,6 +97,7 @@ _SIGS = {
                                           ctypes.POINTER(CsSettings), vp, ctypes.POINTER(CsGrads), vp]),
     "cs_timing_begin": (ctypes.c_int, [vp, i32]),
     "cs_timing_end": (ctypes.c_int, [vp, vp, vp]),
+    "cs_frame_graphs": (ctypes.c_int, [vp]),
     "cs_dump_projected": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "cs_dump_tiles": (ctypes.c_int, [vp, vp, vp, vp]),
     "cs_dump_segments": (ctypes.c_int, [vp, vp, vp, i32, vp, vp]),

@@ -15,7 +15,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -64,6 +66,8 @@ void launch_activate_geom(int64_t K, const float* geom, float4* pos_op, float4* 
                           cudaStream_t s);
 // cs_bin.cu
 int64_t bin_chunks(int64_t capacity);
+const void* lod_select_kernel();
+const void* project_kernel();
 int64_t bin_status_words(int64_t capacity);
 void launch_bin_pairs(const uint32_t* order, const uint2* rects, DevStats* stats, int64_t pair_cap,
                       int64_t capacity, uint64_t* status, int ntx, uint32_t* keys, uint32_t* vals,
@@ -178,6 +182,7 @@ struct DBuf {
 
 struct cs_lod {
   cs_ctx* ctx = nullptr;
+  uint64_t serial = 0;  // unique per scene (frame-graph cache key)
   int n_levels = 0, n_blocks = 0;
   std::vector<cs_cloud> clouds;
   std::vector<int64_t> counts;
@@ -223,6 +228,34 @@ struct cs_ctx {
   const uint2* last_ranges = nullptr;
   int last_tiles = 0;
   int last_width = 0, last_height = 0;
+  // frame graph (see cs_render): the last eligible call's key, and the
+  // captured, instantiated frame for it with the camera-carrying kernel nodes
+  struct FrameKey {
+    cs_source src;
+    cs_settings st;
+    uint64_t lod_serial;
+    int width, height;
+    uint32_t flags;
+    void* out;
+    cudaStream_t stream;
+    int64_t cap_vis, cap_pairs, cap_pw, cap_tiles;
+  };
+  struct CamNode {
+    cudaGraphNode_t node;
+    cudaKernelNodeParams params;
+    std::vector<void*> args;
+    int cam_arg;
+  };
+  struct FrameGraph {
+    FrameKey key;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    std::vector<CamNode> cam_nodes;
+  };
+  std::vector<FrameGraph> graphs;   // most recent last (double-buffered outputs: 2 keys)
+  std::vector<FrameKey> seen;       // recent eligible keys (capture on the second sighting)
+  cudaStream_t capture_stream = nullptr;
+  cs_camera graph_cam{};
   // per-stage CUDA-event timing (cs_timing_begin/end)
   bool timing_on = false;
   int timing_max = 0, timing_frame = 0;
@@ -278,6 +311,11 @@ void cs_destroy(cs_ctx* c) {
   for (DBuf* b : all) b->release();
   if (c->h_stats) cudaFreeHost(c->h_stats);
   for (cudaEvent_t e : c->tev) cudaEventDestroy(e);
+  for (auto& g : c->graphs) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+  }
+  if (c->capture_stream) cudaStreamDestroy(c->capture_stream);
   delete c;
 }
 
@@ -290,6 +328,8 @@ int cs_lod_create(cs_ctx* ctx, const cs_lod_desc* d, cs_lod** out) {
   CS_CUDA(cudaSetDevice(ctx->device));
   cs_lod* L = new cs_lod();
   L->ctx = ctx;
+  static std::atomic<uint64_t> next_serial{1};
+  L->serial = next_serial++;
   L->n_levels = d->n_levels;
   L->n_blocks = d->n_blocks;
   const int LJ = d->n_levels * d->n_blocks;
@@ -571,6 +611,116 @@ static int fetch_stats(cs_ctx* c, cudaStream_t s) {
   return CS_OK;
 }
 
+// Frame graphs.  A frame is ~18 kernels and ~10 memsets whose sizes all live
+// in device memory, so it is graph-capturable; only the camera differs
+// between the frames of a flythrough, and it reaches the device solely as a
+// kernel parameter of K1 (k_lod_select) and K3 (k_project).  When two
+// consecutive asynchronous calls share everything but the camera pose (same
+// source, settings, resolution, output, stream and buffer capacities), the
+// frame is captured once on a private stream and instantiated; later calls
+// patch the two camera parameters with cudaGraphExecKernelNodeSetParams and
+// launch the graph on the caller's stream -- the same kernels on the same
+// buffers, without per-kernel launch gaps.  Synchronous, stats, debug,
+// diagnostics, kept-state and timed frames always take the direct path.
+static bool graph_eligible(const cs_ctx* c, const cs_source* src, uint32_t flags,
+                           const cs_frame_stats* stats_host) {
+  const uint32_t direct = CS_RENDER_SYNC | CS_RENDER_DEBUG | CS_RENDER_PROJECT_ONLY | CS_RENDER_DIAG |
+                          CS_RENDER_KEEP_STATE;
+  if (std::getenv("CS_NO_GRAPH")) return false;
+  return !(flags & direct) && !stats_host && !c->timing_on &&
+         (src->kind == CS_SRC_LOD_BLOCK || src->kind == CS_SRC_CLOUD);
+}
+
+static cs_ctx::FrameKey frame_key(const cs_ctx* c, const cs_source* src, const cs_camera* cam,
+                                  const cs_settings* st, void* out, uint32_t flags, cudaStream_t s) {
+  cs_ctx::FrameKey k;
+  std::memset(&k, 0, sizeof(k));
+  std::memcpy(&k.src, src, sizeof(cs_source));
+  std::memcpy(&k.st, st, sizeof(cs_settings));
+  k.lod_serial = src->kind == CS_SRC_CLOUD ? 0 : src->lod->serial;
+  k.width = cam->width;
+  k.height = cam->height;
+  k.flags = flags;
+  k.out = out;
+  k.stream = s;
+  k.cap_vis = c->cap_vis; k.cap_pairs = c->cap_pairs; k.cap_pw = c->cap_pw; k.cap_tiles = c->cap_tiles;
+  return k;
+}
+
+static bool same_key(const cs_ctx::FrameKey& a, const cs_ctx::FrameKey& b) {
+  return std::memcmp(&a, &b, sizeof(a)) == 0;
+}
+
+constexpr size_t kMaxGraphs = 4;
+
+static int capture_graph(cs_ctx* c, const cs_source* src, const cs_camera* cam, const cs_settings* st,
+                         void* out, uint32_t flags, const cs_ctx::FrameKey& key) {
+  if (!c->capture_stream) CS_CUDA(cudaStreamCreateWithFlags(&c->capture_stream, cudaStreamNonBlocking));
+  CS_CUDA(cudaStreamBeginCapture(c->capture_stream, cudaStreamCaptureModeThreadLocal));
+  const int rc = render_once(c, src, cam, st, out, flags, c->capture_stream);
+  cudaGraph_t g = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(c->capture_stream, &g);
+  if (rc || ce != cudaSuccess || !g) {
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    return rc ? rc : CS_OK;  // not capturable: stay on the direct path
+  }
+  cs_ctx::FrameGraph fg;
+  fg.key = key;
+  fg.graph = g;
+  size_t n = 0;
+  CS_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  CS_CUDA(cudaGraphGetNodes(g, nodes.data(), &n));
+  const void* f_sel = lod_select_kernel();
+  const void* f_proj = project_kernel();
+  for (cudaGraphNode_t nd : nodes) {
+    cudaGraphNodeType t;
+    CS_CUDA(cudaGraphNodeGetType(nd, &t));
+    if (t != cudaGraphNodeTypeKernel) continue;
+    cudaKernelNodeParams p;
+    CS_CUDA(cudaGraphKernelNodeGetParams(nd, &p));
+    // argument index of the cs_camera (k_lod_select(T, cam, ...),
+    // k_project(clouds, segs, stats, cam, ...)) and the argument count
+    int cam_arg = -1, n_args = 0;
+    if (p.func == f_sel) { cam_arg = 1; n_args = 6; }
+    if (p.func == f_proj) { cam_arg = 3; n_args = 7; }
+    if (cam_arg < 0) continue;
+    cs_ctx::CamNode cn;
+    cn.node = nd;
+    cn.params = p;
+    cn.args.assign(p.kernelParams, p.kernelParams + n_args);
+    cn.cam_arg = cam_arg;
+    fg.cam_nodes.push_back(cn);
+  }
+  if (fg.cam_nodes.empty() || cudaGraphInstantiate(&fg.exec, g, 0) != cudaSuccess) {
+    cudaGraphDestroy(g);
+    cudaGetLastError();
+    return CS_OK;
+  }
+  if (c->graphs.size() >= kMaxGraphs) {
+    cudaGraphExecDestroy(c->graphs.front().exec);
+    cudaGraphDestroy(c->graphs.front().graph);
+    c->graphs.erase(c->graphs.begin());
+  }
+  c->graphs.push_back(std::move(fg));
+  return CS_OK;
+}
+
+static int replay_graph(cs_ctx* c, cs_ctx::FrameGraph& fg, const cs_camera* cam, cudaStream_t s) {
+  c->graph_cam = *cam;
+  for (cs_ctx::CamNode& cn : fg.cam_nodes) {
+    cn.args[cn.cam_arg] = &c->graph_cam;
+    cudaKernelNodeParams p = cn.params;
+    p.kernelParams = cn.args.data();
+    CS_CUDA(cudaGraphExecKernelNodeSetParams(fg.exec, cn.node, &p));
+  }
+  CS_CUDA(cudaGraphLaunch(fg.exec, s));
+  return CS_OK;
+}
+
+int cs_frame_graphs(cs_ctx* c) { return c ? (int)c->graphs.size() : 0; }
+
 int cs_render(cs_ctx* c, const cs_source* src, const cs_camera* cam, const cs_settings* st,
               void* out, uint32_t flags, cs_frame_stats* stats_host, void* stream) {
   if (!c || !src || !out) return fail(CS_EINVAL, "NULL argument");
@@ -579,6 +729,21 @@ int cs_render(cs_ctx* c, const cs_source* src, const cs_camera* cam, const cs_se
   std::lock_guard<std::mutex> lock(c->mu);
   CS_CUDA(cudaSetDevice(c->device));
   cudaStream_t s = (cudaStream_t)stream;
+  if (graph_eligible(c, src, flags, stats_host)) {
+    const cs_ctx::FrameKey key = frame_key(c, src, cam, st, out, flags, s);
+    for (cs_ctx::FrameGraph& fg : c->graphs)
+      if (same_key(key, fg.key)) return replay_graph(c, fg, cam, s);
+    rc = render_once(c, src, cam, st, out, flags, s);
+    if (rc) return rc;
+    // capture on the second sighting of a key whose buffers are already sized
+    const cs_ctx::FrameKey after = frame_key(c, src, cam, st, out, flags, s);
+    bool seen = false;
+    for (const cs_ctx::FrameKey& k : c->seen) seen |= same_key(k, after);
+    if (seen && same_key(after, key)) return capture_graph(c, src, cam, st, out, flags, after);
+    c->seen.push_back(after);
+    if (c->seen.size() > kMaxGraphs) c->seen.erase(c->seen.begin());
+    return CS_OK;
+  }
   for (int attempt = 0; attempt < 4; ++attempt) {
     rc = render_once(c, src, cam, st, out, flags, s);
     if (rc) return rc;

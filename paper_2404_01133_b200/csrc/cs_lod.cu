@@ -211,6 +211,8 @@ __global__ void k_select_level(int n, const double* d, int ni, const double* iv,
   out[j] = x < 0.0 ? -2 : select_level_dev(x, iv, ni);
 }
 
+const void* lod_select_kernel() { return reinterpret_cast<const void*>(&k_lod_select); }
+
 void launch_lod_select(const LodTables& T, const cs_camera& cam, int force_level,
                        cs_decision* dec, Seg* segs, DevStats* stats, cudaStream_t s) {
   k_lod_select<<<1, 256, 0, s>>>(T, cam, force_level, dec, segs, stats);

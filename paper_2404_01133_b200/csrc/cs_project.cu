@@ -465,6 +465,8 @@ __global__ void k_setup_cloud(cs_cloud c, cs_cloud* clouds, Seg* segs, DevStats*
   stats->assembled = c.count;
 }
 
+const void* project_kernel() { return reinterpret_cast<const void*>(&k_project); }
+
 void launch_project(const cs_cloud* d_clouds, const Seg* d_segs, DevStats* d_stats,
                     const cs_camera& cam, const cs_settings& st, int64_t capacity,
                     const ProjOutputs& out, const uint64_t* list, cudaStream_t s) {
