@@ -1,15 +1,18 @@
 // cs_sort.cu -- K4/K7: stable LSD radix sort (onesweep-style), device-side count.
 //
 // Used for the global depth order (np.argsort(depths, kind="stable"),
-// render.py:176-177; 64-bit keys = IEEE bits of positive float64 depths) and
-// for the stable tile grouping (np.argsort(tiles, kind="stable"),
-// render.py:245; keys = tile id, only ceil(log2 n_tiles) bits sorted).
+// render.py:176-177; the 32-bit coarsened depth key of cs_project.cu, exact
+// order restored by K4b in cs_depth.cu), for the stable tile grouping
+// (np.argsort(tiles, kind="stable"), render.py:245; keys = tile id, only
+// ceil(log2 n_tiles) bits sorted) and, with 64-bit keys, for the LoD
+// generation's priority and block orders (cs_lodgen.cu).
 //
 // Per pass one kernel reads keys+values once and writes them once:
 //   * chunks of kTile elements are taken in launch order (ticket counter);
-//   * each warp ranks its keys stably with __match_any_sync and per-warp
-//     digit counters; warps are combined in warp order, so the chunk-local
-//     order equals the input order within every digit (stability);
+//   * each warp ranks its keys stably from NB ballots over the digit bits
+//     (the peer mask of every key) and per-warp digit counters; warps are
+//     combined in warp order, so the chunk-local order equals the input order
+//     within every digit (stability);
 //   * per-digit chunk counts are published and a decoupled look-back per
 //     digit gives the chunk's global offset (no separate scan pass);
 //   * keys are first scattered to shared memory in digit order, then written
