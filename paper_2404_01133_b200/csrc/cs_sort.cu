@@ -39,6 +39,36 @@ constexpr uint32_t kStMask = (1u << 30) - 1;
 #endif
 constexpr int kLookback = CS_SORT_LB;
 
+// Programmatic dependent launch between the passes (CS_SORT_PDL): a pass is
+// launched while its predecessor drains, its CTAs wait at griddepcontrol.wait
+// (predecessor complete, memory visible) before touching any data, and every
+// CTA lets its dependents launch as soon as it starts.
+#ifndef CS_SORT_PDL
+#define CS_SORT_PDL 1
+#endif
+__device__ __forceinline__ void pdl_wait() {
+  if (CS_SORT_PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_trigger() {
+  if (CS_SORT_PDL) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... Params, typename... Args>
+static void launch_pdl(void (*kernel)(Params...), unsigned grid, unsigned block, cudaStream_t s,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = CS_SORT_PDL ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 template <typename K> struct SortCfg;
 template <> struct SortCfg<uint64_t> { static constexpr int kItems = 8, kMinBlocks = 1; };
 template <> struct SortCfg<uint32_t> { static constexpr int kItems = 16, kMinBlocks = 3; };
@@ -71,6 +101,8 @@ k_radix_hist(const K* __restrict__ keys, const int64_t* __restrict__ n_ptr, int 
 // status clear nor the pass grids scale with the buffer capacity
 __global__ void k_radix_hist_scan(uint32_t* hist, int n_passes, uint32_t* __restrict__ status,
                                   const int64_t* __restrict__ n_ptr, int tile) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ uint32_t scratch[kSortWarps + 1];
   if (blockIdx.x == 0) {
     for (int p = 0; p < n_passes; ++p) {
@@ -250,6 +282,8 @@ k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
   __shared__ K keys_s[kTile];
   __shared__ uint32_t vals_s[kTile];
 
+  pdl_wait();
+  pdl_trigger();
   const uint32_t n = (uint32_t)*n_ptr;
   status += (size_t)pass * ((n + kTile - 1) / kTile) * 256;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -307,8 +341,8 @@ static void launch_pass(unsigned chunks, cudaStream_t s, const K* kin, const uin
     wave = std::max(1, per_sm * sms);
   }
   const unsigned g = CS_SORT_PERSIST ? std::min<unsigned>(chunks, (unsigned)wave) : chunks;
-  k_onesweep<K, ITEMS, MINB, NB, EARLY><<<g, kSortThreads, 0, s>>>(kin, vin, kout, vout, n_dev,
-                                                                  shift, hist, status, pass, ticket);
+  launch_pdl(k_onesweep<K, ITEMS, MINB, NB, EARLY>, g, kSortThreads, s, kin, vin, kout, vout, n_dev,
+             shift, hist, status, pass, ticket);
 }
 
 template <typename K, int ITEMS, int MINB = SortCfg<K>::kMinBlocks, bool EARLY = true>
@@ -327,8 +361,8 @@ int radix_sort_items(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_
     int hist_grid = (int)std::min<int64_t>(148 * 4, (capacity + kSortThreads - 1) / kSortThreads);
     k_radix_hist<K><<<hist_grid, kSortThreads, 0, s>>>(k0, n_dev, begin_bit, n_passes, width, end_bit, hist);
   }
-  k_radix_hist_scan<<<(unsigned)std::min<int64_t>(148 * 2, chunks), 256, 0, s>>>(hist, n_passes, status,
-                                                                                n_dev, kTile);
+  launch_pdl(k_radix_hist_scan, (unsigned)std::min<int64_t>(148 * 2, chunks), 256, s, hist, n_passes,
+             status, n_dev, (int)kTile);
   K* kin = k0; K* kout = k1;
   uint32_t* vin = v0; uint32_t* vout = v1;
   for (int p = 0; p < n_passes; ++p) {
