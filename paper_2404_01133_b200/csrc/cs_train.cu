@@ -33,7 +33,13 @@ namespace cs {
 
 constexpr int kWin = 11;
 constexpr int kHalo = kWin - 1;
-constexpr int kTX = 32, kTY = 16;
+#ifndef CS_SSIM_TX
+#define CS_SSIM_TX 16
+#endif
+#ifndef CS_SSIM_TY
+#define CS_SSIM_TY 32
+#endif
+constexpr int kTX = CS_SSIM_TX, kTY = CS_SSIM_TY;  // output tile of both loss kernels
 constexpr int kRX = kTX + kHalo, kRY = kTY + kHalo;  // 42 x 26 region
 constexpr int kLossThreads = 256;
 constexpr float kC1 = 0.01f * 0.01f, kC2 = 0.03f * 0.03f;
