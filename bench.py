@@ -38,6 +38,9 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 LOD_BUILD = None
+# stage marks of cs_render; since K5+K6 were fused (k_bin_pairs + k_emit_heavy) all
+# pair emission is timed under "gather_scan" and "duplicate" is an empty slot kept
+# so the JSON schema stays comparable across rounds
 STAGES = ("select", "project", "depth_sort", "gather_scan", "duplicate", "tile_sort", "ranges", "blend")
 SCENES = {
     # name: (gaussians, extent, buildings, blocks, intervals, altitudes, W, H)
