@@ -77,58 +77,73 @@ __device__ __forceinline__ int select_level_dev(double d, const double* iv, int 
   return -1;
 }
 
-// One CTA: all block decisions, then the ascending-block segment table.
-__global__ void k_lod_select(LodTables T, cs_camera cam, int force_level,
-                             cs_decision* __restrict__ dec, Seg* __restrict__ segs,
-                             DevStats* __restrict__ stats) {
+// One CTA: the block decisions, 256 blocks at a time, and the ascending-block
+// segment table from two block scans (pieces kept, rows) -- no serial walk
+// over the decisions (that walk, one thread re-reading every decision and
+// piece count, was most of this kernel's 21 us).
+__global__ void __launch_bounds__(256) k_lod_select(LodTables T, cs_camera cam, int force_level,
+                                                    cs_decision* __restrict__ dec, Seg* __restrict__ segs,
+                                                    DevStats* __restrict__ stats) {
+  __shared__ unsigned int s_scan_n[9];
+  __shared__ unsigned long long s_scan_c[9];
   const int J = T.n_blocks;
-  for (int j = threadIdx.x; j < J; j += blockDim.x) {
-    cs_decision d;
-    d.level = -1;
-    d.visible = 0;
-    d.has_box = 0;
-    d.pad[0] = d.pad[1] = 0;
-    d.box[0] = d.box[1] = d.box[2] = d.box[3] = 0.0;
-    if (!T.occupied[j]) {  // lod.py:334-336
-      d.distance = __longlong_as_double(0x7ff0000000000000ll);
-    } else {
-      bool vis;
-      double dist, box[4];
-      block_decision(T.bmin + 3 * j, T.bmax + 3 * j, cam, vis, dist, box);
-      d.distance = dist;
-      if (vis) {
-        d.visible = 1;
-        d.has_box = 1;
-        for (int a = 0; a < 4; ++a) d.box[a] = box[a];
-        if (force_level >= 0) {
-          d.level = force_level;  // lod.py:342-345
-        } else {
-          d.level = select_level_dev(dist, T.intervals, T.n_levels);
-          if (d.level < 0) atomicOr(&stats->status, 2);  // ValueError in select_level
+  unsigned int n_base = 0;
+  unsigned long long start_base = 0;
+  for (int j0 = 0; j0 < J; j0 += blockDim.x) {
+    const int j = j0 + threadIdx.x;
+    unsigned int keep = 0;
+    unsigned long long cnt = 0;
+    int ci = 0;
+    if (j < J) {
+      cs_decision d;
+      d.level = -1;
+      d.visible = 0;
+      d.has_box = 0;
+      d.pad[0] = d.pad[1] = 0;
+      d.box[0] = d.box[1] = d.box[2] = d.box[3] = 0.0;
+      if (!T.occupied[j]) {  // lod.py:334-336
+        d.distance = __longlong_as_double(0x7ff0000000000000ll);
+      } else {
+        bool vis;
+        double dist, box[4];
+        block_decision(T.bmin + 3 * j, T.bmax + 3 * j, cam, vis, dist, box);
+        d.distance = dist;
+        if (vis) {
+          d.visible = 1;
+          d.has_box = 1;
+          for (int a = 0; a < 4; ++a) d.box[a] = box[a];
+          if (force_level >= 0) {
+            d.level = force_level;  // lod.py:342-345
+          } else {
+            d.level = select_level_dev(dist, T.intervals, T.n_levels);
+            if (d.level < 0) atomicOr(&stats->status, 2);  // ValueError in select_level
+          }
         }
       }
+      dec[j] = d;
+      if (d.visible && d.level >= 0 && d.level < T.n_levels) {
+        ci = d.level * J + j;
+        cnt = (unsigned long long)T.clouds[ci].count;
+        keep = cnt > 0 ? 1u : 0u;  // empty pieces dropped (lod.py:375-377)
+      }
     }
-    dec[j] = d;
+    unsigned int n_tot;
+    unsigned long long c_tot;
+    const unsigned int pos = block_excl_scan<unsigned int>(keep, s_scan_n, n_tot);
+    const unsigned long long off = block_excl_scan<unsigned long long>(keep ? cnt : 0ull, s_scan_c, c_tot);
+    if (keep) {  // ascending block order = concatenation order (lod.py:373-377)
+      Seg& sg = segs[n_base + pos];
+      sg.start = (int64_t)(start_base + off);
+      sg.count = (int64_t)cnt;
+      sg.cloud = ci;
+      sg.pad = 0;
+    }
+    n_base += n_tot;
+    start_base += c_tot;
   }
-  __syncthreads();
   if (threadIdx.x == 0) {
-    int n = 0;
-    int64_t start = 0;
-    for (int j = 0; j < J; ++j) {
-      const cs_decision d = dec[j];
-      if (!d.visible || d.level < 0 || d.level >= T.n_levels) continue;
-      const int ci = d.level * J + j;
-      const int64_t cnt = T.clouds[ci].count;
-      if (cnt == 0) continue;  // empty pieces dropped (lod.py:375-377)
-      segs[n].start = start;
-      segs[n].count = cnt;
-      segs[n].cloud = ci;
-      segs[n].pad = 0;
-      ++n;
-      start += cnt;
-    }
-    stats->n_segs = n;
-    stats->assembled = start;
+    stats->n_segs = (int)n_base;
+    stats->assembled = (int64_t)start_base;
   }
 }
 
