@@ -158,11 +158,16 @@ static int fail(int code, const char* fmt, ...) {
 #define CS_CHECK_LAUNCH() CS_CUDA(cudaGetLastError())
 
 // A growable device buffer.
+// Bumped whenever any device buffer is (re)allocated or freed: part of the
+// frame-graph key, so a captured frame never replays with a stale pointer.
+static std::atomic<uint64_t> g_buf_generation{1};
+
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
   cudaError_t ensure(size_t want) {
     if (want <= bytes) return cudaSuccess;
+    g_buf_generation++;
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
@@ -172,7 +177,10 @@ struct DBuf {
     return e;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      g_buf_generation++;
+      cudaFree(p);
+    }
     p = nullptr;
     bytes = 0;
   }
@@ -239,6 +247,7 @@ struct cs_ctx {
     void* out;
     cudaStream_t stream;
     int64_t cap_vis, cap_pairs, cap_pw, cap_tiles;
+    uint64_t buf_generation;
   };
   struct CamNode {
     cudaGraphNode_t node;
@@ -644,6 +653,7 @@ static cs_ctx::FrameKey frame_key(const cs_ctx* c, const cs_source* src, const c
   k.out = out;
   k.stream = s;
   k.cap_vis = c->cap_vis; k.cap_pairs = c->cap_pairs; k.cap_pw = c->cap_pw; k.cap_tiles = c->cap_tiles;
+  k.buf_generation = g_buf_generation.load();
   return k;
 }
 

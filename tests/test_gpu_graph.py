@@ -64,3 +64,32 @@ def test_graph_replay_matches_direct_cloud(golden_bundle):
     graph = _render_all(cloud, cams, graphs=True)
     for a, b in zip(direct, graph):
         assert np.array_equal(a, b)
+
+
+def test_graph_not_replayed_after_buffer_reallocation():
+    """A captured frame must not replay over workspace buffers another render
+    on the same context has since reallocated (key carries the allocation
+    generation): cloud frames -> a bigger LoD scene -> the cloud again."""
+    from paper_2404_01133_b200 import bundle, render
+    from paper_2404_01133_b200.lod import AssembledCloud
+    from paper_2404_01133_b200.synth import orbit_cameras
+    cloud = bundle.load_lod(GOLDEN / "bundle").full
+    cams = orbit_cameras(np.zeros(3), 20.0, 25.0, 3, 96, 64)
+    out = torch.empty((64, 96, 3), dtype=torch.float32, device="cuda")
+    for cam in cams:  # capture for the cloud source
+        render(cloud, cam, out=out)
+    # a larger render on the same context: grows the frame workspace
+    scene = bundle.load_lod_device(GOLDEN / "bundle")
+    big = orbit_cameras(np.zeros(3), 20.0, 25.0, 1, 640, 480)[0]
+    render(AssembledCloud(scene, big, "block", None, 0, []), big)
+    got = []
+    for cam in cams:
+        render(cloud, cam, out=out)
+        got.append(out.clone())
+    os.environ["CS_NO_GRAPH"] = "1"
+    try:
+        for cam, g in zip(cams, got):
+            render(cloud, cam, out=out)
+            assert torch.equal(out, g)
+    finally:
+        os.environ.pop("CS_NO_GRAPH", None)
