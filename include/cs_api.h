@@ -127,13 +127,18 @@ typedef struct cs_source {
    * cloud.take(nonzero(mask == 0)), the "rest" cloud of assign_b1
    * (partition.py:332-333), without materialising it */
   const uint8_t* exclude;
+  /* CS_SRC_LOD_* only, optional (NULL = the render camera): the camera the LoD
+   * selection runs for.  An AssembledSet (lod.py:351-401) is fixed by the
+   * camera it was assembled for; rendering it from another camera must draw
+   * that set, not re-select for the render camera. */
+  const struct cs_camera* select_cam;
 } cs_source;
 
 /* cs_render flags */
 #define CS_RENDER_SYNC 1u        /* synchronise, grow buffers and re-run on overflow */
 #define CS_RENDER_F64_OUT 2u     /* out_rgb is double (compatibility tier) */
 #define CS_RENDER_NO_CLIP 4u     /* leave the image unclipped */
-#define CS_RENDER_KEEP_STATE 8u  /* keep per-pixel state for cs_render_backward */
+#define CS_RENDER_KEEP_STATE 8u  /* internal: cs_render_train's kept state (cs_render rejects it) */
 #define CS_RENDER_PROJECT_ONLY 16u /* stop after projection + depth order (cs_dump_projected) */
 #define CS_RENDER_DEBUG 32u        /* also keep the full projected records (cs_dump_projected) */
 #define CS_RENDER_DIAG 64u         /* also count evals and warp_hits_empty (blend diagnostics, slower) */
@@ -186,13 +191,25 @@ typedef struct cs_grads {
   float* sh;
 } cs_grads;
 
-/* Backward of the last cs_render on this context (which must have used
- * CS_RENDER_KEEP_STATE with the same single-cloud source, camera and settings):
- * dL/dimage (device (H,W,3) float32) -> parameter gradients.  Not in the
- * reference; semantics in SURVEY.md Appendix A. */
-int cs_render_backward(cs_ctx* ctx, const cs_source* src, const cs_camera* cam,
-                       const cs_settings* st, const float* dl_dimg, const cs_grads* out,
+/* Training forward: rasterize_stats of one cloud (single-cloud source) that
+ * keeps what its backward needs.  The frame's workspace (pair lists,
+ * records, per-pixel transmittance / last fragment / colour) is handed to the
+ * returned state, so other renders on the context -- further training
+ * forwards for a multi-view loss, logging renders, graph replays -- use
+ * other workspaces and never overwrite it.  flags: CS_RENDER_SYNC,
+ * CS_RENDER_NO_CLIP.  Release with cs_state_release. */
+typedef struct cs_state cs_state;
+int cs_render_train(cs_ctx* ctx, const cs_source* src, const cs_camera* cam, const cs_settings* st,
+                    float* out_rgb, uint32_t flags, cs_state** state_out, void* stream);
+/* dL/dimage (device (H,W,3) float32) of that forward -> parameter gradients.
+ * Waits for the forward to complete (not for the work after it) and fails
+ * with CS_ENOMEM if the forward overflowed its pair buffer (the image and the
+ * gradients of that step are invalid; the buffer is grown for the next one).
+ * May be called more than once per state.  Not in the reference
+ * (SPEC.md:76); semantics in SURVEY.md Appendix A. */
+int cs_render_backward(cs_ctx* ctx, cs_state* state, const float* dl_dimg, const cs_grads* out,
                        void* stream);
+void cs_state_release(cs_state* state);
 
 /* Per-stage CUDA-event timing of the next max_frames cs_render calls on this
  * context; cs_timing_end returns per-stage sums in ms over the frames timed:
@@ -210,6 +227,13 @@ int cs_frame_graphs(cs_ctx* ctx);
 
 /* Stats of the last frame (synchronises the stream). */
 int cs_frame_stats_get(cs_ctx* ctx, cs_frame_stats* out, void* stream);
+
+/* Synchronise `stream` and report CS_ENOMEM if an asynchronous frame on this
+ * context overflowed its tile-pair buffer (that frame rendered incompletely;
+ * the buffers are grown).  Every cs_render / cs_render_train call performs
+ * the same (non-synchronising) check on entry, so an overflow is never
+ * silent: it fails the frame's next call at the latest. */
+int cs_check(cs_ctx* ctx, void* stream);
 
 /* Golden-intermediate dumps of the last frame, host destinations.
  * cs_dump_projected mirrors render._Projected (render.py:89-108): arrays in

@@ -465,6 +465,57 @@ def mad_bounds(positions, n_mad):
     return lo, hi
 
 
+def build_lod(cloud, membership, n_blocks, cameras, distance_intervals,
+              compression_rates=(0.5, 0.34, 0.25), lod_sh_degrees=(3, 2, 1), n_mad=4.0,
+              settings=None, nthreads: int = 0):
+    """lod.build_lod (lod.py:211-248) on the host: one global significance
+    ranking over the training views, level L keeps the top
+    _keep_count(rate_L, K) rows split by block (ascending index inside a
+    block), SH truncated to the level degree; per-block MAD bounds of the full
+    cloud's members.  Rates and degrees are finest-first, reversed here.
+    Returns a namespace with levels[L][j] (Arrays, coarsest level first),
+    bounds_min/bounds_max (J, 3), distance_intervals and sh_degrees."""
+    from types import SimpleNamespace
+    k = int(np.asarray(cloud.positions).shape[0])
+    scores, _ = significance_scores(cloud, cameras, settings, nthreads)
+    order = priority(scores)
+    mem = np.asarray(membership).astype(np.int64)
+    rates = tuple(reversed(tuple(compression_rates)))
+    degrees = tuple(reversed(tuple(lod_sh_degrees)))
+    sh = np.asarray(cloud.sh)
+    cols = [np.asarray(cloud.positions), np.asarray(cloud.opacities), np.asarray(cloud.scales),
+            np.asarray(cloud.rotations)]
+    levels = []
+    for rate, deg in zip(rates, degrees):
+        mask = np.zeros(k, dtype=bool)
+        mask[order[:keep_count(rate, k)]] = True
+        idx = np.nonzero(mask)[0]
+        # np.nonzero(mask & (membership == j)) for every j at once: stable split by block
+        by_block = idx[np.argsort(mem[idx], kind="stable")]
+        counts = np.bincount(mem[idx], minlength=n_blocks)
+        width = min((deg + 1) ** 2, sh.shape[2])
+        blocks = []
+        start = 0
+        for j in range(n_blocks):
+            rows = by_block[start:start + counts[j]]
+            start += counts[j]
+            blocks.append(Arrays(*(c[rows] for c in cols), sh[rows][:, :, :width]))
+        levels.append(tuple(blocks))
+    bmin = np.zeros((n_blocks, 3))
+    bmax = np.zeros((n_blocks, 3))
+    members = np.argsort(mem, kind="stable")
+    mcount = np.bincount(mem, minlength=n_blocks)
+    start = 0
+    for j in range(n_blocks):
+        rows = members[start:start + mcount[j]]
+        start += mcount[j]
+        if rows.size:
+            bmin[j], bmax[j] = mad_bounds(cols[0][rows], n_mad)
+    return SimpleNamespace(levels=tuple(levels), bounds_min=bmin, bounds_max=bmax,
+                           distance_intervals=tuple(tuple(map(float, iv)) for iv in distance_intervals),
+                           sh_degrees=degrees)
+
+
 # ---------------------------------------------------------------------------
 # training-data assignment (partition.py:172-439, metrics.py:61-101)
 

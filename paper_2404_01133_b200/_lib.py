@@ -75,7 +75,8 @@ class CsAdamHparams(ctypes.Structure):
 
 
 class CsSource(ctypes.Structure):
-    _fields_ = [("kind", i32), ("force_level", i32), ("cloud", CsCloud), ("lod", vp), ("exclude", vp)]
+    _fields_ = [("kind", i32), ("force_level", i32), ("cloud", CsCloud), ("lod", vp), ("exclude", vp),
+                ("select_cam", ctypes.POINTER(CsCamera))]
 
 
 _SIGS = {
@@ -93,8 +94,12 @@ _SIGS = {
                                  ctypes.POINTER(CsSettings), vp, ctypes.c_uint32,
                                  ctypes.POINTER(CsFrameStats), vp]),
     "cs_frame_stats_get": (ctypes.c_int, [vp, ctypes.POINTER(CsFrameStats), vp]),
-    "cs_render_backward": (ctypes.c_int, [vp, ctypes.POINTER(CsSource), ctypes.POINTER(CsCamera),
-                                          ctypes.POINTER(CsSettings), vp, ctypes.POINTER(CsGrads), vp]),
+    "cs_check": (ctypes.c_int, [vp, vp]),
+    "cs_render_train": (ctypes.c_int, [vp, ctypes.POINTER(CsSource), ctypes.POINTER(CsCamera),
+                                       ctypes.POINTER(CsSettings), vp, ctypes.c_uint32, ctypes.POINTER(vp),
+                                       vp]),
+    "cs_render_backward": (ctypes.c_int, [vp, vp, vp, ctypes.POINTER(CsGrads), vp]),
+    "cs_state_release": (None, [vp]),
     "cs_timing_begin": (ctypes.c_int, [vp, i32]),
     "cs_timing_end": (ctypes.c_int, [vp, vp, vp]),
     "cs_frame_graphs": (ctypes.c_int, [vp]),

@@ -71,7 +71,8 @@ const void* project_kernel();
 int64_t bin_status_words(int64_t capacity);
 void launch_bin_pairs(const uint32_t* order, const uint2* rects, DevStats* stats, int64_t pair_cap,
                       int64_t capacity, uint64_t* status, int ntx, uint32_t* keys, uint32_t* vals,
-                      uint32_t* hist, int key_bits, bool emit, cudaStream_t s);
+                      uint32_t* hist, int key_bits, bool emit, int64_t* host_overflow,
+                      cudaStream_t s);
 
 
 void launch_tile_ranges(const uint32_t* keys, const uint32_t* vals, const short4* boxes,
@@ -212,21 +213,22 @@ struct cs_lod {
   }
 };
 
-struct cs_ctx {
-  int device = 0;
-  std::mutex mu;  // one frame at a time per context (contexts are per thread/stream)
+// The buffers one frame writes and its backward reads (pair lists, HotRecs,
+// depth keys, tile ranges, per-pixel blend state, stats).  A context renders
+// into its current workspace; cs_render_train hands the workspace to a
+// cs_state (held until cs_state_release), and the next frame switches to a
+// free workspace, so any number of renders may run between a training
+// forward and its backward without touching the state the backward reads.
+struct Ws {
   DBuf stats, clouds1, segs, dec;
-  DBuf st_gather, st_pw, st_fuse, st_sort, hist, sort_tickets, fuse_ticket;
+  DBuf st_gather, st_pw, st_sort, hist, sort_tickets;
   DBuf keysA, valsA, keysB, valsB, recs;
   DBuf k32A, k32B, long_runs, fix_ctl;          // K4 32-bit depth sort + K4b run fix-up
   DBuf hot, boxes, rects, tile_order;
   DBuf pkA, pvA, pkB, pvB, ranges, frag_tile, pw_list;
   DBuf st_t, st_last, st_acc;
-  DBuf scratch1, scratch2, scratch3, scratch4;  // API utilities
-  DBuf gacc;                                    // per-rank blend-backward partials
-  DBuf loss_maps, loss_acc;                     // cs_training_loss workspace
-  cs_frame_stats* h_stats = nullptr;            // pinned
   int64_t cap_vis = 0, cap_pairs = 0, cap_pw = 0, cap_tiles = 0;
+  bool held = false;  // owned by a cs_state
   // last frame bookkeeping (for dumps / backward)
   const uint32_t* last_order = nullptr;
   bool last_debug = false;
@@ -236,6 +238,31 @@ struct cs_ctx {
   const uint2* last_ranges = nullptr;
   int last_tiles = 0;
   int last_width = 0, last_height = 0;
+  void release() {
+    DBuf* all[] = {&stats, &clouds1, &segs, &dec, &st_gather, &st_pw, &st_sort, &hist, &sort_tickets,
+                   &keysA, &valsA, &keysB, &valsB, &recs, &k32A, &k32B, &long_runs, &fix_ctl, &hot,
+                   &boxes, &rects, &tile_order, &pkA, &pvA, &pkB, &pvB, &ranges, &frag_tile, &pw_list,
+                   &st_t, &st_last, &st_acc};
+    for (DBuf* b : all) b->release();
+  }
+};
+
+struct cs_ctx {
+  int device = 0;
+  std::mutex mu;  // one frame at a time per context (contexts are per thread/stream)
+  std::vector<Ws*> ws_all;   // every workspace of this context
+  Ws* ws = nullptr;          // the one the next frame renders into
+  Ws* last = nullptr;        // the one the last frame rendered into (dumps, stats)
+  DBuf st_fuse, fuse_ticket;
+  DBuf scratch1, scratch2, scratch3, scratch4;  // API utilities
+  DBuf gacc;                                    // per-rank blend-backward partials
+  DBuf loss_maps, loss_acc;                     // cs_training_loss workspace
+  cs_frame_stats* h_stats = nullptr;            // pinned
+  // pair-buffer overflow of an asynchronous frame, written by k_bin_pairs into
+  // mapped pinned memory: [0] pairs the frame needed, [1] its frame serial
+  volatile int64_t* h_overflow = nullptr;
+  int64_t* d_overflow = nullptr;
+  int64_t serial = 0;        // frames rendered on this context
   // frame graph (see cs_render): the last eligible call's key, and the
   // captured, instantiated frame for it with the camera-carrying kernel nodes
   struct FrameKey {
@@ -246,6 +273,7 @@ struct cs_ctx {
     uint32_t flags;
     void* out;
     cudaStream_t stream;
+    const void* ws;
     int64_t cap_vis, cap_pairs, cap_pw, cap_tiles;
     uint64_t buf_generation;
   };
@@ -263,12 +291,29 @@ struct cs_ctx {
   };
   std::vector<FrameGraph> graphs;   // most recent last (double-buffered outputs: 2 keys)
   std::vector<FrameKey> seen;       // recent eligible keys (capture on the second sighting)
+  std::vector<FrameKey> uncapturable;  // keys whose capture failed (never retried)
   cudaStream_t capture_stream = nullptr;
   cs_camera graph_cam{};
   // per-stage CUDA-event timing (cs_timing_begin/end)
   bool timing_on = false;
   int timing_max = 0, timing_frame = 0;
   std::vector<cudaEvent_t> tev;
+};
+
+// A training forward's kept state (cs_render_train): its workspace, the
+// frame's geometry, and an event + pinned status word that tell the backward
+// whether the forward completed without a pair-buffer overflow.
+struct cs_state {
+  cs_ctx* ctx = nullptr;
+  Ws* ws = nullptr;
+  int64_t count = 0;      // rows of the rendered cloud
+  int width = 0, height = 0;
+  cs_camera cam{};
+  cs_settings st{};
+  cs_cloud cloud{};
+  cudaEvent_t done = nullptr;
+  int32_t* h_status = nullptr;  // pinned: DevStats.status after the forward
+  int64_t* h_pairs = nullptr;   // pinned: DevStats.pairs after the forward
 };
 
 static constexpr int kStages = 8;  // select, project, depth sort, gather+scan, duplicate,
@@ -282,6 +327,30 @@ extern "C" {
 
 int cs_version(void) { return 1; }
 const char* cs_last_error(void) { return g_err.c_str(); }
+
+static int ws_init(Ws* w) {
+  if (w->stats.ensure(sizeof(DevStats)) || w->hist.ensure(sizeof(uint32_t) * 256 * 8) ||
+      w->sort_tickets.ensure(sizeof(uint32_t) * 16) || w->clouds1.ensure(sizeof(cs_cloud)))
+    return fail(CS_ENOMEM, "frame workspace");
+  return CS_OK;
+}
+
+// The workspace the next frame renders into: the current one unless a
+// cs_state holds it, then a free one (new workspaces start from the current
+// pair capacity, so a training loop does not re-learn its sizes).
+static int frame_ws(cs_ctx* c, Ws** out) {
+  if (c->ws && !c->ws->held) { *out = c->ws; return CS_OK; }
+  for (Ws* w : c->ws_all)
+    if (!w->held) { c->ws = w; *out = w; return CS_OK; }
+  Ws* w = new Ws();
+  c->ws_all.push_back(w);
+  int rc = ws_init(w);
+  if (rc) return rc;
+  if (c->ws) w->cap_pairs = c->ws->cap_pairs;
+  c->ws = w;
+  *out = w;
+  return CS_OK;
+}
 
 int cs_create(int device, cs_ctx** out) {
   if (!out) return fail(CS_EINVAL, "out is NULL");
@@ -297,11 +366,15 @@ int cs_create(int device, cs_ctx** out) {
   cs_ctx* c = new cs_ctx();
   c->device = device;
   CS_CUDA(cudaMallocHost(&c->h_stats, sizeof(cs_frame_stats)));
-  if (c->stats.ensure(sizeof(DevStats)) != cudaSuccess) return fail(CS_ENOMEM, "stats");
-  if (c->hist.ensure(sizeof(uint32_t) * 256 * 8) != cudaSuccess) return fail(CS_ENOMEM, "hist");
-  if (c->sort_tickets.ensure(sizeof(uint32_t) * 16) != cudaSuccess) return fail(CS_ENOMEM, "tk");
+  void* ov = nullptr;
+  CS_CUDA(cudaHostAlloc(&ov, 2 * sizeof(int64_t), cudaHostAllocMapped));
+  c->h_overflow = reinterpret_cast<volatile int64_t*>(ov);
+  c->h_overflow[0] = c->h_overflow[1] = 0;
+  CS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->d_overflow), ov, 0));
+  Ws* w = nullptr;
+  int rc = frame_ws(c, &w);
+  if (rc) return rc;
   if (c->fuse_ticket.ensure(sizeof(uint32_t) * 4) != cudaSuccess) return fail(CS_ENOMEM, "tk");
-  if (c->clouds1.ensure(sizeof(cs_cloud)) != cudaSuccess) return fail(CS_ENOMEM, "clouds");
   *out = c;
   return CS_OK;
 }
@@ -310,15 +383,15 @@ void cs_destroy(cs_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
-  DBuf* all[] = {&c->stats, &c->clouds1, &c->segs, &c->dec, &c->st_gather,
-                 &c->st_pw, &c->st_fuse, &c->st_sort, &c->hist, &c->sort_tickets,
-                 &c->fuse_ticket, &c->keysA, &c->valsA, &c->keysB, &c->valsB, &c->recs, &c->k32A, &c->k32B,
-                 &c->long_runs, &c->fix_ctl, &c->hot,
-                 &c->tile_order, &c->boxes, &c->rects, &c->pkA, &c->pvA, &c->pkB,
-                 &c->pvB, &c->ranges, &c->frag_tile, &c->pw_list, &c->st_t, &c->st_last,
-                 &c->st_acc, &c->gacc, &c->loss_maps, &c->loss_acc, &c->scratch1, &c->scratch2, &c->scratch3, &c->scratch4};
+  for (Ws* w : c->ws_all) {
+    w->release();
+    delete w;
+  }
+  DBuf* all[] = {&c->st_fuse, &c->fuse_ticket, &c->gacc, &c->loss_maps, &c->loss_acc,
+                 &c->scratch1, &c->scratch2, &c->scratch3, &c->scratch4};
   for (DBuf* b : all) b->release();
   if (c->h_stats) cudaFreeHost(c->h_stats);
+  if (c->h_overflow) cudaFreeHost(const_cast<int64_t*>(c->h_overflow));
   for (cudaEvent_t e : c->tev) cudaEventDestroy(e);
   for (auto& g : c->graphs) {
     if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -391,42 +464,45 @@ void cs_lod_destroy(cs_lod* L) {
   delete L;
 }
 
-static int ensure_frame_buffers(cs_ctx* c, int64_t cap_vis, int n_segs, int n_blocks,
+static int ensure_frame_buffers(Ws* w, int64_t cap_vis, int n_segs, int n_blocks,
                                 int n_tiles, int64_t cap_pw) {
   cap_vis = std::max<int64_t>(cap_vis, 1);
-  if (c->segs.ensure(sizeof(Seg) * std::max(n_segs, 1)) ||
-      c->dec.ensure(sizeof(cs_decision) * std::max(n_blocks, 1)))
+  if (w->segs.ensure(sizeof(Seg) * std::max(n_segs, 1)) ||
+      w->dec.ensure(sizeof(cs_decision) * std::max(n_blocks, 1)))
     return fail(CS_ENOMEM, "segment tables");
-  if (cap_vis > c->cap_vis) {
-    int64_t cap = std::max<int64_t>(cap_vis, c->cap_vis + c->cap_vis / 2);
+  if (cap_vis > w->cap_vis) {
+    int64_t cap = std::max<int64_t>(cap_vis, w->cap_vis + w->cap_vis / 2);
     if (cap >= (1ll << 30)) return fail(CS_EINVAL, "more than 2^30 assembled Gaussians");
     const int64_t chunks = (cap + 255) / 256 + 1;
-    if (c->st_gather.ensure(8 * std::max<int64_t>(chunks, bin_status_words(cap))) ||
-        c->keysA.ensure(8 * cap) || c->keysB.ensure(8 * cap) || c->valsA.ensure(4 * cap) ||
-        c->k32A.ensure(4 * cap) || c->k32B.ensure(4 * cap) ||
-        c->long_runs.ensure(4 * fix_long_cap(cap)) || c->fix_ctl.ensure(fix_ctl_bytes()) ||
-        c->valsB.ensure(4 * cap) || c->hot.ensure(sizeof(HotRec) * cap) ||
-        c->rects.ensure(8 * cap) || c->boxes.ensure(8 * cap))
+    if (w->st_gather.ensure(8 * std::max<int64_t>(chunks, bin_status_words(cap))) ||
+        w->keysA.ensure(8 * cap) || w->keysB.ensure(8 * cap) || w->valsA.ensure(4 * cap) ||
+        w->k32A.ensure(4 * cap) || w->k32B.ensure(4 * cap) ||
+        w->long_runs.ensure(4 * fix_long_cap(cap)) || w->fix_ctl.ensure(fix_ctl_bytes()) ||
+        w->valsB.ensure(4 * cap) || w->hot.ensure(sizeof(HotRec) * cap) ||
+        w->rects.ensure(8 * cap) || w->boxes.ensure(8 * cap))
       return fail(CS_ENOMEM, "visible-splat buffers (%lld)", (long long)cap);
-    c->cap_vis = cap;
+    w->cap_vis = cap;
+    // the pair capacity follows the visible capacity (8 pairs per splat): a
+    // frame of a larger cloud never starts from a smaller cloud's pair buffer
+    w->cap_pairs = std::max<int64_t>(w->cap_pairs, std::max<int64_t>(1 << 20, 8 * cap));
   }
-  if (c->cap_pairs == 0) c->cap_pairs = std::max<int64_t>(1 << 20, 8 * c->cap_vis);
-  if (c->cap_pairs >= (1ll << 30)) c->cap_pairs = (1ll << 30) - 1;
-  if (c->pkA.ensure(4 * c->cap_pairs) || c->pvA.ensure(4 * c->cap_pairs) ||
-      c->pkB.ensure(4 * c->cap_pairs) || c->pvB.ensure(4 * c->cap_pairs))
-    return fail(CS_ENOMEM, "pair buffers (%lld)", (long long)c->cap_pairs);
-  const size_t sw = std::max(radix_status_words(c->cap_vis, 8), radix_status_words(c->cap_pairs, 4));
-  if (c->st_sort.ensure(4 * sw)) return fail(CS_ENOMEM, "sort status");
-  if (n_tiles > c->cap_tiles) {
-    if (c->ranges.ensure(sizeof(uint2) * n_tiles) || c->frag_tile.ensure(4 * n_tiles) ||
-        c->tile_order.ensure(4 * (n_tiles + 2 * 34 * 16)))  // + launch_tile_order's scratch
+  if (w->cap_pairs == 0) w->cap_pairs = std::max<int64_t>(1 << 20, 8 * w->cap_vis);
+  if (w->cap_pairs >= (1ll << 30)) w->cap_pairs = (1ll << 30) - 1;
+  if (w->pkA.ensure(4 * w->cap_pairs) || w->pvA.ensure(4 * w->cap_pairs) ||
+      w->pkB.ensure(4 * w->cap_pairs) || w->pvB.ensure(4 * w->cap_pairs))
+    return fail(CS_ENOMEM, "pair buffers (%lld)", (long long)w->cap_pairs);
+  const size_t sw = std::max(radix_status_words(w->cap_vis, 8), radix_status_words(w->cap_pairs, 4));
+  if (w->st_sort.ensure(4 * sw)) return fail(CS_ENOMEM, "sort status");
+  if (n_tiles > w->cap_tiles) {
+    if (w->ranges.ensure(sizeof(uint2) * n_tiles) || w->frag_tile.ensure(4 * n_tiles) ||
+        w->tile_order.ensure(4 * (n_tiles + 2 * 34 * 16)))  // + launch_tile_order's scratch
       return fail(CS_ENOMEM, "tile buffers");
-    c->cap_tiles = n_tiles;
+    w->cap_tiles = n_tiles;
   }
-  if (cap_pw > 0 && cap_pw > c->cap_pw) {
-    if (c->pw_list.ensure(8 * cap_pw) || c->st_pw.ensure(8 * ((cap_pw + 255) / 256 + 1)))
+  if (cap_pw > 0 && cap_pw > w->cap_pw) {
+    if (w->pw_list.ensure(8 * cap_pw) || w->st_pw.ensure(8 * ((cap_pw + 255) / 256 + 1)))
       return fail(CS_ENOMEM, "pointwise buffers");
-    c->cap_pw = cap_pw;
+    w->cap_pw = cap_pw;
   }
   return CS_OK;
 }
@@ -451,8 +527,8 @@ static int bits_for(int64_t n) {
   return b;
 }
 
-// One pass of the whole pipeline (no sync).
-static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
+// One pass of the whole pipeline into workspace w (no sync).
+static int render_once(cs_ctx* c, Ws* w, const cs_source* src, const cs_camera* cam,
                        const cs_settings* st, void* out, uint32_t flags, cudaStream_t s) {
   const int ts = st->tile_size;
   const int ntx = (cam->width + ts - 1) / ts, nty = (cam->height + ts - 1) / ts;
@@ -485,92 +561,97 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
       return fail(CS_EINVAL, "unknown source kind %d", src->kind);
     }
   }
-  int rc = ensure_frame_buffers(c, cap_vis, n_segs, n_blocks, n_tiles, cap_pw);
+  int rc = ensure_frame_buffers(w, cap_vis, n_segs, n_blocks, n_tiles, cap_pw);
   if (rc) return rc;
-  DevStats* stats = c->stats.as<DevStats>();
+  c->last = w;
+  ++c->serial;
+  // the LoD selection camera: an AssembledSet keeps the camera it was
+  // assembled for (lod.py:360-401), which may differ from the render camera
+  const cs_camera& scam = src->select_cam ? *src->select_cam : *cam;
+  DevStats* stats = w->stats.as<DevStats>();
   const bool timed = !(flags & CS_RENDER_PROJECT_ONLY);
   if (timed) mark(c, 0, s);
   CS_CUDA(cudaMemsetAsync(stats, 0, sizeof(DevStats), s));
   const cs_cloud* clouds = nullptr;
   const uint64_t* list = nullptr;
   if (src->kind == CS_SRC_CLOUD) {
-    launch_setup_cloud(src->cloud, c->clouds1.as<cs_cloud>(), c->segs.as<Seg>(), stats, s);
-    clouds = c->clouds1.as<cs_cloud>();
+    launch_setup_cloud(src->cloud, w->clouds1.as<cs_cloud>(), w->segs.as<Seg>(), stats, s);
+    clouds = w->clouds1.as<cs_cloud>();
   } else if (src->kind == CS_SRC_LOD_BLOCK) {
-    launch_lod_select(L->tables(), *cam, src->force_level, c->dec.as<cs_decision>(),
-                      c->segs.as<Seg>(), stats, s);
+    launch_lod_select(L->tables(), scam, src->force_level, w->dec.as<cs_decision>(),
+                      w->segs.as<Seg>(), stats, s);
     clouds = L->d_clouds.as<cs_cloud>();
   } else {
-    CS_CUDA(cudaMemsetAsync(c->st_pw.p, 0, 8 * ((cap_pw + 255) / 256 + 1), s));
-    launch_pointwise(L->tables(), *cam, src->force_level, c->st_pw.as<uint64_t>(),
-                     c->pw_list.as<uint64_t>(), c->segs.as<Seg>(), stats, s);
+    CS_CUDA(cudaMemsetAsync(w->st_pw.p, 0, 8 * ((cap_pw + 255) / 256 + 1), s));
+    launch_pointwise(L->tables(), scam, src->force_level, w->st_pw.as<uint64_t>(),
+                     w->pw_list.as<uint64_t>(), w->segs.as<Seg>(), stats, s);
     clouds = L->d_clouds.as<cs_cloud>();
-    list = c->pw_list.as<uint64_t>();
+    list = w->pw_list.as<uint64_t>();
   }
   CS_CHECK_LAUNCH();
   if (timed) mark(c, 1, s);
   const int64_t cap = std::max<int64_t>(cap_vis, 1);
   const bool debug = (flags & (CS_RENDER_DEBUG | CS_RENDER_PROJECT_ONLY)) != 0;
-  if (debug && c->recs.ensure(sizeof(ProjRec) * c->cap_vis)) return fail(CS_ENOMEM, "debug records");
-  ProjOutputs po{c->keysA.as<uint64_t>(), c->k32A.as<uint32_t>(), c->valsA.as<uint32_t>(),
-                 c->hot.as<HotRec>(),
-                 c->rects.as<uint2>(), c->boxes.as<short4>(),
-                 debug ? c->recs.as<ProjRec>() : nullptr,
+  if (debug && w->recs.ensure(sizeof(ProjRec) * w->cap_vis)) return fail(CS_ENOMEM, "debug records");
+  ProjOutputs po{w->keysA.as<uint64_t>(), w->k32A.as<uint32_t>(), w->valsA.as<uint32_t>(),
+                 w->hot.as<HotRec>(),
+                 w->rects.as<uint2>(), w->boxes.as<short4>(),
+                 debug ? w->recs.as<ProjRec>() : nullptr,
                  src->kind == CS_SRC_CLOUD ? src->exclude : nullptr};
-  launch_project(clouds, c->segs.as<Seg>(), stats, *cam, *st, cap, po, list, s);
-  c->last_debug = debug;
+  launch_project(clouds, w->segs.as<Seg>(), stats, *cam, *st, cap, po, list, s);
+  w->last_debug = debug;
   CS_CHECK_LAUNCH();
   if (timed) mark(c, 2, s);
   // K4: global depth order over the assembled set: stable 32-bit radix sort of
   // the float32-rounded depth (culled Gaussians carry ~0 and land behind the M
   // visible ones), then K4b re-sorts runs of equal float32 depth by (float64
   // depth, splat id) -- the exact stable argsort of render.py:176-177.
-  const int which = radix_sort<uint32_t>(c->k32A.as<uint32_t>(), c->valsA.as<uint32_t>(),
-                                         c->k32B.as<uint32_t>(), c->valsB.as<uint32_t>(),
-                                         &stats->assembled, cap, 0, 32, c->hist.as<uint32_t>(),
-                                         c->st_sort.as<uint32_t>(), c->sort_tickets.as<uint32_t>(), s);
+  const int which = radix_sort<uint32_t>(w->k32A.as<uint32_t>(), w->valsA.as<uint32_t>(),
+                                         w->k32B.as<uint32_t>(), w->valsB.as<uint32_t>(),
+                                         &stats->assembled, cap, 0, 32, w->hist.as<uint32_t>(),
+                                         w->st_sort.as<uint32_t>(), w->sort_tickets.as<uint32_t>(), s);
   CS_CHECK_LAUNCH();
-  uint32_t* order = which ? c->valsB.as<uint32_t>() : c->valsA.as<uint32_t>();
-  const uint32_t* k32s = which ? c->k32B.as<uint32_t>() : c->k32A.as<uint32_t>();
-  launch_fix_depth_runs(k32s, order, c->keysA.as<uint64_t>(), stats, cap, c->fix_ctl.p,
-                        c->long_runs.as<uint32_t>(), (uint32_t)fix_long_cap(cap),
-                        c->keysB.as<uint32_t>(), s);
+  uint32_t* order = which ? w->valsB.as<uint32_t>() : w->valsA.as<uint32_t>();
+  const uint32_t* k32s = which ? w->k32B.as<uint32_t>() : w->k32A.as<uint32_t>();
+  launch_fix_depth_runs(k32s, order, w->keysA.as<uint64_t>(), stats, cap, w->fix_ctl.p,
+                        w->long_runs.as<uint32_t>(), (uint32_t)fix_long_cap(cap),
+                        w->keysB.as<uint32_t>(), s);
   CS_CHECK_LAUNCH();
   if (timed) mark(c, 3, s);
   // K5+K6: pair counts in depth order, scanned, and the pairs emitted in one
   // pass (also counts the tile sort's digit histograms, so K7 skips its
   // counting pass)
-  CS_CUDA(cudaMemsetAsync(c->st_gather.p, 0, 8 * (bin_chunks(cap) + 1), s));
+  CS_CUDA(cudaMemsetAsync(w->st_gather.p, 0, 8 * (bin_chunks(cap) + 1), s));
   const bool project_only = (flags & CS_RENDER_PROJECT_ONLY) != 0;
-  launch_bin_pairs(order, c->rects.as<uint2>(), stats, c->cap_pairs, cap,
-                   c->st_gather.as<uint64_t>(), ntx, c->pkA.as<uint32_t>(), c->pvA.as<uint32_t>(),
-                   bits_for(n_tiles) <= 24 ? c->hist.as<uint32_t>() : nullptr, bits_for(n_tiles),
-                   !project_only, s);
+  launch_bin_pairs(order, w->rects.as<uint2>(), stats, w->cap_pairs, cap,
+                   w->st_gather.as<uint64_t>(), ntx, w->pkA.as<uint32_t>(), w->pvA.as<uint32_t>(),
+                   bits_for(n_tiles) <= 24 ? w->hist.as<uint32_t>() : nullptr, bits_for(n_tiles),
+                   !project_only, c->d_overflow, s);
   CS_CHECK_LAUNCH();
   if (timed) mark(c, 4, s);
   if (project_only) {
-    c->last_order = order;
-    c->last_list = nullptr;
+    w->last_order = order;
+    w->last_list = nullptr;
     return CS_OK;
   }
   mark(c, 5, s);
   // K7: stable sort by tile id only (ceil(log2 T) bits)
-  const int which2 = radix_sort<uint32_t>(c->pkA.as<uint32_t>(), c->pvA.as<uint32_t>(),
-                                          c->pkB.as<uint32_t>(), c->pvB.as<uint32_t>(),
-                                          &stats->pairs_eff, c->cap_pairs, 0, bits_for(n_tiles),
-                                          c->hist.as<uint32_t>(), c->st_sort.as<uint32_t>(),
-                                          c->sort_tickets.as<uint32_t>() + 8, s,
+  const int which2 = radix_sort<uint32_t>(w->pkA.as<uint32_t>(), w->pvA.as<uint32_t>(),
+                                          w->pkB.as<uint32_t>(), w->pvB.as<uint32_t>(),
+                                          &stats->pairs_eff, w->cap_pairs, 0, bits_for(n_tiles),
+                                          w->hist.as<uint32_t>(), w->st_sort.as<uint32_t>(),
+                                          w->sort_tickets.as<uint32_t>() + 8, s,
                                           /*hist_ready=*/bits_for(n_tiles) <= 24);
   CS_CHECK_LAUNCH();
-  const uint32_t* tkeys = which2 ? c->pkB.as<uint32_t>() : c->pkA.as<uint32_t>();
-  const uint32_t* tvals = which2 ? c->pvB.as<uint32_t>() : c->pvA.as<uint32_t>();
+  const uint32_t* tkeys = which2 ? w->pkB.as<uint32_t>() : w->pkA.as<uint32_t>();
+  const uint32_t* tvals = which2 ? w->pvB.as<uint32_t>() : w->pvA.as<uint32_t>();
   mark(c, 6, s);
   // K8: tile ranges
-  CS_CUDA(cudaMemsetAsync(c->ranges.p, 0, sizeof(uint2) * n_tiles, s));
+  CS_CUDA(cudaMemsetAsync(w->ranges.p, 0, sizeof(uint2) * n_tiles, s));
   // the sort's other (key, value) buffers are free now: they take the pair-major boxes
-  uint32_t* bxs = which2 ? c->pkA.as<uint32_t>() : c->pkB.as<uint32_t>();
-  uint32_t* bys = which2 ? c->pvA.as<uint32_t>() : c->pvB.as<uint32_t>();
-  launch_tile_ranges(tkeys, tvals, c->boxes.as<short4>(), stats, c->ranges.as<uint2>(), bxs, bys, s);
+  uint32_t* bxs = which2 ? w->pkA.as<uint32_t>() : w->pkB.as<uint32_t>();
+  uint32_t* bys = which2 ? w->pvA.as<uint32_t>() : w->pvB.as<uint32_t>();
+  launch_tile_ranges(tkeys, tvals, w->boxes.as<short4>(), stats, w->ranges.as<uint2>(), bxs, bys, s);
   CS_CHECK_LAUNCH();
   mark(c, 7, s);
   // K9: blend
@@ -586,38 +667,60 @@ static int render_once(cs_ctx* c, const cs_source* src, const cs_camera* cam,
   BlendState keep{nullptr, nullptr, nullptr};
   const int64_t npx = (int64_t)cam->width * cam->height;
   if (flags & CS_RENDER_KEEP_STATE) {
-    if (c->st_t.ensure(8 * npx) || c->st_last.ensure(4 * npx) || c->st_acc.ensure(24 * npx))
+    if (w->st_t.ensure(8 * npx) || w->st_last.ensure(4 * npx) || w->st_acc.ensure(24 * npx))
       return fail(CS_ENOMEM, "blend state");
-    keep = BlendState{c->st_t.as<double>(), c->st_last.as<int32_t>(), c->st_acc.as<double>()};
+    keep = BlendState{w->st_t.as<double>(), w->st_last.as<int32_t>(), w->st_acc.as<double>()};
   }
-  launch_tile_order(c->ranges.as<uint2>(), n_tiles, c->tile_order.as<uint32_t>(), s);
+  launch_tile_order(w->ranges.as<uint2>(), n_tiles, w->tile_order.as<uint32_t>(), s);
   CS_CHECK_LAUNCH();
-  launch_blend(n_tiles, tvals, bxs, bys, c->ranges.as<uint2>(), c->hot.as<HotRec>(),
-               c->tile_order.as<uint32_t>(),
-               bp, out, (flags & CS_RENDER_F64_OUT) != 0, c->frag_tile.as<int32_t>(), stats,
+  launch_blend(n_tiles, tvals, bxs, bys, w->ranges.as<uint2>(), w->hot.as<HotRec>(),
+               w->tile_order.as<uint32_t>(),
+               bp, out, (flags & CS_RENDER_F64_OUT) != 0, w->frag_tile.as<int32_t>(), stats,
                (flags & CS_RENDER_KEEP_STATE) ? &keep : nullptr, s);
   CS_CHECK_LAUNCH();
   mark(c, 8, s);
   if (c->timing_on && c->timing_frame < c->timing_max) ++c->timing_frame;
-  c->last_order = order;
-  c->last_list = tvals;
-  c->last_bxs = bxs;
-  c->last_bys = bys;
-  c->last_ranges = c->ranges.as<uint2>();
-  c->last_tiles = n_tiles;
-  c->last_width = cam->width;
-  c->last_height = cam->height;
+  w->last_order = order;
+  w->last_list = tvals;
+  w->last_bxs = bxs;
+  w->last_bys = bys;
+  w->last_ranges = w->ranges.as<uint2>();
+  w->last_tiles = n_tiles;
+  w->last_width = cam->width;
+  w->last_height = cam->height;
   return CS_OK;
 }
 
 static_assert(offsetof(DevStats, blend_max_item_cycles) == offsetof(cs_frame_stats, blend_max_item_cycles) &&
                   sizeof(cs_frame_stats) <= offsetof(DevStats, pairs_eff) + sizeof(int64_t),
               "DevStats must lead with the cs_frame_stats layout");
-static int fetch_stats(cs_ctx* c, cudaStream_t s) {
+static int fetch_stats(cs_ctx* c, Ws* w, cudaStream_t s) {
   // DevStats and cs_frame_stats share the leading layout
-  CS_CUDA(cudaMemcpyAsync(c->h_stats, c->stats.p, sizeof(cs_frame_stats), cudaMemcpyDeviceToHost, s));
+  if (!w) return fail(CS_EINVAL, "no frame rendered on this context");
+  CS_CUDA(cudaMemcpyAsync(c->h_stats, w->stats.p, sizeof(cs_frame_stats), cudaMemcpyDeviceToHost, s));
   CS_CUDA(cudaStreamSynchronize(s));
   return CS_OK;
+}
+
+// An asynchronous frame that overflowed its pair buffer (k_bin_pairs wrote the
+// pair count it needed into mapped host memory) is reported by the next call
+// on the context: the buffers of every workspace grow to fit, and the call
+// fails with CS_ENOMEM -- that frame's image is background-only and must be
+// re-rendered.  Never silent.
+static int check_overflow(cs_ctx* c) {
+  const int64_t need = c->h_overflow[0];
+  if (!need) return CS_OK;
+  const int64_t cap = c->h_overflow[1];
+  c->h_overflow[0] = 0;
+  c->h_overflow[1] = 0;
+  const int64_t grow = std::min<int64_t>((1ll << 30) - 1, need + need / 4 + 1024);
+  for (Ws* w : c->ws_all) w->cap_pairs = std::max(w->cap_pairs, grow);
+  if (need >= (1ll << 30))
+    return fail(CS_ENOMEM, "an earlier asynchronous frame needed %lld tile pairs (> 2^30)", (long long)need);
+  return fail(CS_ENOMEM,
+              "an earlier asynchronous frame on this context overflowed its pair buffer (%lld pairs > "
+              "%lld) and rendered incompletely; the buffers have been grown -- render it again",
+              (long long)need, (long long)cap);
 }
 
 // Frame graphs.  A frame is ~18 kernels and ~10 memsets whose sizes all live
@@ -625,22 +728,23 @@ static int fetch_stats(cs_ctx* c, cudaStream_t s) {
 // between the frames of a flythrough, and it reaches the device solely as a
 // kernel parameter of K1 (k_lod_select) and K3 (k_project).  When two
 // consecutive asynchronous calls share everything but the camera pose (same
-// source, settings, resolution, output, stream and buffer capacities), the
-// frame is captured once on a private stream and instantiated; later calls
-// patch the two camera parameters with cudaGraphExecKernelNodeSetParams and
-// launch the graph on the caller's stream -- the same kernels on the same
-// buffers, without per-kernel launch gaps.  Synchronous, stats, debug,
-// diagnostics, kept-state and timed frames always take the direct path.
+// source, settings, resolution, output, stream, workspace and buffer
+// capacities), the frame is captured once on a private stream and
+// instantiated; later calls patch the two camera parameters with
+// cudaGraphExecKernelNodeSetParams and launch the graph on the caller's
+// stream -- the same kernels on the same buffers, without per-kernel launch
+// gaps.  Synchronous, stats, debug, diagnostics, kept-state, timed and
+// separate-selection-camera frames always take the direct path.
 static bool graph_eligible(const cs_ctx* c, const cs_source* src, uint32_t flags,
                            const cs_frame_stats* stats_host) {
   const uint32_t direct = CS_RENDER_SYNC | CS_RENDER_DEBUG | CS_RENDER_PROJECT_ONLY | CS_RENDER_DIAG |
                           CS_RENDER_KEEP_STATE;
   if (std::getenv("CS_NO_GRAPH")) return false;
-  return !(flags & direct) && !stats_host && !c->timing_on &&
+  return !(flags & direct) && !stats_host && !c->timing_on && !src->select_cam &&
          (src->kind == CS_SRC_LOD_BLOCK || src->kind == CS_SRC_CLOUD);
 }
 
-static cs_ctx::FrameKey frame_key(const cs_ctx* c, const cs_source* src, const cs_camera* cam,
+static cs_ctx::FrameKey frame_key(const cs_ctx* c, const Ws* w, const cs_source* src, const cs_camera* cam,
                                   const cs_settings* st, void* out, uint32_t flags, cudaStream_t s) {
   cs_ctx::FrameKey k;
   std::memset(&k, 0, sizeof(k));
@@ -652,7 +756,8 @@ static cs_ctx::FrameKey frame_key(const cs_ctx* c, const cs_source* src, const c
   k.flags = flags;
   k.out = out;
   k.stream = s;
-  k.cap_vis = c->cap_vis; k.cap_pairs = c->cap_pairs; k.cap_pw = c->cap_pw; k.cap_tiles = c->cap_tiles;
+  k.ws = w;
+  k.cap_vis = w->cap_vis; k.cap_pairs = w->cap_pairs; k.cap_pw = w->cap_pw; k.cap_tiles = w->cap_tiles;
   k.buf_generation = g_buf_generation.load();
   return k;
 }
@@ -663,33 +768,45 @@ static bool same_key(const cs_ctx::FrameKey& a, const cs_ctx::FrameKey& b) {
 
 constexpr size_t kMaxGraphs = 4;
 
-static int capture_graph(cs_ctx* c, const cs_source* src, const cs_camera* cam, const cs_settings* st,
+// Capture the frame into a graph.  The frame itself was already rendered on
+// the caller's stream, so any failure here only means "stay on the direct
+// path": the key is remembered as uncapturable and the call succeeds.
+static int capture_graph(cs_ctx* c, Ws* w, const cs_source* src, const cs_camera* cam, const cs_settings* st,
                          void* out, uint32_t flags, const cs_ctx::FrameKey& key) {
-  if (!c->capture_stream) CS_CUDA(cudaStreamCreateWithFlags(&c->capture_stream, cudaStreamNonBlocking));
-  CS_CUDA(cudaStreamBeginCapture(c->capture_stream, cudaStreamCaptureModeThreadLocal));
-  const int rc = render_once(c, src, cam, st, out, flags, c->capture_stream);
-  cudaGraph_t g = nullptr;
-  const cudaError_t ce = cudaStreamEndCapture(c->capture_stream, &g);
-  if (rc || ce != cudaSuccess || !g) {
+  auto give_up = [&](cudaGraph_t g) {
     if (g) cudaGraphDestroy(g);
     cudaGetLastError();
-    return rc ? rc : CS_OK;  // not capturable: stay on the direct path
-  }
+    c->uncapturable.push_back(key);
+    if (c->uncapturable.size() > 16) c->uncapturable.erase(c->uncapturable.begin());
+    g_err.clear();
+    return CS_OK;
+  };
+  if (!c->capture_stream &&
+      cudaStreamCreateWithFlags(&c->capture_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return give_up(nullptr);
+  if (cudaStreamBeginCapture(c->capture_stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+    return give_up(nullptr);
+  const int64_t serial = c->serial;
+  const int rc = render_once(c, w, src, cam, st, out, flags, c->capture_stream);
+  c->serial = serial;
+  cudaGraph_t g = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(c->capture_stream, &g);
+  if (rc || ce != cudaSuccess || !g) return give_up(g);
   cs_ctx::FrameGraph fg;
   fg.key = key;
   fg.graph = g;
   size_t n = 0;
-  CS_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+  if (cudaGraphGetNodes(g, nullptr, &n) != cudaSuccess) return give_up(g);
   std::vector<cudaGraphNode_t> nodes(n);
-  CS_CUDA(cudaGraphGetNodes(g, nodes.data(), &n));
+  if (cudaGraphGetNodes(g, nodes.data(), &n) != cudaSuccess) return give_up(g);
   const void* f_sel = lod_select_kernel();
   const void* f_proj = project_kernel();
   for (cudaGraphNode_t nd : nodes) {
     cudaGraphNodeType t;
-    CS_CUDA(cudaGraphNodeGetType(nd, &t));
+    if (cudaGraphNodeGetType(nd, &t) != cudaSuccess) return give_up(g);
     if (t != cudaGraphNodeTypeKernel) continue;
     cudaKernelNodeParams p;
-    CS_CUDA(cudaGraphKernelNodeGetParams(nd, &p));
+    if (cudaGraphKernelNodeGetParams(nd, &p) != cudaSuccess) return give_up(g);
     // argument index of the cs_camera (k_lod_select(T, cam, ...),
     // k_project(clouds, segs, stats, cam, ...)) and the argument count
     int cam_arg = -1, n_args = 0;
@@ -703,11 +820,7 @@ static int capture_graph(cs_ctx* c, const cs_source* src, const cs_camera* cam, 
     cn.cam_arg = cam_arg;
     fg.cam_nodes.push_back(cn);
   }
-  if (fg.cam_nodes.empty() || cudaGraphInstantiate(&fg.exec, g, 0) != cudaSuccess) {
-    cudaGraphDestroy(g);
-    cudaGetLastError();
-    return CS_OK;
-  }
+  if (fg.cam_nodes.empty() || cudaGraphInstantiate(&fg.exec, g, 0) != cudaSuccess) return give_up(g);
   if (c->graphs.size() >= kMaxGraphs) {
     cudaGraphExecDestroy(c->graphs.front().exec);
     cudaGraphDestroy(c->graphs.front().graph);
@@ -726,87 +839,186 @@ static int replay_graph(cs_ctx* c, cs_ctx::FrameGraph& fg, const cs_camera* cam,
     CS_CUDA(cudaGraphExecKernelNodeSetParams(fg.exec, cn.node, &p));
   }
   CS_CUDA(cudaGraphLaunch(fg.exec, s));
+  c->last = reinterpret_cast<Ws*>(const_cast<void*>(fg.key.ws));
+  ++c->serial;
   return CS_OK;
 }
 
 int cs_frame_graphs(cs_ctx* c) { return c ? (int)c->graphs.size() : 0; }
 
-int cs_render(cs_ctx* c, const cs_source* src, const cs_camera* cam, const cs_settings* st,
-              void* out, uint32_t flags, cs_frame_stats* stats_host, void* stream) {
-  if (!c || !src || !out) return fail(CS_EINVAL, "NULL argument");
-  int rc = validate(cam, st);
-  if (rc) return rc;
-  std::lock_guard<std::mutex> lock(c->mu);
-  CS_CUDA(cudaSetDevice(c->device));
-  cudaStream_t s = (cudaStream_t)stream;
+// The frame pipeline with its overflow handling; KEEP_STATE is internal
+// (cs_render_train).
+static int render_frame(cs_ctx* c, Ws* w, const cs_source* src, const cs_camera* cam, const cs_settings* st,
+                        void* out, uint32_t flags, cs_frame_stats* stats_host, cudaStream_t s) {
+  int rc;
   if (graph_eligible(c, src, flags, stats_host)) {
-    const cs_ctx::FrameKey key = frame_key(c, src, cam, st, out, flags, s);
+    const cs_ctx::FrameKey key = frame_key(c, w, src, cam, st, out, flags, s);
     for (cs_ctx::FrameGraph& fg : c->graphs)
       if (same_key(key, fg.key)) return replay_graph(c, fg, cam, s);
-    rc = render_once(c, src, cam, st, out, flags, s);
+    rc = render_once(c, w, src, cam, st, out, flags, s);
     if (rc) return rc;
     // capture on the second sighting of a key whose buffers are already sized
-    const cs_ctx::FrameKey after = frame_key(c, src, cam, st, out, flags, s);
-    bool seen = false;
+    const cs_ctx::FrameKey after = frame_key(c, w, src, cam, st, out, flags, s);
+    bool seen = false, bad = false;
     for (const cs_ctx::FrameKey& k : c->seen) seen |= same_key(k, after);
-    if (seen && same_key(after, key)) return capture_graph(c, src, cam, st, out, flags, after);
+    for (const cs_ctx::FrameKey& k : c->uncapturable) bad |= same_key(k, after);
+    if (seen && !bad && same_key(after, key)) return capture_graph(c, w, src, cam, st, out, flags, after);
     c->seen.push_back(after);
     if (c->seen.size() > kMaxGraphs) c->seen.erase(c->seen.begin());
     return CS_OK;
   }
   for (int attempt = 0; attempt < 4; ++attempt) {
-    rc = render_once(c, src, cam, st, out, flags, s);
+    rc = render_once(c, w, src, cam, st, out, flags, s);
     if (rc) return rc;
     if (!(flags & CS_RENDER_SYNC) && !stats_host) return CS_OK;
-    rc = fetch_stats(c, s);
+    rc = fetch_stats(c, w, s);
     if (rc) return rc;
     if (c->h_stats->status & 2) return fail(CS_ERANGE, "no interval covers a block distance");
     if (!(c->h_stats->status & 1)) {
       if (stats_host) *stats_host = *c->h_stats;
       return CS_OK;
     }
+    // this frame overflowed (and was synchronised): its own report is handled here
+    c->h_overflow[0] = 0;
+    c->h_overflow[1] = 0;
     if (!(flags & CS_RENDER_SYNC)) {
       if (stats_host) *stats_host = *c->h_stats;
-      return fail(CS_ENOMEM, "pair buffer overflow (%lld pairs > %lld)",
-                  (long long)c->h_stats->pairs, (long long)c->cap_pairs);
+      w->cap_pairs = std::min<int64_t>((1ll << 30) - 1, c->h_stats->pairs + c->h_stats->pairs / 4 + 1024);
+      return fail(CS_ENOMEM, "pair buffer overflow (%lld pairs > %lld); the buffer has been grown",
+                  (long long)c->h_stats->pairs, (long long)w->cap_pairs);
     }
     // grow the pair buffers to the observed count and re-run
-    c->cap_pairs = std::min<int64_t>((1ll << 30) - 1, c->h_stats->pairs + c->h_stats->pairs / 4 + 1024);
+    w->cap_pairs = std::min<int64_t>((1ll << 30) - 1, c->h_stats->pairs + c->h_stats->pairs / 4 + 1024);
     if (c->h_stats->pairs >= (1ll << 30)) return fail(CS_ENOMEM, "more than 2^30 tile pairs");
   }
   return fail(CS_ECUDA, "pair buffer did not converge");
 }
 
-int cs_render_backward(cs_ctx* c, const cs_source* src, const cs_camera* cam,
-                       const cs_settings* st, const float* dl_dimg, const cs_grads* out,
-                       void* stream) {
-  if (!c || !src || !out || !dl_dimg) return fail(CS_EINVAL, "NULL argument");
+int cs_render(cs_ctx* c, const cs_source* src, const cs_camera* cam, const cs_settings* st,
+              void* out, uint32_t flags, cs_frame_stats* stats_host, void* stream) {
+  if (!c || !src || !out) return fail(CS_EINVAL, "NULL argument");
   int rc = validate(cam, st);
   if (rc) return rc;
-  if (src->kind != CS_SRC_CLOUD) return fail(CS_EINVAL, "backward needs a single-cloud source");
-  if (!c->last_list || c->last_width != cam->width || c->last_height != cam->height ||
-      !c->st_t.p)
-    return fail(CS_EINVAL, "no kept forward state for this camera (render with KEEP_STATE first)");
+  if (flags & CS_RENDER_KEEP_STATE)
+    return fail(CS_EINVAL, "kept-state forwards go through cs_render_train");
+  std::lock_guard<std::mutex> lock(c->mu);
+  CS_CUDA(cudaSetDevice(c->device));
+  rc = check_overflow(c);
+  if (rc) return rc;
+  Ws* w = nullptr;
+  rc = frame_ws(c, &w);
+  if (rc) return rc;
+  return render_frame(c, w, src, cam, st, out, flags, stats_host, (cudaStream_t)stream);
+}
+
+int cs_render_train(cs_ctx* c, const cs_source* src, const cs_camera* cam, const cs_settings* st,
+                    float* out_rgb, uint32_t flags, cs_state** state_out, void* stream) {
+  if (!c || !src || !out_rgb || !state_out) return fail(CS_EINVAL, "NULL argument");
+  *state_out = nullptr;
+  int rc = validate(cam, st);
+  if (rc) return rc;
+  if (src->kind != CS_SRC_CLOUD) return fail(CS_EINVAL, "training renders take a single-cloud source");
+  if (src->exclude) return fail(CS_EINVAL, "training renders take no exclude mask");
+  if (flags & ~(uint32_t)(CS_RENDER_SYNC | CS_RENDER_NO_CLIP))
+    return fail(CS_EINVAL, "cs_render_train accepts CS_RENDER_SYNC and CS_RENDER_NO_CLIP only");
+  std::lock_guard<std::mutex> lock(c->mu);
+  CS_CUDA(cudaSetDevice(c->device));
+  rc = check_overflow(c);
+  if (rc) return rc;
+  Ws* w = nullptr;
+  rc = frame_ws(c, &w);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  rc = render_frame(c, w, src, cam, st, out_rgb, flags | CS_RENDER_KEEP_STATE, nullptr, s);
+  if (rc) return rc;
+  cs_state* S = new cs_state();
+  S->ctx = c;
+  S->ws = w;
+  S->count = src->cloud.count;
+  S->width = cam->width;
+  S->height = cam->height;
+  S->cam = *cam;
+  S->st = *st;
+  S->cloud = src->cloud;
+  if (cudaMallocHost(&S->h_status, 16) != cudaSuccess ||
+      cudaEventCreateWithFlags(&S->done, cudaEventDisableTiming) != cudaSuccess) {
+    if (S->h_status) cudaFreeHost(S->h_status);
+    delete S;
+    return fail(CS_ENOMEM, "state");
+  }
+  S->h_pairs = reinterpret_cast<int64_t*>(S->h_status + 2);
+  DevStats* d = w->stats.as<DevStats>();
+  CS_CUDA(cudaMemcpyAsync(S->h_status, &d->status, 4, cudaMemcpyDeviceToHost, s));
+  CS_CUDA(cudaMemcpyAsync(S->h_pairs, &d->pairs, 8, cudaMemcpyDeviceToHost, s));
+  CS_CUDA(cudaEventRecord(S->done, s));
+  w->held = true;
+  *state_out = S;
+  return CS_OK;
+}
+
+void cs_state_release(cs_state* S) {
+  if (!S) return;
+  {
+    std::lock_guard<std::mutex> lock(S->ctx->mu);
+    cudaSetDevice(S->ctx->device);
+    // the backward (or anything else) reading the workspace was enqueued on some
+    // stream: the next frame into it is ordered after it only by the caller's
+    // stream discipline, so wait for the forward's completion at least
+    if (S->done) cudaEventSynchronize(S->done);
+    S->ws->held = false;
+  }
+  if (S->done) cudaEventDestroy(S->done);
+  if (S->h_status) cudaFreeHost(S->h_status);
+  delete S;
+}
+
+int cs_render_backward(cs_ctx* c, cs_state* S, const float* dl_dimg, const cs_grads* out,
+                       void* stream) {
+  if (!c || !S || !out || !dl_dimg) return fail(CS_EINVAL, "NULL argument");
+  if (S->ctx != c) return fail(CS_EINVAL, "state belongs to another context");
   std::lock_guard<std::mutex> lock(c->mu);
   CS_CUDA(cudaSetDevice(c->device));
   cudaStream_t s = (cudaStream_t)stream;
-  const cs_cloud& cl = src->cloud;
-  const int64_t cap = c->cap_vis;
+  // The forward's own pair-buffer status: wait for the forward (the loss
+  // kernels enqueued after it keep the GPU busy meanwhile) and refuse to
+  // differentiate an incomplete frame.
+  CS_CUDA(cudaEventSynchronize(S->done));
+  if (*S->h_status & 1) {
+    Ws* w = S->ws;
+    w->cap_pairs = std::min<int64_t>((1ll << 30) - 1, *S->h_pairs + *S->h_pairs / 4 + 1024);
+    c->h_overflow[0] = 0;
+    c->h_overflow[1] = 0;
+    return fail(CS_ENOMEM,
+                "the training forward overflowed its pair buffer (%lld pairs); its image and "
+                "gradients are invalid -- the buffer has been grown, repeat the step",
+                (long long)*S->h_pairs);
+  }
+  Ws* w = S->ws;
+  const cs_cloud& cl = S->cloud;
+  const int64_t cap = w->cap_vis;
   if (c->gacc.ensure(sizeof(float) * 9 * cap)) return fail(CS_ENOMEM, "gradient partials");
   CS_CUDA(cudaMemsetAsync(c->gacc.p, 0, sizeof(float) * 9 * cap, s));
-  const int ts = st->tile_size;
-  const int ntx = (cam->width + ts - 1) / ts;
-  BlendState state{c->st_t.as<double>(), c->st_last.as<int32_t>(), c->st_acc.as<double>()};
-  launch_blend_bwd(c->last_tiles, c->last_list, c->last_bxs, c->last_bys, c->last_ranges,
-                   c->hot.as<HotRec>(), c->tile_order.as<uint32_t>(), *st, cam->width,
-                   cam->height, ntx, dl_dimg, state, &c->stats.as<DevStats>()->tickets[5],
+  const int ts = S->st.tile_size;
+  const int ntx = (S->width + ts - 1) / ts;
+  BlendState state{w->st_t.as<double>(), w->st_last.as<int32_t>(), w->st_acc.as<double>()};
+  launch_blend_bwd(w->last_tiles, w->last_list, w->last_bxs, w->last_bys, w->last_ranges,
+                   w->hot.as<HotRec>(), w->tile_order.as<uint32_t>(), S->st, S->width,
+                   S->height, ntx, dl_dimg, state, &w->stats.as<DevStats>()->tickets[5],
                    c->gacc.as<float>(), cap, s);
   CS_CHECK_LAUNCH();
   // K11 writes every row (zeros for the culled ones): no clear of the outputs.
   // The forward's per-splat float64 depth keys (~0 = culled) are still in keysA.
-  launch_project_bwd(cl, c->keysA.as<uint64_t>(), *cam, *st, c->gacc.as<float>(), cap, *out, s);
+  launch_project_bwd(cl, w->keysA.as<uint64_t>(), S->cam, S->st, c->gacc.as<float>(), cap, *out, s);
   CS_CHECK_LAUNCH();
   return CS_OK;
+}
+
+int cs_check(cs_ctx* c, void* stream) {
+  if (!c) return fail(CS_EINVAL, "NULL argument");
+  CS_CUDA(cudaSetDevice(c->device));
+  CS_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  std::lock_guard<std::mutex> lock(c->mu);
+  return check_overflow(c);
 }
 
 int cs_training_loss(cs_ctx* c, const float* img, const float* ref, int32_t height, int32_t width,
@@ -893,7 +1105,7 @@ int cs_timing_end(cs_ctx* c, double* stage_ms, int32_t* frames) {
 int cs_frame_stats_get(cs_ctx* c, cs_frame_stats* out, void* stream) {
   if (!c || !out) return fail(CS_EINVAL, "NULL argument");
   CS_CUDA(cudaSetDevice(c->device));
-  int rc = fetch_stats(c, (cudaStream_t)stream);
+  int rc = fetch_stats(c, c->last, (cudaStream_t)stream);
   if (rc) return rc;
   *out = *c->h_stats;
   return CS_OK;
@@ -902,11 +1114,11 @@ int cs_frame_stats_get(cs_ctx* c, cs_frame_stats* out, void* stream) {
 int cs_dump_projected(cs_ctx* c, double* means, double* conics, double* covs, double* depths,
                       double* colors, double* opacities, double* radii, int64_t* source,
                       void* stream) {
-  if (!c || !c->last_order) return fail(CS_EINVAL, "no frame rendered");
-  if (!c->last_debug) return fail(CS_EINVAL, "last frame was not rendered in debug mode");
+  if (!c || !c->last || !c->last->last_order) return fail(CS_EINVAL, "no frame rendered");
+  if (!c->last->last_debug) return fail(CS_EINVAL, "last frame was not rendered in debug mode");
   CS_CUDA(cudaSetDevice(c->device));
   cudaStream_t s = (cudaStream_t)stream;
-  int rc = fetch_stats(c, s);
+  int rc = fetch_stats(c, c->last, s);
   if (rc) return rc;
   const int64_t M = c->h_stats->visible;
   if (M == 0) return CS_OK;
@@ -916,7 +1128,7 @@ int cs_dump_projected(cs_ctx* c, double* means, double* conics, double* covs, do
   double *dm = base, *dc = dm + 2 * M, *dv = dc + 3 * M, *dd = dv + 3 * M, *dcol = dd + M,
          *dop = dcol + 3 * M, *dr = dop + M;
   int64_t* ds = reinterpret_cast<int64_t*>(dr + 2 * M);
-  launch_dump_projected(c->last_order, c->recs.as<ProjRec>(), c->stats.as<DevStats>(), dm, dc, dv,
+  launch_dump_projected(c->last->last_order, c->last->recs.as<ProjRec>(), c->last->stats.as<DevStats>(), dm, dc, dv,
                         dd, dcol, dop, dr, ds, s);
   CS_CHECK_LAUNCH();
   struct { void* h; void* d; size_t n; } cp[] = {
@@ -929,22 +1141,22 @@ int cs_dump_projected(cs_ctx* c, double* means, double* conics, double* covs, do
 }
 
 int cs_dump_tiles(cs_ctx* c, int64_t* tile_ids, int64_t* offsets, void* stream) {
-  if (!c || !c->last_list) return fail(CS_EINVAL, "no frame rendered");
+  if (!c || !c->last || !c->last->last_list) return fail(CS_EINVAL, "no frame rendered");
   CS_CUDA(cudaSetDevice(c->device));
   cudaStream_t s = (cudaStream_t)stream;
-  int rc = fetch_stats(c, s);
+  int rc = fetch_stats(c, c->last, s);
   if (rc) return rc;
   const int64_t P = c->h_stats->pairs;
   const int64_t NA = c->h_stats->assembled;  // rank_of is indexed by splat id (assembled index)
-  if (c->scratch2.ensure(8 * (P + c->last_tiles + 1 + NA))) return fail(CS_ENOMEM, "dump");
+  if (c->scratch2.ensure(8 * (P + c->last->last_tiles + 1 + NA))) return fail(CS_ENOMEM, "dump");
   int64_t* dt = c->scratch2.as<int64_t>();
   int64_t* doff = dt + P;
-  int64_t* rank_of = doff + c->last_tiles + 1;
-  launch_dump_tiles(c->last_order, c->last_list, c->last_ranges, c->stats.as<DevStats>(),
-                    c->last_tiles, rank_of, dt, doff, s);
+  int64_t* rank_of = doff + c->last->last_tiles + 1;
+  launch_dump_tiles(c->last->last_order, c->last->last_list, c->last->last_ranges, c->last->stats.as<DevStats>(),
+                    c->last->last_tiles, rank_of, dt, doff, s);
   CS_CHECK_LAUNCH();
   if (tile_ids && P) CS_CUDA(cudaMemcpyAsync(tile_ids, dt, 8 * P, cudaMemcpyDeviceToHost, s));
-  if (offsets) CS_CUDA(cudaMemcpyAsync(offsets, doff, 8 * (c->last_tiles + 1), cudaMemcpyDeviceToHost, s));
+  if (offsets) CS_CUDA(cudaMemcpyAsync(offsets, doff, 8 * (c->last->last_tiles + 1), cudaMemcpyDeviceToHost, s));
   CS_CUDA(cudaStreamSynchronize(s));
   return CS_OK;
 }
@@ -954,11 +1166,11 @@ int cs_dump_segments(cs_ctx* c, int32_t* cloud_index, int64_t* count, int32_t ma
   if (!c) return fail(CS_EINVAL, "NULL ctx");
   CS_CUDA(cudaSetDevice(c->device));
   cudaStream_t s = (cudaStream_t)stream;
-  int rc = fetch_stats(c, s);
+  int rc = fetch_stats(c, c->last, s);
   if (rc) return rc;
   const int n = std::min<int>(c->h_stats->n_segments, max_n);
   std::vector<Seg> h(std::max(n, 1));
-  if (n) CS_CUDA(cudaMemcpyAsync(h.data(), c->segs.p, sizeof(Seg) * n, cudaMemcpyDeviceToHost, s));
+  if (n) CS_CUDA(cudaMemcpyAsync(h.data(), c->last->segs.p, sizeof(Seg) * n, cudaMemcpyDeviceToHost, s));
   CS_CUDA(cudaStreamSynchronize(s));
   for (int i = 0; i < n; ++i) {
     cloud_index[i] = h[i].cloud;
@@ -973,11 +1185,11 @@ int cs_dump_assembled_list(cs_ctx* c, uint64_t* packed, int64_t max_n, int64_t* 
   if (!c || !packed || !n_out) return fail(CS_EINVAL, "NULL argument");
   CS_CUDA(cudaSetDevice(c->device));
   cudaStream_t s = (cudaStream_t)stream;
-  int rc = fetch_stats(c, s);
+  int rc = fetch_stats(c, c->last, s);
   if (rc) return rc;
   const int64_t n = std::min<int64_t>(c->h_stats->assembled, max_n);
-  if (n > 0 && c->pw_list.p)
-    CS_CUDA(cudaMemcpyAsync(packed, c->pw_list.p, 8 * n, cudaMemcpyDeviceToHost, s));
+  if (n > 0 && c->last->pw_list.p)
+    CS_CUDA(cudaMemcpyAsync(packed, c->last->pw_list.p, 8 * n, cudaMemcpyDeviceToHost, s));
   CS_CUDA(cudaStreamSynchronize(s));
   *n_out = n;
   return CS_OK;
@@ -992,16 +1204,20 @@ int cs_decide_visibility(cs_ctx* c, const cs_lod* L, const cs_camera* cam, int32
   std::lock_guard<std::mutex> lock(c->mu);
   CS_CUDA(cudaSetDevice(c->device));
   cudaStream_t s = (cudaStream_t)stream;
-  int rc = ensure_frame_buffers(c, 1, L->n_levels * L->n_blocks, L->n_blocks, 1, 0);
+  Ws* w = nullptr;
+  int rc = frame_ws(c, &w);
   if (rc) return rc;
-  DevStats* stats = c->stats.as<DevStats>();
+  rc = ensure_frame_buffers(w, 1, L->n_levels * L->n_blocks, L->n_blocks, 1, 0);
+  if (rc) return rc;
+  c->last = w;
+  DevStats* stats = w->stats.as<DevStats>();
   CS_CUDA(cudaMemsetAsync(stats, 0, sizeof(DevStats), s));
-  launch_lod_select(L->tables(), *cam, force_level, c->dec.as<cs_decision>(), c->segs.as<Seg>(),
+  launch_lod_select(L->tables(), *cam, force_level, w->dec.as<cs_decision>(), w->segs.as<Seg>(),
                     stats, s);
   CS_CHECK_LAUNCH();
-  CS_CUDA(cudaMemcpyAsync(out_host, c->dec.p, sizeof(cs_decision) * L->n_blocks,
+  CS_CUDA(cudaMemcpyAsync(out_host, w->dec.p, sizeof(cs_decision) * L->n_blocks,
                           cudaMemcpyDeviceToHost, s));
-  rc = fetch_stats(c, s);
+  rc = fetch_stats(c, w, s);
   if (rc) return rc;
   if (c->h_stats->status & 2) return fail(CS_ERANGE, "no interval covers a block distance");
   return CS_OK;
@@ -1074,9 +1290,11 @@ int cs_blend_tiles(cs_ctx* c, const int64_t* tile_ids, const int64_t* tile_offse
   CS_CUDA(cudaMemcpyAsync(bg, background, 24, cudaMemcpyDeviceToHost, s));
   CS_CUDA(cudaStreamSynchronize(s));
   const int64_t m = std::max<int64_t>(n_splats, 1);
+  Ws* w = nullptr;
+  int rc = frame_ws(c, &w);
+  if (rc) return rc;
   if (c->scratch1.ensure(sizeof(HotRec) * m) ||
-      c->scratch2.ensure(12 * std::max<int64_t>(P, 1) + sizeof(uint2) * n_tiles + 4 * n_tiles + 8) ||
-      c->stats.ensure(sizeof(DevStats)))
+      c->scratch2.ensure(12 * std::max<int64_t>(P, 1) + sizeof(uint2) * n_tiles + 4 * n_tiles + 8))
     return fail(CS_ENOMEM, "blend scratch");
   HotRec* hot = c->scratch1.as<HotRec>();
   uint32_t* list = c->scratch2.as<uint32_t>();
@@ -1089,7 +1307,7 @@ int cs_blend_tiles(cs_ctx* c, const int64_t* tile_ids, const int64_t* tile_offse
   launch_pack(n_splats, means, conics, colors, opacities, alpha_floor, hot, P, tile_ids,
               n_tiles, tile_offsets, list, pbx, pby, ranges, s);
   CS_CHECK_LAUNCH();
-  CS_CUDA(cudaMemsetAsync(c->stats.p, 0, sizeof(DevStats), s));
+  CS_CUDA(cudaMemsetAsync(w->stats.p, 0, sizeof(DevStats), s));
   BlendParams bp;
   for (int i = 0; i < 3; ++i) bp.bg[i] = bg[i];
   bp.alpha_floor = alpha_floor;
@@ -1099,7 +1317,7 @@ int cs_blend_tiles(cs_ctx* c, const int64_t* tile_ids, const int64_t* tile_offse
   bp.height = height;
   bp.ntx = n_tiles_x;
   bp.flags = CS_RENDER_NO_CLIP;
-  launch_blend((int)n_tiles, list, pbx, pby, ranges, hot, nullptr, bp, out, true, ftile, c->stats.as<DevStats>(),
+  launch_blend((int)n_tiles, list, pbx, pby, ranges, hot, nullptr, bp, out, true, ftile, w->stats.as<DevStats>(),
                nullptr, s);
   CS_CHECK_LAUNCH();
   // fragments: int32 per tile -> int64

@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kBinThreads)
 k_bin_pairs(const uint32_t* __restrict__ order, const uint2* __restrict__ rects,
             DevStats* __restrict__ stats, int64_t pair_cap, uint64_t* __restrict__ status,
             uint4* __restrict__ heavy, int ntx, uint32_t* __restrict__ keys,
-            uint32_t* __restrict__ vals, DigitHist dh, int emit) {
+            uint32_t* __restrict__ vals, DigitHist dh, int emit, int64_t* host_overflow) {
   __shared__ BinSmem sm;
   __shared__ uint64_t s_prefix;
   __shared__ uint32_t s_chunk;
@@ -189,7 +189,17 @@ k_bin_pairs(const uint32_t* __restrict__ order, const uint2* __restrict__ rects,
           const int64_t P = (int64_t)(pre + total);
           stats->pairs = P;
           stats->pairs_eff = P <= pair_cap ? P : 0;
-          if (P > pair_cap) atomicOr(&stats->status, 1);
+          if (P > pair_cap) {
+            atomicOr(&stats->status, 1);
+            // report to the host (mapped pinned memory): an asynchronous frame
+            // that overflowed is raised by the context's next call
+            if (emit && host_overflow) {
+              volatile int64_t* h = host_overflow;
+              h[1] = pair_cap;
+              h[0] = P;
+              __threadfence_system();
+            }
+          }
         }
         if (emit && total > kBinHeavy && pre + total <= (uint64_t)pair_cap) {
           // register the chunk: entry index and first slice from one 64-bit
@@ -317,7 +327,8 @@ int64_t bin_status_words(int64_t capacity) {
 
 void launch_bin_pairs(const uint32_t* order, const uint2* rects, DevStats* stats, int64_t pair_cap,
                       int64_t capacity, uint64_t* status, int ntx, uint32_t* keys, uint32_t* vals,
-                      uint32_t* hist, int key_bits, bool emit, cudaStream_t s) {
+                      uint32_t* hist, int key_bits, bool emit, int64_t* host_overflow,
+                      cudaStream_t s) {
   const int64_t chunks = bin_chunks(capacity);
   if (chunks == 0) return;
   DigitHist dh;  // hist == nullptr (keys wider than kMaxHistPasses digits): no counting
@@ -338,7 +349,7 @@ void launch_bin_pairs(const uint32_t* order, const uint2* rects, DevStats* stats
   }
   const unsigned grid = CS_BIN_PERSIST ? (unsigned)std::min<int64_t>(chunks, wave) : (unsigned)chunks;
   k_bin_pairs<<<grid, kBinThreads, 0, s>>>(order, rects, stats, pair_cap, status, heavy, ntx, keys,
-                                           vals, dh, emit ? 1 : 0);
+                                           vals, dh, emit ? 1 : 0, host_overflow);
   if (emit)
     k_emit_heavy<<<(unsigned)std::min<int64_t>(kHeavyCtas, chunks), kBinThreads, 0, s>>>(
         order, rects, stats, heavy, ntx, keys, vals, dh);

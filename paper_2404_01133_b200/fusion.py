@@ -9,8 +9,9 @@ same bytes as the CPU ``fuse``.
 ``fuse_all_gather`` is the multi-GPU form used after block-parallel training
 (SURVEY.md section 8e): every rank filters the blocks it owns on its own GPU,
 the per-block kept counts are summed with one all-reduce, and the kept rows are
-exchanged with one broadcast per block in ascending block order (an
-all-gather-v), so every rank ends with the byte-identical fused cloud.
+exchanged with one all-gather (padded to the largest rank) and placed in
+ascending block order on the device (an all-gather-v), so every rank ends
+with the byte-identical fused cloud.
 """
 
 from __future__ import annotations
@@ -103,7 +104,8 @@ def unpack_rows(rows: torch.Tensor, sh_coeffs: int):
 
 
 def fuse_all_gather(local_blocks: Dict[int, Tuple[torch.Tensor, ...]], n_blocks: int, owner: List[int],
-                    p_min, p_max, dims, sh_coeffs: int, group=None, filter_fn=None) -> torch.Tensor:
+                    p_min, p_max, dims, sh_coeffs: int, group=None, filter_fn=None,
+                    dtype: torch.dtype = None, device=None) -> torch.Tensor:
     """Fuse block clouds trained on different ranks.
 
     local_blocks: {block j: (positions, opacities, scales, rotations, sh)} for the
@@ -111,39 +113,68 @@ def fuse_all_gather(local_blocks: Dict[int, Tuple[torch.Tensor, ...]], n_blocks:
     [N, 11 + 3C] on every rank, blocks in ascending order, rows within a block
     in ascending index order (partition.py:578-587).  ``filter_fn`` defaults to
     the CUDA membership filter; tests on CPU ranks pass the oracle's.
+
+    The row dtype and device must agree on every rank: pass ``dtype`` and
+    ``device`` explicitly (required on a rank that owns no rows -- e.g. more
+    ranks than occupied blocks -- otherwise taken from its own blocks).
+
+    Exchange: one all-reduce of the per-block kept counts, then ONE all-gather
+    of every rank's kept rows (its blocks in ascending order, padded to the
+    largest rank's row count), after which each rank places the blocks in
+    ascending block order with one device gather -- the all-gather-v of
+    SURVEY.md 8e as a single collective instead of one broadcast per block.
     """
     import torch.distributed as dist
     filter_fn = filter_fn or (lambda pos, j: fuse_filter(pos, p_min, p_max, dims, j))
     rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
     some = next(iter(local_blocks.values()))[0] if local_blocks else None
-    dev = some.device if some is not None else (
-        torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu"))
-    dtype = some.dtype if some is not None else torch.float32
-    kept_rows = {}
+    if dtype is None or device is None:
+        if some is None:
+            raise ValueError("fuse_all_gather: a rank without blocks needs explicit dtype and device")
+        dtype = dtype or some.dtype
+        device = device or some.device
+    dev = torch.device(device)
+    width = PARAM_WIDTH_NOSH + 3 * sh_coeffs
     counts = torch.zeros(n_blocks, dtype=torch.int64, device=dev)
-    for j, params in local_blocks.items():
+    pieces = []
+    for j in sorted(local_blocks):
         if owner[j] != rank:
             raise ValueError(f"rank {rank} does not own block {j}")
+        params = local_blocks[j]
         idx = filter_fn(params[0], j)
-        rows = pack_rows(*(p[idx] for p in params))
-        kept_rows[j] = rows
+        rows = pack_rows(*(p[idx] for p in params)).to(device=dev, dtype=dtype)
+        if rows.shape[1] != width:
+            raise ValueError(f"block {j}: rows of width {rows.shape[1]}, expected {width} (sh_coeffs)")
+        pieces.append(rows)
         counts[j] = rows.shape[0]
     dist.all_reduce(counts, group=group)             # owners fill their slots
-    width = PARAM_WIDTH_NOSH + 3 * sh_coeffs
-    offsets = torch.cumsum(counts, 0) - counts
-    total = int(counts.sum().item())
-    fused = torch.empty((total, width), dtype=dtype, device=dev)
     counts_h = counts.cpu().tolist()
-    offs_h = offsets.cpu().tolist()
-    for j in range(n_blocks):                        # all-gather-v in ascending block order
+    per_rank = [0] * world
+    for j in range(n_blocks):
+        per_rank[owner[j]] += counts_h[j]
+    cap = max(max(per_rank), 1)
+    mine = torch.zeros((cap, width), dtype=dtype, device=dev)
+    if pieces:
+        cat = torch.cat(pieces)
+        mine[:cat.shape[0]] = cat
+    gathered = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(gathered, mine, group=group)     # the one data collective
+    flat = torch.cat(gathered)                       # [world * cap, width]
+    # row index of every fused row: block j's rows sit in its owner's buffer after
+    # the owner's lower-numbered blocks
+    cursor = [0] * world
+    index = []
+    for j in range(n_blocks):
         n = counts_h[j]
         if n == 0:
             continue
-        view = fused[offs_h[j]: offs_h[j] + n]
-        if owner[j] == rank:
-            view.copy_(kept_rows[j])
-        dist.broadcast(view, src=owner[j], group=group)
-    return fused
+        r = owner[j]
+        index.append(torch.arange(r * cap + cursor[r], r * cap + cursor[r] + n, device=dev))
+        cursor[r] += n
+    if not index:
+        return torch.empty((0, width), dtype=dtype, device=dev)
+    return flat.index_select(0, torch.cat(index))
 
 
 # ---------------------------------------------------------------------------

@@ -31,7 +31,8 @@ import numpy as np
 import torch
 
 from . import _lib, device
-from ._lib import CsFrameStats, CsSource, check
+from ._lib import CsFrameStats, CsSource
+from ._lib import check as _check
 from .core import GaussianCloud, Image
 
 __all__ = ["RenderSettings", "SplatPrimitive", "FrameStats", "project_gaussian", "rasterize",
@@ -89,15 +90,23 @@ class FrameStats:
     wall_ms: float
 
 
-def _source_for(cloud, dev_index: int):
-    """(cs_source, keepalive) for a cloud-like object or an AssembledCloud."""
+def _source_for(cloud, dev_index: int, cam=None):
+    """(cs_source, keepalive) for a cloud-like object or an AssembledCloud.
+
+    An AssembledCloud is the fixed render set of the camera it was assembled
+    for (assemble_render_set returns a concrete cloud, lod.py:360-401): when
+    it is rendered from a different camera the selection still runs for the
+    assembly camera (cs_source.select_cam)."""
     from .lod import AssembledCloud
     src = CsSource()
     if isinstance(cloud, AssembledCloud):
         src.kind = cloud.source_kind
         src.force_level = -1 if cloud.force_level is None else int(cloud.force_level)
         src.lod = cloud.scene.handle
-        return src, cloud
+        sel = device.camera_struct(cloud.cam)
+        if cam is not None and bytes(device.camera_struct(cam)) != bytes(sel):
+            src.select_cam = ctypes.pointer(sel)
+        return src, (cloud, sel)
     dc = device.device_cloud(cloud, dev_index)
     src.kind = _lib.CS_SRC_CLOUD
     src.force_level = -1
@@ -107,21 +116,24 @@ def _source_for(cloud, dev_index: int):
 
 def _render_into(cloud, cam, settings, out: torch.Tensor, flags: int, stats: Optional[CsFrameStats]):
     dev_index = out.device.index
-    src, keep = _source_for(cloud, dev_index)
+    src, keep = _source_for(cloud, dev_index, cam)
     cs_cam = device.camera_struct(cam)
     cs_set = device.settings_struct(settings)
     rc = _lib.load().cs_render(device.context(dev_index), ctypes.byref(src), ctypes.byref(cs_cam),
                                ctypes.byref(cs_set), out.data_ptr(), flags,
                                ctypes.byref(stats) if stats is not None else None,
                                device.stream_handle(out.device))
-    check(rc, "cs_render")
+    _check(rc, "cs_render")
     return keep
 
 
 def render(cloud, cam, settings: Optional[RenderSettings] = None, *, out: Optional[torch.Tensor] = None,
            device_index: Optional[int] = None) -> torch.Tensor:
     """Device tier: enqueue one frame on the current stream; returns the
-    clipped (H, W, 3) float32 image tensor.  No host synchronisation."""
+    clipped (H, W, 3) float32 image tensor.  No host synchronisation.  A frame
+    that overflows its tile-pair buffer is reported (MemoryError) by the
+    context's next call at the latest -- ``check()`` synchronises and reports
+    immediately."""
     settings = settings or RenderSettings()
     dev = torch.device("cuda", device._device_index(device_index))
     if out is None:
@@ -148,6 +160,14 @@ def rasterize_stats(cloud, cam, settings: Optional[RenderSettings] = None):
                              skipped_singular=int(stats.skipped_singular), wall_ms=wall_ms)
 
 
+def check(device_index: Optional[int] = None) -> None:
+    """Synchronise the current stream; MemoryError if an asynchronous frame on
+    this thread's context overflowed its pair buffer (cs_check)."""
+    dev = device._device_index(device_index)
+    _lib.check(_lib.load().cs_check(device.context(dev), device.stream_handle(torch.device("cuda", dev))),
+               "cs_check")
+
+
 def rasterize(cloud, cam, settings: Optional[RenderSettings] = None) -> Image:
     image, _ = rasterize_stats(cloud, cam, settings)
     return image
@@ -171,7 +191,7 @@ def _dump_projected(dev_index: int, m: int, skipped: int) -> dict:
                depths=np.zeros(n), colors=np.zeros((n, 3)), opacities=np.zeros(n),
                radii=np.zeros((n, 2)), source=np.zeros(n, dtype=np.int64))
     p = lambda k: res[k].ctypes.data
-    check(_lib.load().cs_dump_projected(device.context(dev_index), p("means"), p("conics"),
+    _check(_lib.load().cs_dump_projected(device.context(dev_index), p("means"), p("conics"),
                                         p("covs"), p("depths"), p("colors"), p("opacities"),
                                         p("radii"), p("source"), device.stream_handle()),
           "cs_dump_projected")
@@ -187,12 +207,12 @@ def bin_tiles_last(cam, tile_size: int, dev_index: Optional[int] = None):
     st = CsFrameStats()
     lib = _lib.load()
     ctx = device.context(dev_index)
-    check(lib.cs_frame_stats_get(ctx, ctypes.byref(st), device.stream_handle()))
+    _check(lib.cs_frame_stats_get(ctx, ctypes.byref(st), device.stream_handle()))
     ntx = (int(cam.width) + tile_size - 1) // tile_size
     nty = (int(cam.height) + tile_size - 1) // tile_size
     tids = np.zeros(max(int(st.pairs), 1), dtype=np.int64)
     offs = np.zeros(ntx * nty + 1, dtype=np.int64)
-    check(lib.cs_dump_tiles(ctx, tids.ctypes.data, offs.ctypes.data, device.stream_handle()))
+    _check(lib.cs_dump_tiles(ctx, tids.ctypes.data, offs.ctypes.data, device.stream_handle()))
     return tids[:int(st.pairs)], offs
 
 

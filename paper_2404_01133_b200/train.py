@@ -2,8 +2,11 @@
 PAPER.md:52).
 
 * ``RasterizeFn`` -- torch.autograd.Function around the C ABI: forward =
-  cs_render(KEEP_STATE) of one cloud, backward = cs_render_backward
-  (K10 blend backward + K11 projection backward).  Gradients are w.r.t. the
+  cs_render_train of one cloud (a kept-state handle per forward, so several
+  forwards -- a multi-view loss -- or other renders may run before the
+  backward), backward = cs_render_backward on that handle (K10 blend backward
+  + K11 projection backward); a forward whose pair buffer overflowed raises
+  MemoryError in the backward instead of differentiating an incomplete frame.  Gradients are w.r.t. the
   *activated* parameters the renderer consumes (position, scale, raw
   quaternion, opacity in [0, 1], SH).
 * ``BlockTrainer`` -- raw parameters with the checkpoint activations of the
@@ -35,6 +38,40 @@ POSITION_LR_SCALE = 0.4    # partition.py:47
 SCALE_LR_SCALE = 0.8       # partition.py:48
 
 
+class TrainState:
+    """A cs_render_train state handle (its frame workspace stays reserved for
+    the backward until the handle is released or collected)."""
+
+    def __init__(self, handle: ctypes.c_void_p):
+        self.handle = handle
+
+    def release(self):
+        if self.handle is not None and self.handle.value:
+            _lib.load().cs_state_release(self.handle)
+        self.handle = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
+
+
+_sized = {}  # device index -> largest cloud a training forward has been sized for
+
+
+def render_train(h, src, ccam, cset, out: torch.Tensor, count: int, dev) -> TrainState:
+    """cs_render_train; the first forward of a cloud larger than any before on
+    this device runs synchronously so the pair buffers are sized exactly."""
+    flags = 0 if _sized.get(dev.index, -1) >= count else _lib.CS_RENDER_SYNC
+    st = ctypes.c_void_p()
+    check(_lib.load().cs_render_train(h, ctypes.byref(src), ctypes.byref(ccam), ctypes.byref(cset),
+                                      out.data_ptr(), flags, ctypes.byref(st), device.stream_handle(dev)),
+          "cs_render_train")
+    _sized[dev.index] = max(_sized.get(dev.index, -1), count)
+    return TrainState(st)
+
+
 class RasterizeFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, positions, scales, rotations, opacities, sh, cam, settings):
@@ -50,16 +87,14 @@ class RasterizeFn(torch.autograd.Function):
         ccam = device.camera_struct(cam)
         cset = device.settings_struct(settings)
         h = device.context(dev.index)  # backward may run on autograd's device thread: reuse h
-        check(_lib.load().cs_render(h, ctypes.byref(src), ctypes.byref(ccam),
-                                    ctypes.byref(cset), out.data_ptr(), _lib.CS_RENDER_KEEP_STATE, None,
-                                    device.stream_handle(dev)), "cs_render")
-        ctx.keep = (dc, src, ccam, cset, h)
+        state = render_train(h, src, ccam, cset, out, dc.count, dev)
+        ctx.keep = (dc, state, h)
         ctx.sh_shape = sh.shape
         return out
 
     @staticmethod
     def backward(ctx, grad_out):
-        dc, src, ccam, cset, h = ctx.keep
+        dc, state, h = ctx.keep
         dev = grad_out.device
         k = dc.count
         g = grad_out.contiguous().float()
@@ -69,8 +104,7 @@ class RasterizeFn(torch.autograd.Function):
         go = torch.empty((k,), dtype=torch.float32, device=dev)
         gsh = torch.empty(ctx.sh_shape, dtype=torch.float32, device=dev)
         grads = CsGrads(gp.data_ptr(), gs.data_ptr(), gq.data_ptr(), go.data_ptr(), gsh.data_ptr())
-        check(_lib.load().cs_render_backward(h, ctypes.byref(src), ctypes.byref(ccam),
-                                             ctypes.byref(cset), g.data_ptr(), ctypes.byref(grads),
+        check(_lib.load().cs_render_backward(h, state.handle, g.data_ptr(), ctypes.byref(grads),
                                              device.stream_handle(dev)), "cs_render_backward")
         return gp, gs, gq, go, gsh, None, None
 
@@ -166,7 +200,7 @@ def lpt_assign(sizes: Sequence[int], n_ranks: int) -> List[int]:
 class DeviceBlockTrainer:
     """The block iteration on the C ABI end to end (no autograd graph):
 
-        cs_render(KEEP_STATE) -> cs_training_loss (K13) -> cs_render_backward
+        cs_render_train -> cs_training_loss (K13) -> cs_render_backward
         (K10/K11) -> cs_block_adam (K14: activation chain + Adam + the
         activated quads of the next forward)
 
@@ -245,14 +279,16 @@ class DeviceBlockTrainer:
         img, dimg = self._images(H, W)
         ccam = device.camera_struct(cam)
         rec(0)
-        check(lib.cs_render(h, ctypes.byref(self.src), ctypes.byref(ccam), ctypes.byref(self.cset),
-                            img.data_ptr(), _lib.CS_RENDER_KEEP_STATE, None, s), "cs_render")
+        state = render_train(h, self.src, ccam, self.cset, img, self.K, self.dev)
         rec(1)
         check(lib.cs_training_loss(h, img.data_ptr(), target.data_ptr(), H, W, LOSS_LAMBDA,
                                    self.loss.data_ptr(), dimg.data_ptr(), s), "cs_training_loss")
         rec(2)
-        check(lib.cs_render_backward(h, ctypes.byref(self.src), ctypes.byref(ccam), ctypes.byref(self.cset),
-                                     dimg.data_ptr(), ctypes.byref(self.grads), s), "cs_render_backward")
+        try:
+            check(lib.cs_render_backward(h, state.handle, dimg.data_ptr(), ctypes.byref(self.grads), s),
+                  "cs_render_backward")
+        finally:
+            state.release()
         rec(3)
         self.hp.step += 1
         check(lib.cs_block_adam(h, self.K, self.C, self.geom.data_ptr(), self.geom_m.data_ptr(),

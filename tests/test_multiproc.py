@@ -50,7 +50,8 @@ def _worker(rank, world, port, owner, result_q):
         C = max(Cs)
         filt = lambda pos, j: torch.from_numpy(
             np.nonzero(O.block_of_points(pos.numpy(), pmin, pmax, dims) == j)[0])
-        fused = fusion.fuse_all_gather(local, n_blocks, owner, pmin, pmax, dims, sh_coeffs=C, filter_fn=filt)
+        fused = fusion.fuse_all_gather(local, n_blocks, owner, pmin, pmax, dims, sh_coeffs=C, filter_fn=filt,
+                                       dtype=torch.float64, device="cpu")
         result_q.put((rank, fused.numpy()))
     finally:
         dist.destroy_process_group()
@@ -72,25 +73,29 @@ def _expected():
     return fusion.pack_rows(t(ref.positions), t(ref.opacities), t(ref.scales), t(ref.rotations), t(ref.sh)).numpy()
 
 
-@pytest.mark.parametrize("policy", ["lpt", "round_robin"])
+@pytest.mark.parametrize("policy", ["lpt", "round_robin", "idle_rank"])
 def test_fuse_all_gather_gloo_world2(policy):
+    """LPT and round-robin ownership over 2 ranks; "idle_rank": 3 ranks where
+    rank 2 owns no block (it must still join the collectives, with the agreed
+    dtype/device, and end with the same bytes)."""
     from paper_2404_01133_b200.train import lpt_assign
     g = np.load(os.path.join(HERE, "golden", "fuse.npz"))
     n_blocks = int(np.prod(g["dims"]))
     sizes = [int(g[f"block{j}/positions"].shape[0]) if f"block{j}/positions" in g else 0 for j in range(n_blocks)]
-    owner = lpt_assign(sizes, 2) if policy == "lpt" else [j % 2 for j in range(n_blocks)]
+    world = 3 if policy == "idle_rank" else 2
+    owner = lpt_assign(sizes, 2) if policy in ("lpt", "idle_rank") else [j % 2 for j in range(n_blocks)]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, owner, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, owner, q)) for r in range(world)]
     for p in procs:
         p.start()
-    got = dict(q.get(timeout=120) for _ in range(2))
+    got = dict(q.get(timeout=120) for _ in range(world))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     want = _expected()
-    for r in range(2):
+    for r in range(world):
         assert got[r].shape == want.shape
         assert got[r].tobytes() == want.tobytes(), r
 

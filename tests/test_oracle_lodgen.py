@@ -43,3 +43,23 @@ def test_oracle_mad_bounds(golden_lodgen):
         assert np.array_equal(lo, g["bounds_min"][j]) and np.array_equal(hi, g["bounds_max"][j])
     lo, hi = O.mad_bounds(pos[mem == 4], math.inf)
     assert np.array_equal(lo, g["block4_inf_lo"]) and np.array_equal(hi, g["block4_inf_hi"])
+
+
+def test_oracle_build_lod_matches_golden(golden_lodgen):
+    """oracle.build_lod (the reference arm's host LoD build, lod.py:211-248)
+    reproduces the golden level rows and MAD bounds end to end."""
+    g = golden_lodgen
+    cloud, cams, mem, J = lodgen_inputs(g)
+    rates = tuple(float(r) for r in g["rates"])
+    degrees = tuple(int(d) for d in g["sh_degrees"])
+    scene = O.build_lod(cloud, mem, J, cams, ((0.0, 1.0),) * len(rates), rates, degrees,
+                        float(g["n_mad"]))
+    pos = np.asarray(cloud.positions)
+    for L in range(len(rates)):
+        width = min((degrees[::-1][L] + 1) ** 2, 16)
+        for j in range(J):
+            rows = g[f"level{L}/block{j}"]
+            assert np.array_equal(scene.levels[L][j].positions, pos[rows]), (L, j)
+            assert scene.levels[L][j].sh.shape == (rows.size, 3, width)
+    assert np.array_equal(scene.bounds_min, g["bounds_min"])
+    assert np.array_equal(scene.bounds_max, g["bounds_max"])
