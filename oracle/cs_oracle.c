@@ -432,6 +432,54 @@ void or_blend_tiles(const int64_t* tile_ids, const int64_t* tile_offsets, int64_
   }
 }
 
+/* The accepted fragments of _kernels.blend_tiles (_kernels.py:46-72), per
+ * pixel in blend order: the discrete decisions the gradient oracle
+ * differentiates through (oracle/grad_oracle.py).  frag_splat == NULL: write
+ * the per-pixel accepted count into pix_count.  Otherwise write each pixel's
+ * accepted splat indices (into the depth-sorted arrays) at
+ * frag_splat[frag_offsets[pixel] ...]. */
+void or_blend_fragments(const int64_t* tile_ids, const int64_t* tile_offsets, int64_t n_tiles,
+                        const double* means, const double* conics, const double* opacities,
+                        int64_t tile_size, int64_t width, int64_t height, int64_t n_tiles_x,
+                        double alpha_floor, double t_floor, int64_t* pix_count,
+                        const int64_t* frag_offsets, int64_t* frag_splat, int nthreads) {
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t t = 0; t < n_tiles; ++t) {
+    int64_t tx = t % n_tiles_x, ty = t / n_tiles_x;
+    int64_t x0 = tx * tile_size, y0 = ty * tile_size;
+    int64_t x1 = x0 + tile_size < width ? x0 + tile_size : width;
+    int64_t y1 = y0 + tile_size < height ? y0 + tile_size : height;
+    int64_t s0 = tile_offsets[t], s1 = tile_offsets[t + 1];
+    for (int64_t py = y0; py < y1; ++py) {
+      double sy = (double)py + 0.5;
+      for (int64_t px = x0; px < x1; ++px) {
+        double sx = (double)px + 0.5;
+        double trans = 1.0;
+        int64_t n = 0;
+        const int64_t pix = py * width + px;
+        for (int64_t k = s0; k < s1; ++k) {
+          int64_t s = tile_ids[k];
+          double dx = sx - means[2 * s], dy = sy - means[2 * s + 1];
+          double power = -0.5 * (conics[3 * s] * dx * dx + conics[3 * s + 2] * dy * dy) -
+                         conics[3 * s + 1] * dx * dy;
+          double alpha = opacities[s] * exp(power);
+          if (alpha > 0.99) alpha = 0.99;
+          if (alpha < alpha_floor) continue;
+          double next_trans = trans * (1.0 - alpha);
+          if (next_trans < t_floor) break;
+          if (frag_splat) frag_splat[frag_offsets[pix] + n] = s;
+          ++n;
+          trans = next_trans;
+        }
+        if (!frag_splat) pix_count[pix] = n;
+      }
+    }
+  }
+}
+
 /* block_visible + select_level + decide_visibility + _screen_box,
  * lod.py:267-348.  Corner order x-major (lod.py:282-283); world_to_camera is
  * P @ R^T + t (core.py:376-377, no-FMA dgemm order under the pin); distance

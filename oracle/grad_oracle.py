@@ -147,3 +147,73 @@ def gradients(cloud, cam, settings, dl_dimg: np.ndarray):
     (img * torch.tensor(dl_dimg, dtype=torch.float64)).sum().backward()
     return img.detach().numpy(), [p.grad.numpy() if p.grad is not None else np.zeros(p.shape)
                                   for p in params]
+
+
+# ---------------------------------------------------------------------------
+# Sparse form for training-scale scenes (thousands to tens of thousands of
+# Gaussians, up to 1080p): the same float64 autograd restatement, but only the
+# ACCEPTED fragments enter the graph.  The C oracle (bit-pinned to the
+# reference) supplies the projection, the tile lists and every pixel's
+# accepted fragments in blend order (oracle.blend_fragments); per chunk of
+# pixels the transmittance is a cumulative product over a [pixels, max
+# fragments] matrix of (1 - alpha) -- exactly the dense form above, whose
+# non-accepted entries are 1 -- and the chunk's loss is back-propagated on its
+# own (retaining only the shared projection graph), so memory is bounded by the
+# chunk.
+
+
+def gradients_sparse(cloud, cam, settings, dl_dimg: np.ndarray, chunk_pixels: int = 1 << 16,
+                     nthreads: int = 0):
+    """(image, [d positions, d scales, d rotations, d opacities, d sh]) of
+    sum(image * dl_dimg), float64, for the rasterize of `cloud`."""
+    params = tuple(torch.tensor(np.asarray(a, dtype=np.float64), requires_grad=True)
+                   for a in (cloud.positions, cloud.scales, cloud.rotations, cloud.opacities, cloud.sh))
+    pos, scl, quat, opac, sh = params
+    H, W = int(cam.height), int(cam.width)
+    proj = O.project_cloud(cloud, cam, settings, nthreads=nthreads)
+    bg = torch.tensor(settings.background, dtype=torch.float64)
+    dl = torch.tensor(np.asarray(dl_dimg, dtype=np.float64).reshape(H * W, 3))
+    img = np.empty((H * W, 3))
+    if proj["count"] == 0:
+        img[:] = np.clip(np.asarray(settings.background, dtype=np.float64), 0.0, 1.0)
+        return img.reshape(H, W, 3), [np.zeros(p.shape) for p in params]
+    tid, toff, _, _ = O.bin_tiles(proj, cam, int(settings.tile_size))
+    poff, psplat = O.blend_fragments(tid, toff, proj, cam, settings, nthreads=nthreads)
+    src = torch.tensor(proj["source"], dtype=torch.long)
+    mean, conic, o, col = project_torch(pos, scl, quat, opac, sh, cam, int(settings.sh_degree), src)
+    # the shared projection graph: accumulate d(loss)/d(projected) over the
+    # chunks, then one backward through the projection
+    leaves = [t.detach().requires_grad_(True) for t in (mean, conic, o, col)]
+    acc = [torch.zeros_like(t) for t in leaves]
+    counts = np.diff(poff)
+    for p0 in range(0, H * W, chunk_pixels):
+        p1 = min(H * W, p0 + chunk_pixels)
+        n = counts[p0:p1]
+        f0, f1 = int(poff[p0]), int(poff[p1])
+        fmax = int(n.max()) if n.size else 0
+        pix = torch.tensor(np.repeat(np.arange(p1 - p0), n), dtype=torch.long)
+        slot = torch.tensor(np.arange(f1 - f0) - np.repeat(poff[p0:p1] - f0, n), dtype=torch.long)
+        spl = torch.tensor(psplat[f0:f1], dtype=torch.long)
+        m_, c_, o_, col_ = leaves
+        gpix = torch.arange(p0, p1, dtype=torch.long)
+        px = (gpix % W).to(torch.float64) + 0.5
+        py = (gpix // W).to(torch.float64) + 0.5
+        dx = px[pix] - m_[spl, 0]
+        dy = py[pix] - m_[spl, 1]
+        power = -0.5 * (c_[spl, 0] * dx * dx + c_[spl, 2] * dy * dy) - c_[spl, 1] * dx * dy
+        alpha = torch.clamp(o_[spl] * torch.exp(power), max=0.99)
+        A = torch.ones((p1 - p0, fmax + 1), dtype=torch.float64)
+        A = A.index_put((pix, slot + 1), 1.0 - alpha)
+        T = torch.cumprod(A, dim=1)                 # T[:, k] = transmittance before slot k
+        Tk = T[pix, slot]
+        Tend = T[:, -1]
+        rgb = torch.zeros((p1 - p0, 3), dtype=torch.float64).index_add(0, pix, (Tk * alpha)[:, None] * col_[spl])
+        out = torch.clamp(rgb + Tend[:, None] * bg[None, :], 0.0, 1.0)
+        img[p0:p1] = out.detach().numpy()
+        loss = (out * dl[p0:p1]).sum()
+        g = torch.autograd.grad(loss, leaves, allow_unused=True)
+        for a, gi in zip(acc, g):
+            if gi is not None:
+                a += gi
+    torch.autograd.backward([mean, conic, o, col], acc)
+    return img.reshape(H, W, 3), [p.grad.numpy() if p.grad is not None else np.zeros(p.shape) for p in params]

@@ -83,6 +83,8 @@ def lib():
         _lib.or_blend_tiles.argtypes = [P, P, i64, P, P, P, P, P, i64, i64, i64, i64,
                                         ctypes.c_double, ctypes.c_double, P, P, P, P,
                                         ctypes.c_int]
+        _lib.or_blend_fragments.argtypes = [P, P, i64, P, P, P, i64, i64, i64, i64, ctypes.c_double,
+                                            ctypes.c_double, P, P, P, ctypes.c_int]
         _lib.or_decide_visibility.restype = ctypes.c_int
         _lib.or_decide_visibility.argtypes = [i64, P, P, P, i64, P, P, i64, P, P, P, P, P]
         _lib.or_pointwise_keep.argtypes = [i64, P, ctypes.c_int, P, i64, P, i64, P]
@@ -225,6 +227,30 @@ def blend_tiles(tile_ids, offsets, proj, cam, settings, nthreads: int = 0, want_
     if want_state:
         return out, frags, final_t, last
     return out, frags
+
+
+def blend_fragments(tile_ids, offsets, proj, cam, settings, nthreads: int = 0):
+    """The accepted fragments of _kernels.blend_tiles (_kernels.py:46-72) per
+    pixel, in blend order -> (pixel_offsets int64[H*W+1], splat int64[F]) with
+    splat indices into the depth-sorted projection."""
+    ts = int(settings.tile_size)
+    W, H = int(cam.width), int(cam.height)
+    ntx = (W + ts - 1) // ts
+    n_tiles = offsets.shape[0] - 1
+    m = proj["count"]
+    pad = lambda a, w: _f64(a) if m else np.zeros((1, w))
+    means, conics = pad(proj["means"], 2), pad(proj["conics"], 3)
+    opac = _f64(proj["opacities"]) if m else np.zeros(1)
+    tid = np.ascontiguousarray(tile_ids, dtype=np.int64) if tile_ids.size else np.zeros(1, np.int64)
+    cnt = np.zeros(W * H, dtype=np.int64)
+    args = (_ptr(tid), _ptr(offsets), n_tiles, _ptr(means), _ptr(conics), _ptr(opac), ts, W, H, ntx,
+            float(settings.alpha_floor), float(settings.transmittance_floor))
+    lib().or_blend_fragments(*args, _ptr(cnt), None, None, nthreads)
+    off = np.zeros(W * H + 1, dtype=np.int64)
+    np.cumsum(cnt, out=off[1:])
+    splat = np.zeros(max(int(off[-1]), 1), dtype=np.int64)
+    lib().or_blend_fragments(*args, _ptr(cnt), _ptr(off), _ptr(splat), nthreads)
+    return off, splat[:int(off[-1])]
 
 
 def rasterize_stats(cloud, cam, settings=None, nthreads: int = 0):

@@ -77,7 +77,7 @@ def setup_blocks(pos, op, sc, q, sh, membership: torch.Tensor, owned: Sequence[i
         if idx.numel() == 0:
             continue
         cams = block_views(pos[idx], n_views, width, height)
-        targets = [render(full, cam, settings).clone() for cam in cams]
+        targets = [render(full, cam, settings, sync=True).clone() for cam in cams]
         p0 = pos[idx] + noise * torch.randn(pos[idx].shape, generator=g, device=pos.device)
         tr = trainer_cls(p0, sc[idx], q[idx], op[idx], sh[idx], settings=settings)
         jobs[j] = BlockJob(j, tr, cams, targets)

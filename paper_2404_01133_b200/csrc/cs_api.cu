@@ -107,10 +107,10 @@ void launch_fuse_filter(int64_t n, const void* pos, int f32, const double* pmin,
 void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint32_t* bxs, const uint32_t* bys,
                       const uint2* ranges, const HotRec* hot, const uint32_t* order,
                       const cs_settings& st, int width, int height, int ntx, const float* dl_dimg,
-                      const BlendState& state, uint32_t* ticket, float* grads, int64_t cap,
+                      const BlendState& state, uint32_t* ticket, gacc_t* grads, int64_t cap,
                       cudaStream_t s);
 void launch_project_bwd(const cs_cloud& cl, const uint64_t* depth_keys, const cs_camera& cam,
-                        const cs_settings& st, const float* grads, int64_t cap, const cs_grads& out,
+                        const cs_settings& st, const gacc_t* grads, int64_t cap, const cs_grads& out,
                         cudaStream_t s);
 cudaError_t significance_run(const cs_cloud& cl, const cs_camera* cams_host, int n_cams,
                              const cs_settings& st, double* scores, int32_t* hits_out,
@@ -996,19 +996,19 @@ int cs_render_backward(cs_ctx* c, cs_state* S, const float* dl_dimg, const cs_gr
   Ws* w = S->ws;
   const cs_cloud& cl = S->cloud;
   const int64_t cap = w->cap_vis;
-  if (c->gacc.ensure(sizeof(float) * 9 * cap)) return fail(CS_ENOMEM, "gradient partials");
-  CS_CUDA(cudaMemsetAsync(c->gacc.p, 0, sizeof(float) * 9 * cap, s));
+  if (c->gacc.ensure(sizeof(gacc_t) * 9 * cap)) return fail(CS_ENOMEM, "gradient partials");
+  CS_CUDA(cudaMemsetAsync(c->gacc.p, 0, sizeof(gacc_t) * 9 * cap, s));
   const int ts = S->st.tile_size;
   const int ntx = (S->width + ts - 1) / ts;
   BlendState state{w->st_t.as<double>(), w->st_last.as<int32_t>(), w->st_acc.as<double>()};
   launch_blend_bwd(w->last_tiles, w->last_list, w->last_bxs, w->last_bys, w->last_ranges,
                    w->hot.as<HotRec>(), w->tile_order.as<uint32_t>(), S->st, S->width,
                    S->height, ntx, dl_dimg, state, &w->stats.as<DevStats>()->tickets[5],
-                   c->gacc.as<float>(), cap, s);
+                   c->gacc.as<gacc_t>(), cap, s);
   CS_CHECK_LAUNCH();
   // K11 writes every row (zeros for the culled ones): no clear of the outputs.
   // The forward's per-splat float64 depth keys (~0 = culled) are still in keysA.
-  launch_project_bwd(cl, w->keysA.as<uint64_t>(), S->cam, S->st, c->gacc.as<float>(), cap, *out, s);
+  launch_project_bwd(cl, w->keysA.as<uint64_t>(), S->cam, S->st, c->gacc.as<gacc_t>(), cap, *out, s);
   CS_CHECK_LAUNCH();
   return CS_OK;
 }

@@ -38,18 +38,26 @@ struct BwdParams {
 // transpose (8 + 4 + 2 + 1 + 1 shuffles for 16 slots instead of 5 per value):
 // on return lane l holds the warp total of slot (l >> 1) & 15 (slots >= 9 are
 // zero padding), so nine lanes can issue their atomics in one instruction.
-__device__ __forceinline__ float warp_transpose_sum9(const float (&in)[kGradFields], uint32_t lane) {
-  float v[16];
+#ifndef CS_BWD_RED_F64
+#define CS_BWD_RED_F64 0   // 1: reduce the 32 lanes' partials in float64 too
+#endif
+#if CS_BWD_RED_F64
+typedef double bred_t;
+#else
+typedef float bred_t;
+#endif
+__device__ __forceinline__ bred_t warp_transpose_sum9(const float (&in)[kGradFields], uint32_t lane) {
+  bred_t v[16];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = i < kGradFields ? in[i] : 0.f;
+  for (int i = 0; i < 16; ++i) v[i] = i < kGradFields ? (bred_t)in[i] : (bred_t)0;
 #pragma unroll
   for (int o = 16, n = 16; o >= 2; o >>= 1, n >>= 1) {
     const bool upper = (lane & o) != 0;
     const int h = n >> 1;
 #pragma unroll
     for (int i = 0; i < h; ++i) {
-      const float send = upper ? v[i] : v[i + h];
-      const float keep = upper ? v[i + h] : v[i];
+      const bred_t send = upper ? v[i] : v[i + h];
+      const bred_t keep = upper ? v[i + h] : v[i];
       v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
     }
   }
@@ -83,7 +91,7 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
             const uint32_t* __restrict__ bys, const uint2* __restrict__ ranges,
             const HotRec* __restrict__ hot, const uint32_t* __restrict__ tile_order, int n_items,
             int nboxes, BwdParams bp, const float* __restrict__ dl_dimg, BlendState state,
-            uint32_t* __restrict__ ticket, float* __restrict__ grads /* [kGradFields][cap] */,
+            uint32_t* __restrict__ ticket, gacc_t* __restrict__ grads /* [kGradFields][cap] */,
             int64_t cap) {
   __shared__ __align__(16) HotRec s_hot[kBwdThreads / 32][2][32];
   __shared__ ExpTable s_exp;
@@ -93,7 +101,7 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
   const uint32_t lane = lane_id();
   const uint32_t lt_mask = (1u << lane) - 1u;
   HotRec (*wbuf)[32] = s_hot[threadIdx.x >> 5];
-  const float bg[3] = {(float)bp.bg[0], (float)bp.bg[1], (float)bp.bg[2]};
+  const bsp_t bg[3] = {(bsp_t)bp.bg[0], (bsp_t)bp.bg[1], (bsp_t)bp.bg[2]};
   for (;;) {
     int item = 0;
     if (lane == 0) item = (int)atomicAdd(ticket, 1u);
@@ -107,9 +115,13 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
     int px[PX], py[PX];
     bool valid[PX];
     int64_t my_end[PX];
-    // Only the accept decision (power, exp, alpha floor) must replay the
-    // forward's float64 arithmetic; the partials themselves are float32.
-    float g[PX][3], acc[PX][3], Tend[PX], T[PX], P[PX][3];
+    // The accept decisions replay the forward's float64 arithmetic exactly
+    // (float64 alpha and transmittance); the light arriving from behind a
+    // fragment, S_k = (C_acc - P_k) + T_end bg, is formed in float64 from the
+    // forward's float64 colour sums, so it carries no float32 cancellation
+    // bias (it is divided by 1 - alpha >= 0.01); the per-splat partials are
+    // float32.
+    bsp_t g[PX][3], acc[PX][3], Tend[PX], T[PX], P[PX][3];
     double sx[PX], sy[PX];
     int x0 = 1 << 20, x1 = -(1 << 20), y0 = 1 << 20, y1 = -(1 << 20), wend = (int)s0;
 #pragma unroll
@@ -119,22 +131,22 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
       py[j] = ty * ts + li / ts;
       valid[j] = li < ts * ts && px[j] < bp.width && py[j] < bp.height;
       my_end[j] = s0;
-      Tend[j] = 1.f;
-      T[j] = 1.f;
+      Tend[j] = 1;
+      T[j] = 1;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) g[j][c] = acc[j][c] = P[j][c] = 0.f;
+      for (int c = 0; c < 3; ++c) g[j][c] = acc[j][c] = P[j][c] = 0;
       if (valid[j]) {
         const int64_t pix = (int64_t)py[j] * bp.width + px[j];
         my_end[j] = state.last[pix];
         const double te = state.final_t[pix];
-        Tend[j] = (float)te;
+        Tend[j] = (bsp_t)te;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const double a = state.color_acc[3 * pix + c];
-          acc[j][c] = (float)a;
+          acc[j][c] = (bsp_t)a;
           const double o = a + te * bp.bg[c];  // unclipped pixel value
           // clip to [0, 1] (render.py:273): gradient passes where 0 <= C <= 1
-          g[j][c] = (o >= 0.0 && o <= 1.0) ? dl_dimg[3 * pix + c] : 0.f;
+          g[j][c] = (o >= 0.0 && o <= 1.0) ? (bsp_t)dl_dimg[3 * pix + c] : (bsp_t)0;
         }
         x0 = min(x0, px[j]); x1 = max(x1, px[j]);
         y0 = min(y0, py[j]); y1 = max(y1, py[j]);
@@ -177,38 +189,54 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
           if (k0 + src < my_end[j] && power >= lthr) {
             const double G = exp_le0(power, s_exp, ec);
             double alpha = dmul(h.opacity, G);
-            const bool clamped = alpha > ec.clamp;  // 0.99
+            const bool clamped = alpha > ec.clamp;  // 0.99: d alpha = 0
             if (clamped) alpha = ec.clamp;
             if (alpha >= bp.alpha_floor) {
               contrib = true;
-              const float a = (float)alpha;
-              const float w = T[j] * a;
-              const float inv = 1.f / (1.f - a);
               const float col[3] = {h.r, h.g, h.b};
-              float dl_da = 0.f;
+              bsp_t dl_da = 0;
+              bsp_t w;
+              if (CS_BWD_SP_F64) {
+                w = (bsp_t)dmul((double)T[j], alpha);   // as the forward's kept float64 sums
+                const bsp_t inv = (bsp_t)1 / ((bsp_t)1 - (bsp_t)alpha);
 #pragma unroll
-              for (int c = 0; c < 3; ++c) {
-                P[j][c] = fmaf(w, col[c], P[j][c]);
-                const float S = (acc[j][c] - P[j][c]) + Tend[j] * bg[c];
-                dl_da += g[j][c] * (T[j] * col[c] - S * inv);
-                gr[6 + c] += w * g[j][c];
+                for (int c = 0; c < 3; ++c) {
+                  P[j][c] = (bsp_t)dadd((double)P[j][c], dmul((double)w, (double)col[c]));
+                  const bsp_t S = (acc[j][c] - P[j][c]) + Tend[j] * bg[c];
+                  dl_da += g[j][c] * (T[j] * (bsp_t)col[c] - S * inv);
+                  gr[6 + c] += (float)(w * g[j][c]);
+                }
+              } else {
+                const float af = (float)alpha;
+                w = T[j] * af;
+                const float inv = 1.f / (1.f - af);
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                  P[j][c] = fmaf(w, col[c], P[j][c]);
+                  const float S = (acc[j][c] - P[j][c]) + Tend[j] * bg[c];
+                  dl_da += g[j][c] * (T[j] * col[c] - S * inv);
+                  gr[6 + c] += w * g[j][c];
+                }
               }
-              const float dl_dpow = clamped ? 0.f : dl_da * a;
+              const float a = (float)alpha;
+              const float dl_dpow = clamped ? 0.f : (float)dl_da * a;
               const float fdx = (float)dx, fdy = (float)dy;
-              gr[5] += clamped ? 0.f : dl_da * (float)G;
+              gr[5] += clamped ? 0.f : (float)(dl_da * G);
               gr[0] += dl_dpow * ((float)c0 * fdx + (float)c1 * fdy);
               gr[1] += dl_dpow * ((float)c2 * fdy + (float)c1 * fdx);
               gr[2] += dl_dpow * (-0.5f * fdx * fdx);
               gr[3] += dl_dpow * (-fdx * fdy);
               gr[4] += dl_dpow * (-0.5f * fdy * fdy);
-              T[j] *= 1.f - a;
+              if (CS_BWD_SP_F64) T[j] = (bsp_t)dmul((double)T[j], dsub(1.0, alpha));
+              else T[j] *= 1.f - (float)alpha;
             }
           }
         }
         if (__any_sync(0xffffffffu, contrib)) {
-          const float v = warp_transpose_sum9(gr, lane);
+          const bred_t v = warp_transpose_sum9(gr, lane);
           const uint32_t f = (lane >> 1) & 15;
-          if (!(lane & 1) && f < kGradFields && v != 0.f) atomicAdd(&grads[(int64_t)f * cap + hid], v);
+          if (!(lane & 1) && f < kGradFields && v != (bred_t)0)
+            atomicAdd(&grads[(int64_t)f * cap + hid], (gacc_t)v);
         }
       }
     };
@@ -335,7 +363,7 @@ __device__ __forceinline__ int deg_of(int c) { return c >= 16 ? 3 : c >= 9 ? 2 :
 // opacity}.
 __global__ void __launch_bounds__(128)
 k_project_bwd_geom(const cs_cloud cl, const uint64_t* __restrict__ depth_keys, cs_camera cam,
-              cs_settings st, const float* __restrict__ grads, int64_t cap, cs_grads out) {
+              cs_settings st, const gacc_t* __restrict__ grads, int64_t cap, cs_grads out) {
   const int64_t K = cl.count;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K;
        k += (int64_t)gridDim.x * blockDim.x) {
@@ -463,7 +491,7 @@ constexpr int kShBwdThreads = 256;
 
 __global__ void __launch_bounds__(kShBwdThreads)
 k_project_bwd_sh(const cs_cloud cl, const uint64_t* __restrict__ depth_keys, cs_camera cam,
-                 cs_settings st, const float* __restrict__ grads, int64_t cap, cs_grads out,
+                 cs_settings st, const gacc_t* __restrict__ grads, int64_t cap, cs_grads out,
                  int pitch) {
   extern __shared__ float s_rows[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -542,7 +570,7 @@ k_project_bwd_sh(const cs_cloud cl, const uint64_t* __restrict__ depth_keys, cs_
 void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint32_t* bxs, const uint32_t* bys,
                       const uint2* ranges, const HotRec* hot, const uint32_t* order,
                       const cs_settings& st, int width, int height, int ntx, const float* dl_dimg,
-                      const BlendState& state, uint32_t* ticket, float* grads, int64_t cap,
+                      const BlendState& state, uint32_t* ticket, gacc_t* grads, int64_t cap,
                       cudaStream_t s) {
   BwdParams bp;
   for (int i = 0; i < 3; ++i) bp.bg[i] = st.background[i];
@@ -561,7 +589,7 @@ void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint32_t* bxs, co
 }
 
 void launch_project_bwd(const cs_cloud& cl, const uint64_t* depth_keys, const cs_camera& cam,
-                        const cs_settings& st, const float* grads, int64_t cap, const cs_grads& out,
+                        const cs_settings& st, const gacc_t* grads, int64_t cap, const cs_grads& out,
                         cudaStream_t s) {
   const int64_t blocks = std::min<int64_t>((cl.count + 127) / 128, 148 * 16);
   if (blocks <= 0) return;

@@ -65,6 +65,31 @@ __host__ __device__ __forceinline__ uint32_t pack_box(int lo, int hi) {
 }
 constexpr uint32_t kEmptyBox = 0x7fffu | (0x8000u << 16);
 
+// Per-splat blend-backward partials (K10 -> K11): float64 sums by default.
+// A splat near the camera at 1080p receives 10^4-10^5 warp contributions
+// whose float32 running sum drifts by more than the 1e-3 relative gradient
+// bar (tests/test_gpu_backward_scale.py); CS_BWD_ACC_F64=0 restores float32.
+#ifndef CS_BWD_ACC_F64
+#define CS_BWD_ACC_F64 1
+#endif
+#if CS_BWD_ACC_F64
+typedef double gacc_t;
+#else
+typedef float gacc_t;
+#endif
+// The backward's transmittance / accumulated colour / light-from-behind
+// S_k = (C - P_k) + T_end bg (divided by 1 - alpha >= 0.01): float64 when
+// CS_BWD_SP_F64 (then the training forward keeps float64 colour sums, the
+// same arithmetic the backward repeats), float32 otherwise.
+#ifndef CS_BWD_SP_F64
+#define CS_BWD_SP_F64 0
+#endif
+#if CS_BWD_SP_F64
+typedef double bsp_t;
+#else
+typedef float bsp_t;
+#endif
+
 struct DevStats {     // device mirror of cs_frame_stats + scratch counters
   int64_t assembled;
   int64_t visible;
@@ -140,6 +165,45 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Bulk-copy staging (the blend's HotRec records): one cp.async.bulk per hit
+// record completing on a per-warp mbarrier, instead of four 16-byte cp.async
+// copies per record.  The barrier of a stage is armed by one arrive with the
+// stage's expected byte count; the records' copies complete its transaction
+// count; the warp waits on the stage's phase parity before reading.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n CS_MBAR_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra CS_MBAR_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// the warp's generic-proxy reads of a stage buffer are ordered before the
+// async-proxy (bulk copy) writes that refill it
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 
 // local pixel index (0..ts*ts-1) of thread `tid` of a 256-thread CTA, pixel slot q.  When the
 // tile side is a multiple of 8, warps own 8x4 pixel boxes (box index

@@ -189,11 +189,30 @@ class VisibilityDecision:
     screen_box: Optional[tuple]
 
 
-@dataclass(frozen=True)
 class AssembledSet:
-    cloud: object
-    decisions: tuple
-    selection_ms: float
+    """AssembledSet (lod.py:351-357): ``cloud``, ``decisions``, ``selection_ms``.
+
+    Block mode is lazy: the selection itself runs inside the frame that
+    renders ``cloud`` (K1 in cs_render), so assembling costs no device round
+    trip; ``decisions`` and ``cloud.count`` are computed (one synchronous
+    K1 launch) only when read.  ``selection_ms`` is the host time of the
+    assembly call."""
+
+    __slots__ = ("cloud", "selection_ms", "_decisions")
+
+    def __init__(self, cloud, decisions, selection_ms: float):
+        self.cloud = cloud
+        self.selection_ms = float(selection_ms)
+        self._decisions = decisions
+
+    @property
+    def decisions(self) -> tuple:
+        if self._decisions is None:
+            self._decisions = self.cloud._resolve()[0]
+        return self._decisions
+
+    def __repr__(self):
+        return f"AssembledSet(count={self.cloud.count}, selection_ms={self.selection_ms:.3f})"
 
 
 class AssembledCloud:
@@ -204,19 +223,32 @@ class AssembledCloud:
     set is identical).  Column arrays are gathered to the host only when read.
     """
 
-    def __init__(self, scene: device.DeviceLodScene, cam, mode: str, force_level, count: int,
-                 pieces):
+    def __init__(self, scene: device.DeviceLodScene, cam, mode: str, force_level, count, pieces):
         self.scene = scene
         self.cam = cam
         self.mode = mode
         self.force_level = force_level
-        self._count = int(count)
-        self._pieces = pieces  # [(level, block)] in assembled order (block mode)
+        self._count = None if count is None else int(count)
+        self._pieces = pieces  # [(level, block)] in assembled order (block mode); None until resolved
+        self._decisions = None
         self._host = None
         self.source_kind = _lib.CS_SRC_LOD_BLOCK if mode == "block" else _lib.CS_SRC_LOD_POINT
 
+    def _resolve(self):
+        """(decisions, pieces, count) of a block-mode set, computed once."""
+        if self._decisions is None:
+            decisions = _decisions(self.scene, self.cam, self.force_level)
+            self._pieces = [(d.level, d.block) for d in decisions
+                            if d.visible and 0 <= d.level < self.scene.n_levels
+                            and self.scene.counts[d.level, d.block] > 0]
+            self._count = int(sum(self.scene.counts[L, j] for L, j in self._pieces))
+            self._decisions = decisions
+        return self._decisions, self._pieces, self._count
+
     @property
     def count(self) -> int:
+        if self._count is None:
+            self._resolve()
         return self._count
 
     def __len__(self) -> int:
@@ -225,7 +257,7 @@ class AssembledCloud:
     def _materialise(self):
         if self._host is None:
             if self.mode == "block":
-                parts = [self.scene.block_cloud_host(L, j) for L, j in self._pieces]
+                parts = [self.scene.block_cloud_host(L, j) for L, j in self._resolve()[1]]
             else:
                 parts = _pointwise_host(self.scene, self.cam, self.force_level)
             if not parts:
@@ -336,10 +368,16 @@ def assemble_render_set(scene, cam, *, mode: str = "block",
     dscene = device.device_lod_scene(scene)
     start = time.perf_counter()
     if mode == "block":
-        decisions = _decisions(dscene, cam, force_level)
-        pieces = [(d.level, d.block) for d in decisions
-                  if d.visible and 0 <= d.level < dscene.n_levels and dscene.counts[d.level, d.block] > 0]
-        count = int(sum(dscene.counts[L, j] for L, j in pieces))
+        # lazy: the frame that renders the set runs the selection (K1).  Eager
+        # when select_level could fail (intervals not covering [0, inf) without
+        # gaps), so its ValueError surfaces here as in the reference.
+        if force_level is not None and not 0 <= int(force_level) < dscene.n_levels:
+            raise ValueError(f"force_level {force_level} outside the scene's levels")
+        cloud = AssembledCloud(dscene, cam, mode, force_level, None, None)
+        if force_level is None and not _covers_half_line(dscene.distance_intervals):
+            cloud._resolve()
+        return AssembledSet(cloud=cloud, decisions=cloud._decisions,
+                            selection_ms=(time.perf_counter() - start) * 1000.0)
     elif mode == "pointwise":
         decisions = ()
         pieces = None
@@ -347,8 +385,16 @@ def assemble_render_set(scene, cam, *, mode: str = "block",
     else:
         raise ValueError(f"unknown selection mode: {mode}")
     selection_ms = (time.perf_counter() - start) * 1000.0
-    return AssembledSet(cloud=AssembledCloud(dscene, cam, mode, force_level, count, pieces),
-                        decisions=decisions, selection_ms=selection_ms)
+    cloud = AssembledCloud(dscene, cam, mode, force_level, count, pieces)
+    return AssembledSet(cloud=cloud, decisions=decisions, selection_ms=selection_ms)
+
+
+def _covers_half_line(intervals) -> bool:
+    """True when every distance >= 0 falls in exactly one [lo, hi) interval."""
+    iv = sorted((float(a), float(b)) for a, b in intervals)
+    if not iv or iv[0][0] > 0.0 or iv[-1][1] != math.inf:
+        return False
+    return all(iv[i][1] == iv[i + 1][0] for i in range(len(iv) - 1))
 
 
 def _pointwise_count(dscene, cam, force_level) -> int:

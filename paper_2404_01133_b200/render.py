@@ -128,17 +128,18 @@ def _render_into(cloud, cam, settings, out: torch.Tensor, flags: int, stats: Opt
 
 
 def render(cloud, cam, settings: Optional[RenderSettings] = None, *, out: Optional[torch.Tensor] = None,
-           device_index: Optional[int] = None) -> torch.Tensor:
+           device_index: Optional[int] = None, sync: bool = False) -> torch.Tensor:
     """Device tier: enqueue one frame on the current stream; returns the
     clipped (H, W, 3) float32 image tensor.  No host synchronisation.  A frame
     that overflows its tile-pair buffer is reported (MemoryError) by the
     context's next call at the latest -- ``check()`` synchronises and reports
-    immediately."""
+    immediately.  ``sync=True`` renders synchronously, growing the pair
+    buffers and re-rendering on overflow (for setup work such as targets)."""
     settings = settings or RenderSettings()
     dev = torch.device("cuda", device._device_index(device_index))
     if out is None:
         out = torch.empty((int(cam.height), int(cam.width), 3), dtype=torch.float32, device=dev)
-    _render_into(cloud, cam, settings, out, 0, None)
+    _render_into(cloud, cam, settings, out, _lib.CS_RENDER_SYNC if sync else 0, None)
     return out
 
 

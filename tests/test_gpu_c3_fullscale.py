@@ -15,8 +15,9 @@ the C oracle on identical inputs (the level clouds copied to the host):
 * one frame with every visible block forced to the finest level
   (cmd_bench's ``finest`` mode, cli.py:250-258);
 * one no-LoD frame of the whole 23M cloud (cmd_bench's ``full`` mode, the
-  paper's ablation PAPER.md:276-280) from the 150 m orbit: > 10^8 tile pairs,
-  which exercises the heavy-chunk emission and the large pair buffers.
+  paper's ablation PAPER.md:276-280) from a low orbit inside the city: > 10^8
+  tile pairs, which exercises the heavy-chunk emission and the large pair
+  buffers.
 
 Bar (north star): visible set, LoD levels and sorted tile keys bit-exact;
 images within max-abs 1e-4; fragment counts equal.
@@ -104,14 +105,32 @@ def test_c3_finest_mode_frame(c3):
 
 
 def test_c3_full_cloud_frame_over_1e8_pairs(c3):
-    """No LoD: the whole 23M-Gaussian cloud from the 150 m orbit."""
+    """No LoD: the whole 23M-Gaussian cloud from a low orbit inside the city
+    (the flythrough's 150 m frames give ~3e7 pairs without LoD; lower, nearer
+    views reach the 1e8-2e8 pairs of SURVEY.md Appendix C).  The view with the
+    most pairs among a few low-altitude candidates is checked."""
     from types import SimpleNamespace
+    import paper_2404_01133_b200 as cs
     from paper_2404_01133_b200 import device
+    from paper_2404_01133_b200.synth import orbit_cameras
     scene, hs, cams, raw = c3
     pos, op, sc, q, sh, _, _ = raw
     full = device.DeviceCloud.from_torch(pos, op, sc, q, sh)
+    lo = pos.double().min(dim=0).values.cpu().numpy()
+    hi = pos.double().max(dim=0).values.cpu().numpy()
+    center = 0.5 * (lo + hi)
+    cands = []
+    for alt, rad in ((60.0, 150.0), (40.0, 250.0), (30.0, 100.0), (80.0, 300.0)):
+        cands += orbit_cameras(center, rad, alt, 3, 1920, 1080)
+    pairs = []
+    for cam in cands:
+        _, st = cs.rasterize_stats(full, cam)
+        from paper_2404_01133_b200.render import bin_tiles_last
+        pairs.append(int(bin_tiles_last(cam, 16)[0].shape[0]))
+    best = int(np.argmax(pairs))
+    print("candidate pairs (M):", [round(p / 1e6, 1) for p in pairs])
     host = SimpleNamespace(positions=pos.cpu().numpy(), opacities=op.cpu().numpy(),
                            scales=sc.cpu().numpy(), rotations=q.cpu().numpy(), sh=sh.cpu().numpy(),
                            count=int(pos.shape[0]))
-    r = _check_frame(full, host, cams[0], min_pairs=100_000_000)
+    r = _check_frame(full, host, cands[best], min_pairs=100_000_000)
     print("full-cloud frame:", r)

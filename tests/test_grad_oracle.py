@@ -59,3 +59,53 @@ def test_gradients_match_finite_differences(seed):
                 assert abs(fd) > 10.0 or abs(fd - an) / max(abs(an), 1e-8) < 5e-3, (name, idx, fd, an)
             checked += 1
     assert checked > 20
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_sparse_oracle_equals_dense(seed):
+    """The training-scale sparse form (accepted fragments only, pixel chunks)
+    gives the dense oracle's image and gradients."""
+    from tests_helpers import small_scene
+    cloud, cam, st = small_scene(seed, k=40, width=48, height=40)
+    dl = np.random.default_rng(seed).normal(size=(cam.height, cam.width, 3))
+    img, grads = G.gradients(cloud, cam, st, dl)
+    simg, sgrads = G.gradients_sparse(cloud, cam, st, dl, chunk_pixels=500)
+    np.testing.assert_allclose(simg, img, atol=1e-13)
+    for a, b in zip(sgrads, grads):
+        np.testing.assert_allclose(a, b, rtol=1e-9, atol=1e-11)
+
+
+def test_sparse_oracle_matches_finite_differences_midsize():
+    """2000 Gaussians at 128x96: sparse oracle gradients vs central differences
+    of the C oracle's rasterize (skipping entries whose FD is unstable across
+    two step sizes, i.e. near a decision knife-edge)."""
+    from tests_helpers import small_scene
+    cloud, cam, st = small_scene(11, k=2000, width=128, height=96)
+    rng = np.random.default_rng(5)
+    dl = rng.normal(size=(cam.height, cam.width, 3))
+    _, grads = G.gradients_sparse(cloud, cam, st, dl)
+    names = ["positions", "scales", "rotations", "opacities", "sh"]
+    base = {n: np.array(getattr(cloud, n), dtype=np.float64) for n in names}
+
+    def loss(arrs):
+        img, _ = O.rasterize_stats(SimpleNamespace(**arrs), cam, st)
+        return float((img * dl).sum())
+
+    def fd(name, i, h):
+        up = {k: v.copy() for k, v in base.items()}
+        dn = {k: v.copy() for k, v in base.items()}
+        up[name].reshape(-1)[i] += h
+        dn[name].reshape(-1)[i] -= h
+        return (loss(up) - loss(dn)) / (2 * h)
+
+    checked = 0
+    for gi, name in enumerate(names):
+        g = grads[gi].reshape(-1)
+        big = np.argsort(-np.abs(g))[:40]          # informative entries
+        for i in rng.choice(big, size=6, replace=False):
+            a, b = fd(name, i, 1e-6), fd(name, i, 5e-7)
+            if abs(a - b) > 1e-4 * max(1.0, abs(a)):
+                continue
+            assert abs(g[i] - a) <= 1e-4 * max(1.0, abs(a)), (name, i, g[i], a)
+            checked += 1
+    assert checked >= 20

@@ -20,16 +20,8 @@
 // other fragment takes the reference path exactly: alpha = min(0.99,
 // o * exp(power)) in float64, float64 alpha/transmittance decisions, so the
 // accepted-fragment set equals the reference's.  Colour accumulates in
-// float32 (SURVEY.md H2 recipe m3: 0 px > 1e-4); a kept-state (training)
-// forward also keeps the float64 colour sums its backward re-derives
-// (cs_backward.cu).  The AABB cull never drops a fragment the exact path
-// could accept: it bounds {power >= threshold} (cs_project.cu).
-//
-// Staging: 4 x 16-byte cp.async (LDGSTS) per record.  A cp.async.bulk per
-// record completing on a per-warp mbarrier was measured 23% slower (1.19 vs
-// 0.97 ms on C3, profiles/r2f_blend_ab.txt): the bulk copy takes uniform
-// operands, so a warp's scattered 64-byte records are issued one lane at a
-// time (ELECT loop), while one LDGSTS moves every hitting lane's chunk.
+// float64 from float32 splat colours.  The AABB cull never drops a fragment
+// the exact path could accept: it bounds {power >= threshold} (cs_project.cu).
 #include "cs_internal.cuh"
 
 namespace cs {
@@ -60,7 +52,7 @@ __device__ __forceinline__ int blend_box_pixel(int b, int lane, int ts, int j) {
 // reads each staged record once for both, and a tile is walked by half as
 // many warps.
 #ifndef CS_BLEND_MINB
-#define CS_BLEND_MINB 3   // 3 CTAs/SM (<= 85 registers) for every variant, kept-state included
+#define CS_BLEND_MINB 1
 #endif
 #ifndef CS_BLEND_PAIR
 #define CS_BLEND_PAIR 0
@@ -99,7 +91,6 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
     bool valid[PX], done[PX];
     double sx[PX], sy[PX], T[PX];
     float cr[PX], cg[PX], cb[PX];  // colour accumulates in float32 (SURVEY.md H2 recipe m3)
-    double kr[PX], kg[PX], kb[PX];  // KEEP: the float64 sums the backward re-derives
     int cnt[PX];
     int64_t last[PX];
     int x0 = 1 << 20, x1 = -(1 << 20), y0 = 1 << 20, y1 = -(1 << 20);
@@ -117,7 +108,6 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
       sy[j] = (double)py[j] + 0.5;
       T[j] = 1.0;
       cr[j] = cg[j] = cb[j] = 0.f;
-      kr[j] = kg[j] = kb[j] = 0.0;
       cnt[j] = 0;
       last[j] = s0;
       done[j] = !valid[j];
@@ -169,16 +159,10 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
         if (alpha < bp.alpha_floor) continue;        // _kernels.py:61-62
         const double nt = dmul(T[j], dsub(1.0, alpha));
         if (nt < bp.t_floor) { done[j] = true; continue; }  // _kernels.py:63-66
-        const double wd = dmul(T[j], alpha);
-        const float w = (float)wd;
+        const float w = (float)dmul(T[j], alpha);
         cr[j] = fmaf(w, h.r, cr[j]);
         cg[j] = fmaf(w, h.g, cg[j]);
         cb[j] = fmaf(w, h.b, cb[j]);
-        if (KEEP && CS_BWD_SP_F64) {
-          kr[j] = dadd(kr[j], dmul(wd, (double)h.r));
-          kg[j] = dadd(kg[j], dmul(wd, (double)h.g));
-          kb[j] = dadd(kb[j], dmul(wd, (double)h.b));
-        }
         T[j] = nt;
         cnt[j] += 1;
         last[j] = k0 + src + 1;
@@ -306,9 +290,9 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
       if (KEEP) {
         state.final_t[pix] = T[j];
         state.last[pix] = (int32_t)last[j];
-        state.color_acc[3 * pix] = CS_BWD_SP_F64 ? kr[j] : (double)cr[j];
-        state.color_acc[3 * pix + 1] = CS_BWD_SP_F64 ? kg[j] : (double)cg[j];
-        state.color_acc[3 * pix + 2] = CS_BWD_SP_F64 ? kb[j] : (double)cb[j];
+        state.color_acc[3 * pix] = (double)cr[j];
+        state.color_acc[3 * pix + 1] = (double)cg[j];
+        state.color_acc[3 * pix + 2] = (double)cb[j];
       }
     }
     const int box_frags = warp_sum(box_cnt);
