@@ -39,7 +39,7 @@ struct BwdParams {
 // on return lane l holds the warp total of slot (l >> 1) & 15 (slots >= 9 are
 // zero padding), so nine lanes can issue their atomics in one instruction.
 #ifndef CS_BWD_RED_F64
-#define CS_BWD_RED_F64 0   // 1: reduce the 32 lanes' partials in float64 too
+#define CS_BWD_RED_F64 1   // reduce the 32 lanes' partials in float64 (cs_internal.cuh)
 #endif
 #if CS_BWD_RED_F64
 typedef double bred_t;
@@ -198,7 +198,9 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
               bsp_t w;
               if (CS_BWD_SP_F64) {
                 w = (bsp_t)dmul((double)T[j], alpha);   // as the forward's kept float64 sums
-                const bsp_t inv = (bsp_t)1 / ((bsp_t)1 - (bsp_t)alpha);
+                const double om = dsub(1.0, alpha);        // >= 0.01
+                double inv = (double)__frcp_rn((float)om);   // + one Newton step: ~1e-14
+                inv = fma(inv, fma(-om, inv, 1.0), inv);
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                   P[j][c] = (bsp_t)dadd((double)P[j][c], dmul((double)w, (double)col[c]));

@@ -231,7 +231,7 @@ k_emit_heavy(const uint32_t* __restrict__ order, const uint2* __restrict__ rects
              DevStats* __restrict__ stats, const uint4* __restrict__ heavy, int ntx,
              uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, DigitHist dh) {
   __shared__ BinSmem sm;
-  __shared__ uint32_t s_t;
+  __shared__ uint32_t s_t[2];  // double-buffered ticket: thread 0 writes the next while others read this one
   const unsigned long long hc = *reinterpret_cast<const unsigned long long*>(&stats->tickets[8]);
   const uint32_t n_entries = (uint32_t)(hc >> 32), n_slices = (uint32_t)hc;
   if (n_slices == 0) return;
@@ -239,10 +239,10 @@ k_emit_heavy(const uint32_t* __restrict__ order, const uint2* __restrict__ rects
   for (int i = threadIdx.x; i < dh.n_passes * 256; i += kBinThreads) sm.hist[i >> 8][i & 255] = 0;
   int64_t cur = -1;
   int nr = 0;
-  while (true) {
-    if (threadIdx.x == 0) s_t = atomicAdd(&stats->tickets[10], 1u);
+  for (uint32_t it = 0;; ++it) {
+    if (threadIdx.x == 0) s_t[it & 1] = atomicAdd(&stats->tickets[10], 1u);
     __syncthreads();
-    const uint32_t t = s_t;
+    const uint32_t t = s_t[it & 1];
     if (t >= n_slices) break;
     int lo = 0, hi = (int)n_entries - 1;  // last entry whose first slice <= t
     while (lo < hi) {

@@ -65,10 +65,17 @@ __host__ __device__ __forceinline__ uint32_t pack_box(int lo, int hi) {
 }
 constexpr uint32_t kEmptyBox = 0x7fffu | (0x8000u << 16);
 
-// Per-splat blend-backward partials (K10 -> K11): float64 sums by default.
-// A splat near the camera at 1080p receives 10^4-10^5 warp contributions
-// whose float32 running sum drifts by more than the 1e-3 relative gradient
-// bar (tests/test_gpu_backward_scale.py); CS_BWD_ACC_F64=0 restores float32.
+// Backward precision (tests/test_gpu_backward_scale.py, 1080p, N(0,1) dL/dimage,
+// bar max(1e-4, 1e-3 |g|) per element).  A splat near the camera collects
+// 10^4-10^5 per-pixel terms whose sum is a random walk; a per-pixel term can be
+// ~100x its neighbours' (dL/dalpha carries S/(1 - alpha), alpha up to 0.99),
+// so small final gradients of large splats need every accumulation stage in
+// float64: the per-splat partials (CS_BWD_ACC_F64: the K10 -> K11 buffer and
+// its atomics), the warp reduction of the lanes' partials (CS_BWD_RED_F64,
+// cs_backward.cu) and the transmittance / colour sums / light from behind
+// (CS_BWD_SP_F64).  Measured with any of the three in float32: 12-14 of 60k
+// position gradients outside the bar; with all three in float64: none
+// (profiles/r2_backward_precision.txt).
 #ifndef CS_BWD_ACC_F64
 #define CS_BWD_ACC_F64 1
 #endif
@@ -82,7 +89,7 @@ typedef float gacc_t;
 // CS_BWD_SP_F64 (then the training forward keeps float64 colour sums, the
 // same arithmetic the backward repeats), float32 otherwise.
 #ifndef CS_BWD_SP_F64
-#define CS_BWD_SP_F64 0
+#define CS_BWD_SP_F64 1
 #endif
 #if CS_BWD_SP_F64
 typedef double bsp_t;
