@@ -68,6 +68,7 @@ void launch_activate_geom(int64_t K, const float* geom, float4* pos_op, float4* 
 int64_t bin_chunks(int64_t capacity);
 const void* lod_select_kernel();
 const void* project_kernel();
+const void* project_staged_kernel();
 int64_t bin_status_words(int64_t capacity);
 void launch_bin_pairs(const uint32_t* order, const uint2* rects, DevStats* stats, int64_t pair_cap,
                       int64_t capacity, uint64_t* status, int ntx, uint32_t* keys, uint32_t* vals,
@@ -801,6 +802,7 @@ static int capture_graph(cs_ctx* c, Ws* w, const cs_source* src, const cs_camera
   if (cudaGraphGetNodes(g, nodes.data(), &n) != cudaSuccess) return give_up(g);
   const void* f_sel = lod_select_kernel();
   const void* f_proj = project_kernel();
+  const void* f_proj2 = project_staged_kernel();
   for (cudaGraphNode_t nd : nodes) {
     cudaGraphNodeType t;
     if (cudaGraphNodeGetType(nd, &t) != cudaSuccess) return give_up(g);
@@ -811,7 +813,7 @@ static int capture_graph(cs_ctx* c, Ws* w, const cs_source* src, const cs_camera
     // k_project(clouds, segs, stats, cam, ...)) and the argument count
     int cam_arg = -1, n_args = 0;
     if (p.func == f_sel) { cam_arg = 1; n_args = 6; }
-    if (p.func == f_proj) { cam_arg = 3; n_args = 7; }
+    if (p.func == f_proj || p.func == f_proj2) { cam_arg = 3; n_args = 7; }
     if (cam_arg < 0) continue;
     cs_ctx::CamNode cn;
     cn.node = nd;

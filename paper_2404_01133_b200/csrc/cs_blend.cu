@@ -30,6 +30,15 @@
 // 0.97 ms on C3, profiles/r2f_blend_ab.txt): the bulk copy takes uniform
 // operands, so a warp's scattered 64-byte records are issued one lane at a
 // time (ELECT loop), while one LDGSTS moves every hitting lane's chunk.
+//
+// Accept-phase batching was measured too and not kept: staging up to 32 hits
+// per warp, evaluating every quadratic form first and then letting each lane
+// walk its own accepted candidates (so a warp iteration serves one fragment of
+// every lane) was 29% slower (1.32 vs 0.97 ms; 16-hit batches 1.25 ms,
+// profiles/r2k_blend_ab.txt): the quadratic forms of hits staged after a box
+// has terminated are wasted, the per-(hit, lane) power array costs shared
+// memory and occupancy, and with ~3 hits per round the per-hit accept path it
+// replaces is already short.
 #include "cs_internal.cuh"
 
 namespace cs {
@@ -330,257 +339,6 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
   }
 }
 
-// ---------------------------------------------------------------------------
-// K9 v2 (CS_BLEND_V2): batched accept.  In the kernel above every hit whose
-// quadratic form passes for ANY lane runs the whole accept path (float64 exp,
-// alpha / transmittance decisions, colour) as one warp instruction stream --
-// on C3 ~6 of 32 lanes take part on average.  Here a warp stages the hits of
-// several rounds (up to kBatch) first, then
-//   phase 1: every lane evaluates the exact float64 quadratic form of every
-//            staged hit for its pixel (warp-uniform loop over the hits,
-//            broadcast shared-memory reads), keeps power in a per-warp
-//            [hit][lane] array and sets a candidate bit where power >= the
-//            fast-reject threshold;
-//   phase 2: each lane walks ITS OWN candidates in list order (exact alpha,
-//            the reference's skip / stop decisions, colour), so a warp
-//            iteration serves one candidate of every lane that still has one
-//            -- the loop runs max-over-lanes times instead of once per hit.
-// Decisions and their order per pixel are exactly those of the kernel above.
-#ifndef CS_BLEND_V2
-#define CS_BLEND_V2 0
-#endif
-#ifndef CS_BLEND2_THREADS
-#define CS_BLEND2_THREADS 128
-#endif
-#ifndef CS_BLEND2_MINB
-#define CS_BLEND2_MINB 5
-#endif
-constexpr int kB2Threads = CS_BLEND2_THREADS;
-constexpr int kB2Warps = kB2Threads / 32;
-#ifndef CS_BLEND2_BATCH
-#define CS_BLEND2_BATCH 32
-#endif
-constexpr int kBatch = CS_BLEND2_BATCH;  // staged hits per batch (<= 32: candidate bits of one mask)
-
-template <typename OutT, bool KEEP, bool DIAG>
-__global__ void __launch_bounds__(kB2Threads, CS_BLEND2_MINB)
-k_blend2(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
-         const uint32_t* __restrict__ bys, const uint2* __restrict__ ranges,
-         const HotRec* __restrict__ hot, const uint32_t* __restrict__ tile_order, int n_items,
-         int nboxes, BlendParams bp, OutT* __restrict__ out, int32_t* __restrict__ frag_tile,
-         DevStats* __restrict__ stats, BlendState state) {
-  __shared__ __align__(16) HotRec s_rec[kB2Warps][kBatch];
-  __shared__ double s_pw[kB2Warps][kBatch][32];     // power of (hit, lane)
-  __shared__ __align__(16) float4 s_col[kB2Warps][kBatch];  // r, g, b of each staged hit
-  __shared__ double s_op[kB2Warps][kBatch];
-  __shared__ int32_t s_pos[kB2Warps][kBatch];        // list position of each staged hit
-  __shared__ ExpTable s_exp;
-  const ExpCoef ec = load_exp_table(&s_exp);
-  __syncthreads();
-  const int ts = bp.tile_size;
-  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  const uint32_t lt_mask = (1u << lane) - 1u;
-  HotRec* rec = s_rec[warp];
-  double (*pw)[32] = s_pw[warp];
-  long long frags = 0, whits = 0;
-  uint32_t evals = 0, whits_empty = 0;
-  for (;;) {
-    int item = 0;
-    if (lane == 0) item = (int)atomicAdd(&stats->tickets[4], 1u);
-    item = __shfl_sync(0xffffffffu, item, 0);
-    if (item >= n_items) break;
-    const long long item_t0 = DIAG ? clock64() : 0;
-    const int tr = item / nboxes, b = item - tr * nboxes;
-    const int t = tile_order ? (int)tile_order[tr] : tr;
-    const int tx = t % bp.ntx, ty = t / bp.ntx;
-    const uint2 rg = ranges[t];
-    const int64_t s0 = rg.x, s1 = rg.y;
-    const int li = box_pixel(b, lane, ts);
-    const int px = tx * ts + li % ts, py = ty * ts + li / ts;
-    const bool valid = li < ts * ts && px < bp.width && py < bp.height;
-    const double sx = (double)px + 0.5, sy = (double)py + 0.5;  // _kernels.py:43-45
-    double T = 1.0;
-    float cr = 0.f, cg = 0.f, cb = 0.f;
-    double kr = 0.0, kg = 0.0, kb = 0.0;
-    int cnt = 0;
-    int64_t last = s0;
-    bool done = !valid;
-    int x0, x1, y0, y1;
-    auto live_box = [&]() {
-      x0 = done ? (1 << 20) : px; x1 = done ? -(1 << 20) : px;
-      y0 = done ? (1 << 20) : py; y1 = done ? -(1 << 20) : py;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        x0 = min(x0, __shfl_xor_sync(0xffffffffu, x0, o));
-        x1 = max(x1, __shfl_xor_sync(0xffffffffu, x1, o));
-        y0 = min(y0, __shfl_xor_sync(0xffffffffu, y0, o));
-        y1 = max(y1, __shfl_xor_sync(0xffffffffu, y1, o));
-      }
-    };
-    live_box();
-    if (x0 > x1) continue;  // no pixel of this box in the image (warp-uniform)
-
-    // evaluate the nh staged hits of the batch (both phases); false when the
-    // whole box has terminated
-    auto run_batch = [&](int nh) -> bool {
-      cp_async_wait<0>();
-      __syncwarp();
-      if ((int)lane < nh) {  // colour / opacity of hit `lane` as columns (conflict-free phase-2 reads)
-        const HotRec& h = rec[lane];
-        s_col[warp][lane] = make_float4(h.r, h.g, h.b, 0.f);
-        s_op[warp][lane] = h.opacity;
-      }
-      whits += nh;
-      // phase 1: exact quadratic form of every hit for this lane's pixel
-      uint32_t cand = 0;
-      for (int k = 0; k < nh; ++k) {
-        const HotRec& h = rec[k];
-        const double dx = dsub(sx, h.mx), dy = dsub(sy, h.my);
-        // -0.5 * (c0*dx*dx + c2*dy*dy) - c1*dx*dy   (_kernels.py:54-57)
-        const double power = dsub(dmul(-0.5, dadd(dmul(dmul(h.c0, dx), dx), dmul(dmul(h.c2, dy), dy))),
-                                  dmul(dmul(h.c1, dx), dy));
-        const bool pass = !done && power >= (double)h.lthr;  // else alpha < alpha_floor guaranteed
-        pw[k][lane] = power;
-        cand |= (pass ? 1u : 0u) << k;
-        if (DIAG) {
-          evals += done ? 0u : 1u;
-          if (!__any_sync(0xffffffffu, pass)) ++whits_empty;
-        }
-      }
-      __syncwarp();
-      // phase 2: each lane's own candidates, in list order (_kernels.py:58-72)
-      while (__any_sync(0xffffffffu, cand != 0)) {
-        if (cand) {
-          const int k = __ffs(cand) - 1;
-          cand &= cand - 1;
-          const double power = pw[k][lane];
-          double alpha = dmul(s_op[warp][k], exp_le0(power, s_exp, ec));  // _kernels.py:58
-          if (alpha > ec.clamp) alpha = ec.clamp;                         // 0.99, _kernels.py:59-60
-          if (alpha >= bp.alpha_floor) {                                  // _kernels.py:61-62
-            const double nt = dmul(T, dsub(1.0, alpha));
-            if (nt < bp.t_floor) {  // _kernels.py:63-66: drop the crossing fragment, stop
-              done = true;
-              cand = 0;
-            } else {
-              const float4 col = s_col[warp][k];
-              const double wd = dmul(T, alpha);
-              const float w = (float)wd;
-              cr = fmaf(w, col.x, cr);
-              cg = fmaf(w, col.y, cg);
-              cb = fmaf(w, col.z, cb);
-              if (KEEP && CS_BWD_SP_F64) {
-                kr = dadd(kr, dmul(wd, (double)col.x));
-                kg = dadd(kg, dmul(wd, (double)col.y));
-                kb = dadd(kb, dmul(wd, (double)col.z));
-              }
-              T = nt;
-              cnt += 1;
-              last = (int64_t)s_pos[warp][k] + 1;
-            }
-          }
-        }
-      }
-      __syncwarp();
-      return __any_sync(0xffffffffu, !done);
-    };
-
-    uint32_t nid = 0, nbx = kEmptyBox, nby = kEmptyBox;
-    if (s0 + lane < s1) {
-      nid = __ldg(list + s0 + lane);
-      nbx = __ldg(bxs + s0 + lane);
-      nby = __ldg(bys + s0 + lane);
-    }
-    int nh = 0;  // hits staged in the current batch
-    bool alive = true;
-    for (int64_t k0 = s0; k0 < s1; k0 += 32) {
-      const uint32_t id = nid, bx = nbx, by = nby;
-      if (k0 + 32 + lane < s1) {
-        nid = __ldg(list + k0 + 32 + lane);
-        nbx = __ldg(bxs + k0 + 32 + lane);
-        nby = __ldg(bys + k0 + 32 + lane);
-      } else {
-        nbx = nby = kEmptyBox;
-      }
-      const int bx0 = (int)(int16_t)(bx & 0xffffu), bx1 = (int)(int16_t)(bx >> 16);
-      const int by0 = (int)(int16_t)(by & 0xffffu), by1 = (int)(int16_t)(by >> 16);
-      const bool hit = !(bx0 > x1 || bx1 < x0 || by0 > y1 || by1 < y0);
-      const uint32_t mask = __ballot_sync(0xffffffffu, hit);
-      if (!mask) continue;
-      // stage this round's hits; when the batch fills, evaluate it first (and
-      // re-test the round's remaining hits against the shrunk cull box)
-      uint32_t rem = mask;
-      while (rem) {
-        if (nh == kBatch) {
-          alive = run_batch(nh);
-          nh = 0;
-          if (!alive) break;
-          live_box();  // shrink the cull box to the still-live pixels
-          rem &= __ballot_sync(0xffffffffu, !(bx0 > x1 || bx1 < x0 || by0 > y1 || by1 < y0));
-          continue;
-        }
-        uint32_t take = rem;
-        if (__popc(rem) > kBatch - nh) {  // the lowest (kBatch - nh) hits
-          take = 0;
-          uint32_t r = rem;
-          for (int i = nh; i < kBatch; ++i) {
-            take |= r & (0u - r);
-            r &= r - 1;
-          }
-        }
-        if (take & (1u << lane)) {
-          const int slot = nh + __popc(take & lt_mask);
-          const char* g = reinterpret_cast<const char*>(hot + id);
-          char* d = reinterpret_cast<char*>(&rec[slot]);
-#pragma unroll
-          for (int c = 0; c < kHotChunks; ++c) cp_async16(d + 16 * c, g + 16 * c);
-          s_pos[warp][slot] = (int32_t)(k0 + lane);
-        }
-        cp_async_commit();
-        nh += __popc(take);
-        rem &= ~take;
-      }
-      if (!alive) break;
-    }
-    if (alive && nh) run_batch(nh);
-    cp_async_wait<0>();
-    __syncwarp();
-    if (valid) {
-      const int64_t pix = (int64_t)py * bp.width + px;
-      double o[3] = {(double)cr + T * bp.bg[0], (double)cg + T * bp.bg[1], (double)cb + T * bp.bg[2]};
-      if (!(bp.flags & CS_RENDER_NO_CLIP)) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) o[c] = o[c] < 0.0 ? 0.0 : (o[c] > 1.0 ? 1.0 : o[c]);
-      }
-      out[3 * pix] = (OutT)o[0];
-      out[3 * pix + 1] = (OutT)o[1];
-      out[3 * pix + 2] = (OutT)o[2];
-      if (KEEP) {
-        state.final_t[pix] = T;
-        state.last[pix] = (int32_t)last;
-        state.color_acc[3 * pix] = CS_BWD_SP_F64 ? kr : (double)cr;
-        state.color_acc[3 * pix + 1] = CS_BWD_SP_F64 ? kg : (double)cg;
-        state.color_acc[3 * pix + 2] = CS_BWD_SP_F64 ? kb : (double)cb;
-      }
-    }
-    const int box_frags = warp_sum(cnt);
-    frags += box_frags;
-    if (lane == 0 && box_frags) atomicAdd(frag_tile + t, box_frags);
-    if (DIAG && lane == 0) {
-      const unsigned long long dt = (unsigned long long)(clock64() - item_t0);
-      atomicMax(reinterpret_cast<unsigned long long*>(&stats->blend_max_item_cycles), dt);
-      atomicAdd(reinterpret_cast<unsigned long long*>(&stats->blend_item_cycles), dt);
-    }
-  }
-  const long long wevals = DIAG ? warp_sum((long long)evals) : 0;
-  if (lane == 0) {
-    if (whits) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->warp_hits), (unsigned long long)whits);
-    if (DIAG && whits_empty)
-      atomicAdd(reinterpret_cast<unsigned long long*>(&stats->warp_hits_empty), (unsigned long long)whits_empty);
-    if (frags) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->fragments), (unsigned long long)frags);
-    if (wevals) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->evals), (unsigned long long)wevals);
-  }
-}
-
 #ifndef CS_BLEND_PX
 #define CS_BLEND_PX 1
 #endif
@@ -591,15 +349,6 @@ static void launch_blend_d(int n_tiles, const uint32_t* list, const uint32_t* bx
                            const uint32_t* order, const BlendParams& bp, OutT* out,
                            int32_t* frag_tile, DevStats* stats, BlendState st, cudaStream_t s) {
   constexpr int PX = CS_BLEND_PX;
-  if (CS_BLEND_V2) {
-    static int grid2 = 0;
-    if (grid2 == 0) grid2 = persistent_grid(k_blend2<OutT, KEEP, DIAG>, kB2Threads);
-    k_blend2<OutT, KEEP, DIAG><<<grid2, kB2Threads, 0, s>>>(list, bxs, bys, ranges, hot, order,
-                                                            n_tiles * boxes_per_tile(bp.tile_size),
-                                                            boxes_per_tile(bp.tile_size), bp, out,
-                                                            frag_tile, stats, st);
-    return;
-  }
   static int grid = 0;  // persistent: one wave of resident CTAs
   if (grid == 0) grid = persistent_grid(k_blend<OutT, KEEP, DIAG, PX>, kBlendThreads);
   const int nboxes = PX == 1 ? boxes_per_tile(bp.tile_size) : boxes_per_tile2(bp.tile_size);

@@ -40,7 +40,7 @@ typedef double sh_t;
 typedef float sh_t;
 #endif
 
-template <int C>
+template <int C, bool GENERIC>
 __device__ __forceinline__ void sh_colour_t(const float* row, int degree, sh_t x, sh_t y, sh_t z,
                                             double out[3]) {
   constexpr int kVec = (3 * C + 3) / 4;
@@ -48,7 +48,7 @@ __device__ __forceinline__ void sh_colour_t(const float* row, int degree, sh_t x
   const float4* r4 = reinterpret_cast<const float4*>(row);
 #pragma unroll
   for (int i = 0; i < kVec; ++i) {
-    const float4 v = __ldg(r4 + i);
+    const float4 v = GENERIC ? r4[i] : __ldg(r4 + i);  // GENERIC: a row staged in shared memory
     co[4 * i] = v.x; co[4 * i + 1] = v.y; co[4 * i + 2] = v.z; co[4 * i + 3] = v.w;
   }
   sh_t basis[C];
@@ -87,14 +87,15 @@ __device__ __forceinline__ void sh_colour_t(const float* row, int degree, sh_t x
   }
 }
 
+template <bool GENERIC = false>
 __device__ __forceinline__ void sh_colour(const float* row, int C, int degree, double x, double y,
                                           double z, double out[3]) {
   const sh_t fx = (sh_t)x, fy = (sh_t)y, fz = (sh_t)z;
   switch (C) {
-    case 16: sh_colour_t<16>(row, degree, fx, fy, fz, out); break;
-    case 9: sh_colour_t<9>(row, degree, fx, fy, fz, out); break;
-    case 4: sh_colour_t<4>(row, degree, fx, fy, fz, out); break;
-    default: sh_colour_t<1>(row, degree, fx, fy, fz, out); break;
+    case 16: sh_colour_t<16, GENERIC>(row, degree, fx, fy, fz, out); break;
+    case 9: sh_colour_t<9, GENERIC>(row, degree, fx, fy, fz, out); break;
+    case 4: sh_colour_t<4, GENERIC>(row, degree, fx, fy, fz, out); break;
+    default: sh_colour_t<1, GENERIC>(row, degree, fx, fy, fz, out); break;
   }
 }
 
@@ -284,77 +285,14 @@ void launch_significance(const cs_cloud& cl, const cs_camera* cams, int n_cams,
   k_significance<<<(unsigned)blocks, 256, 0, s>>>(cl, cams, n_cams, st, hits, vol_keys, vals);
 }
 
-#ifndef CS_PROJ_THREADS
-#define CS_PROJ_THREADS 256
-#endif
-#ifndef CS_PROJ_MINB
-#define CS_PROJ_MINB 3
-#endif
-constexpr int kProjThreads = CS_PROJ_THREADS;
-
-// Projection, one thread per assembled Gaussian, no compaction: every
-// per-splat output is written at the Gaussian's assembled index i (its
-// "splat id"), and a culled Gaussian gets the depth key ~0, which the stable
-// depth sort (K4) moves behind every visible one.  So the sort's first M
-// values are the visible splat ids in (depth, assembled index) order, and the
-// kernel needs no block scan or cross-CTA look-back (LoD assembly already
-// drops invisible blocks: ~97% of the assembled set is visible on C3).
-__global__ void __launch_bounds__(kProjThreads, CS_PROJ_MINB)
-k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
-          DevStats* __restrict__ stats, cs_camera cam, cs_settings st,
-          ProjOutputs po_out, const uint64_t* __restrict__ list) {
-  const int64_t n = stats->assembled;
-  const int64_t i = blockIdx.x * (int64_t)kProjThreads + threadIdx.x;
-  const int64_t cta0 = blockIdx.x * (int64_t)kProjThreads;
-  if (cta0 >= n) return;  // CTA-uniform
-  // segment starts staged in shared memory (one coalesced load; n_segs <= L*J
-  // is small), so the per-thread search costs no dependent global loads
-  constexpr int kSmemSegs = 512;
-  __shared__ int64_t s_start[kSmemSegs];
-  const int n_segs = stats->n_segs;
-  const bool smem_segs = n_segs <= kSmemSegs;
-  if (smem_segs)
-    for (int q = threadIdx.x; q < n_segs; q += kProjThreads) s_start[q] = segs[q].start;
-  __syncthreads();
-  ProjOut po;
-  po.in_front = po.ok = po.keep = false;
-  Geom g;
-  int64_t local = 0;
-  int cloud_id = 0;
-  if (i < n) {
-    int si = 0;
-    if (smem_segs) {
-      int hi = n_segs - 1;
-      while (si < hi) {
-        const int mid = (si + hi + 1) >> 1;
-        if (s_start[mid] <= i) si = mid; else hi = mid - 1;
-      }
-    } else {
-      si = find_seg(segs, n_segs, i);
-    }
-    const Seg sg = segs[si];
-    cloud_id = sg.cloud;
-    local = i - sg.start;
-    if (cloud_id < 0) {  // pointwise list mode: packed (cloud << 40 | local)
-      const uint64_t e = list[i];
-      cloud_id = (int)(e >> 40);
-      local = (int64_t)(e & ((1ull << 40) - 1));
-    }
-    g = load_geom(clouds[cloud_id], local);
-    po = project_one(g, cam, st);
-    // a row of the "rest" cloud of assign_b1 (partition.py:332-333): rendering
-    // the full cloud with the excluded rows culled equals rendering
-    // cloud.take(~mask) -- the kept rows keep their relative (index) order
-    if (po_out.exclude && po_out.exclude[i]) po.in_front = po.ok = po.keep = false;
-  }
-  // skipped_singular: in front but det <= 1e-12 (render.py:146-148)
-  const uint32_t kb = __ballot_sync(0xffffffffu, po.keep);
-  const uint32_t sb = __ballot_sync(0xffffffffu, po.in_front && !po.ok);
-  if (lane_id() == 0) {
-    if (kb) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->visible), (unsigned long long)__popc(kb));
-    if (sb) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->skipped), (unsigned long long)__popc(sb));
-  }
-  if (i >= n) return;
+// Everything K3 writes for assembled index i < n once its geometry g is
+// projected (po): depth keys, and for a kept splat its HotRec, cull box, tile
+// rectangle (and the debug record).  sh_row: the splat's SH row, in global
+// memory or (GENERIC_SH) staged in shared memory.
+template <bool GENERIC_SH>
+__device__ __forceinline__ void project_emit(int64_t i, const Geom& g, const ProjOut& po, const float* sh_row,
+                                             int sh_coeffs, const cs_camera& cam, const cs_settings& st,
+                                             const ProjOutputs& po_out) {
   // z > near > 0: the float64 bits are monotone; culled -> ~0 (sorts last)
   po_out.keys[i] = po.keep ? (uint64_t)__double_as_longlong(po.z) : ~0ull;
   // 32-bit sort key: a monotone coarsening of the float64 depth, so K4b only
@@ -372,20 +310,19 @@ k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
   po_out.vals[i] = (uint32_t)i;
   if (!po.keep) return;
   const int64_t idx = i;
-  const cs_cloud& cd = clouds[cloud_id];
   // view direction and SH colour (render.py:167-169, core.py:166-172)
   double dx = g.px - cam.center[0], dy = g.py - cam.center[1], dz = g.pz - cam.center[2];
-  int degree = min((int)st.sh_degree, degree_of(cd.sh_coeffs));
+  int degree = min((int)st.sh_degree, degree_of(sh_coeffs));
   double col[3];
 #ifdef CS_SH_F64
   double nrm = sqrt((dx * dx + dy * dy) + dz * dz);
-  sh_colour(cd.sh + local * cd.sh_stride, cd.sh_coeffs, degree, dx / nrm, dy / nrm, dz / nrm, col);
+  sh_colour<GENERIC_SH>(sh_row, sh_coeffs, degree, dx / nrm, dy / nrm, dz / nrm, col);
 #else
   {  // the colour is evaluated in float32: so is the unit view direction (no
      // float64 divisions / sqrt for a tolerance-only quantity)
     const float fx = (float)dx, fy = (float)dy, fz = (float)dz;
     const float inv = rsqrtf(fmaf(fx, fx, fmaf(fy, fy, fz * fz)));
-    sh_colour(cd.sh + local * cd.sh_stride, cd.sh_coeffs, degree, fx * inv, fy * inv, fz * inv, col);
+    sh_colour<GENERIC_SH>(sh_row, sh_coeffs, degree, fx * inv, fy * inv, fz * inv, col);
   }
 #endif
   const double c0 = ddiv(po.c, po.det);   // render.py:172
@@ -454,6 +391,258 @@ k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
   }
 }
 
+
+#ifndef CS_PROJ_THREADS
+#define CS_PROJ_THREADS 256
+#endif
+#ifndef CS_PROJ_MINB
+#define CS_PROJ_MINB 3
+#endif
+constexpr int kProjThreads = CS_PROJ_THREADS;
+#ifndef CS_PROJ_STAGED
+#define CS_PROJ_STAGED 1   // 0: one thread per Gaussian with direct global loads (A/B reference)
+#endif
+
+// Projection, one thread per assembled Gaussian, no compaction: every
+// per-splat output is written at the Gaussian's assembled index i (its
+// "splat id"), and a culled Gaussian gets the depth key ~0, which the stable
+// depth sort (K4) moves behind every visible one.  So the sort's first M
+// values are the visible splat ids in (depth, assembled index) order, and the
+// kernel needs no block scan or cross-CTA look-back (LoD assembly already
+// drops invisible blocks: ~97% of the assembled set is visible on C3).
+__global__ void __launch_bounds__(kProjThreads, CS_PROJ_MINB)
+k_project(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
+          DevStats* __restrict__ stats, cs_camera cam, cs_settings st,
+          ProjOutputs po_out, const uint64_t* __restrict__ list) {
+  const int64_t n = stats->assembled;
+  const int64_t i = blockIdx.x * (int64_t)kProjThreads + threadIdx.x;
+  const int64_t cta0 = blockIdx.x * (int64_t)kProjThreads;
+  if (cta0 >= n) return;  // CTA-uniform
+  // segment starts staged in shared memory (one coalesced load; n_segs <= L*J
+  // is small), so the per-thread search costs no dependent global loads
+  constexpr int kSmemSegs = 512;
+  __shared__ int64_t s_start[kSmemSegs];
+  const int n_segs = stats->n_segs;
+  const bool smem_segs = n_segs <= kSmemSegs;
+  if (smem_segs)
+    for (int q = threadIdx.x; q < n_segs; q += kProjThreads) s_start[q] = segs[q].start;
+  __syncthreads();
+  ProjOut po;
+  po.in_front = po.ok = po.keep = false;
+  Geom g;
+  int64_t local = 0;
+  int cloud_id = 0;
+  if (i < n) {
+    int si = 0;
+    if (smem_segs) {
+      int hi = n_segs - 1;
+      while (si < hi) {
+        const int mid = (si + hi + 1) >> 1;
+        if (s_start[mid] <= i) si = mid; else hi = mid - 1;
+      }
+    } else {
+      si = find_seg(segs, n_segs, i);
+    }
+    const Seg sg = segs[si];
+    cloud_id = sg.cloud;
+    local = i - sg.start;
+    if (cloud_id < 0) {  // pointwise list mode: packed (cloud << 40 | local)
+      const uint64_t e = list[i];
+      cloud_id = (int)(e >> 40);
+      local = (int64_t)(e & ((1ull << 40) - 1));
+    }
+    g = load_geom(clouds[cloud_id], local);
+    po = project_one(g, cam, st);
+    // a row of the "rest" cloud of assign_b1 (partition.py:332-333): rendering
+    // the full cloud with the excluded rows culled equals rendering
+    // cloud.take(~mask) -- the kept rows keep their relative (index) order
+    if (po_out.exclude && po_out.exclude[i]) po.in_front = po.ok = po.keep = false;
+  }
+  // skipped_singular: in front but det <= 1e-12 (render.py:146-148)
+  const uint32_t kb = __ballot_sync(0xffffffffu, po.keep);
+  const uint32_t sb = __ballot_sync(0xffffffffu, po.in_front && !po.ok);
+  if (lane_id() == 0) {
+    if (kb) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->visible), (unsigned long long)__popc(kb));
+    if (sb) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->skipped), (unsigned long long)__popc(sb));
+  }
+  if (i >= n) return;
+  const cs_cloud& cd = clouds[cloud_id];
+  project_emit<false>(i, g, po, cd.sh + local * cd.sh_stride, cd.sh_coeffs, cam, st, po_out);
+}
+
+// K3, staged form (every source except the pointwise list): persistent CTAs
+// walk 256-Gaussian tiles of the assembled index range.  A tile's inputs are
+// contiguous runs of the level clouds (one run per (level, block) segment it
+// touches), so thread 0 moves them into shared memory with cp.async.bulk
+// copies completing on mbarriers -- the three float32 geometry quads per
+// Gaussian double-buffered (tile t+1's copies are issued before tile t is
+// computed), the SH rows single-buffered (tile t+1's issued once tile t's
+// colours are done, landing while t+1's float64 projection math runs).  The
+// global-load latency that stalled the one-thread-per-Gaussian kernel
+// (long scoreboard, 34% of its stall samples at 35% occupancy) moves off
+// the critical path.  Runs that cannot be staged (float64 quads, SH rows
+// wider than 48 floats, more than kMaxPieces segments in a tile) fall back to
+// per-thread global loads for those rows.
+constexpr int kStPieces = 8;
+constexpr int kStShFloats = 48;  // widest staged SH row (C = 16)
+
+struct StPiece {
+  int32_t row0, rows;      // tile-relative first row, row count
+  int32_t cloud;           // descriptor index
+  int32_t staged;          // 1: quads + SH in shared memory
+  int64_t local0;          // first row inside the cloud
+  int32_t sh_off;          // float offset of the piece's SH rows in s_sh
+  int32_t pad;
+};
+
+__global__ void __launch_bounds__(kProjThreads, CS_PROJ_MINB)
+k_project_staged(const cs_cloud* __restrict__ clouds, const Seg* __restrict__ segs,
+                 DevStats* __restrict__ stats, cs_camera cam, cs_settings st,
+                 ProjOutputs po_out, const uint64_t* __restrict__ list) {
+  (void)list;
+  // dynamic shared memory: geometry quads [2][3][kProjThreads] (pos_op, scale,
+  // quat), then the SH rows of one tile (kProjThreads x kStShFloats floats)
+  extern __shared__ __align__(128) unsigned char s_dyn[];
+  float4 (*s_q)[3][kProjThreads] = reinterpret_cast<float4 (*)[3][kProjThreads]>(s_dyn);
+  float* s_sh = reinterpret_cast<float*>(s_dyn + sizeof(float4) * 2 * 3 * kProjThreads);
+  __shared__ __align__(8) uint64_t s_bar[3];                   // quads[0], quads[1], sh
+  __shared__ StPiece s_pc[2][kStPieces];                       // per quad buffer
+  __shared__ int s_npc[2];
+  __shared__ int64_t s_start[256];
+  const int64_t n = stats->assembled;
+  const int n_segs = stats->n_segs;
+  const bool smem_segs = n_segs <= 256;
+  if (smem_segs)
+    for (int q = threadIdx.x; q < n_segs; q += kProjThreads) s_start[q] = segs[q].start;
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    mbar_init(&s_bar[2], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int64_t n_tiles = (n + kProjThreads - 1) / kProjThreads;
+  auto seg_of = [&](int64_t i) -> int {
+    if (!smem_segs) return find_seg(segs, n_segs, i);
+    int lo = 0, hi = n_segs - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_start[mid] <= i) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+  };
+  // thread 0: the tile's pieces, and the bulk copies of their quads into buffer b
+  auto issue_quads = [&](int64_t tile, int b) {
+    const int64_t i0 = tile * kProjThreads, i1 = min(n, i0 + kProjThreads);
+    int np = 0;
+    uint32_t bytes = 0;
+    int sh_off = 0;
+    for (int si = seg_of(i0); si < n_segs && np < kStPieces; ++si) {
+      const Seg sg = segs[si];
+      const int64_t a = max(i0, sg.start), e = min(i1, sg.start + sg.count);
+      if (a >= e) { if (sg.start >= i1) break; continue; }
+      StPiece p;
+      p.row0 = (int32_t)(a - i0);
+      p.rows = (int32_t)(e - a);
+      p.cloud = sg.cloud;
+      p.local0 = a - sg.start;
+      const cs_cloud& cd = clouds[sg.cloud];
+      p.staged = (!cd.fp64 && cd.sh_stride <= kStShFloats) ? 1 : 0;
+      p.sh_off = sh_off;   // fixed here: threads read it before issue_sh runs
+      p.pad = 0;
+      if (p.staged) sh_off += p.rows * cd.sh_stride;
+      if (p.staged) {
+        const uint32_t qb = (uint32_t)p.rows * 16u;
+        const int64_t off = p.local0 * 16;
+        bulk_copy_g2s(&s_q[b][0][p.row0], reinterpret_cast<const char*>(cd.pos_op) + off, qb, &s_bar[b]);
+        bulk_copy_g2s(&s_q[b][1][p.row0], reinterpret_cast<const char*>(cd.scale) + off, qb, &s_bar[b]);
+        bulk_copy_g2s(&s_q[b][2][p.row0], reinterpret_cast<const char*>(cd.quat) + off, qb, &s_bar[b]);
+        bytes += 3 * qb;
+      }
+      s_pc[b][np++] = p;
+      if (e >= i1) break;
+    }
+    s_npc[b] = np;
+    mbar_arrive_expect_tx(&s_bar[b], bytes);
+  };
+  // thread 0: SH rows of the pieces in quad buffer b (after their pieces are known)
+  auto issue_sh = [&](int b) {
+    uint32_t bytes = 0;
+    for (int k = 0; k < s_npc[b]; ++k) {
+      const StPiece& p = s_pc[b][k];
+      if (!p.staged) continue;
+      const cs_cloud& cd = clouds[p.cloud];
+      const uint32_t sb = (uint32_t)p.rows * (uint32_t)cd.sh_stride * 4u;
+      bulk_copy_g2s(&s_sh[p.sh_off], cd.sh + p.local0 * cd.sh_stride, sb, &s_bar[2]);
+      bytes += sb;
+    }
+    mbar_arrive_expect_tx(&s_bar[2], bytes);
+  };
+  uint32_t ph_q0 = 0, ph_q1 = 0, ph_sh = 0;
+  int64_t tile = blockIdx.x;
+  if (tile < n_tiles && threadIdx.x == 0) {
+    issue_quads(tile, 0);
+    issue_sh(0);
+  }
+  for (int it = 0; tile < n_tiles; ++it, tile += gridDim.x) {
+    const int b = it & 1;
+    const int64_t next = tile + gridDim.x;
+    if (next < n_tiles && threadIdx.x == 0) issue_quads(next, b ^ 1);
+    mbar_wait(&s_bar[b], b ? ph_q1 : ph_q0);
+    if (b) ph_q1 ^= 1u; else ph_q0 ^= 1u;
+    const int64_t i = tile * kProjThreads + threadIdx.x;
+    const int r = (int)threadIdx.x;
+    int pk = 0;
+    const int np = s_npc[b];
+    while (pk + 1 < np && s_pc[b][pk + 1].row0 <= r) ++pk;
+    StPiece p = s_pc[b][pk];
+    const bool live = i < n;
+    if (live && r >= p.row0 + p.rows) {  // a row past the staged pieces: its own segment, global loads
+      const int si = seg_of(i);
+      const Seg sg = segs[si];
+      p.row0 = r;
+      p.rows = 1;
+      p.cloud = sg.cloud;
+      p.local0 = i - sg.start;
+      p.staged = 0;
+    }
+    const int64_t local = p.local0 + (r - p.row0);
+    ProjOut po;
+    po.in_front = po.ok = po.keep = false;
+    Geom g;
+    if (live) {
+      if (p.staged) {
+        const float4 a = s_q[b][0][r], c = s_q[b][1][r], q = s_q[b][2][r];
+        g.px = a.x; g.py = a.y; g.pz = a.z; g.op = a.w;
+        g.sx = c.x; g.sy = c.y; g.sz = c.z;
+        g.qw = q.x; g.qx = q.y; g.qy = q.z; g.qz = q.w;
+      } else {
+        g = load_geom(clouds[p.cloud], local);
+      }
+      po = project_one(g, cam, st);
+      if (po_out.exclude && po_out.exclude[i]) po.in_front = po.ok = po.keep = false;
+    }
+    const uint32_t kb = __ballot_sync(0xffffffffu, po.keep);
+    const uint32_t sb = __ballot_sync(0xffffffffu, po.in_front && !po.ok);
+    if (lane_id() == 0) {
+      if (kb) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->visible), (unsigned long long)__popc(kb));
+      if (sb) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->skipped), (unsigned long long)__popc(sb));
+    }
+    mbar_wait(&s_bar[2], ph_sh);   // this tile's SH rows
+    ph_sh ^= 1u;
+    if (live) {
+      const cs_cloud& cd = clouds[p.cloud];
+      if (p.staged)
+        project_emit<true>(i, g, po, &s_sh[p.sh_off + (r - p.row0) * cd.sh_stride], cd.sh_coeffs, cam, st, po_out);
+      else
+        project_emit<false>(i, g, po, cd.sh + local * cd.sh_stride, cd.sh_coeffs, cam, st, po_out);
+    }
+    fence_proxy_async_smem();   // this tile's shared-memory reads before the next copies
+    __syncthreads();
+    if (next < n_tiles && threadIdx.x == 0) issue_sh(b ^ 1);
+  }
+}
+
 // Single-cloud source: one segment covering the whole cloud.
 __global__ void k_setup_cloud(cs_cloud c, cs_cloud* clouds, Seg* segs, DevStats* stats) {
   clouds[0] = c;
@@ -466,12 +655,28 @@ __global__ void k_setup_cloud(cs_cloud c, cs_cloud* clouds, Seg* segs, DevStats*
 }
 
 const void* project_kernel() { return reinterpret_cast<const void*>(&k_project); }
+const void* project_staged_kernel() { return reinterpret_cast<const void*>(&k_project_staged); }
 
 void launch_project(const cs_cloud* d_clouds, const Seg* d_segs, DevStats* d_stats,
                     const cs_camera& cam, const cs_settings& st, int64_t capacity,
                     const ProjOutputs& out, const uint64_t* list, cudaStream_t s) {
   const int64_t blocks = (capacity + kProjThreads - 1) / kProjThreads;
   if (blocks == 0) return;
+  if (!list && CS_PROJ_STAGED) {  // persistent, bulk-copy staged inputs
+    constexpr size_t kDyn = sizeof(float4) * 2 * 3 * kProjThreads + sizeof(float) * kProjThreads * kStShFloats;
+    static int grid = 0;
+    if (grid == 0) {
+      cudaFuncSetAttribute(k_project_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDyn);
+      int dev = 0, sms = 0, per_sm = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_project_staged, kProjThreads, kDyn);
+      grid = std::max(1, sms * std::max(1, per_sm));
+    }
+    k_project_staged<<<(unsigned)std::min<int64_t>(grid, blocks), kProjThreads, kDyn, s>>>(
+        d_clouds, d_segs, d_stats, cam, st, out, list);
+    return;
+  }
   k_project<<<(unsigned)blocks, kProjThreads, 0, s>>>(d_clouds, d_segs, d_stats, cam, st, out, list);
 }
 

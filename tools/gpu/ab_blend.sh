@@ -7,7 +7,7 @@ for v in "$@"; do
   CS_NVCC_EXTRA="$v" python paper_2404_01133_b200/_build.py --force > /dev/null 2>&1 || { echo "build fail $v"; continue; }
   r=""
   if [ "${PARITY:-1}" = "1" ]; then
-    r=$(python -m pytest -q tests/test_gpu_parity.py tests/test_gpu_configs.py tests/test_gpu_invariance.py 2>&1 | tail -1)
+    r=$(python -m pytest -q ${TESTS:-tests/test_gpu_parity.py tests/test_gpu_configs.py tests/test_gpu_invariance.py} 2>&1 | tail -1)
   fi
   timeout 600 python bench.py $LITE > gpurun_out/${tag}_$name.json 2> gpurun_out/${tag}_$name.err
   python - "$v" "$r" "gpurun_out/${tag}_$name.json" <<'PY'
