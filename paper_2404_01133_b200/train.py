@@ -57,18 +57,22 @@ class TrainState:
             pass
 
 
-_sized = {}  # device index -> largest cloud a training forward has been sized for
+_sized = {}  # device index -> (largest cloud, largest image) a training forward was sized for
 
 
 def render_train(h, src, ccam, cset, out: torch.Tensor, count: int, dev) -> TrainState:
-    """cs_render_train; the first forward of a cloud larger than any before on
-    this device runs synchronously so the pair buffers are sized exactly."""
-    flags = 0 if _sized.get(dev.index, -1) >= count else _lib.CS_RENDER_SYNC
+    """cs_render_train; a forward of a larger cloud or a larger image than any
+    before on this device runs synchronously, so the pair buffers are sized by
+    the frame itself (pairs grow with both).  A later asynchronous forward that
+    still overflows (a much nearer view) fails loudly in its backward."""
+    pixels = int(ccam.width) * int(ccam.height)
+    k0, p0 = _sized.get(dev.index, (-1, -1))
+    flags = 0 if (k0 >= count and p0 >= pixels) else _lib.CS_RENDER_SYNC
     st = ctypes.c_void_p()
     check(_lib.load().cs_render_train(h, ctypes.byref(src), ctypes.byref(ccam), ctypes.byref(cset),
                                       out.data_ptr(), flags, ctypes.byref(st), device.stream_handle(dev)),
           "cs_render_train")
-    _sized[dev.index] = max(_sized.get(dev.index, -1), count)
+    _sized[dev.index] = (max(k0, count), max(p0, pixels))
     return TrainState(st)
 
 
@@ -278,17 +282,24 @@ class DeviceBlockTrainer:
         H, W = int(cam.height), int(cam.width)
         img, dimg = self._images(H, W)
         ccam = device.camera_struct(cam)
-        rec(0)
-        state = render_train(h, self.src, ccam, self.cset, img, self.K, self.dev)
-        rec(1)
-        check(lib.cs_training_loss(h, img.data_ptr(), target.data_ptr(), H, W, LOSS_LAMBDA,
-                                   self.loss.data_ptr(), dimg.data_ptr(), s), "cs_training_loss")
-        rec(2)
-        try:
-            check(lib.cs_render_backward(h, state.handle, dimg.data_ptr(), ctypes.byref(self.grads), s),
-                  "cs_render_backward")
-        finally:
-            state.release()
+        for attempt in range(2):
+            rec(0)
+            state = render_train(h, self.src, ccam, self.cset, img, self.K, self.dev)
+            rec(1)
+            check(lib.cs_training_loss(h, img.data_ptr(), target.data_ptr(), H, W, LOSS_LAMBDA,
+                                       self.loss.data_ptr(), dimg.data_ptr(), s), "cs_training_loss")
+            rec(2)
+            try:
+                check(lib.cs_render_backward(h, state.handle, dimg.data_ptr(), ctypes.byref(self.grads), s),
+                      "cs_render_backward")
+                break
+            except MemoryError:
+                # the forward overflowed its pair buffer (nothing was differentiated
+                # and the buffers have grown): the step is repeated once
+                if attempt:
+                    raise
+            finally:
+                state.release()
         rec(3)
         self.hp.step += 1
         check(lib.cs_block_adam(h, self.K, self.C, self.geom.data_ptr(), self.geom_m.data_ptr(),
