@@ -419,7 +419,7 @@ def frame_counts(fr: "Frames", ccams, ctx, sh, lod_scene=None, sh_coeffs_full=16
     from paper_2404_01133_b200.device import sh_stride
     lib = _lib.load()
     counts = dict(assembled=0, visible=0, pairs=0, evals=0, fragments=0, sh_bytes_visible=0, warp_hits=0,
-                  warp_hits_empty=0)
+                  warp_hits_empty=0, blend_exact_hits=0, blend_floor_resolved=0, blend_replays=0)
     seg_idx = (ctypes.c_int32 * 4096)()
     seg_cnt = (ctypes.c_int64 * 4096)()
     n_seg = ctypes.c_int32(0)
@@ -427,7 +427,8 @@ def frame_counts(fr: "Frames", ccams, ctx, sh, lod_scene=None, sh_coeffs_full=16
     for c in ccams:
         s = CsFrameStats()
         fr(c, _lib.CS_RENDER_SYNC | _lib.CS_RENDER_DIAG, s)
-        for k_ in ("assembled", "visible", "pairs", "evals", "fragments", "warp_hits", "warp_hits_empty"):
+        for k_ in ("assembled", "visible", "pairs", "evals", "fragments", "warp_hits", "warp_hits_empty",
+                   "blend_exact_hits", "blend_floor_resolved", "blend_replays"):
             counts[k_] += getattr(s, k_)
         item_max.append(s.blend_max_item_cycles)
         item_sum.append(s.blend_item_cycles)

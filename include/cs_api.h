@@ -86,6 +86,10 @@ typedef struct cs_frame_stats {
   int64_t warp_hits_empty;  /* ... of which no live pixel passed the alpha-floor test (CS_RENDER_DIAG only) */
   int64_t blend_max_item_cycles; /* longest blend work item (one pixel box), SM clocks (CS_RENDER_DIAG only) */
   int64_t blend_item_cycles;     /* sum over the blend's work items, SM clocks (CS_RENDER_DIAG only) */
+  /* certified float32 blend (CS_RENDER_DIAG only): */
+  int64_t blend_exact_hits;      /* (box, splat) hits of ill-conditioned splats decided in float64 */
+  int64_t blend_floor_resolved;  /* fragments whose alpha-floor test fell inside the error bound (float64 re-decision) */
+  int64_t blend_replays;         /* pixels whose termination test fell inside the error bound (float64 transmittance replay) */
 } cs_frame_stats;
 
 /* One block decision, VisibilityDecision (lod.py:255-264). level -1 = None. */

@@ -48,7 +48,8 @@ class CsFrameStats(ctypes.Structure):
     _fields_ = [("assembled", i64), ("visible", i64), ("skipped_singular", i64),
                 ("pairs", i64), ("fragments", i64), ("n_segments", i32), ("status", i32),
                 ("evals", i64), ("warp_hits", i64), ("warp_hits_empty", i64),
-                ("blend_max_item_cycles", i64), ("blend_item_cycles", i64)]
+                ("blend_max_item_cycles", i64), ("blend_item_cycles", i64),
+                ("blend_exact_hits", i64), ("blend_floor_resolved", i64), ("blend_replays", i64)]
 
 
 class CsDecision(ctypes.Structure):

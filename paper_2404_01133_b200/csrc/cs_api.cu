@@ -90,7 +90,7 @@ void launch_dump_tiles(const uint32_t* order, const uint32_t* vals, const uint2*
 int blend_ppt(int tile_size);
 void launch_tile_order(const uint2* ranges, int n_tiles, uint32_t* order, cudaStream_t s);
 void launch_blend(int n_tiles, const uint32_t* list, const uint32_t* bxs, const uint32_t* bys,
-                  const uint2* ranges, const HotRec* hot, const uint32_t* order,
+                  const uint2* ranges, const HotRec* hot, const FastRec* fast, const uint32_t* order,
                   const BlendParams& bp, void* out, bool f64_out, int32_t* frag_tile,
                   DevStats* stats, const BlendState* keep, cudaStream_t s);
 void launch_pack(int64_t m, const double* means, const double* conics, const double* colors,
@@ -225,7 +225,7 @@ struct Ws {
   DBuf st_gather, st_pw, st_sort, hist, sort_tickets;
   DBuf keysA, valsA, keysB, valsB, recs;
   DBuf k32A, k32B, long_runs, fix_ctl;          // K4 32-bit depth sort + K4b run fix-up
-  DBuf hot, boxes, rects, tile_order;
+  DBuf hot, fast, boxes, rects, tile_order;
   DBuf pkA, pvA, pkB, pvB, ranges, frag_tile, pw_list;
   DBuf st_t, st_last, st_acc;
   int64_t cap_vis = 0, cap_pairs = 0, cap_pw = 0, cap_tiles = 0;
@@ -242,7 +242,7 @@ struct Ws {
   void release() {
     DBuf* all[] = {&stats, &clouds1, &segs, &dec, &st_gather, &st_pw, &st_sort, &hist, &sort_tickets,
                    &keysA, &valsA, &keysB, &valsB, &recs, &k32A, &k32B, &long_runs, &fix_ctl, &hot,
-                   &boxes, &rects, &tile_order, &pkA, &pvA, &pkB, &pvB, &ranges, &frag_tile, &pw_list,
+                   &fast, &boxes, &rects, &tile_order, &pkA, &pvA, &pkB, &pvB, &ranges, &frag_tile, &pw_list,
                    &st_t, &st_last, &st_acc};
     for (DBuf* b : all) b->release();
   }
@@ -594,8 +594,11 @@ static int render_once(cs_ctx* c, Ws* w, const cs_source* src, const cs_camera* 
   const int64_t cap = std::max<int64_t>(cap_vis, 1);
   const bool debug = (flags & (CS_RENDER_DEBUG | CS_RENDER_PROJECT_ONLY)) != 0;
   if (debug && w->recs.ensure(sizeof(ProjRec) * w->cap_vis)) return fail(CS_ENOMEM, "debug records");
+  // the certified float32 blend's records (frames without kept state)
+  const bool fast_blend = !(flags & CS_RENDER_KEEP_STATE);
+  if (fast_blend && w->fast.ensure(sizeof(FastRec) * w->cap_vis)) return fail(CS_ENOMEM, "blend records");
   ProjOutputs po{w->keysA.as<uint64_t>(), w->k32A.as<uint32_t>(), w->valsA.as<uint32_t>(),
-                 w->hot.as<HotRec>(),
+                 w->hot.as<HotRec>(), fast_blend ? w->fast.as<FastRec>() : nullptr,
                  w->rects.as<uint2>(), w->boxes.as<short4>(),
                  debug ? w->recs.as<ProjRec>() : nullptr,
                  src->kind == CS_SRC_CLOUD ? src->exclude : nullptr};
@@ -675,7 +678,7 @@ static int render_once(cs_ctx* c, Ws* w, const cs_source* src, const cs_camera* 
   launch_tile_order(w->ranges.as<uint2>(), n_tiles, w->tile_order.as<uint32_t>(), s);
   CS_CHECK_LAUNCH();
   launch_blend(n_tiles, tvals, bxs, bys, w->ranges.as<uint2>(), w->hot.as<HotRec>(),
-               w->tile_order.as<uint32_t>(),
+               fast_blend ? w->fast.as<FastRec>() : nullptr, w->tile_order.as<uint32_t>(),
                bp, out, (flags & CS_RENDER_F64_OUT) != 0, w->frag_tile.as<int32_t>(), stats,
                (flags & CS_RENDER_KEEP_STATE) ? &keep : nullptr, s);
   CS_CHECK_LAUNCH();
@@ -693,7 +696,8 @@ static int render_once(cs_ctx* c, Ws* w, const cs_source* src, const cs_camera* 
 }
 
 static_assert(offsetof(DevStats, blend_max_item_cycles) == offsetof(cs_frame_stats, blend_max_item_cycles) &&
-                  sizeof(cs_frame_stats) <= offsetof(DevStats, pairs_eff) + sizeof(int64_t),
+                  offsetof(DevStats, blend_replays) == offsetof(cs_frame_stats, blend_replays) &&
+                  sizeof(cs_frame_stats) == offsetof(DevStats, pairs_eff),
               "DevStats must lead with the cs_frame_stats layout");
 static int fetch_stats(cs_ctx* c, Ws* w, cudaStream_t s) {
   // DevStats and cs_frame_stats share the leading layout
@@ -1319,7 +1323,7 @@ int cs_blend_tiles(cs_ctx* c, const int64_t* tile_ids, const int64_t* tile_offse
   bp.height = height;
   bp.ntx = n_tiles_x;
   bp.flags = CS_RENDER_NO_CLIP;
-  launch_blend((int)n_tiles, list, pbx, pby, ranges, hot, nullptr, bp, out, true, ftile, w->stats.as<DevStats>(),
+  launch_blend((int)n_tiles, list, pbx, pby, ranges, hot, nullptr, nullptr, bp, out, true, ftile, w->stats.as<DevStats>(),
                nullptr, s);
   CS_CHECK_LAUNCH();
   // fragments: int32 per tile -> int64

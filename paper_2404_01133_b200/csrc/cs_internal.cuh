@@ -58,6 +58,123 @@ struct __align__(16) HotRec {   // everything the blend reads per splat (64 B: 4
 static_assert(sizeof(HotRec) == 64, "HotRec layout");
 constexpr int kHotChunks = (int)(sizeof(HotRec) / 16);  // cp.async 16-byte copies per record
 
+// ---------------------------------------------------------------------------
+// FastRec: what the certified float32 blend (cs_blend.cu, k_blend_fast) stages
+// per splat instead of the float64 HotRec.  The reference decides every
+// fragment in float64 (_kernels.py:52-66); the fast blend evaluates the same
+// quantities in float32 and carries, per splat, a PROVEN bound on how far its
+// float32 results can be from the float64 ones, so that every decision whose
+// float32 value is farther than the bound from its threshold is the
+// reference's decision.  Decisions inside the bound are re-made in float64
+// (cs_blend.cu).  Fields:
+//   mean   = (mxh + mxl, myh + myl): float hi/lo split of the float64 mean, so
+//            dx = (sx - mxh) - mxl loses only ~2u |dx| (u = 2^-24);
+//   A, B, C: float(-c0/2), float(-c1), float(-c2/2): power = (A dx + B dy) dx + C dy^2;
+//   pthr   : fast-reject threshold on the float32 power: lthr - dp, rounded
+//            down, where dp bounds |power32 - power64| wherever
+//            power64 >= lthr - 1 (the float64 fast reject of the exact kernel
+//            is power64 < lthr; outside that region power32 < lthr - 1 too);
+//   ek1/ek0: per-fragment bound on |alpha32 / alpha64 - 1|:
+//            ek1 |power32| + ek0 (the float32 power's error is proportional to
+//            |power| through S(d) <= ratio |power|, plus exp2 argument
+//            rounding, MUFU.EX2 error, opacity rounding) -- near the centre of
+//            an opaque splat, where 1/(1 - alpha) amplifies it, it is ~6e-7;
+//   flo/fhi: alpha_floor (1 -/+ eps), eps the bound at the alpha-floor
+//            contour, rounded outward: alpha32 < flo is a certain skip,
+//            alpha32 >= fhi a certain accept (_kernels.py:61).
+// Ill-conditioned splats (thin, edge-on: dp > kFastMaxDp, non-positive-definite
+// or non-finite conic) are flagged in their cull box (kBoxExact): every lane
+// takes the float64 path for them.
+struct __align__(16) FastRec {
+  float mxh, mxl, myh, myl;
+  float A, B, C, of;
+  float r, g, b, pthr;
+  float ek1, ek0, flo, fhi;
+  // a staging slot holding a flagged splat's HotRec instead (k_blend_fast)
+  __device__ const HotRec& as_hot() const { return *reinterpret_cast<const HotRec*>(this); }
+};
+static_assert(sizeof(FastRec) == 64, "FastRec layout");
+// A flagged splat's cull box carries x0 = kBoxExact (K3, fast-blend frames
+// only): the blend then stages its float64 HotRec instead of the FastRec.  The
+// box only widens to the left (x0 = -32768 never rejects), so the cull stays
+// conservative; pixels outside the splat are rejected by its float64 power.
+constexpr int kBoxExact = -32768;
+constexpr float kFastMaxDp = 2e-5f;      // power-error bound above which a splat is decided in float64
+// max relative error of ex2.approx.ftz.f32 over [-32, 1]: measured exhaustively
+// on the B200 by tools/ex2_check.cu (profiles/r2_ex2_check.txt); the bound
+// used here is twice that.
+constexpr float kEx2RelErr = 4.0e-7f;
+
+// Build the FastRec of a visible splat from the float64 values the exact path
+// uses (mean, conic = inverse of (a, b, c), opacity, lthr) -- K3 and the
+// cs_blend_tiles packer.  (ca, cc): diagonal of the conic's inverse (the
+// 2D covariance incl. low pass), which bounds the pixel offsets of the region
+// {power >= lthr - 1}: |dx| <= sqrt(2 (L + 1) ca), |dy| <= sqrt(2 (L + 1) cc).
+__device__ __forceinline__ FastRec make_fast_rec(double mx, double my, double c0, double c1, double c2,
+                                                 double opacity, float lthr, float r, float g, float b,
+                                                 double ca, double cc, double alpha_floor, bool& exact) {
+  constexpr float u = 5.9604645e-8f;  // 2^-24
+  FastRec f;
+  f.mxh = (float)mx;
+  f.mxl = (float)(mx - (double)f.mxh);
+  f.myh = (float)my;
+  f.myl = (float)(my - (double)f.myh);
+  f.A = (float)(-0.5 * c0);
+  f.B = (float)(-c1);
+  f.C = (float)(-0.5 * c2);
+  f.of = (float)opacity;
+  f.r = r; f.g = g; f.b = b;
+  exact = false;
+  const float L = -lthr;  // > 0 for any alpha_floor < opacity (else lthr >= 0: never passes)
+  if (!(L > 0.0f) || !(opacity > 0.0)) {   // nothing can pass: keep the fast path, never passes
+    f.pthr = __int_as_float(0x7f800000);
+    f.ek1 = f.ek0 = 0.f; f.flo = f.fhi = (float)alpha_floor;
+    return f;
+  }
+  const bool pd = c0 > 0.0 && c2 > 0.0 && c0 * c2 - c1 * c1 > 0.0 && ca > 0.0 && cc > 0.0 && fabs(c1) < sqrt(c0 * c2) &&
+                  isfinite(mx) && isfinite(my) && isfinite(c0) && isfinite(c1) && isfinite(c2) &&
+                  isfinite(ca) && isfinite(cc);
+  // Error of the float32 power on R = {power64 >= lthr - 1} = {d^T C d <= Q},
+  // C = [[c0, c1], [c1, c2]], Q = 2 (L + 1):
+  //  * rounding (coefficients, two products, two fmas): <= 4u S(d),
+  //    S(d) = 0.5 c0 dx^2 + |c1 dx dy| + 0.5 c2 dy^2 = 0.5 d^T |C| d (|C|: |c1|);
+  //  * offsets: |dx32 - dx| <= 2u |dx| + u |mxl| (dx = (sx - mxh) - mxl), so
+  //    |grad . e| <= 2u (|c0 dx + c1 dy| |dx| + |c1 dx + c2 dy| |dy|) <= 4u S(d)
+  //    plus the |mxl| terms;
+  //  * max of S on R: 0.5 Q lambda_max(|C|, C) = 0.5 Q (1 + rho) / (1 - rho),
+  //    rho = |c1| / sqrt(c0 c2) (the generalized eigenvalue of the pair).
+  // Thin, edge-on splats (rho -> 1) exceed kFastMaxDp and are flagged.
+  const float Q = 2.0f * (L + 1.0f) * 1.0001f;
+  const double rho = fabs(c1) / sqrt(c0 * c2);
+  const float ratio = (float)((1.0 + rho) / (1.0 - rho)) * 1.0001f;   // max of S(d) / |power(d)|
+  const float Smax = 0.5f * Q * ratio;
+  const float DX = sqrtf(Q * (float)ca) * 1.0001f + 1e-3f;   // |dx| on R
+  const float DY = sqrtf(Q * (float)cc) * 1.0001f + 1e-3f;
+  const float a0 = fabsf((float)c0) * 1.0001f, a1 = fabsf((float)c1) * 1.0001f,
+              a2 = fabsf((float)c2) * 1.0001f;
+  const float lo_terms = 2.0f * u * ((a0 * DX + a1 * DY) * (fabsf(f.mxl) + 1e-30f) + (a1 * DX + a2 * DY) * fabsf(f.myl));
+  const float dp = 1.25f * (8.0f * u * Smax + lo_terms) + 1e-9f;
+  if (!pd || !(dp <= kFastMaxDp)) {
+    exact = true;
+    f.pthr = lthr;
+    f.ek1 = f.ek0 = 0.f; f.flo = f.fhi = (float)alpha_floor;
+    return f;
+  }
+  f.pthr = __fsub_rd(lthr, dp);
+  // alpha32 = of * ex2(power32 * log2e): relative error <= (e^dp - 1) + argument
+  // rounding (log2e and the product: 2u |power| * ln2 * log2e) + ex2 + 2u
+  const float pmax = L + dp + 1.0f;
+  const float eps = 1.01f * (dp * (1.0f + dp) + 2.0f * u * pmax + kEx2RelErr + 3.0f * u);
+  f.flo = __fmul_rd((float)alpha_floor, 1.0f - eps - 2.0f * u);
+  f.fhi = __fmul_ru((float)alpha_floor, 1.0f + eps + 2.0f * u);
+  // per fragment: |power32 - power64| <= 10u S(d) + lo_terms, S(d) <= ratio |power_real|,
+  // |power_real| <= |power32| + dp; so eps(d) <= ek1 |power32| + ek0
+  const float k8 = 1.01f * (1.0f + dp) * 10.0f * u * ratio;
+  f.ek1 = k8 + 2.02f * u;
+  f.ek0 = k8 * dp + 1.01f * (1.0f + dp) * (lo_terms + 1e-9f) + 2.02f * u * dp + 1.01f * (kEx2RelErr + 3.0f * u);
+  return f;
+}
+
 // pair-major cull boxes for the blend: (lo | hi << 16) as two int16, one word
 // per axis; kEmptyBox = (32767, -32768) never intersects
 __host__ __device__ __forceinline__ uint32_t pack_box(int lo, int hi) {
@@ -110,6 +227,9 @@ struct DevStats {     // device mirror of cs_frame_stats + scratch counters
   int64_t warp_hits_empty;  // ... where no live pixel passed the fast reject
   int64_t blend_max_item_cycles;  // longest blend work item (DIAG)
   int64_t blend_item_cycles;      // sum over blend work items (DIAG)
+  int64_t blend_exact_hits;       // certified float32 blend (DIAG): hits decided in float64
+  int64_t blend_floor_resolved;   // ... alpha-floor tests re-decided in float64
+  int64_t blend_replays;          // ... transmittance replays
   int64_t pairs_eff;     // pairs actually processed (0 when the pair buffer overflowed)
   uint32_t tickets[16];  // chunk tickets for single-pass kernels, zeroed per frame
 };
@@ -131,6 +251,7 @@ struct ProjOutputs {
   uint32_t* keys32;  // float32-rounded depth bits (~0 for culled): the radix-sorted key
   uint32_t* vals;    // splat id
   HotRec* hot;
+  FastRec* fast;     // optional: the certified float32 blend's records (non-kept-state frames)
   uint2* rects;      // tile rectangle, 16-bit packed: (x0 | x1 << 16, y0 | y1 << 16)
   short4* boxes;     // copy of HotRec's cull box, dense (8 B)
   ProjRec* recs;     // optional (debug / dumps)
@@ -155,6 +276,9 @@ struct BlendParams {
   double alpha_floor, t_floor;
   int tile_size, width, height, ntx;
   uint32_t flags;
+  // certified float32 blend: t_floor as float, the termination band
+  // t_floor (1.01 en + 4u) = en * tfl_b + tfl_c, and 1.5 t_floor
+  float tfl, tfl_b, tfl_c, tfl_far;
 };
 
 struct BlendState {  // per-pixel state kept for the backward pass

@@ -363,6 +363,13 @@ __device__ __forceinline__ void project_emit(int64_t i, const Geom& g, const Pro
     box.w = (int16_t)fmin(fmax(floor(po.my + hy - 0.5), -1.0), lim);
   }
   po_out.hot[idx] = h;
+  if (po_out.fast) {
+    bool exact;
+    const FastRec f = make_fast_rec(po.mx, po.my, c0, c1, c2, g.op, lthr, h.r, h.g, h.b, po.a, po.c,
+                                    st.alpha_floor, exact);
+    po_out.fast[idx] = f;
+    if (exact) box.x = (int16_t)kBoxExact;
+  }
   po_out.boxes[idx] = box;
   // tile rectangle exactly as numpy (render.py:226-231): floor, astype(int64), clip
   {

@@ -78,5 +78,5 @@ def test_struct_layouts_match_header():
     import ctypes
     assert ctypes.sizeof(_lib.CsCamera) == 8 * 19 + 8
     assert ctypes.sizeof(_lib.CsCloud) == 4 * 8 + 8 + 16
-    assert ctypes.sizeof(_lib.CsFrameStats) == 5 * 8 + 8 + 5 * 8
+    assert ctypes.sizeof(_lib.CsFrameStats) == 5 * 8 + 8 + 8 * 8
     assert ctypes.sizeof(_lib.CsDecision) == 5 * 8 + 8
