@@ -169,6 +169,7 @@ k_bin_pairs(const uint32_t* __restrict__ order, const uint2* __restrict__ rects,
   __shared__ BinSmem sm;
   __shared__ uint64_t s_prefix;
   __shared__ uint32_t s_chunk;
+  if (stats->tl_mode == 1) return;  // the tile-local path (cs_tiles.cu) bins this frame
   const int64_t M = stats->visible;
   for (int i = threadIdx.x; i < dh.n_passes * 256; i += kBinThreads) sm.hist[i >> 8][i & 255] = 0;
   // CS_BIN_PERSIST: one wave of CTAs looping over chunk tickets (the grid is
@@ -232,6 +233,7 @@ k_emit_heavy(const uint32_t* __restrict__ order, const uint2* __restrict__ rects
              uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, DigitHist dh) {
   __shared__ BinSmem sm;
   __shared__ uint32_t s_t[2];  // double-buffered ticket: thread 0 writes the next while others read this one
+  if (stats->tl_mode == 1) return;
   const unsigned long long hc = *reinterpret_cast<const unsigned long long*>(&stats->tickets[8]);
   const uint32_t n_entries = (uint32_t)(hc >> 32), n_slices = (uint32_t)hc;
   if (n_slices == 0) return;
@@ -270,12 +272,12 @@ k_emit_heavy(const uint32_t* __restrict__ order, const uint2* __restrict__ rects
 // pair-major cull boxes the blend tests (boxes[vals[p]] split into one u32 per
 // axis, so a warp's 32 box reads are two coalesced 128-byte loads).
 __global__ void k_tile_ranges(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
-                              const uint2* __restrict__ boxes, const DevStats* __restrict__ stats,
+                              const uint2* __restrict__ boxes, const int64_t* __restrict__ n_pairs,
                               uint2* __restrict__ ranges, uint32_t* __restrict__ bxs,
                               uint32_t* __restrict__ bys) {
   // four consecutive pairs per thread (16-byte loads / stores, four independent
   // box gathers in flight); pairs < 2^30, so 32-bit indices
-  const uint32_t P = (uint32_t)stats->pairs_eff;
+  const uint32_t P = (uint32_t)*n_pairs;
   const uint32_t groups = (P + 3) / 4;
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += stride) {
@@ -356,9 +358,9 @@ void launch_bin_pairs(const uint32_t* order, const uint2* rects, DevStats* stats
 }
 
 void launch_tile_ranges(const uint32_t* keys, const uint32_t* vals, const short4* boxes,
-                        const DevStats* stats, uint2* ranges, uint32_t* bxs, uint32_t* bys,
+                        const int64_t* n_pairs, uint2* ranges, uint32_t* bxs, uint32_t* bys,
                         cudaStream_t s) {
-  k_tile_ranges<<<148 * 8, 256, 0, s>>>(keys, vals, reinterpret_cast<const uint2*>(boxes), stats,
+  k_tile_ranges<<<148 * 8, 256, 0, s>>>(keys, vals, reinterpret_cast<const uint2*>(boxes), n_pairs,
                                         ranges, bxs, bys);
 }
 

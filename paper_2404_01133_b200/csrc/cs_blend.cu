@@ -348,10 +348,10 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
 // in float32 on the FMA pipe and MUFU.EX2 instead of the float64 chain.  Every
 // reference decision (_kernels.py:52-66) is taken from float32 values only
 // when a proven error bound keeps it on the same side of its threshold:
-//   * power < lthr (the exact kernel's guaranteed skip): power32 < pthr;
-//   * alpha < alpha_floor: alpha32 < flo skips, alpha32 >= fhi accepts; in
-//     between (|alpha32/alpha - 1| <= eps straddles the floor) the fragment's
-//     float64 alpha is computed from its HotRec (exact_alpha);
+//   * alpha < alpha_floor, in the log2 domain: P32 = log2(alpha32) < Flo
+//     skips, P32 >= Fhi accepts (one compare each; the skip test is all an
+//     empty hit costs); in between (|P32 - P| <= dP straddles log2(afl)) the
+//     fragment's float64 alpha is computed from its HotRec (exact_alpha);
 //   * T (1 - alpha) < t_floor: the pixel carries its float32 transmittance T
 //     and a bound eT on |T32/T - 1| (each accepted fragment adds
 //     eps alpha/(1 - alpha) for the error of (1 - alpha), plus roundings);
@@ -492,7 +492,6 @@ k_blend_fast(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs
              float guard_scale, OutT* __restrict__ out, int32_t* __restrict__ frag_tile,
              DevStats* __restrict__ stats) {
   constexpr float u = 5.9604645e-8f;
-  constexpr float kLog2e = 1.44269504f;
   __shared__ __align__(16) FastRec s_rec[kBlendThreads / 32][2][32];
   __shared__ uint32_t s_id[kBlendThreads / 32][2][32];
   __shared__ ExpTable s_exp;
@@ -508,6 +507,7 @@ k_blend_fast(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs
   uint32_t wbase;
   asm volatile("mov.b32 %0, %1;" : "=r"(wbase) : "r"(smem_u32(&wrec[0][0])));
   uint32_t frags = 0, whits = 0, evals = 0, whits_empty = 0, n_exact = 0, n_floor = 0, n_replay = 0;
+  const float l2afl = (float)log2(bp.alpha_floor);  // GUARD only
   for (;;) {
     int item = 0;
     if (lane == 0) item = (int)atomicAdd(&stats->tickets[4], 1u);
@@ -573,29 +573,31 @@ k_blend_fast(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs
       done = done || stop;
       return !(acc && !stop && !cont);
     };
-    // The float32 evaluation of FastRec `ra` for this lane: the fast reject, the
-    // alpha, and the alpha-floor decision (acc; amb when inside the bound).
-    auto fast_alpha = [&](uint32_t ra, float& a, float& eps, bool& acc, bool& amb) {
-      const float4 q0 = lds128(ra);          // mxh mxl myh myl
-      const float4 q1 = lds128(ra + 16);     // A B C of
-      const float pthr = lds32(ra + 44);
+    // The float32 evaluation of FastRec `ra` for this lane: P32 = log2 of the
+    // unclamped alpha, and the alpha-floor pass (P32 >= Flo: may reach the floor).
+    auto fast_power = [&](uint32_t ra, float& P) -> bool {
+      const float4 q0 = lds128(ra + kFrMean);   // mxh mxl myh myl
+      const float4 q1 = lds128(ra + kFrQuad);   // A B C L2o
+      const float flo = lds32(ra + kFrFloor);
       const float dx = (sx - q0.x) - q0.y;
       const float dy = (sy - q0.z) - q0.w;
-      const float pf = fmaf(fmaf(q1.x, dx, q1.y * dy), dx, (q1.z * dy) * dy);
-      const bool pass = pf >= pthr;                  // power < lthr: skipped (_kernels.py:61-62)
-      const float4 q3 = lds128(ra + 48);     // ek1 ek0 flo fhi
-      a = q1.w * ex2_approx(pf * kLog2e);           // alpha = o exp(power)  (_kernels.py:58)
-      eps = fmaf(fabsf(pf), q3.x, q3.y);            // this fragment's alpha error bound
-      float lo = q3.z, hi = q3.w;
+      P = fmaf(fmaf(q1.x, dx, q1.y * dy), dx, fmaf(q1.z * dy, dy, q1.w));
+      return P >= (GUARD ? flo - (l2afl - flo) * (guard_scale - 1.0f) : flo);  // else skipped (_kernels.py:61-62)
+    };
+    // ... and for a passing lane: alpha32 = 2^P32, its error bound, and the
+    // alpha-floor decision (acc; amb when inside the bound)
+    auto fast_alpha = [&](uint32_t ra, float P, float& a, float& eps, bool& acc, bool& amb) {
+      const float4 q2 = lds128(ra + kFrFloor);  // flo fhi ek1 ek0
+      const float l2o = lds32(ra + kFrQuad + 12);
+      a = ex2_approx(P);                              // alpha = o exp(power)  (_kernels.py:58)
+      eps = fmaf(fabsf(P - l2o), q2.z, q2.w);         // this fragment's alpha error bound
+      float fhi = q2.y;
       if (GUARD) {
-        const float afl = (float)bp.alpha_floor;
         eps *= guard_scale;
-        hi = afl * (1.0f + eps + 2.0f * u);
-        lo = afl * (1.0f - eps - 2.0f * u);
+        fhi = l2afl + (fhi - l2afl) * guard_scale;
       }
-      acc = pass && a >= hi;
-      amb = pass && !acc && a >= lo;   // alpha straddles alpha_floor within its bound
-      return pass;
+      acc = P >= fhi;
+      amb = !acc;   // (callers pass only lanes with P >= flo): alpha straddles alpha_floor within its bound
     };
 
     // the nh hits of one staged round, slots in list order; fslot: slots
@@ -609,17 +611,19 @@ k_blend_fast(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs
       // one float32-path hit for every lane (warp-converged)
       auto fast_hit = [&](int sl, bool live) {
         const uint32_t ra = rbase + (uint32_t)sl * (uint32_t)sizeof(FastRec);
-        float a, eps;
-        bool acc, amb;
-        const bool pass = fast_alpha(ra, a, eps, acc, amb) && live;
+        float P;
+        const bool pass = fast_power(ra, P) && live;
         if (!__any_sync(0xffffffffu, pass)) {
           if (DIAG) whits_empty += lane == 0;
           return;
         }
-        acc = acc && live;
-        amb = amb && live;
-        const float4 q2 = lds128(ra + 32);   // r g b pthr
-        const bool ok = apply(acc, a, eps, q2.x, q2.y, q2.z);
+        float a, eps;
+        bool acc, amb;
+        fast_alpha(ra, P, a, eps, acc, amb);
+        acc = acc && pass;
+        amb = amb && pass;
+        const float4 q3 = lds128(ra + kFrColour);   // r g b -
+        const bool ok = apply(acc, a, eps, q3.x, q3.y, q3.z);
         if (amb || !ok) { frozen = sl; famb = amb; }
       };
       if (fslot == 0) {   // (almost every round) no flagged splat
@@ -654,9 +658,9 @@ k_blend_fast(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs
           const int sl = frozen;
           const uint32_t ra = rbase + (uint32_t)sl * (uint32_t)sizeof(FastRec);
           const bool flg = (fslot >> sl) & 1u;
-          const float fr = flg ? wrec[st_][sl].as_hot().r : lds32(ra + 32);
-          const float fg = flg ? wrec[st_][sl].as_hot().g : lds32(ra + 36);
-          const float fb = flg ? wrec[st_][sl].as_hot().b : lds32(ra + 40);
+          const float fr = flg ? wrec[st_][sl].as_hot().r : lds32(ra + kFrColour);
+          const float fg = flg ? wrec[st_][sl].as_hot().g : lds32(ra + kFrColour + 4);
+          const float fb = flg ? wrec[st_][sl].as_hot().b : lds32(ra + kFrColour + 8);
           if (famb) {   // the alpha-floor test in float64, then the termination test as usual
             if (DIAG) ++n_floor;
             const double ad = exact_alpha_at(hot, wid[st_][sl], (int)sx, (int)sy, &s_exp);
@@ -680,9 +684,9 @@ k_blend_fast(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs
             if (DIAG) ++n_replay;
             const uint32_t ra = rbase + (uint32_t)sl * (uint32_t)sizeof(FastRec);
             const bool flg = (fslot >> sl) & 1u;
-            const float fr = flg ? wrec[st_][sl].as_hot().r : lds32(ra + 32);
-            const float fg = flg ? wrec[st_][sl].as_hot().g : lds32(ra + 36);
-            const float fb = flg ? wrec[st_][sl].as_hot().b : lds32(ra + 40);
+            const float fr = flg ? wrec[st_][sl].as_hot().r : lds32(ra + kFrColour);
+            const float fg = flg ? wrec[st_][sl].as_hot().g : lds32(ra + kFrColour + 4);
+            const float fb = flg ? wrec[st_][sl].as_hot().b : lds32(ra + kFrColour + 8);
             const double nt = dmul(Tb, dsub(1.0, akq));
             if (akq < bp.alpha_floor) {
               T = (float)Tb;          // (not reached: the fragment was accepted)
@@ -714,12 +718,13 @@ k_blend_fast(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs
               }
               continue;
             }
-            float a, eps;
+            float P, a, eps;
             bool acc, amb;
-            if (!fast_alpha(ra, a, eps, acc, amb)) continue;
+            if (!fast_power(ra, P)) continue;
+            fast_alpha(ra, P, a, eps, acc, amb);
             if (amb) { frozen = sl; famb = true; break; }
-            const float4 q2 = lds128(ra + 32);
-            if (!apply(acc, a, eps, q2.x, q2.y, q2.z)) { frozen = sl; famb = false; break; }
+            const float4 q3 = lds128(ra + kFrColour);
+            if (!apply(acc, a, eps, q3.x, q3.y, q3.z)) { frozen = sl; famb = false; break; }
           }
         }
         fz = __ballot_sync(0xffffffffu, frozen < nh);

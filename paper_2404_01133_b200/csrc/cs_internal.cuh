@@ -66,34 +66,39 @@ constexpr int kHotChunks = (int)(sizeof(HotRec) / 16);  // cp.async 16-byte copi
 // float32 results can be from the float64 ones, so that every decision whose
 // float32 value is farther than the bound from its threshold is the
 // reference's decision.  Decisions inside the bound are re-made in float64
-// (cs_blend.cu).  Fields:
+// (cs_blend.cu).  Everything is in the log2 domain of alpha:
+//   P = log2(o exp(power)) = log2(e) power + log2(o),  alpha = 2^P (before the
+//   0.99 clamp), evaluated as P32 = (A dx + B dy) dx + (C dy dy + L2o):
 //   mean   = (mxh + mxl, myh + myl): float hi/lo split of the float64 mean, so
 //            dx = (sx - mxh) - mxl loses only ~2u |dx| (u = 2^-24);
-//   A, B, C: float(-c0/2), float(-c1), float(-c2/2): power = (A dx + B dy) dx + C dy^2;
-//   pthr   : fast-reject threshold on the float32 power: lthr - dp, rounded
-//            down, where dp bounds |power32 - power64| wherever
-//            power64 >= lthr - 1 (the float64 fast reject of the exact kernel
-//            is power64 < lthr; outside that region power32 < lthr - 1 too);
+//   A, B, C: float(-log2(e) c0 / 2), float(-log2(e) c1), float(-log2(e) c2 / 2);
+//   L2o    : float(log2(o)) -- folded into the last FMA, so alpha32 = ex2(P32)
+//            costs no multiply and the floor test is one compare;
+//   Flo/Fhi: log2(alpha_floor) -/+ dP, rounded outward, dP bounding
+//            |P32 - P| on R = {power64 >= lthr - 1} (which holds the floor
+//            contour): P32 < Flo is a certain skip, P32 >= Fhi a certain
+//            accept (_kernels.py:61); outside R, P32 < Flo as well (the
+//            error there is a tiny fraction of |P|, and P < log2(afl) - 1.44);
 //   ek1/ek0: per-fragment bound on |alpha32 / alpha64 - 1|:
-//            ek1 |power32| + ek0 (the float32 power's error is proportional to
-//            |power| through S(d) <= ratio |power|, plus exp2 argument
-//            rounding, MUFU.EX2 error, opacity rounding) -- near the centre of
-//            an opaque splat, where 1/(1 - alpha) amplifies it, it is ~6e-7;
-//   flo/fhi: alpha_floor (1 -/+ eps), eps the bound at the alpha-floor
-//            contour, rounded outward: alpha32 < flo is a certain skip,
-//            alpha32 >= fhi a certain accept (_kernels.py:61).
+//            ek1 |P32 - L2o| + ek0 (the quadratic form's error is proportional
+//            to |power| through S(d) <= ratio |power|, plus the L2o roundings,
+//            MUFU.EX2 error) -- near the centre of an opaque splat (L2o ~ 0),
+//            where 1/(1 - alpha) amplifies it, it is ~6e-7;
+//   r, g, b: SH colour.
 // Ill-conditioned splats (thin, edge-on: dp > kFastMaxDp, non-positive-definite
 // or non-finite conic) are flagged in their cull box (kBoxExact): every lane
 // takes the float64 path for them.
 struct __align__(16) FastRec {
   float mxh, mxl, myh, myl;
-  float A, B, C, of;
-  float r, g, b, pthr;
-  float ek1, ek0, flo, fhi;
+  float A, B, C, L2o;
+  float flo, fhi, ek1, ek0;
+  float r, g, b, pad;
   // a staging slot holding a flagged splat's HotRec instead (k_blend_fast)
   __device__ const HotRec& as_hot() const { return *reinterpret_cast<const HotRec*>(this); }
 };
 static_assert(sizeof(FastRec) == 64, "FastRec layout");
+// byte offsets inside a staged FastRec (k_blend_fast reads them with ld.shared)
+constexpr uint32_t kFrMean = 0, kFrQuad = 16, kFrFloor = 32, kFrColour = 48;
 // A flagged splat's cull box carries x0 = kBoxExact (K3, fast-blend frames
 // only): the blend then stages its float64 HotRec instead of the FastRec.  The
 // box only widens to the left (x0 = -32768 never rejects), so the cull stays
@@ -106,36 +111,38 @@ constexpr float kFastMaxDp = 2e-5f;      // power-error bound above which a spla
 constexpr float kEx2RelErr = 4.0e-7f;
 
 // Build the FastRec of a visible splat from the float64 values the exact path
-// uses (mean, conic = inverse of (a, b, c), opacity, lthr) -- K3 and the
-// cs_blend_tiles packer.  (ca, cc): diagonal of the conic's inverse (the
-// 2D covariance incl. low pass), which bounds the pixel offsets of the region
-// {power >= lthr - 1}: |dx| <= sqrt(2 (L + 1) ca), |dy| <= sqrt(2 (L + 1) cc).
+// uses (mean, conic = inverse of (a, b, c), opacity, lthr) -- K3.  (ca, cc):
+// diagonal of the conic's inverse (the 2D covariance incl. low pass), which
+// bounds the pixel offsets of the region R = {power >= lthr - 1}:
+// |dx| <= sqrt(2 (L + 1) ca), |dy| <= sqrt(2 (L + 1) cc).
 __device__ __forceinline__ FastRec make_fast_rec(double mx, double my, double c0, double c1, double c2,
                                                  double opacity, float lthr, float r, float g, float b,
                                                  double ca, double cc, double alpha_floor, bool& exact) {
   constexpr float u = 5.9604645e-8f;  // 2^-24
+  constexpr double kLog2e = 1.4426950408889634;
+  constexpr float kLn2 = 0.69314718f;
   FastRec f;
   f.mxh = (float)mx;
   f.mxl = (float)(mx - (double)f.mxh);
   f.myh = (float)my;
   f.myl = (float)(my - (double)f.myh);
-  f.A = (float)(-0.5 * c0);
-  f.B = (float)(-c1);
-  f.C = (float)(-0.5 * c2);
-  f.of = (float)opacity;
-  f.r = r; f.g = g; f.b = b;
+  f.A = (float)(-0.5 * kLog2e * c0);
+  f.B = (float)(-kLog2e * c1);
+  f.C = (float)(-0.5 * kLog2e * c2);
+  f.L2o = opacity > 0.0 ? (float)log2(opacity) : 0.0f;
+  f.r = r; f.g = g; f.b = b; f.pad = 0.f;
   exact = false;
   const float L = -lthr;  // > 0 for any alpha_floor < opacity (else lthr >= 0: never passes)
   if (!(L > 0.0f) || !(opacity > 0.0)) {   // nothing can pass: keep the fast path, never passes
-    f.pthr = __int_as_float(0x7f800000);
-    f.ek1 = f.ek0 = 0.f; f.flo = f.fhi = (float)alpha_floor;
+    f.flo = f.fhi = __int_as_float(0x7f800000);
+    f.ek1 = f.ek0 = 0.f;
     return f;
   }
   const bool pd = c0 > 0.0 && c2 > 0.0 && c0 * c2 - c1 * c1 > 0.0 && ca > 0.0 && cc > 0.0 && fabs(c1) < sqrt(c0 * c2) &&
                   isfinite(mx) && isfinite(my) && isfinite(c0) && isfinite(c1) && isfinite(c2) &&
                   isfinite(ca) && isfinite(cc);
-  // Error of the float32 power on R = {power64 >= lthr - 1} = {d^T C d <= Q},
-  // C = [[c0, c1], [c1, c2]], Q = 2 (L + 1):
+  // Error of the float32 quadratic form on R = {power64 >= lthr - 1} = {d^T C d <= Q},
+  // C = [[c0, c1], [c1, c2]], Q = 2 (L + 1), in natural-log units:
   //  * rounding (coefficients, two products, two fmas): <= 4u S(d),
   //    S(d) = 0.5 c0 dx^2 + |c1 dx dy| + 0.5 c2 dy^2 = 0.5 d^T |C| d (|C|: |c1|);
   //  * offsets: |dx32 - dx| <= 2u |dx| + u |mxl| (dx = (sx - mxh) - mxl), so
@@ -144,6 +151,8 @@ __device__ __forceinline__ FastRec make_fast_rec(double mx, double my, double c0
   //  * max of S on R: 0.5 Q lambda_max(|C|, C) = 0.5 Q (1 + rho) / (1 - rho),
   //    rho = |c1| / sqrt(c0 c2) (the generalized eigenvalue of the pair).
   // Thin, edge-on splats (rho -> 1) exceed kFastMaxDp and are flagged.
+  // The L2o term adds its own rounding and two roundings of sums that contain
+  // it: <= 3u |L2o| (log2 units).
   const float Q = 2.0f * (L + 1.0f) * 1.0001f;
   const double rho = fabs(c1) / sqrt(c0 * c2);
   const float ratio = (float)((1.0 + rho) / (1.0 - rho)) * 1.0001f;   // max of S(d) / |power(d)|
@@ -156,22 +165,23 @@ __device__ __forceinline__ FastRec make_fast_rec(double mx, double my, double c0
   const float dp = 1.25f * (8.0f * u * Smax + lo_terms) + 1e-9f;
   if (!pd || !(dp <= kFastMaxDp)) {
     exact = true;
-    f.pthr = lthr;
-    f.ek1 = f.ek0 = 0.f; f.flo = f.fhi = (float)alpha_floor;
+    f.flo = lthr;
+    f.fhi = f.ek1 = f.ek0 = 0.f;
     return f;
   }
-  f.pthr = __fsub_rd(lthr, dp);
-  // alpha32 = of * ex2(power32 * log2e): relative error <= (e^dp - 1) + argument
-  // rounding (log2e and the product: 2u |power| * ln2 * log2e) + ex2 + 2u
-  const float pmax = L + dp + 1.0f;
-  const float eps = 1.01f * (dp * (1.0f + dp) + 2.0f * u * pmax + kEx2RelErr + 3.0f * u);
-  f.flo = __fmul_rd((float)alpha_floor, 1.0f - eps - 2.0f * u);
-  f.fhi = __fmul_ru((float)alpha_floor, 1.0f + eps + 2.0f * u);
-  // per fragment: |power32 - power64| <= 10u S(d) + lo_terms, S(d) <= ratio |power_real|,
-  // |power_real| <= |power32| + dp; so eps(d) <= ek1 |power32| + ek0
-  const float k8 = 1.01f * (1.0f + dp) * 10.0f * u * ratio;
-  f.ek1 = k8 + 2.02f * u;
-  f.ek0 = k8 * dp + 1.01f * (1.0f + dp) * (lo_terms + 1e-9f) + 2.02f * u * dp + 1.01f * (kEx2RelErr + 3.0f * u);
+  // |P32 - P| on R, log2 units (the reference's own float64 rounding of
+  // o * exp(power) is ~1e-16: inside the 1e-9 slack)
+  const float l2o_err = 3.03f * u * fabsf(f.L2o);
+  const float dP = 1.01f * ((float)kLog2e * dp + l2o_err) + 1e-9f;
+  const double F = log2(alpha_floor);
+  f.flo = __double2float_rd(F - (double)dP);
+  f.fhi = __double2float_ru(F + (double)dP);
+  // per fragment, |alpha32 / alpha - 1| <= ln2 dP(d) (1 + dP) + ex2 error, with
+  // dP(d) <= log2e (10u S(d) + lo_terms) + l2o_err, S(d) <= ratio |power|,
+  // |power| <= ln2 (|P32 - L2o| + dP): eps(d) <= ek1 |P32 - L2o| + ek0
+  const float k10 = 1.01f * (1.0f + dP) * 10.0f * u * ratio * kLn2;
+  f.ek1 = k10 + 2.02f * u;
+  f.ek0 = k10 * dP + 1.01f * (1.0f + dP) * (lo_terms + kLn2 * l2o_err + 1e-9f) + 1.01f * (kEx2RelErr + 3.0f * u);
   return f;
 }
 
@@ -231,6 +241,9 @@ struct DevStats {     // device mirror of cs_frame_stats + scratch counters
   int64_t blend_floor_resolved;   // ... alpha-floor tests re-decided in float64
   int64_t blend_replays;          // ... transmittance replays
   int64_t pairs_eff;     // pairs actually processed (0 when the pair buffer overflowed)
+  int64_t pairs_sort;    // pairs the global tile sort processes (0 on the tile-local path)
+  int32_t tl_mode;       // 1: tile-local binning (cs_tiles.cu) took this frame
+  uint32_t tl_nq[3];     // tile-local size-class queue lengths
   uint32_t tickets[16];  // chunk tickets for single-pass kernels, zeroed per frame
 };
 

@@ -73,6 +73,13 @@ template <typename K> struct SortCfg;
 template <> struct SortCfg<uint64_t> { static constexpr int kItems = 8, kMinBlocks = 1; };
 template <> struct SortCfg<uint32_t> { static constexpr int kItems = 16, kMinBlocks = 3; };
 
+// Digit counts of every pass in one read of the keys.  Keys that arrive in
+// assembled order are spatially coherent (the depth key's top digits repeat
+// for long stretches), so each thread counts a run of 8 consecutive keys and
+// adds each run of equal digits with one shared atomic: a hot bin is not hit
+// by every lane of every warp.  (match.any-aggregation measured slower: its
+// latency sits on every key.)
+constexpr int kHistRun = 8;
 template <typename K>
 __global__ void __launch_bounds__(kSortThreads)
 k_radix_hist(const K* __restrict__ keys, const int64_t* __restrict__ n_ptr, int begin_bit,
@@ -81,13 +88,39 @@ k_radix_hist(const K* __restrict__ keys, const int64_t* __restrict__ n_ptr, int 
   for (int i = threadIdx.x; i < n_passes * 256; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   const int64_t n = *n_ptr;
+  const int64_t groups = (n + kHistRun - 1) / kHistRun;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
-    const K k = keys[i];
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < groups; g += stride) {
+    const int64_t i0 = g * kHistRun;
+    K k[kHistRun];
+    int cnt = kHistRun;
+    if (sizeof(K) == 4 && i0 + kHistRun <= n) {
+      const uint4* q = reinterpret_cast<const uint4*>(keys + i0);
+      const uint4 a = q[0], b = q[1];
+      k[0] = (K)a.x; k[1] = (K)a.y; k[2] = (K)a.z; k[3] = (K)a.w;
+      k[4] = (K)b.x; k[5] = (K)b.y; k[6] = (K)b.z; k[7] = (K)b.w;
+    } else {
+      cnt = (int)(n - i0 < kHistRun ? n - i0 : kHistRun);
+#pragma unroll
+      for (int j = 0; j < kHistRun; ++j) k[j] = j < cnt ? keys[i0 + j] : K(0);
+    }
     for (int p = 0; p < n_passes; ++p) {
       const int sh_p = begin_bit + width * p;
       const uint32_t m = (1u << min(width, end_bit - sh_p)) - 1u;
-      atomicAdd(&sh[p * 256 + ((uint32_t)(k >> sh_p) & m)], 1u);
+      uint32_t cur = (uint32_t)(k[0] >> sh_p) & m, run = 1;
+#pragma unroll
+      for (int j = 1; j < kHistRun; ++j) {
+        if (j >= cnt) break;
+        const uint32_t d = (uint32_t)(k[j] >> sh_p) & m;
+        if (d == cur) {
+          ++run;
+        } else {
+          atomicAdd(&sh[p * 256 + cur], run);
+          cur = d;
+          run = 1;
+        }
+      }
+      atomicAdd(&sh[p * 256 + cur], run);
     }
   }
   __syncthreads();
