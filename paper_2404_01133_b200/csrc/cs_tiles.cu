@@ -459,13 +459,11 @@ int64_t tl_words(int n_tiles) {
 }
 
 bool tile_local_enabled(int n_tiles) {
-  static int v = -1;
-  if (v < 0) {
-    // opt-in while its kernels are slower than the global path (CS_TILE_LOCAL=1)
-    const char* e = getenv("CS_TILE_LOCAL");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1 && n_tiles <= kTLMaxTiles;
+  // opt-in while its kernels are slower than the global path (CS_TILE_LOCAL=1);
+  // read per frame (direct frames follow changes; a cached frame graph keeps
+  // the binning it was captured with)
+  const char* e = getenv("CS_TILE_LOCAL");
+  return e && e[0] == '1' && n_tiles <= kTLMaxTiles;
 }
 
 struct TLLayout {

@@ -13,9 +13,11 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-# the tile-local path is opt-in (CS_TILE_LOCAL=1, read once per process): these
-# tests run it in a subprocess-free way by enabling it before the library loads
-os.environ.setdefault("CS_TILE_LOCAL", "1")
+
+@pytest.fixture(autouse=True)
+def _tile_local_on(monkeypatch):
+    """The tile-local path is opt-in (CS_TILE_LOCAL=1, read per frame)."""
+    monkeypatch.setenv("CS_TILE_LOCAL", "1")
 
 
 @pytest.fixture(scope="module")
