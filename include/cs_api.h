@@ -239,13 +239,6 @@ int cs_frame_stats_get(cs_ctx* ctx, cs_frame_stats* out, void* stream);
  * silent: it fails the frame's next call at the latest. */
 int cs_check(cs_ctx* ctx, void* stream);
 
-/* Which binning built the last frame's tile lists (synchronises the stream):
- * 1 = tile-local (per-tile counts, slots and shared-memory sorts of depth
- * ranks, cs_tiles.cu), 0 = global (pairs emitted in depth order + stable
- * radix sort by tile).  Both produce render._bin_tiles' lists
- * (render.py:217-249); diagnostics and tests only. */
-int cs_binning_path(cs_ctx* ctx, int32_t* path, void* stream);
-
 /* Golden-intermediate dumps of the last frame, host destinations.
  * cs_dump_projected mirrors render._Projected (render.py:89-108): arrays in
  * depth order; source = index into the assembled cloud.

@@ -96,7 +96,6 @@ _SIGS = {
                                  ctypes.POINTER(CsFrameStats), vp]),
     "cs_frame_stats_get": (ctypes.c_int, [vp, ctypes.POINTER(CsFrameStats), vp]),
     "cs_check": (ctypes.c_int, [vp, vp]),
-    "cs_binning_path": (ctypes.c_int, [vp, vp, vp]),
     "cs_render_train": (ctypes.c_int, [vp, ctypes.POINTER(CsSource), ctypes.POINTER(CsCamera),
                                        ctypes.POINTER(CsSettings), vp, ctypes.c_uint32, ctypes.POINTER(vp),
                                        vp]),

@@ -79,17 +79,6 @@ void launch_bin_pairs(const uint32_t* order, const uint2* rects, DevStats* stats
 void launch_tile_ranges(const uint32_t* keys, const uint32_t* vals, const short4* boxes,
                         const int64_t* n_pairs, uint2* ranges, uint32_t* bxs, uint32_t* bys,
                         cudaStream_t s);
-// cs_tiles.cu
-int64_t tl_words(int n_tiles);
-bool tile_local_enabled(int n_tiles);
-void launch_tl_count_scan(const uint32_t* order, const uint2* rects, DevStats* stats, int ntx, int n_tiles,
-                          uint32_t* tl, int64_t pair_cap, uint2* ranges, bool emit, int64_t* host_overflow,
-                          cudaStream_t s);
-void launch_tl_scatter(const uint32_t* order, const uint2* rects, DevStats* stats, int ntx, int n_tiles,
-                       uint32_t* tl, const uint2* ranges, uint32_t* slots, cudaStream_t s);
-void launch_tl_sort(const uint32_t* order, const uint2* boxes, DevStats* stats, int n_tiles, uint32_t* tl,
-                    const uint32_t* slots, const uint2* ranges, uint32_t* list, uint32_t* bxs, uint32_t* bys,
-                    cudaStream_t s);
 void launch_dump_projected(const uint32_t* order, const ProjRec* recs, const DevStats* stats,
                            double* means, double* conics, double* covs, double* depths,
                            double* colors, double* opac, double* radii, int64_t* src,
@@ -237,7 +226,7 @@ struct Ws {
   DBuf keysA, valsA, keysB, valsB, recs;
   DBuf k32A, k32B, long_runs, fix_ctl;          // K4 32-bit depth sort + K4b run fix-up
   DBuf hot, fast, boxes, rects, tile_order;
-  DBuf pkA, pvA, pkB, pvB, ranges, frag_tile, pw_list, tl;
+  DBuf pkA, pvA, pkB, pvB, ranges, frag_tile, pw_list;
   DBuf st_t, st_last, st_acc;
   int64_t cap_vis = 0, cap_pairs = 0, cap_pw = 0, cap_tiles = 0;
   bool held = false;  // owned by a cs_state
@@ -254,7 +243,7 @@ struct Ws {
     DBuf* all[] = {&stats, &clouds1, &segs, &dec, &st_gather, &st_pw, &st_sort, &hist, &sort_tickets,
                    &keysA, &valsA, &keysB, &valsB, &recs, &k32A, &k32B, &long_runs, &fix_ctl, &hot,
                    &fast, &boxes, &rects, &tile_order, &pkA, &pvA, &pkB, &pvB, &ranges, &frag_tile, &pw_list,
-                   &tl, &st_t, &st_last, &st_acc};
+                   &st_t, &st_last, &st_acc};
     for (DBuf* b : all) b->release();
   }
 };
@@ -507,7 +496,6 @@ static int ensure_frame_buffers(Ws* w, int64_t cap_vis, int n_segs, int n_blocks
   if (w->st_sort.ensure(4 * sw)) return fail(CS_ENOMEM, "sort status");
   if (n_tiles > w->cap_tiles) {
     if (w->ranges.ensure(sizeof(uint2) * n_tiles) || w->frag_tile.ensure(4 * n_tiles) ||
-        w->tl.ensure(4 * tl_words(n_tiles)) ||
         w->tile_order.ensure(4 * (n_tiles + 2 * 34 * 16)))  // + launch_tile_order's scratch
       return fail(CS_ENOMEM, "tile buffers");
     w->cap_tiles = n_tiles;
@@ -634,18 +622,11 @@ static int render_once(cs_ctx* c, Ws* w, const cs_source* src, const cs_camera* 
                         w->keysB.as<uint32_t>(), s);
   CS_CHECK_LAUNCH();
   if (timed) mark(c, 3, s);
-  // Binning.  Tile-local path (cs_tiles.cu): TL1+TL2 count the pairs per
-  // tile and decide on the device whether every tile fits the per-tile sort;
-  // the kernels of the path not taken return at once.
-  const bool project_only = (flags & CS_RENDER_PROJECT_ONLY) != 0;
-  const bool tl = tile_local_enabled(n_tiles) && !project_only;
-  if (tl)
-    launch_tl_count_scan(order, w->rects.as<uint2>(), stats, ntx, n_tiles, w->tl.as<uint32_t>(), w->cap_pairs,
-                         w->ranges.as<uint2>(), true, c->d_overflow, s);
-  // K5+K6 (global path): pair counts in depth order, scanned, and the pairs
-  // emitted in one pass (also counts the tile sort's digit histograms, so K7
-  // skips its counting pass)
+  // K5+K6: pair counts in depth order, scanned, and the pairs emitted in one
+  // pass (also counts the tile sort's digit histograms, so K7 skips its
+  // counting pass)
   CS_CUDA(cudaMemsetAsync(w->st_gather.p, 0, 8 * (bin_chunks(cap) + 1), s));
+  const bool project_only = (flags & CS_RENDER_PROJECT_ONLY) != 0;
   launch_bin_pairs(order, w->rects.as<uint2>(), stats, w->cap_pairs, cap,
                    w->st_gather.as<uint64_t>(), ntx, w->pkA.as<uint32_t>(), w->pvA.as<uint32_t>(),
                    bits_for(n_tiles) <= 24 ? w->hist.as<uint32_t>() : nullptr, bits_for(n_tiles),
@@ -659,31 +640,22 @@ static int render_once(cs_ctx* c, Ws* w, const cs_source* src, const cs_camera* 
   }
   mark(c, 5, s);
   // K7: stable sort by tile id only (ceil(log2 T) bits)
-  const int64_t* n_sort = tl ? &stats->pairs_sort : &stats->pairs_eff;
   const int which2 = radix_sort<uint32_t>(w->pkA.as<uint32_t>(), w->pvA.as<uint32_t>(),
                                           w->pkB.as<uint32_t>(), w->pvB.as<uint32_t>(),
-                                          n_sort, w->cap_pairs, 0, bits_for(n_tiles),
+                                          &stats->pairs_eff, w->cap_pairs, 0, bits_for(n_tiles),
                                           w->hist.as<uint32_t>(), w->st_sort.as<uint32_t>(),
                                           w->sort_tickets.as<uint32_t>() + 8, s,
                                           /*hist_ready=*/bits_for(n_tiles) <= 24);
   CS_CHECK_LAUNCH();
-  uint32_t* tkeys = which2 ? w->pkB.as<uint32_t>() : w->pkA.as<uint32_t>();
-  uint32_t* tvals = which2 ? w->pvB.as<uint32_t>() : w->pvA.as<uint32_t>();
+  const uint32_t* tkeys = which2 ? w->pkB.as<uint32_t>() : w->pkA.as<uint32_t>();
+  const uint32_t* tvals = which2 ? w->pvB.as<uint32_t>() : w->pvA.as<uint32_t>();
+  mark(c, 6, s);
+  // K8: tile ranges
+  CS_CUDA(cudaMemsetAsync(w->ranges.p, 0, sizeof(uint2) * n_tiles, s));
   // the sort's other (key, value) buffers are free now: they take the pair-major boxes
   uint32_t* bxs = which2 ? w->pkA.as<uint32_t>() : w->pkB.as<uint32_t>();
   uint32_t* bys = which2 ? w->pvA.as<uint32_t>() : w->pvB.as<uint32_t>();
-  // TL3: tile-local slots (ranks) into the sorted-keys buffer, unused on that path
-  if (tl)
-    launch_tl_scatter(order, w->rects.as<uint2>(), stats, ntx, n_tiles, w->tl.as<uint32_t>(), w->ranges.as<uint2>(),
-                      tkeys, s);
-  mark(c, 6, s);
-  // K8: tile ranges (TL2 already wrote them on either path)
-  if (!tl) CS_CUDA(cudaMemsetAsync(w->ranges.p, 0, sizeof(uint2) * n_tiles, s));
-  launch_tile_ranges(tkeys, tvals, w->boxes.as<short4>(), n_sort, w->ranges.as<uint2>(), bxs, bys, s);
-  // TL4: per-tile sorts -> the same (list, boxes) arrays
-  if (tl)
-    launch_tl_sort(order, reinterpret_cast<const uint2*>(w->boxes.as<short4>()), stats, n_tiles,
-                   w->tl.as<uint32_t>(), tkeys, w->ranges.as<uint2>(), tvals, bxs, bys, s);
+  launch_tile_ranges(tkeys, tvals, w->boxes.as<short4>(), &stats->pairs_eff, w->ranges.as<uint2>(), bxs, bys, s);
   CS_CHECK_LAUNCH();
   mark(c, 7, s);
   // K9: blend
@@ -1053,17 +1025,6 @@ int cs_check(cs_ctx* c, void* stream) {
   CS_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
   std::lock_guard<std::mutex> lock(c->mu);
   return check_overflow(c);
-}
-
-int cs_binning_path(cs_ctx* c, int32_t* path, void* stream) {
-  if (!c || !path) return fail(CS_EINVAL, "NULL argument");
-  std::lock_guard<std::mutex> lock(c->mu);
-  if (!c->last) return fail(CS_EINVAL, "no frame rendered on this context");
-  CS_CUDA(cudaSetDevice(c->device));
-  CS_CUDA(cudaMemcpyAsync(path, &c->last->stats.as<DevStats>()->tl_mode, sizeof(int32_t),
-                          cudaMemcpyDeviceToHost, (cudaStream_t)stream));
-  CS_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
-  return CS_OK;
 }
 
 int cs_training_loss(cs_ctx* c, const float* img, const float* ref, int32_t height, int32_t width,

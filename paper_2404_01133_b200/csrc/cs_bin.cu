@@ -169,7 +169,6 @@ k_bin_pairs(const uint32_t* __restrict__ order, const uint2* __restrict__ rects,
   __shared__ BinSmem sm;
   __shared__ uint64_t s_prefix;
   __shared__ uint32_t s_chunk;
-  if (stats->tl_mode == 1) return;  // the tile-local path (cs_tiles.cu) bins this frame
   const int64_t M = stats->visible;
   for (int i = threadIdx.x; i < dh.n_passes * 256; i += kBinThreads) sm.hist[i >> 8][i & 255] = 0;
   // CS_BIN_PERSIST: one wave of CTAs looping over chunk tickets (the grid is
@@ -233,7 +232,6 @@ k_emit_heavy(const uint32_t* __restrict__ order, const uint2* __restrict__ rects
              uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, DigitHist dh) {
   __shared__ BinSmem sm;
   __shared__ uint32_t s_t[2];  // double-buffered ticket: thread 0 writes the next while others read this one
-  if (stats->tl_mode == 1) return;
   const unsigned long long hc = *reinterpret_cast<const unsigned long long*>(&stats->tickets[8]);
   const uint32_t n_entries = (uint32_t)(hc >> 32), n_slices = (uint32_t)hc;
   if (n_slices == 0) return;

@@ -241,9 +241,6 @@ struct DevStats {     // device mirror of cs_frame_stats + scratch counters
   int64_t blend_floor_resolved;   // ... alpha-floor tests re-decided in float64
   int64_t blend_replays;          // ... transmittance replays
   int64_t pairs_eff;     // pairs actually processed (0 when the pair buffer overflowed)
-  int64_t pairs_sort;    // pairs the global tile sort processes (0 on the tile-local path)
-  int32_t tl_mode;       // 1: tile-local binning (cs_tiles.cu) took this frame
-  uint32_t tl_nq[3];     // tile-local size-class queue lengths
   uint32_t tickets[16];  // chunk tickets for single-pass kernels, zeroed per frame
 };
 

@@ -217,15 +217,6 @@ def bin_tiles_last(cam, tile_size: int, dev_index: Optional[int] = None):
     return tids[:int(st.pairs)], offs
 
 
-def binning_path_last(dev_index: Optional[int] = None) -> str:
-    """'tile_local' or 'global': which binning built this thread's last frame
-    (cs_binning_path; diagnostics and tests)."""
-    dev_index = device._device_index(dev_index)
-    v = ctypes.c_int32(-1)
-    _check(_lib.load().cs_binning_path(device.context(dev_index), ctypes.byref(v), device.stream_handle()))
-    return "tile_local" if v.value == 1 else "global"
-
-
 def project_gaussian(g, cam, settings: Optional[RenderSettings] = None,
                      source_index: int = 0) -> Optional[SplatPrimitive]:
     """render.project_gaussian (render.py:191-214): None when culled."""
