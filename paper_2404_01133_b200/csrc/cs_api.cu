@@ -48,7 +48,7 @@ size_t radix_status_words(int64_t capacity, int key_bytes);
 template <typename K>
 int radix_sort(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_dev, int64_t capacity,
                int begin_bit, int end_bit, uint32_t* hist, uint32_t* status, uint32_t* tickets,
-               cudaStream_t s, bool hist_ready = false);
+               cudaStream_t s, bool hist_ready = false, bool identity_vals = false);
 // cs_depth.cu
 void launch_fix_depth_runs(const uint32_t* k32_sorted, uint32_t* order, const uint64_t* k64,
                            const DevStats* stats, int64_t capacity, void* ctl_mem,
@@ -601,7 +601,7 @@ static int render_once(cs_ctx* c, Ws* w, const cs_source* src, const cs_camera* 
                  w->hot.as<HotRec>(), fast_blend ? w->fast.as<FastRec>() : nullptr,
                  w->rects.as<uint2>(), w->boxes.as<short4>(),
                  debug ? w->recs.as<ProjRec>() : nullptr,
-                 src->kind == CS_SRC_CLOUD ? src->exclude : nullptr};
+                 src->kind == CS_SRC_CLOUD ? src->exclude : nullptr, std::log2(st->alpha_floor)};
   launch_project(clouds, w->segs.as<Seg>(), stats, *cam, *st, cap, po, list, s);
   w->last_debug = debug;
   CS_CHECK_LAUNCH();
@@ -613,7 +613,8 @@ static int render_once(cs_ctx* c, Ws* w, const cs_source* src, const cs_camera* 
   const int which = radix_sort<uint32_t>(w->k32A.as<uint32_t>(), w->valsA.as<uint32_t>(),
                                          w->k32B.as<uint32_t>(), w->valsB.as<uint32_t>(),
                                          &stats->assembled, cap, 0, 32, w->hist.as<uint32_t>(),
-                                         w->st_sort.as<uint32_t>(), w->sort_tickets.as<uint32_t>(), s);
+                                         w->st_sort.as<uint32_t>(), w->sort_tickets.as<uint32_t>(), s, false,
+                                         /*identity_vals=*/true);
   CS_CHECK_LAUNCH();
   uint32_t* order = which ? w->valsB.as<uint32_t>() : w->valsA.as<uint32_t>();
   const uint32_t* k32s = which ? w->k32B.as<uint32_t>() : w->k32A.as<uint32_t>();

@@ -117,7 +117,7 @@ constexpr float kEx2RelErr = 4.0e-7f;
 // |dx| <= sqrt(2 (L + 1) ca), |dy| <= sqrt(2 (L + 1) cc).
 __device__ __forceinline__ FastRec make_fast_rec(double mx, double my, double c0, double c1, double c2,
                                                  double opacity, float lthr, float r, float g, float b,
-                                                 double ca, double cc, double alpha_floor, bool& exact) {
+                                                 double ca, double cc, double log2_afl, bool& exact) {
   constexpr float u = 5.9604645e-8f;  // 2^-24
   constexpr double kLog2e = 1.4426950408889634;
   constexpr float kLn2 = 0.69314718f;
@@ -129,7 +129,9 @@ __device__ __forceinline__ FastRec make_fast_rec(double mx, double my, double c0
   f.A = (float)(-0.5 * kLog2e * c0);
   f.B = (float)(-kLog2e * c1);
   f.C = (float)(-0.5 * kLog2e * c2);
-  f.L2o = opacity > 0.0 ? (float)log2(opacity) : 0.0f;
+  // float log2 of the float opacity: |L2o - log2(o)| <= log2(e) u (opacity
+  // rounding) + 2u |L2o| (log2f, <= 1 ulp), in l2o_err below
+  f.L2o = opacity > 0.0 ? log2f((float)opacity) : 0.0f;
   f.r = r; f.g = g; f.b = b; f.pad = 0.f;
   exact = false;
   const float L = -lthr;  // > 0 for any alpha_floor < opacity (else lthr >= 0: never passes)
@@ -138,7 +140,8 @@ __device__ __forceinline__ FastRec make_fast_rec(double mx, double my, double c0
     f.ek1 = f.ek0 = 0.f;
     return f;
   }
-  const bool pd = c0 > 0.0 && c2 > 0.0 && c0 * c2 - c1 * c1 > 0.0 && ca > 0.0 && cc > 0.0 && fabs(c1) < sqrt(c0 * c2) &&
+  const double det = c0 * c2 - c1 * c1;   // > 0 <=> |c1| < sqrt(c0 c2)
+  const bool pd = c0 > 0.0 && c2 > 0.0 && det > 0.0 && ca > 0.0 && cc > 0.0 &&
                   isfinite(mx) && isfinite(my) && isfinite(c0) && isfinite(c1) && isfinite(c2) &&
                   isfinite(ca) && isfinite(cc);
   // Error of the float32 quadratic form on R = {power64 >= lthr - 1} = {d^T C d <= Q},
@@ -154,8 +157,11 @@ __device__ __forceinline__ FastRec make_fast_rec(double mx, double my, double c0
   // The L2o term adds its own rounding and two roundings of sums that contain
   // it: <= 3u |L2o| (log2 units).
   const float Q = 2.0f * (L + 1.0f) * 1.0001f;
-  const double rho = fabs(c1) / sqrt(c0 * c2);
-  const float ratio = (float)((1.0 + rho) / (1.0 - rho)) * 1.0001f;   // max of S(d) / |power(d)|
+  // max of S(d) / |power(d)|: (1 + rho) / (1 - rho) = (s + |c1|)^2 / det, s = sqrt(c0 c2),
+  // in float (relative error < 1e-6 while det / (c0 c2) > 1e-6; below that the
+  // ratio exceeds 4e6 and dp flags the splat whatever the rounding)
+  const float sq = sqrtf((float)(c0 * c2)) + fabsf((float)c1);
+  const float ratio = __fdiv_ru(sq * sq, (float)det) * 1.0002f;
   const float Smax = 0.5f * Q * ratio;
   const float DX = sqrtf(Q * (float)ca) * 1.0001f + 1e-3f;   // |dx| on R
   const float DY = sqrtf(Q * (float)cc) * 1.0001f + 1e-3f;
@@ -171,9 +177,9 @@ __device__ __forceinline__ FastRec make_fast_rec(double mx, double my, double c0
   }
   // |P32 - P| on R, log2 units (the reference's own float64 rounding of
   // o * exp(power) is ~1e-16: inside the 1e-9 slack)
-  const float l2o_err = 3.03f * u * fabsf(f.L2o);
+  const float l2o_err = 1.01f * (1.4426950f * u + 4.0f * u * fabsf(f.L2o));
   const float dP = 1.01f * ((float)kLog2e * dp + l2o_err) + 1e-9f;
-  const double F = log2(alpha_floor);
+  const double F = log2_afl;
   f.flo = __double2float_rd(F - (double)dP);
   f.fhi = __double2float_ru(F + (double)dP);
   // per fragment, |alpha32 / alpha - 1| <= ln2 dP(d) (1 + dP) + ex2 error, with
@@ -266,6 +272,7 @@ struct ProjOutputs {
   short4* boxes;     // copy of HotRec's cull box, dense (8 B)
   ProjRec* recs;     // optional (debug / dumps)
   const uint8_t* exclude;  // input, optional: rows culled as if absent (assignment renders)
+  double log2_afl;         // log2(alpha_floor) (the FastRec floor thresholds), set by the host
 };
 
 // LoD scene tables on device (cs_lod.cu)

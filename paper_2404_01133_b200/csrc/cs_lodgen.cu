@@ -33,7 +33,7 @@ void launch_significance(const cs_cloud& cl, const cs_camera* cams, int n_cams,
 template <typename K>
 int radix_sort(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_dev, int64_t capacity,
                int begin_bit, int end_bit, uint32_t* hist, uint32_t* status, uint32_t* tickets,
-               cudaStream_t s, bool hist_ready = false);
+               cudaStream_t s, bool hist_ready = false, bool identity_vals = false);
 
 static inline unsigned grid_for(int64_t n, int threads, int cap = 148 * 16) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, cap));

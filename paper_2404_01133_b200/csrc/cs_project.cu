@@ -307,7 +307,7 @@ __device__ __forceinline__ void project_emit(int64_t i, const Geom& g, const Pro
     const uint64_t code = (zb - nb) >> 24;
     po_out.keys32[i] = po.keep ? (uint32_t)min(code, (uint64_t)0xfffffffeu) : 0xffffffffu;
   }
-  po_out.vals[i] = (uint32_t)i;
+  // (no id array: the depth sort's first pass takes the identity as its values)
   if (!po.keep) return;
   const int64_t idx = i;
   // view direction and SH colour (render.py:167-169, core.py:166-172)
@@ -366,7 +366,7 @@ __device__ __forceinline__ void project_emit(int64_t i, const Geom& g, const Pro
   if (po_out.fast) {
     bool exact;
     const FastRec f = make_fast_rec(po.mx, po.my, c0, c1, c2, g.op, lthr, h.r, h.g, h.b, po.a, po.c,
-                                    st.alpha_floor, exact);
+                                    po_out.log2_afl, exact);
     po_out.fast[idx] = f;
     if (exact) box.x = (int16_t)kBoxExact;
   }

@@ -156,7 +156,7 @@ __global__ void k_radix_hist_scan(uint32_t* hist, int n_passes, uint32_t* __rest
 // The pass body, FULL = the chunk holds kTile keys (no bounds checks, the
 // common case), NB = digit width (ballot count known at compile time).
 // Indices are 32-bit (n < 2^31).
-template <typename K, int ITEMS, bool FULL, int NB, bool EARLY>
+template <typename K, int ITEMS, bool FULL, int NB, bool EARLY, bool IDV>
 __device__ __forceinline__ void onesweep_body(
     const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, K* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, uint32_t n, uint32_t chunk, int shift,
@@ -178,7 +178,7 @@ __device__ __forceinline__ void onesweep_body(
     const uint32_t idx = wbase + r * 32 + lane;
     if (FULL || idx < n) {
       key[r] = keys_in[idx];
-      val[r] = vals_in[idx];
+      val[r] = IDV ? idx : vals_in[idx];  // IDV: the identity as input values (first depth pass)
     }
   }
   // 1) EARLY: chunk histogram first, published immediately so successors'
@@ -298,7 +298,8 @@ __device__ __forceinline__ void onesweep_body(
 #define CS_SORT_PERSIST 1
 #endif
 
-template <typename K, int ITEMS = SortCfg<K>::kItems, int MINB = 1, int NB = 8, bool EARLY = true>
+template <typename K, int ITEMS = SortCfg<K>::kItems, int MINB = 1, int NB = 8, bool EARLY = true,
+          bool IDV = false>
 __global__ void __launch_bounds__(kSortThreads, MINB)
 k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
            K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
@@ -332,11 +333,11 @@ k_onesweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     const uint64_t base = (uint64_t)chunk * kTile;
     if (base >= n) return;
     if (base + kTile <= n)
-      onesweep_body<K, ITEMS, true, NB, EARLY>(keys_in, vals_in, keys_out, vals_out, n, chunk, shift,
+      onesweep_body<K, ITEMS, true, NB, EARLY, IDV>(keys_in, vals_in, keys_out, vals_out, n, chunk, shift,
                                                digit_base, status, warp_hist, chunk_hist, digit_off,
                                                gbase, scratch, keys_s, vals_s);
     else
-      onesweep_body<K, ITEMS, false, NB, EARLY>(keys_in, vals_in, keys_out, vals_out, n, chunk, shift,
+      onesweep_body<K, ITEMS, false, NB, EARLY, IDV>(keys_in, vals_in, keys_out, vals_out, n, chunk, shift,
                                                 digit_base, status, warp_hist, chunk_hist, digit_off,
                                                 gbase, scratch, keys_s, vals_s);
     if (!CS_SORT_PERSIST) return;
@@ -354,37 +355,39 @@ size_t radix_status_words(int64_t capacity, int key_bytes) {
 // Sorts (keys, vals) of length *n_dev (<= capacity) by bits [begin_bit, end_bit).
 // Ping-pongs between (k0,v0) and (k1,v1); returns 1 when the result is in
 // (k1,v1), 0 when in (k0,v0).
-template <typename K, int ITEMS, int MINB, int NB, bool EARLY>
+template <typename K, int ITEMS, int MINB, int NB, bool EARLY, bool IDV = false>
 static void launch_pass(unsigned chunks, cudaStream_t s, const K* kin, const uint32_t* vin, K* kout,
                         uint32_t* vout, const int64_t* n_dev, int shift, const uint32_t* hist,
                         uint32_t* status, int pass, uint32_t* ticket) {
   static bool carveout = false;  // shared memory is the occupancy limit: take all of it
   if (!carveout) {
-    cudaFuncSetAttribute(k_onesweep<K, ITEMS, MINB, NB, EARLY>,
+    cudaFuncSetAttribute(k_onesweep<K, ITEMS, MINB, NB, EARLY, IDV>,
                          cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     carveout = true;
   }
   static int wave = 0;  // resident CTAs of this instantiation on the whole GPU
   if (!wave) {
     int per_sm = 0, dev = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_onesweep<K, ITEMS, MINB, NB, EARLY>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_onesweep<K, ITEMS, MINB, NB, EARLY, IDV>,
                                                   kSortThreads, 0);
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     wave = std::max(1, per_sm * sms);
   }
   const unsigned g = CS_SORT_PERSIST ? std::min<unsigned>(chunks, (unsigned)wave) : chunks;
-  launch_pdl(k_onesweep<K, ITEMS, MINB, NB, EARLY>, g, kSortThreads, s, kin, vin, kout, vout, n_dev,
+  launch_pdl(k_onesweep<K, ITEMS, MINB, NB, EARLY, IDV>, g, kSortThreads, s, kin, vin, kout, vout, n_dev,
              shift, hist, status, pass, ticket);
 }
 
 template <typename K, int ITEMS, int MINB = SortCfg<K>::kMinBlocks, bool EARLY = true>
 int radix_sort_items(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_dev,
                      int64_t capacity, int begin_bit, int end_bit, uint32_t* hist,
-                     uint32_t* status, uint32_t* tickets, cudaStream_t s, bool hist_ready = false) {
+                     uint32_t* status, uint32_t* tickets, cudaStream_t s, bool hist_ready = false,
+                     bool identity_vals = false) {
   // equal-width digits of <= 8 bits (13 tile bits -> 7 + 6: fewer ballots per key)
   const int n_passes = (end_bit - begin_bit + 7) / 8;
   if (n_passes <= 0 || capacity <= 0) return 0;
+  if (identity_vals && (end_bit - begin_bit) % 8) return -1;  // identity values need 8-bit digits
   const int width = (end_bit - begin_bit + n_passes - 1) / n_passes;
   constexpr int kTile = kSortThreads * ITEMS;
   const int64_t chunks = (capacity + kTile - 1) / kTile;
@@ -401,18 +404,23 @@ int radix_sort_items(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_
   for (int p = 0; p < n_passes; ++p) {
     const int shift = begin_bit + width * p;
     const int nb = std::min(width, end_bit - shift);
+    // identity input values (first pass, 8-bit digits: the depth sort) are
+    // generated in the pass instead of read
+    const uint32_t* vsrc = (p == 0 && identity_vals) ? nullptr : vin;
     const unsigned g = (unsigned)chunks;
     uint32_t* tk = tickets + p;
     const uint32_t* hp = hist + 256 * p;
-    switch (nb) {
-      case 8: launch_pass<K, ITEMS, MINB, 8, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, p, tk); break;
-      case 7: launch_pass<K, ITEMS, MINB, 7, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, p, tk); break;
-      case 6: launch_pass<K, ITEMS, MINB, 6, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, p, tk); break;
-      case 5: launch_pass<K, ITEMS, MINB, 5, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, p, tk); break;
-      case 4: launch_pass<K, ITEMS, MINB, 4, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, p, tk); break;
-      case 3: launch_pass<K, ITEMS, MINB, 3, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, p, tk); break;
-      case 2: launch_pass<K, ITEMS, MINB, 2, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, p, tk); break;
-      default: launch_pass<K, ITEMS, MINB, 1, EARLY>(g, s, kin, vin, kout, vout, n_dev, shift, hp, status, p, tk); break;
+    if (!vsrc) {  // identity values (callers use 8-bit digits)
+      launch_pass<K, ITEMS, MINB, 8, EARLY, true>(g, s, kin, vsrc, kout, vout, n_dev, shift, hp, status, p, tk);
+    } else switch (nb) {
+      case 8: launch_pass<K, ITEMS, MINB, 8, EARLY>(g, s, kin, vsrc, kout, vout, n_dev, shift, hp, status, p, tk); break;
+      case 7: launch_pass<K, ITEMS, MINB, 7, EARLY>(g, s, kin, vsrc, kout, vout, n_dev, shift, hp, status, p, tk); break;
+      case 6: launch_pass<K, ITEMS, MINB, 6, EARLY>(g, s, kin, vsrc, kout, vout, n_dev, shift, hp, status, p, tk); break;
+      case 5: launch_pass<K, ITEMS, MINB, 5, EARLY>(g, s, kin, vsrc, kout, vout, n_dev, shift, hp, status, p, tk); break;
+      case 4: launch_pass<K, ITEMS, MINB, 4, EARLY>(g, s, kin, vsrc, kout, vout, n_dev, shift, hp, status, p, tk); break;
+      case 3: launch_pass<K, ITEMS, MINB, 3, EARLY>(g, s, kin, vsrc, kout, vout, n_dev, shift, hp, status, p, tk); break;
+      case 2: launch_pass<K, ITEMS, MINB, 2, EARLY>(g, s, kin, vsrc, kout, vout, n_dev, shift, hp, status, p, tk); break;
+      default: launch_pass<K, ITEMS, MINB, 1, EARLY>(g, s, kin, vsrc, kout, vout, n_dev, shift, hp, status, p, tk); break;
     }
     K* t0 = kin; kin = kout; kout = t0;
     uint32_t* t1 = vin; vin = vout; vout = t1;
@@ -423,16 +431,17 @@ int radix_sort_items(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_
 template <typename K>
 int radix_sort(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const int64_t* n_dev, int64_t capacity,
                int begin_bit, int end_bit, uint32_t* hist, uint32_t* status, uint32_t* tickets,
-               cudaStream_t s, bool hist_ready) {
+               cudaStream_t s, bool hist_ready, bool identity_vals) {
   return radix_sort_items<K, SortCfg<K>::kItems>(k0, v0, k1, v1, n_dev, capacity, begin_bit,
-                                                 end_bit, hist, status, tickets, s, hist_ready);
+                                                 end_bit, hist, status, tickets, s, hist_ready,
+                                                 identity_vals);
 }
 
 template int radix_sort<uint64_t>(uint64_t*, uint32_t*, uint64_t*, uint32_t*, const int64_t*,
                                   int64_t, int, int, uint32_t*, uint32_t*, uint32_t*, cudaStream_t,
-                                  bool);
+                                  bool, bool);
 template int radix_sort<uint32_t>(uint32_t*, uint32_t*, uint32_t*, uint32_t*, const int64_t*,
                                   int64_t, int, int, uint32_t*, uint32_t*, uint32_t*, cudaStream_t,
-                                  bool);
+                                  bool, bool);
 
 }  // namespace cs
