@@ -27,7 +27,7 @@
 //
 // Staging: 4 x 16-byte cp.async (LDGSTS) per record.  A cp.async.bulk per
 // record completing on a per-warp mbarrier was measured 23% slower (1.19 vs
-// 0.97 ms on C3, profiles/r2f_blend_ab.txt): the bulk copy takes uniform
+// 0.97 ms on C3, profiles/r2k_blend_ab.txt): the bulk copy takes uniform
 // operands, so a warp's scattered 64-byte records are issued one lane at a
 // time (ELECT loop), while one LDGSTS moves every hitting lane's chunk.
 //

@@ -124,3 +124,34 @@ def test_select_level_edges_oracle():
         dd = dec[0][3]
         expect = [2 - i for i, (a, b) in enumerate(ints) if a <= dd < b][0]
         assert dec[0][2] == expect
+
+
+def test_primitive_golden_vs_oracle():
+    """tests/golden/primitive.npz (the reference's project_gaussian,
+    render.py:191-214) against the oracle's projection of the same single
+    Gaussians: geometry bit-exact, culled cases absent."""
+    from pathlib import Path
+    from types import SimpleNamespace
+    z = np.load(Path(__file__).resolve().parent / "golden" / "primitive.npz")
+
+    class _Cam(SimpleNamespace):
+        pass
+    for i in range(len(z["culled"])):
+        row = z["cam"][i]
+        R = row[6:15].reshape(3, 3)
+        t = row[15:18]
+        cam = _Cam(width=int(row[0]), height=int(row[1]), fx=row[2], fy=row[3], cx=row[4], cy=row[5],
+                   rotation_w2c=R, translation_w2c=t, camera_center=-(R.T @ t))
+        cloud = SimpleNamespace(positions=z["pos"][i][None], opacities=np.array([z["op"][i]]),
+                                scales=z["scale"][i][None], rotations=z["rot"][i][None], sh=z["sh"][i][None])
+        st = O.DefaultSettings()
+        st.sh_degree = int(z["degree"][i])
+        p = O.project_cloud(cloud, cam, st)
+        if z["culled"][i]:
+            assert p["count"] == 0, i
+            continue
+        assert p["count"] == 1, i
+        assert np.array_equal(p["means"][0], z["mean2d"][i]), i
+        a, b, c = p["covs"][0]
+        assert np.array_equal(np.array([[a, b], [b, c]]), z["cov2d"][i]), i
+        assert p["depths"][0] == z["depth"][i], i
