@@ -371,6 +371,11 @@ __device__ __forceinline__ float4 lds128(uint32_t a) {
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
   return v;
 }
+__device__ __forceinline__ double lds64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ float lds32(uint32_t a) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
@@ -639,11 +644,25 @@ k_blend_fast(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs
           if ((fslot >> sl) & 1u) {  // warp-uniform: a flagged splat; float64 decides
             if (DIAG) n_exact += lane == 0;
             if (!__any_sync(0xffffffffu, live)) continue;
-            const HotRec& h = wrec[st_][sl].as_hot();
+            // the slot holds the splat's HotRec (mx my c0 c1 c2 opacity lthr r g b)
+            const uint32_t ra = rbase + (uint32_t)sl * (uint32_t)sizeof(FastRec);
+            const double dx = dsub((double)sx, lds64(ra)), dy = dsub((double)sy, lds64(ra + 8));
+            const double c0 = lds64(ra + 16), c1 = lds64(ra + 24), c2 = lds64(ra + 32);
+            const double power = dsub(dmul(-0.5, dadd(dmul(dmul(c0, dx), dx), dmul(dmul(c2, dy), dy))),
+                                      dmul(dmul(c1, dx), dy));      // _kernels.py:52-57
+            const bool pass = live && power >= (double)lds32(ra + 48);  // else alpha < alpha_floor
+            if (!__any_sync(0xffffffffu, pass)) continue;   // no lane reaches the floor
             double ad = 0.0;
-            if (live) ad = exact_alpha(h, (double)sx, (double)sy, s_exp, exp_coef_const());
-            const bool acc = live && ad >= bp.alpha_floor;
-            if (!apply(acc, (float)ad, 2.0f * u, h.r, h.g, h.b)) { frozen = sl; famb = false; }
+            if (pass) {
+              const ExpCoef ec = exp_coef_const();
+              ad = dmul(lds64(ra + 40), exp_le0(power, s_exp, ec));
+              ad = ad > ec.clamp ? ec.clamp : ad;
+            }
+            const bool acc = pass && ad >= bp.alpha_floor;
+            if (!__any_sync(0xffffffffu, acc)) continue;    // nothing accepted: no state changes
+            if (!apply(acc, (float)ad, 2.0f * u, lds32(ra + 52), lds32(ra + 56), lds32(ra + 60))) {
+              frozen = sl; famb = false;
+            }
             continue;
           }
           fast_hit(sl, live);
