@@ -566,17 +566,20 @@ k_blend_fast(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs
       const float en = fmaf(fmaf(eps, ac, 3.0f * u), rcp_approx(om), eT);
       const float band = fmaf(en, bp.tfl_b, bp.tfl_c);
       const float r = nt - bp.tfl;
-      const bool stop = acc && r < -band;          // the crossing fragment is dropped (_kernels.py:64-66)
-      const bool cont = acc && r >= band;          // _kernels.py:67-72
+      // |r| >= band: the float32 test is the reference's; inside the band the
+      // lane freezes (returns false) for a float64 replay
+      const bool sure = acc && !(fabsf(r) < band);
+      const bool cont = sure && r >= 0.0f;         // _kernels.py:67-72
+      const bool stop = sure && r < 0.0f;          // the crossing fragment is dropped (_kernels.py:64-66)
       const float wgt = cont ? T * ac : 0.0f;
       cr = fmaf(wgt, fr, cr);
       cg = fmaf(wgt, fg, cg);
       cb = fmaf(wgt, fb, cb);
       T = cont ? nt : T;
       eT = cont ? en : eT;
-      cnt += cont ? 1 : 0;
+      asm("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %1, 0;\n\t@p add.s32 %0, %0, 1;\n\t}" : "+r"(cnt) : "r"((int)cont));
       done = done || stop;
-      return !(acc && !stop && !cont);
+      return sure || !acc;
     };
     // The float32 evaluation of FastRec `ra` for this lane: P32 = log2 of the
     // unclamped alpha, and the alpha-floor pass (P32 >= Flo: may reach the floor).
