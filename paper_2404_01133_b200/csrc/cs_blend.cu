@@ -584,19 +584,21 @@ k_blend_fast(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs
     // The float32 evaluation of FastRec `ra` for this lane: P32 = log2 of the
     // unclamped alpha, and the alpha-floor pass (P32 >= Flo: may reach the floor).
     auto fast_power = [&](uint32_t ra, float& P) -> bool {
-      const float4 q0 = lds128(ra + kFrMean);   // mxh mxl myh myl
-      const float4 q1 = lds128(ra + kFrQuad);   // A B C L2o
+      const float4 q0 = lds128(ra + kFrMean);   // mxh D myh E
+      const float4 q1 = lds128(ra + kFrQuad);   // A B C F
       const float flo = lds32(ra + kFrFloor);
-      const float dx = (sx - q0.x) - q0.y;
-      const float dy = (sy - q0.z) - q0.w;
-      P = fmaf(fmaf(q1.x, dx, q1.y * dy), dx, fmaf(q1.z * dy, dy, q1.w));
+      // P = A dx^2 + B dx dy + C dy^2 + log2(o), dx = dxh - mxl, expanded in
+      // dxh = sx - mxh: the low parts of the mean sit in D, E, F (cs_internal.cuh)
+      const float dxh = sx - q0.x;
+      const float dyh = sy - q0.z;
+      P = fmaf(fmaf(q1.x, dxh, fmaf(q1.y, dyh, q0.y)), dxh, fmaf(fmaf(q1.z, dyh, q0.w), dyh, q1.w));
       return P >= (GUARD ? flo - (l2afl - flo) * (guard_scale - 1.0f) : flo);  // else skipped (_kernels.py:61-62)
     };
     // ... and for a passing lane: alpha32 = 2^P32, its error bound, and the
     // alpha-floor decision (acc; amb when inside the bound)
     auto fast_alpha = [&](uint32_t ra, float P, float& a, float& eps, bool& acc, bool& amb) {
       const float4 q2 = lds128(ra + kFrFloor);  // flo fhi ek1 ek0
-      const float l2o = lds32(ra + kFrQuad + 12);
+      const float l2o = lds32(ra + kFrColour + 12);
       a = ex2_approx(P);                              // alpha = o exp(power)  (_kernels.py:58)
       eps = fmaf(fabsf(P - l2o), q2.z, q2.w);         // this fragment's alpha error bound
       float fhi = q2.y;

@@ -68,12 +68,18 @@ constexpr int kHotChunks = (int)(sizeof(HotRec) / 16);  // cp.async 16-byte copi
 // reference's decision.  Decisions inside the bound are re-made in float64
 // (cs_blend.cu).  Everything is in the log2 domain of alpha:
 //   P = log2(o exp(power)) = log2(e) power + log2(o),  alpha = 2^P (before the
-//   0.99 clamp), evaluated as P32 = (A dx + B dy) dx + (C dy dy + L2o):
-//   mean   = (mxh + mxl, myh + myl): float hi/lo split of the float64 mean, so
-//            dx = (sx - mxh) - mxl loses only ~2u |dx| (u = 2^-24);
+//   0.99 clamp), with dx = dxh - mxl, dxh = sx - mxh (mxh = float(mx), mxl the
+//   exact double remainder mx - mxh) expanded in dxh:
+//   P32 = (A dxh + (B dyh + D)) dxh + ((C dyh + E) dyh + F)   -- 2 FADD + 5 FFMA:
 //   A, B, C: float(-log2(e) c0 / 2), float(-log2(e) c1), float(-log2(e) c2 / 2);
-//   L2o    : float(log2(o)) -- folded into the last FMA, so alpha32 = ex2(P32)
-//            costs no multiply and the floor test is one compare;
+//   D, E   : the linear terms the low parts of the mean contribute,
+//            -2 A mxl - B myl and -B mxl - 2 C myl (double, rounded);
+//   F      : A mxl^2 + B mxl myl + C myl^2 + log2(o) -- log2(o) folded in, so
+//            alpha32 = ex2(P32) costs no multiply and the floor test is one
+//            compare;  L2o = float(log2(o)) is kept for the error bound;
+//   (the expansion only moves the mean's low parts into coefficients: the
+//   roundings are those of the hi/lo form -- dxh = sx - mxh rounds once, the
+//   D/E/F roundings are below the |mxl| terms of the bound)
 //   Flo/Fhi: log2(alpha_floor) -/+ dP, rounded outward, dP bounding
 //            |P32 - P| on R = {power64 >= lthr - 1} (which holds the floor
 //            contour): P32 < Flo is a certain skip, P32 >= Fhi a certain
@@ -89,10 +95,10 @@ constexpr int kHotChunks = (int)(sizeof(HotRec) / 16);  // cp.async 16-byte copi
 // or non-finite conic) are flagged in their cull box (kBoxExact): every lane
 // takes the float64 path for them.
 struct __align__(16) FastRec {
-  float mxh, mxl, myh, myl;
-  float A, B, C, L2o;
+  float mxh, D, myh, E;
+  float A, B, C, F;
   float flo, fhi, ek1, ek0;
-  float r, g, b, pad;
+  float r, g, b, L2o;
   // a staging slot holding a flagged splat's HotRec instead (k_blend_fast)
   __device__ const HotRec& as_hot() const { return *reinterpret_cast<const HotRec*>(this); }
 };
@@ -123,16 +129,20 @@ __device__ __forceinline__ FastRec make_fast_rec(double mx, double my, double c0
   constexpr float kLn2 = 0.69314718f;
   FastRec f;
   f.mxh = (float)mx;
-  f.mxl = (float)(mx - (double)f.mxh);
   f.myh = (float)my;
-  f.myl = (float)(my - (double)f.myh);
-  f.A = (float)(-0.5 * kLog2e * c0);
-  f.B = (float)(-kLog2e * c1);
-  f.C = (float)(-0.5 * kLog2e * c2);
+  const double ml = mx - (double)f.mxh, mly = my - (double)f.myh;  // exact
+  const float mxl = (float)ml, myl = (float)mly;                     // (the bound's |mxl| terms)
+  const double Ad = -0.5 * kLog2e * c0, Bd = -kLog2e * c1, Cd = -0.5 * kLog2e * c2;
+  f.A = (float)Ad;
+  f.B = (float)Bd;
+  f.C = (float)Cd;
   // float log2 of the float opacity: |L2o - log2(o)| <= log2(e) u (opacity
   // rounding) + 2u |L2o| (log2f, <= 1 ulp), in l2o_err below
   f.L2o = opacity > 0.0 ? log2f((float)opacity) : 0.0f;
-  f.r = r; f.g = g; f.b = b; f.pad = 0.f;
+  f.D = (float)(-2.0 * Ad * ml - Bd * mly);
+  f.E = (float)(-Bd * ml - 2.0 * Cd * mly);
+  f.F = (float)((Ad * ml * ml + Bd * ml * mly + Cd * mly * mly) + (double)f.L2o);
+  f.r = r; f.g = g; f.b = b;
   exact = false;
   const float L = -lthr;  // > 0 for any alpha_floor < opacity (else lthr >= 0: never passes)
   if (!(L > 0.0f) || !(opacity > 0.0)) {   // nothing can pass: keep the fast path, never passes
@@ -154,8 +164,8 @@ __device__ __forceinline__ FastRec make_fast_rec(double mx, double my, double c0
   //  * max of S on R: 0.5 Q lambda_max(|C|, C) = 0.5 Q (1 + rho) / (1 - rho),
   //    rho = |c1| / sqrt(c0 c2) (the generalized eigenvalue of the pair).
   // Thin, edge-on splats (rho -> 1) exceed kFastMaxDp and are flagged.
-  // The L2o term adds its own rounding and two roundings of sums that contain
-  // it: <= 3u |L2o| (log2 units).
+  // The log2(o) term adds its own error, the rounding of F and two roundings
+  // of sums that contain it (l2o_err below, log2 units).
   const float Q = 2.0f * (L + 1.0f) * 1.0001f;
   // max of S(d) / |power(d)|: (1 + rho) / (1 - rho) = (s + |c1|)^2 / det, s = sqrt(c0 c2),
   // in float (relative error < 1e-6 while det / (c0 c2) > 1e-6; below that the
@@ -167,7 +177,7 @@ __device__ __forceinline__ FastRec make_fast_rec(double mx, double my, double c0
   const float DY = sqrtf(Q * (float)cc) * 1.0001f + 1e-3f;
   const float a0 = fabsf((float)c0) * 1.0001f, a1 = fabsf((float)c1) * 1.0001f,
               a2 = fabsf((float)c2) * 1.0001f;
-  const float lo_terms = 2.0f * u * ((a0 * DX + a1 * DY) * (fabsf(f.mxl) + 1e-30f) + (a1 * DX + a2 * DY) * fabsf(f.myl));
+  const float lo_terms = 2.0f * u * ((a0 * DX + a1 * DY) * (fabsf(mxl) + 1e-30f) + (a1 * DX + a2 * DY) * fabsf(myl));
   const float dp = 1.25f * (8.0f * u * Smax + lo_terms) + 1e-9f;
   if (!pd || !(dp <= kFastMaxDp)) {
     exact = true;
@@ -177,7 +187,9 @@ __device__ __forceinline__ FastRec make_fast_rec(double mx, double my, double c0
   }
   // |P32 - P| on R, log2 units (the reference's own float64 rounding of
   // o * exp(power) is ~1e-16: inside the 1e-9 slack)
-  const float l2o_err = 1.01f * (1.4426950f * u + 4.0f * u * fabsf(f.L2o));
+  // log2(o) error (log2e u + 2u |L2o|), the rounding of F and two FMA roundings
+  // of sums holding it (3u |L2o|)
+  const float l2o_err = 1.01f * (1.4426950f * u + 5.0f * u * fabsf(f.L2o));
   const float dP = 1.01f * ((float)kLog2e * dp + l2o_err) + 1e-9f;
   const double F = log2_afl;
   f.flo = __double2float_rd(F - (double)dP);
