@@ -601,7 +601,8 @@ static int render_once(cs_ctx* c, Ws* w, const cs_source* src, const cs_camera* 
                  w->hot.as<HotRec>(), fast_blend ? w->fast.as<FastRec>() : nullptr,
                  w->rects.as<uint2>(), w->boxes.as<short4>(),
                  debug ? w->recs.as<ProjRec>() : nullptr,
-                 src->kind == CS_SRC_CLOUD ? src->exclude : nullptr, std::log2(st->alpha_floor)};
+                 src->kind == CS_SRC_CLOUD ? src->exclude : nullptr, std::log2(st->alpha_floor),
+                 std::log((float)st->alpha_floor)};
   launch_project(clouds, w->segs.as<Seg>(), stats, *cam, *st, cap, po, list, s);
   w->last_debug = debug;
   CS_CHECK_LAUNCH();

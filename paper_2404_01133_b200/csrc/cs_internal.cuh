@@ -122,7 +122,7 @@ constexpr float kEx2RelErr = 4.0e-7f;
 // bounds the pixel offsets of the region R = {power >= lthr - 1}:
 // |dx| <= sqrt(2 (L + 1) ca), |dy| <= sqrt(2 (L + 1) cc).
 __device__ __forceinline__ FastRec make_fast_rec(double mx, double my, double c0, double c1, double c2,
-                                                 double opacity, float lthr, float r, float g, float b,
+                                                 double opacity, float ln_o, float lthr, float r, float g, float b,
                                                  double ca, double cc, double log2_afl, bool& exact) {
   constexpr float u = 5.9604645e-8f;  // 2^-24
   constexpr double kLog2e = 1.4426950408889634;
@@ -136,9 +136,10 @@ __device__ __forceinline__ FastRec make_fast_rec(double mx, double my, double c0
   f.A = (float)Ad;
   f.B = (float)Bd;
   f.C = (float)Cd;
-  // float log2 of the float opacity: |L2o - log2(o)| <= log2(e) u (opacity
-  // rounding) + 2u |L2o| (log2f, <= 1 ulp), in l2o_err below
-  f.L2o = opacity > 0.0 ? log2f((float)opacity) : 0.0f;
+  // log2(o) from the float log of the float opacity K3 already has (ln_o =
+  // logf(float(o))): |L2o - log2(o)| <= log2(e) u (opacity rounding)
+  // + 3.5u |L2o| (logf <= 1 ulp, log2(e) as a float, the multiply), in l2o_err below
+  f.L2o = opacity > 0.0 ? ln_o * 1.44269504f : 0.0f;
   f.D = (float)(-2.0 * Ad * ml - Bd * mly);
   f.E = (float)(-Bd * ml - 2.0 * Cd * mly);
   f.F = (float)((Ad * ml * ml + Bd * ml * mly + Cd * mly * mly) + (double)f.L2o);
@@ -187,9 +188,10 @@ __device__ __forceinline__ FastRec make_fast_rec(double mx, double my, double c0
   }
   // |P32 - P| on R, log2 units (the reference's own float64 rounding of
   // o * exp(power) is ~1e-16: inside the 1e-9 slack)
-  // log2(o) error (log2e u + 2u |L2o|), the rounding of F and two FMA roundings
+  // log2(o) error (log2e u + 3.5u |L2o|: logf, log2(e) as a float, the multiply),
+  // the rounding of F and two FMA roundings
   // of sums holding it (3u |L2o|)
-  const float l2o_err = 1.01f * (1.4426950f * u + 5.0f * u * fabsf(f.L2o));
+  const float l2o_err = 1.01f * (1.4426950f * u + 7.0f * u * fabsf(f.L2o));
   const float dP = 1.01f * ((float)kLog2e * dp + l2o_err) + 1e-9f;
   const double F = log2_afl;
   f.flo = __double2float_rd(F - (double)dP);
@@ -285,6 +287,7 @@ struct ProjOutputs {
   ProjRec* recs;     // optional (debug / dumps)
   const uint8_t* exclude;  // input, optional: rows culled as if absent (assignment renders)
   double log2_afl;         // log2(alpha_floor) (the FastRec floor thresholds), set by the host
+  float ln_afl;            // logf(float(alpha_floor)) (the fast-reject threshold lthr), set by the host
 };
 
 // LoD scene tables on device (cs_lod.cu)

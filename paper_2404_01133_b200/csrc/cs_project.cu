@@ -334,8 +334,9 @@ __device__ __forceinline__ void project_emit(int64_t i, const Geom& g, const Pro
   // |log| <= ~20, i.e. < 5e-6): the threshold stays conservative, only the
   // exact float64 path decides a fragment.
   float lthr;
+  const float ln_o = g.op > 0.0 ? logf((float)g.op) : 0.0f;   // (also the FastRec's log2(o))
   if (g.op > 0.0) {
-    const float lf = __fsub_rn(logf((float)st.alpha_floor), logf((float)g.op));
+    const float lf = __fsub_rn(po_out.ln_afl, ln_o);
     lthr = __fsub_rd(lf, 1e-5f + 1e-6f * fabsf(lf));
   } else {
     lthr = __int_as_float(0x7f800000);
@@ -365,7 +366,7 @@ __device__ __forceinline__ void project_emit(int64_t i, const Geom& g, const Pro
   po_out.hot[idx] = h;
   if (po_out.fast) {
     bool exact;
-    const FastRec f = make_fast_rec(po.mx, po.my, c0, c1, c2, g.op, lthr, h.r, h.g, h.b, po.a, po.c,
+    const FastRec f = make_fast_rec(po.mx, po.my, c0, c1, c2, g.op, ln_o, lthr, h.r, h.g, h.b, po.a, po.c,
                                     po_out.log2_afl, exact);
     po_out.fast[idx] = f;
     if (exact) box.x = (int16_t)kBoxExact;
