@@ -616,6 +616,7 @@ static int render_once(cs_ctx* c, Ws* w, const cs_source* src, const cs_camera* 
                                          &stats->assembled, cap, 0, 32, w->hist.as<uint32_t>(),
                                          w->st_sort.as<uint32_t>(), w->sort_tickets.as<uint32_t>(), s, false,
                                          /*identity_vals=*/true);
+  if (which < 0) return fail(CS_EINVAL, "depth sort: identity values need 8-bit digits");
   CS_CHECK_LAUNCH();
   uint32_t* order = which ? w->valsB.as<uint32_t>() : w->valsA.as<uint32_t>();
   const uint32_t* k32s = which ? w->k32B.as<uint32_t>() : w->k32A.as<uint32_t>();

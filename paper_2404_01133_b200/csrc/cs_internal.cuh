@@ -10,6 +10,7 @@
 //   ProjRec   : 128 B -- full _Projected record, written only in debug/dump mode
 //   pairs     :  u32 tile key + u32 splat id, sorted stably by tile
 #pragma once
+#include <cstddef>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -56,6 +57,11 @@ struct __align__(16) HotRec {   // everything the blend reads per splat (64 B: 4
   float r, g, b;                 // SH colour (fp32 of the float64 value)
 };
 static_assert(sizeof(HotRec) == 64, "HotRec layout");
+// byte offsets k_blend_fast reads a staged HotRec at (ld.shared): mx 0, my 8,
+// c0 16, c1 24, c2 32, opacity 40, lthr 48, r g b 52 56 60
+static_assert(offsetof(HotRec, c0) == 16 && offsetof(HotRec, opacity) == 40 && offsetof(HotRec, lthr) == 48 &&
+                  offsetof(HotRec, r) == 52 && offsetof(HotRec, b) == 60,
+              "HotRec field offsets");
 constexpr int kHotChunks = (int)(sizeof(HotRec) / 16);  // cp.async 16-byte copies per record
 
 // ---------------------------------------------------------------------------
@@ -103,6 +109,9 @@ struct __align__(16) FastRec {
   __device__ const HotRec& as_hot() const { return *reinterpret_cast<const HotRec*>(this); }
 };
 static_assert(sizeof(FastRec) == 64, "FastRec layout");
+static_assert(offsetof(FastRec, A) == 16 && offsetof(FastRec, flo) == 32 && offsetof(FastRec, r) == 48 &&
+                  offsetof(FastRec, L2o) == 60,
+              "FastRec field offsets (kFrMean / kFrQuad / kFrFloor / kFrColour)");
 // byte offsets inside a staged FastRec (k_blend_fast reads them with ld.shared)
 constexpr uint32_t kFrMean = 0, kFrQuad = 16, kFrFloor = 32, kFrColour = 48;
 // A flagged splat's cull box carries x0 = kBoxExact (K3, fast-blend frames
