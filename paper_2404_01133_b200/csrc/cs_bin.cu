@@ -88,7 +88,10 @@ __device__ __forceinline__ void emit_pairs(uint32_t p, uint32_t p1, int nr, cons
 // pairs emitted by k_emit_heavy in kBinSlice-pair slices spread over the
 // whole GPU.  The output is the same: every pair lands at prefix + local.
 constexpr int kBinThreads = 256;
-constexpr int kBinItems = 8;
+#ifndef CS_BIN_ITEMS
+#define CS_BIN_ITEMS 8
+#endif
+constexpr int kBinItems = CS_BIN_ITEMS;
 constexpr int kBinRanks = kBinThreads * kBinItems;
 #ifndef CS_BIN_HEAVY
 #define CS_BIN_HEAVY 32768

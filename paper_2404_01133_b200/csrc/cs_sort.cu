@@ -71,7 +71,13 @@ static void launch_pdl(void (*kernel)(Params...), unsigned grid, unsigned block,
 
 template <typename K> struct SortCfg;
 template <> struct SortCfg<uint64_t> { static constexpr int kItems = 8, kMinBlocks = 1; };
-template <> struct SortCfg<uint32_t> { static constexpr int kItems = 16, kMinBlocks = 3; };
+#ifndef CS_SORT_ITEMS32
+#define CS_SORT_ITEMS32 16
+#endif
+#ifndef CS_SORT_MINB32
+#define CS_SORT_MINB32 3
+#endif
+template <> struct SortCfg<uint32_t> { static constexpr int kItems = CS_SORT_ITEMS32, kMinBlocks = CS_SORT_MINB32; };
 
 // Digit counts of every pass in one read of the keys.  Keys that arrive in
 // assembled order are spatially coherent (the depth key's top digits repeat
