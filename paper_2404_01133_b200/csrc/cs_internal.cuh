@@ -390,28 +390,41 @@ __device__ __forceinline__ int local_pixel(int tid, int q, int ts) {
 }
 
 // Blend work items are (tile, box) pairs: a box is 32 pixels of a tile --
-// an 8x4 block when the tile side is a multiple of 8, else 32 consecutive
+// a kBoxW x kBoxH block when the tile side allows, else 32 consecutive
 // row-major pixels.  box_pixel -> local pixel index (>= ts*ts: no pixel).
+// The forward blends' warp box: CS_BOX_W x (32 / CS_BOX_W) pixels: 4 x 8 (tall) measured
+// faster than 8 x 4 on the C3 flythrough (blend 0.749 -> 0.727 ms), 2 x 16 and
+// 16 x 2 slower (0.850 / 0.936 ms; profiles/r4_build_flag_sweeps.txt)
+#ifndef CS_BOX_W
+#define CS_BOX_W 4
+#endif
+constexpr int kBoxW = CS_BOX_W, kBoxH = 32 / CS_BOX_W;
 __host__ __device__ __forceinline__ int boxes_per_tile(int ts) {
-  return (ts & 7) == 0 ? (ts >> 3) * (ts >> 2) : (ts * ts + 31) / 32;
+  return (ts % kBoxW == 0 && ts % kBoxH == 0) ? (ts / kBoxW) * (ts / kBoxH) : (ts * ts + 31) / 32;
 }
 __device__ __forceinline__ int box_pixel(int b, int lane, int ts) {
-  if ((ts & 7) == 0) {
-    const int nbx = ts >> 3, bx = b % nbx, by = b / nbx;
-    return (by * 4 + (lane >> 3)) * ts + bx * 8 + (lane & 7);
+  if (ts % kBoxW == 0 && ts % kBoxH == 0) {
+    const int nbx = ts / kBoxW, bx = b % nbx, by = b / nbx;
+    return (by * kBoxH + lane / kBoxW) * ts + bx * kBoxW + lane % kBoxW;
   }
   return b * 32 + lane;
 }
 // Two pixels per lane: 8x8 boxes, lane (x, y) of the upper 8x4 half and
 // (x, y + 4) of the lower; tile sizes that are not multiples of 8 use
 // row-major 64-pixel chunks (pixel j of the lane at 32 j + lane).
+// two pixels per lane (the backward): a kBox2W x (64 / kBox2W) block, the
+// lane's pixels 32 / kBox2W rows apart
+#ifndef CS_BOX2_W
+#define CS_BOX2_W 8
+#endif
+constexpr int kBox2W = CS_BOX2_W, kBox2H = 64 / CS_BOX2_W;
 __host__ __device__ __forceinline__ int boxes_per_tile2(int ts) {
-  return (ts & 7) == 0 ? (ts >> 3) * (ts >> 3) : (ts * ts + 63) / 64;
+  return (ts % kBox2W == 0 && ts % kBox2H == 0) ? (ts / kBox2W) * (ts / kBox2H) : (ts * ts + 63) / 64;
 }
 __device__ __forceinline__ int box_pixel2(int b, int lane, int ts, int j) {
-  if ((ts & 7) == 0) {
-    const int nbx = ts >> 3, bx = b % nbx, by = b / nbx;
-    return (by * 8 + (lane >> 3) + 4 * j) * ts + bx * 8 + (lane & 7);
+  if (ts % kBox2W == 0 && ts % kBox2H == 0) {
+    const int nbx = ts / kBox2W, bx = b % nbx, by = b / nbx;
+    return (by * kBox2H + lane / kBox2W + (32 / kBox2W) * j) * ts + bx * kBox2W + lane % kBox2W;
   }
   return b * 64 + 32 * j + lane;
 }
