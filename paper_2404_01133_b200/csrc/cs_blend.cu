@@ -3,7 +3,7 @@
 // Replaces _kernels.blend_tiles (_kernels.py:17-76), the reference's only
 // native kernel.  One CTA per tile, one thread per pixel (tile_size <= 16;
 // 4 or 16 pixels per thread for 32/64).  For 16x16 tiles each warp owns an
-// 8x4 pixel box.
+// 4x8 pixel box (CS_BOX_W).
 //
 // Every warp walks the tile's splat list (depth order) independently, 32
 // entries per round: each lane tests one splat's 8-byte alpha-floor support
@@ -49,7 +49,7 @@ namespace cs {
 constexpr int kBlendThreads = CS_BLEND_THREADS;
 
 // Warp-independent blend, persistent: every warp repeatedly takes the next
-// work item -- one 8x4 pixel box of one tile, tiles in heaviest-list-first
+// work item -- one 4x8 pixel box of one tile, tiles in heaviest-list-first
 // order -- from a device-wide ticket, so no warp ever waits for another and a
 // CTA's slots are never held by finished warps.  For its box a warp walks the
 // tile's depth-ordered list 32 entries per round: each lane reads one entry's
@@ -65,7 +65,7 @@ __device__ __forceinline__ int blend_box_pixel(int b, int lane, int ts, int j) {
   return PX == 1 ? box_pixel(b, lane, ts) : box_pixel2(b, lane, ts, j);
 }
 
-// PX pixels per lane (1: 8x4 boxes, 2: 8x8 boxes).  With two pixels a lane
+// PX pixels per lane (1: 4x8 boxes, 2: 8x8 boxes).  With two pixels a lane
 // reads each staged record once for both, and a tile is walked by half as
 // many warps.
 #ifndef CS_BLEND_MINB
@@ -342,7 +342,7 @@ k_blend(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
 // ---------------------------------------------------------------------------
 // K9f: the certified float32 blend (frames without kept state).
 //
-// Same work decomposition as k_blend (persistent warps, 8x4 pixel boxes,
+// Same work decomposition as k_blend (persistent warps, 4x8 pixel boxes,
 // list rounds of 32 entries culled by box, hit records cp.async-staged two
 // rounds deep), but each hit's 64-byte FastRec (cs_internal.cuh) is evaluated
 // in float32 on the FMA pipe and MUFU.EX2 instead of the float64 chain.  Every
