@@ -1,6 +1,6 @@
 # round-2 milestone capture: smoke, GPU tests, default bench, reference arm,
 # launch list, --set full of the timed frames (summarised on the box)
-TAG=${1:-r3s}
+TAG=${1:-r4z}
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; tail -1 gpurun_out/${TAG}_smoke.log
 timeout 1500 python -m pytest tests -m gpu -q -rf > gpurun_out/${TAG}_pytest.log 2>&1; tail -2 gpurun_out/${TAG}_pytest.log
 timeout 1200 python bench.py > gpurun_out/${TAG}_bench.log 2>&1
