@@ -222,7 +222,10 @@ void launch_fix_depth_runs(const uint32_t* k32_sorted, uint32_t* order, const ui
                            cudaStream_t s) {
   RunCtl* ctl = reinterpret_cast<RunCtl*>(ctl_mem);
   cudaMemsetAsync(ctl, 0, sizeof(RunCtl), s);
-  const int grid = (int)std::min<int64_t>(148 * 8, (capacity + 255) / 256 + 1);
+#ifndef CS_FIX_GRID_MULT
+#define CS_FIX_GRID_MULT 8
+#endif
+  const int grid = (int)std::min<int64_t>(148 * CS_FIX_GRID_MULT, (capacity + 255) / 256 + 1);
   k_fix_short_runs<<<grid, 256, 0, s>>>(k32_sorted, order, k64, stats, ctl, long_runs, long_cap);
   k_fix_long_runs<<<148, 256, 0, s>>>(k32_sorted, order, k64, stats, ctl, long_runs, long_cap,
                                       scratch);
