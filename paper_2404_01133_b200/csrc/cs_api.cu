@@ -1037,7 +1037,7 @@ int cs_training_loss(cs_ctx* c, const float* img, const float* ref, int32_t heig
   if (!(lam >= 0.0 && lam <= 1.0)) return fail(CS_EINVAL, "lam must be in [0, 1]");
   std::lock_guard<std::mutex> lock(c->mu);
   CS_CUDA(cudaSetDevice(c->device));
-  const size_t maps = (size_t)9 * (height - 10) * (width - 10);
+  const size_t maps = (size_t)9 * (height - 10) * (((width - 10) + 3) & ~3);  // row pitch mult. of 4
   if (c->loss_maps.ensure(4 * maps) || c->loss_acc.ensure(16)) return fail(CS_ENOMEM, "loss maps");
   launch_training_loss(img, ref, height, width, lam, c->loss_maps.as<float>(),
                        c->loss_acc.as<double>(), loss_out, grad_out, (cudaStream_t)stream);

@@ -13,8 +13,9 @@
 //   k_ssim_grad: dL/dx(p) = (1-lam)/(3HW) sign(x-y)
 //                         - lam/(3 Nv) sum_k w(k) [A + 2 x(p) B + y(p) C](p - k)
 //     (the adjoint correlation of the three maps), plus the L1 sum.
-// Both stage an input tile with its 10-pixel halo in shared memory and run
-// the 11-tap window as a horizontal then a vertical pass.
+// Both run one block per (32x32 tile, channel): the tile's 42x42 region is
+// staged in shared memory and the 11-tap window runs as a horizontal then a
+// vertical register-sliding pass (8 outputs per thread, each input read once).
 //
 // K14 Adam + activations (ply.py:108-123 conventions, torch.optim.Adam
 // semantics): per Gaussian the gradient w.r.t. the activated parameters
@@ -33,14 +34,15 @@ namespace cs {
 
 constexpr int kWin = 11;
 constexpr int kHalo = kWin - 1;
-#ifndef CS_SSIM_TX
-#define CS_SSIM_TX 16
-#endif
-#ifndef CS_SSIM_TY
-#define CS_SSIM_TY 32
-#endif
-constexpr int kTX = CS_SSIM_TX, kTY = CS_SSIM_TY;  // output tile of both loss kernels
-constexpr int kRX = kTX + kHalo, kRY = kTY + kHalo;  // 42 x 26 region
+constexpr int kTX = 32, kTY = 32;                   // output tile of both loss kernels
+constexpr int kSeg = 8;                             // outputs per thread along a sliding pass
+constexpr int kRX = kTX + kHalo, kRY = kTY + kHalo;  // 42 x 42 region
+constexpr int kRP = kRX + 1;                        // odd region pitch: conflict-free rows
+constexpr int kHP = kTX + 1;                        // pass-1 output pitch
+constexpr int kSegsX = kTX / kSeg, kSegsY = kTY / kSeg;
+constexpr int kGOff = 12;                           // grad region starts 12 columns left (aligned)
+constexpr int kGChunks = (kTX + kGOff) / 4;         // 11 float4 chunks per region row
+constexpr int kGP = 4 * kGChunks;                   // 44: 16-byte rows, conflict-free LDS.128
 constexpr int kLossThreads = 256;
 constexpr float kC1 = 0.01f * 0.01f, kC2 = 0.03f * 0.03f;
 
@@ -48,79 +50,156 @@ __constant__ float c_win[kWin];
 
 struct LossDims {
   int H, W, Hv, Wv;
+  int Wp;        // maps row pitch: Wv rounded up to 4 (pad columns hold zeros)
   float k_l1;    // (1 - lam) / (3 H W)
   float k_ssim;  // -lam / (3 Hv Wv)
 };
 
-// maps layout: [ch][3][Hv][Wv]  (A, B, C)
-__global__ void __launch_bounds__(kLossThreads)
+// 4-byte asynchronous copy into shared memory, zero-filled when !valid (the
+// staging loops issue every copy of the region before the first wait instead
+// of one dependent load/store round trip per loop iteration).
+__device__ __forceinline__ void cp_async4(float* smem, const float* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sa), "l"(gmem), "r"(valid ? 4 : 0)
+               : "memory");
+}
+
+__device__ __forceinline__ void cp_async16z(float* smem, const float* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0)
+               : "memory");
+}
+
+// One step of a register-sliding 11-tap pass: input j (of kSeg + kHalo) adds
+// into every output o it falls under, tap j - o (the correlation of the
+// forward statistics) or kHalo - (j - o) (the adjoint correlation of the
+// gradient).  j is a compile-time index of an unrolled loop, so the tap
+// selection folds away and each thread reads each input once instead of 11x.
+template <int N, bool ADJ>
+__device__ __forceinline__ void win_step(float (&acc)[kSeg][N], int j, const float (&v)[N]) {
+#pragma unroll
+  for (int o = 0; o < kSeg; ++o) {
+    const int k = ADJ ? kHalo - (j - o) : j - o;
+    if (j - o >= 0 && j - o < kWin) {
+#pragma unroll
+      for (int n = 0; n < N; ++n) acc[o][n] = fmaf(c_win[k], v[n], acc[o][n]);
+    }
+  }
+}
+
+// maps layout: [ch][3][Hv][Wp]  (A, B, C); columns Wv..Wp-1 are written as zeros.
+// One block per 32x32 window tile, all three channels: the tile's 42 image
+// rows x 42 pixels x 3 channels are staged interleaved, as they lie in HWC
+// (16-byte copies when a row of 3W floats keeps 16-byte alignment, VEC), and
+// each channel then runs the two sliding passes; the horizontal pass picks
+// its channel out of 16-byte shared loads.
+constexpr int kSX = 132;  // staged row pitch: 126 floats -> 33 float4 (odd: conflict-free LDS.128)
+constexpr int kStatsSmem = (2 * kRY * kSX + 5 * kRY * kHP) * 4;
+
+template <bool VEC>
+__global__ void __launch_bounds__(kLossThreads, 3)
 k_ssim_stats(const float* __restrict__ img, const float* __restrict__ ref, LossDims d,
              float* __restrict__ maps, double* __restrict__ acc) {
-  __shared__ float sx[kRY][kRX * 3];
-  __shared__ float sy[kRY][kRX * 3];
-  __shared__ float hs[5][kRY][kTX];
+  extern __shared__ __align__(16) float dsm[];  // kStatsSmem bytes
+  float(*sx)[kSX] = reinterpret_cast<float(*)[kSX]>(dsm);
+  float(*sy)[kSX] = reinterpret_cast<float(*)[kSX]>(dsm + kRY * kSX);
+  float(*hs)[kRY][kHP] = reinterpret_cast<float(*)[kRY][kHP]>(dsm + 2 * kRY * kSX);
   __shared__ double s_red[kLossThreads / 32];
   const int ox = blockIdx.x * kTX, oy = blockIdx.y * kTY;
-  // stage the 3-channel region (rows contiguous in HWC: coalesced)
-  for (int i = threadIdx.x; i < kRY * kRX * 3; i += kLossThreads) {
-    const int r = i / (kRX * 3), cc = i - r * (kRX * 3);
-    const int gy = oy + r, gx = ox + cc / 3;
-    float vx = 0.f, vy = 0.f;
-    if (gy < d.H && gx < d.W) {
-      const size_t o = ((size_t)gy * d.W + gx) * 3 + (cc % 3);
-      vx = __ldg(img + o);
-      vy = __ldg(ref + o);
+  const int rowlen = 3 * d.W;
+  if (VEC) {
+    for (int i = threadIdx.x; i < kRY * 32; i += kLossThreads) {
+      const int r = i >> 5, k = i & 31;
+      const int gy = oy + r, f = 3 * ox + 4 * k;
+      const bool in = gy < d.H && f < rowlen;
+      const size_t o = in ? (size_t)gy * rowlen + f : 0;
+      cp_async16z(&sx[r][4 * k], img + o, in);
+      cp_async16z(&sy[r][4 * k], ref + o, in);
     }
-    sx[r][cc] = vx;
-    sy[r][cc] = vy;
+  } else {
+    for (int i = threadIdx.x; i < kRY * 128; i += kLossThreads) {
+      const int r = i >> 7, k = i & 127;
+      const int gy = oy + r, f = 3 * ox + k;
+      const bool in = gy < d.H && f < rowlen;
+      const size_t o = in ? (size_t)gy * rowlen + f : 0;
+      cp_async4(&sx[r][k], img + o, in);
+      cp_async4(&sy[r][k], ref + o, in);
+    }
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   double ssum = 0.0;
+  const size_t plane = (size_t)d.Hv * d.Wp;
+#pragma unroll
   for (int ch = 0; ch < 3; ++ch) {
-    // horizontal pass: 26 rows x 32 output columns
-    for (int i = threadIdx.x; i < kRY * kTX; i += kLossThreads) {
-      const int r = i / kTX, c = i - r * kTX;
-      float mx = 0.f, my = 0.f, xx = 0.f, yy = 0.f, xy = 0.f;
+  // horizontal pass: (row, 8-column segment) per thread, segment fastest;
+  // input pixel c0 + j, channel ch = float 3 (c0 + j) + ch of the staged row
+  for (int i = threadIdx.x; i < kRY * kSegsX; i += kLossThreads) {
+    const int r = i / kSegsX, s4 = i - r * kSegsX, c0 = s4 * kSeg;
+    const float* rx = &sx[r][3 * c0];
+    const float* ry = &sy[r][3 * c0];
+    float a[kSeg][5] = {};
+    float4 qx = make_float4(0.f, 0.f, 0.f, 0.f), qy = qx;
 #pragma unroll
-      for (int k = 0; k < kWin; ++k) {
-        const float w = c_win[k];
-        const float a = sx[r][(c + k) * 3 + ch], b = sy[r][(c + k) * 3 + ch];
-        mx += w * a; my += w * b;
-        xx += w * a * a; yy += w * b * b; xy += w * a * b;
+    for (int j = 0; j < kSeg + kHalo; ++j) {
+      const int e = 3 * j + ch;
+      if (j == 0 || (e >> 2) != ((e - 3) >> 2)) {  // compile-time: first use of this chunk
+        qx = *reinterpret_cast<const float4*>(rx + 4 * (e >> 2));
+        qy = *reinterpret_cast<const float4*>(ry + 4 * (e >> 2));
       }
-      hs[0][r][c] = mx; hs[1][r][c] = my; hs[2][r][c] = xx; hs[3][r][c] = yy; hs[4][r][c] = xy;
+      const int w = e & 3;
+      const float x = w == 0 ? qx.x : w == 1 ? qx.y : w == 2 ? qx.z : qx.w;
+      const float y = w == 0 ? qy.x : w == 1 ? qy.y : w == 2 ? qy.z : qy.w;
+      const float v[5] = {x, y, x * x, y * y, x * y};
+      win_step<5, false>(a, j, v);
     }
-    __syncthreads();
-    // vertical pass + per-window SSIM and partials
-    for (int i = threadIdx.x; i < kTY * kTX; i += kLossThreads) {
-      const int r = i / kTX, c = i - r * kTX;
-      const int qy = oy + r, qx = ox + c;
-      if (qy >= d.Hv || qx >= d.Wv) continue;
-      float mx = 0.f, my = 0.f, xx = 0.f, yy = 0.f, xy = 0.f;
 #pragma unroll
-      for (int k = 0; k < kWin; ++k) {
-        const float w = c_win[k];
-        mx += w * hs[0][r + k][c]; my += w * hs[1][r + k][c];
-        xx += w * hs[2][r + k][c]; yy += w * hs[3][r + k][c]; xy += w * hs[4][r + k][c];
-      }
+    for (int o = 0; o < kSeg; ++o)
+#pragma unroll
+      for (int n = 0; n < 5; ++n) hs[n][r][c0 + o] = a[o][n];
+  }
+  __syncthreads();
+  float* m = maps + (size_t)ch * 3 * plane;
+  // vertical pass + per-window SSIM and partials: (column, 8-row segment)
+  for (int i = threadIdx.x; i < kTX * kSegsY; i += kLossThreads) {
+    const int c = i % kTX, r0 = (i / kTX) * kSeg;
+    float a[kSeg][5] = {};
+#pragma unroll
+    for (int j = 0; j < kSeg + kHalo; ++j) {
+      const float v[5] = {hs[0][r0 + j][c], hs[1][r0 + j][c], hs[2][r0 + j][c], hs[3][r0 + j][c],
+                          hs[4][r0 + j][c]};
+      win_step<5, false>(a, j, v);
+    }
+    const int qx = ox + c;
+    const size_t q0 = (size_t)(oy + r0) * d.Wp + qx;
+#pragma unroll
+    for (int o = 0; o < kSeg; ++o) {
+      // the zero-filled region keeps out-of-range windows finite (d1 >= C1,
+      // d2 >= C2): evaluate unconditionally, predicate the sum and the stores
+      const bool row_ok = oy + r0 + o < d.Hv;
+      const bool valid = row_ok && qx < d.Wv;
+      const float mx = a[o][0], my = a[o][1], xx = a[o][2], yy = a[o][3], xy = a[o][4];
       const float vx = xx - mx * mx, vy = yy - my * my, cv = xy - mx * my;
       const float n1 = 2.f * mx * my + kC1, n2 = 2.f * cv + kC2;
       const float d1 = mx * mx + my * my + kC1, d2 = vx + vy + kC2;
-      const float den = d1 * d2;
-      const float S = n1 * n2 / den;
-      ssum += (double)S;
-      // dS/dmu_x with E[xx], E[xy] held fixed (var_x, cov depend on mu_x)
-      const float A = (2.f * my * n2 - 2.f * my * n1) / den - S * (2.f * mx / d1 - 2.f * mx / d2);
-      const float B = -S / d2;            // dS/dE[xx]
-      const float C = 2.f * n1 / den;     // dS/dE[xy]
-      const size_t plane = (size_t)d.Hv * d.Wv;
-      const size_t o = (size_t)qy * d.Wv + qx;
-      float* m = maps + (size_t)ch * 3 * plane;
-      m[o] = A;
-      m[plane + o] = B;
-      m[2 * plane + o] = C;
+      const float inv = 1.f / (d1 * d2);
+      const float S = n1 * n2 * inv;
+      ssum += valid ? (double)S : 0.0;
+      // dS/dmu_x with E[xx], E[xy] held fixed (var_x, cov depend on mu_x);
+      // 1/d1 = d2 inv, 1/d2 = d1 inv
+      const float A = 2.f * my * (n2 - n1) * inv - S * 2.f * mx * (d2 - d1) * inv;
+      const float B = -S * d1 * inv;      // dS/dE[xx]
+      const float C = 2.f * n1 * inv;     // dS/dE[xy]
+      if (row_ok && qx < d.Wp) {
+        const size_t q = q0 + (size_t)o * d.Wp;
+        m[q] = valid ? A : 0.f;
+        m[plane + q] = valid ? B : 0.f;
+        m[2 * plane + q] = valid ? C : 0.f;
+      }
     }
-    __syncthreads();
+  }
+  __syncthreads();  // hs is rewritten by the next channel
   }
   ssum = warp_sum(ssum);
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = ssum;
@@ -136,60 +215,75 @@ __global__ void __launch_bounds__(kLossThreads)
 k_ssim_grad(const float* __restrict__ img, const float* __restrict__ ref,
             const float* __restrict__ maps, LossDims d, float* __restrict__ grad,
             double* __restrict__ acc) {
-  __shared__ float sm[3][kRY][kRX];     // A, B, C region of one channel
-  __shared__ float hs[3][kRY][kTX];
-  __shared__ float so[kTY][kTX * 3];    // gradient tile, HWC
+  // A, B, C region of this channel: windows rows oy-10 .. oy+31, columns
+  // ox-12 .. ox+31 (16-byte aligned: ox and the pitch Wp are multiples of 4)
+  __shared__ __align__(16) float sm[3][kRY][kGP];
+  __shared__ float hs[3][kRY][kHP];
   __shared__ double s_red[kLossThreads / 32];
+  const int ch = blockIdx.z;
   const int ox = blockIdx.x * kTX, oy = blockIdx.y * kTY;
-  const size_t plane = (size_t)d.Hv * d.Wv;
+  const size_t plane = (size_t)d.Hv * d.Wp;
+  const float* m = maps + (size_t)ch * 3 * plane;
+  for (int i = threadIdx.x; i < 3 * kRY * kGChunks; i += kLossThreads) {
+    const int row = i / kGChunks, k = i - row * kGChunks;
+    const int mi = row / kRY, r = row - mi * kRY;
+    const int qy = oy - kHalo + r, qx = ox - kGOff + 4 * k;
+    const bool in = qy >= 0 && qy < d.Hv && qx >= 0 && qx < d.Wp;
+    cp_async16z(&sm[mi][r][4 * k], m + (in ? mi * plane + (size_t)qy * d.Wp + qx : 0), in);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  for (int i = threadIdx.x; i < 3 * kRY * kSegsX; i += kLossThreads) {
+    const int mi = i / (kRY * kSegsX), rem = i - mi * (kRY * kSegsX);
+    const int r = rem / kSegsX, c0 = (rem - r * kSegsX) * kSeg;
+    float a[kSeg][1] = {};
+    float in[kSeg + 16];  // region columns c0 .. c0+23 (taps use c0+2 .. c0+19)
+#pragma unroll
+    for (int t = 0; t < 6; ++t) {
+      const float4 q = *reinterpret_cast<const float4*>(&sm[mi][r][c0 + 4 * t]);
+      in[4 * t] = q.x; in[4 * t + 1] = q.y; in[4 * t + 2] = q.z; in[4 * t + 3] = q.w;
+    }
+#pragma unroll
+    for (int j = 0; j < kSeg + kHalo; ++j) {
+      const float v[1] = {in[kGOff - kHalo + j]};
+      win_step<1, true>(a, j, v);
+    }
+#pragma unroll
+    for (int o = 0; o < kSeg; ++o) hs[mi][r][c0 + o] = a[o][0];
+  }
+  __syncthreads();
   double l1 = 0.0;
-  for (int ch = 0; ch < 3; ++ch) {
-    const float* m = maps + (size_t)ch * 3 * plane;
-    // windows q = p - k, k in [0, 10]: rows oy-10 .. oy+15, cols ox-10 .. ox+31
-    for (int i = threadIdx.x; i < 3 * kRY * kRX; i += kLossThreads) {
-      const int mi = i / (kRY * kRX), rem = i - mi * (kRY * kRX);
-      const int r = rem / kRX, c = rem - r * kRX;
-      const int qy = oy - kHalo + r, qx = ox - kHalo + c;
-      float v = 0.f;
-      if (qy >= 0 && qy < d.Hv && qx >= 0 && qx < d.Wv) v = __ldg(m + mi * plane + (size_t)qy * d.Wv + qx);
-      sm[mi][r][c] = v;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < 3 * kRY * kTX; i += kLossThreads) {
-      const int mi = i / (kRY * kTX), rem = i - mi * (kRY * kTX);
-      const int r = rem / kTX, c = rem - r * kTX;
-      float s = 0.f;
+  for (int i = threadIdx.x; i < kTX * kSegsY; i += kLossThreads) {
+    const int c = i % kTX, r0 = (i / kTX) * kSeg;
+    const int px = ox + c;
+    // issue the 8 pixels' image loads before the window sums hide their latency
+    float xs[kSeg], ys[kSeg];
 #pragma unroll
-      for (int k = 0; k < kWin; ++k) s += c_win[k] * sm[mi][r][c + kHalo - k];
-      hs[mi][r][c] = s;
+    for (int o = 0; o < kSeg; ++o) {
+      const int py = oy + r0 + o;
+      const bool in = py < d.H && px < d.W;
+      const size_t q = in ? ((size_t)py * d.W + px) * 3 + ch : 0;
+      xs[o] = in ? __ldg(img + q) : 0.f;
+      ys[o] = in ? __ldg(ref + q) : 0.f;
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < kTY * kTX; i += kLossThreads) {
-      const int r = i / kTX, c = i - r * kTX;
-      const int py = oy + r, px = ox + c;
+    float a[kSeg][3] = {};
+#pragma unroll
+    for (int j = 0; j < kSeg + kHalo; ++j) {
+      const float v[3] = {hs[0][r0 + j][c], hs[1][r0 + j][c], hs[2][r0 + j][c]};
+      win_step<3, true>(a, j, v);
+    }
+#pragma unroll
+    for (int o = 0; o < kSeg; ++o) {
+      const int py = oy + r0 + o;
       if (py >= d.H || px >= d.W) continue;
-      float a = 0.f, b = 0.f, cc = 0.f;
-#pragma unroll
-      for (int k = 0; k < kWin; ++k) {
-        const float w = c_win[k];
-        a += w * hs[0][r + kHalo - k][c];
-        b += w * hs[1][r + kHalo - k][c];
-        cc += w * hs[2][r + kHalo - k][c];
-      }
-      const size_t o = ((size_t)py * d.W + px) * 3 + ch;
-      const float x = __ldg(img + o), y = __ldg(ref + o);
+      const size_t q = ((size_t)py * d.W + px) * 3 + ch;
+      const float x = xs[o], y = ys[o];
       const float diff = x - y;
       l1 += (double)fabsf(diff);
       const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
-      so[r][c * 3 + ch] = d.k_l1 * sgn + d.k_ssim * (a + 2.f * x * b + y * cc);
+      grad[q] = d.k_l1 * sgn + d.k_ssim * (a[o][0] + 2.f * x * a[o][1] + y * a[o][2]);
     }
-    __syncthreads();
-  }
-  // coalesced HWC write of the tile
-  for (int i = threadIdx.x; i < kTY * kTX * 3; i += kLossThreads) {
-    const int r = i / (kTX * 3), cc = i - r * (kTX * 3);
-    const int py = oy + r, px = ox + cc / 3;
-    if (py < d.H && px < d.W) grad[((size_t)py * d.W + px) * 3 + (cc % 3)] = so[r][cc];
   }
   l1 = warp_sum(l1);
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = l1;
@@ -226,13 +320,22 @@ void launch_training_loss(const float* img, const float* ref, int H, int W, doub
                           float* maps, double* acc, double* loss, float* grad, cudaStream_t s) {
   set_window();
   LossDims d;
-  d.H = H; d.W = W; d.Hv = H - kHalo; d.Wv = W - kHalo;
+  d.H = H; d.W = W; d.Hv = H - kHalo; d.Wv = W - kHalo; d.Wp = (d.Wv + 3) & ~3;
   d.k_l1 = (float)((1.0 - lam) / (3.0 * H * W));
   d.k_ssim = (float)(-lam / (3.0 * (double)d.Hv * d.Wv));
   cudaMemsetAsync(acc, 0, 2 * sizeof(double), s);
   dim3 g1((d.Wv + kTX - 1) / kTX, (d.Hv + kTY - 1) / kTY);
-  k_ssim_stats<<<g1, kLossThreads, 0, s>>>(img, ref, d, maps, acc);
-  dim3 g2((W + kTX - 1) / kTX, (H + kTY - 1) / kTY);
+  // 16-byte staging needs every image row (3W floats) 16-byte aligned
+  const bool vec = (W & 3) == 0 && ((reinterpret_cast<uintptr_t>(img) | reinterpret_cast<uintptr_t>(ref)) & 15) == 0;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_ssim_stats<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStatsSmem);
+    cudaFuncSetAttribute(k_ssim_stats<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStatsSmem);
+    attr = true;
+  }
+  if (vec) k_ssim_stats<true><<<g1, kLossThreads, kStatsSmem, s>>>(img, ref, d, maps, acc);
+  else k_ssim_stats<false><<<g1, kLossThreads, kStatsSmem, s>>>(img, ref, d, maps, acc);
+  dim3 g2((W + kTX - 1) / kTX, (H + kTY - 1) / kTY, 3);
   k_ssim_grad<<<g2, kLossThreads, 0, s>>>(img, ref, maps, d, grad, acc);
   k_loss_finalize<<<1, 1, 0, s>>>(acc, d, lam, loss);
 }
