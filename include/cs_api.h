@@ -293,7 +293,7 @@ typedef struct cs_adam_hparams {
 } cs_adam_hparams;
 /* One Adam step of a block's raw parameters with the PLY activations
  * (ply.py:108-123: exp scale, sigmoid opacity, normalised quaternion).
- * geom: device (K,11) float32 rows (16-byte aligned, as are the moments, grads->rotations and the quads) [x,y,z, log s0..2, q w,x,y,z (raw), logit o];
+ * geom: device (K,11) float32 rows (16-byte aligned, as are the moments, sh, sh moments, grads->rotations, grads->sh and the quads) [x,y,z, log s0..2, q w,x,y,z (raw), logit o];
  * geom_m/geom_v its Adam moments; sh (K,3C) float32 and its moments.
  * grads: cs_render_backward's output for the activated parameters.
  * Writes the activated (K,4) float32 quads pos_op/scale/quat that a cs_cloud

@@ -1057,8 +1057,8 @@ int cs_block_adam(cs_ctx* c, int64_t K, int32_t sh_coeffs, float* geom, float* g
   if (hp->step < 1) return fail(CS_EINVAL, "step must be >= 1");
   auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (K > 0 && !(a16(geom) && a16(geom_m) && a16(geom_v) && a16(grads->rotations) && a16(pos_op) &&
-                 a16(scale) && a16(quat)))
-    return fail(CS_EINVAL, "geom, moments, rotation gradients and quads must be 16-byte aligned");
+                 a16(scale) && a16(quat) && a16(sh) && a16(sh_m) && a16(sh_v) && a16(grads->sh)))
+    return fail(CS_EINVAL, "geom, SH, moments, rotation/SH gradients and quads must be 16-byte aligned");
   CS_CUDA(cudaSetDevice(c->device));
   launch_block_adam(K, sh_coeffs, geom, geom_m, geom_v, sh, sh_m, sh_v, *grads, *hp,
                     reinterpret_cast<float4*>(pos_op), reinterpret_cast<float4*>(scale),

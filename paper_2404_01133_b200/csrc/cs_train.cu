@@ -357,16 +357,16 @@ __device__ __forceinline__ void adam1(float& p, float& m, float& v, float g, flo
 // updated per lane, and written back the same way.
 constexpr int kAdamThreads = 256;
 
-__global__ void __launch_bounds__(kAdamThreads)
-k_adam_geom(int64_t K, float* __restrict__ geom, float* __restrict__ gm,
-            float* __restrict__ gv, cs_grads g, cs_adam_hparams h, float bc1,
-            float bc2s, float4* __restrict__ pos_op, float4* __restrict__ scale,
-            float4* __restrict__ quat) {
-  __shared__ __align__(16) float s_buf[kAdamThreads / 32][3][32 * 11];
+__device__ __forceinline__ void adam_geom(int blk, int nblk, int64_t K, float* __restrict__ geom,
+                                          float* __restrict__ gm, float* __restrict__ gv,
+                                          const cs_grads& g, const cs_adam_hparams& h, float bc1,
+                                          float bc2s, float4* __restrict__ pos_op,
+                                          float4* __restrict__ scale, float4* __restrict__ quat,
+                                          float (*s_buf)[3][32 * 11]) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* arrs[3] = {geom, gm, gv};
-  for (int64_t base = ((int64_t)blockIdx.x * (kAdamThreads / 32) + warp) * 32; base < K;
-       base += (int64_t)gridDim.x * (kAdamThreads / 32) * 32) {
+  for (int64_t base = ((int64_t)blk * (kAdamThreads / 32) + warp) * 32; base < K;
+       base += (int64_t)nblk * (kAdamThreads / 32) * 32) {
     const int n_rows = (int)min((int64_t)32, K - base);
     const int nf = n_rows * 11;
 #pragma unroll
@@ -439,26 +439,58 @@ k_adam_geom(int64_t K, float* __restrict__ geom, float* __restrict__ gm,
   }
 }
 
-__global__ void k_adam_flat(int64_t n, float* __restrict__ p, float* __restrict__ m,
-                            float* __restrict__ v, const float* __restrict__ g, float lr,
-                            cs_adam_hparams h, float bc1, float bc2s) {
+// SH moments: elementwise, two float4 groups per thread per iteration (16
+// independent 16-byte loads in flight per thread)
+__device__ __forceinline__ void adam_flat(int blk, int nblk, int64_t n, float* __restrict__ p,
+                                          float* __restrict__ m, float* __restrict__ v,
+                                          const float* __restrict__ g, float lr,
+                                          const cs_adam_hparams& h, float bc1, float bc2s) {
   const int64_t n4 = n / 4;
   float4* p4 = reinterpret_cast<float4*>(p);
   float4* m4 = reinterpret_cast<float4*>(m);
   float4* v4 = reinterpret_cast<float4*>(v);
   const float4* g4 = reinterpret_cast<const float4*>(g);
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
-    float4 pp = p4[i], mm = m4[i], vv = v4[i];
-    const float4 gg = __ldg(g4 + i);
+  const int64_t stride = (int64_t)nblk * blockDim.x;
+  const int64_t t = blk * (int64_t)blockDim.x + threadIdx.x;
+  auto upd = [&](float4& pp, float4& mm, float4& vv, const float4& gg) {
     adam1(pp.x, mm.x, vv.x, gg.x, lr, h, bc1, bc2s);
     adam1(pp.y, mm.y, vv.y, gg.y, lr, h, bc1, bc2s);
     adam1(pp.z, mm.z, vv.z, gg.z, lr, h, bc1, bc2s);
     adam1(pp.w, mm.w, vv.w, gg.w, lr, h, bc1, bc2s);
-    p4[i] = pp; m4[i] = mm; v4[i] = vv;
+  };
+  int64_t i = t;
+  for (; i + stride < n4; i += 2 * stride) {
+    const int64_t j = i + stride;
+    float4 pa = p4[i], ma = m4[i], va = v4[i];
+    float4 pb = p4[j], mb = m4[j], vb = v4[j];
+    const float4 ga = __ldg(g4 + i), gb = __ldg(g4 + j);
+    upd(pa, ma, va, ga);
+    upd(pb, mb, vb, gb);
+    p4[i] = pa; m4[i] = ma; v4[i] = va;
+    p4[j] = pb; m4[j] = mb; v4[j] = vb;
   }
-  for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
-    adam1(p[i], m[i], v[i], g[i], lr, h, bc1, bc2s);
+  if (i < n4) {
+    float4 pa = p4[i], ma = m4[i], va = v4[i];
+    upd(pa, ma, va, __ldg(g4 + i));
+    p4[i] = pa; m4[i] = ma; v4[i] = va;
+  }
+  for (int64_t k = 4 * n4 + t; k < n; k += stride) adam1(p[k], m[k], v[k], g[k], lr, h, bc1, bc2s);
+}
+
+// One launch for both parameter groups: the first geom_blocks CTAs run the
+// geometry rows, the rest the SH moments, so the latency-bound geometry
+// update overlaps the bandwidth-bound SH stream instead of preceding it.
+__global__ void __launch_bounds__(kAdamThreads, 4)
+k_adam(int64_t K, int geom_blocks, float* __restrict__ geom, float* __restrict__ gm,
+       float* __restrict__ gv, int64_t n_sh, float* __restrict__ sh, float* __restrict__ shm,
+       float* __restrict__ shv, cs_grads g, cs_adam_hparams h, float bc1, float bc2s,
+       float4* __restrict__ pos_op, float4* __restrict__ scale, float4* __restrict__ quat) {
+  __shared__ __align__(16) float s_buf[kAdamThreads / 32][3][32 * 11];
+  if ((int)blockIdx.x < geom_blocks)
+    adam_geom(blockIdx.x, geom_blocks, K, geom, gm, gv, g, h, bc1, bc2s, pos_op, scale, quat, s_buf);
+  else
+    adam_flat(blockIdx.x - geom_blocks, gridDim.x - geom_blocks, n_sh, sh, shm, shv, g.sh, h.lr_sh, h,
+              bc1, bc2s);
 }
 
 __global__ void k_activate_geom(int64_t K, const float* __restrict__ geom, float4* __restrict__ pos_op,
@@ -480,12 +512,14 @@ void launch_block_adam(int64_t K, int C, float* geom, float* gm, float* gv, floa
   const double bc2 = 1.0 - pow((double)h.beta2, (double)h.step);
   const float bc2s = (float)sqrt(bc2);
   if (K <= 0) return;
-  const int grid = (int)std::min<int64_t>(148 * 8, (K + kAdamThreads - 1) / kAdamThreads);
-  k_adam_geom<<<grid, kAdamThreads, 0, s>>>(K, geom, gm, gv, g, h, (float)bc1, bc2s, pos_op, scale,
-                                            quat);
+  // one resident wave (4 CTAs/SM: 64 registers), split by traffic: the
+  // geometry rows are ~1/5 of the bytes but latency-bound, so ~1/3 of the CTAs
   const int64_t n = K * 3 * C;
-  const int grid2 = (int)std::min<int64_t>(148 * 8, (n / 4 + 255) / 256 + 1);
-  k_adam_flat<<<grid2, 256, 0, s>>>(n, sh, shm, shv, g.sh, h.lr_sh, h, (float)bc1, bc2s);
+  const int wave = 148 * 4;
+  const int gb = (int)std::max<int64_t>(1, std::min<int64_t>(wave / 3, (K + kAdamThreads - 1) / kAdamThreads));
+  const int fb = (int)std::max<int64_t>(1, std::min<int64_t>(wave - gb, (n / 4 + kAdamThreads - 1) / kAdamThreads));
+  k_adam<<<gb + fb, kAdamThreads, 0, s>>>(K, gb, geom, gm, gv, n, sh, shm, shv, g, h, (float)bc1, bc2s,
+                                          pos_op, scale, quat);
 }
 
 void launch_activate_geom(int64_t K, const float* geom, float4* pos_op, float4* scale, float4* quat,

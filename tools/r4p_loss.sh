@@ -6,5 +6,5 @@ python -c "
 import json
 d=json.loads(open('gpurun_out/r4p_bench.log').read().strip().splitlines()[-1])
 t=d['train']; print('FPS', round(d['value'],1), 'train', round(t['value'],1), {k: round(v,4) for k,v in t['phases_ms'].items()})"
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'k_ssim|k_adam' -c 6 --csv --log-file gpurun_out/r4p_launches.csv python bench.py --no-cpu-baseline --no-assign --no-modes --no-c12 --no-c5 --no-e2e --steps 2 --warmup 1 --train-steps 2 --train-warmup 1 > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'k_ssim|k_adam' -c 8 --csv --log-file gpurun_out/r4p_launches.csv python bench.py --no-cpu-baseline --no-assign --no-modes --no-c12 --no-c5 --no-e2e --steps 2 --warmup 1 --train-steps 2 --train-warmup 1 > /dev/null 2>&1
 grep -o '"k_[a-z_]*(.*' gpurun_out/r4p_launches.csv | awk -F'","' '{print $1, $NF}' | cut -c1-20,200-
