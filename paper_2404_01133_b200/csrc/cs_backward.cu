@@ -502,6 +502,7 @@ k_project_bwd_sh(const cs_cloud cl, const uint64_t* __restrict__ depth_keys, cs_
   const int C = cl.sh_coeffs, C3 = 3 * C, stride = cl.sh_stride;
   const int degree = min((int)st.sh_degree, deg_of(C));
   const int nb = (degree + 1) * (degree + 1);
+  const float inv_stride = 1.f / (float)stride, inv_c3 = 1.f / (float)C3;
   for (int64_t base = ((int64_t)blockIdx.x * (kShBwdThreads / 32) + warp) * 32; base < K;
        base += (int64_t)gridDim.x * (kShBwdThreads / 32) * 32) {
     const int n_rows = (int)min((int64_t)32, K - base);
@@ -510,7 +511,9 @@ k_project_bwd_sh(const cs_cloud cl, const uint64_t* __restrict__ depth_keys, cs_
       const int n4 = n_rows * stride / 4;
       for (int i = lane; i < n4; i += 32) {
         const float4 v = __ldg(src + i);
-        const int e = 4 * i, r = e / stride, c = e - r * stride;
+        // row of element e: (e + 0.5) / stride in float is exact here (e < 2^12,
+        // the half offset keeps the quotient >= 0.5/stride away from integers)
+        const int e = 4 * i, r = (int)(((float)e + 0.5f) * inv_stride), c = e - r * stride;
         float* d = buf + r * pitch + c;
         d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
       }
@@ -559,11 +562,25 @@ k_project_bwd_sh(const cs_cloud cl, const uint64_t* __restrict__ depth_keys, cs_
       }
     }
     __syncwarp();
-    // gradient rows are packed (3C floats per row): coalesced scalar stores
+    // gradient rows are packed (3C floats per row): coalesced stores, 16-byte
+    // when the packed block is 16-byte aligned (3C % 4 == 0 or an even base)
     float* dst = out.sh + base * C3;
-    for (int e = lane; e < n_rows * C3; e += 32) {
-      const int r = e / C3, c = e - r * C3;
-      dst[e] = buf[r * pitch + c];
+    if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0 && (n_rows * C3) % 4 == 0) {
+      float4* d4 = reinterpret_cast<float4*>(dst);
+      for (int i = lane; i < n_rows * C3 / 4; i += 32) {
+        float t[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int e = 4 * i + q, r = (int)(((float)e + 0.5f) * inv_c3), c = e - r * C3;
+          t[q] = buf[r * pitch + c];
+        }
+        d4[i] = make_float4(t[0], t[1], t[2], t[3]);
+      }
+    } else {
+      for (int e = lane; e < n_rows * C3; e += 32) {
+        const int r = (int)(((float)e + 0.5f) * inv_c3), c = e - r * C3;
+        dst[e] = buf[r * pitch + c];
+      }
     }
     __syncwarp();
   }
