@@ -343,12 +343,22 @@ void launch_training_loss(const float* img, const float* ref, int H, int W, doub
 // ---------------------------------------------------------------------------
 // K14: Adam on raw block parameters + activation chain + activated quads
 
-__device__ __forceinline__ void adam1(float& p, float& m, float& v, float g, float lr,
-                                      const cs_adam_hparams& h, float bc1, float bc2s) {
+// torch.optim.Adam (bias-corrected, eps outside the root) with the root and
+// the quotient as single MUFU-based approximations (relative error ~1e-7,
+// far inside the trainer-vs-torch bound) instead of IEEE sqrt / division
+// sequences: the SH stream was issue-bound on them.  step = lr / bc1,
+// ibc2s = 1 / sqrt(bc2).
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void adam1(float& p, float& m, float& v, float g, float step,
+                                      const cs_adam_hparams& h, float ibc2s) {
   m = h.beta1 * m + (1.f - h.beta1) * g;
   v = h.beta2 * v + (1.f - h.beta2) * g * g;
-  const float denom = sqrtf(v) / bc2s + h.eps;
-  p -= (lr / bc1) * (m / denom);
+  const float denom = fmaf(sqrt_approx(v), ibc2s, h.eps);
+  p -= step * __fdividef(m, denom);
 }
 
 // One warp per 32 consecutive Gaussians: their (K, 11) rows of parameters and
@@ -356,11 +366,14 @@ __device__ __forceinline__ void adam1(float& p, float& m, float& v, float g, flo
 // coalesced float4 copies (odd row pitch 11: conflict-free per-lane access),
 // updated per lane, and written back the same way.
 constexpr int kAdamThreads = 256;
+#ifndef CS_ADAM_GEOM_DIV
+#define CS_ADAM_GEOM_DIV 3  // 1 / (fraction of the Adam CTAs on geometry rows)
+#endif
 
 __device__ __forceinline__ void adam_geom(int blk, int nblk, int64_t K, float* __restrict__ geom,
                                           float* __restrict__ gm, float* __restrict__ gv,
-                                          const cs_grads& g, const cs_adam_hparams& h, float bc1,
-                                          float bc2s, float4* __restrict__ pos_op,
+                                          const cs_grads& g, const cs_adam_hparams& h, float ibc1,
+                                          float ibc2s, float4* __restrict__ pos_op,
                                           float4* __restrict__ scale, float4* __restrict__ quat,
                                           float (*s_buf)[3][32 * 11]) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -369,17 +382,20 @@ __device__ __forceinline__ void adam_geom(int blk, int nblk, int64_t K, float* _
        base += (int64_t)nblk * (kAdamThreads / 32) * 32) {
     const int n_rows = (int)min((int64_t)32, K - base);
     const int nf = n_rows * 11;
+    // asynchronous staging: all 3 x 88 16-byte copies in flight at once
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const float* src = arrs[a] + base * 11;
       if (n_rows == 32) {
-        const float4* s4 = reinterpret_cast<const float4*>(src);
-        float4* d4 = reinterpret_cast<float4*>(s_buf[warp][a]);
-        for (int i = lane; i < 88; i += 32) d4[i] = s4[i];
+#pragma unroll
+        for (int i = lane; i < 88 + 32; i += 32)
+          if (i < 88) cp_async16(&s_buf[warp][a][4 * i], src + 4 * i);
       } else {
         for (int i = lane; i < nf; i += 32) s_buf[warp][a][i] = src[i];
       }
     }
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncwarp();
     const int64_t k = base + lane;
     if (lane < n_rows) {
@@ -414,7 +430,7 @@ __device__ __forceinline__ void adam_geom(int blk, int nblk, int64_t K, float* _
 #pragma unroll
       for (int i = 0; i < 11; ++i) {
         pr[i] = p[i]; mr[i] = m[i]; vr[i] = v[i];
-        adam1(pr[i], mr[i], vr[i], gr[i], lrs[i], h, bc1, bc2s);
+        adam1(pr[i], mr[i], vr[i], gr[i], lrs[i] * ibc1, h, ibc2s);
         p[i] = pr[i]; m[i] = mr[i]; v[i] = vr[i];
       }
       // activated quads for the next forward
@@ -443,8 +459,8 @@ __device__ __forceinline__ void adam_geom(int blk, int nblk, int64_t K, float* _
 // independent 16-byte loads in flight per thread)
 __device__ __forceinline__ void adam_flat(int blk, int nblk, int64_t n, float* __restrict__ p,
                                           float* __restrict__ m, float* __restrict__ v,
-                                          const float* __restrict__ g, float lr,
-                                          const cs_adam_hparams& h, float bc1, float bc2s) {
+                                          const float* __restrict__ g, float step,
+                                          const cs_adam_hparams& h, float ibc2s) {
   const int64_t n4 = n / 4;
   float4* p4 = reinterpret_cast<float4*>(p);
   float4* m4 = reinterpret_cast<float4*>(m);
@@ -453,10 +469,10 @@ __device__ __forceinline__ void adam_flat(int blk, int nblk, int64_t n, float* _
   const int64_t stride = (int64_t)nblk * blockDim.x;
   const int64_t t = blk * (int64_t)blockDim.x + threadIdx.x;
   auto upd = [&](float4& pp, float4& mm, float4& vv, const float4& gg) {
-    adam1(pp.x, mm.x, vv.x, gg.x, lr, h, bc1, bc2s);
-    adam1(pp.y, mm.y, vv.y, gg.y, lr, h, bc1, bc2s);
-    adam1(pp.z, mm.z, vv.z, gg.z, lr, h, bc1, bc2s);
-    adam1(pp.w, mm.w, vv.w, gg.w, lr, h, bc1, bc2s);
+    adam1(pp.x, mm.x, vv.x, gg.x, step, h, ibc2s);
+    adam1(pp.y, mm.y, vv.y, gg.y, step, h, ibc2s);
+    adam1(pp.z, mm.z, vv.z, gg.z, step, h, ibc2s);
+    adam1(pp.w, mm.w, vv.w, gg.w, step, h, ibc2s);
   };
   int64_t i = t;
   for (; i + stride < n4; i += 2 * stride) {
@@ -474,7 +490,7 @@ __device__ __forceinline__ void adam_flat(int blk, int nblk, int64_t n, float* _
     upd(pa, ma, va, __ldg(g4 + i));
     p4[i] = pa; m4[i] = ma; v4[i] = va;
   }
-  for (int64_t k = 4 * n4 + t; k < n; k += stride) adam1(p[k], m[k], v[k], g[k], lr, h, bc1, bc2s);
+  for (int64_t k = 4 * n4 + t; k < n; k += stride) adam1(p[k], m[k], v[k], g[k], step, h, ibc2s);
 }
 
 // One launch for both parameter groups: the first geom_blocks CTAs run the
@@ -483,14 +499,14 @@ __device__ __forceinline__ void adam_flat(int blk, int nblk, int64_t n, float* _
 __global__ void __launch_bounds__(kAdamThreads, 4)
 k_adam(int64_t K, int geom_blocks, float* __restrict__ geom, float* __restrict__ gm,
        float* __restrict__ gv, int64_t n_sh, float* __restrict__ sh, float* __restrict__ shm,
-       float* __restrict__ shv, cs_grads g, cs_adam_hparams h, float bc1, float bc2s,
+       float* __restrict__ shv, cs_grads g, cs_adam_hparams h, float ibc1, float ibc2s,
        float4* __restrict__ pos_op, float4* __restrict__ scale, float4* __restrict__ quat) {
   __shared__ __align__(16) float s_buf[kAdamThreads / 32][3][32 * 11];
   if ((int)blockIdx.x < geom_blocks)
-    adam_geom(blockIdx.x, geom_blocks, K, geom, gm, gv, g, h, bc1, bc2s, pos_op, scale, quat, s_buf);
+    adam_geom(blockIdx.x, geom_blocks, K, geom, gm, gv, g, h, ibc1, ibc2s, pos_op, scale, quat, s_buf);
   else
-    adam_flat(blockIdx.x - geom_blocks, gridDim.x - geom_blocks, n_sh, sh, shm, shv, g.sh, h.lr_sh, h,
-              bc1, bc2s);
+    adam_flat(blockIdx.x - geom_blocks, gridDim.x - geom_blocks, n_sh, sh, shm, shv, g.sh, h.lr_sh * ibc1, h,
+              ibc2s);
 }
 
 __global__ void k_activate_geom(int64_t K, const float* __restrict__ geom, float4* __restrict__ pos_op,
@@ -510,15 +526,15 @@ void launch_block_adam(int64_t K, int C, float* geom, float* gm, float* gv, floa
                        float4* scale, float4* quat, cudaStream_t s) {
   const double bc1 = 1.0 - pow((double)h.beta1, (double)h.step);
   const double bc2 = 1.0 - pow((double)h.beta2, (double)h.step);
-  const float bc2s = (float)sqrt(bc2);
+  const float ibc1 = (float)(1.0 / bc1), ibc2s = (float)(1.0 / sqrt(bc2));
   if (K <= 0) return;
   // one resident wave (4 CTAs/SM: 64 registers), split by traffic: the
   // geometry rows are ~1/5 of the bytes but latency-bound, so ~1/3 of the CTAs
   const int64_t n = K * 3 * C;
   const int wave = 148 * 4;
-  const int gb = (int)std::max<int64_t>(1, std::min<int64_t>(wave / 3, (K + kAdamThreads - 1) / kAdamThreads));
+  const int gb = (int)std::max<int64_t>(1, std::min<int64_t>(wave / CS_ADAM_GEOM_DIV, (K + kAdamThreads - 1) / kAdamThreads));
   const int fb = (int)std::max<int64_t>(1, std::min<int64_t>(wave - gb, (n / 4 + kAdamThreads - 1) / kAdamThreads));
-  k_adam<<<gb + fb, kAdamThreads, 0, s>>>(K, gb, geom, gm, gv, n, sh, shm, shv, g, h, (float)bc1, bc2s,
+  k_adam<<<gb + fb, kAdamThreads, 0, s>>>(K, gb, geom, gm, gv, n, sh, shm, shv, g, h, ibc1, ibc2s,
                                           pos_op, scale, quat);
 }
 
