@@ -106,7 +106,7 @@ void launch_fuse_filter(int64_t n, const void* pos, int f32, const double* pmin,
                         int64_t* kept, int64_t* kept_count, cudaStream_t s);
 // cs_backward.cu
 void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint32_t* bxs, const uint32_t* bys,
-                      const uint2* ranges, const HotRec* hot, const uint32_t* order,
+                      const uint2* ranges, const HotRec* hot, const FastRec* fast, const uint32_t* order,
                       const cs_settings& st, int width, int height, int ntx, const float* dl_dimg,
                       const BlendState& state, uint32_t* ticket, gacc_t* grads, int64_t cap,
                       cudaStream_t s);
@@ -596,13 +596,15 @@ static int render_once(cs_ctx* c, Ws* w, const cs_source* src, const cs_camera* 
   if (debug && w->recs.ensure(sizeof(ProjRec) * w->cap_vis)) return fail(CS_ENOMEM, "debug records");
   // the certified float32 blend's records (frames without kept state)
   const bool fast_blend = !(flags & CS_RENDER_KEEP_STATE);
-  if (fast_blend && w->fast.ensure(sizeof(FastRec) * w->cap_vis)) return fail(CS_ENOMEM, "blend records");
+  // kept-state frames write them too for the backward's certified pre-reject
+  const bool want_fast = fast_blend || CS_BWD_FAST;
+  if (want_fast && w->fast.ensure(sizeof(FastRec) * w->cap_vis)) return fail(CS_ENOMEM, "blend records");
   ProjOutputs po{w->keysA.as<uint64_t>(), w->k32A.as<uint32_t>(), w->valsA.as<uint32_t>(),
-                 w->hot.as<HotRec>(), fast_blend ? w->fast.as<FastRec>() : nullptr,
+                 w->hot.as<HotRec>(), want_fast ? w->fast.as<FastRec>() : nullptr,
                  w->rects.as<uint2>(), w->boxes.as<short4>(),
                  debug ? w->recs.as<ProjRec>() : nullptr,
                  src->kind == CS_SRC_CLOUD ? src->exclude : nullptr, std::log2(st->alpha_floor),
-                 std::log((float)st->alpha_floor)};
+                 std::log((float)st->alpha_floor), fast_blend ? 1 : 0};
   launch_project(clouds, w->segs.as<Seg>(), stats, *cam, *st, cap, po, list, s);
   w->last_debug = debug;
   CS_CHECK_LAUNCH();
@@ -1011,7 +1013,8 @@ int cs_render_backward(cs_ctx* c, cs_state* S, const float* dl_dimg, const cs_gr
   const int ntx = (S->width + ts - 1) / ts;
   BlendState state{w->st_t.as<double>(), w->st_last.as<int32_t>(), w->st_acc.as<double>()};
   launch_blend_bwd(w->last_tiles, w->last_list, w->last_bxs, w->last_bys, w->last_ranges,
-                   w->hot.as<HotRec>(), w->tile_order.as<uint32_t>(), S->st, S->width,
+                   w->hot.as<HotRec>(), CS_BWD_FAST ? w->fast.as<FastRec>() : nullptr,
+                   w->tile_order.as<uint32_t>(), S->st, S->width,
                    S->height, ntx, dl_dimg, state, &w->stats.as<DevStats>()->tickets[5],
                    c->gacc.as<gacc_t>(), cap, s);
   CS_CHECK_LAUNCH();

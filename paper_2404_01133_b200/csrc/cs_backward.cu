@@ -27,6 +27,7 @@ namespace cs {
 
 constexpr int kBwdThreads = 256;
 constexpr int kGradFields = 9;  // mx, my, c0, c1, c2, opacity, r, g, b
+constexpr int kBwdFastSmem = (kBwdThreads / 32) * 2 * 32 * 3 * 16;  // staged FastRec heads
 
 struct BwdParams {
   double bg[3];
@@ -89,11 +90,15 @@ template <int PX>
 __global__ void __launch_bounds__(kBwdThreads, CS_BWD_MINB)
 k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
             const uint32_t* __restrict__ bys, const uint2* __restrict__ ranges,
-            const HotRec* __restrict__ hot, const uint32_t* __restrict__ tile_order, int n_items,
+            const HotRec* __restrict__ hot, const FastRec* __restrict__ fast,
+            const uint32_t* __restrict__ tile_order, int n_items,
             int nboxes, BwdParams bp, const float* __restrict__ dl_dimg, BlendState state,
             uint32_t* __restrict__ ticket, gacc_t* __restrict__ grads /* [kGradFields][cap] */,
             int64_t cap) {
   __shared__ __align__(16) HotRec s_hot[kBwdThreads / 32][2][32];
+  // CS_BWD_FAST: the hits' FastRec heads (mxh D myh E | A B C F | flo fhi ek1 ek0),
+  // dynamic shared memory (kBwdFastSmem bytes; the static total would pass 48 KB)
+  extern __shared__ __align__(16) float4 s_fq[];
   __shared__ ExpTable s_exp;
   const ExpCoef ec = load_exp_table(&s_exp);
   __syncthreads();
@@ -101,6 +106,8 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
   const uint32_t lane = lane_id();
   const uint32_t lt_mask = (1u << lane) - 1u;
   HotRec (*wbuf)[32] = s_hot[threadIdx.x >> 5];
+  float4 (*fbuf)[32][3] = reinterpret_cast<float4 (*)[32][3]>(s_fq + (threadIdx.x >> 5) * 2 * 32 * 3);
+  const bool use_fast = CS_BWD_FAST && fast != nullptr;
   const bsp_t bg[3] = {(bsp_t)bp.bg[0], (bsp_t)bp.bg[1], (bsp_t)bp.bg[2]};
   for (;;) {
     int item = 0;
@@ -123,6 +130,7 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
     // float32.
     bsp_t g[PX][3], acc[PX][3], Tend[PX], T[PX], P[PX][3];
     double sx[PX], sy[PX];
+    float fsx[PX], fsy[PX];  // pixel centres in float (exact)
     int x0 = 1 << 20, x1 = -(1 << 20), y0 = 1 << 20, y1 = -(1 << 20), wend = (int)s0;
 #pragma unroll
     for (int j = 0; j < PX; ++j) {
@@ -154,6 +162,8 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
       }
       sx[j] = (double)px[j] + 0.5;
       sy[j] = (double)py[j] + 0.5;
+      fsx[j] = (float)px[j] + 0.5f;
+      fsy[j] = (float)py[j] + 0.5f;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -168,11 +178,21 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
 
     // ids: each lane's list entry of the staged round (the hit's splat id is
     // the entry of lane src, the gradient slot of its atomics)
-    auto eval_round = [&](const HotRec* buf, uint32_t mask, int64_t k0, uint32_t ids) {
+    auto eval_round = [&](const HotRec* buf, const float4 (*fb)[3], uint32_t mask, int64_t k0, uint32_t ids) {
       int slot = 0;
       while (mask) {
         const int src = __ffs(mask) - 1;
         mask &= mask - 1;
+        // certified float32 pre-reject (make_fast_rec's bound; flagged and
+        // never-passing splats have ek0 == 0 and are always evaluated exactly)
+        float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0;
+        float flo = -__int_as_float(0x7f800000);
+        if (use_fast) {
+          q0 = fb[slot][0];
+          q1 = fb[slot][1];
+          const float4 q2 = fb[slot][2];
+          if (q2.w != 0.f) flo = q2.x;
+        }
         const HotRec& h = buf[slot++];
         const uint32_t hid = __shfl_sync(0xffffffffu, ids, src);
         const double mx = h.mx, my = h.my, c0 = h.c0, c1 = h.c1, c2 = h.c2, lthr = (double)h.lthr;
@@ -182,7 +202,13 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
         bool contrib = false;
 #pragma unroll
         for (int j = 0; j < PX; ++j) {
-          // the quadratic form for every lane (as in the forward: cheaper than a branch)
+          if (use_fast) {
+            const float dxh = fsx[j] - q0.x, dyh = fsy[j] - q0.z;
+            const float P = fmaf(fmaf(q1.x, dxh, fmaf(q1.y, dyh, q0.y)), dxh,
+                                 fmaf(fmaf(q1.z, dyh, q0.w), dyh, q1.w));
+            if (P < flo) continue;  // alpha < alpha_floor for sure: not accepted by the forward
+          }
+          // the quadratic form for every remaining lane (cheaper than a branch)
           const double dx = dsub(sx[j], mx), dy = dsub(sy[j], my);
           const double power = dsub(dmul(-0.5, dadd(dmul(dmul(c0, dx), dx), dmul(dmul(c2, dy), dy))),
                                     dmul(dmul(c1, dx), dy));
@@ -274,12 +300,18 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
         char* d = reinterpret_cast<char*>(&wbuf[stage][__popc(mask & lt_mask)]);
 #pragma unroll
         for (int c = 0; c < kHotChunks; ++c) cp_async16(d + 16 * c, gp + 16 * c);
+        if (use_fast) {
+          const char* fp = reinterpret_cast<const char*>(fast + id);
+          char* fd = reinterpret_cast<char*>(fbuf[stage][__popc(mask & lt_mask)]);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) cp_async16(fd + 16 * c, fp + 16 * c);
+        }
       }
       cp_async_commit();
       if (pmask) {
         cp_async_wait<1>();
         __syncwarp();
-        eval_round(wbuf[stage ^ 1], pmask, pk0, pid);
+        eval_round(wbuf[stage ^ 1], fbuf[stage ^ 1], pmask, pk0, pid);
         __syncwarp();
       }
       // shrink the cull box to the pixels whose last fragment lies beyond
@@ -312,7 +344,7 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
     }
     cp_async_wait<0>();
     __syncwarp();
-    if (pmask) eval_round(wbuf[stage ^ 1], pmask, pk0, pid);
+    if (pmask) eval_round(wbuf[stage ^ 1], fbuf[stage ^ 1], pmask, pk0, pid);
     __syncwarp();
   }
 }
@@ -587,7 +619,7 @@ k_project_bwd_sh(const cs_cloud cl, const uint64_t* __restrict__ depth_keys, cs_
 }
 
 void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint32_t* bxs, const uint32_t* bys,
-                      const uint2* ranges, const HotRec* hot, const uint32_t* order,
+                      const uint2* ranges, const HotRec* hot, const FastRec* fast, const uint32_t* order,
                       const cs_settings& st, int width, int height, int ntx, const float* dl_dimg,
                       const BlendState& state, uint32_t* ticket, gacc_t* grads, int64_t cap,
                       cudaStream_t s) {
@@ -600,10 +632,14 @@ void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint32_t* bxs, co
   bp.ntx = ntx;
   constexpr int PX = CS_BWD_PX;
   static int grid = 0;
-  if (grid == 0) grid = persistent_grid(k_blend_bwd<PX>, kBwdThreads);
+  const int dyn = CS_BWD_FAST ? kBwdFastSmem : 0;
+  if (grid == 0) {
+    if (dyn) cudaFuncSetAttribute(k_blend_bwd<PX>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    grid = persistent_grid(k_blend_bwd<PX>, kBwdThreads, dyn);
+  }
   const int nboxes = PX == 1 ? boxes_per_tile(st.tile_size) : boxes_per_tile2(st.tile_size);
   cudaMemsetAsync(ticket, 0, sizeof(uint32_t), s);
-  k_blend_bwd<PX><<<grid, kBwdThreads, 0, s>>>(list, bxs, bys, ranges, hot, order, n_tiles * nboxes,
+  k_blend_bwd<PX><<<grid, kBwdThreads, dyn, s>>>(list, bxs, bys, ranges, hot, fast, order, n_tiles * nboxes,
                                                nboxes, bp, dl_dimg, state, ticket, grads, cap);
 }
 

@@ -297,7 +297,22 @@ struct ProjOutputs {
   const uint8_t* exclude;  // input, optional: rows culled as if absent (assignment renders)
   double log2_afl;         // log2(alpha_floor) (the FastRec floor thresholds), set by the host
   float ln_afl;            // logf(float(alpha_floor)) (the fast-reject threshold lthr), set by the host
+  int mark_exact = 1;      // flagged splats' cull boxes carry kBoxExact (fast-blend frames only)
 };
+
+// K10 certified pre-reject (CS_BWD_FAST=1, off): a kept-state (training)
+// forward also writes the FastRecs (without marking flagged boxes), and the
+// blend backward skips a pixel's float64 re-evaluation of a hit whenever the
+// FastRec's float32 power is below its certified floor threshold (P32 < Flo =>
+// the float64 alpha is below alpha_floor, so the exact forward did not accept
+// that fragment).  Parity-green (81/81 GPU tests) but measured slower: K10
+// 1.886 -> 2.04 ms per iteration, 324 -> 308 it/s (profiles/r5e_bwd_fast_ab.txt;
+// the extra 48-byte staging per hit and register pressure outweigh the
+// float64 forms it skips -- the backward walks only up to each pixel's last
+// accepted fragment, where few hits are sure rejects).
+#ifndef CS_BWD_FAST
+#define CS_BWD_FAST 0
+#endif
 
 // LoD scene tables on device (cs_lod.cu)
 struct LodTables {
@@ -625,11 +640,11 @@ __device__ __forceinline__ double exp_le0(double x, const ExpTable& T, const Exp
 
 // grid of a persistent kernel: as many CTAs as are co-resident on all SMs
 template <typename K>
-static int persistent_grid(K kernel, int threads) {
+static int persistent_grid(K kernel, int threads, size_t dyn_smem = 0) {
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, dyn_smem);
   return std::max(1, sms * std::max(1, per_sm));
 }
 

@@ -369,7 +369,7 @@ __device__ __forceinline__ void project_emit(int64_t i, const Geom& g, const Pro
     const FastRec f = make_fast_rec(po.mx, po.my, c0, c1, c2, g.op, ln_o, lthr, h.r, h.g, h.b, po.a, po.c,
                                     po_out.log2_afl, exact);
     po_out.fast[idx] = f;
-    if (exact) box.x = (int16_t)kBoxExact;
+    if (exact && po_out.mark_exact) box.x = (int16_t)kBoxExact;
   }
   po_out.boxes[idx] = box;
   // tile rectangle exactly as numpy (render.py:226-231): floor, astype(int64), clip
