@@ -27,7 +27,14 @@ namespace cs {
 
 constexpr int kBwdThreads = 256;
 constexpr int kGradFields = 9;  // mx, my, c0, c1, c2, opacity, r, g, b
-constexpr int kBwdFastSmem = (kBwdThreads / 32) * 2 * 32 * 3 * 16;  // staged FastRec heads
+constexpr int kBwdFastSmem = CS_BWD_FAST ? (kBwdThreads / 32) * 2 * 32 * 3 * 16 : 0;  // staged FastRec heads
+// CS_BWD_RED_SMEM: the warp's nine float64 partial sums go through a per-warp
+// shared-memory transpose (32 x 9 doubles) instead of the shuffle tree
+#ifndef CS_BWD_RED_SMEM
+#define CS_BWD_RED_SMEM 1
+#endif
+constexpr int kBwdRedSmem = CS_BWD_RED_SMEM ? (kBwdThreads / 32) * 32 * kGradFields * 8 : 0;
+constexpr int kBwdDynSmem = kBwdFastSmem + kBwdRedSmem;
 
 struct BwdParams {
   double bg[3];
@@ -47,6 +54,30 @@ typedef double bred_t;
 #else
 typedef float bred_t;
 #endif
+// The same result through shared memory: lane l stores its nine partials at
+// red[l * 9 + f] (stride 72 B: conflict-free 64-bit stores), then lane
+// L < 18 sums half h = L & 1 of field f = L >> 1 (16 rows, the odd half
+// starting 8 rows later so the two halves of a field sit 16 banks apart) and
+// the pair (2f, 2f + 1) combines with one shuffle: ~45 warp instructions
+// instead of the tree's ~110 (double shuffles and selects).
+__device__ __forceinline__ double warp_smem_sum9(const float (&in)[kGradFields], uint32_t lane,
+                                                 double* __restrict__ red) {
+  __syncwarp();  // the previous call's reads are done
+#pragma unroll
+  for (int f = 0; f < kGradFields; ++f) red[lane * kGradFields + f] = (double)in[f];
+  __syncwarp();
+  double v = 0.0;
+  const int f = (int)(lane >> 1), h = (int)(lane & 1);
+  if (lane < 2 * kGradFields) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int row = h * 16 + ((i + 8 * h) & 15);
+      v += red[row * kGradFields + f];
+    }
+  }
+  return v + __shfl_xor_sync(0xffffffffu, v, 1);
+}
+
 __device__ __forceinline__ bred_t warp_transpose_sum9(const float (&in)[kGradFields], uint32_t lane) {
   bred_t v[16];
 #pragma unroll
@@ -98,7 +129,9 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
   __shared__ __align__(16) HotRec s_hot[kBwdThreads / 32][2][32];
   // CS_BWD_FAST: the hits' FastRec heads (mxh D myh E | A B C F | flo fhi ek1 ek0),
   // dynamic shared memory (kBwdFastSmem bytes; the static total would pass 48 KB)
-  extern __shared__ __align__(16) float4 s_fq[];
+  extern __shared__ __align__(16) float4 s_fq[];  // [kBwdFastSmem | kBwdRedSmem]
+  double* red = reinterpret_cast<double*>(reinterpret_cast<char*>(s_fq) + kBwdFastSmem) +
+                (threadIdx.x >> 5) * 32 * kGradFields;
   __shared__ ExpTable s_exp;
   const ExpCoef ec = load_exp_table(&s_exp);
   __syncthreads();
@@ -261,7 +294,8 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
           }
         }
         if (__any_sync(0xffffffffu, contrib)) {
-          const bred_t v = warp_transpose_sum9(gr, lane);
+          const bred_t v = CS_BWD_RED_SMEM && CS_BWD_RED_F64 ? (bred_t)warp_smem_sum9(gr, lane, red)
+                                                             : warp_transpose_sum9(gr, lane);
           const uint32_t f = (lane >> 1) & 15;
           if (!(lane & 1) && f < kGradFields && v != (bred_t)0)
             atomicAdd(&grads[(int64_t)f * cap + hid], (gacc_t)v);
@@ -632,7 +666,7 @@ void launch_blend_bwd(int n_tiles, const uint32_t* list, const uint32_t* bxs, co
   bp.ntx = ntx;
   constexpr int PX = CS_BWD_PX;
   static int grid = 0;
-  const int dyn = CS_BWD_FAST ? kBwdFastSmem : 0;
+  const int dyn = kBwdDynSmem;
   if (grid == 0) {
     if (dyn) cudaFuncSetAttribute(k_blend_bwd<PX>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
     grid = persistent_grid(k_blend_bwd<PX>, kBwdThreads, dyn);
