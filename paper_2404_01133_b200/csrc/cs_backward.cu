@@ -31,7 +31,7 @@ constexpr int kBwdFastSmem = CS_BWD_FAST ? (kBwdThreads / 32) * 2 * 32 * 3 * 16 
 // CS_BWD_RED_SMEM: the warp's nine float64 partial sums go through a per-warp
 // shared-memory transpose (32 x 9 doubles) instead of the shuffle tree
 #ifndef CS_BWD_RED_SMEM
-#define CS_BWD_RED_SMEM 1
+#define CS_BWD_RED_SMEM 2   // 1: two lanes per field, 2: three (profiles/r5i_bwd_red3_ab.txt)
 #endif
 constexpr int kBwdRedSmem = CS_BWD_RED_SMEM ? (kBwdThreads / 32) * 32 * kGradFields * 8 : 0;
 constexpr int kBwdDynSmem = kBwdFastSmem + kBwdRedSmem;
@@ -76,6 +76,27 @@ __device__ __forceinline__ double warp_smem_sum9(const float (&in)[kGradFields],
     }
   }
   return v + __shfl_xor_sync(0xffffffffu, v, 1);
+}
+
+// CS_BWD_RED_SMEM=2: three lanes per field (rows 0-10 / 11-21 / 22-31; lane
+// 3f + p), summed with two shuffles into lane 3f: fewer loads per lane
+__device__ __forceinline__ double warp_smem_sum9_3(const float (&in)[kGradFields], uint32_t lane,
+                                                   double* __restrict__ red) {
+  __syncwarp();
+#pragma unroll
+  for (int f = 0; f < kGradFields; ++f) red[lane * kGradFields + f] = (double)in[f];
+  __syncwarp();
+  double v = 0.0;
+  const int f = (int)(lane / 3u), part = (int)(lane - 3u * (uint32_t)f);
+  if (lane < 3 * kGradFields) {
+    const int r0 = 11 * part;
+#pragma unroll
+    for (int i = 0; i < 11; ++i)
+      if (part < 2 || i < 10) v += red[(r0 + i) * kGradFields + f];
+  }
+  const double t1 = __shfl_down_sync(0xffffffffu, v, 1);
+  const double t2 = __shfl_down_sync(0xffffffffu, v, 2);
+  return (v + t1) + t2;  // valid in lane 3f
 }
 
 __device__ __forceinline__ bred_t warp_transpose_sum9(const float (&in)[kGradFields], uint32_t lane) {
@@ -294,11 +315,18 @@ k_blend_bwd(const uint32_t* __restrict__ list, const uint32_t* __restrict__ bxs,
           }
         }
         if (__any_sync(0xffffffffu, contrib)) {
-          const bred_t v = CS_BWD_RED_SMEM && CS_BWD_RED_F64 ? (bred_t)warp_smem_sum9(gr, lane, red)
-                                                             : warp_transpose_sum9(gr, lane);
-          const uint32_t f = (lane >> 1) & 15;
-          if (!(lane & 1) && f < kGradFields && v != (bred_t)0)
-            atomicAdd(&grads[(int64_t)f * cap + hid], (gacc_t)v);
+          if (CS_BWD_RED_SMEM == 2 && CS_BWD_RED_F64) {
+            const double v = warp_smem_sum9_3(gr, lane, red);
+            const uint32_t f = lane / 3u;
+            if (lane == 3u * f && f < kGradFields && v != 0.0)
+              atomicAdd(&grads[(int64_t)f * cap + hid], (gacc_t)v);
+          } else {
+            const bred_t v = CS_BWD_RED_SMEM && CS_BWD_RED_F64 ? (bred_t)warp_smem_sum9(gr, lane, red)
+                                                               : warp_transpose_sum9(gr, lane);
+            const uint32_t f = (lane >> 1) & 15;
+            if (!(lane & 1) && f < kGradFields && v != (bred_t)0)
+              atomicAdd(&grads[(int64_t)f * cap + hid], (gacc_t)v);
+          }
         }
       }
     };
