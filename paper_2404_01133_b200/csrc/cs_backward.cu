@@ -80,6 +80,9 @@ __device__ __forceinline__ double warp_smem_sum9(const float (&in)[kGradFields],
 
 // CS_BWD_RED_SMEM=2: three lanes per field (rows 0-10 / 11-21 / 22-31; lane
 // 3f + p), summed with two shuffles into lane 3f: fewer loads per lane
+#ifndef CS_BWD_RED_T
+#define CS_BWD_RED_T 0  // float rows field-major with a 33-float stride: conflict-free stores and reads
+#endif
 #ifndef CS_BWD_RED_F32STORE
 #define CS_BWD_RED_F32STORE 1  // rows stored as float (exact), widened when summed (profiles/r5l_bwd_f32store_ab.txt)
 #endif
@@ -89,7 +92,8 @@ __device__ __forceinline__ double warp_smem_sum9_3(const float (&in)[kGradFields
   __syncwarp();
 #pragma unroll
   for (int f = 0; f < kGradFields; ++f) {
-    if (CS_BWD_RED_F32STORE) redf[lane * kGradFields + f] = in[f];
+    if (CS_BWD_RED_F32STORE && CS_BWD_RED_T) redf[f * 33 + lane] = in[f];
+    else if (CS_BWD_RED_F32STORE) redf[lane * kGradFields + f] = in[f];
     else red[lane * kGradFields + f] = (double)in[f];
   }
   __syncwarp();
@@ -100,7 +104,9 @@ __device__ __forceinline__ double warp_smem_sum9_3(const float (&in)[kGradFields
 #pragma unroll
     for (int i = 0; i < 11; ++i)
       if (part < 2 || i < 10)
-        v += CS_BWD_RED_F32STORE ? (double)redf[(r0 + i) * kGradFields + f] : red[(r0 + i) * kGradFields + f];
+        v += CS_BWD_RED_F32STORE && CS_BWD_RED_T ? (double)redf[f * 33 + r0 + i]
+             : CS_BWD_RED_F32STORE                ? (double)redf[(r0 + i) * kGradFields + f]
+                                                  : red[(r0 + i) * kGradFields + f];
   }
   const double t1 = __shfl_down_sync(0xffffffffu, v, 1);
   const double t2 = __shfl_down_sync(0xffffffffu, v, 2);
